@@ -1,0 +1,210 @@
+/*
+ * oracle.c -- plain scalar lookup-table base64 codec.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (paper_1910_05109_b200/) never links, imports or calls it,
+ * and this file shares no code, header, table or constant with the CUDA path.
+ *
+ * What it computes is the plain definition of base64 as the paper states it
+ * (arXiv 1910.05109, Mula & Lemire), written out one byte / one quad at a time
+ * with no blocking, fusion or reordering:
+ *
+ *   encode  PAPER.md:88-92 (Sec. 2): s1 div 4, (s2 div 16) + (s1*16) mod 64,
+ *           (s2*4) mod 64 + (s3 div 64), s3 mod 64, each mapped to a char
+ *           through the 64-entry alphabet.
+ *           Padding '=' so the length is a multiple of 4.
+ *   decode  PAPER.md:96-99 (Sec. 2): a char -> [0,64) or a special "invalid"
+ *           value via a lookup table; (a*4) + (b div 16),
+ *           (b*16) mod 256 + (c div 4), (c*64) mod 256 + d.
+ *
+ * Where the paper is silent (strict padding, error offset) this follows the
+ * readings listed in DESIGN.md "Readings of the paper" (R5-R8), which are
+ * SURVEY.md Sec. 8(c):
+ *   - m % 4 != 0  -> status LENGTH, err_off = m - m % 4, nothing decoded;
+ *   - err_off = smallest bad position; interior chars must be in the alphabet;
+ *     the final quad allows '=' at m-2 and m-1 only, no data after '=',
+ *     and zero trailing bits (canonical), checked in that order;
+ *   - out_len = bytes that are exact: the whole decoded length when valid,
+ *     3 * floor(err_off / 4) otherwise.
+ *
+ * Pinned by tests/test_oracle_pins.py (Python base64 library exhaustively,
+ * the paper's Sec. 3.1 / 3.2 vector algorithms emulated from their printed
+ * constants, Fig. 2's worked values, the padding round-trip invariant, and
+ * error injection).  Parity status per function is listed in DESIGN.md.
+ */
+#include <stdint.h>
+#include <string.h>
+
+#define ORACLE_INVALID 0xFFu /* the paper's "special value" */
+
+enum {
+    ORACLE_ST_OK = 0,
+    ORACLE_ST_BADCHAR = 1,  /* byte outside the alphabet (or misplaced pad) */
+    ORACLE_ST_BADPAD = 2,   /* data after padding                          */
+    ORACLE_ST_NONCANON = 3, /* non-zero trailing bits in a padded quad     */
+    ORACLE_ST_LENGTH = 4    /* m % 4 != 0                                  */
+};
+
+/* Alphabet validity (R4): 64 distinct chars < 0x80,
+ * pad < 0x80 and not one of them.  Returns 0, or -3 duplicate, -4 non-ASCII,
+ * -5 pad in alphabet; *bad_index gets the offending index (64 = the pad). */
+int oracle_alphabet_check(const uint8_t chars[64], uint8_t pad, int *bad_index)
+{
+    int i, j;
+    *bad_index = -1;
+    for (i = 0; i < 64; i++) {
+        if (chars[i] >= 0x80) { *bad_index = i; return -4; }
+    }
+    if (pad >= 0x80) { *bad_index = 64; return -4; }
+    for (i = 0; i < 64; i++) {
+        for (j = 0; j < i; j++) {
+            if (chars[i] == chars[j]) { *bad_index = i; return -3; }
+        }
+    }
+    for (i = 0; i < 64; i++) {
+        if (chars[i] == pad) { *bad_index = i; return -5; }
+    }
+    return 0;
+}
+
+/* Length law: 4 * ceil(n / 3). */
+int64_t oracle_encoded_len(int64_t n)
+{
+    return 4 * ((n + 2) / 3);
+}
+
+/* Encode n bytes; writes exactly oracle_encoded_len(n) chars; returns that. */
+int64_t oracle_encode(const uint8_t *in, int64_t n, uint8_t *out,
+                      const uint8_t chars[64], uint8_t pad)
+{
+    int64_t i = 0, o = 0;
+    /* full triples */
+    for (; i + 3 <= n; i += 3) {
+        unsigned s1 = in[i], s2 = in[i + 1], s3 = in[i + 2];
+        out[o++] = chars[s1 / 4];
+        out[o++] = chars[(s2 / 16) + (s1 * 16) % 64];
+        out[o++] = chars[(s2 * 4) % 64 + (s3 / 64)];
+        out[o++] = chars[s3 % 64];
+    }
+    /* leftover 1 or 2 bytes: the same formulas with the missing bytes taken
+     * as zero, then '=' so the output length is a multiple of four
+     * ("conventional code path"). */
+    if (n - i == 1) {
+        unsigned s1 = in[i], s2 = 0;
+        out[o++] = chars[s1 / 4];
+        out[o++] = chars[(s2 / 16) + (s1 * 16) % 64];
+        out[o++] = pad;
+        out[o++] = pad;
+    } else if (n - i == 2) {
+        unsigned s1 = in[i], s2 = in[i + 1], s3 = 0;
+        out[o++] = chars[s1 / 4];
+        out[o++] = chars[(s2 / 16) + (s1 * 16) % 64];
+        out[o++] = chars[(s2 * 4) % 64 + (s3 / 64)];
+        out[o++] = pad;
+    }
+    return o;
+}
+
+/* The decode look-up table of: every byte value maps to the
+ * special value except the 64 alphabet chars, which map to their index. */
+static void build_decode_table(const uint8_t chars[64], uint8_t dec[256])
+{
+    int v;
+    memset(dec, ORACLE_INVALID, 256);
+    for (v = 0; v < 64; v++) dec[chars[v]] = (uint8_t)v;
+}
+
+/* Decode m chars.  Returns the status kind; *out_len and *err_off as in the
+ * header comment (err_off = -1 when valid). */
+int oracle_decode(const uint8_t *in, int64_t m, uint8_t *out,
+                  const uint8_t chars[64], uint8_t pad,
+                  int64_t *out_len, int64_t *err_off)
+{
+    uint8_t dec[256];
+    int64_t q, nq;
+    build_decode_table(chars, dec);
+    *out_len = 0;
+    *err_off = -1;
+    if (m % 4 != 0) {
+        *err_off = m - m % 4;
+        return ORACLE_ST_LENGTH;
+    }
+    nq = m / 4;
+    for (q = 0; q < nq; q++) {
+        const uint8_t *c = in + 4 * q;
+        int64_t p = 4 * q;
+        uint8_t *o = out + 3 * q;
+        if (q < nq - 1) {
+            /* interior quad: all four chars must be in the alphabet */
+            int j;
+            for (j = 0; j < 4; j++) {
+                if (dec[c[j]] == ORACLE_INVALID) {
+                    *err_off = p + j;
+                    *out_len = 3 * q;
+                    return ORACLE_ST_BADCHAR;
+                }
+            }
+            {
+                unsigned a = dec[c[0]], b = dec[c[1]], cc = dec[c[2]], d = dec[c[3]];
+                o[0] = (uint8_t)((a * 4) + (b / 16));
+                o[1] = (uint8_t)((b * 16) % 256 + (cc / 4));
+                o[2] = (uint8_t)((cc * 64) % 256 + d);
+            }
+        } else {
+            /* the final quad ("final and separate code path") */
+            int kind = ORACLE_ST_OK;
+            int64_t bad = -1;
+            int pad2 = (c[2] == pad), pad3 = (c[3] == pad);
+            if (dec[c[0]] == ORACLE_INVALID) { bad = p; kind = ORACLE_ST_BADCHAR; }
+            else if (dec[c[1]] == ORACLE_INVALID) { bad = p + 1; kind = ORACLE_ST_BADCHAR; }
+            else if (dec[c[2]] == ORACLE_INVALID && !pad2) { bad = p + 2; kind = ORACLE_ST_BADCHAR; }
+            else if (dec[c[3]] == ORACLE_INVALID && !pad3) { bad = p + 3; kind = ORACLE_ST_BADCHAR; }
+            else if (pad2 && !pad3) { bad = p + 3; kind = ORACLE_ST_BADPAD; }
+            else if (pad2 && pad3 && (dec[c[1]] % 16) != 0) { bad = p + 1; kind = ORACLE_ST_NONCANON; }
+            else if (!pad2 && pad3 && (dec[c[2]] % 4) != 0) { bad = p + 2; kind = ORACLE_ST_NONCANON; }
+            if (kind != ORACLE_ST_OK) {
+                *err_off = bad;
+                *out_len = 3 * q;
+                return kind;
+            }
+            {
+                unsigned a = dec[c[0]], b = dec[c[1]];
+                unsigned cc = pad2 ? 0 : dec[c[2]];
+                unsigned d = pad3 ? 0 : dec[c[3]];
+                int k = pad2 ? 1 : (pad3 ? 2 : 3);
+                o[0] = (uint8_t)((a * 4) + (b / 16));
+                if (k >= 2) o[1] = (uint8_t)((b * 16) % 256 + (cc / 4));
+                if (k >= 3) o[2] = (uint8_t)((cc * 64) % 256 + d);
+                *out_len = 3 * q + k;
+            }
+        }
+    }
+    if (nq == 0) *out_len = 0;
+    return ORACLE_ST_OK;
+}
+
+/* Batched forms: the single-stream definitions applied string by string over
+ * concatenated buffers with int64 offsets[count + 1] (BASELINE.json
+ * configs[3]).  Encode output string i starts at out_off[i]. */
+void oracle_encode_batch(const uint8_t *in, const int64_t *in_off, int64_t count,
+                         uint8_t *out, const int64_t *out_off,
+                         const uint8_t chars[64], uint8_t pad)
+{
+    int64_t i;
+    for (i = 0; i < count; i++)
+        oracle_encode(in + in_off[i], in_off[i + 1] - in_off[i], out + out_off[i], chars, pad);
+}
+
+/* Decode output string i starts at out_off[i]; err_off is relative to the
+ * string start, -1 when valid. */
+void oracle_decode_batch(const uint8_t *in, const int64_t *in_off, int64_t count,
+                         uint8_t *out, const int64_t *out_off,
+                         const uint8_t chars[64], uint8_t pad,
+                         int32_t *status, int64_t *err_off, int64_t *out_len)
+{
+    int64_t i;
+    for (i = 0; i < count; i++)
+        status[i] = oracle_decode(in + in_off[i], in_off[i + 1] - in_off[i], out + out_off[i],
+                                  chars, pad, &out_len[i], &err_off[i]);
+}
