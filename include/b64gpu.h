@@ -1,0 +1,171 @@
+/*
+ * b64gpu.h -- C ABI of the B200-native (sm_100a) base64 codec.
+ *
+ * Method: W. Mula, D. Lemire, "Base64 encoding and decoding at almost the
+ * speed of a memory copy", arXiv 1910.05109 (PAPER.md in the task reference).
+ * Citations "PAPER.md:L" are line numbers of that file; "DESIGN.md Rn" are the
+ * numbered readings of the paper listed in DESIGN.md.
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ *  - Every pointer named d_* is a DEVICE pointer (cudaMalloc / torch CUDA
+ *    storage) on the current device; every other pointer is a host pointer.
+ *  - All sizes, offsets and positions are int64_t (streams may exceed 2^32).
+ *  - Ownership: the caller allocates and owns every buffer.  The library never
+ *    allocates, frees or keeps per-call state and is re-entrant on any stream.
+ *  - Ordering: every call only enqueues work on `stream` (0 = legacy default
+ *    stream) and returns; results are visible to later work on that stream.
+ *  - Return value: synchronous argument / launch errors only (B64_OK or a
+ *    negative B64_E* code).  Data errors (invalid base64) are asynchronous and
+ *    are written to device memory (err_off / status).
+ *  - Input bytes are only read and output bytes only written inside the
+ *    ranges stated per call, except that the generic (unaligned / batched)
+ *    kernels may read the naturally aligned 4-byte words that contain input
+ *    bytes (at most 3 bytes before the first / after the last input byte,
+ *    never crossing into another 4-byte-aligned word).
+ *  - Inputs and outputs must not overlap.
+ */
+#ifndef B64GPU_H
+#define B64GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same type as cudaStream_t (struct CUstream_st*); no CUDA header needed. */
+typedef struct CUstream_st *b64_stream_t;
+
+/* ---- status codes ------------------------------------------------------ */
+enum {
+    B64_OK = 0,
+    B64_EINVAL = -1,          /* null pointer with non-zero size, negative size, bad flag */
+    B64_ELENGTH = -2,         /* b64_decode*: m % 4 != 0 (nothing launched, nothing written) */
+    B64_EALPHA_DUP = -3,      /* alphabet: duplicate character        */
+    B64_EALPHA_NONASCII = -4, /* alphabet: character or pad >= 0x80   */
+    B64_EALPHA_PAD = -5,      /* alphabet: pad is one of the 64 chars */
+    B64_ECUDA = -6            /* a CUDA launch / runtime call failed  */
+};
+
+/* per-stream / per-string decode status (asynchronous, device memory) */
+enum {
+    B64_ST_OK = 0,
+    B64_ST_BADCHAR = 1,  /* byte outside the alphabet, or '=' where it may not be  */
+    B64_ST_BADPAD = 2,   /* alphabet char after '=' in the final quad              */
+    B64_ST_NONCANON = 3, /* non-zero trailing bits in 'xx==' / 'xxx=' (DESIGN R6)  */
+    B64_ST_LENGTH = 4    /* batched string with len % 4 != 0                        */
+};
+
+/* Packed error word used by the chunk API and the multi-GPU MIN reduction:
+ * (global_position << 3) | status.  Positions are unique, so the MIN over
+ * packed words is the first error together with its kind.  B64_ERR_NONE
+ * means "no error" (R8); it is the byte 0x7F repeated, so a
+ * cudaMemsetAsync(p, 0x7F, 8) initialises a cell, and it exceeds every packed
+ * word of a position < 2^59. */
+#define B64_ERR_NONE ((int64_t)0x7F7F7F7F7F7F7F7FLL)
+#define B64_ERR_POS(w) ((int64_t)(w) >> 3)
+#define B64_ERR_KIND(w) ((int)((w)&7))
+
+/* ---- alphabet ----------------------------- */
+/* A validated alphabet, passed BY VALUE to the kernels as runtime constants
+ * ("adapted -- even at runtime -- to any base64 variant by only changing
+ * constants"; "any 64-byte mapping is feasible, even if
+ * determined dynamically at runtime").
+ *   enc[v]  : the character for 6-bit value v (v < 64).
+ *   dec[c]  : the 6-bit value of character c, or 0x80 when c is not one of
+ *             the 64 (the paper's sentinel, indexed here by
+ *             the full byte instead of its low 7 bits).
+ *   pad     : the padding character, '=' for both variants. */
+typedef struct b64_alphabet {
+    uint8_t enc[64];
+    uint8_t dec[256];
+    uint8_t pad;
+    uint8_t reserved[3];
+} b64_alphabet;
+
+/* Validate `chars` (64 bytes) + `pad` and fill `*a`.  Rules (R4):
+ * 64 distinct bytes < 0x80, pad < 0x80 and not among them.  On failure
+ * returns B64_EALPHA_* and sets *bad_index (nullable) to the offending index
+ * (64 = the pad); *a is then unspecified.  Host only, O(1). */
+int b64_alphabet_init(b64_alphabet *a, const char chars[64], char pad, int *bad_index);
+
+/* Built-in alphabets (static storage, never freed). */
+const b64_alphabet *b64_alphabet_standard(void);
+const b64_alphabet *b64_alphabet_url(void);
+
+/* ---- sizes ----------------------------------------------------------------- */
+int64_t b64_encoded_len(int64_t n);     /* 4*ceil(n/3); -1 if n < 0 */
+int64_t b64_decoded_len_max(int64_t m); /* 3*(m/4): capacity a decode output needs   */
+
+/* ---- single stream --------------------------------------------------------- */
+/* Encode n bytes d_in[0..n) to exactly b64_encoded_len(n) chars at d_out, with
+ * '=' padding (R5).  No NUL terminator.
+ * d_out capacity >= b64_encoded_len(n).  n == 0 is valid and launches nothing. */
+int b64_encode(const uint8_t *d_in, int64_t n, uint8_t *d_out, const b64_alphabet *a,
+               b64_stream_t stream);
+
+/* Validating decode of m chars (DESIGN.md
+ * R5-R8).  m % 4 != 0 returns B64_ELENGTH synchronously.  Asynchronously
+ * writes *d_err_off (device int64) = -1 when the text is valid, else the
+ * position of the first invalid character.  Output: 3*m/4 - pads bytes at
+ * d_out when valid; on error only the bytes of quads before the quad holding
+ * err_off are defined.  d_out capacity >= b64_decoded_len_max(m). */
+int b64_decode(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a,
+               int64_t *d_err_off, b64_stream_t stream);
+
+/* b64_decode plus the status kind and the number of exact output bytes
+ * (3*m/4 - pads when valid, else 3*floor(err_off/4)).  d_status and
+ * d_out_len are nullable device pointers; d_err_off is required. */
+int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a,
+                  int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len,
+                  b64_stream_t stream);
+
+/* Shard-aware decode used by the multi-GPU driver.
+ * Decodes chars [base_offset, base_offset + m) of a larger stream, m % 4 == 0.
+ * Only when is_final_chunk != 0 is the last quad treated as the stream's
+ * final quad (padding allowed); otherwise every quad is interior.
+ * *d_err_min (device, caller-initialised to B64_ERR_NONE) is lowered with an
+ * atomic MIN to the packed word (global_pos << 3 | status) of every error found
+ * (at least the first one of this chunk).  *d_out_len (nullable) receives the
+ * bytes written assuming the chunk is valid (3*m/4, minus the pads when final). */
+int b64_decode_chunk(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a,
+                     int64_t base_offset, int is_final_chunk, int64_t *d_err_min,
+                     int64_t *d_out_len, b64_stream_t stream);
+
+/* Map a packed error word (after any cross-rank MIN) to the API form:
+ * *d_err_off = -1 or position, *d_status (nullable) = kind.  One tiny kernel. */
+int b64_decode_finalize(const int64_t *d_err_min, int64_t *d_err_off, int32_t *d_status,
+                        b64_stream_t stream);
+
+/* ---- batched (BASELINE.json configs[3]) ------------------------------------ */
+/* `count` independent strings concatenated in d_in; string i is
+ * d_in[d_in_off[i] .. d_in_off[i+1]) (d_in_off: device int64[count+1],
+ * non-decreasing, d_in_off[0] >= 0).  Output string i is written at
+ * d_out + d_out_off[i] (device int64[count], caller-computed):
+ *   encode: d_out_off = exclusive scan of 4*ceil(len_i/3); each string padded.
+ *   decode: d_out_off = exclusive scan of 3*(len_i/4).                        */
+int b64_encode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t count,
+                     uint8_t *d_out, const int64_t *d_out_off, const b64_alphabet *a,
+                     b64_stream_t stream);
+
+/* Per string i (all device arrays of length count; d_err_off required, the
+ * other two nullable): d_status[i] (B64_ST_*), d_err_off[i] = -1 or the first
+ * invalid position RELATIVE to the string start (len - len%4 for
+ * B64_ST_LENGTH), d_out_len[i] = exact output bytes (as b64_decode_ex). */
+int b64_decode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t count,
+                     uint8_t *d_out, const int64_t *d_out_off, const b64_alphabet *a,
+                     int32_t *d_status, int64_t *d_err_off, int64_t *d_out_len,
+                     b64_stream_t stream);
+
+/* ---- introspection ---------------------------------------------------------- */
+/* Number of kernels the library launched on this process so far (all calls),
+ * counted on the host at each launch -- used by bench.py's gpu_launches. */
+int64_t b64_launch_count(void);
+/* Static description of the build ("sm_100a ..."). */
+const char *b64_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B64GPU_H */

@@ -1,0 +1,212 @@
+"""B200-native base64 codec (arXiv 1910.05109, Mula & Lemire) -- Python binding.
+
+Thin argument marshalling over the C ABI in ``include/b64gpu.h``
+(``libb64gpu.so``, hand-written sm_100a kernels).  torch supplies device memory
+and streams only; every step of encode / decode runs in the library's kernels.
+There is no CPU fallback: the calls raise if the library is missing or the
+tensors are not CUDA uint8 tensors.
+
+    enc = encode(x)                      # x: uint8 CUDA tensor -> chars
+    out, err = decode(enc)               # err = -1 or first invalid offset (R7)
+    out, info = decode_async(enc)        # no host sync; info = int64[3] (err, status, out_len)
+    enc, off = encode_batch(x, in_off)   # BASELINE.json configs[3]
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Tuple
+
+import torch
+
+from . import _lib
+from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH, ST_NONCANON, ST_OK  # noqa: F401
+
+__all__ = [
+    "Alphabet", "B64Error", "alphabet", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
+    "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count",
+    "ERR_NONE",
+]
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_u8(t: torch.Tensor, name: str) -> None:
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.uint8 or not t.is_cuda or not t.is_contiguous():
+        raise B64Error(f"{name} must be a contiguous uint8 CUDA tensor")
+
+
+def _check_i64(t: torch.Tensor, name: str) -> None:
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.int64 or not t.is_cuda or not t.is_contiguous():
+        raise B64Error(f"{name} must be a contiguous int64 CUDA tensor")
+
+
+# ------------------------------------------------------------------ alphabets
+
+def alphabet(chars: bytes, pad: bytes = b"=") -> Alphabet:
+    """Validate a 64-char alphabet + pad (R4); returns the by-value table struct."""
+    if len(chars) != 64 or len(pad) != 1:
+        raise B64Error("alphabet needs 64 chars and a 1-byte pad")
+    a = Alphabet()
+    bad = ctypes.c_int(0)
+    rc = _lib.lib().b64_alphabet_init(ctypes.byref(a), bytes(chars), pad, ctypes.byref(bad))
+    if rc != 0:
+        raise B64Error(f"invalid alphabet: {_lib.ERRORS.get(rc, rc)} at index {bad.value}")
+    return a
+
+
+def standard() -> Alphabet:
+    return _lib.lib().b64_alphabet_standard().contents
+
+
+def url() -> Alphabet:
+    return _lib.lib().b64_alphabet_url().contents
+
+
+def _alpha(a: Optional[Alphabet]):
+    return ctypes.byref(a if a is not None else standard())
+
+
+def encoded_len(n: int) -> int:
+    return int(_lib.lib().b64_encoded_len(n))
+
+
+def decoded_len_max(m: int) -> int:
+    return int(_lib.lib().b64_decoded_len_max(m))
+
+
+# ------------------------------------------------------------------ single stream
+
+def encode(x: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
+           stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Encode bytes to base64 chars with '=' padding (b64_encode)."""
+    _check_u8(x, "x")
+    m = encoded_len(x.numel())
+    if out is None:
+        out = torch.empty(m, dtype=torch.uint8, device=x.device)
+    else:
+        _check_u8(out, "out")
+        if out.numel() < m:
+            raise B64Error("out too small")
+    _lib.check(_lib.lib().b64_encode(_ptr(x), x.numel(), _ptr(out), _alpha(a), _stream(stream)), "b64_encode")
+    return out[:m]
+
+
+def decode_async(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
+                 info: Optional[torch.Tensor] = None,
+                 stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Validating decode (b64_decode_ex) without a host sync.
+
+    Returns (out, info) where info is a device int64[3]: (err_off, status, out_len)."""
+    _check_u8(t, "t")
+    m = t.numel()
+    if m % 4:
+        raise B64Error("B64_ELENGTH: text length is not a multiple of 4")
+    cap = decoded_len_max(m)
+    if out is None:
+        out = torch.empty(max(cap, 1), dtype=torch.uint8, device=t.device)
+    if info is None:
+        info = torch.empty(3, dtype=torch.int64, device=t.device)
+    st = info[1:2].view(torch.int32)[:1]  # status stored in the low half of info[1]
+    info[1].zero_()
+    _lib.check(_lib.lib().b64_decode_ex(_ptr(t), m, _ptr(out), _alpha(a), _ptr(info[0:1]), _ptr(st),
+                                        _ptr(info[2:3]), _stream(stream)), "b64_decode_ex")
+    return out, info
+
+
+def decode(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
+           stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, int]:
+    """Validating decode.  Returns (decoded bytes, err_off); err_off = -1 when valid.
+    Forces one 24-byte device->host read of (err_off, status, out_len)."""
+    out, info = decode_async(t, a, out=out, stream=stream)
+    err, _, olen = info.tolist()
+    return out[:olen], err
+
+
+def decode_chunk(t: torch.Tensor, base_offset: int, is_final: bool, err_cell: torch.Tensor,
+                 a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
+                 out_len: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Shard-aware decode (b64_decode_chunk): lowers err_cell (int64[1], init ERR_NONE) with the
+    packed first error (global_pos << 3 | status)."""
+    _check_u8(t, "t")
+    _check_i64(err_cell, "err_cell")
+    m = t.numel()
+    if out is None:
+        out = torch.empty(max(decoded_len_max(m), 1), dtype=torch.uint8, device=t.device)
+    _lib.check(_lib.lib().b64_decode_chunk(_ptr(t), m, _ptr(out), _alpha(a), base_offset, 1 if is_final else 0,
+                                           _ptr(err_cell), _ptr(out_len), _stream(stream)), "b64_decode_chunk")
+    return out
+
+
+def decode_finalize(err_cell: torch.Tensor, err_off: torch.Tensor, status: Optional[torch.Tensor] = None,
+                    stream: Optional[torch.cuda.Stream] = None) -> None:
+    """Packed error word -> (err_off = -1 | position, status) on the device."""
+    _check_i64(err_cell, "err_cell")
+    _check_i64(err_off, "err_off")
+    _lib.check(_lib.lib().b64_decode_finalize(_ptr(err_cell), _ptr(err_off), _ptr(status), _stream(stream)),
+               "b64_decode_finalize")
+
+
+# ------------------------------------------------------------------ batched
+
+def encode_batch(x: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = None,
+                 out: Optional[torch.Tensor] = None, out_off: Optional[torch.Tensor] = None,
+                 total_out: Optional[int] = None,
+                 stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Per-string padded encode of strings concatenated in x (offsets int64[count+1]).
+    Returns (out, out_off) with out_off = exclusive scan of 4*ceil(len/3) (int64[count+1])."""
+    _check_u8(x, "x")
+    _check_i64(in_off, "in_off")
+    count = in_off.numel() - 1
+    if out_off is None:
+        lens = in_off[1:] - in_off[:-1]
+        out_off = torch.zeros(count + 1, dtype=torch.int64, device=x.device)
+        torch.cumsum(4 * torch.div(lens + 2, 3, rounding_mode="floor"), 0, out=out_off[1:])
+    if out is None:
+        if total_out is None:
+            total_out = int(out_off[-1].item())
+        out = torch.empty(max(total_out, 1), dtype=torch.uint8, device=x.device)
+    _lib.check(_lib.lib().b64_encode_batch(_ptr(x), _ptr(in_off), count, _ptr(out), _ptr(out_off), _alpha(a),
+                                           _stream(stream)), "b64_encode_batch")
+    return out, out_off
+
+
+def decode_batch(t: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = None,
+                 out: Optional[torch.Tensor] = None, out_off: Optional[torch.Tensor] = None,
+                 total_out: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None):
+    """Per-string validating decode.  Returns (out, out_off, status int32, err_off int64
+    (relative, -1 = ok), out_len int64); out_off = exclusive scan of 3*(len//4)."""
+    _check_u8(t, "t")
+    _check_i64(in_off, "in_off")
+    count = in_off.numel() - 1
+    dev = t.device
+    if out_off is None:
+        lens = in_off[1:] - in_off[:-1]
+        out_off = torch.zeros(count + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(3 * torch.div(lens, 4, rounding_mode="floor"), 0, out=out_off[1:])
+    if out is None:
+        if total_out is None:
+            total_out = int(out_off[-1].item())
+        out = torch.empty(max(total_out, 1), dtype=torch.uint8, device=dev)
+    status = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
+    err = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
+    olen = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().b64_decode_batch(_ptr(t), _ptr(in_off), count, _ptr(out), _ptr(out_off), _alpha(a),
+                                           _ptr(status), _ptr(err), _ptr(olen), _stream(stream)),
+               "b64_decode_batch")
+    return out, out_off, status[:count], err[:count], olen[:count]
+
+
+def launch_count() -> int:
+    """Kernels this process launched through the library (host-side counter)."""
+    return int(_lib.lib().b64_launch_count())
+
+
+def build_info() -> str:
+    return _lib.lib().b64_build_info().decode()

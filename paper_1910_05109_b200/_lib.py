@@ -1,0 +1,87 @@
+"""ctypes loader for libb64gpu.so (the C ABI of include/b64gpu.h).
+
+Argument marshalling only.  There is deliberately no fallback: if the shared
+library is missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libb64gpu.so")
+
+B64_OK = 0
+B64_EINVAL = -1
+B64_ELENGTH = -2
+B64_EALPHA_DUP = -3
+B64_EALPHA_NONASCII = -4
+B64_EALPHA_PAD = -5
+B64_ECUDA = -6
+
+ERR_NONE = 0x7F7F7F7F7F7F7F7F
+
+ST_OK, ST_BADCHAR, ST_BADPAD, ST_NONCANON, ST_LENGTH = 0, 1, 2, 3, 4
+
+ERRORS = {
+    B64_EINVAL: "B64_EINVAL",
+    B64_ELENGTH: "B64_ELENGTH",
+    B64_EALPHA_DUP: "B64_EALPHA_DUP",
+    B64_EALPHA_NONASCII: "B64_EALPHA_NONASCII",
+    B64_EALPHA_PAD: "B64_EALPHA_PAD",
+    B64_ECUDA: "B64_ECUDA",
+}
+
+# (name, restype, argtypes) for every symbol include/b64gpu.h declares.
+P, I64, I32, INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
+
+
+class Alphabet(ctypes.Structure):
+    _fields_ = [("enc", ctypes.c_uint8 * 64), ("dec", ctypes.c_uint8 * 256), ("pad", ctypes.c_uint8),
+                ("reserved", ctypes.c_uint8 * 3)]
+
+
+AP = ctypes.POINTER(Alphabet)
+
+SIGNATURES = [
+    ("b64_alphabet_init", INT, [AP, ctypes.c_char_p, ctypes.c_char, ctypes.POINTER(INT)]),
+    ("b64_alphabet_standard", AP, []),
+    ("b64_alphabet_url", AP, []),
+    ("b64_encoded_len", I64, [I64]),
+    ("b64_decoded_len_max", I64, [I64]),
+    ("b64_encode", INT, [P, I64, P, AP, P]),
+    ("b64_decode", INT, [P, I64, P, AP, P, P]),
+    ("b64_decode_ex", INT, [P, I64, P, AP, P, P, P, P]),
+    ("b64_decode_chunk", INT, [P, I64, P, AP, I64, INT, P, P, P]),
+    ("b64_decode_finalize", INT, [P, P, P, P]),
+    ("b64_encode_batch", INT, [P, P, I64, P, P, AP, P]),
+    ("b64_decode_batch", INT, [P, P, I64, P, P, AP, P, P, P, P]),
+    ("b64_launch_count", I64, []),
+    ("b64_build_info", ctypes.c_char_p, []),
+]
+
+_lib = None
+
+
+class B64Error(RuntimeError):
+    pass
+
+
+def lib():
+    """Load the CUDA library (raises if it is missing: no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise B64Error(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != B64_OK:
+        raise B64Error(f"{what} failed: {ERRORS.get(rc, rc)}")

@@ -1,0 +1,223 @@
+// b64_device.cuh -- device building blocks of the sm_100a base64 codec.
+//
+// The paper's AVX-512 design (Sec. 3, 512-bit registers, vpermb /
+// vpmultishiftqb / vpermi2b / vpmaddubsw / vpmaddwd) is prior art; the B200
+// mapping used here:
+//   * one 32-bit register holds one triple (encode) or one quad (decode);
+//     PRMT (__byte_perm) is the vpermb gather and the
+//     vpermb compaction, SHF/LOP3 the bit relayout
+//     (PAPER.md:201-237), IMAD the multiply-add packing;
+//   * the alphabet / decode tables are runtime kernel parameters staged to a
+//     64 B / 256 B shared-memory table per CTA: the vpermb / vpermi2b lookups
+//     become one LDS.U8 per character (64 B spans 16 banks and ASCII indexes of
+//     the 256 B table fall in 32 distinct banks: conflict-free);
+//   * deferred validation: a per-thread OR accumulator of the
+//     translated values, tested once per 32 characters; only when a bit 0x80 is
+//     set does the warp locate the first bad character (vote + __reduce_min_sync
+//     + one 64-bit atomicMin) -- the paper stops at "invalid", we report where.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace b64 {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kThreads = 256;          // threads per CTA for every kernel
+constexpr uint32_t kInvalid = 0x80u;   // decode-table sentinel
+
+constexpr unsigned long long kErrNone = 0x7F7F7F7F7F7F7F7FULL;  // B64_ERR_NONE
+enum : uint32_t { kOk = 0, kBadChar = 1, kBadPad = 2, kNonCanon = 3, kLength = 4 };
+
+// Alphabet tables passed BY VALUE as kernel parameters (runtime constants,
+// PAPER.md:240).
+struct EncTab { uint32_t w[16]; };             // enc[64] chars
+struct DecTab { uint32_t w[64]; uint32_t pad; };  // dec[256] + pad char
+
+__device__ __forceinline__ unsigned long long pack_err(int64_t pos, uint32_t kind) {
+    return ((unsigned long long)pos << 3) | kind;
+}
+
+// ----------------------------------------------------------------- memory ops
+// 256-bit lane-linear load, no L1 allocation (streamed once).
+__device__ __forceinline__ void ld256_stream(const void* p, uint32_t (&r)[8]) {
+    asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+        : "l"(p));
+}
+// 64-bit load that allocates in L1: three of them at a lane stride of 24 B
+// cover 768 contiguous bytes per warp; the first one brings every sector into
+// L1 and the next two hit there (DRAM reads each byte once).
+__device__ __forceinline__ uint2 ld64_l1(const void* p) {
+    uint2 r;
+    asm("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld32(const void* p) {
+    uint32_t r;
+    asm("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st256(void* p, const uint32_t (&v)[8]) {
+    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void st64(void* p, uint32_t a, uint32_t b) {
+    asm volatile("st.global.v2.u32 [%0], {%1,%2};" :: "l"(p), "r"(a), "r"(b) : "memory");
+}
+
+// 4 aligned words starting at an arbitrary byte address p, funnel-shifted to
+// the bytes p[0..16) (little-endian).  Reads only the aligned words that
+// contain p[0..16) (b64gpu.h conventions).
+template <int NW>
+__device__ __forceinline__ void ld_unaligned(const uint8_t* p, uint32_t (&w)[NW]) {
+    const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* pa = reinterpret_cast<const uint32_t*>(u & ~uintptr_t(3));
+    const uint32_t sh = uint32_t(u & 3) * 8u;
+    uint32_t a[NW + 1];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) a[i] = ld32(pa + i);
+    if (sh == 0) {
+#pragma unroll
+        for (int i = 0; i < NW; ++i) w[i] = a[i];
+    } else {
+        a[NW] = ld32(pa + NW);
+#pragma unroll
+        for (int i = 0; i < NW; ++i) w[i] = __funnelshift_r(a[i], a[i + 1], sh);
+    }
+}
+
+// ----------------------------------------------------------------- encode
+// One triple, given x with byte3 = s1, byte2 = s2, byte1 = s3 (byte0 unused):
+// the four 6-bit values of PAPER.md:88-92 are bits [26,32), [20,26), [14,20),
+// [8,14) of x; each indexes the 64-entry alphabet.
+__device__ __forceinline__ uint32_t enc_triple(uint32_t x, const uint8_t* __restrict__ lut) {
+    const uint32_t c0 = lut[x >> 26];
+    const uint32_t c1 = lut[(x >> 20) & 63u];
+    const uint32_t c2 = lut[(x >> 14) & 63u];
+    const uint32_t c3 = lut[(x >> 8) & 63u];
+    return __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+}
+
+// 12 input bytes (3 LE words) -> 16 chars (4 LE words).  The PRMT selectors
+// gather (s1, s2, s3) of triple t from bytes 3t..3t+2 -- the role of the
+// paper's first vpermb with indexes (3i+1, 3i, 3i+2, 3i+1).
+__device__ __forceinline__ void enc12(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t (&o)[4],
+                                      const uint8_t* __restrict__ lut) {
+    o[0] = enc_triple(__byte_perm(w0, w1, 0x0122), lut);
+    o[1] = enc_triple(__byte_perm(w0, w1, 0x3455), lut);
+    o[2] = enc_triple(__byte_perm(w1, w2, 0x2344), lut);
+    o[3] = enc_triple(__byte_perm(w2, w2, 0x1233), lut);
+}
+
+// r (1 or 2) leftover bytes s1[, s2] -> 4 chars with '=' padding.
+__device__ __forceinline__ uint32_t enc_partial(uint32_t s1, uint32_t s2, int r,
+                                                const uint8_t* __restrict__ lut, uint32_t pad) {
+    const uint32_t x = (s1 << 24) | (r == 2 ? (s2 << 16) : 0u);
+    const uint32_t c0 = lut[x >> 26];
+    const uint32_t c1 = lut[(x >> 20) & 63u];
+    const uint32_t c2 = (r == 2) ? uint32_t(lut[(x >> 14) & 63u]) : pad;
+    return c0 | (c1 << 8) | (c2 << 16) | (pad << 24);
+}
+
+// ----------------------------------------------------------------- decode
+// One quad (4 chars, LE in x) -> 24-bit value a*2^18 + b*2^12 + c*2^6 + d
+// (PAPER.md:98-99, 540-548); err collects the translated values so a set bit
+// 0x80 marks an invalid character.
+__device__ __forceinline__ uint32_t dec_quad(uint32_t x, const uint8_t* __restrict__ lut, uint32_t& err) {
+    const uint32_t a = lut[x & 0xffu];
+    const uint32_t b = lut[__byte_perm(x, 0, 0x4441)];
+    const uint32_t c = lut[__byte_perm(x, 0, 0x4442)];
+    const uint32_t d = lut[x >> 24];
+    err |= a | b | c | d;
+    return (((a * 64u + b) * 64u + c) * 64u) + d;
+}
+
+// 4 decoded quads -> 12 output bytes in 3 LE words, in stream order
+// (v>>16, v>>8, v per quad): the paper's compaction vpermb (PAPER.md:551-556,
+// read most-significant byte first per dword, R3).
+__device__ __forceinline__ void dec_pack12(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3,
+                                           uint32_t& o0, uint32_t& o1, uint32_t& o2) {
+    o0 = __byte_perm(v0, v1, 0x6012);
+    o1 = __byte_perm(v1, v2, 0x5601);
+    o2 = __byte_perm(v2, v3, 0x4560);
+}
+
+// Index (0..3) of the first invalid char of quad x, or 4.
+__device__ __forceinline__ int first_bad_in_quad(uint32_t x, const uint8_t* __restrict__ lut) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (lut[(x >> (8 * j)) & 0xffu] & kInvalid) return j;
+    return 4;
+}
+
+// The stream's final quad (R6, "final and separate code path",
+// PAPER.md:569).  Returns the error kind (kOk when valid); *bad = 0..3 the
+// offending position within the quad; *k = output bytes (1..3) when valid and
+// *v = the 24-bit value.
+__device__ __forceinline__ uint32_t final_quad(uint32_t x, const uint8_t* __restrict__ lut, uint32_t pad,
+                                               int* bad, int* k, uint32_t* v) {
+    const uint32_t ch0 = x & 0xffu, ch1 = (x >> 8) & 0xffu, ch2 = (x >> 16) & 0xffu, ch3 = x >> 24;
+    const uint32_t a = lut[ch0], b = lut[ch1], c = lut[ch2], d = lut[ch3];
+    const bool p2 = ch2 == pad, p3 = ch3 == pad;
+    *k = p2 ? 1 : (p3 ? 2 : 3);
+    *v = 0;
+    if (a & kInvalid) { *bad = 0; return kBadChar; }
+    if (b & kInvalid) { *bad = 1; return kBadChar; }
+    if ((c & kInvalid) && !p2) { *bad = 2; return kBadChar; }
+    if ((d & kInvalid) && !p3) { *bad = 3; return kBadChar; }
+    if (p2 && !p3) { *bad = 3; return kBadPad; }
+    if (p2 && (b & 15u)) { *bad = 1; return kNonCanon; }
+    if (!p2 && p3 && (c & 3u)) { *bad = 2; return kNonCanon; }
+    *v = (a << 18) | (b << 12) | ((p2 ? 0u : c) << 6) | (p3 ? 0u : d);
+    return kOk;
+}
+
+__device__ __forceinline__ void store_bytes(uint8_t* o, uint32_t v, int k) {
+    o[0] = uint8_t(v >> 16);
+    if (k >= 2) o[1] = uint8_t(v >> 8);
+    if (k >= 3) o[2] = uint8_t(v);
+}
+
+// Offsets of a batch of strings concatenated in one buffer; in_off == nullptr
+// means a single stream [0, n).  (b64gpu.h batched conventions.)
+struct Offsets {
+    const int64_t* in_off;
+    const int64_t* out_off;
+    int64_t count;
+    int64_t n;
+    __device__ __forceinline__ int64_t in(int64_t i) const { return in_off ? in_off[i] : (i == 0 ? 0 : n); }
+    __device__ __forceinline__ int64_t out(int64_t i) const { return out_off ? out_off[i] : 0; }
+};
+
+// First string s whose end in_off[s+1] > pos: strings ending at or before pos
+// own nothing at or after pos.
+__device__ __forceinline__ int64_t first_string_ending_after(const Offsets& off, int64_t pos) {
+    int64_t lo = 0, hi = off.count;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (off.in(mid + 1) > pos) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+// Kernel entry points (defined in encode.cu / decode.cu, launched by capi.cu).
+__global__ void enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab,
+                                uint32_t pad);
+__global__ void enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab,
+                                   uint32_t pad);
+__global__ void dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
+                                int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
+                                int64_t* __restrict__ out_len);
+__global__ void dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off,
+                                   DecTab tab, int64_t base, int is_final_single,
+                                   unsigned long long* __restrict__ err_cells, int64_t* __restrict__ out_len_single);
+__global__ void dec_finalize_single_kernel(int64_t* err_off, int32_t* status, int64_t* out_len,
+                                           const uint8_t* __restrict__ in, int64_t m, uint32_t pad);
+__global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off, int32_t* status);
+__global__ void dec_batch_init_kernel(int64_t* err, int64_t count);
+__global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
+                                          int64_t count, uint32_t pad, int32_t* status, int64_t* err,
+                                          int64_t* out_len);
+
+}  // namespace b64

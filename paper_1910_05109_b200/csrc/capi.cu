@@ -1,0 +1,241 @@
+// capi.cu -- the C ABI of include/b64gpu.h: argument checks, alphabet
+// validation, launch configuration and kernel dispatch.  No allocation, no
+// per-call state; every launch goes to the caller's stream.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/b64gpu.h"
+#include "b64_device.cuh"
+
+using namespace b64;
+
+namespace {
+
+std::atomic<int64_t> g_launches{0};
+
+// PAPER.md:239 (standard) and PAPER.md:93 (url: '+' '/' -> '-' '_').
+const char kStdChars[65] = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz0123456789+/";
+const char kUrlChars[65] = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz0123456789-_";
+
+struct DevInfo {
+    int sms = 0;
+    int occ_enc_fast = 0, occ_dec_fast = 0, occ_enc_gen = 0, occ_dec_gen = 0;
+};
+constexpr int kMaxDev = 64;
+DevInfo g_dev[kMaxDev];
+bool g_dev_ready[kMaxDev];
+std::mutex g_dev_mu;
+
+const DevInfo* dev_info() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) return nullptr;
+    std::lock_guard<std::mutex> lock(g_dev_mu);
+    if (g_dev_ready[d]) return &g_dev[d];
+    DevInfo info;
+    if (cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) return nullptr;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast, enc_fast_kernel, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast, dec_fast_kernel, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0))
+        return nullptr;
+    info.occ_enc_fast = info.occ_enc_fast < 1 ? 1 : info.occ_enc_fast;
+    info.occ_dec_fast = info.occ_dec_fast < 1 ? 1 : info.occ_dec_fast;
+    info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
+    info.occ_dec_gen = info.occ_dec_gen < 1 ? 1 : info.occ_dec_gen;
+    g_dev[d] = info;
+    g_dev_ready[d] = true;
+    return &g_dev[d];
+}
+
+EncTab enc_tab(const b64_alphabet* a) {
+    EncTab t;
+    std::memcpy(t.w, a->enc, 64);
+    return t;
+}
+DecTab dec_tab(const b64_alphabet* a) {
+    DecTab t;
+    std::memcpy(t.w, a->dec, 256);
+    t.pad = a->pad;
+    return t;
+}
+
+int launched() {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaPeekAtLastError() == cudaSuccess ? B64_OK : (cudaGetLastError(), B64_ECUDA);
+}
+
+int64_t clamp_grid(int64_t want, int64_t cap) { return want < 1 ? 1 : (want > cap ? cap : want); }
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+int alpha_ok(const b64_alphabet* a) { return a != nullptr; }
+
+}  // namespace
+
+extern "C" {
+
+int b64_alphabet_init(b64_alphabet* a, const char chars[64], char pad, int* bad_index) {
+    if (bad_index) *bad_index = -1;
+    if (!a || !chars) return B64_EINVAL;
+    const uint8_t* c = reinterpret_cast<const uint8_t*>(chars);
+    const uint8_t p = static_cast<uint8_t>(pad);
+    for (int i = 0; i < 64; ++i)
+        if (c[i] >= 0x80) { if (bad_index) *bad_index = i; return B64_EALPHA_NONASCII; }
+    if (p >= 0x80) { if (bad_index) *bad_index = 64; return B64_EALPHA_NONASCII; }
+    bool seen[128] = {false};
+    for (int i = 0; i < 64; ++i) {
+        if (seen[c[i]]) { if (bad_index) *bad_index = i; return B64_EALPHA_DUP; }
+        seen[c[i]] = true;
+    }
+    for (int i = 0; i < 64; ++i)
+        if (c[i] == p) { if (bad_index) *bad_index = i; return B64_EALPHA_PAD; }
+    std::memcpy(a->enc, c, 64);
+    std::memset(a->dec, 0x80, 256);
+    for (int v = 0; v < 64; ++v) a->dec[c[v]] = static_cast<uint8_t>(v);
+    a->pad = p;
+    a->reserved[0] = a->reserved[1] = a->reserved[2] = 0;
+    return B64_OK;
+}
+
+const b64_alphabet* b64_alphabet_standard(void) {
+    static b64_alphabet a;
+    static int once = (b64_alphabet_init(&a, kStdChars, '=', nullptr), 0);
+    (void)once;
+    return &a;
+}
+
+const b64_alphabet* b64_alphabet_url(void) {
+    static b64_alphabet a;
+    static int once = (b64_alphabet_init(&a, kUrlChars, '=', nullptr), 0);
+    (void)once;
+    return &a;
+}
+
+int64_t b64_encoded_len(int64_t n) { return n < 0 ? -1 : 4 * ((n + 2) / 3); }
+int64_t b64_decoded_len_max(int64_t m) { return m < 0 ? -1 : 3 * (m / 4); }
+
+int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabet* a, b64_stream_t stream) {
+    if (n < 0 || !alpha_ok(a)) return B64_EINVAL;
+    if (n == 0) return B64_OK;
+    if (!d_in || !d_out) return B64_EINVAL;
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (aligned(d_in, 8) && aligned(d_out, 32)) {
+        const int64_t nchunk = n / 768;
+        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_fast);
+        enc_fast_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, n, d_out, enc_tab(a), a->pad);
+    } else {
+        Offsets off{nullptr, nullptr, 1, n};
+        const int64_t blocks = clamp_grid((n / 12 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_gen);
+        enc_generic_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, d_out, off, enc_tab(a), a->pad);
+    }
+    return launched();
+}
+
+static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t base,
+                         int is_final, int64_t* cell, int64_t* out_len, cudaStream_t s) {
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(cell);
+    if (aligned(d_in, 32) && aligned(d_out, 8)) {
+        const int64_t nchunk = (m / 4) / 256;
+        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_fast);
+        dec_fast_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, m, d_out, dec_tab(a), base, is_final, c, out_len);
+    } else {
+        Offsets off{nullptr, nullptr, 1, m};
+        const int64_t blocks = clamp_grid((m / 16 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_gen);
+        dec_generic_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, d_out, off, dec_tab(a), base, is_final, c, out_len);
+    }
+    return launched();
+}
+
+int b64_decode_ex(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t* d_err_off,
+                  int32_t* d_status, int64_t* d_out_len, b64_stream_t stream) {
+    if (m < 0 || !alpha_ok(a) || !d_err_off) return B64_EINVAL;
+    if (m % 4) return B64_ELENGTH;
+    if (m > 0 && (!d_in || !d_out)) return B64_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), s) != cudaSuccess) return B64_ECUDA;
+    if (m > 0) {
+        const int r = decode_launch(d_in, m, d_out, a, 0, 1, d_err_off, nullptr, s);
+        if (r != B64_OK) return r;
+    }
+    dec_finalize_single_kernel<<<1, 1, 0, s>>>(d_err_off, d_status, d_out_len, d_in, m, a->pad);
+    return launched();
+}
+
+int b64_decode(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t* d_err_off,
+               b64_stream_t stream) {
+    return b64_decode_ex(d_in, m, d_out, a, d_err_off, nullptr, nullptr, stream);
+}
+
+int b64_decode_chunk(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t base_offset,
+                     int is_final_chunk, int64_t* d_err_min, int64_t* d_out_len, b64_stream_t stream) {
+    if (m < 0 || base_offset < 0 || !alpha_ok(a) || !d_err_min) return B64_EINVAL;
+    if (m % 4) return B64_ELENGTH;
+    if (m > 0 && (!d_in || !d_out)) return B64_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (m == 0) {
+        if (d_out_len && cudaMemsetAsync(d_out_len, 0, sizeof(int64_t), s) != cudaSuccess) return B64_ECUDA;
+        return B64_OK;
+    }
+    return decode_launch(d_in, m, d_out, a, base_offset, is_final_chunk ? 1 : 0, d_err_min, d_out_len, s);
+}
+
+int b64_decode_finalize(const int64_t* d_err_min, int64_t* d_err_off, int32_t* d_status, b64_stream_t stream) {
+    if (!d_err_min || !d_err_off) return B64_EINVAL;
+    dec_finalize_packed_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_err_min, d_err_off, d_status);
+    return launched();
+}
+
+int b64_encode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count, uint8_t* d_out,
+                     const int64_t* d_out_off, const b64_alphabet* a, b64_stream_t stream) {
+    if (count < 0 || !alpha_ok(a)) return B64_EINVAL;
+    if (count == 0) return B64_OK;
+    if (!d_in || !d_in_off || !d_out || !d_out_off) return B64_EINVAL;
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    Offsets off{d_in_off, d_out_off, count, 0};
+    const int64_t blocks = int64_t(di->sms) * di->occ_enc_gen;
+    enc_generic_kernel<<<unsigned(blocks), kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        d_in, d_out, off, enc_tab(a), a->pad);
+    return launched();
+}
+
+int b64_decode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count, uint8_t* d_out,
+                     const int64_t* d_out_off, const b64_alphabet* a, int32_t* d_status, int64_t* d_err_off,
+                     int64_t* d_out_len, b64_stream_t stream) {
+    if (count < 0 || !alpha_ok(a)) return B64_EINVAL;
+    if (count == 0) return B64_OK;
+    if (!d_in || !d_in_off || !d_out || !d_out_off || !d_err_off) return B64_EINVAL;
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t small = clamp_grid((count + kThreads - 1) / kThreads, int64_t(di->sms) * 8);
+    dec_batch_init_kernel<<<unsigned(small), kThreads, 0, s>>>(d_err_off, count);
+    int r = launched();
+    if (r != B64_OK) return r;
+    Offsets off{d_in_off, d_out_off, count, 0};
+    const int64_t blocks = int64_t(di->sms) * di->occ_dec_gen;
+    dec_generic_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, d_out, off, dec_tab(a), 0, 1,
+                                                             reinterpret_cast<unsigned long long*>(d_err_off), nullptr);
+    r = launched();
+    if (r != B64_OK) return r;
+    dec_batch_finalize_kernel<<<unsigned(small), kThreads, 0, s>>>(d_in, d_in_off, count, a->pad, d_status,
+                                                                   d_err_off, d_out_len);
+    return launched();
+}
+
+int64_t b64_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char* b64_build_info(void) {
+#define B64_STR2(x) #x
+#define B64_STR(x) B64_STR2(x)
+    return "b64gpu sm_100a, nvcc " B64_STR(__CUDACC_VER_MAJOR__) "." B64_STR(__CUDACC_VER_MINOR__)
+           "; kernels enc_fast enc_generic dec_fast dec_generic dec_finalize_* dec_batch_*";
+}
+
+}  // extern "C"

@@ -1,0 +1,265 @@
+// decode.cu -- sm_100a validating base64 decode kernels (Sec. 2, 3.2).
+//
+// dec_fast_kernel: one stream (or one shard of it), d_in 32-byte and d_out
+//   8-byte aligned.  Warp-chunk = 1024 chars (256 quads) -> 768 bytes.  Lane l
+//   owns chars [32l, 32l+32): ONE lane-linear LDG.256 (sector-perfect, fully
+//   coalesced) and three STG.64 at a lane stride of 24 B that together cover
+//   768 contiguous bytes (merged in L2 before write-back).  Every lane ORs its
+//   translated values into one register (the paper's error register,
+//   PAPER.md:305-313); the warp votes once per chunk and only on a set 0x80
+//   bit locates the first bad char (__reduce_min_sync + one 64-bit atomicMin
+//   of the packed word pos<<3|kind).  Interior quads left over after the
+//   chunks go one per thread; the stream's final quad (padding, R6)
+//   is done by the grid's last thread -- "a final and separate code path"
+//   (PAPER.md:569).
+// dec_generic_kernel: any alignment, one stream or a batch of strings.
+//   Same byte-range-per-warp split as enc_generic_kernel with 16-char units
+//   -> 12 bytes.  Per string, the first (out_addr & 3) quads are done one by
+//   one so every unit's 12-byte output is 4-byte aligned (3 STG.32).
+// dec_finalize_*: map the packed error word to (err_off, status, out_len).
+#include "b64_device.cuh"
+
+namespace b64 {
+
+__device__ __forceinline__ void warp_report(bool bad, uint32_t rel, int64_t pos0, unsigned long long* cell) {
+    // rel: position of this lane's first bad char relative to pos0 (only read if bad)
+    const uint32_t r = __reduce_min_sync(kFull, bad ? rel : 0xffffffffu);
+    if ((threadIdx.x & 31) == 0) atomicMin(cell, pack_err(pos0 + int64_t(r), kBadChar));
+}
+
+__global__ void __launch_bounds__(kThreads)
+dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
+                int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
+                int64_t* __restrict__ out_len) {
+    __shared__ uint32_t s_lut[64];
+    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+
+    const int lane = threadIdx.x & 31;
+    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t nwarp = gthreads >> 5;
+    const int64_t Q = m >> 2;
+    const int64_t Qint = (is_final && Q > 0) ? Q - 1 : Q;
+    const int64_t nchunk = Qint >> 8;
+
+    for (int64_t c = gtid >> 5; c < nchunk; c += nwarp) {
+        uint32_t x[8];
+        ld256_stream(in + c * 1024 + lane * 32, x);
+        uint32_t err = 0, v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = dec_quad(x[q], lut, err);
+        uint32_t o[6];
+        dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
+        dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
+        uint8_t* dst = out + c * 768 + lane * 24;
+        st64(dst, o[0], o[1]);
+        st64(dst + 8, o[2], o[3]);
+        st64(dst + 16, o[4], o[5]);
+        const bool bad = (err & kInvalid) != 0;
+        if (__any_sync(kFull, bad)) {  // rare: locate the first invalid char of the chunk
+            uint32_t rel = 0xffffffffu;
+            if (bad) {
+                for (int q = 0; q < 8 && rel == 0xffffffffu; ++q) {
+                    const int j = first_bad_in_quad(x[q], lut);
+                    if (j < 4) rel = uint32_t(lane * 32 + q * 4 + j);
+                }
+            }
+            warp_report(bad, rel, base + c * 1024, err_cell);
+        }
+    }
+
+    // leftover interior quads, one per thread
+    for (int64_t q = (nchunk << 8) + gtid; q < Qint; q += gthreads) {
+        const uint32_t x = ld32(in + 4 * q);
+        uint32_t err = 0;
+        const uint32_t v = dec_quad(x, lut, err);
+        store_bytes(out + 3 * q, v, 3);
+        if (err & kInvalid) atomicMin(err_cell, pack_err(base + 4 * q + first_bad_in_quad(x, lut), kBadChar));
+    }
+
+    if (gtid == gthreads - 1) {
+        if (is_final && Q > 0) {
+            const int64_t q = Q - 1;
+            int bad, k;
+            uint32_t v;
+            const uint32_t kind = final_quad(ld32(in + 4 * q), lut, tab.pad, &bad, &k, &v);
+            if (kind == kOk) store_bytes(out + 3 * q, v, k);
+            else atomicMin(err_cell, pack_err(base + 4 * q + bad, kind));
+            if (out_len) *out_len = 3 * q + k;
+        } else if (out_len) {
+            *out_len = 3 * Q;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- generic / batch
+
+// Batch: err cell per string, positions relative to the string start.
+// Single: one cell, positions base + offset; is_final as given.
+__global__ void __launch_bounds__(kThreads)
+dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, DecTab tab,
+                   int64_t base, int is_final_single, unsigned long long* __restrict__ err_cells,
+                   int64_t* __restrict__ out_len_single) {
+    __shared__ uint32_t s_lut[64];
+    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const bool batch = off.in_off != nullptr;
+
+    const int lane = threadIdx.x & 31;
+    const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+
+    if (!batch && out_len_single && w == 0 && lane == 0) {
+        // bytes written assuming the chunk is valid
+        const int64_t Q = off.n >> 2;
+        int64_t ol = 3 * Q;
+        if (is_final_single && Q > 0) {
+            const uint8_t c2 = in[off.n - 2], c3 = in[off.n - 1];
+            ol -= (c2 == tab.pad) ? 2 : (c3 == tab.pad ? 1 : 0);
+        }
+        *out_len_single = ol;
+    }
+
+    const int64_t first = off.in(0);
+    const int64_t total = off.in(off.count) - first;
+    if (total <= 0) return;
+    const int64_t lo = first + (total * w) / W;
+    const int64_t hi = first + (total * (w + 1)) / W;
+    if (lo >= hi) return;
+
+    for (int64_t s = first_string_ending_after(off, lo); s < off.count; ++s) {
+        const int64_t a = off.in(s);
+        if (a >= hi) break;
+        const int64_t L = off.in(s + 1) - a;
+        if (L <= 0 || (L & 3)) continue;  // empty / LENGTH: settled by the finalize kernel
+        const int64_t ob = off.out(s);
+        const bool fin = batch ? true : (is_final_single != 0);
+        unsigned long long* cell = batch ? err_cells + s : err_cells;
+        const int64_t pbase = batch ? 0 : base;  // reported position = pbase + (char index in string)
+        const int64_t Qs = L >> 2;
+        const int64_t Qint = fin ? Qs - 1 : Qs;
+        const int64_t H = min(int64_t(reinterpret_cast<uintptr_t>(out + ob) & 3), Qint);
+        const int64_t U = (Qint - H) >> 2;       // full 4-quad units
+        const int64_t ua = a + 4 * H;             // first char of unit 0
+        const int64_t kb = lo > ua ? (lo - ua + 15) / 16 : 0;
+        const int64_t ke = min(U, (hi - ua + 15) / 16);
+        for (int64_t k0 = kb; k0 < ke; k0 += 32) {
+            const int64_t k = k0 + lane;
+            const bool act = k < ke;
+            uint32_t err = 0, x[4];
+            if (act) {
+                ld_unaligned<4>(in + ua + 16 * k, x);
+                const uint32_t v0 = dec_quad(x[0], lut, err), v1 = dec_quad(x[1], lut, err);
+                const uint32_t v2 = dec_quad(x[2], lut, err), v3 = dec_quad(x[3], lut, err);
+                uint32_t o0, o1, o2;
+                dec_pack12(v0, v1, v2, v3, o0, o1, o2);
+                uint32_t* dst = reinterpret_cast<uint32_t*>(out + ob + 3 * H + 12 * k);
+                dst[0] = o0; dst[1] = o1; dst[2] = o2;
+            }
+            const bool bad = act && (err & kInvalid);
+            if (__any_sync(kFull, bad)) {
+                uint32_t rel = 0xffffffffu;
+                if (bad) {
+                    for (int q = 0; q < 4 && rel == 0xffffffffu; ++q) {
+                        const int j = first_bad_in_quad(x[q], lut);
+                        if (j < 4) rel = uint32_t(lane * 16 + q * 4 + j);
+                    }
+                }
+                warp_report(bad, rel, pbase + (ua - a) + 16 * k0, cell);
+            }
+        }
+        // quads outside full units: head [0,H), tail [H+4U, Qint), final Qs-1
+        const int64_t ntail = Qint - (H + 4 * U);
+        const int nsc = int(H + ntail + (fin ? 1 : 0));
+        if (lane < nsc) {
+            int64_t j;
+            if (lane < H) j = lane;
+            else if (lane < H + ntail) j = H + 4 * U + (lane - H);
+            else j = Qs - 1;
+            const int64_t p = a + 4 * j;
+            if (p >= lo && p < hi) {
+                const uint8_t* src = in + p;
+                const uint32_t x = uint32_t(src[0]) | (uint32_t(src[1]) << 8) | (uint32_t(src[2]) << 16) |
+                                   (uint32_t(src[3]) << 24);
+                if (fin && j == Qs - 1) {
+                    int badj, kk;
+                    uint32_t v;
+                    const uint32_t kind = final_quad(x, lut, tab.pad, &badj, &kk, &v);
+                    if (kind == kOk) store_bytes(out + ob + 3 * j, v, kk);
+                    else atomicMin(cell, pack_err(pbase + 4 * j + badj, kind));
+                } else {
+                    uint32_t err = 0;
+                    const uint32_t v = dec_quad(x, lut, err);
+                    store_bytes(out + ob + 3 * j, v, 3);
+                    if (err & kInvalid) atomicMin(cell, pack_err(pbase + 4 * j + first_bad_in_quad(x, lut), kBadChar));
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- finalize
+
+// Single stream: the cell IS *err_off (initialised to kErrNone by memset).
+__global__ void dec_finalize_single_kernel(int64_t* err_off, int32_t* status, int64_t* out_len,
+                                           const uint8_t* __restrict__ in, int64_t m, uint32_t pad) {
+    const unsigned long long wv = *reinterpret_cast<unsigned long long*>(err_off);
+    if (wv >= kErrNone) {
+        *err_off = -1;
+        if (status) *status = kOk;
+        if (out_len) {
+            int64_t ol = 3 * (m >> 2);
+            if (m >= 4) ol -= (in[m - 2] == pad) ? 2 : (in[m - 1] == pad ? 1 : 0);
+            *out_len = ol;
+        }
+    } else {
+        const int64_t pos = int64_t(wv >> 3);
+        *err_off = pos;
+        if (status) *status = int32_t(wv & 7);
+        if (out_len) *out_len = 3 * (pos >> 2);
+    }
+}
+
+// Chunk / multi-GPU: packed word -> (err_off, status).
+__global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off, int32_t* status) {
+    const unsigned long long wv = *reinterpret_cast<const unsigned long long*>(cell);
+    if (wv >= kErrNone) {
+        *err_off = -1;
+        if (status) *status = kOk;
+    } else {
+        *err_off = int64_t(wv >> 3);
+        if (status) *status = int32_t(wv & 7);
+    }
+}
+
+__global__ void dec_batch_init_kernel(int64_t* err, int64_t count) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+        err[i] = int64_t(kErrNone);
+}
+
+__global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
+                                          int64_t count, uint32_t pad, int32_t* status, int64_t* err,
+                                          int64_t* out_len) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t a = in_off[i], L = in_off[i + 1] - a;
+        const unsigned long long wv = static_cast<unsigned long long>(err[i]);
+        int32_t st;
+        int64_t e, ol;
+        if (L & 3) {
+            st = kLength; e = L - (L & 3); ol = 0;
+        } else if (wv >= kErrNone) {
+            st = kOk; e = -1; ol = 3 * (L >> 2);
+            if (L >= 4) ol -= (in[a + L - 2] == pad) ? 2 : (in[a + L - 1] == pad ? 1 : 0);
+        } else {
+            e = int64_t(wv >> 3); st = int32_t(wv & 7); ol = 3 * (e >> 2);
+        }
+        err[i] = e;
+        if (status) status[i] = st;
+        if (out_len) out_len[i] = ol;
+    }
+}
+
+}  // namespace b64

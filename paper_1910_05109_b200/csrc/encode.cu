@@ -1,0 +1,156 @@
+// encode.cu -- sm_100a base64 encode kernels (Sec. 2 / Sec. 3.1).
+//
+// enc_fast_kernel: one stream, d_in 8-byte and d_out 32-byte aligned.
+//   Warp-chunk = 768 input bytes (256 triples) -> 1024 chars.  Lane l owns
+//   bytes [24l, 24l+24) = 8 triples -> 32 chars: three LDG.64 at a lane stride
+//   of 24 B (together one contiguous 768 B range, L1-merged) and ONE lane-linear
+//   STG.256 (32 lanes x 32 B = 1 KiB, fully coalesced, sector-perfect).
+//   Two chunks per warp per iteration keep >= 1.5 KiB of reads in flight per
+//   warp (Little's law).  The <768 B remainder (full
+//   triples + the 1-2 byte padded tail) is done by the
+//   first threads of the grid, one output quad each.
+// enc_generic_kernel: any alignment, one stream or a batch of strings
+//   (BASELINE.json configs[3]).  The concatenated input is split into equal
+//   byte ranges, one per warp; a warp encodes every 12-byte unit (4 triples ->
+//   16 chars) whose first byte lies in its range, so long strings spread over
+//   many warps and short strings pack many per warp.
+#include "b64_device.cuh"
+
+namespace b64 {
+
+__device__ __forceinline__ void enc_lane24(const uint8_t* __restrict__ src, uint32_t (&w)[6]) {
+    const uint2 a = ld64_l1(src), b = ld64_l1(src + 8), c = ld64_l1(src + 16);
+    w[0] = a.x; w[1] = a.y; w[2] = b.x; w[3] = b.y; w[4] = c.x; w[5] = c.y;
+}
+
+__device__ __forceinline__ void enc_lane_compute(const uint32_t (&w)[6], uint32_t (&o)[8],
+                                                 const uint8_t* __restrict__ lut) {
+    o[0] = enc_triple(__byte_perm(w[0], w[1], 0x0122), lut);
+    o[1] = enc_triple(__byte_perm(w[0], w[1], 0x3455), lut);
+    o[2] = enc_triple(__byte_perm(w[1], w[2], 0x2344), lut);
+    o[3] = enc_triple(__byte_perm(w[2], w[3], 0x1233), lut);
+    o[4] = enc_triple(__byte_perm(w[3], w[4], 0x0122), lut);
+    o[5] = enc_triple(__byte_perm(w[3], w[4], 0x3455), lut);
+    o[6] = enc_triple(__byte_perm(w[4], w[5], 0x2344), lut);
+    o[7] = enc_triple(__byte_perm(w[5], w[5], 0x1233), lut);
+}
+
+__global__ void __launch_bounds__(kThreads)
+enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab, uint32_t pad) {
+    __shared__ uint32_t s_lut[16];
+    if (threadIdx.x < 16) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+
+    const int lane = threadIdx.x & 31;
+    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t nwarp = gthreads >> 5;
+    const int64_t nchunk = n / 768;
+
+    int64_t c = gtid >> 5;
+    for (; c + nwarp < nchunk; c += 2 * nwarp) {
+        uint32_t wa[6], wb[6], o[8];
+        enc_lane24(in + c * 768 + lane * 24, wa);
+        enc_lane24(in + (c + nwarp) * 768 + lane * 24, wb);
+        enc_lane_compute(wa, o, lut);
+        st256(out + c * 1024 + lane * 32, o);
+        enc_lane_compute(wb, o, lut);
+        st256(out + (c + nwarp) * 1024 + lane * 32, o);
+    }
+    if (c < nchunk) {
+        uint32_t w[6], o[8];
+        enc_lane24(in + c * 768 + lane * 24, w);
+        enc_lane_compute(w, o, lut);
+        st256(out + c * 1024 + lane * 32, o);
+    }
+
+    // remainder: output quads [256*nchunk, ceil(n/3)), one per thread
+    const int64_t T = n / 3;
+    const int64_t Q = (n + 2) / 3;
+    for (int64_t q = nchunk * 256 + gtid; q < Q; q += gthreads) {
+        const uint8_t* s = in + 3 * q;
+        uint32_t word;
+        if (q < T) {
+            const uint32_t x = (uint32_t(s[0]) << 24) | (uint32_t(s[1]) << 16) | (uint32_t(s[2]) << 8);
+            word = enc_triple(x, lut);
+        } else {
+            const int r = int(n - 3 * q);
+            word = enc_partial(s[0], r == 2 ? s[1] : 0u, r, lut, pad);
+        }
+        *reinterpret_cast<uint32_t*>(out + 4 * q) = word;  // out 32-aligned => 4-aligned
+    }
+}
+
+// ---------------------------------------------------------------- generic / batch
+
+__device__ __forceinline__ void store16(uint8_t* dst, const uint32_t (&o)[4]) {
+    const uintptr_t u = reinterpret_cast<uintptr_t>(dst);
+    if ((u & 15) == 0) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+    } else if ((u & 3) == 0) {
+        uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+        d[0] = o[0]; d[1] = o[1]; d[2] = o[2]; d[3] = o[3];
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) dst[i] = uint8_t(o[i >> 2] >> (8 * (i & 3)));
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab, uint32_t pad) {
+    __shared__ uint32_t s_lut[16];
+    if (threadIdx.x < 16) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+
+    const int lane = threadIdx.x & 31;
+    const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t base = off.in(0);
+    const int64_t total = off.in(off.count) - base;
+    if (total <= 0) return;
+    const int64_t lo = base + (total * w) / W;
+    const int64_t hi = base + (total * (w + 1)) / W;
+    if (lo >= hi) return;
+
+    for (int64_t s = first_string_ending_after(off, lo); s < off.count; ++s) {
+        const int64_t a = off.in(s);
+        if (a >= hi) break;
+        const int64_t L = off.in(s + 1) - a;
+        if (L <= 0) continue;
+        const int64_t ob = off.out(s);
+        const int64_t nunit = (L + 11) / 12;
+        const int64_t kb = lo > a ? (lo - a + 11) / 12 : 0;
+        const int64_t ke = min(nunit, (hi - a + 11) / 12);
+        for (int64_t k = kb + lane; k < ke; k += 32) {
+            const uint8_t* src = in + a + 12 * k;
+            uint8_t* dst = out + ob + 16 * k;
+            const int64_t rem = L - 12 * k;
+            if (rem >= 12) {
+                uint32_t wv[3], o[4];
+                ld_unaligned<3>(src, wv);
+                enc12(wv[0], wv[1], wv[2], o, lut);
+                store16(dst, o);
+            } else {
+                // last unit of the string: whole triples, then the padded tail
+                int t = 0;
+                for (; 3 * t + 3 <= rem; ++t) {
+                    const uint32_t x = (uint32_t(src[3 * t]) << 24) | (uint32_t(src[3 * t + 1]) << 16) |
+                                       (uint32_t(src[3 * t + 2]) << 8);
+                    const uint32_t v = enc_triple(x, lut);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) dst[4 * t + i] = uint8_t(v >> (8 * i));
+                }
+                const int r = int(rem - 3 * t);
+                if (r > 0) {
+                    const uint32_t v = enc_partial(src[3 * t], r == 2 ? src[3 * t + 1] : 0u, r, lut, pad);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) dst[4 * t + i] = uint8_t(v >> (8 * i));
+                }
+            }
+        }
+    }
+}
+
+}  // namespace b64

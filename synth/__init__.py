@@ -114,3 +114,47 @@ def pick(count: int, frac: float, seed: int = 0) -> np.ndarray:
     w = words(seed, SID_PICK, 0, count)
     thr = np.uint64(int(frac * 2.0 ** 64) if frac < 1 else 0xFFFFFFFFFFFFFFFF)
     return np.nonzero(w < thr)[0].astype(np.int64)
+
+
+# ---------------------------------------------------------------- device twin
+
+_dev_lib = None
+
+
+def _device_lib():
+    global _dev_lib
+    if _dev_lib is None:
+        import ctypes
+        import os
+
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsynth.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} not built (run __graft_entry__.build())")
+        L = ctypes.CDLL(path)
+        L.synth_fill.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
+                                 ctypes.c_void_p]
+        L.synth_fill.restype = ctypes.c_int
+        _dev_lib = L
+    return _dev_lib
+
+
+def device_fill(t, seed: int = 0, sid: int = SID_DATA, offset: int = 0, stream=None):
+    """Fill a contiguous uint8 CUDA tensor with bytes [offset, offset + numel) of stream (seed, sid)."""
+    import ctypes
+
+    import torch
+
+    assert t.dtype == torch.uint8 and t.is_cuda and t.is_contiguous()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    rc = _device_lib().synth_fill(ctypes.c_void_p(t.data_ptr()), t.numel(), seed, sid, offset,
+                                  ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"synth_fill failed: {rc}")
+    return t
+
+
+def device_data(n: int, seed: int = 0, offset: int = 0, device="cuda"):
+    import torch
+
+    t = torch.empty(n, dtype=torch.uint8, device=device)
+    return device_fill(t, seed, SID_DATA, offset)

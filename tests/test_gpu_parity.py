@@ -1,0 +1,420 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, bit-exact.
+
+Every comparison is element by element on the same seeded inputs (synth/):
+encoded chars, decoded bytes (the exact prefix on error), err_off, status and
+out_len.  Sizes span several warp-chunks (768 B / 1024 chars) with ragged
+tails, misaligned pointers (the generic kernels), every byte value at every
+position of small texts, and BASELINE.json's configs at full size (sampled
+windows where the oracle would need more host memory than is sensible).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def b64():
+    import __graft_entry__ as g
+
+    g.build()
+    import paper_1910_05109_b200 as m
+
+    assert torch.cuda.is_available()
+    return m
+
+
+def _alphabets(b64):
+    rng = np.random.default_rng(7)
+    out = [(oracle.STANDARD, oracle.PAD, b64.standard()), (oracle.URL, oracle.PAD, b64.url())]
+    while len(out) < 7:
+        perm = rng.permutation(127)[:65]
+        chars, pad = bytes(perm[:64].tolist()), int(perm[64])
+        out.append((chars, pad, b64.alphabet(chars, bytes([pad]))))
+    return out
+
+
+def to_dev(x: np.ndarray, offset: int = 0) -> torch.Tensor:
+    """Copy to the device at a chosen byte misalignment (offset) inside a fresh buffer."""
+    buf = torch.empty(x.size + offset + 64, dtype=torch.uint8, device=DEV)
+    t = buf[offset: offset + x.size]
+    if x.size:
+        t.copy_(torch.from_numpy(x))
+    return t
+
+
+def dec_check(b64, text: np.ndarray, chars, pad, alpha, off_in=0, off_out=0):
+    t = to_dev(text, off_in)
+    cap = 3 * (text.size // 4)
+    obuf = torch.empty(cap + off_out + 64, dtype=torch.uint8, device=DEV)
+    out, info = b64.decode_async(t, alpha, out=obuf[off_out: off_out + max(cap, 1)])
+    err, st, olen = info.tolist()
+    ref, rerr, rst = oracle.decode(text, chars, pad)
+    assert (err, st) == (rerr, rst), (err, st, rerr, rst)
+    assert olen == ref.size
+    assert np.array_equal(out[:olen].cpu().numpy(), ref)
+    return err
+
+
+# ------------------------------------------------------------------ generator twin
+
+def test_synth_device_matches_host(b64):
+    for n, off in ((0, 0), (1, 0), (7, 3), (4096, 0), (100003, 5), (1 << 20, 13), (3000, 1 << 33)):
+        d = torch.empty(n + 16, dtype=torch.uint8, device=DEV)
+        for shift in (0, 3):
+            t = d[shift: shift + n]
+            synth.device_fill(t, seed=0, offset=off)
+            assert np.array_equal(t.cpu().numpy(), synth.data(n, 0, off)), (n, off, shift)
+
+
+# ------------------------------------------------------------------ encode
+
+def test_encode_fuzz_lengths(b64):
+    al = _alphabets(b64)
+    for n in range(0, 4097):
+        chars, pad, alpha = al[n % len(al)]
+        x = synth.data(n, seed=n)
+        t = b64.encode(to_dev(x), alpha)
+        assert np.array_equal(t.cpu().numpy(), oracle.encode(x, chars, pad)), n
+
+
+def test_encode_chunk_boundaries(b64):
+    for k in (1, 2, 3, 37, 148 * 8, 148 * 8 * 2 + 5):
+        for r in range(0, 24):
+            n = 768 * k + r
+            x = synth.data(n, seed=k * 100 + r)
+            t = b64.encode(to_dev(x))
+            assert np.array_equal(t.cpu().numpy(), oracle.encode(x)), n
+
+
+def test_encode_misaligned_generic(b64):
+    al = _alphabets(b64)
+    for i, n in enumerate((1, 2, 11, 12, 13, 100, 767, 768, 769, 5000, 100003)):
+        for oi in (0, 1, 2, 3, 5):
+            for oo in (0, 1, 2, 4, 16):
+                if oi == 0 and oo == 0:
+                    continue
+                chars, pad, alpha = al[(i + oi + oo) % len(al)]
+                x = synth.data(n, seed=n + oi)
+                obuf = torch.empty(b64.encoded_len(n) + oo + 64, dtype=torch.uint8, device=DEV)
+                t = b64.encode(to_dev(x, oi), alpha, out=obuf[oo:])
+                assert np.array_equal(t.cpu().numpy(), oracle.encode(x, chars, pad)), (n, oi, oo)
+
+
+# ------------------------------------------------------------------ decode
+
+def test_decode_fuzz_valid_and_corrupted(b64):
+    al = _alphabets(b64)
+    for n in range(0, 3100, 7):
+        chars, pad, alpha = al[n % len(al)]
+        x = synth.data(n, seed=n)
+        text = oracle.encode(x, chars, pad)
+        assert dec_check(b64, text, chars, pad, alpha) == -1
+        if text.size:
+            k = 1 + n % 3
+            pos, bad = synth.corruption(min(k, text.size), text.size, chars, seed=n, pad=pad)
+            t2 = text.copy()
+            t2[pos] = bad
+            assert dec_check(b64, t2, chars, pad, alpha) == int(pos.min())
+            # non-ASCII bytes and a misplaced pad are invalid too
+            t3 = text.copy()
+            p = int(pos[0])
+            t3[p] = 0x80 | (n & 0x7F)
+            dec_check(b64, t3, chars, pad, alpha)
+            if p < text.size - 4:
+                t3[p] = pad
+                assert dec_check(b64, t3, chars, pad, alpha) == p
+
+
+def test_decode_every_byte_every_position(b64):
+    """Exhaustive substitution on small texts (interior + all final-quad forms)."""
+    std = b64.standard()
+    for raw_len in (30, 31, 32):  # final quad 'xxxx', 'xx==', 'xxx='
+        text = oracle.encode(synth.data(raw_len, seed=raw_len))
+        for p in range(text.size):
+            for v in range(256):
+                t = text.copy()
+                t[p] = v
+                dec_check(b64, t, oracle.STANDARD, oracle.PAD, std)
+
+
+def test_decode_chunk_boundaries_and_errors(b64):
+    std = b64.standard()
+    for k in (1, 2, 5, 148 * 8 + 3):
+        for r in (0, 4, 8, 1020):
+            m_raw = (1024 * k + r) // 4 * 3 - (k % 3)
+            x = synth.data(m_raw, seed=k + r)
+            text = oracle.encode(x)
+            dec_check(b64, text, oracle.STANDARD, oracle.PAD, std)
+            for j in range(4):
+                pos, bad = synth.corruption(1 + j, text.size, oracle.STANDARD, seed=100 * k + r + j)
+                t2 = text.copy()
+                t2[pos] = bad
+                dec_check(b64, t2, oracle.STANDARD, oracle.PAD, std)
+            # error in the last char of a warp-chunk / the very last char
+            for p in {1023, min(text.size - 1, 2047), text.size - 5, text.size - 1}:
+                if 0 <= p < text.size:
+                    t2 = text.copy()
+                    t2[p] = ord("*")
+                    dec_check(b64, t2, oracle.STANDARD, oracle.PAD, std)
+
+
+def test_decode_misaligned_generic(b64):
+    al = _alphabets(b64)
+    for i, n in enumerate((0, 1, 2, 3, 4, 12, 13, 47, 48, 49, 767, 768, 4000, 100001)):
+        chars, pad, alpha = al[i % len(al)]
+        text = oracle.encode(synth.data(n, seed=n), chars, pad)
+        for oi in (0, 1, 3, 4, 16):
+            for oo in (0, 1, 2, 3, 8):
+                if oi == 0 and oo == 0:
+                    continue
+                dec_check(b64, text, chars, pad, alpha, oi, oo)
+                if text.size > 8:
+                    pos, bad = synth.corruption(2, text.size, chars, seed=n + oi + oo, pad=pad)
+                    t2 = text.copy()
+                    t2[pos] = bad
+                    dec_check(b64, t2, chars, pad, alpha, oi, oo)
+
+
+def test_decode_length_error_sync(b64):
+    with pytest.raises(b64.B64Error, match="ELENGTH"):
+        b64.decode(torch.zeros(5, dtype=torch.uint8, device=DEV))
+    out, err = b64.decode(torch.zeros(0, dtype=torch.uint8, device=DEV))
+    assert err == -1 and out.numel() == 0
+
+
+def test_decode_chunk_api_shards(b64):
+    """b64_decode_chunk over shards at arbitrary 4-char boundaries + device MIN == oracle."""
+    std = b64.standard()
+    x = synth.data(300_001, seed=5)
+    text = oracle.encode(x)
+    m = text.size
+    for trial in range(6):
+        t2 = text.copy()
+        if trial:
+            pos, bad = synth.corruption(trial, m, oracle.STANDARD, seed=trial)
+            t2[pos] = bad
+        ref, rerr, rst = oracle.decode(t2)
+        Q = m // 4
+        cuts = sorted({0, Q} | {int(q) for q in synth.words(9, 9, trial * 8, 5) % Q})
+        dt = to_dev(t2)
+        out = torch.empty(3 * Q, dtype=torch.uint8, device=DEV)
+        cells = torch.full((len(cuts) - 1,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+        for i in range(len(cuts) - 1):
+            a, b = 4 * cuts[i], 4 * cuts[i + 1]
+            b64.decode_chunk(dt[a:b], a, b == m, cells[i: i + 1], std, out=out[3 * cuts[i]: 3 * cuts[i + 1]])
+        cell = cells.min().reshape(1)
+        eo = torch.empty(1, dtype=torch.int64, device=DEV)
+        st = torch.zeros(1, dtype=torch.int32, device=DEV)
+        b64.decode_finalize(cell, eo, st)
+        assert (int(eo.item()), int(st.item())) == (rerr, rst)
+        assert np.array_equal(out[: ref.size].cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------ batched
+
+def _batch_case(count, hi, seed, corrupt_frac=0.01):
+    L = synth.loguniform_lengths(count, hi=hi, seed=seed)
+    off = synth.offsets(L)
+    x = synth.data(int(off[-1]), seed=seed)
+    return L, off, x
+
+
+def test_batch_encode_decode_vs_oracle(b64):
+    for count, hi, seed in ((1, 10, 1), (7, 100, 2), (5000, 65536, 3), (20000, 4096, 4)):
+        L, off, x = _batch_case(count, hi, seed)
+        doff = torch.from_numpy(off).to(DEV)
+        enc, eoff = b64.encode_batch(to_dev(x), doff)
+        renc, reoff = oracle.encode_batch(x, off)
+        assert np.array_equal(eoff.cpu().numpy(), reoff)
+        assert np.array_equal(enc[: reoff[-1]].cpu().numpy(), renc)
+        # corrupt ~1% of strings (seeded), plus a few length errors
+        text = renc.copy()
+        tl = np.diff(reoff)
+        picks = synth.pick(count, 0.01, seed=seed)
+        for i in picks:
+            if tl[i]:
+                pos, bad = synth.corruption(1, int(tl[i]), oracle.STANDARD, seed=int(i))
+                text[reoff[i] + pos] = bad
+        din = reoff.copy()
+        if count > 3:  # make string 1 end mid-quad: shift the boundary by 1
+            din[2] -= 1 if tl[1] > 0 else 0
+        out, ooff, st, err, olen = b64.decode_batch(to_dev(text), torch.from_numpy(din).to(DEV))
+        rout, rooff, rst, rerr, rolen = oracle.decode_batch(text, din)
+        assert np.array_equal(ooff.cpu().numpy(), rooff)
+        assert np.array_equal(st.cpu().numpy(), rst)
+        assert np.array_equal(err.cpu().numpy(), rerr)
+        assert np.array_equal(olen.cpu().numpy(), rolen)
+        o = out.cpu().numpy()
+        for i in range(count):
+            assert np.array_equal(o[rooff[i]: rooff[i] + rolen[i]], rout[rooff[i]: rooff[i] + rolen[i]]), i
+
+
+def test_batch_misaligned_offsets(b64):
+    """String starts at every alignment: input offsets shifted by a 1..3 byte prefix gap."""
+    for gap in (1, 2, 3):
+        L = np.array([0, 1, 2, 3, 4, 5, 47, 48, 49, 100, 0, 767, 1024, 3000, 1], dtype=np.int64)
+        Lg = L + gap
+        off = synth.offsets(Lg)
+        x = synth.data(int(off[-1]), seed=gap)
+        in_off = off.copy()
+        in_off[:-1] += gap  # each string starts gap bytes into its slot
+        starts, ends = in_off[:-1], off[1:]
+        # encode: strings [starts[i], ends[i])
+        # (offsets must be non-decreasing: represent as pairs via interleaved empty strings)
+        pairs = np.empty(2 * len(L) + 1, dtype=np.int64)
+        pairs[0] = 0
+        pairs[1::2] = starts
+        pairs[2::2] = ends
+        enc, eoff = b64.encode_batch(to_dev(x), torch.from_numpy(pairs).to(DEV))
+        renc, reoff = oracle.encode_batch(x, pairs)
+        assert np.array_equal(enc[: reoff[-1]].cpu().numpy(), renc)
+        # decode the encoded strings placed back at odd offsets
+        tl = np.diff(reoff)
+        text = np.concatenate([np.concatenate([np.full(gap, ord("A"), np.uint8), renc[reoff[i]: reoff[i + 1]]])
+                               for i in range(len(tl))])
+        toff = synth.offsets(tl + gap)
+        tp = np.empty(2 * len(tl) + 1, dtype=np.int64)
+        tp[0] = 0
+        tp[1::2] = toff[:-1] + gap
+        tp[2::2] = toff[1:]
+        out, ooff, st, err, olen = b64.decode_batch(to_dev(text), torch.from_numpy(tp).to(DEV))
+        rout, rooff, rst, rerr, rolen = oracle.decode_batch(text, tp)
+        assert np.array_equal(st.cpu().numpy(), rst)
+        assert np.array_equal(err.cpu().numpy(), rerr)
+        assert np.array_equal(olen.cpu().numpy(), rolen)
+        o = out.cpu().numpy()
+        for i in range(len(rolen)):
+            assert np.array_equal(o[rooff[i]: rooff[i] + rolen[i]], rout[rooff[i]: rooff[i] + rolen[i]])
+
+
+# ------------------------------------------------------------------ BASELINE.json configs at full size
+
+def test_config1_full(b64):
+    """1 MiB seed 0, std: encode 1,398,104 chars ('=='), round trip, 16 corruptions."""
+    std = b64.standard()
+    x = synth.data(1048576, seed=0)
+    t = b64.encode(to_dev(x), std)
+    ref = oracle.encode(x)
+    assert t.numel() == 1398104 and np.array_equal(t.cpu().numpy(), ref)
+    y, err = b64.decode(t, std)
+    assert err == -1 and np.array_equal(y.cpu().numpy(), x)
+    pos, bad = synth.corruption(16, ref.size, oracle.STANDARD, seed=0)
+    t2 = ref.copy()
+    t2[pos] = bad
+    assert dec_check(b64, t2, oracle.STANDARD, oracle.PAD, std) == int(pos.min())
+
+
+def test_config2_full(b64):
+    """64 MiB at n, n+1, n+2 with std and url selected at runtime; full outputs vs oracle."""
+    for n in (67108864, 67108865, 67108866):
+        x = synth.data(n, seed=0)
+        xd = to_dev(x)
+        for chars, alpha in ((oracle.STANDARD, b64.standard()), (oracle.URL, b64.url())):
+            t = b64.encode(xd, alpha)
+            ref = oracle.encode(x, chars)
+            assert t.numel() == 89478488
+            assert np.array_equal(t.cpu().numpy(), ref)
+            y, err = b64.decode(t, alpha)
+            assert err == -1 and y.numel() == n and torch.equal(y, xd)
+
+
+def _windows(total, count, width, seed):
+    starts = (synth.words(seed, 7, 0, count) % np.uint64(max(total - width, 1))).astype(np.int64)
+    return sorted(set([0, max(total - width, 0)] + starts.tolist()))
+
+
+def test_config3_full_1gib(b64):
+    """1 GiB encoded to 1,431,655,768 chars (device-generated); sampled windows vs oracle,
+    round trip on device, and one corruption located exactly."""
+    n = 1 << 30
+    x = synth.device_data(n, seed=0)
+    t = b64.encode(x)
+    assert t.numel() == 1431655768
+    for s in _windows(n // 3, 48, 4096, seed=3):
+        a = 3 * s
+        w = min(3 * 4096, n - a)
+        ref = oracle.encode(synth.data(w, seed=0, offset=a))
+        assert np.array_equal(t[4 * s: 4 * s + ref.size].cpu().numpy(), ref), s
+    y, err = b64.decode(t)
+    assert err == -1 and y.numel() == n and torch.equal(y, x)
+    del y
+    pos = 987_654_321
+    t[pos] = ord("%")
+    y, err = b64.decode(t)
+    assert err == pos
+
+
+def test_config4_full_batch(b64):
+    """10^6 strings, log-uniform lengths in [1, 64 KiB]; sampled strings vs oracle, 1% corrupted."""
+    count = 1_000_000
+    L = synth.loguniform_lengths(count, seed=0)
+    off = synth.offsets(L)
+    total = int(off[-1])
+    x = synth.device_data(total, seed=0)
+    doff = torch.from_numpy(off).to(DEV)
+    enc, eoff = b64.encode_batch(x, doff)
+    reoff = np.zeros(count + 1, np.int64)
+    np.cumsum(4 * ((L + 2) // 3), out=reoff[1:])
+    assert np.array_equal(eoff.cpu().numpy(), reoff)
+    sample = sorted(set((synth.words(0, 8, 0, 3000) % np.uint64(count)).astype(np.int64).tolist()) | {0, count - 1})
+    for i in sample:
+        xi = synth.data(int(L[i]), seed=0, offset=int(off[i]))
+        assert np.array_equal(enc[reoff[i]: reoff[i + 1]].cpu().numpy(), oracle.encode(xi)), i
+    picks = synth.pick(count, 0.01, seed=0)
+    tl = np.diff(reoff)
+    ppos = []
+    for i in picks[:5000]:
+        pos, bad = synth.corruption(1, int(tl[i]), oracle.STANDARD, seed=int(i))
+        enc[int(reoff[i] + pos[0])] = int(bad[0])
+        ppos.append(int(pos[0]))
+    out, ooff, st, err, olen = b64.decode_batch(enc, eoff)
+    stc, errc, olenc = st.cpu().numpy(), err.cpu().numpy(), olen.cpu().numpy()
+    bad_idx = picks[:5000]
+    assert np.array_equal(errc[bad_idx], np.array(ppos))
+    assert (stc[bad_idx] == oracle.ST_BADCHAR).all()
+    good = np.ones(count, bool)
+    good[bad_idx] = False
+    assert (errc[good] == -1).all() and (stc[good] == 0).all() and np.array_equal(olenc[good], L[good])
+    oo = ooff.cpu().numpy()
+    for i in sample:
+        if good[i]:
+            xi = synth.data(int(L[i]), seed=0, offset=int(off[i]))
+            assert np.array_equal(out[oo[i]: oo[i] + L[i]].cpu().numpy(), xi), i
+
+
+def test_config5_single_gpu_sampled(b64):
+    """Config 5's 16 GiB stream on one GPU in 4 GiB shards (chunk API, aligned cuts),
+    1000 corruptions, global err = min(positions); sampled windows vs oracle."""
+    N = 1 << 34
+    G = 4
+    T = N // 3
+    m = 4 * ((N + 2) // 3)
+    pos, bad = synth.corruption(1000, m, oracle.STANDARD, seed=0)
+    cells = torch.full((G,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+    for r in range(G):
+        t0 = (T * r // G) // 256 * 256
+        t1 = (T * (r + 1) // G) // 256 * 256 if r < G - 1 else T
+        a, b = 3 * t0, (3 * t1 if r < G - 1 else N)
+        x = synth.device_data(b - a, seed=0, offset=a)
+        t = b64.encode(x)
+        for s in _windows((b - a) // 3, 6, 2048, seed=r):
+            ref = oracle.encode(synth.data(min(3 * 2048, b - a - 3 * s), seed=0, offset=a + 3 * s))
+            assert np.array_equal(t[4 * s: 4 * s + ref.size].cpu().numpy(), ref)
+        c0, c1 = 4 * t0, 4 * t0 + t.numel()
+        sel = (pos >= c0) & (pos < c1)
+        if sel.any():
+            t[torch.from_numpy(pos[sel] - c0).to(DEV)] = torch.from_numpy(bad[sel]).to(DEV)
+        del x
+        b64.decode_chunk(t, c0, r == G - 1, cells[r: r + 1])
+        del t
+        torch.cuda.empty_cache()
+    eo = torch.empty(1, dtype=torch.int64, device=DEV)
+    b64.decode_finalize(cells.min().reshape(1), eo)
+    assert int(eo.item()) == int(pos.min())
