@@ -33,6 +33,12 @@ enum : uint32_t { kOk = 0, kBadChar = 1, kBadPad = 2, kNonCanon = 3, kLength = 4
 struct EncTab { uint32_t w[16]; };             // enc[64] chars
 struct DecTab { uint32_t w[64]; uint32_t pad; };  // dec[256] + pad char
 
+// Programmatic dependent launch (PDL): kernels are launched so the next
+// kernel on the stream may start its prologue while this one drains; each
+// kernel waits for its predecessor's memory before touching global memory.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ unsigned long long pack_err(int64_t pos, uint32_t kind) {
     return ((unsigned long long)pos << 3) | kind;
 }
@@ -64,6 +70,58 @@ __device__ __forceinline__ void st256(void* p, const uint32_t (&v)[8]) {
 }
 __device__ __forceinline__ void st64(void* p, uint32_t a, uint32_t b) {
     asm volatile("st.global.v2.u32 [%0], {%1,%2};" :: "l"(p), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void st128(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// ----------------------------------------------------------------- shared memory by 32-bit address
+// The look-up tables are addressed with 32-bit shared-window addresses so the
+// table base can be merged into the index computation (one PRMT or LOP3 per
+// character instead of extract + add).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t r;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(r) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" :: "r"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a)
+                 : "memory");
+    return v;
+}
+
+// Encode one triple (x: byte3 = s1, byte2 = s2, byte1 = s3) with the 64-entry
+// alphabet at the 64-byte-aligned shared address lb: index | lb == lb + index.
+__device__ __forceinline__ uint32_t enc_triple_s(uint32_t x, uint32_t lb) {
+    const uint32_t c0 = lds_u8((x >> 26) + lb);
+    const uint32_t c1 = lds_u8(((x >> 20) & 63u) | lb);
+    const uint32_t c2 = lds_u8(((x >> 14) & 63u) | lb);
+    const uint32_t c3 = lds_u8(((x >> 8) & 63u) | lb);
+    return __byte_perm(__byte_perm(c0, c1, 0x0040), __byte_perm(c2, c3, 0x0040), 0x5410);
+}
+
+// Decode one quad with the 256-entry table at the 256-byte-aligned shared
+// address lb: PRMT drops each char into the low byte of lb -> its entry address.
+__device__ __forceinline__ uint32_t dec_quad_s(uint32_t x, uint32_t lb, uint32_t& err) {
+    const uint32_t a = lds_u8(__byte_perm(x, lb, 0x7650));
+    const uint32_t b = lds_u8(__byte_perm(x, lb, 0x7651));
+    const uint32_t c = lds_u8(__byte_perm(x, lb, 0x7652));
+    const uint32_t d = lds_u8(__byte_perm(x, lb, 0x7653));
+    err |= a | b | c | d;
+    return (((a * 64u + b) * 64u + c) * 64u) + d;
 }
 
 // 4 aligned words starting at an arbitrary byte address p, funnel-shifted to

@@ -3,6 +3,7 @@
 // per-call state; every launch goes to the caller's stream.
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -66,6 +67,33 @@ int launched() {
     return cudaPeekAtLastError() == cudaSuccess ? B64_OK : (cudaGetLastError(), B64_ECUDA);
 }
 
+// Launch with programmatic dependent launch allowed (the kernels call
+// griddepcontrol.wait before touching global memory), so back-to-back calls on
+// one stream overlap launch latency and prologue with the previous kernel's
+// tail.  B64_NO_PDL=1 in the environment falls back to plain launches.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("B64_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch(void (*kernel)(KArgs...), int64_t grid, int block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(unsigned(block));
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 int64_t clamp_grid(int64_t want, int64_t cap) { return want < 1 ? 1 : (want > cap ? cap : want); }
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
@@ -126,11 +154,11 @@ int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabe
     if (aligned(d_in, 8) && aligned(d_out, 32)) {
         const int64_t nchunk = n / 768;
         const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_fast);
-        enc_fast_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, n, d_out, enc_tab(a), a->pad);
+        launch(enc_fast_kernel, blocks, kThreads, s, d_in, n, d_out, enc_tab(a), a->pad);
     } else {
         Offsets off{nullptr, nullptr, 1, n};
         const int64_t blocks = clamp_grid((n / 12 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_gen);
-        enc_generic_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, d_out, off, enc_tab(a), a->pad);
+        launch(enc_generic_kernel, blocks, kThreads, s, d_in, d_out, off, enc_tab(a), a->pad);
     }
     return launched();
 }
@@ -140,14 +168,14 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
     const DevInfo* di = dev_info();
     if (!di) return B64_ECUDA;
     unsigned long long* c = reinterpret_cast<unsigned long long*>(cell);
-    if (aligned(d_in, 32) && aligned(d_out, 8)) {
+    if (aligned(d_in, 32) && aligned(d_out, 16)) {
         const int64_t nchunk = (m / 4) / 256;
         const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_fast);
-        dec_fast_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, m, d_out, dec_tab(a), base, is_final, c, out_len);
+        launch(dec_fast_kernel, blocks, kThreads, s, d_in, m, d_out, dec_tab(a), base, is_final, c, out_len);
     } else {
         Offsets off{nullptr, nullptr, 1, m};
         const int64_t blocks = clamp_grid((m / 16 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_gen);
-        dec_generic_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, d_out, off, dec_tab(a), base, is_final, c, out_len);
+        launch(dec_generic_kernel, blocks, kThreads, s, d_in, d_out, off, dec_tab(a), base, is_final, c, out_len);
     }
     return launched();
 }
@@ -163,7 +191,7 @@ int b64_decode_ex(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
         const int r = decode_launch(d_in, m, d_out, a, 0, 1, d_err_off, nullptr, s);
         if (r != B64_OK) return r;
     }
-    dec_finalize_single_kernel<<<1, 1, 0, s>>>(d_err_off, d_status, d_out_len, d_in, m, a->pad);
+    launch(dec_finalize_single_kernel, 1, 1, s, d_err_off, d_status, d_out_len, d_in, m, a->pad);
     return launched();
 }
 
@@ -187,7 +215,7 @@ int b64_decode_chunk(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_a
 
 int b64_decode_finalize(const int64_t* d_err_min, int64_t* d_err_off, int32_t* d_status, b64_stream_t stream) {
     if (!d_err_min || !d_err_off) return B64_EINVAL;
-    dec_finalize_packed_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_err_min, d_err_off, d_status);
+    launch(dec_finalize_packed_kernel, 1, 1, reinterpret_cast<cudaStream_t>(stream), d_err_min, d_err_off, d_status);
     return launched();
 }
 
@@ -200,8 +228,7 @@ int b64_encode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count
     if (!di) return B64_ECUDA;
     Offsets off{d_in_off, d_out_off, count, 0};
     const int64_t blocks = int64_t(di->sms) * di->occ_enc_gen;
-    enc_generic_kernel<<<unsigned(blocks), kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        d_in, d_out, off, enc_tab(a), a->pad);
+    launch(enc_generic_kernel, blocks, kThreads, reinterpret_cast<cudaStream_t>(stream), d_in, d_out, off, enc_tab(a), a->pad);
     return launched();
 }
 
@@ -215,16 +242,16 @@ int b64_decode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count
     if (!di) return B64_ECUDA;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int64_t small = clamp_grid((count + kThreads - 1) / kThreads, int64_t(di->sms) * 8);
-    dec_batch_init_kernel<<<unsigned(small), kThreads, 0, s>>>(d_err_off, count);
+    launch(dec_batch_init_kernel, small, kThreads, s, d_err_off, count);
     int r = launched();
     if (r != B64_OK) return r;
     Offsets off{d_in_off, d_out_off, count, 0};
     const int64_t blocks = int64_t(di->sms) * di->occ_dec_gen;
-    dec_generic_kernel<<<unsigned(blocks), kThreads, 0, s>>>(d_in, d_out, off, dec_tab(a), 0, 1,
+    launch(dec_generic_kernel, blocks, kThreads, s, d_in, d_out, off, dec_tab(a), 0, 1,
                                                              reinterpret_cast<unsigned long long*>(d_err_off), nullptr);
     r = launched();
     if (r != B64_OK) return r;
-    dec_batch_finalize_kernel<<<unsigned(small), kThreads, 0, s>>>(d_in, d_in_off, count, a->pad, d_status,
+    launch(dec_batch_finalize_kernel, small, kThreads, s, d_in, d_in_off, count, a->pad, d_status,
                                                                    d_err_off, d_out_len);
     return launched();
 }

@@ -27,14 +27,27 @@ __device__ __forceinline__ void warp_report(bool bad, uint32_t rel, int64_t pos0
     if ((threadIdx.x & 31) == 0) atomicMin(cell, pack_err(pos0 + int64_t(r), kBadChar));
 }
 
+// Rare path: position (0 .. 4*nquads-1) of the first invalid char of the
+// nquads quads at p (4-byte aligned), re-read from global memory, or ~0u.
+__device__ __forceinline__ uint32_t scan_first_bad(const uint8_t* p, int nquads, const uint8_t* __restrict__ lut) {
+    for (int q = 0; q < nquads; ++q) {
+        const int j = first_bad_in_quad(ld32(p + 4 * q), lut);
+        if (j < 4) return uint32_t(4 * q + j);
+    }
+    return 0xffffffffu;
+}
+
 __global__ void __launch_bounds__(kThreads)
 dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
                 int64_t* __restrict__ out_len) {
-    __shared__ uint32_t s_lut[64];
+    __shared__ __align__(256) uint32_t s_lut[64];
+    __shared__ __align__(16) uint32_t s_stage[kThreads / 32][768 / 4];  // per-warp output staging
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
+    griddep_launch_dependents();
 
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -43,31 +56,49 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     const int64_t Q = m >> 2;
     const int64_t Qint = (is_final && Q > 0) ? Q - 1 : Q;
     const int64_t nchunk = Qint >> 8;
+    const uint32_t sb = smem_u32(&s_stage[threadIdx.x >> 5][0]);
 
-    for (int64_t c = gtid >> 5; c < nchunk; c += nwarp) {
-        uint32_t x[8];
-        ld256_stream(in + c * 1024 + lane * 32, x);
+    // Bulk: grid-stride over warp-chunks (1024 chars -> 768 bytes), so the
+    // whole grid sweeps one contiguous window of memory at a time.  Software
+    // pipeline: the next chunk's lane-linear LDG.256 is issued before the
+    // current chunk is translated.  The 24-byte lane outputs are re-laid through
+    // a per-warp shared buffer (conflict-free STS.64 at a 24 B stride) so the
+    // global stores are lane-linear STG.64 writing whole sectors.
+    griddep_wait();
+    int64_t c = gtid >> 5;
+    uint32_t x[8];
+    if (c < nchunk) ld256_stream(in + c * 1024 + lane * 32, x);
+    for (; c < nchunk; c += nwarp) {
+        uint32_t y[8];
+        const int64_t cn = c + nwarp;
+        if (cn < nchunk) ld256_stream(in + cn * 1024 + lane * 32, y);
         uint32_t err = 0, v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = dec_quad(x[q], lut, err);
+        for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(x[q], lb, err);
         uint32_t o[6];
         dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
         dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
-        uint8_t* dst = out + c * 768 + lane * 24;
-        st64(dst, o[0], o[1]);
-        st64(dst + 8, o[2], o[3]);
-        st64(dst + 16, o[4], o[5]);
+        sts64(sb + lane * 24, o[0], o[1]);
+        sts64(sb + lane * 24 + 8, o[2], o[3]);
+        sts64(sb + lane * 24 + 16, o[4], o[5]);
+        __syncwarp();
+        uint8_t* dst = out + c * 768 + lane * 8;
+        const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8), s2 = lds64(sb + 512 + lane * 8);
+        st64(dst, s0.x, s0.y);
+        st64(dst + 256, s1.x, s1.y);
+        st64(dst + 512, s2.x, s2.y);
+        __syncwarp();
         const bool bad = (err & kInvalid) != 0;
         if (__any_sync(kFull, bad)) {  // rare: locate the first invalid char of the chunk
             uint32_t rel = 0xffffffffu;
             if (bad) {
-                for (int q = 0; q < 8 && rel == 0xffffffffu; ++q) {
-                    const int j = first_bad_in_quad(x[q], lut);
-                    if (j < 4) rel = uint32_t(lane * 32 + q * 4 + j);
-                }
+                rel = scan_first_bad(in + c * 1024 + lane * 32, 8, lut);
+                if (rel != 0xffffffffu) rel += lane * 32;
             }
             warp_report(bad, rel, base + c * 1024, err_cell);
         }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = y[i];
     }
 
     // leftover interior quads, one per thread
@@ -107,6 +138,7 @@ dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const bool batch = off.in_off != nullptr;
+    griddep_wait();
 
     const int lane = threadIdx.x & 31;
     const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -206,6 +238,7 @@ dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
 // Single stream: the cell IS *err_off (initialised to kErrNone by memset).
 __global__ void dec_finalize_single_kernel(int64_t* err_off, int32_t* status, int64_t* out_len,
                                            const uint8_t* __restrict__ in, int64_t m, uint32_t pad) {
+    griddep_wait();
     const unsigned long long wv = *reinterpret_cast<unsigned long long*>(err_off);
     if (wv >= kErrNone) {
         *err_off = -1;
@@ -225,6 +258,7 @@ __global__ void dec_finalize_single_kernel(int64_t* err_off, int32_t* status, in
 
 // Chunk / multi-GPU: packed word -> (err_off, status).
 __global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off, int32_t* status) {
+    griddep_wait();
     const unsigned long long wv = *reinterpret_cast<const unsigned long long*>(cell);
     if (wv >= kErrNone) {
         *err_off = -1;
@@ -236,6 +270,7 @@ __global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off
 }
 
 __global__ void dec_batch_init_kernel(int64_t* err, int64_t count) {
+    griddep_wait();
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
         err[i] = int64_t(kErrNone);
 }
@@ -243,6 +278,7 @@ __global__ void dec_batch_init_kernel(int64_t* err, int64_t count) {
 __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
                                           int64_t count, uint32_t pad, int32_t* status, int64_t* err,
                                           int64_t* out_len) {
+    griddep_wait();
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t a = in_off[i], L = in_off[i + 1] - a;
         const unsigned long long wv = static_cast<unsigned long long>(err[i]);

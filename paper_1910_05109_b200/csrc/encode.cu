@@ -23,24 +23,28 @@ __device__ __forceinline__ void enc_lane24(const uint8_t* __restrict__ src, uint
     w[0] = a.x; w[1] = a.y; w[2] = b.x; w[3] = b.y; w[4] = c.x; w[5] = c.y;
 }
 
-__device__ __forceinline__ void enc_lane_compute(const uint32_t (&w)[6], uint32_t (&o)[8],
-                                                 const uint8_t* __restrict__ lut) {
-    o[0] = enc_triple(__byte_perm(w[0], w[1], 0x0122), lut);
-    o[1] = enc_triple(__byte_perm(w[0], w[1], 0x3455), lut);
-    o[2] = enc_triple(__byte_perm(w[1], w[2], 0x2344), lut);
-    o[3] = enc_triple(__byte_perm(w[2], w[3], 0x1233), lut);
-    o[4] = enc_triple(__byte_perm(w[3], w[4], 0x0122), lut);
-    o[5] = enc_triple(__byte_perm(w[3], w[4], 0x3455), lut);
-    o[6] = enc_triple(__byte_perm(w[4], w[5], 0x2344), lut);
-    o[7] = enc_triple(__byte_perm(w[5], w[5], 0x1233), lut);
+__device__ __forceinline__ void enc_lane_compute(const uint32_t (&w)[6], uint32_t (&o)[8], uint32_t lb) {
+    o[0] = enc_triple_s(__byte_perm(w[0], w[1], 0x0122), lb);
+    o[1] = enc_triple_s(__byte_perm(w[0], w[1], 0x3455), lb);
+    o[2] = enc_triple_s(__byte_perm(w[1], w[2], 0x2344), lb);
+    o[3] = enc_triple_s(__byte_perm(w[2], w[3], 0x1233), lb);
+    o[4] = enc_triple_s(__byte_perm(w[3], w[4], 0x0122), lb);
+    o[5] = enc_triple_s(__byte_perm(w[3], w[4], 0x3455), lb);
+    o[6] = enc_triple_s(__byte_perm(w[4], w[5], 0x2344), lb);
+    o[7] = enc_triple_s(__byte_perm(w[5], w[5], 0x1233), lb);
 }
 
 __global__ void __launch_bounds__(kThreads)
 enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab, uint32_t pad) {
-    __shared__ uint32_t s_lut[16];
-    if (threadIdx.x < 16) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __shared__ __align__(64) uint32_t s_lut[16];
+    if (threadIdx.x == 0) {  // static indices: the table stays in the constant bank, no stack copy
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
+    }
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
+    griddep_launch_dependents();
 
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -48,21 +52,21 @@ enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__
     const int64_t nwarp = gthreads >> 5;
     const int64_t nchunk = n / 768;
 
+    // Grid-stride over warp-chunks: at any moment the whole grid works on one
+    // contiguous window of memory (DRAM row locality).  Software pipeline: the
+    // next chunk's three loads are issued before the current chunk is encoded.
+    griddep_wait();
     int64_t c = gtid >> 5;
-    for (; c + nwarp < nchunk; c += 2 * nwarp) {
-        uint32_t wa[6], wb[6], o[8];
-        enc_lane24(in + c * 768 + lane * 24, wa);
-        enc_lane24(in + (c + nwarp) * 768 + lane * 24, wb);
-        enc_lane_compute(wa, o, lut);
+    uint32_t wv[6];
+    if (c < nchunk) enc_lane24(in + c * 768 + lane * 24, wv);
+    for (; c < nchunk; c += nwarp) {
+        uint32_t yv[6], o[8];
+        const int64_t cn = c + nwarp;
+        if (cn < nchunk) enc_lane24(in + cn * 768 + lane * 24, yv);
+        enc_lane_compute(wv, o, lb);
         st256(out + c * 1024 + lane * 32, o);
-        enc_lane_compute(wb, o, lut);
-        st256(out + (c + nwarp) * 1024 + lane * 32, o);
-    }
-    if (c < nchunk) {
-        uint32_t w[6], o[8];
-        enc_lane24(in + c * 768 + lane * 24, w);
-        enc_lane_compute(w, o, lut);
-        st256(out + c * 1024 + lane * 32, o);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) wv[i] = yv[i];
     }
 
     // remainder: output quads [256*nchunk, ceil(n/3)), one per thread
@@ -102,6 +106,7 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
     __shared__ uint32_t s_lut[16];
     if (threadIdx.x < 16) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     __syncthreads();
+    griddep_wait();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
 
     const int lane = threadIdx.x & 31;

@@ -1,0 +1,53 @@
+#!/usr/bin/env python3
+"""Small fixed workload for ncu captures: a few encode / decode launches of one size.
+
+    python tools/prof_case.py --op dec --n 1073741824 --reps 3
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1910_05109_b200 as b64  # noqa: E402
+import synth  # noqa: E402
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--op", choices=("enc", "dec", "both", "batch"), default="both")
+    p.add_argument("--n", type=int, default=1 << 30)
+    p.add_argument("--reps", type=int, default=3)
+    a = p.parse_args()
+    if a.op == "batch":
+        Ls = synth.loguniform_lengths(1_000_000, seed=0)
+        off = synth.offsets(Ls)
+        x = synth.device_data(int(off[-1]), seed=0)
+        doff = torch.from_numpy(off).cuda()
+        enc, eoff = b64.encode_batch(x, doff)
+        for _ in range(a.reps):
+            b64.encode_batch(x, doff, out=enc, out_off=eoff)
+            b64.decode_batch(enc, eoff)
+        torch.cuda.synchronize()
+        print("ok batch")
+        return
+    x = synth.device_data(a.n, seed=0)
+    t = b64.encode(x)
+    out = torch.empty(3 * (t.numel() // 4), dtype=torch.uint8, device="cuda")
+    cell = torch.empty(1, dtype=torch.int64, device="cuda")
+    for _ in range(a.reps):
+        if a.op in ("enc", "both"):
+            b64.encode(x, out=t)
+        if a.op in ("dec", "both"):
+            cell.fill_(b64.ERR_NONE)
+            b64.decode_chunk(t, 0, True, cell, out=out)
+    torch.cuda.synchronize()
+    assert int(cell.item()) == b64.ERR_NONE or a.op == "enc"
+    print("ok", a.op, a.n)
+
+
+if __name__ == "__main__":
+    main()
