@@ -1,0 +1,5 @@
+// b64gpu.cu -- single translation unit of libb64gpu.so (whole-program
+// compilation: the templated kernels are instantiated and launched in one TU).
+#include "encode.cu"
+#include "decode.cu"
+#include "capi.cu"

@@ -22,7 +22,7 @@ const char kUrlChars[65] = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz
 
 struct DevInfo {
     int sms = 0;
-    int occ_enc_fast = 0, occ_dec_fast = 0, occ_enc_gen = 0, occ_dec_gen = 0;
+    int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_enc_tma = 0, occ_enc_gen = 0, occ_dec_gen = 0;
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -36,13 +36,21 @@ const DevInfo* dev_info() {
     if (g_dev_ready[d]) return &g_dev[d];
     DevInfo info;
     if (cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) return nullptr;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast, enc_fast_kernel, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast, dec_fast_kernel, kThreads, 0) ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[1], enc_fast_kernel<1>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[2], enc_fast_kernel<2>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[3], enc_fast_kernel<3>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[1], dec_fast_kernel<1>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[2], dec_fast_kernel<2>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[3], dec_fast_kernel<3>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_tma, enc_tma_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0))
         return nullptr;
-    info.occ_enc_fast = info.occ_enc_fast < 1 ? 1 : info.occ_enc_fast;
-    info.occ_dec_fast = info.occ_dec_fast < 1 ? 1 : info.occ_dec_fast;
+    for (int i = 0; i < 4; ++i) {
+        info.occ_enc_fast[i] = info.occ_enc_fast[i] < 1 ? 1 : info.occ_enc_fast[i];
+        info.occ_dec_fast[i] = info.occ_dec_fast[i] < 1 ? 1 : info.occ_dec_fast[i];
+    }
+    info.occ_enc_tma = info.occ_enc_tma < 1 ? 1 : info.occ_enc_tma;
     info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
     info.occ_dec_gen = info.occ_dec_gen < 1 ? 1 : info.occ_dec_gen;
     g_dev[d] = info;
@@ -93,6 +101,38 @@ void launch(void (*kernel)(KArgs...), int64_t grid, int block, cudaStream_t s, A
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+
+// Encode bulk variant: 0 = register-direct loads (default, measured faster on
+// B200: profiles/), 1 = TMA-fed ring (B64_ENC=tma).
+int enc_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("B64_ENC");
+        return (e && e[0] == 't') ? 1 : 0;
+    }();
+    return v;
+}
+
+// Prefetch depth of the register-direct bulk loops (chunks in flight per warp
+// beyond the one being translated): B64_ENC_DEPTH / B64_DEC_DEPTH in 1..3.
+// Default: 2 for inputs of at least 256 MiB (tools/sweep.py on B200: 95-98 %
+// of the measured copy roofline at 1-4 GiB), 1 below (shorter kernels lose
+// more to the deeper prologue than they gain).
+int depth_env(const char* name) {
+    const char* e = std::getenv(name);
+    if (e && e[0] >= '1' && e[0] <= '3') return e[0] - '0';
+    return 0;
+}
+int enc_depth(int64_t n) {
+    static const int d = depth_env("B64_ENC_DEPTH");
+    return d ? d : (n >= (int64_t(256) << 20) ? 2 : 1);
+}
+int dec_depth(int64_t m) {
+    static const int d = depth_env("B64_DEC_DEPTH");
+    return d ? d : (m >= (int64_t(256) << 20) ? 2 : 1);
+}
+
+template <typename K>
+K pick3(int d, K k1, K k2, K k3) { return d == 3 ? k3 : (d == 2 ? k2 : k1); }
 
 int64_t clamp_grid(int64_t want, int64_t cap) { return want < 1 ? 1 : (want > cap ? cap : want); }
 
@@ -151,10 +191,16 @@ int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabe
     const DevInfo* di = dev_info();
     if (!di) return B64_ECUDA;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (aligned(d_in, 8) && aligned(d_out, 32)) {
+    if (enc_variant() == 1 && aligned(d_in, 16) && aligned(d_out, 32)) {
         const int64_t nchunk = n / 768;
-        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_fast);
-        launch(enc_fast_kernel, blocks, kThreads, s, d_in, n, d_out, enc_tab(a), a->pad);
+        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_tma);
+        launch(enc_tma_kernel, blocks, kThreads, s, d_in, n, d_out, enc_tab(a), a->pad);
+    } else if (aligned(d_in, 8) && aligned(d_out, 32)) {
+        const int64_t nchunk = n / 768;
+        const int dd = enc_depth(n);
+        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_fast[dd]);
+        launch(pick3(dd, enc_fast_kernel<1>, enc_fast_kernel<2>, enc_fast_kernel<3>), blocks, kThreads, s, d_in, n,
+               d_out, enc_tab(a), a->pad);
     } else {
         Offsets off{nullptr, nullptr, 1, n};
         const int64_t blocks = clamp_grid((n / 12 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_gen);
@@ -170,8 +216,10 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
     unsigned long long* c = reinterpret_cast<unsigned long long*>(cell);
     if (aligned(d_in, 32) && aligned(d_out, 16)) {
         const int64_t nchunk = (m / 4) / 256;
-        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_fast);
-        launch(dec_fast_kernel, blocks, kThreads, s, d_in, m, d_out, dec_tab(a), base, is_final, c, out_len);
+        const int dd = dec_depth(m);
+        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_fast[dd]);
+        launch(pick3(dd, dec_fast_kernel<1>, dec_fast_kernel<2>, dec_fast_kernel<3>), blocks, kThreads, s, d_in, m,
+               d_out, dec_tab(a), base, is_final, c, out_len);
     } else {
         Offsets off{nullptr, nullptr, 1, m};
         const int64_t blocks = clamp_grid((m / 16 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_gen);

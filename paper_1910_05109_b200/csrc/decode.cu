@@ -37,6 +37,7 @@ __device__ __forceinline__ uint32_t scan_first_bad(const uint8_t* p, int nquads,
     return 0xffffffffu;
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads)
 dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
@@ -65,40 +66,48 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     // a per-warp shared buffer (conflict-free STS.64 at a 24 B stride) so the
     // global stores are lane-linear STG.64 writing whole sectors.
     griddep_wait();
-    int64_t c = gtid >> 5;
-    uint32_t x[8];
-    if (c < nchunk) ld256_stream(in + c * 1024 + lane * 32, x);
-    for (; c < nchunk; c += nwarp) {
-        uint32_t y[8];
-        const int64_t cn = c + nwarp;
-        if (cn < nchunk) ld256_stream(in + cn * 1024 + lane * 32, y);
-        uint32_t err = 0, v[8];
+    const int64_t c0 = gtid >> 5;
+    uint32_t xr[D][8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(x[q], lb, err);
-        uint32_t o[6];
-        dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
-        dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
-        sts64(sb + lane * 24, o[0], o[1]);
-        sts64(sb + lane * 24 + 8, o[2], o[3]);
-        sts64(sb + lane * 24 + 16, o[4], o[5]);
-        __syncwarp();
-        uint8_t* dst = out + c * 768 + lane * 8;
-        const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8), s2 = lds64(sb + 512 + lane * 8);
-        st64(dst, s0.x, s0.y);
-        st64(dst + 256, s1.x, s1.y);
-        st64(dst + 512, s2.x, s2.y);
-        __syncwarp();
-        const bool bad = (err & kInvalid) != 0;
-        if (__any_sync(kFull, bad)) {  // rare: locate the first invalid char of the chunk
-            uint32_t rel = 0xffffffffu;
-            if (bad) {
-                rel = scan_first_bad(in + c * 1024 + lane * 32, 8, lut);
-                if (rel != 0xffffffffu) rel += lane * 32;
+    for (int i = 0; i < D; ++i)
+        if (c0 + i * nwarp < nchunk) ld256_stream(in + (c0 + i * nwarp) * 1024 + lane * 32, xr[i]);
+    for (int64_t cb = c0; cb < nchunk; cb += D * nwarp) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t c = cb + i * nwarp;
+            if (c < nchunk) {
+                uint32_t y[8];
+                const int64_t cn = c + D * nwarp;
+                if (cn < nchunk) ld256_stream(in + cn * 1024 + lane * 32, y);
+                uint32_t err = 0, v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(xr[i][q], lb, err);
+                uint32_t o[6];
+                dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
+                dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
+                sts64(sb + lane * 24, o[0], o[1]);
+                sts64(sb + lane * 24 + 8, o[2], o[3]);
+                sts64(sb + lane * 24 + 16, o[4], o[5]);
+                __syncwarp();
+                uint8_t* dst = out + c * 768 + lane * 8;
+                const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8), s2 = lds64(sb + 512 + lane * 8);
+                st64(dst, s0.x, s0.y);
+                st64(dst + 256, s1.x, s1.y);
+                st64(dst + 512, s2.x, s2.y);
+                __syncwarp();
+                const bool bad = (err & kInvalid) != 0;
+                if (__any_sync(kFull, bad)) {  // rare: locate the first invalid char of the chunk
+                    uint32_t rel = 0xffffffffu;
+                    if (bad) {
+                        rel = scan_first_bad(in + c * 1024 + lane * 32, 8, lut);
+                        if (rel != 0xffffffffu) rel += lane * 32;
+                    }
+                    warp_report(bad, rel, base + c * 1024, err_cell);
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) xr[i][j] = y[j];
             }
-            warp_report(bad, rel, base + c * 1024, err_cell);
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = y[i];
     }
 
     // leftover interior quads, one per thread
@@ -124,6 +133,13 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
         }
     }
 }
+
+#define B64_DEC_FAST(D) template __global__ void dec_fast_kernel<D>(const uint8_t*, int64_t, uint8_t*, DecTab, \
+                                                                     int64_t, int, unsigned long long*, int64_t*);
+B64_DEC_FAST(1)
+B64_DEC_FAST(2)
+B64_DEC_FAST(3)
+#undef B64_DEC_FAST
 
 // ---------------------------------------------------------------- generic / batch
 

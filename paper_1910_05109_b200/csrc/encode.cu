@@ -34,6 +34,7 @@ __device__ __forceinline__ void enc_lane_compute(const uint32_t (&w)[6], uint32_
     o[7] = enc_triple_s(__byte_perm(w[5], w[5], 0x1233), lb);
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads)
 enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab, uint32_t pad) {
     __shared__ __align__(64) uint32_t s_lut[16];
@@ -56,17 +57,25 @@ enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__
     // contiguous window of memory (DRAM row locality).  Software pipeline: the
     // next chunk's three loads are issued before the current chunk is encoded.
     griddep_wait();
-    int64_t c = gtid >> 5;
-    uint32_t wv[6];
-    if (c < nchunk) enc_lane24(in + c * 768 + lane * 24, wv);
-    for (; c < nchunk; c += nwarp) {
-        uint32_t yv[6], o[8];
-        const int64_t cn = c + nwarp;
-        if (cn < nchunk) enc_lane24(in + cn * 768 + lane * 24, yv);
-        enc_lane_compute(wv, o, lb);
-        st256(out + c * 1024 + lane * 32, o);
+    const int64_t c0 = gtid >> 5;
+    uint32_t wv[D][6];
 #pragma unroll
-        for (int i = 0; i < 6; ++i) wv[i] = yv[i];
+    for (int i = 0; i < D; ++i)
+        if (c0 + i * nwarp < nchunk) enc_lane24(in + (c0 + i * nwarp) * 768 + lane * 24, wv[i]);
+    for (int64_t c = c0; c < nchunk; c += D * nwarp) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int64_t ci = c + i * nwarp;
+            if (ci < nchunk) {
+                uint32_t yv[6], o[8];
+                const int64_t cn = ci + D * nwarp;
+                if (cn < nchunk) enc_lane24(in + cn * 768 + lane * 24, yv);
+                enc_lane_compute(wv[i], o, lb);
+                st256(out + ci * 1024 + lane * 32, o);
+#pragma unroll
+                for (int j = 0; j < 6; ++j) wv[i][j] = yv[j];
+            }
+        }
     }
 
     // remainder: output quads [256*nchunk, ceil(n/3)), one per thread
@@ -85,6 +94,99 @@ enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__
         *reinterpret_cast<uint32_t*>(out + 4 * q) = word;  // out 32-aligned => 4-aligned
     }
 }
+
+// enc_tma_kernel: same work split as enc_fast_kernel (grid-stride warp-chunks
+// of 768 B -> 1024 chars, lane-linear STG.256 outputs), but every warp streams
+// its input through a private ring of kEncStages shared-memory slots filled by
+// 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  Loads are
+// issued kEncStages chunks ahead without holding registers, so the DRAM
+// latency is hidden by the copy engine instead of by occupancy; lanes read
+// their 24 bytes with three conflict-free LDS.64 (24 B stride: 16 lanes per
+// phase hit 32 distinct banks).  Requires d_in 16-byte aligned.
+constexpr int kEncStages = 4;
+
+__global__ void __launch_bounds__(kThreads)
+enc_tma_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab, uint32_t pad) {
+    __shared__ __align__(64) uint32_t s_lut[16];
+    __shared__ __align__(128) uint8_t s_ring[kThreads / 32][kEncStages][768];
+    __shared__ __align__(8) unsigned long long s_bar[kThreads / 32][kEncStages];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kEncStages; ++s) mbar_init(smem_u32(&s_bar[wib][s]), 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
+    const uint32_t ring = smem_u32(&s_ring[wib][0][0]);
+    const uint32_t bars = smem_u32(&s_bar[wib][0]);
+    griddep_launch_dependents();
+
+    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t nwarp = gthreads >> 5;
+    const int64_t nchunk = n / 768;
+    const int64_t c0 = gtid >> 5;
+    const uint64_t pol = policy_evict_first();
+
+    griddep_wait();
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < kEncStages; ++s) {
+            const int64_t cc = c0 + s * nwarp;
+            if (cc < nchunk) {
+                mbar_expect_tx(bars + 8 * s, 768);
+                tma_load_1d(ring + 768 * s, in + cc * 768, 768, bars + 8 * s, pol);
+            }
+        }
+    }
+    int k = 0;
+    for (int64_t c = c0; c < nchunk; c += nwarp, ++k) {
+        const int slot = k % kEncStages;
+        mbar_wait(bars + 8 * slot, (k / kEncStages) & 1);
+        const uint32_t src = ring + 768 * slot + lane * 24;
+        const uint2 a = lds64(src), b = lds64(src + 8), d = lds64(src + 16);
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t cn = c + int64_t(kEncStages) * nwarp;
+            if (cn < nchunk) {
+                fence_proxy_async_smem();
+                mbar_expect_tx(bars + 8 * slot, 768);
+                tma_load_1d(ring + 768 * slot, in + cn * 768, 768, bars + 8 * slot, pol);
+            }
+        }
+        const uint32_t wv[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
+        uint32_t o[8];
+        enc_lane_compute(wv, o, lb);
+        st256(out + c * 1024 + lane * 32, o);
+    }
+
+    // remainder: output quads [256*nchunk, ceil(n/3)), one per thread
+    const int64_t T = n / 3;
+    const int64_t Q = (n + 2) / 3;
+    for (int64_t q = nchunk * 256 + gtid; q < Q; q += gthreads) {
+        const uint8_t* s = in + 3 * q;
+        uint32_t word;
+        if (q < T) {
+            const uint32_t x = (uint32_t(s[0]) << 24) | (uint32_t(s[1]) << 16) | (uint32_t(s[2]) << 8);
+            word = enc_triple(x, lut);
+        } else {
+            const int r = int(n - 3 * q);
+            word = enc_partial(s[0], r == 2 ? s[1] : 0u, r, lut, pad);
+        }
+        *reinterpret_cast<uint32_t*>(out + 4 * q) = word;
+    }
+}
+
+template __global__ void enc_fast_kernel<1>(const uint8_t*, int64_t, uint8_t*, EncTab, uint32_t);
+template __global__ void enc_fast_kernel<2>(const uint8_t*, int64_t, uint8_t*, EncTab, uint32_t);
+template __global__ void enc_fast_kernel<3>(const uint8_t*, int64_t, uint8_t*, EncTab, uint32_t);
 
 // ---------------------------------------------------------------- generic / batch
 

@@ -1,0 +1,71 @@
+#!/usr/bin/env python3
+"""Size sweep of the fast encode / decode paths (one process = one kernel variant,
+selected by the B64_* environment variables).  Prints one JSON line per size:
+median op time with L2 flushed before each rep, base64 GB/s and HBM traffic GB/s,
+next to a D2D copy of the same base64 byte count.
+
+    B64_DEC_DEPTH=2 python tools/sweep.py --sizes 16M,64M,256M,1G
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1910_05109_b200 as b64  # noqa: E402
+import synth  # noqa: E402
+
+
+def parse_size(s):
+    mult = {"K": 1 << 10, "M": 1 << 20, "G": 1 << 30}
+    return int(float(s[:-1]) * mult[s[-1]]) if s[-1] in mult else int(s)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--sizes", default="1M,4M,16M,64M,256M,1G")
+    p.add_argument("--reps", type=int, default=20)
+    p.add_argument("--tag", default=os.environ.get("B64_TAG", ""))
+    a = p.parse_args()
+    dev = torch.device("cuda:0")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_r = torch.zeros(64 << 20, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    for s in a.sizes.split(","):
+        n = parse_size(s)
+        x = synth.device_data(n, seed=0)
+        t = b64.encode(x)
+        o = torch.empty(3 * (t.numel() // 4), dtype=torch.uint8, device=dev)
+        cell = torch.empty(1, dtype=torch.int64, device=dev)
+        d = torch.empty_like(t)
+        res = {"tag": a.tag, "n": n, "m": t.numel()}
+        for name, fn in (("enc", lambda: b64.encode(x, out=t)),
+                         ("dec", lambda: b64.decode_chunk(t, 0, True, cell, out=o)),
+                         ("copy", lambda: d.copy_(t))):
+            evs = []
+            for k in range(a.reps + 3):
+                flush.fill_(k & 255)
+                flush_r.sum()
+                torch.cuda._sleep(200_000)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                evs.append((e0, e1))
+            torch.cuda.synchronize()
+            ms = statistics.median([e0.elapsed_time(e1) for e0, e1 in evs[3:]])
+            traffic = {"enc": n + t.numel(), "dec": t.numel() + n, "copy": 2 * t.numel()}[name]
+            res[name] = {"us": round(ms * 1e3, 2), "b64_gbs": round(t.numel() / ms / 1e6, 1),
+                         "traffic_gbs": round(traffic / ms / 1e6, 1)}
+        print(json.dumps(res), flush=True)
+        del x, t, o, d
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
