@@ -116,6 +116,9 @@ __device__ __forceinline__ void mbar_fence_init() {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -323,7 +326,7 @@ __global__ void enc_tma_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_
                                uint32_t pad);
 __global__ void enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab,
                                    uint32_t pad);
-template <int D>
+template <int D, bool TS>
 __global__ void dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
                                 int64_t* __restrict__ out_len);

@@ -22,7 +22,7 @@ const char kUrlChars[65] = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz
 
 struct DevInfo {
     int sms = 0;
-    int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_enc_tma = 0, occ_enc_gen = 0, occ_dec_gen = 0;
+    int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_dec_ts[4] = {0, 0, 0, 0}, occ_enc_tma = 0, occ_enc_gen = 0, occ_dec_gen = 0;
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -39,9 +39,12 @@ const DevInfo* dev_info() {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[1], enc_fast_kernel<1>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[2], enc_fast_kernel<2>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[3], enc_fast_kernel<3>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[1], dec_fast_kernel<1>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[2], dec_fast_kernel<2>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[3], dec_fast_kernel<3>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[1], dec_fast_kernel<1, false>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[2], dec_fast_kernel<2, false>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[3], dec_fast_kernel<3, false>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_ts[1], dec_fast_kernel<1, true>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_ts[2], dec_fast_kernel<2, true>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_ts[3], dec_fast_kernel<3, true>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_tma, enc_tma_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0))
@@ -49,6 +52,7 @@ const DevInfo* dev_info() {
     for (int i = 0; i < 4; ++i) {
         info.occ_enc_fast[i] = info.occ_enc_fast[i] < 1 ? 1 : info.occ_enc_fast[i];
         info.occ_dec_fast[i] = info.occ_dec_fast[i] < 1 ? 1 : info.occ_dec_fast[i];
+        info.occ_dec_ts[i] = info.occ_dec_ts[i] < 1 ? 1 : info.occ_dec_ts[i];
     }
     info.occ_enc_tma = info.occ_enc_tma < 1 ? 1 : info.occ_enc_tma;
     info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
@@ -131,8 +135,32 @@ int dec_depth(int64_t m) {
     return d ? d : (m >= (int64_t(256) << 20) ? 2 : 1);
 }
 
+// Decode output path: TMA bulk stores from the per-warp staging buffer
+// (B64_DEC_TS=1) or lane-linear STG.64 (default).
+bool dec_tma_store() {
+    static const bool v = [] {
+        const char* e = std::getenv("B64_DEC_TS");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 template <typename K>
 K pick3(int d, K k1, K k2, K k3) { return d == 3 ? k3 : (d == 2 ? k2 : k1); }
+
+// Blocks for a grid-stride loop over `units` warp-sized work units with at most
+// `max_blocks` resident blocks: the number of rounds is fixed by the resident
+// capacity, then the grid is shrunk so every round is (nearly) full -- no
+// partial last round in which most warps idle.
+int64_t balanced_blocks(int64_t units, int64_t max_blocks) {
+    const int64_t wpb = kThreads / 32;
+    const int64_t wmax = max_blocks * wpb;
+    if (units <= 0) return 1;
+    const int64_t rounds = (units + wmax - 1) / wmax;
+    const int64_t w = (units + rounds - 1) / rounds;
+    const int64_t b = (w + wpb - 1) / wpb;
+    return b < 1 ? 1 : (b > max_blocks ? max_blocks : b);
+}
 
 int64_t clamp_grid(int64_t want, int64_t cap) { return want < 1 ? 1 : (want > cap ? cap : want); }
 
@@ -192,13 +220,13 @@ int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabe
     if (!di) return B64_ECUDA;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (enc_variant() == 1 && aligned(d_in, 16) && aligned(d_out, 32)) {
-        const int64_t nchunk = n / 768;
-        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_tma);
+        const int64_t ntile = n / (768 * (kThreads / 32));
+        const int64_t blocks = clamp_grid(ntile, int64_t(di->sms) * di->occ_enc_tma);
         launch(enc_tma_kernel, blocks, kThreads, s, d_in, n, d_out, enc_tab(a), a->pad);
     } else if (aligned(d_in, 8) && aligned(d_out, 32)) {
         const int64_t nchunk = n / 768;
         const int dd = enc_depth(n);
-        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_fast[dd]);
+        const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * di->occ_enc_fast[dd]);
         launch(pick3(dd, enc_fast_kernel<1>, enc_fast_kernel<2>, enc_fast_kernel<3>), blocks, kThreads, s, d_in, n,
                d_out, enc_tab(a), a->pad);
     } else {
@@ -217,9 +245,11 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
     if (aligned(d_in, 32) && aligned(d_out, 16)) {
         const int64_t nchunk = (m / 4) / 256;
         const int dd = dec_depth(m);
-        const int64_t blocks = clamp_grid((nchunk * 32 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_fast[dd]);
-        launch(pick3(dd, dec_fast_kernel<1>, dec_fast_kernel<2>, dec_fast_kernel<3>), blocks, kThreads, s, d_in, m,
-               d_out, dec_tab(a), base, is_final, c, out_len);
+        const bool ts = dec_tma_store();
+        const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * (ts ? di->occ_dec_ts[dd] : di->occ_dec_fast[dd]));
+        auto k = ts ? pick3(dd, dec_fast_kernel<1, true>, dec_fast_kernel<2, true>, dec_fast_kernel<3, true>)
+                    : pick3(dd, dec_fast_kernel<1, false>, dec_fast_kernel<2, false>, dec_fast_kernel<3, false>);
+        launch(k, blocks, kThreads, s, d_in, m, d_out, dec_tab(a), base, is_final, c, out_len);
     } else {
         Offsets off{nullptr, nullptr, 1, m};
         const int64_t blocks = clamp_grid((m / 16 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_gen);

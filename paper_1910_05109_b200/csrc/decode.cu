@@ -37,19 +37,14 @@ __device__ __forceinline__ uint32_t scan_first_bad(const uint8_t* p, int nquads,
     return 0xffffffffu;
 }
 
-template <int D>
+template <int D, bool TS>
 __global__ void __launch_bounds__(kThreads)
 dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
                 int64_t* __restrict__ out_len) {
     __shared__ __align__(256) uint32_t s_lut[64];
-    __shared__ __align__(16) uint32_t s_stage[kThreads / 32][768 / 4];  // per-warp output staging
-    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
-    __syncthreads();
-    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
-    const uint32_t lb = smem_u32(s_lut);
+    __shared__ __align__(128) uint32_t s_stage[kThreads / 32][(TS ? 2 : 1) * 768 / 4];  // per-warp output staging
     griddep_launch_dependents();
-
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
@@ -61,16 +56,22 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
 
     // Bulk: grid-stride over warp-chunks (1024 chars -> 768 bytes), so the
     // whole grid sweeps one contiguous window of memory at a time.  Software
-    // pipeline: the next chunk's lane-linear LDG.256 is issued before the
-    // current chunk is translated.  The 24-byte lane outputs are re-laid through
-    // a per-warp shared buffer (conflict-free STS.64 at a 24 B stride) so the
-    // global stores are lane-linear STG.64 writing whole sectors.
+    // pipeline: D chunks per warp are in flight ahead of the one being
+    // translated (the first ones are issued before the table is staged).  The
+    // 24-byte lane outputs are re-laid through a per-warp shared buffer
+    // (conflict-free STS.64 at a 24 B stride) so the global stores are
+    // lane-linear STG.64 writing whole sectors.
     griddep_wait();
     const int64_t c0 = gtid >> 5;
+    uint32_t kk = 0;  // chunks done by this warp (TMA-store buffer parity)
     uint32_t xr[D][8];
 #pragma unroll
     for (int i = 0; i < D; ++i)
         if (c0 + i * nwarp < nchunk) ld256_stream(in + (c0 + i * nwarp) * 1024 + lane * 32, xr[i]);
+    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
     for (int64_t cb = c0; cb < nchunk; cb += D * nwarp) {
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -85,16 +86,34 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
                 uint32_t o[6];
                 dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
                 dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
-                sts64(sb + lane * 24, o[0], o[1]);
-                sts64(sb + lane * 24 + 8, o[2], o[3]);
-                sts64(sb + lane * 24 + 16, o[4], o[5]);
-                __syncwarp();
-                uint8_t* dst = out + c * 768 + lane * 8;
-                const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8), s2 = lds64(sb + 512 + lane * 8);
-                st64(dst, s0.x, s0.y);
-                st64(dst + 256, s1.x, s1.y);
-                st64(dst + 512, s2.x, s2.y);
-                __syncwarp();
+                if constexpr (TS) {
+                    // double-buffered staging drained by a 768 B TMA bulk store
+                    const uint32_t sbuf = sb + (kk & 1) * 768;
+                    if (lane == 0) tma_store_wait_read<1>();  // the store from this buffer 2 chunks ago read it
+                    __syncwarp();
+                    sts64(sbuf + lane * 24, o[0], o[1]);
+                    sts64(sbuf + lane * 24 + 8, o[2], o[3]);
+                    sts64(sbuf + lane * 24 + 16, o[4], o[5]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_1d(out + c * 768, sbuf, 768);
+                        tma_store_commit();
+                    }
+                    ++kk;
+                } else {
+                    sts64(sb + lane * 24, o[0], o[1]);
+                    sts64(sb + lane * 24 + 8, o[2], o[3]);
+                    sts64(sb + lane * 24 + 16, o[4], o[5]);
+                    __syncwarp();
+                    uint8_t* dst = out + c * 768 + lane * 8;
+                    const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8),
+                                s2 = lds64(sb + 512 + lane * 8);
+                    st64(dst, s0.x, s0.y);
+                    st64(dst + 256, s1.x, s1.y);
+                    st64(dst + 512, s2.x, s2.y);
+                    __syncwarp();
+                }
                 const bool bad = (err & kInvalid) != 0;
                 if (__any_sync(kFull, bad)) {  // rare: locate the first invalid char of the chunk
                     uint32_t rel = 0xffffffffu;
@@ -108,6 +127,10 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
                 for (int j = 0; j < 8; ++j) xr[i][j] = y[j];
             }
         }
+    }
+
+    if constexpr (TS) {
+        if (lane == 0) tma_store_wait<0>();  // bulk stores complete before the CTA (and its smem) retires
     }
 
     // leftover interior quads, one per thread
@@ -134,12 +157,6 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     }
 }
 
-#define B64_DEC_FAST(D) template __global__ void dec_fast_kernel<D>(const uint8_t*, int64_t, uint8_t*, DecTab, \
-                                                                     int64_t, int, unsigned long long*, int64_t*);
-B64_DEC_FAST(1)
-B64_DEC_FAST(2)
-B64_DEC_FAST(3)
-#undef B64_DEC_FAST
 
 // ---------------------------------------------------------------- generic / batch
 

@@ -38,6 +38,24 @@ template <int D>
 __global__ void __launch_bounds__(kThreads)
 enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab, uint32_t pad) {
     __shared__ __align__(64) uint32_t s_lut[16];
+    griddep_launch_dependents();
+    const int lane = threadIdx.x & 31;
+    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t nwarp = gthreads >> 5;
+    const int64_t nchunk = n / 768;
+    const int64_t c0 = gtid >> 5;
+
+    // Grid-stride over warp-chunks: at any moment the whole grid works on one
+    // contiguous window of memory (DRAM row locality).  Software pipeline: D
+    // chunks per warp are in flight ahead of the one being encoded.  The first
+    // loads are issued before the alphabet is staged, so the table set-up
+    // hides under the first DRAM latency.
+    griddep_wait();
+    uint32_t wv[D][6];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        if (c0 + i * nwarp < nchunk) enc_lane24(in + (c0 + i * nwarp) * 768 + lane * 24, wv[i]);
     if (threadIdx.x == 0) {  // static indices: the table stays in the constant bank, no stack copy
 #pragma unroll
         for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
@@ -45,23 +63,6 @@ enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const uint32_t lb = smem_u32(s_lut);
-    griddep_launch_dependents();
-
-    const int lane = threadIdx.x & 31;
-    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
-    const int64_t nwarp = gthreads >> 5;
-    const int64_t nchunk = n / 768;
-
-    // Grid-stride over warp-chunks: at any moment the whole grid works on one
-    // contiguous window of memory (DRAM row locality).  Software pipeline: the
-    // next chunk's three loads are issued before the current chunk is encoded.
-    griddep_wait();
-    const int64_t c0 = gtid >> 5;
-    uint32_t wv[D][6];
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-        if (c0 + i * nwarp < nchunk) enc_lane24(in + (c0 + i * nwarp) * 768 + lane * 24, wv[i]);
     for (int64_t c = c0; c < nchunk; c += D * nwarp) {
 #pragma unroll
         for (int i = 0; i < D; ++i) {
@@ -95,74 +96,90 @@ enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__
     }
 }
 
-// enc_tma_kernel: same work split as enc_fast_kernel (grid-stride warp-chunks
-// of 768 B -> 1024 chars, lane-linear STG.256 outputs), but every warp streams
-// its input through a private ring of kEncStages shared-memory slots filled by
-// 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx).  Loads are
-// issued kEncStages chunks ahead without holding registers, so the DRAM
-// latency is hidden by the copy engine instead of by occupancy; lanes read
-// their 24 bytes with three conflict-free LDS.64 (24 B stride: 16 lanes per
-// phase hit 32 distinct banks).  Requires d_in 16-byte aligned.
+// enc_tma_kernel: the input streams through a per-CTA ring of kEncStages
+// shared-memory tiles (one 768 B warp-chunk per warp: 6 KiB per tile) filled
+// by 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) that complete on a "full"
+// mbarrier; warps release a tile on an "empty" mbarrier (8 arrivals) and thread
+// 0 refills it kEncStages tiles ahead.  Loads then hold no registers and use no
+// LSU instructions; lanes read their 24 bytes with three conflict-free LDS.64
+// (24 B stride: 16 lanes per phase hit 32 distinct banks).  Tiles are taken
+// grid-stride so the grid sweeps one window of memory.  Outputs: lane-linear
+// STG.256 as in enc_fast_kernel.  Requires d_in 16-byte aligned.
 constexpr int kEncStages = 4;
+constexpr int kEncTile = (kThreads / 32) * 768;
 
 __global__ void __launch_bounds__(kThreads)
 enc_tma_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab, uint32_t pad) {
     __shared__ __align__(64) uint32_t s_lut[16];
-    __shared__ __align__(128) uint8_t s_ring[kThreads / 32][kEncStages][768];
-    __shared__ __align__(8) unsigned long long s_bar[kThreads / 32][kEncStages];
+    __shared__ __align__(128) uint8_t s_ring[kEncStages][kEncTile];
+    __shared__ __align__(8) unsigned long long s_full[kEncStages], s_empty[kEncStages];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
-    }
-    if (lane == 0) {
 #pragma unroll
-        for (int s = 0; s < kEncStages; ++s) mbar_init(smem_u32(&s_bar[wib][s]), 1);
+        for (int st = 0; st < kEncStages; ++st) {
+            mbar_init(smem_u32(&s_full[st]), 1);
+            mbar_init(smem_u32(&s_empty[st]), kThreads / 32);
+        }
         mbar_fence_init();
     }
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const uint32_t lb = smem_u32(s_lut);
-    const uint32_t ring = smem_u32(&s_ring[wib][0][0]);
-    const uint32_t bars = smem_u32(&s_bar[wib][0]);
+    const uint32_t ring = smem_u32(&s_ring[0][0]);
+    const uint32_t full = smem_u32(&s_full[0]);
+    const uint32_t empty = smem_u32(&s_empty[0]);
     griddep_launch_dependents();
 
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
     const int64_t nwarp = gthreads >> 5;
     const int64_t nchunk = n / 768;
-    const int64_t c0 = gtid >> 5;
+    const int64_t ntile = nchunk / (kThreads / 32);
+    const int64_t G = gridDim.x;
     const uint64_t pol = policy_evict_first();
 
     griddep_wait();
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
 #pragma unroll
-        for (int s = 0; s < kEncStages; ++s) {
-            const int64_t cc = c0 + s * nwarp;
-            if (cc < nchunk) {
-                mbar_expect_tx(bars + 8 * s, 768);
-                tma_load_1d(ring + 768 * s, in + cc * 768, 768, bars + 8 * s, pol);
+        for (int st = 0; st < kEncStages; ++st) {
+            const int64_t t = blockIdx.x + st * G;
+            if (t < ntile) {
+                mbar_expect_tx(full + 8 * st, kEncTile);
+                tma_load_1d(ring + kEncTile * st, in + t * kEncTile, kEncTile, full + 8 * st, pol);
             }
         }
     }
-    int k = 0;
-    for (int64_t c = c0; c < nchunk; c += nwarp, ++k) {
-        const int slot = k % kEncStages;
-        mbar_wait(bars + 8 * slot, (k / kEncStages) & 1);
-        const uint32_t src = ring + 768 * slot + lane * 24;
+    uint32_t k = 0;
+    for (int64_t t = blockIdx.x; t < ntile; t += G, ++k) {
+        const uint32_t slot = k % kEncStages;
+        const uint32_t ph = (k / kEncStages) & 1;
+        mbar_wait(full + 8 * slot, ph);
+        const uint32_t src = ring + kEncTile * slot + wib * 768 + lane * 24;
         const uint2 a = lds64(src), b = lds64(src + 8), d = lds64(src + 16);
         __syncwarp();
-        if (lane == 0) {
-            const int64_t cn = c + int64_t(kEncStages) * nwarp;
-            if (cn < nchunk) {
+        if (lane == 0) mbar_arrive(empty + 8 * slot);
+        if (threadIdx.x == 0) {
+            const int64_t tn = t + kEncStages * G;
+            if (tn < ntile) {
+                mbar_wait(empty + 8 * slot, ph);
                 fence_proxy_async_smem();
-                mbar_expect_tx(bars + 8 * slot, 768);
-                tma_load_1d(ring + 768 * slot, in + cn * 768, 768, bars + 8 * slot, pol);
+                mbar_expect_tx(full + 8 * slot, kEncTile);
+                tma_load_1d(ring + kEncTile * slot, in + tn * kEncTile, kEncTile, full + 8 * slot, pol);
             }
         }
         const uint32_t wv[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
         uint32_t o[8];
+        enc_lane_compute(wv, o, lb);
+        st256(out + (t * (kThreads / 32) + wib) * 1024 + lane * 32, o);
+    }
+
+    // chunks after the last full tile: register path, grid-stride by warp
+    for (int64_t c = ntile * (kThreads / 32) + (gtid >> 5); c < nchunk; c += nwarp) {
+        uint32_t wv[6], o[8];
+        enc_lane24(in + c * 768 + lane * 24, wv);
         enc_lane_compute(wv, o, lb);
         st256(out + c * 1024 + lane * 32, o);
     }
@@ -183,10 +200,6 @@ enc_tma_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ 
         *reinterpret_cast<uint32_t*>(out + 4 * q) = word;
     }
 }
-
-template __global__ void enc_fast_kernel<1>(const uint8_t*, int64_t, uint8_t*, EncTab, uint32_t);
-template __global__ void enc_fast_kernel<2>(const uint8_t*, int64_t, uint8_t*, EncTab, uint32_t);
-template __global__ void enc_fast_kernel<3>(const uint8_t*, int64_t, uint8_t*, EncTab, uint32_t);
 
 // ---------------------------------------------------------------- generic / batch
 
