@@ -138,6 +138,27 @@ int b64_decode_chunk(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_a
 int b64_decode_finalize(const int64_t *d_err_min, int64_t *d_err_off, int32_t *d_status,
                         b64_stream_t stream);
 
+/* ---- host buffers, overlapped (SURVEY.md Sec. 8(f) f3 ingest pipeline) ------ */
+/* Encode / decode HOST buffers (h_*: host pointers, pinned for the copies to be
+ * asynchronous) through a caller-owned DEVICE workspace d_ws of ws_bytes.  The
+ * stream is cut into chunks that rotate through 3 device buffers: chunk j is
+ * copied H2D on s_h2d, coded on s_comp, copied D2H on s_d2h, so both PCIe
+ * directions and the kernels overlap.  Results are complete once all three
+ * streams have been synchronised (they may be the same stream).
+ * b64_host_workspace_bytes(c) = workspace for encode chunks of ~c input bytes
+ * (decode with the same workspace uses chunks of ~4c/3 chars).
+ * Encode writes b64_encoded_len(n) chars to h_out.  Decode writes up to 3*m/4
+ * bytes to h_out and, on s_comp, *d_err_off (device) = -1 or the first invalid
+ * position and *d_status (nullable, device) = its kind; the exact output
+ * length is 3*m/4 - (number of '=' at m-2, m-1) when valid, 3*floor(err/4)
+ * otherwise (same rules as b64_decode_ex). */
+int64_t b64_host_workspace_bytes(int64_t chunk_bytes);
+int b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, const b64_alphabet *a, uint8_t *d_ws,
+                    int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h);
+int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, const b64_alphabet *a, uint8_t *d_ws,
+                    int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, b64_stream_t s_h2d,
+                    b64_stream_t s_comp, b64_stream_t s_d2h);
+
 /* ---- batched (BASELINE.json configs[3]) ------------------------------------ */
 /* `count` independent strings concatenated in d_in; string i is
  * d_in[d_in_off[i] .. d_in_off[i+1]) (d_in_off: device int64[count+1],

@@ -23,7 +23,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
-    "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count",
+    "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline",
     "ERR_NONE",
 ]
 
@@ -151,6 +151,75 @@ def decode_finalize(err_cell: torch.Tensor, err_off: torch.Tensor, status: Optio
     _check_i64(err_off, "err_off")
     _lib.check(_lib.lib().b64_decode_finalize(_ptr(err_cell), _ptr(err_off), _ptr(status), _stream(stream)),
                "b64_decode_finalize")
+
+
+# ------------------------------------------------------------------ host buffers (overlapped pipeline)
+
+class HostPipeline:
+    """Device workspace + three streams for b64_encode_host / b64_decode_host.
+
+    Chunks of a host buffer rotate through 3 device buffers: H2D copy, kernel
+    and D2H copy of consecutive chunks overlap (both PCIe directions busy)."""
+
+    def __init__(self, chunk_bytes: int = 16 << 20, device=None):
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.device = dev
+        self.ws_bytes = int(_lib.lib().b64_host_workspace_bytes(chunk_bytes))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
+        self.info = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def _sp(self):
+        return [ctypes.c_void_p(s.cuda_stream) for s in self.streams]
+
+    def _join(self):
+        cur = torch.cuda.current_stream(self.device)
+        for s in self.streams:
+            cur.wait_stream(s)
+
+    def encode(self, x: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
+               sync: bool = True) -> torch.Tensor:
+        if x.is_cuda or x.dtype != torch.uint8 or not x.is_contiguous():
+            raise B64Error("x must be a contiguous uint8 host tensor (pinned for overlap)")
+        m = encoded_len(x.numel())
+        if out is None:
+            out = torch.empty(m, dtype=torch.uint8, pin_memory=True)
+        for s in self.streams:
+            s.wait_stream(torch.cuda.current_stream(self.device))
+        _lib.check(_lib.lib().b64_encode_host(_ptr(x), x.numel(), _ptr(out), _alpha(a), _ptr(self.ws), self.ws_bytes,
+                                              *self._sp()), "b64_encode_host")
+        self._join()
+        if sync:
+            torch.cuda.current_stream(self.device).synchronize()
+        return out[:m]
+
+    def decode(self, t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
+               sync: bool = True):
+        """Returns (host bytes, err_off) when sync, else (host buffer, device info int64[2] = err, status)."""
+        if t.is_cuda or t.dtype != torch.uint8 or not t.is_contiguous():
+            raise B64Error("t must be a contiguous uint8 host tensor (pinned for overlap)")
+        m = t.numel()
+        if m % 4:
+            raise B64Error("B64_ELENGTH: text length is not a multiple of 4")
+        if out is None:
+            out = torch.empty(max(3 * (m // 4), 1), dtype=torch.uint8, pin_memory=True)
+        for s in self.streams:
+            s.wait_stream(torch.cuda.current_stream(self.device))
+        self.info[1].zero_()
+        st = self.info[1:2].view(torch.int32)[:1]
+        _lib.check(_lib.lib().b64_decode_host(_ptr(t), m, _ptr(out), _alpha(a), _ptr(self.ws), self.ws_bytes,
+                                              _ptr(self.info[0:1]), _ptr(st), *self._sp()), "b64_decode_host")
+        self._join()
+        if not sync:
+            return out, self.info
+        err = int(self.info[0].item())
+        if err < 0:
+            pads = (2 if m >= 4 and int(t[m - 2]) == (a or standard()).pad else
+                    (1 if m >= 4 and int(t[m - 1]) == (a or standard()).pad else 0))
+            olen = 3 * (m // 4) - pads
+        else:
+            olen = 3 * (err // 4)
+        return out[:olen], err
 
 
 # ------------------------------------------------------------------ batched

@@ -54,6 +54,9 @@ SIGNATURES = [
     ("b64_decode_ex", INT, [P, I64, P, AP, P, P, P, P]),
     ("b64_decode_chunk", INT, [P, I64, P, AP, I64, INT, P, P, P]),
     ("b64_decode_finalize", INT, [P, P, P, P]),
+    ("b64_host_workspace_bytes", I64, [I64]),
+    ("b64_encode_host", INT, [P, I64, P, AP, P, I64, P, P, P]),
+    ("b64_decode_host", INT, [P, I64, P, AP, P, I64, P, P, P, P, P]),
     ("b64_encode_batch", INT, [P, P, I64, P, P, AP, P]),
     ("b64_decode_batch", INT, [P, P, I64, P, P, AP, P, P, P, P]),
     ("b64_launch_count", I64, []),

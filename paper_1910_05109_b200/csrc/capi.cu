@@ -297,6 +297,123 @@ int b64_decode_finalize(const int64_t* d_err_min, int64_t* d_err_off, int32_t* d
     return launched();
 }
 
+// ---------------------------------------------------------------- host-buffer pipelines
+// Chunks of the host input are copied H2D on s_h2d, coded on s_comp and copied
+// back D2H on s_d2h through kHostBufs rotating device buffers, so both PCIe
+// directions and the kernels overlap.  Cross-stream order uses events created
+// for the call and released at its end (the library keeps no state).
+namespace {
+constexpr int kHostBufs = 3;
+
+struct HostPipe {
+    cudaEvent_t h2d[kHostBufs], comp[kHostBufs], d2h[kHostBufs];
+    bool ok = true;
+    HostPipe() {
+        for (int i = 0; i < kHostBufs; ++i) {
+            ok &= cudaEventCreateWithFlags(&h2d[i], cudaEventDisableTiming) == cudaSuccess;
+            ok &= cudaEventCreateWithFlags(&comp[i], cudaEventDisableTiming) == cudaSuccess;
+            ok &= cudaEventCreateWithFlags(&d2h[i], cudaEventDisableTiming) == cudaSuccess;
+        }
+    }
+    ~HostPipe() {
+        for (int i = 0; i < kHostBufs; ++i) {
+            cudaEventDestroy(h2d[i]);
+            cudaEventDestroy(comp[i]);
+            cudaEventDestroy(d2h[i]);
+        }
+    }
+};
+
+int64_t align_down(int64_t v, int64_t a) { return v / a * a; }
+}  // namespace
+
+int64_t b64_host_workspace_bytes(int64_t chunk_bytes) {
+    if (chunk_bytes <= 0) return -1;
+    const int64_t c = align_down(chunk_bytes, 3072) > 0 ? align_down(chunk_bytes, 3072) : 3072;
+    return kHostBufs * (c + (c / 3) * 4 + 512) + 256;
+}
+
+int b64_encode_host(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
+                    int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h) {
+    if (n < 0 || !alpha_ok(a)) return B64_EINVAL;
+    if (n == 0) return B64_OK;
+    if (!h_in || !h_out || !d_ws) return B64_EINVAL;
+    // per buffer: C input bytes + 4C/3 output chars; C a multiple of 3072 (= 4 * 768, keeps both aligned)
+    const int64_t per = (ws_bytes - 256) / kHostBufs - 512;
+    const int64_t C = align_down(per * 3 / 7, 3072);
+    if (C <= 0) return B64_EINVAL;
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
+    cudaStream_t sh = reinterpret_cast<cudaStream_t>(s_h2d), sc = reinterpret_cast<cudaStream_t>(s_comp),
+                 sd = reinterpret_cast<cudaStream_t>(s_d2h);
+    HostPipe pipe;
+    if (!pipe.ok) return B64_ECUDA;
+    const int64_t stride = C + C / 3 * 4 + 512;
+    int64_t j = 0;
+    for (int64_t off = 0; off < n; off += C, ++j) {
+        const int b = int(j % kHostBufs);
+        uint8_t* din = base + b * stride;
+        uint8_t* dout = din + C + 256;
+        const int64_t len = (n - off < C) ? n - off : C;
+        const int64_t olen = b64_encoded_len(len);
+        if (j >= kHostBufs && cudaStreamWaitEvent(sh, pipe.d2h[b], 0) != cudaSuccess) return B64_ECUDA;
+        if (cudaMemcpyAsync(din, h_in + off, size_t(len), cudaMemcpyHostToDevice, sh) != cudaSuccess) return B64_ECUDA;
+        cudaEventRecord(pipe.h2d[b], sh);
+        cudaStreamWaitEvent(sc, pipe.h2d[b], 0);
+        const int r = b64_encode(din, len, dout, a, s_comp);
+        if (r != B64_OK) return r;
+        cudaEventRecord(pipe.comp[b], sc);
+        cudaStreamWaitEvent(sd, pipe.comp[b], 0);
+        if (cudaMemcpyAsync(h_out + off / 3 * 4, dout, size_t(olen), cudaMemcpyDeviceToHost, sd) != cudaSuccess)
+            return B64_ECUDA;
+        cudaEventRecord(pipe.d2h[b], sd);
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? B64_OK : (cudaGetLastError(), B64_ECUDA);
+}
+
+int b64_decode_host(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
+                    int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, b64_stream_t s_h2d,
+                    b64_stream_t s_comp, b64_stream_t s_d2h) {
+    if (m < 0 || !alpha_ok(a) || !d_err_off) return B64_EINVAL;
+    if (m % 4) return B64_ELENGTH;
+    if (m > 0 && (!h_in || !h_out || !d_ws)) return B64_EINVAL;
+    cudaStream_t sh = reinterpret_cast<cudaStream_t>(s_h2d), sc = reinterpret_cast<cudaStream_t>(s_comp),
+                 sd = reinterpret_cast<cudaStream_t>(s_d2h);
+    if (m == 0) {
+        if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), sc) != cudaSuccess) return B64_ECUDA;
+        return b64_decode_finalize(d_err_off, d_err_off, d_status, s_comp);
+    }
+    if (!d_ws) return B64_EINVAL;
+    // per buffer: C chars + 3C/4 bytes; C a multiple of 4096 (= 4 * 1024)
+    const int64_t per = (ws_bytes - 256) / kHostBufs - 512;
+    const int64_t C = align_down(per * 4 / 7, 4096);
+    if (C <= 0) return B64_EINVAL;
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
+    HostPipe pipe;
+    if (!pipe.ok) return B64_ECUDA;
+    if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), sc) != cudaSuccess) return B64_ECUDA;
+    const int64_t stride = C + C / 4 * 3 + 512;
+    int64_t j = 0;
+    for (int64_t off = 0; off < m; off += C, ++j) {
+        const int b = int(j % kHostBufs);
+        uint8_t* din = base + b * stride;
+        uint8_t* dout = din + C + 256;
+        const int64_t len = (m - off < C) ? m - off : C;
+        const bool fin = off + len == m;
+        if (j >= kHostBufs && cudaStreamWaitEvent(sh, pipe.d2h[b], 0) != cudaSuccess) return B64_ECUDA;
+        if (cudaMemcpyAsync(din, h_in + off, size_t(len), cudaMemcpyHostToDevice, sh) != cudaSuccess) return B64_ECUDA;
+        cudaEventRecord(pipe.h2d[b], sh);
+        cudaStreamWaitEvent(sc, pipe.h2d[b], 0);
+        const int r = b64_decode_chunk(din, len, dout, a, off, fin ? 1 : 0, d_err_off, nullptr, s_comp);
+        if (r != B64_OK) return r;
+        cudaEventRecord(pipe.comp[b], sc);
+        cudaStreamWaitEvent(sd, pipe.comp[b], 0);
+        if (cudaMemcpyAsync(h_out + off / 4 * 3, dout, size_t(len / 4 * 3), cudaMemcpyDeviceToHost, sd) != cudaSuccess)
+            return B64_ECUDA;
+        cudaEventRecord(pipe.d2h[b], sd);
+    }
+    return b64_decode_finalize(d_err_off, d_err_off, d_status, s_comp);
+}
+
 int b64_encode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count, uint8_t* d_out,
                      const int64_t* d_out_off, const b64_alphabet* a, b64_stream_t stream) {
     if (count < 0 || !alpha_ok(a)) return B64_EINVAL;

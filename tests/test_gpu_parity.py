@@ -418,3 +418,27 @@ def test_config5_single_gpu_sampled(b64):
     eo = torch.empty(1, dtype=torch.int64, device=DEV)
     b64.decode_finalize(cells.min().reshape(1), eo)
     assert int(eo.item()) == int(pos.min())
+
+
+# ------------------------------------------------------------------ host-buffer pipeline
+
+def test_host_pipeline_vs_oracle(b64):
+    """b64_encode_host / b64_decode_host with small chunks (many rotations of the 3 buffers)."""
+    pipe = b64.HostPipeline(chunk_bytes=3072 * 5)
+    for n in (0, 1, 2, 3, 3071, 3072, 3073, 15360 * 3 + 5, 200_003):
+        for chars, alpha in ((oracle.STANDARD, b64.standard()), (oracle.URL, b64.url())):
+            x = synth.data(n, seed=n + 1)
+            xh = torch.from_numpy(x).pin_memory()
+            t = pipe.encode(xh, alpha)
+            ref = oracle.encode(x, chars)
+            assert np.array_equal(t.numpy(), ref), n
+            y, err = pipe.decode(t.clone().pin_memory(), alpha)
+            assert err == -1 and np.array_equal(y.numpy(), x), n
+            if ref.size > 8:
+                pos, bad = synth.corruption(3, ref.size, chars, seed=n)
+                t2 = ref.copy()
+                t2[pos] = bad
+                y, err = pipe.decode(torch.from_numpy(t2).pin_memory(), alpha)
+                rref, rerr, rst = oracle.decode(t2, chars)
+                assert err == rerr == int(pos.min())
+                assert np.array_equal(y.numpy(), rref)
