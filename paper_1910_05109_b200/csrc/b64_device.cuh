@@ -204,6 +204,41 @@ __device__ __forceinline__ void ld_unaligned(const uint8_t* p, uint32_t (&w)[NW]
     }
 }
 
+// 24 / 32 bytes at any address, as 8-byte-aligned LDG.64 + funnel shifts.
+// Reads only the naturally aligned 8-byte words that contain p[0..NB)
+// (b64gpu.h conventions).
+template <int NW>  // NW = 6 (24 B) or 8 (32 B)
+__device__ __forceinline__ void ld_unaligned64(const uint8_t* p, uint32_t (&w)[NW]) {
+    const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+    const uint2* pa = reinterpret_cast<const uint2*>(u & ~uintptr_t(7));
+    const uint32_t sb = uint32_t(u & 7);
+    uint32_t v[NW + 4];
+#pragma unroll
+    for (int i = 0; i < NW / 2; ++i) {
+        const uint2 q = ld64_l1(pa + i);
+        v[2 * i] = q.x;
+        v[2 * i + 1] = q.y;
+    }
+    if (sb) {
+        const uint2 q = ld64_l1(pa + NW / 2);
+        v[NW] = q.x;
+        v[NW + 1] = q.y;
+    } else {
+        v[NW] = 0;
+        v[NW + 1] = 0;
+    }
+    const bool ws = sb >= 4;
+    const uint32_t sh = (sb & 3) * 8;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        const uint32_t lo = ws ? v[i + 1] : v[i];
+        const uint32_t hi = ws ? v[i + 2] : v[i + 1];
+        w[i] = __funnelshift_r(lo, hi, sh);
+    }
+}
+__device__ __forceinline__ void ld24_unaligned(const uint8_t* p, uint32_t (&w)[6]) { ld_unaligned64<6>(p, w); }
+__device__ __forceinline__ void ld32_unaligned(const uint8_t* p, uint32_t (&w)[8]) { ld_unaligned64<8>(p, w); }
+
 // ----------------------------------------------------------------- encode
 // One triple, given x with byte3 = s1, byte2 = s2, byte1 = s3 (byte0 unused):
 // the four 6-bit values of PAPER.md:88-92 are bits [26,32), [20,26), [14,20),

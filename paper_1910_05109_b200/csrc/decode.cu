@@ -166,10 +166,11 @@ __global__ void __launch_bounds__(kThreads)
 dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, DecTab tab,
                    int64_t base, int is_final_single, unsigned long long* __restrict__ err_cells,
                    int64_t* __restrict__ out_len_single) {
-    __shared__ uint32_t s_lut[64];
+    __shared__ __align__(256) uint32_t s_lut[64];
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
     const bool batch = off.in_off != nullptr;
     griddep_wait();
 
@@ -201,48 +202,54 @@ dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
         const int64_t L = off.in(s + 1) - a;
         if (L <= 0 || (L & 3)) continue;  // empty / LENGTH: settled by the finalize kernel
         const int64_t ob = off.out(s);
+        uint8_t* o = out + ob;
         const bool fin = batch ? true : (is_final_single != 0);
         unsigned long long* cell = batch ? err_cells + s : err_cells;
         const int64_t pbase = batch ? 0 : base;  // reported position = pbase + (char index in string)
         const int64_t Qs = L >> 2;
         const int64_t Qint = fin ? Qs - 1 : Qs;
-        const int64_t H = min(int64_t(reinterpret_cast<uintptr_t>(out + ob) & 3), Qint);
-        const int64_t U = (Qint - H) >> 2;       // full 4-quad units
-        const int64_t ua = a + 4 * H;             // first char of unit 0
-        const int64_t kb = lo > ua ? (lo - ua + 15) / 16 : 0;
-        const int64_t ke = min(U, (hi - ua + 15) / 16);
+        // h head quads make the unit outputs 8-byte aligned: 3h == -o (mod 8), 3^-1 == 3 (mod 8)
+        const int64_t h = min(int64_t(((8 - (reinterpret_cast<uintptr_t>(o) & 7)) * 3) & 7), Qint);
+        const int64_t U = (Qint - h) >> 3;       // full 8-quad units (32 chars -> 24 bytes)
+        const int64_t ua = a + 4 * h;             // first char of unit 0
+        const int64_t kb = lo > ua ? (lo - ua + 31) / 32 : 0;
+        const int64_t ke = min(U, (hi - ua + 31) / 32);
         for (int64_t k0 = kb; k0 < ke; k0 += 32) {
             const int64_t k = k0 + lane;
             const bool act = k < ke;
-            uint32_t err = 0, x[4];
+            uint32_t err = 0;
             if (act) {
-                ld_unaligned<4>(in + ua + 16 * k, x);
-                const uint32_t v0 = dec_quad(x[0], lut, err), v1 = dec_quad(x[1], lut, err);
-                const uint32_t v2 = dec_quad(x[2], lut, err), v3 = dec_quad(x[3], lut, err);
-                uint32_t o0, o1, o2;
-                dec_pack12(v0, v1, v2, v3, o0, o1, o2);
-                uint32_t* dst = reinterpret_cast<uint32_t*>(out + ob + 3 * H + 12 * k);
-                dst[0] = o0; dst[1] = o1; dst[2] = o2;
+                uint32_t x[8], v[8], ov[6];
+                ld32_unaligned(in + ua + 32 * k, x);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(x[q], lb, err);
+                dec_pack12(v[0], v[1], v[2], v[3], ov[0], ov[1], ov[2]);
+                dec_pack12(v[4], v[5], v[6], v[7], ov[3], ov[4], ov[5]);
+                uint8_t* dst = o + 3 * h + 24 * k;
+                st64(dst, ov[0], ov[1]);
+                st64(dst + 8, ov[2], ov[3]);
+                st64(dst + 16, ov[4], ov[5]);
             }
             const bool bad = act && (err & kInvalid);
             if (__any_sync(kFull, bad)) {
                 uint32_t rel = 0xffffffffu;
                 if (bad) {
-                    for (int q = 0; q < 4 && rel == 0xffffffffu; ++q) {
-                        const int j = first_bad_in_quad(x[q], lut);
-                        if (j < 4) rel = uint32_t(lane * 16 + q * 4 + j);
+                    const uint8_t* src = in + ua + 32 * k;
+                    for (int c = 0; c < 32; ++c) {
+                        if (lut[src[c]] & kInvalid) { rel = uint32_t(lane * 32 + c); break; }
                     }
                 }
-                warp_report(bad, rel, pbase + (ua - a) + 16 * k0, cell);
+                warp_report(bad, rel, pbase + (ua - a) + 32 * k0, cell);
             }
         }
-        // quads outside full units: head [0,H), tail [H+4U, Qint), final Qs-1
-        const int64_t ntail = Qint - (H + 4 * U);
-        const int nsc = int(H + ntail + (fin ? 1 : 0));
+        // quads outside full units: head [0,h), tail [h+8U, Qint), final Qs-1 (at most 15)
+        const int64_t t0 = h + 8 * U;
+        const int64_t ntail = Qint - t0;
+        const int nsc = int(h + ntail + (fin ? 1 : 0));
         if (lane < nsc) {
             int64_t j;
-            if (lane < H) j = lane;
-            else if (lane < H + ntail) j = H + 4 * U + (lane - H);
+            if (lane < h) j = lane;
+            else if (lane < h + ntail) j = t0 + (lane - h);
             else j = Qs - 1;
             const int64_t p = a + 4 * j;
             if (p >= lo && p < hi) {
@@ -253,12 +260,12 @@ dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
                     int badj, kk;
                     uint32_t v;
                     const uint32_t kind = final_quad(x, lut, tab.pad, &badj, &kk, &v);
-                    if (kind == kOk) store_bytes(out + ob + 3 * j, v, kk);
+                    if (kind == kOk) store_bytes(o + 3 * j, v, kk);
                     else atomicMin(cell, pack_err(pbase + 4 * j + badj, kind));
                 } else {
                     uint32_t err = 0;
                     const uint32_t v = dec_quad(x, lut, err);
-                    store_bytes(out + ob + 3 * j, v, 3);
+                    store_bytes(o + 3 * j, v, 3);
                     if (err & kInvalid) atomicMin(cell, pack_err(pbase + 4 * j + first_bad_in_quad(x, lut), kBadChar));
                 }
             }

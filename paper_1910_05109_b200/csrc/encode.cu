@@ -216,13 +216,62 @@ __device__ __forceinline__ void store16(uint8_t* dst, const uint32_t (&o)[4]) {
     }
 }
 
+// Path B (output not 4-byte aligned: only the single-stream API with a
+// misaligned d_out): 12-byte units -> 16 chars with byte-granular stores.
+__device__ __forceinline__ void enc_string_unaligned_out(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                         int64_t a, int64_t L, int64_t ob, int64_t lo, int64_t hi,
+                                                         int lane, const uint8_t* __restrict__ lut, uint32_t pad) {
+    const int64_t nunit = (L + 11) / 12;
+    const int64_t kb = lo > a ? (lo - a + 11) / 12 : 0;
+    const int64_t ke = min(nunit, (hi - a + 11) / 12);
+    for (int64_t k = kb + lane; k < ke; k += 32) {
+        const uint8_t* src = in + a + 12 * k;
+        uint8_t* dst = out + ob + 16 * k;
+        const int64_t rem = L - 12 * k;
+        if (rem >= 12) {
+            uint32_t wv[3], o[4];
+            ld_unaligned<3>(src, wv);
+            enc12(wv[0], wv[1], wv[2], o, lut);
+            store16(dst, o);
+        } else {
+            int t = 0;
+            for (; 3 * t + 3 <= rem; ++t) {
+                const uint32_t x = (uint32_t(src[3 * t]) << 24) | (uint32_t(src[3 * t + 1]) << 16) |
+                                   (uint32_t(src[3 * t + 2]) << 8);
+                const uint32_t v = enc_triple(x, lut);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dst[4 * t + i] = uint8_t(v >> (8 * i));
+            }
+            const int r = int(rem - 3 * t);
+            if (r > 0) {
+                const uint32_t v = enc_partial(src[3 * t], r == 2 ? src[3 * t + 1] : 0u, r, lut, pad);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dst[4 * t + i] = uint8_t(v >> (8 * i));
+            }
+        }
+    }
+}
+
+// Any alignment, one stream or a batch.  The concatenated input is cut into
+// equal byte ranges, one per warp; a warp owns every work item whose first
+// input byte lies in its range.  Per string with a 4-byte-aligned output
+// (always the case for batches, whose output offsets are multiples of 4):
+//   * h < 8 head triples, one per lane, bring the output to a 32-byte boundary;
+//   * then units of 8 triples (24 bytes, read at any alignment as 8-byte-aligned
+//     LDG.64 + funnel shifts) -> 32 chars, one lane-linear-ish STG.256 each, the
+//     same per-lane code as enc_fast_kernel;
+//   * the < 8 leftover triples and the padded tail, one per lane.
 __global__ void __launch_bounds__(kThreads)
 enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab, uint32_t pad) {
-    __shared__ uint32_t s_lut[16];
-    if (threadIdx.x < 16) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __shared__ __align__(64) uint32_t s_lut[16];
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
+    }
     __syncthreads();
     griddep_wait();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
 
     const int lane = threadIdx.x & 31;
     const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -240,34 +289,41 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
         const int64_t L = off.in(s + 1) - a;
         if (L <= 0) continue;
         const int64_t ob = off.out(s);
-        const int64_t nunit = (L + 11) / 12;
-        const int64_t kb = lo > a ? (lo - a + 11) / 12 : 0;
-        const int64_t ke = min(nunit, (hi - a + 11) / 12);
+        uint8_t* o = out + ob;
+        const uintptr_t oa = reinterpret_cast<uintptr_t>(o);
+        if (oa & 3) {
+            enc_string_unaligned_out(in, out, a, L, ob, lo, hi, lane, lut, pad);
+            continue;
+        }
+        const int64_t T = L / 3;
+        const int r = int(L - 3 * T);
+        const int64_t h = min(T, int64_t(((32 - (oa & 31)) & 31) >> 2));
+        const int64_t U = (T - h) >> 3;
+        const int64_t ua = a + 3 * h;
+        const int64_t kb = lo > ua ? (lo - ua + 23) / 24 : 0;
+        const int64_t ke = min(U, (hi - ua + 23) / 24);
         for (int64_t k = kb + lane; k < ke; k += 32) {
-            const uint8_t* src = in + a + 12 * k;
-            uint8_t* dst = out + ob + 16 * k;
-            const int64_t rem = L - 12 * k;
-            if (rem >= 12) {
-                uint32_t wv[3], o[4];
-                ld_unaligned<3>(src, wv);
-                enc12(wv[0], wv[1], wv[2], o, lut);
-                store16(dst, o);
-            } else {
-                // last unit of the string: whole triples, then the padded tail
-                int t = 0;
-                for (; 3 * t + 3 <= rem; ++t) {
-                    const uint32_t x = (uint32_t(src[3 * t]) << 24) | (uint32_t(src[3 * t + 1]) << 16) |
-                                       (uint32_t(src[3 * t + 2]) << 8);
-                    const uint32_t v = enc_triple(x, lut);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) dst[4 * t + i] = uint8_t(v >> (8 * i));
+            uint32_t wv[6], ov[8];
+            ld24_unaligned(in + ua + 24 * k, wv);
+            enc_lane_compute(wv, ov, lb);
+            st256(o + 4 * h + 32 * k, ov);
+        }
+        // scalar triples: head [0, h), tail [h + 8U, T), and the padded partial triple T
+        const int64_t t0 = h + 8 * U;
+        const int nsc = int(h + (T - t0) + (r > 0 ? 1 : 0));
+        if (lane < nsc) {
+            const int64_t j = lane < h ? int64_t(lane) : t0 + (lane - h);
+            const int64_t p = a + 3 * j;
+            if (p >= lo && p < hi) {
+                const uint8_t* src = in + p;
+                uint32_t word;
+                if (j < T) {
+                    word = enc_triple((uint32_t(src[0]) << 24) | (uint32_t(src[1]) << 16) | (uint32_t(src[2]) << 8),
+                                      lut);
+                } else {
+                    word = enc_partial(src[0], r == 2 ? src[1] : 0u, r, lut, pad);
                 }
-                const int r = int(rem - 3 * t);
-                if (r > 0) {
-                    const uint32_t v = enc_partial(src[3 * t], r == 2 ? src[3 * t + 1] : 0u, r, lut, pad);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) dst[4 * t + i] = uint8_t(v >> (8 * i));
-                }
+                *reinterpret_cast<uint32_t*>(o + 4 * j) = word;
             }
         }
     }

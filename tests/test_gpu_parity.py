@@ -442,3 +442,58 @@ def test_host_pipeline_vs_oracle(b64):
                 rref, rerr, rst = oracle.decode(t2, chars)
                 assert err == rerr == int(pos.min())
                 assert np.array_equal(y.numpy(), rref)
+
+
+# ------------------------------------------------------------------ guard bands (no writes outside the output)
+
+def test_no_writes_outside_outputs(b64):
+    """Canary bytes around (and, for decode, after out_len inside) every output buffer stay intact:
+    fast and generic kernels, single stream and batch."""
+    G = 256
+    for n in (1, 2, 3, 100, 767, 768, 769, 4096 * 3 + 1, 300_001):
+        for oi, oo in ((0, 0), (1, 3), (5, 16), (0, 7)):
+            x = synth.data(n, seed=n)
+            m = b64.encoded_len(n)
+            buf = torch.full((m + 2 * G + 32,), 0xA5, dtype=torch.uint8, device=DEV)
+            dst = buf[G + oo: G + oo + m]
+            b64.encode(to_dev(x, oi), out=dst)
+            hb = buf.cpu().numpy()
+            assert (hb[: G + oo] == 0xA5).all() and (hb[G + oo + m:] == 0xA5).all(), (n, oi, oo)
+            text = oracle.encode(x)
+            cap = 3 * (m // 4)
+            buf = torch.full((cap + 2 * G + 32,), 0xA5, dtype=torch.uint8, device=DEV)
+            dst = buf[G + oo: G + oo + cap]
+            out, info = b64.decode_async(to_dev(text, oi), out=dst)
+            err, st, olen = info.tolist()
+            assert err == -1 and olen == n
+            hb = buf.cpu().numpy()
+            assert (hb[: G + oo] == 0xA5).all() and (hb[G + oo + n:] == 0xA5).all(), (n, oi, oo)
+    # batch: outputs land exactly in their slots; gaps left between slots stay intact
+    L = synth.loguniform_lengths(2000, hi=3000, seed=9)
+    off = synth.offsets(L)
+    x = synth.data(int(off[-1]), seed=9)
+    el = 4 * ((L + 2) // 3)
+    eoff = np.zeros(L.size + 1, np.int64)
+    np.cumsum(el + 8, out=eoff[1:])  # 8 canary bytes after every string's slot
+    buf = torch.full((int(eoff[-1]) + 64,), 0xA5, dtype=torch.uint8, device=DEV)
+    b64.encode_batch(to_dev(x), torch.from_numpy(off).to(DEV), out=buf, out_off=torch.from_numpy(eoff).to(DEV))
+    hb = buf.cpu().numpy()
+    for i in range(L.size):
+        assert (hb[eoff[i] + el[i]: eoff[i + 1]] == 0xA5).all(), i
+
+
+def test_dist_layer_world1_cuda(b64):
+    """dist.encode_sharded / decode_sharded with the CUDA codec and no process group (world 1)."""
+    from paper_1910_05109_b200 import dist as b64dist
+
+    x = synth.data(768 * 40 + 2, seed=77)
+    sh = b64dist.encode_shard(x.size, 1, 0)
+    t = b64dist.encode_sharded(to_dev(x))
+    ref = oracle.encode(x)
+    assert sh.is_final and np.array_equal(t.cpu().numpy(), ref)
+    t2 = ref.copy()
+    t2[5000] = ord("~")
+    ds = b64dist.decode_shard(t2.size, 1, 0)
+    out, err, st = b64dist.decode_sharded(to_dev(t2), ds)
+    assert (err, st) == (5000, oracle.ST_BADCHAR)
+    assert np.array_equal(out[: 3 * (5000 // 4)].cpu().numpy(), x[: 3 * (5000 // 4)])
