@@ -187,9 +187,15 @@ def run_ours(args):
     flush_r = torch.zeros(64 << 20, dtype=torch.int32, device=dev)
 
     # pre-bound C-ABI calls (argument marshalling once, outside the timed region)
+    k = len(cases)
+    enc_items = (b64._lib.EncodeItem * k)()
+    dec_items = (b64._lib.DecodeItem * k)()
     enc_calls, dec_calls, fin_calls = [], [], []
     for i, c in enumerate(cases):
-        ap = ctypes.byref(c.alpha)
+        ap = ctypes.pointer(c.alpha)
+        enc_items[i] = b64._lib.EncodeItem(c.x.data_ptr(), c.n, c.enc_out.data_ptr(), ap)
+        dec_items[i] = b64._lib.DecodeItem(c.text.data_ptr(), c.m, c.dec_out.data_ptr(), ap, c.c0,
+                                           1 if c.last else 0, 0, cells[i:].data_ptr())
         enc_calls.append((V(c.x.data_ptr()), c.n, V(c.enc_out.data_ptr()), ap, sp))
         dec_calls.append((V(c.text.data_ptr()), c.m, V(c.dec_out.data_ptr()), ap, c.c0, 1 if c.last else 0,
                           V(cells[i:].data_ptr()), None, sp))
@@ -201,123 +207,152 @@ def run_ours(args):
         def allreduce():
             dist.all_reduce(cells, op=dist.ReduceOp.MIN)
 
+    enc_g, dec_g, fin_n = L.b64_encode_group, L.b64_decode_group, L.b64_decode_finalize_n
     enc_f, dec_f, fin_f = L.b64_encode, L.b64_decode_chunk, L.b64_decode_finalize
+    cells_p, err_p, st_p = V(cells.data_ptr()), V(err_off.data_ptr()), V(status.data_ptr())
     Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def flush(i):
         flush_w.fill_(i & 0xFF)
         flush_r.sum()
 
-    def step(rec):
-        """One step; rec = list to append (kind, idx, ev0, ev1) to, or None."""
+    def timed(kind, rec, fn, *fa):
+        if rec is None:
+            return fn(*fa)
+        e0, e1 = Ev(), Ev()
+        e0.record(stream)
+        rc = fn(*fa)
+        e1.record(stream)
+        rec.append((kind, e0, e1))
+        return rc
+
+    def step_group(rec):
+        """One step, grouped: ONE encode launch for the 6 cases, ONE decode launch, one finalize."""
         cells.fill_(b64.ERR_NONE)
-        for i in range(len(cases)):
-            if rec is not None:
-                e0, e1 = Ev(), Ev()
-                e0.record(stream)
-            rc = enc_f(*enc_calls[i])
-            if rec is not None:
-                e1.record(stream)
-                rec.append(("enc", i, e0, e1))
-                e0, e1 = Ev(), Ev()
-                e0.record(stream)
-            rc |= dec_f(*dec_calls[i])
-            if rec is not None:
-                e1.record(stream)
-                rec.append(("dec", i, e0, e1))
+        rc = timed("enc", rec, enc_g, enc_items, k, sp)
+        rc |= timed("dec", rec, dec_g, dec_items, k, sp)
+        if rc:
+            raise RuntimeError(f"C ABI returned {rc}")
+        if allreduce is not None:
+            allreduce()
+        fin_n(cells_p, k, err_p, st_p, sp)
+
+    def step_per_call(rec):
+        """One step, one C-ABI call (one launch) per op."""
+        cells.fill_(b64.ERR_NONE)
+        for i in range(k):
+            rc = timed("enc", rec, enc_f, *enc_calls[i])
+            rc |= timed("dec", rec, dec_f, *dec_calls[i])
             if rc:
                 raise RuntimeError(f"C ABI returned {rc}")
         if allreduce is not None:
             allreduce()
-        for i in range(len(cases)):
+        for i in range(k):
             fin_f(*fin_calls[i])
 
-    for i in range(args.warmup):
-        flush(i)
-        step(None)
-    torch.cuda.synchronize()
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
-    torch.cuda.synchronize()
-
-    launches0 = b64.launch_count()
-    recs, steps_ev = [], []
-    sampler = ClockSampler(dev.index)
-    wall0 = time.perf_counter()
-    with sampler:
-        for k in range(args.steps):
-            flush(k)
-            torch.cuda._sleep(400_000)  # let the host enqueue the whole step before it starts (no launch gaps)
-            s0, s1 = Ev(), Ev()
-            s0.record(stream)
-            step(recs)
-            s1.record(stream)
-            steps_ev.append((s0, s1))
+    def run(step, nsteps, nwarm):
+        for i in range(nwarm):
+            flush(i)
+            step(None)
         torch.cuda.synchronize()
-    if world > 1:
-        import torch.distributed as dist
+        if world > 1:
+            import torch.distributed as dist
 
-        dist.barrier()
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
-    launches = b64.launch_count() - launches0
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = b64.launch_count()
+        recs, steps_ev = [], []
+        sampler = ClockSampler(dev.index)
+        wall0 = time.perf_counter()
+        with sampler:
+            for j in range(nsteps):
+                flush(j)
+                torch.cuda._sleep(400_000)  # let the host enqueue the whole step before it starts (no launch gaps)
+                s0, s1 = Ev(), Ev()
+                s0.record(stream)
+                step(recs)
+                s1.record(stream)
+                steps_ev.append((s0, s1))
+            torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
 
-    step_ms = [a.elapsed_time(b) for a, b in steps_ev]
-    total_ms = sum(step_ms)
-    if world > 1:
-        import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+        launches = b64.launch_count() - launches0
+        total_ms = sum(a.elapsed_time(b) for a, b in steps_ev)
+        if world > 1:
+            import torch.distributed as dist
 
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-
-    # correctness of the timed outputs (cheap, device-side)
-    errs = err_off.tolist()
-    assert all(e == -1 for e in errs), errs
-    for c in cases:
-        assert torch.equal(c.enc_out, c.text) and torch.equal(c.dec_out[: c.n], c.x)
+            t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total_ms = float(t.item())
+        # correctness of the timed outputs (cheap, device-side)
+        errs = err_off.tolist()
+        assert all(e == -1 for e in errs), errs
+        for c in cases:
+            assert torch.equal(c.enc_out, c.text) and torch.equal(c.dec_out[: c.n], c.x)
+        enc_ms = [a.elapsed_time(b) for kind, a, b in recs if kind == "enc"]
+        dec_ms = [a.elapsed_time(b) for kind, a, b in recs if kind == "dec"]
+        return total_ms, enc_ms, dec_ms, launches, wall, sampler
 
     b64_bytes_rank = sum(2 * c.m for c in cases)
     b64_bytes_all = b64_bytes_rank * world
-    value = b64_bytes_all * args.steps / (total_ms * 1e-3) / 1e9
-
-    enc_ms = [a.elapsed_time(b) for kind, i, a, b in recs if kind == "enc"]
-    dec_ms = [a.elapsed_time(b) for kind, i, a, b in recs if kind == "dec"]
-    enc_alg = sum(c.n + c.m for c in cases) / len(cases)  # bytes per encode launch (read n, write m)
+    enc_alg = sum(c.n + c.m for c in cases)  # algorithmic bytes: read n, write m
     dec_alg = sum(c.m + c.mlen - (2 if c.last and c.Lg % 3 == 1 else (1 if c.last and c.Lg % 3 == 2 else 0))
-                  for c in cases) / len(cases)
-    enc_avg, dec_avg = statistics.mean(enc_ms), statistics.mean(dec_ms)
+                  for c in cases)
     peak, peak_src = peaks()
 
-    # D2D memcpy yardstick of the same base64 byte count (PAPER.md:22, 603)
-    mc_ms = []
-    src = cases[0].text
-    dst = torch.empty_like(src)
-    for k in range(max(10, min(args.steps, 30))):
-        flush(k)
-        e0, e1 = Ev(), Ev()
-        e0.record(stream)
-        dst.copy_(src)
-        e1.record(stream)
-        mc_ms.append((e0, e1))
-    torch.cuda.synchronize()
-    mc_ms = [a.elapsed_time(b) for a, b in mc_ms]
-    mc_avg = statistics.median(mc_ms)
-    m0 = cases[0].m
-    memcpy_gbs = m0 / (mc_avg * 1e-3) / 1e9  # base64 bytes per second, same convention as the codec
-    enc_gbs = statistics.mean(c.m for c in cases) / (enc_avg * 1e-3) / 1e9
-    dec_gbs = statistics.mean(c.m for c in cases) / (dec_avg * 1e-3) / 1e9
+    total_ms, enc_ms, dec_ms, launches, wall, sampler = run(step_group, args.steps, args.warmup)
+    value = b64_bytes_all * args.steps / (total_ms * 1e-3) / 1e9
+    enc_avg, dec_avg = statistics.mean(enc_ms), statistics.mean(dec_ms)  # one grouped launch each, 6 cases
+    enc_gbs = sum(c.m for c in cases) / (enc_avg * 1e-3) / 1e9
+    dec_gbs = sum(c.m for c in cases) / (dec_avg * 1e-3) / 1e9
 
-    dom = "decode" if dec_avg * len(dec_ms) >= enc_avg * len(enc_ms) else "encode"
+    # the same step with one launch per op (per-call API), for comparison
+    pc_steps = max(10, args.steps // 2)
+    pc_total, pc_enc, pc_dec, _, _, _ = run(step_per_call, pc_steps, max(3, args.warmup // 2))
+    pc_enc_avg, pc_dec_avg = statistics.mean(pc_enc), statistics.mean(pc_dec)
+    per_call = {"value": round(b64_bytes_all * pc_steps / (pc_total * 1e-3) / 1e9, 2),
+                "ms_per_step": round(pc_total / pc_steps, 5),
+                "encode_gbs": round(statistics.mean(c.m for c in cases) / (pc_enc_avg * 1e-3) / 1e9, 1),
+                "decode_gbs": round(statistics.mean(c.m for c in cases) / (pc_dec_avg * 1e-3) / 1e9, 1),
+                "roofline_frac_enc_fast": round(enc_alg / k / (pc_enc_avg * 1e-3) / 1e9 / peak, 4),
+                "roofline_frac_dec_fast": round(dec_alg / k / (pc_dec_avg * 1e-3) / 1e9 / peak, 4),
+                "note": "12 launches per step (b64_encode / b64_decode_chunk per 64 MiB op)"}
+
+    # D2D memcpy yardstick of the same base64 byte count (PAPER.md:22, 603), one case and all six
+    def copy_time(srcs, reps):
+        dsts = [torch.empty_like(x) for x in srcs]
+        evs = []
+        for j in range(reps):
+            flush(j)
+            torch.cuda._sleep(200_000)
+            e0, e1 = Ev(), Ev()
+            e0.record(stream)
+            for d, x in zip(dsts, srcs):
+                d.copy_(x)
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return statistics.median([a.elapsed_time(b) for a, b in evs])
+
+    reps = max(10, min(args.steps, 30))
+    mc1 = copy_time([cases[0].text], reps)
+    mc6 = copy_time([c.text for c in cases], reps)
+    memcpy_gbs = cases[0].m / (mc1 * 1e-3) / 1e9  # base64 bytes per second, same convention as the codec
+    memcpy6_gbs = sum(c.m for c in cases) / (mc6 * 1e-3) / 1e9
+
+    dom = "decode" if dec_avg >= enc_avg else "encode"
     ach = (dec_alg / (dec_avg * 1e-3) if dom == "decode" else enc_alg / (enc_avg * 1e-3)) / 1e9
+    oth = (enc_alg / (enc_avg * 1e-3) if dom == "decode" else dec_alg / (dec_avg * 1e-3)) / 1e9
+    kname = "dec_group_kernel" if dom == "decode" else "enc_group_kernel"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            tj = json.load(open(tp))
-            traffic = tj.get("dec_fast_kernel" if dom == "decode" else "enc_fast_kernel")
+            traffic = json.load(open(tp)).get(kname)
         except Exception:  # noqa: BLE001
             traffic = None
 
@@ -327,20 +362,24 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (splitmix64 seed 0, uniform bytes)",
         "config": {"workload": "configs[1]: 64 MiB x {n, n+1, n+2} x {standard, base64url} encode + validating decode "
                                "per rank (weak scaling, shards of one stream)",
-                   "bytes_per_rank_per_case": N_BYTES, "ops_per_step": 2 * len(cases),
+                   "bytes_per_rank_per_case": N_BYTES, "ops_per_step": 2 * k,
+                   "launches_per_step": "b64_encode_group (6 cases, 1 kernel) + b64_decode_group (1 kernel) + "
+                                        "b64_decode_finalize_n (1 kernel)",
                    "l2": "flushed before every step (256 MiB write + 256 MiB read); 1.7 GB of disjoint buffers per step",
                    "parallelism": f"dp{world}", "volume": "base64 bytes (encode output + decode input), GB=1e9"},
         "encode_gbs": round(enc_gbs, 1), "decode_gbs": round(dec_gbs, 1),
-        "memcpy_d2d_gbs": round(memcpy_gbs, 1),
-        "codec_vs_memcpy": {"encode_time_ratio": round(enc_avg / mc_avg, 4), "decode_time_ratio": round(dec_avg / mc_avg, 4),
-                            "note": "op time / D2D cudaMemcpy time of the same base64 byte count (<=1 beats memcpy)"},
-        "roofline": {"bound": "hbm", "kernel": "dec_fast_kernel" if dom == "decode" else "enc_fast_kernel",
+        "memcpy_d2d_gbs": round(memcpy_gbs, 1), "memcpy_d2d_6cases_gbs": round(memcpy6_gbs, 1),
+        "codec_vs_memcpy": {"encode_time_ratio": round(enc_avg / mc6, 4), "decode_time_ratio": round(dec_avg / mc6, 4),
+                            "note": "grouped op time / time of D2D copies of the same base64 bytes (6 cases); "
+                                    "<= 1 beats memcpy"},
+        "per_call": per_call,
+        "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                      "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": int(dec_alg if dom == "decode" else enc_alg),
                      "avg_launch_ms": round(dec_avg if dom == "decode" else enc_avg, 5),
-                     "other": {"kernel": "enc_fast_kernel" if dom == "decode" else "dec_fast_kernel",
-                               "achieved": round((enc_alg / (enc_avg * 1e-3) if dom == "decode" else dec_alg / (dec_avg * 1e-3)) / 1e9, 1)}},
+                     "other": {"kernel": "enc_group_kernel" if dom == "decode" else "dec_group_kernel",
+                               "achieved": round(oth, 1), "frac": round(oth / peak, 4)}},
         "gpu_launches": int(launches), "wall_s_timed_region": round(wall, 3),
         "clocks": sampler.summary(),
     }

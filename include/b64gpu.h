@@ -138,6 +138,37 @@ int b64_decode_chunk(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_a
 int b64_decode_finalize(const int64_t *d_err_min, int64_t *d_err_off, int32_t *d_status,
                         b64_stream_t stream);
 
+/* ---- grouped launches -------------------------------------------------------- */
+/* Several independent streams (each with its own alphabet, input, output and
+ * length) processed by one kernel per group of up to 8: the same computation as
+ * one b64_encode / b64_decode_chunk per item, with the per-launch fixed cost
+ * paid once per group.  Items whose pointers are not fast-path aligned (encode:
+ * d_in 8 B, d_out 32 B; decode: d_in 32 B, d_out 16 B) get their own launch.
+ * `items` is a host array read during the call only. */
+typedef struct b64_encode_item {
+    const uint8_t *d_in; /* device, n bytes                         */
+    int64_t n;
+    uint8_t *d_out;      /* device, b64_encoded_len(n) bytes        */
+    const b64_alphabet *a;
+} b64_encode_item;
+
+typedef struct b64_decode_item {
+    const uint8_t *d_in; /* device, m chars, m % 4 == 0             */
+    int64_t m;
+    uint8_t *d_out;      /* device, 3*m/4 bytes capacity             */
+    const b64_alphabet *a;
+    int64_t base_offset; /* as b64_decode_chunk                      */
+    int32_t is_final;    /* as b64_decode_chunk                      */
+    int32_t reserved;
+    int64_t *d_err_min;  /* device packed error word, caller-initialised to B64_ERR_NONE */
+} b64_decode_item;
+
+int b64_encode_group(const b64_encode_item *items, int64_t count, b64_stream_t stream);
+int b64_decode_group(const b64_decode_item *items, int64_t count, b64_stream_t stream);
+/* b64_decode_finalize for `count` consecutive packed words. */
+int b64_decode_finalize_n(const int64_t *d_err_min, int64_t count, int64_t *d_err_off, int32_t *d_status,
+                          b64_stream_t stream);
+
 /* ---- host buffers, overlapped (SURVEY.md Sec. 8(f) f3 ingest pipeline) ------ */
 /* Encode / decode HOST buffers (h_*: host pointers, pinned for the copies to be
  * asynchronous) through a caller-owned DEVICE workspace d_ws of ws_bytes.  The

@@ -24,6 +24,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
     "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline",
+    "encode_group", "decode_group",
     "ERR_NONE",
 ]
 
@@ -151,6 +152,53 @@ def decode_finalize(err_cell: torch.Tensor, err_off: torch.Tensor, status: Optio
     _check_i64(err_off, "err_off")
     _lib.check(_lib.lib().b64_decode_finalize(_ptr(err_cell), _ptr(err_off), _ptr(status), _stream(stream)),
                "b64_decode_finalize")
+
+
+# ------------------------------------------------------------------ grouped launches
+
+def encode_group(xs, alphabets=None, outs=None, stream: Optional[torch.cuda.Stream] = None):
+    """Encode several independent device buffers with one kernel per group of 8 (b64_encode_group).
+    alphabets: one Alphabet for all, or a list; returns the list of outputs."""
+    k = len(xs)
+    al = alphabets if isinstance(alphabets, (list, tuple)) else [alphabets] * k
+    al = [a if a is not None else standard() for a in al]
+    if outs is None:
+        outs = [torch.empty(encoded_len(x.numel()), dtype=torch.uint8, device=x.device) for x in xs]
+    items = (_lib.EncodeItem * max(k, 1))()
+    for i, (x, o) in enumerate(zip(xs, outs)):
+        _check_u8(x, "x")
+        _check_u8(o, "out")
+        items[i] = _lib.EncodeItem(x.data_ptr(), x.numel(), o.data_ptr(), ctypes.pointer(al[i]))
+    _lib.check(_lib.lib().b64_encode_group(items, k, _stream(stream)), "b64_encode_group")
+    return [o[: encoded_len(x.numel())] for x, o in zip(xs, outs)]
+
+
+def decode_group(ts, alphabets=None, outs=None, cells: Optional[torch.Tensor] = None, bases=None, finals=None,
+                 stream: Optional[torch.cuda.Stream] = None):
+    """Validating decode of several device buffers, one kernel per group of 8 (b64_decode_group).
+    Returns (outs, err_off int64[k] device tensor, status int32[k] device tensor)."""
+    k = len(ts)
+    dev = ts[0].device
+    al = alphabets if isinstance(alphabets, (list, tuple)) else [alphabets] * k
+    al = [a if a is not None else standard() for a in al]
+    if outs is None:
+        outs = [torch.empty(max(decoded_len_max(t.numel()), 1), dtype=torch.uint8, device=dev) for t in ts]
+    if cells is None:
+        cells = torch.full((k,), ERR_NONE, dtype=torch.int64, device=dev)
+    items = (_lib.DecodeItem * max(k, 1))()
+    for i, (t, o) in enumerate(zip(ts, outs)):
+        _check_u8(t, "t")
+        if t.numel() % 4:
+            raise B64Error("B64_ELENGTH: text length is not a multiple of 4")
+        items[i] = _lib.DecodeItem(t.data_ptr(), t.numel(), o.data_ptr(), ctypes.pointer(al[i]),
+                                   0 if bases is None else bases[i], 1 if finals is None else int(finals[i]), 0,
+                                   cells[i:].data_ptr())
+    _lib.check(_lib.lib().b64_decode_group(items, k, _stream(stream)), "b64_decode_group")
+    err = torch.empty(k, dtype=torch.int64, device=dev)
+    st = torch.empty(k, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib().b64_decode_finalize_n(_ptr(cells), k, _ptr(err), _ptr(st), _stream(stream)),
+               "b64_decode_finalize_n")
+    return outs, err, st
 
 
 # ------------------------------------------------------------------ host buffers (overlapped pipeline)

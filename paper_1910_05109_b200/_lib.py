@@ -43,6 +43,16 @@ class Alphabet(ctypes.Structure):
 
 AP = ctypes.POINTER(Alphabet)
 
+
+class EncodeItem(ctypes.Structure):
+    _fields_ = [("d_in", ctypes.c_void_p), ("n", ctypes.c_int64), ("d_out", ctypes.c_void_p), ("a", AP)]
+
+
+class DecodeItem(ctypes.Structure):
+    _fields_ = [("d_in", ctypes.c_void_p), ("m", ctypes.c_int64), ("d_out", ctypes.c_void_p), ("a", AP),
+                ("base_offset", ctypes.c_int64), ("is_final", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("d_err_min", ctypes.c_void_p)]
+
 SIGNATURES = [
     ("b64_alphabet_init", INT, [AP, ctypes.c_char_p, ctypes.c_char, ctypes.POINTER(INT)]),
     ("b64_alphabet_standard", AP, []),
@@ -54,6 +64,9 @@ SIGNATURES = [
     ("b64_decode_ex", INT, [P, I64, P, AP, P, P, P, P]),
     ("b64_decode_chunk", INT, [P, I64, P, AP, I64, INT, P, P, P]),
     ("b64_decode_finalize", INT, [P, P, P, P]),
+    ("b64_encode_group", INT, [P, I64, P]),
+    ("b64_decode_group", INT, [P, I64, P]),
+    ("b64_decode_finalize_n", INT, [P, I64, P, P, P]),
     ("b64_host_workspace_bytes", I64, [I64]),
     ("b64_encode_host", INT, [P, I64, P, AP, P, I64, P, P, P]),
     ("b64_decode_host", INT, [P, I64, P, AP, P, I64, P, P, P, P, P]),

@@ -2,4 +2,5 @@
 // compilation: the templated kernels are instantiated and launched in one TU).
 #include "encode.cu"
 #include "decode.cu"
+#include "group.cu"
 #include "capi.cu"

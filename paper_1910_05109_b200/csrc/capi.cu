@@ -22,6 +22,7 @@ const char kUrlChars[65] = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz
 
 struct DevInfo {
     int sms = 0;
+    int occ_enc_group[4] = {0, 0, 0, 0}, occ_dec_group[4] = {0, 0, 0, 0};
     int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_dec_ts[4] = {0, 0, 0, 0}, occ_enc_tma = 0, occ_enc_gen = 0, occ_dec_gen = 0;
 };
 constexpr int kMaxDev = 64;
@@ -45,6 +46,12 @@ const DevInfo* dev_info() {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_ts[1], dec_fast_kernel<1, true>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_ts[2], dec_fast_kernel<2, true>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_ts[3], dec_fast_kernel<3, true>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_group[1], enc_group_kernel<1>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_group[2], enc_group_kernel<2>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_group[1], dec_group_kernel<1>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_group[2], dec_group_kernel<2>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_group[3], enc_group_kernel<3>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_group[3], dec_group_kernel<3>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_tma, enc_tma_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0))
@@ -53,6 +60,8 @@ const DevInfo* dev_info() {
         info.occ_enc_fast[i] = info.occ_enc_fast[i] < 1 ? 1 : info.occ_enc_fast[i];
         info.occ_dec_fast[i] = info.occ_dec_fast[i] < 1 ? 1 : info.occ_dec_fast[i];
         info.occ_dec_ts[i] = info.occ_dec_ts[i] < 1 ? 1 : info.occ_dec_ts[i];
+        info.occ_enc_group[i] = info.occ_enc_group[i] < 1 ? 1 : info.occ_enc_group[i];
+        info.occ_dec_group[i] = info.occ_dec_group[i] < 1 ? 1 : info.occ_dec_group[i];
     }
     info.occ_enc_tma = info.occ_enc_tma < 1 ? 1 : info.occ_enc_tma;
     info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
@@ -412,6 +421,118 @@ int b64_decode_host(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_al
         cudaEventRecord(pipe.d2h[b], sd);
     }
     return b64_decode_finalize(d_err_off, d_err_off, d_status, s_comp);
+}
+
+// ---------------------------------------------------------------- grouped launches
+int b64_encode_group(const b64_encode_item* items, int64_t count, b64_stream_t stream) {
+    if (count < 0 || (count > 0 && !items)) return B64_EINVAL;
+    for (int64_t i = 0; i < count; ++i)
+        if (items[i].n < 0 || !alpha_ok(items[i].a) || (items[i].n > 0 && (!items[i].d_in || !items[i].d_out)))
+            return B64_EINVAL;
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    EncGroup g;
+    std::memset(&g, 0, sizeof(g));
+    int64_t bytes = 0;
+    auto flush = [&]() -> int {
+        if (g.count == 0) return B64_OK;
+        const int d = enc_depth(bytes);
+        const int64_t blocks = balanced_blocks(g.cstart[g.count], int64_t(di->sms) * di->occ_enc_group[d]);
+        launch(pick3(d, enc_group_kernel<1>, enc_group_kernel<2>, enc_group_kernel<3>), blocks, kThreads, s, g);
+        const int r = launched();
+        std::memset(&g, 0, sizeof(g));
+        bytes = 0;
+        return r;
+    };
+    for (int64_t i = 0; i < count; ++i) {
+        const b64_encode_item& it = items[i];
+        if (it.n == 0) continue;
+        if (!(aligned(it.d_in, 8) && aligned(it.d_out, 32))) {  // not groupable: its own launch
+            const int r = b64_encode(it.d_in, it.n, it.d_out, it.a, stream);
+            if (r != B64_OK) return r;
+            continue;
+        }
+        const int k = g.count;
+        g.in[k] = it.d_in;
+        g.out[k] = it.d_out;
+        g.n[k] = it.n;
+        g.pad[k] = it.a->pad;
+        std::memcpy(g.lut[k], it.a->enc, 64);
+        g.cstart[k + 1] = g.cstart[k] + it.n / 768;
+        g.count = k + 1;
+        bytes += it.n;
+        if (g.count == kGroupMax) {
+            const int r = flush();
+            if (r != B64_OK) return r;
+        }
+    }
+    return flush();
+}
+
+int b64_decode_group(const b64_decode_item* items, int64_t count, b64_stream_t stream) {
+    if (count < 0 || (count > 0 && !items)) return B64_EINVAL;
+    for (int64_t i = 0; i < count; ++i) {
+        const b64_decode_item& it = items[i];
+        if (it.m < 0 || it.base_offset < 0 || !alpha_ok(it.a) || !it.d_err_min || (it.m > 0 && (!it.d_in || !it.d_out)))
+            return B64_EINVAL;
+        if (it.m % 4) return B64_ELENGTH;
+    }
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    DecGroup g;
+    std::memset(&g, 0, sizeof(g));
+    int64_t bytes = 0;
+    auto flush = [&]() -> int {
+        if (g.count == 0) return B64_OK;
+        const int d = dec_depth(bytes);
+        const int64_t blocks = balanced_blocks(g.cstart[g.count], int64_t(di->sms) * di->occ_dec_group[d]);
+        launch(pick3(d, dec_group_kernel<1>, dec_group_kernel<2>, dec_group_kernel<3>), blocks, kThreads, s, g);
+        const int r = launched();
+        std::memset(&g, 0, sizeof(g));
+        bytes = 0;
+        return r;
+    };
+    for (int64_t i = 0; i < count; ++i) {
+        const b64_decode_item& it = items[i];
+        if (it.m == 0) continue;
+        if (!(aligned(it.d_in, 32) && aligned(it.d_out, 16))) {
+            const int r = b64_decode_chunk(it.d_in, it.m, it.d_out, it.a, it.base_offset, it.is_final, it.d_err_min,
+                                           nullptr, stream);
+            if (r != B64_OK) return r;
+            continue;
+        }
+        const int k = g.count;
+        g.in[k] = it.d_in;
+        g.out[k] = it.d_out;
+        g.m[k] = it.m;
+        g.base[k] = it.base_offset;
+        g.cell[k] = reinterpret_cast<unsigned long long*>(it.d_err_min);
+        g.is_final[k] = it.is_final ? 1 : 0;
+        g.pad[k] = it.a->pad;
+        std::memcpy(g.lut[k], it.a->dec, 256);
+        const int64_t Q = it.m / 4;
+        const int64_t Qint = (it.is_final && Q > 0) ? Q - 1 : Q;
+        g.cstart[k + 1] = g.cstart[k] + Qint / 256;
+        g.count = k + 1;
+        bytes += it.m;
+        if (g.count == kGroupMax) {
+            const int r = flush();
+            if (r != B64_OK) return r;
+        }
+    }
+    return flush();
+}
+
+int b64_decode_finalize_n(const int64_t* d_err_min, int64_t count, int64_t* d_err_off, int32_t* d_status,
+                          b64_stream_t stream) {
+    if (count < 0 || (count > 0 && (!d_err_min || !d_err_off))) return B64_EINVAL;
+    if (count == 0) return B64_OK;
+    const int64_t blocks = (count + kThreads - 1) / kThreads;
+    launch(dec_finalize_n_kernel, blocks > 1024 ? 1024 : blocks, kThreads, reinterpret_cast<cudaStream_t>(stream),
+           d_err_min, count, d_err_off, d_status);
+    return launched();
 }
 
 int b64_encode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count, uint8_t* d_out,

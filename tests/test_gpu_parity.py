@@ -7,6 +7,8 @@ tails, misaligned pointers (the generic kernels), every byte value at every
 position of small texts, and BASELINE.json's configs at full size (sampled
 windows where the oracle would need more host memory than is sensible).
 """
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -497,3 +499,66 @@ def test_dist_layer_world1_cuda(b64):
     out, err, st = b64dist.decode_sharded(to_dev(t2), ds)
     assert (err, st) == (5000, oracle.ST_BADCHAR)
     assert np.array_equal(out[: 3 * (5000 // 4)].cpu().numpy(), x[: 3 * (5000 // 4)])
+
+
+# ------------------------------------------------------------------ grouped launches
+
+def test_group_encode_decode_vs_oracle(b64):
+    al = _alphabets(b64)
+    sizes = [0, 1, 2, 3, 767, 768, 769, 5000, 100_003, 768 * 300 + 1, 768 * 1000 + 2, 64, 3 * 1024]
+    for rep in range(2):
+        xs, refs, chars_l, alph_l, offs = [], [], [], [], []
+        for i, n in enumerate(sizes):
+            chars, pad, alpha = al[(i + rep) % len(al)]
+            x = synth.data(n, seed=1000 * rep + i)
+            xs.append(x)
+            refs.append(oracle.encode(x, chars, pad))
+            chars_l.append((chars, pad))
+            alph_l.append(alpha)
+        # some items misaligned (own launch), others grouped (more than 8 -> two groups)
+        dx = [to_dev(x, 1 if (i % 5 == 4) else 0) for i, x in enumerate(xs)]
+        outs = b64.encode_group(dx, alph_l)
+        for i in range(len(sizes)):
+            assert np.array_equal(outs[i].cpu().numpy(), refs[i]), (rep, i)
+        texts = []
+        for i, r in enumerate(refs):
+            t = r.copy()
+            if i % 3 == 1 and t.size > 4:
+                pos, bad = synth.corruption(2, t.size, chars_l[i][0], seed=i, pad=chars_l[i][1])
+                t[pos] = bad
+            texts.append(t)
+        dt = [to_dev(t, 3 if (i % 4 == 3) else 0) for i, t in enumerate(texts)]
+        douts, err, st = b64.decode_group(dt, alph_l)
+        errc, stc = err.cpu().numpy(), st.cpu().numpy()
+        for i, t in enumerate(texts):
+            ref, rerr, rst = oracle.decode(t, *chars_l[i])
+            assert (errc[i], stc[i]) == (rerr, rst), (rep, i)
+            assert np.array_equal(douts[i][: ref.size].cpu().numpy(), ref), (rep, i)
+
+
+def test_group_decode_as_shards(b64):
+    """Grouped items as shards of one stream: global bases, only the last is final, one cell."""
+    x = synth.data(768 * 500 + 1, seed=3)
+    text = oracle.encode(x)
+    for trial in range(4):
+        t2 = text.copy()
+        if trial:
+            pos, bad = synth.corruption(trial, text.size, oracle.STANDARD, seed=trial)
+            t2[pos] = bad
+        ref, rerr, rst = oracle.decode(t2)
+        cuts = [0, 1024 * 100, 1024 * 101, 1024 * 350, t2.size]
+        dt = to_dev(t2)
+        parts = [dt[cuts[i]: cuts[i + 1]] for i in range(len(cuts) - 1)]
+        cell = torch.full((1,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+        items = (b64._lib.DecodeItem * len(parts))()
+        outs = [torch.empty(3 * (p.numel() // 4), dtype=torch.uint8, device=DEV) for p in parts]
+        std = b64.standard()
+        for i, p in enumerate(parts):
+            items[i] = b64._lib.DecodeItem(p.data_ptr(), p.numel(), outs[i].data_ptr(), ctypes.pointer(std),
+                                           cuts[i], int(i == len(parts) - 1), 0, cell.data_ptr())
+        b64._lib.check(b64._lib.lib().b64_decode_group(items, len(parts), None), "group")
+        eo = torch.empty(1, dtype=torch.int64, device=DEV)
+        b64.decode_finalize(cell, eo)
+        assert int(eo.item()) == rerr
+        got = torch.cat(outs).cpu().numpy()
+        assert np.array_equal(got[: ref.size], ref)

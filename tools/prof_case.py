@@ -18,10 +18,21 @@ import synth  # noqa: E402
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--op", choices=("enc", "dec", "both", "batch"), default="both")
+    p.add_argument("--op", choices=("enc", "dec", "both", "batch", "group"), default="both")
     p.add_argument("--n", type=int, default=1 << 30)
     p.add_argument("--reps", type=int, default=3)
     a = p.parse_args()
+    if a.op == "group":  # configs[1]: 6 x 64 MiB (+0/1/2) grouped encode + decode
+        xs = [synth.device_data(a.n + d, seed=0) for d in (0, 0, 1, 1, 2, 2)]
+        al = [b64.standard(), b64.url()] * 3
+        ts = b64.encode_group(xs, al)
+        for _ in range(a.reps):
+            b64.encode_group(xs, al, outs=ts)
+            outs, err, st = b64.decode_group(ts, al)
+        torch.cuda.synchronize()
+        assert (err == -1).all()
+        print("ok group")
+        return
     if a.op == "batch":
         Ls = synth.loguniform_lengths(1_000_000, seed=0)
         off = synth.offsets(Ls)
