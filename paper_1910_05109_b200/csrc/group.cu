@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreads) enc_group_kernel(const __grid_consta
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads) dec_group_kernel(const __grid_constant__ DecGroup g) {
+__global__ void __launch_bounds__(kThreads, 5) dec_group_kernel(const __grid_constant__ DecGroup g) {
     __shared__ __align__(256) uint32_t s_lut[kGroupMax][64];
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];
     griddep_launch_dependents();
