@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (profiling runs)")
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
     return p.parse_args()
 
 
@@ -127,8 +128,11 @@ def dist_setup(args):
         import torch.distributed as dist
 
         if args.impl == "ours":
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            torch.cuda.set_device(local % torch.cuda.device_count())
+            if args.dist_backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            else:
+                dist.init_process_group(args.dist_backend)
         else:
             dist.init_process_group("gloo")
     elif args.impl == "ours":
