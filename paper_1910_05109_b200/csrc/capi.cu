@@ -3,6 +3,7 @@
 // per-call state; every launch goes to the caller's stream.
 #include <atomic>
 #include <cstdio>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -453,6 +454,15 @@ int b64_encode_group(const b64_encode_item* items, int64_t count, b64_stream_t s
             if (r != B64_OK) return r;
             continue;
         }
+        if (it.n / 768 >= int64_t(INT32_MAX) / 2) {  // > 800 GB: too many chunks for a group's int32 cursor
+            const int r = b64_encode(it.d_in, it.n, it.d_out, it.a, stream);
+            if (r != B64_OK) return r;
+            continue;
+        }
+        if (g.count && g.cstart[g.count] + it.n / 768 >= int64_t(INT32_MAX) / 2) {
+            const int r = flush();
+            if (r != B64_OK) return r;
+        }
         const int k = g.count;
         g.in[k] = it.d_in;
         g.out[k] = it.d_out;
@@ -502,6 +512,16 @@ int b64_decode_group(const b64_decode_item* items, int64_t count, b64_stream_t s
                                            nullptr, stream);
             if (r != B64_OK) return r;
             continue;
+        }
+        if (it.m / 1024 >= int64_t(INT32_MAX) / 2) {  // too many chunks for a group's int32 cursor
+            const int r = b64_decode_chunk(it.d_in, it.m, it.d_out, it.a, it.base_offset, it.is_final, it.d_err_min,
+                                           nullptr, stream);
+            if (r != B64_OK) return r;
+            continue;
+        }
+        if (g.count && g.cstart[g.count] + it.m / 1024 >= int64_t(INT32_MAX) / 2) {
+            const int r = flush();
+            if (r != B64_OK) return r;
         }
         const int k = g.count;
         g.in[k] = it.d_in;

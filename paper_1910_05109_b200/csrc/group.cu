@@ -36,26 +36,36 @@ struct DecGroup {
     int count;
 };
 
-// Monotone cursor over the concatenated chunk space of a group: a warp visits
-// chunks c0, c0 + W, c0 + 2W, ... so the owning stream only moves forward;
-// advancing costs one compare per chunk (the stream's pointers stay in
-// registers instead of being re-read from the parameter bank).
+// Monotone cursor over the concatenated chunk space of a group.  A warp visits
+// chunks c0, c0 + W, c0 + 2W, ... so the owning stream only moves forward:
+// `next` is one compare and one pointer add per chunk; the stream's base
+// pointer is re-read from the parameter bank only when a stream boundary is
+// crossed (a per-chunk search cost ~35 % more instructions, profiles/).
+template <int UNIT, bool IN>
 struct GroupCursor {
     int it;
-    int64_t lo, hi;  // [cstart[it], cstart[it+1])
+    int32_t lo, hi;   // chunk range [lo, hi) of stream it (a group holds < 2^31 chunks)
+    const uint8_t* p; // address of the current chunk (+ the lane offset)
     template <typename G>
-    __device__ __forceinline__ void init(const G& g) {
-        it = 0;
-        lo = g.cstart[0];
-        hi = g.cstart[1];
-    }
-    template <typename G>
-    __device__ __forceinline__ void seek(const G& g, int64_t c) {
+    __device__ __forceinline__ void locate(const G& g, int32_t c, int lane_off) {
         while (c >= hi && it + 1 < g.count) {
             ++it;
             lo = hi;
-            hi = g.cstart[it + 1];
+            hi = int32_t(g.cstart[it + 1]);
         }
+        p = (IN ? g.in[it] : static_cast<const uint8_t*>(g.out[it])) + int64_t(c - lo) * UNIT + lane_off;
+    }
+    template <typename G>
+    __device__ __forceinline__ void start(const G& g, int32_t c, int lane_off) {
+        it = 0;
+        lo = int32_t(g.cstart[0]);
+        hi = int32_t(g.cstart[1]);
+        locate(g, c, lane_off);
+    }
+    template <typename G>
+    __device__ __forceinline__ void next(const G& g, int32_t c, int64_t step, int lane_off) {
+        if (c < hi) p += step;
+        else locate(g, c, lane_off);
     }
 };
 
@@ -67,40 +77,44 @@ __global__ void __launch_bounds__(kThreads) enc_group_kernel(const __grid_consta
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
     const int64_t nwarp = gthreads >> 5;
-    const int64_t C = g.cstart[g.count];
-    const int64_t c0 = gtid >> 5;
-    GroupCursor cur, pre;  // the chunk being encoded / the chunk being prefetched
-    cur.init(g);
-    pre.init(g);
+    const int32_t C = int32_t(g.cstart[g.count]);
+    const int32_t c0 = int32_t(gtid >> 5);
+    const int32_t W = int32_t(nwarp);
+    GroupCursor<768, true> pre;    // input of the chunk being prefetched
+    GroupCursor<1024, false> cur;  // output of the chunk being encoded
 
     griddep_wait();
     uint32_t wv[D][6];
+    if (c0 < C) {
+        pre.start(g, c0, lane * 24);
+        cur.start(g, c0, lane * 32);
+    }
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        const int64_t c = c0 + j * nwarp;
+        const int32_t c = c0 + j * W;
         if (c < C) {
-            pre.seek(g, c);
-            enc_lane24(g.in[pre.it] + (c - pre.lo) * 768 + lane * 24, wv[j]);
+            if (j) pre.next(g, c, nwarp * 768, lane * 24);
+            enc_lane24(pre.p, wv[j]);
         }
     }
     if (threadIdx.x < g.count * 16) (&s_lut[0][0])[threadIdx.x] = (&g.lut[0][0])[threadIdx.x];
     __syncthreads();
     const uint32_t lb0 = smem_u32(&s_lut[0][0]);
 
-    for (int64_t cb = c0; cb < C; cb += D * nwarp) {
+    for (int32_t cb = c0; cb < C; cb += D * W) {
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            const int64_t c = cb + j * nwarp;
+            const int32_t c = cb + j * W;
             if (c < C) {
                 uint32_t yv[6], o[8];
-                const int64_t cn = c + D * nwarp;
+                const int32_t cn = c + D * W;
                 if (cn < C) {
-                    pre.seek(g, cn);
-                    enc_lane24(g.in[pre.it] + (cn - pre.lo) * 768 + lane * 24, yv);
+                    pre.next(g, cn, nwarp * 768, lane * 24);
+                    enc_lane24(pre.p, yv);
                 }
-                cur.seek(g, c);
+                if (c != c0) cur.next(g, c, nwarp * 1024, lane * 32);
                 enc_lane_compute(wv[j], o, lb0 + 64 * cur.it);
-                st256(g.out[cur.it] + (c - cur.lo) * 1024 + lane * 32, o);
+                st256(const_cast<uint8_t*>(cur.p), o);
 #pragma unroll
                 for (int k = 0; k < 6; ++k) wv[j][k] = yv[k];
             }
@@ -128,7 +142,7 @@ __global__ void __launch_bounds__(kThreads) enc_group_kernel(const __grid_consta
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 5) dec_group_kernel(const __grid_constant__ DecGroup g) {
+__global__ void __launch_bounds__(kThreads) dec_group_kernel(const __grid_constant__ DecGroup g) {
     __shared__ __align__(256) uint32_t s_lut[kGroupMax][64];
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];
     griddep_launch_dependents();
@@ -136,41 +150,44 @@ __global__ void __launch_bounds__(kThreads, 5) dec_group_kernel(const __grid_con
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
     const int64_t nwarp = gthreads >> 5;
-    const int64_t C = g.cstart[g.count];
-    const int64_t c0 = gtid >> 5;
+    const int32_t C = int32_t(g.cstart[g.count]);
+    const int32_t c0 = int32_t(gtid >> 5);
+    const int32_t W = int32_t(nwarp);
     const uint32_t sb = smem_u32(&s_stage[threadIdx.x >> 5][0]);
-    GroupCursor cur, pre;
-    cur.init(g);
-    pre.init(g);
+    GroupCursor<1024, true> pre;  // input of the chunk being prefetched
+    GroupCursor<768, false> cur;  // output of the chunk being decoded
 
     griddep_wait();
     uint32_t xr[D][8];
+    if (c0 < C) {
+        pre.start(g, c0, lane * 32);
+        cur.start(g, c0, lane * 8);
+    }
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        const int64_t c = c0 + j * nwarp;
+        const int32_t c = c0 + j * W;
         if (c < C) {
-            pre.seek(g, c);
-            ld256_stream(g.in[pre.it] + (c - pre.lo) * 1024 + lane * 32, xr[j]);
+            if (j) pre.next(g, c, nwarp * 1024, lane * 32);
+            ld256_stream(pre.p, xr[j]);
         }
     }
     for (int t = threadIdx.x; t < g.count * 64; t += blockDim.x) (&s_lut[0][0])[t] = (&g.lut[0][0])[t];
     __syncthreads();
     const uint32_t lb0 = smem_u32(&s_lut[0][0]);
 
-    for (int64_t cb = c0; cb < C; cb += D * nwarp) {
+    for (int32_t cb = c0; cb < C; cb += D * W) {
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            const int64_t c = cb + j * nwarp;
+            const int32_t c = cb + j * W;
             if (c < C) {
                 uint32_t y[8];
-                const int64_t cn = c + D * nwarp;
+                const int32_t cn = c + D * W;
                 if (cn < C) {
-                    pre.seek(g, cn);
-                    ld256_stream(g.in[pre.it] + (cn - pre.lo) * 1024 + lane * 32, y);
+                    pre.next(g, cn, nwarp * 1024, lane * 32);
+                    ld256_stream(pre.p, y);
                 }
-                cur.seek(g, c);
+                if (c != c0) cur.next(g, c, nwarp * 768, lane * 8);
                 const int it = cur.it;
-                const int64_t lc = c - cur.lo;
                 const uint32_t lb = lb0 + 256 * it;
                 uint32_t err = 0, v[8];
 #pragma unroll
@@ -182,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 5) dec_group_kernel(const __grid_con
                 sts64(sb + lane * 24 + 8, o[2], o[3]);
                 sts64(sb + lane * 24 + 16, o[4], o[5]);
                 __syncwarp();
-                uint8_t* dst = g.out[it] + lc * 768 + lane * 8;
+                uint8_t* dst = const_cast<uint8_t*>(cur.p);
                 const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8), s2 = lds64(sb + 512 + lane * 8);
                 st64(dst, s0.x, s0.y);
                 st64(dst + 256, s1.x, s1.y);
@@ -191,6 +208,7 @@ __global__ void __launch_bounds__(kThreads, 5) dec_group_kernel(const __grid_con
                 const bool bad = (err & kInvalid) != 0;
                 if (__any_sync(kFull, bad)) {
                     const uint8_t* lut = reinterpret_cast<const uint8_t*>(&s_lut[it][0]);
+                    const int64_t lc = int64_t(c - cur.lo);
                     uint32_t rel = 0xffffffffu;
                     if (bad) {
                         rel = scan_first_bad(g.in[it] + lc * 1024 + lane * 32, 8, lut);
