@@ -155,6 +155,16 @@ bool dec_tma_store() {
     return v;
 }
 
+// Resident CTAs per SM used by the single-stream kernels: at most 5 (40 warps;
+// measured best for 64 MiB ops on B200, bench per_call), B64_MAX_BPS overrides.
+int cap_bps(int occ) {
+    static const int cap = [] {
+        const char* e = std::getenv("B64_MAX_BPS");
+        return e ? std::atoi(e) : 5;
+    }();
+    return (cap > 0 && cap < occ) ? cap : occ;
+}
+
 template <typename K>
 K pick3(int d, K k1, K k2, K k3) { return d == 3 ? k3 : (d == 2 ? k2 : k1); }
 
@@ -236,7 +246,7 @@ int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabe
     } else if (aligned(d_in, 8) && aligned(d_out, 32)) {
         const int64_t nchunk = n / 768;
         const int dd = enc_depth(n);
-        const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * di->occ_enc_fast[dd]);
+        const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(di->occ_enc_fast[dd]));
         launch(pick3(dd, enc_fast_kernel<1>, enc_fast_kernel<2>, enc_fast_kernel<3>), blocks, kThreads, s, d_in, n,
                d_out, enc_tab(a), a->pad);
     } else {
@@ -256,7 +266,8 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
         const int64_t nchunk = (m / 4) / 256;
         const int dd = dec_depth(m);
         const bool ts = dec_tma_store();
-        const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * (ts ? di->occ_dec_ts[dd] : di->occ_dec_fast[dd]));
+        const int64_t blocks =
+            balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(ts ? di->occ_dec_ts[dd] : di->occ_dec_fast[dd]));
         auto k = ts ? pick3(dd, dec_fast_kernel<1, true>, dec_fast_kernel<2, true>, dec_fast_kernel<3, true>)
                     : pick3(dd, dec_fast_kernel<1, false>, dec_fast_kernel<2, false>, dec_fast_kernel<3, false>);
         launch(k, blocks, kThreads, s, d_in, m, d_out, dec_tab(a), base, is_final, c, out_len);

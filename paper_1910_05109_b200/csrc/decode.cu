@@ -61,25 +61,36 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     // 24-byte lane outputs are re-laid through a per-warp shared buffer
     // (conflict-free STS.64 at a 24 B stride) so the global stores are
     // lane-linear STG.64 writing whole sectors.
+    // int32 chunk indices and pointers advanced by the grid stride.
     griddep_wait();
     const int64_t c0 = gtid >> 5;
+    const int32_t C = int32_t(nchunk), W = int32_t(nwarp), c0i = int32_t(c0);
+    const int64_t sin = nwarp * 1024, sout = nwarp * 768;
+    const uint8_t* pin = in + c0 * 1024 + lane * 32;  // next chunk to load
+    const uint8_t* pcur = in + c0 * 1024 + lane * 32; // chunk being decoded (rare error rescan)
+    uint8_t* pout = out + c0 * 768;                   // its output
     uint32_t kk = 0;  // chunks done by this warp (TMA-store buffer parity)
     uint32_t xr[D][8];
 #pragma unroll
     for (int i = 0; i < D; ++i)
-        if (c0 + i * nwarp < nchunk) ld256_stream(in + (c0 + i * nwarp) * 1024 + lane * 32, xr[i]);
+        if (c0i + i * W < C) {
+            ld256_stream(pin, xr[i]);
+            pin += sin;
+        }
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const uint32_t lb = smem_u32(s_lut);
-    for (int64_t cb = c0; cb < nchunk; cb += D * nwarp) {
+    for (int32_t cb = c0i; cb < C; cb += D * W) {
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            const int64_t c = cb + i * nwarp;
-            if (c < nchunk) {
+            const int32_t c = cb + i * W;
+            if (c < C) {
                 uint32_t y[8];
-                const int64_t cn = c + D * nwarp;
-                if (cn < nchunk) ld256_stream(in + cn * 1024 + lane * 32, y);
+                if (c + D * W < C) {
+                    ld256_stream(pin, y);
+                    pin += sin;
+                }
                 uint32_t err = 0, v[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(xr[i][q], lb, err);
@@ -97,7 +108,7 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_1d(out + c * 768, sbuf, 768);
+                        tma_store_1d(pout, sbuf, 768);
                         tma_store_commit();
                     }
                     ++kk;
@@ -106,7 +117,7 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
                     sts64(sb + lane * 24 + 8, o[2], o[3]);
                     sts64(sb + lane * 24 + 16, o[4], o[5]);
                     __syncwarp();
-                    uint8_t* dst = out + c * 768 + lane * 8;
+                    uint8_t* dst = pout + lane * 8;
                     const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8),
                                 s2 = lds64(sb + 512 + lane * 8);
                     st64(dst, s0.x, s0.y);
@@ -118,11 +129,13 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
                 if (__any_sync(kFull, bad)) {  // rare: locate the first invalid char of the chunk
                     uint32_t rel = 0xffffffffu;
                     if (bad) {
-                        rel = scan_first_bad(in + c * 1024 + lane * 32, 8, lut);
+                        rel = scan_first_bad(pcur, 8, lut);
                         if (rel != 0xffffffffu) rel += lane * 32;
                     }
-                    warp_report(bad, rel, base + c * 1024, err_cell);
+                    warp_report(bad, rel, base + int64_t(c) * 1024, err_cell);
                 }
+                pout += sout;
+                pcur += sin;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) xr[i][j] = y[j];
             }

@@ -51,11 +51,20 @@ enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__
     // chunks per warp are in flight ahead of the one being encoded.  The first
     // loads are issued before the alphabet is staged, so the table set-up
     // hides under the first DRAM latency.
+    // int32 chunk indices (an HBM-resident stream has < 2^31 chunks) and
+    // pointers advanced by the grid stride: no 64-bit index math per chunk.
     griddep_wait();
+    const int32_t C = int32_t(nchunk), W = int32_t(nwarp), c0i = int32_t(c0);
+    const int64_t sin = nwarp * 768, sout = nwarp * 1024;
+    const uint8_t* pin = in + c0 * 768 + lane * 24;  // next chunk to load
+    uint8_t* pout = out + c0 * 1024 + lane * 32;     // next chunk to store
     uint32_t wv[D][6];
 #pragma unroll
     for (int i = 0; i < D; ++i)
-        if (c0 + i * nwarp < nchunk) enc_lane24(in + (c0 + i * nwarp) * 768 + lane * 24, wv[i]);
+        if (c0i + i * W < C) {
+            enc_lane24(pin, wv[i]);
+            pin += sin;
+        }
     if (threadIdx.x == 0) {  // static indices: the table stays in the constant bank, no stack copy
 #pragma unroll
         for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
@@ -63,16 +72,19 @@ enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const uint32_t lb = smem_u32(s_lut);
-    for (int64_t c = c0; c < nchunk; c += D * nwarp) {
+    for (int32_t c = c0i; c < C; c += D * W) {
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            const int64_t ci = c + i * nwarp;
-            if (ci < nchunk) {
+            const int32_t ci = c + i * W;
+            if (ci < C) {
                 uint32_t yv[6], o[8];
-                const int64_t cn = ci + D * nwarp;
-                if (cn < nchunk) enc_lane24(in + cn * 768 + lane * 24, yv);
+                if (ci + D * W < C) {
+                    enc_lane24(pin, yv);
+                    pin += sin;
+                }
                 enc_lane_compute(wv[i], o, lb);
-                st256(out + ci * 1024 + lane * 32, o);
+                st256(pout, o);
+                pout += sout;
 #pragma unroll
                 for (int j = 0; j < 6; ++j) wv[i][j] = yv[j];
             }
