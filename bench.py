@@ -535,6 +535,64 @@ def extra_configs(b64, synth, torch, dev, stream, flush, Ev):
                                 "decode_gbs": round(tot_out / (td * 1e-3) / 1e9, 1),
                                 "encode_ms": round(te, 3), "decode_ms": round(td, 3),
                                 "input_bytes": total, "base64_bytes": tot_out}
+    del x, enc, eoff, dout, doff
+    torch.cuda.empty_cache()
+    res["config5_16GiB_1gpu"] = config5_one_gpu(b64, synth, torch, dev, timeit)
+    return res
+
+
+def config5_one_gpu(b64, synth, torch, dev, timeit):
+    """configs[4] on ONE B200: the 16 GiB stream cut into the 8 shards an 8-GPU run would
+    own (paper_1910_05109_b200.dist rules), encoded / decoded as grouped launches; 1000
+    seeded non-alphabet bytes injected on the decode side; global first error checked."""
+    import numpy as np
+
+    import oracle
+    from paper_1910_05109_b200 import dist as b64dist
+
+    N, G = 1 << 34, 8
+    x = synth.device_data(N, seed=0)
+    m = b64.encoded_len(N)
+    text = torch.empty(m, dtype=torch.uint8, device=dev)
+    es = [b64dist.encode_shard(N, G, r) for r in range(G)]
+    xs = [x[sh.start: sh.stop] for sh in es]
+    ts = [text[sh.out_start: sh.out_start + b64.encoded_len(sh.stop - sh.start) if sh.is_final
+               else sh.out_start + 4 * ((sh.stop - sh.start) // 3)] for sh in es]
+    b64.encode_group(xs, outs=ts)
+    te = timeit(lambda: b64.encode_group(xs, outs=ts), reps=5)
+    pos, bad = synth.corruption(1000, m, oracle.STANDARD, seed=0)
+    text[torch.from_numpy(pos).to(dev)] = torch.from_numpy(bad).to(dev)
+    del x, xs
+    torch.cuda.empty_cache()
+    out = torch.empty(3 * (m // 4), dtype=torch.uint8, device=dev)
+    ds = [b64dist.decode_shard(m, G, r) for r in range(G)]
+    tparts = [text[sh.start: sh.stop] for sh in ds]
+    oparts = [out[sh.out_start: sh.out_start + 3 * ((sh.stop - sh.start) // 4)] for sh in ds]
+    cell = torch.empty(1, dtype=torch.int64, device=dev)
+    items = (b64._lib.DecodeItem * G)()
+    std = b64.standard()
+    for r, sh in enumerate(ds):
+        items[r] = b64._lib.DecodeItem(tparts[r].data_ptr(), tparts[r].numel(), oparts[r].data_ptr(),
+                                       ctypes.pointer(std), sh.start, int(sh.is_final), 0, cell.data_ptr())
+    eo = torch.empty(1, dtype=torch.int64, device=dev)
+
+    def dec():
+        cell.fill_(b64.ERR_NONE)
+        b64._lib.check(b64._lib.lib().b64_decode_group(items, G, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                       "b64_decode_group")
+        b64.decode_finalize(cell, eo)
+
+    dec()
+    assert int(eo.item()) == int(pos.min())
+    td = timeit(dec, reps=5)
+    res = {"encode_gbs": round(m / (te * 1e-3) / 1e9, 1), "decode_gbs": round(m / (td * 1e-3) / 1e9, 1),
+           "encode_ms": round(te, 3), "decode_ms": round(td, 3),
+           "encode_traffic_gbs": round((N + m) / (te * 1e-3) / 1e9, 1),
+           "decode_traffic_gbs": round((m + 3 * (m // 4)) / (td * 1e-3) / 1e9, 1),
+           "first_error": int(eo.item()), "expected_first_error": int(pos.min()), "injected": 1000,
+           "note": "8 dist shards of one stream on one GPU (grouped launches): the strong-scaling N=1 point"}
+    del text, out, tparts, oparts
+    torch.cuda.empty_cache()
     return res
 
 

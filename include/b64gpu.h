@@ -175,7 +175,9 @@ int b64_decode_finalize_n(const int64_t *d_err_min, int64_t count, int64_t *d_er
  * stream is cut into chunks that rotate through 3 device buffers: chunk j is
  * copied H2D on s_h2d, coded on s_comp, copied D2H on s_d2h, so both PCIe
  * directions and the kernels overlap.  Results are complete once all three
- * streams have been synchronised (they may be the same stream).
+ * streams have been synchronised (they may be the same stream).  A call's
+ * first copy waits for the work already queued on s_comp and s_d2h, so
+ * back-to-back calls may share one workspace and stream triple.
  * b64_host_workspace_bytes(c) = workspace for encode chunks of ~c input bytes
  * (decode with the same workspace uses chunks of ~4c/3 chars).
  * Encode writes b64_encoded_len(n) chars to h_out.  Decode writes up to 3*m/4

@@ -336,6 +336,15 @@ struct HostPipe {
             ok &= cudaEventCreateWithFlags(&d2h[i], cudaEventDisableTiming) == cudaSuccess;
         }
     }
+    // The workspace buffers may still be in use by work already queued on the
+    // three streams (a previous call): the first copy of this call waits for it.
+    cudaError_t order_after_previous(cudaStream_t sh, cudaStream_t sc, cudaStream_t sd) {
+        cudaError_t e = cudaEventRecord(comp[0], sc);
+        if (e == cudaSuccess) e = cudaEventRecord(d2h[0], sd);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sh, comp[0], 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sh, d2h[0], 0);
+        return e;
+    }
     ~HostPipe() {
         for (int i = 0; i < kHostBufs; ++i) {
             cudaEventDestroy(h2d[i]);
@@ -367,7 +376,7 @@ int b64_encode_host(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_al
     cudaStream_t sh = reinterpret_cast<cudaStream_t>(s_h2d), sc = reinterpret_cast<cudaStream_t>(s_comp),
                  sd = reinterpret_cast<cudaStream_t>(s_d2h);
     HostPipe pipe;
-    if (!pipe.ok) return B64_ECUDA;
+    if (!pipe.ok || pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
     const int64_t stride = C + C / 3 * 4 + 512;
     int64_t j = 0;
     for (int64_t off = 0; off < n; off += C, ++j) {
@@ -410,7 +419,7 @@ int b64_decode_host(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_al
     if (C <= 0) return B64_EINVAL;
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
     HostPipe pipe;
-    if (!pipe.ok) return B64_ECUDA;
+    if (!pipe.ok || pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
     if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), sc) != cudaSuccess) return B64_ECUDA;
     const int64_t stride = C + C / 4 * 3 + 512;
     int64_t j = 0;
