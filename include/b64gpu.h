@@ -20,9 +20,10 @@
  *    are written to device memory (err_off / status).
  *  - Input bytes are only read and output bytes only written inside the
  *    ranges stated per call, except that the generic (unaligned / batched)
- *    kernels may read the naturally aligned 4-byte words that contain input
- *    bytes (at most 3 bytes before the first / after the last input byte,
- *    never crossing into another 4-byte-aligned word).
+ *    kernels may read the naturally aligned 8-byte words that contain input
+ *    bytes (at most 7 bytes before the first / after the last input byte,
+ *    never crossing into another 8-byte-aligned word; CUDA allocations are
+ *    at least 256-byte granular, so such reads stay inside the allocation).
  *  - Inputs and outputs must not overlap.
  */
 #ifndef B64GPU_H
