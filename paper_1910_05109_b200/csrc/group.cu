@@ -77,46 +77,47 @@ __global__ void __launch_bounds__(kThreads) enc_group_kernel(const __grid_consta
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
     const int64_t nwarp = gthreads >> 5;
-    const int32_t C = int32_t(g.cstart[g.count]);
-    const int32_t c0 = int32_t(gtid >> 5);
-    const int32_t W = int32_t(nwarp);
-    GroupCursor<768, true> pre;    // input of the chunk being prefetched
-    GroupCursor<1024, false> cur;  // output of the chunk being encoded
+    const int32_t W = int32_t(nwarp), w = int32_t(gtid >> 5);
+    const int64_t sin = nwarp * 768, sout = nwarp * 1024;
 
     griddep_wait();
-    uint32_t wv[D][6];
-    if (c0 < C) {
-        pre.start(g, c0, lane * 24);
-        cur.start(g, c0, lane * 32);
-    }
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        const int32_t c = c0 + j * W;
-        if (c < C) {
-            if (j) pre.next(g, c, nwarp * 768, lane * 24);
-            enc_lane24(pre.p, wv[j]);
-        }
-    }
     if (threadIdx.x < g.count * 16) (&s_lut[0][0])[threadIdx.x] = (&g.lut[0][0])[threadIdx.x];
     __syncthreads();
     const uint32_t lb0 = smem_u32(&s_lut[0][0]);
 
-    for (int32_t cb = c0; cb < C; cb += D * W) {
+    // Stream by stream, the warp walks the chunks c == w (mod W) of the
+    // concatenated chunk space -- within a stream exactly enc_fast_kernel's
+    // loop (pointer increments, D chunks prefetched in registers).
+    for (int it = 0; it < g.count; ++it) {
+        const int32_t lo = int32_t(g.cstart[it]), hi = int32_t(g.cstart[it + 1]);
+        const int32_t first = lo + int32_t((int64_t(w) - lo % W + W) % W);
+        if (first >= hi) continue;
+        const int32_t nloc = (hi - first + W - 1) / W;  // chunks of this stream for this warp
+        const uint8_t* pin = g.in[it] + int64_t(first - lo) * 768 + lane * 24;
+        uint8_t* pout = g.out[it] + int64_t(first - lo) * 1024 + lane * 32;
+        const uint32_t lb = lb0 + 64 * it;
+        uint32_t wv[D][6];
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            const int32_t c = cb + j * W;
-            if (c < C) {
-                uint32_t yv[6], o[8];
-                const int32_t cn = c + D * W;
-                if (cn < C) {
-                    pre.next(g, cn, nwarp * 768, lane * 24);
-                    enc_lane24(pre.p, yv);
+        for (int i = 0; i < D; ++i)
+            if (i < nloc) {
+                enc_lane24(pin, wv[i]);
+                pin += sin;
+            }
+        for (int32_t k = 0; k < nloc; k += D) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+                if (k + i < nloc) {
+                    uint32_t yv[6], o[8];
+                    if (k + i + D < nloc) {
+                        enc_lane24(pin, yv);
+                        pin += sin;
+                    }
+                    enc_lane_compute(wv[i], o, lb);
+                    st256(pout, o);
+                    pout += sout;
+#pragma unroll
+                    for (int j = 0; j < 6; ++j) wv[i][j] = yv[j];
                 }
-                if (c != c0) cur.next(g, c, nwarp * 1024, lane * 32);
-                enc_lane_compute(wv[j], o, lb0 + 64 * cur.it);
-                st256(const_cast<uint8_t*>(cur.p), o);
-#pragma unroll
-                for (int k = 0; k < 6; ++k) wv[j][k] = yv[k];
             }
         }
     }

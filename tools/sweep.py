@@ -31,6 +31,7 @@ def main():
     p.add_argument("--sizes", default="1M,4M,16M,64M,256M,1G")
     p.add_argument("--reps", type=int, default=20)
     p.add_argument("--tag", default=os.environ.get("B64_TAG", ""))
+    p.add_argument("--group", type=int, default=0, help="also time k grouped streams of each size (one launch)")
     a = p.parse_args()
     dev = torch.device("cuda:0")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -62,6 +63,29 @@ def main():
             traffic = {"enc": n + t.numel(), "dec": t.numel() + n, "copy": 2 * t.numel()}[name]
             res[name] = {"us": round(ms * 1e3, 2), "b64_gbs": round(t.numel() / ms / 1e6, 1),
                          "traffic_gbs": round(traffic / ms / 1e6, 1)}
+        if a.group:
+            xs = [synth.device_data(n + (i % 3), seed=0) for i in range(a.group)]
+            ts = b64.encode_group(xs)
+            cells = torch.full((a.group,), b64.ERR_NONE, dtype=torch.int64, device=dev)
+            outs = [torch.empty(3 * (tt.numel() // 4), dtype=torch.uint8, device=dev) for tt in ts]
+            tot_n = sum(xx.numel() for xx in xs)
+            tot_m = sum(tt.numel() for tt in ts)
+            for name, fn in (("genc", lambda: b64.encode_group(xs, outs=ts)),
+                             ("gdec", lambda: b64.decode_group(ts, outs=outs, cells=cells))):
+                evs = []
+                for k in range(a.reps + 3):
+                    flush.fill_(k & 255)
+                    flush_r.sum()
+                    torch.cuda._sleep(200_000)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    fn()
+                    e1.record(stream)
+                    evs.append((e0, e1))
+                torch.cuda.synchronize()
+                ms = statistics.median([e0.elapsed_time(e1) for e0, e1 in evs[3:]])
+                res[name] = {"us": round(ms * 1e3, 2), "traffic_gbs": round((tot_n + tot_m) / ms / 1e6, 1)}
+            del xs, ts, outs
         print(json.dumps(res), flush=True)
         del x, t, o, d
         torch.cuda.empty_cache()
