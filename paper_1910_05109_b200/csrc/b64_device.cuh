@@ -103,62 +103,6 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
     return v;
 }
 
-// ----------------------------------------------------------------- TMA bulk copies + mbarriers
-// 1-D bulk copies (cp.async.bulk, SASS UBLKCP) move whole warp-chunks between
-// HBM and shared memory without occupying registers or LSU instructions; an
-// mbarrier per ring slot tracks the transaction bytes (complete_tx).
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" :: "r"(bar), "r"(parity) : "memory");
-}
-// global -> shared bulk copy completing on mbarrier `bar`; dst, src 16 B aligned, bytes % 16 == 0.
-__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
-                                            uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-        :: "r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(policy) : "memory");
-}
-// shared -> global bulk copy (bulk-group completion).
-__device__ __forceinline__ void tma_store_1d(void* dst, uint32_t src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" :: "l"(dst), "r"(src), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void tma_store_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void tma_store_wait() {
-    asm volatile("cp.async.bulk.wait_group %0;" :: "n"(N) : "memory");
-}
-// generic-proxy shared accesses -> async-proxy (TMA) accesses ordering
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
 // Encode one triple (x: byte3 = s1, byte2 = s2, byte1 = s3) with the 64-entry
 // alphabet at the 64-byte-aligned shared address lb: index | lb == lb + index.
 // The right shifts are done as high halves of multiplies (IMAD.HI, FMA pipe)
@@ -357,11 +301,9 @@ __device__ __forceinline__ int64_t first_string_ending_after(const Offsets& off,
 template <int D>
 __global__ void enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab,
                                 uint32_t pad);
-__global__ void enc_tma_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab,
-                               uint32_t pad);
 __global__ void enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab,
                                    uint32_t pad);
-template <int D, bool TS>
+template <int D>
 __global__ void dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
                                 int64_t* __restrict__ out_len);

@@ -24,7 +24,7 @@ const char kUrlChars[65] = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz
 struct DevInfo {
     int sms = 0;
     int occ_enc_group[4] = {0, 0, 0, 0}, occ_dec_group[4] = {0, 0, 0, 0};
-    int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_dec_ts[4] = {0, 0, 0, 0}, occ_enc_tma = 0, occ_enc_gen = 0, occ_dec_gen = 0;
+    int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_enc_gen = 0, occ_dec_gen = 0;
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -40,31 +40,21 @@ const DevInfo* dev_info() {
     if (cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) return nullptr;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[1], enc_fast_kernel<1>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[2], enc_fast_kernel<2>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[3], enc_fast_kernel<3>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[1], dec_fast_kernel<1, false>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[2], dec_fast_kernel<2, false>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[3], dec_fast_kernel<3, false>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_ts[1], dec_fast_kernel<1, true>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_ts[2], dec_fast_kernel<2, true>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_ts[3], dec_fast_kernel<3, true>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[1], dec_fast_kernel<1>, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[2], dec_fast_kernel<2>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_group[1], enc_group_kernel<1>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_group[2], enc_group_kernel<2>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_group[1], dec_group_kernel<1>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_group[2], dec_group_kernel<2>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_group[3], enc_group_kernel<3>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_group[3], dec_group_kernel<3>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_tma, enc_tma_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0))
         return nullptr;
     for (int i = 0; i < 4; ++i) {
         info.occ_enc_fast[i] = info.occ_enc_fast[i] < 1 ? 1 : info.occ_enc_fast[i];
         info.occ_dec_fast[i] = info.occ_dec_fast[i] < 1 ? 1 : info.occ_dec_fast[i];
-        info.occ_dec_ts[i] = info.occ_dec_ts[i] < 1 ? 1 : info.occ_dec_ts[i];
         info.occ_enc_group[i] = info.occ_enc_group[i] < 1 ? 1 : info.occ_enc_group[i];
         info.occ_dec_group[i] = info.occ_dec_group[i] < 1 ? 1 : info.occ_dec_group[i];
     }
-    info.occ_enc_tma = info.occ_enc_tma < 1 ? 1 : info.occ_enc_tma;
     info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
     info.occ_dec_gen = info.occ_dec_gen < 1 ? 1 : info.occ_dec_gen;
     g_dev[d] = info;
@@ -116,24 +106,14 @@ void launch(void (*kernel)(KArgs...), int64_t grid, int block, cudaStream_t s, A
     cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
-// Encode bulk variant: 0 = register-direct loads (default, measured faster on
-// B200: profiles/), 1 = TMA-fed ring (B64_ENC=tma).
-int enc_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("B64_ENC");
-        return (e && e[0] == 't') ? 1 : 0;
-    }();
-    return v;
-}
-
 // Prefetch depth of the register-direct bulk loops (chunks in flight per warp
-// beyond the one being translated): B64_ENC_DEPTH / B64_DEC_DEPTH in 1..3.
+// beyond the one being translated): B64_ENC_DEPTH / B64_DEC_DEPTH in 1..2.
 // Default: 2 for inputs of at least 256 MiB (tools/sweep.py on B200: 95-98 %
 // of the measured copy roofline at 1-4 GiB), 1 below (shorter kernels lose
 // more to the deeper prologue than they gain).
 int depth_env(const char* name) {
     const char* e = std::getenv(name);
-    if (e && e[0] >= '1' && e[0] <= '3') return e[0] - '0';
+    if (e && e[0] >= '1' && e[0] <= '2') return e[0] - '0';
     return 0;
 }
 int enc_depth(int64_t n) {
@@ -143,16 +123,6 @@ int enc_depth(int64_t n) {
 int dec_depth(int64_t m) {
     static const int d = depth_env("B64_DEC_DEPTH");
     return d ? d : (m >= (int64_t(256) << 20) ? 2 : 1);
-}
-
-// Decode output path: TMA bulk stores from the per-warp staging buffer
-// (B64_DEC_TS=1) or lane-linear STG.64 (default).
-bool dec_tma_store() {
-    static const bool v = [] {
-        const char* e = std::getenv("B64_DEC_TS");
-        return e && e[0] == '1';
-    }();
-    return v;
 }
 
 // Resident CTAs per SM used by the single-stream kernels: at most 5 (40 warps;
@@ -166,7 +136,7 @@ int cap_bps(int occ) {
 }
 
 template <typename K>
-K pick3(int d, K k1, K k2, K k3) { return d == 3 ? k3 : (d == 2 ? k2 : k1); }
+K pick2(int d, K k1, K k2) { return d == 2 ? k2 : k1; }
 
 // Blocks for a grid-stride loop over `units` warp-sized work units with at most
 // `max_blocks` resident blocks: the number of rounds is fixed by the resident
@@ -239,15 +209,11 @@ int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabe
     const DevInfo* di = dev_info();
     if (!di) return B64_ECUDA;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (enc_variant() == 1 && aligned(d_in, 16) && aligned(d_out, 32)) {
-        const int64_t ntile = n / (768 * (kThreads / 32));
-        const int64_t blocks = clamp_grid(ntile, int64_t(di->sms) * di->occ_enc_tma);
-        launch(enc_tma_kernel, blocks, kThreads, s, d_in, n, d_out, enc_tab(a), a->pad);
-    } else if (aligned(d_in, 8) && aligned(d_out, 32)) {
+    if (aligned(d_in, 8) && aligned(d_out, 32)) {
         const int64_t nchunk = n / 768;
         const int dd = enc_depth(n);
         const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(di->occ_enc_fast[dd]));
-        launch(pick3(dd, enc_fast_kernel<1>, enc_fast_kernel<2>, enc_fast_kernel<3>), blocks, kThreads, s, d_in, n,
+        launch(pick2(dd, enc_fast_kernel<1>, enc_fast_kernel<2>), blocks, kThreads, s, d_in, n,
                d_out, enc_tab(a), a->pad);
     } else {
         Offsets off{nullptr, nullptr, 1, n};
@@ -265,11 +231,8 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
     if (aligned(d_in, 32) && aligned(d_out, 16)) {
         const int64_t nchunk = (m / 4) / 256;
         const int dd = dec_depth(m);
-        const bool ts = dec_tma_store();
-        const int64_t blocks =
-            balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(ts ? di->occ_dec_ts[dd] : di->occ_dec_fast[dd]));
-        auto k = ts ? pick3(dd, dec_fast_kernel<1, true>, dec_fast_kernel<2, true>, dec_fast_kernel<3, true>)
-                    : pick3(dd, dec_fast_kernel<1, false>, dec_fast_kernel<2, false>, dec_fast_kernel<3, false>);
+        const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(di->occ_dec_fast[dd]));
+        auto k = pick2(dd, dec_fast_kernel<1>, dec_fast_kernel<2>);
         launch(k, blocks, kThreads, s, d_in, m, d_out, dec_tab(a), base, is_final, c, out_len);
     } else {
         Offsets off{nullptr, nullptr, 1, m};
@@ -460,7 +423,7 @@ int b64_encode_group(const b64_encode_item* items, int64_t count, b64_stream_t s
         if (g.count == 0) return B64_OK;
         const int d = enc_depth(bytes);
         const int64_t blocks = balanced_blocks(g.cstart[g.count], int64_t(di->sms) * di->occ_enc_group[d]);
-        launch(pick3(d, enc_group_kernel<1>, enc_group_kernel<2>, enc_group_kernel<3>), blocks, kThreads, s, g);
+        launch(pick2(d, enc_group_kernel<1>, enc_group_kernel<2>), blocks, kThreads, s, g);
         const int r = launched();
         std::memset(&g, 0, sizeof(g));
         bytes = 0;
@@ -518,7 +481,7 @@ int b64_decode_group(const b64_decode_item* items, int64_t count, b64_stream_t s
         if (g.count == 0) return B64_OK;
         const int d = dec_depth(bytes);
         const int64_t blocks = balanced_blocks(g.cstart[g.count], int64_t(di->sms) * di->occ_dec_group[d]);
-        launch(pick3(d, dec_group_kernel<1>, dec_group_kernel<2>, dec_group_kernel<3>), blocks, kThreads, s, g);
+        launch(pick2(d, dec_group_kernel<1>, dec_group_kernel<2>), blocks, kThreads, s, g);
         const int r = launched();
         std::memset(&g, 0, sizeof(g));
         bytes = 0;

@@ -1,11 +1,11 @@
 // decode.cu -- sm_100a validating base64 decode kernels (Sec. 2, 3.2).
 //
-// dec_fast_kernel: one stream (or one shard of it), d_in 32-byte and d_out
-//   8-byte aligned.  Warp-chunk = 1024 chars (256 quads) -> 768 bytes.  Lane l
-//   owns chars [32l, 32l+32): ONE lane-linear LDG.256 (sector-perfect, fully
-//   coalesced) and three STG.64 at a lane stride of 24 B that together cover
-//   768 contiguous bytes (merged in L2 before write-back).  Every lane ORs its
-//   translated values into one register (the paper's error register,
+// dec_fast_kernel<D>: one stream (or one shard of it), d_in 32-byte and d_out
+//   16-byte aligned.  Warp-chunk = 1024 chars (256 quads) -> 768 bytes.  Lane l
+//   owns chars [32l, 32l+32): ONE lane-linear LDG.256 (whole sectors, fully
+//   coalesced); its 24 output bytes go through a per-warp shared buffer so the
+//   global stores are three lane-linear STG.64 of whole sectors.  Every lane
+//   ORs its translated values into one register (the paper's error register,
 //   PAPER.md:305-313); the warp votes once per chunk and only on a set 0x80
 //   bit locates the first bad char (__reduce_min_sync + one 64-bit atomicMin
 //   of the packed word pos<<3|kind).  Interior quads left over after the
@@ -13,9 +13,9 @@
 //   is done by the grid's last thread -- "a final and separate code path"
 //   (PAPER.md:569).
 // dec_generic_kernel: any alignment, one stream or a batch of strings.
-//   Same byte-range-per-warp split as enc_generic_kernel with 16-char units
-//   -> 12 bytes.  Per string, the first (out_addr & 3) quads are done one by
-//   one so every unit's 12-byte output is 4-byte aligned (3 STG.32).
+//   Same byte-range-per-warp split as enc_generic_kernel with 32-char units
+//   -> 24 bytes; per string, h < 8 head quads make every unit's output 8-byte
+//   aligned (3 STG.64).
 // dec_finalize_*: map the packed error word to (err_off, status, out_len).
 #include "b64_device.cuh"
 
@@ -37,13 +37,13 @@ __device__ __forceinline__ uint32_t scan_first_bad(const uint8_t* p, int nquads,
     return 0xffffffffu;
 }
 
-template <int D, bool TS>
+template <int D>
 __global__ void __launch_bounds__(kThreads)
 dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
                 int64_t* __restrict__ out_len) {
     __shared__ __align__(256) uint32_t s_lut[64];
-    __shared__ __align__(128) uint32_t s_stage[kThreads / 32][(TS ? 2 : 1) * 768 / 4];  // per-warp output staging
+    __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];  // per-warp output staging
     griddep_launch_dependents();
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -69,7 +69,6 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     const uint8_t* pin = in + c0 * 1024 + lane * 32;  // next chunk to load
     const uint8_t* pcur = in + c0 * 1024 + lane * 32; // chunk being decoded (rare error rescan)
     uint8_t* pout = out + c0 * 768;                   // its output
-    uint32_t kk = 0;  // chunks done by this warp (TMA-store buffer parity)
     uint32_t xr[D][8];
 #pragma unroll
     for (int i = 0; i < D; ++i)
@@ -97,34 +96,17 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
                 uint32_t o[6];
                 dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
                 dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
-                if constexpr (TS) {
-                    // double-buffered staging drained by a 768 B TMA bulk store
-                    const uint32_t sbuf = sb + (kk & 1) * 768;
-                    if (lane == 0) tma_store_wait_read<1>();  // the store from this buffer 2 chunks ago read it
-                    __syncwarp();
-                    sts64(sbuf + lane * 24, o[0], o[1]);
-                    sts64(sbuf + lane * 24 + 8, o[2], o[3]);
-                    sts64(sbuf + lane * 24 + 16, o[4], o[5]);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tma_store_1d(pout, sbuf, 768);
-                        tma_store_commit();
-                    }
-                    ++kk;
-                } else {
-                    sts64(sb + lane * 24, o[0], o[1]);
-                    sts64(sb + lane * 24 + 8, o[2], o[3]);
-                    sts64(sb + lane * 24 + 16, o[4], o[5]);
-                    __syncwarp();
-                    uint8_t* dst = pout + lane * 8;
-                    const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8),
-                                s2 = lds64(sb + 512 + lane * 8);
-                    st64(dst, s0.x, s0.y);
-                    st64(dst + 256, s1.x, s1.y);
-                    st64(dst + 512, s2.x, s2.y);
-                    __syncwarp();
-                }
+                sts64(sb + lane * 24, o[0], o[1]);
+                sts64(sb + lane * 24 + 8, o[2], o[3]);
+                sts64(sb + lane * 24 + 16, o[4], o[5]);
+                __syncwarp();
+                uint8_t* dst = pout + lane * 8;
+                const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8),
+                            s2 = lds64(sb + 512 + lane * 8);
+                st64(dst, s0.x, s0.y);
+                st64(dst + 256, s1.x, s1.y);
+                st64(dst + 512, s2.x, s2.y);
+                __syncwarp();
                 const bool bad = (err & kInvalid) != 0;
                 if (__any_sync(kFull, bad)) {  // rare: locate the first invalid char of the chunk
                     uint32_t rel = 0xffffffffu;
@@ -140,10 +122,6 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
                 for (int j = 0; j < 8; ++j) xr[i][j] = y[j];
             }
         }
-    }
-
-    if constexpr (TS) {
-        if (lane == 0) tma_store_wait<0>();  // bulk stores complete before the CTA (and its smem) retires
     }
 
     // leftover interior quads, one per thread

@@ -1,18 +1,18 @@
 // encode.cu -- sm_100a base64 encode kernels (Sec. 2 / Sec. 3.1).
 //
-// enc_fast_kernel: one stream, d_in 8-byte and d_out 32-byte aligned.
+// enc_fast_kernel<D>: one stream, d_in 8-byte and d_out 32-byte aligned.
 //   Warp-chunk = 768 input bytes (256 triples) -> 1024 chars.  Lane l owns
 //   bytes [24l, 24l+24) = 8 triples -> 32 chars: three LDG.64 at a lane stride
-//   of 24 B (together one contiguous 768 B range, L1-merged) and ONE lane-linear
-//   STG.256 (32 lanes x 32 B = 1 KiB, fully coalesced, sector-perfect).
-//   Two chunks per warp per iteration keep >= 1.5 KiB of reads in flight per
-//   warp (Little's law).  The <768 B remainder (full
-//   triples + the 1-2 byte padded tail) is done by the
-//   first threads of the grid, one output quad each.
+//   of 24 B (together one contiguous 768 B range: the first brings every
+//   sector into L1, the other two hit) and ONE lane-linear STG.256 (32 lanes x
+//   32 B = 1 KiB, whole sectors).  Grid-stride over chunks with D chunks per
+//   warp prefetched in registers (Little's law).  The
+//   < 768 B remainder (full triples + the 1-2 byte padded tail, PAPER.md:84-87,
+//   251) is done by the first threads of the grid, one output quad each.
 // enc_generic_kernel: any alignment, one stream or a batch of strings
 //   (BASELINE.json configs[3]).  The concatenated input is split into equal
-//   byte ranges, one per warp; a warp encodes every 12-byte unit (4 triples ->
-//   16 chars) whose first byte lies in its range, so long strings spread over
+//   byte ranges, one per warp; a warp encodes every 24-byte unit (8 triples ->
+//   32 chars) whose first byte lies in its range, so long strings spread over
 //   many warps and short strings pack many per warp.
 #include "b64_device.cuh"
 
@@ -105,111 +105,6 @@ enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__
             word = enc_partial(s[0], r == 2 ? s[1] : 0u, r, lut, pad);
         }
         *reinterpret_cast<uint32_t*>(out + 4 * q) = word;  // out 32-aligned => 4-aligned
-    }
-}
-
-// enc_tma_kernel: the input streams through a per-CTA ring of kEncStages
-// shared-memory tiles (one 768 B warp-chunk per warp: 6 KiB per tile) filled
-// by 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) that complete on a "full"
-// mbarrier; warps release a tile on an "empty" mbarrier (8 arrivals) and thread
-// 0 refills it kEncStages tiles ahead.  Loads then hold no registers and use no
-// LSU instructions; lanes read their 24 bytes with three conflict-free LDS.64
-// (24 B stride: 16 lanes per phase hit 32 distinct banks).  Tiles are taken
-// grid-stride so the grid sweeps one window of memory.  Outputs: lane-linear
-// STG.256 as in enc_fast_kernel.  Requires d_in 16-byte aligned.
-constexpr int kEncStages = 4;
-constexpr int kEncTile = (kThreads / 32) * 768;
-
-__global__ void __launch_bounds__(kThreads)
-enc_tma_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab, uint32_t pad) {
-    __shared__ __align__(64) uint32_t s_lut[16];
-    __shared__ __align__(128) uint8_t s_ring[kEncStages][kEncTile];
-    __shared__ __align__(8) unsigned long long s_full[kEncStages], s_empty[kEncStages];
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
-#pragma unroll
-        for (int st = 0; st < kEncStages; ++st) {
-            mbar_init(smem_u32(&s_full[st]), 1);
-            mbar_init(smem_u32(&s_empty[st]), kThreads / 32);
-        }
-        mbar_fence_init();
-    }
-    __syncthreads();
-    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
-    const uint32_t lb = smem_u32(s_lut);
-    const uint32_t ring = smem_u32(&s_ring[0][0]);
-    const uint32_t full = smem_u32(&s_full[0]);
-    const uint32_t empty = smem_u32(&s_empty[0]);
-    griddep_launch_dependents();
-
-    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
-    const int64_t nwarp = gthreads >> 5;
-    const int64_t nchunk = n / 768;
-    const int64_t ntile = nchunk / (kThreads / 32);
-    const int64_t G = gridDim.x;
-    const uint64_t pol = policy_evict_first();
-
-    griddep_wait();
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int st = 0; st < kEncStages; ++st) {
-            const int64_t t = blockIdx.x + st * G;
-            if (t < ntile) {
-                mbar_expect_tx(full + 8 * st, kEncTile);
-                tma_load_1d(ring + kEncTile * st, in + t * kEncTile, kEncTile, full + 8 * st, pol);
-            }
-        }
-    }
-    uint32_t k = 0;
-    for (int64_t t = blockIdx.x; t < ntile; t += G, ++k) {
-        const uint32_t slot = k % kEncStages;
-        const uint32_t ph = (k / kEncStages) & 1;
-        mbar_wait(full + 8 * slot, ph);
-        const uint32_t src = ring + kEncTile * slot + wib * 768 + lane * 24;
-        const uint2 a = lds64(src), b = lds64(src + 8), d = lds64(src + 16);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + 8 * slot);
-        if (threadIdx.x == 0) {
-            const int64_t tn = t + kEncStages * G;
-            if (tn < ntile) {
-                mbar_wait(empty + 8 * slot, ph);
-                fence_proxy_async_smem();
-                mbar_expect_tx(full + 8 * slot, kEncTile);
-                tma_load_1d(ring + kEncTile * slot, in + tn * kEncTile, kEncTile, full + 8 * slot, pol);
-            }
-        }
-        const uint32_t wv[6] = {a.x, a.y, b.x, b.y, d.x, d.y};
-        uint32_t o[8];
-        enc_lane_compute(wv, o, lb);
-        st256(out + (t * (kThreads / 32) + wib) * 1024 + lane * 32, o);
-    }
-
-    // chunks after the last full tile: register path, grid-stride by warp
-    for (int64_t c = ntile * (kThreads / 32) + (gtid >> 5); c < nchunk; c += nwarp) {
-        uint32_t wv[6], o[8];
-        enc_lane24(in + c * 768 + lane * 24, wv);
-        enc_lane_compute(wv, o, lb);
-        st256(out + c * 1024 + lane * 32, o);
-    }
-
-    // remainder: output quads [256*nchunk, ceil(n/3)), one per thread
-    const int64_t T = n / 3;
-    const int64_t Q = (n + 2) / 3;
-    for (int64_t q = nchunk * 256 + gtid; q < Q; q += gthreads) {
-        const uint8_t* s = in + 3 * q;
-        uint32_t word;
-        if (q < T) {
-            const uint32_t x = (uint32_t(s[0]) << 24) | (uint32_t(s[1]) << 16) | (uint32_t(s[2]) << 8);
-            word = enc_triple(x, lut);
-        } else {
-            const int r = int(n - 3 * q);
-            word = enc_partial(s[0], r == 2 ? s[1] : 0u, r, lut, pad);
-        }
-        *reinterpret_cast<uint32_t*>(out + 4 * q) = word;
     }
 }
 
