@@ -23,7 +23,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
-    "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline",
+    "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline", "new_info",
     "encode_group", "decode_group",
     "ERR_NONE",
 ]
@@ -88,15 +88,21 @@ def encode(x: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Te
            stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """Encode bytes to base64 chars with '=' padding (b64_encode)."""
     _check_u8(x, "x")
-    m = encoded_len(x.numel())
+    n = x.numel()
+    m = 4 * ((n + 2) // 3)  # b64_encoded_len (PAPER.md:84-87)
     if out is None:
         out = torch.empty(m, dtype=torch.uint8, device=x.device)
     else:
         _check_u8(out, "out")
         if out.numel() < m:
             raise B64Error("out too small")
-    _lib.check(_lib.lib().b64_encode(_ptr(x), x.numel(), _ptr(out), _alpha(a), _stream(stream)), "b64_encode")
-    return out[:m]
+    _lib.check(_lib.lib().b64_encode(_ptr(x), n, _ptr(out), _alpha(a), _stream(stream)), "b64_encode")
+    return out if out.numel() == m else out[:m]
+
+
+def new_info(device=None) -> torch.Tensor:
+    """A zeroed device int64[3] for decode_async: (err_off, status, out_len)."""
+    return torch.zeros(3, dtype=torch.int64, device=device if device is not None else "cuda")
 
 
 def decode_async(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
@@ -104,20 +110,21 @@ def decode_async(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[to
                  stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, torch.Tensor]:
     """Validating decode (b64_decode_ex) without a host sync.
 
-    Returns (out, info) where info is a device int64[3]: (err_off, status, out_len)."""
+    Returns (out, info) where info is a device int64[3]: (err_off, status, out_len).
+    A caller-provided info must come from new_info() (the status is written as an
+    int32 into the low half of info[1]; the high half must stay zero)."""
     _check_u8(t, "t")
     m = t.numel()
     if m % 4:
         raise B64Error("B64_ELENGTH: text length is not a multiple of 4")
-    cap = decoded_len_max(m)
     if out is None:
-        out = torch.empty(max(cap, 1), dtype=torch.uint8, device=t.device)
+        out = torch.empty(max(decoded_len_max(m), 1), dtype=torch.uint8, device=t.device)
     if info is None:
-        info = torch.empty(3, dtype=torch.int64, device=t.device)
-    st = info[1:2].view(torch.int32)[:1]  # status stored in the low half of info[1]
-    info[1].zero_()
-    _lib.check(_lib.lib().b64_decode_ex(_ptr(t), m, _ptr(out), _alpha(a), _ptr(info[0:1]), _ptr(st),
-                                        _ptr(info[2:3]), _stream(stream)), "b64_decode_ex")
+        info = new_info(t.device)
+    ip = info.data_ptr()
+    _lib.check(_lib.lib().b64_decode_ex(_ptr(t), m, _ptr(out), _alpha(a), ctypes.c_void_p(ip),
+                                        ctypes.c_void_p(ip + 8), ctypes.c_void_p(ip + 16), _stream(stream)),
+               "b64_decode_ex")
     return out, info
 
 

@@ -310,6 +310,9 @@ __global__ void dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8
 __global__ void dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off,
                                    DecTab tab, int64_t base, int is_final_single,
                                    unsigned long long* __restrict__ err_cells, int64_t* __restrict__ out_len_single);
+__global__ void dec_small_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
+                                 int64_t* __restrict__ err_off, int32_t* __restrict__ status,
+                                 int64_t* __restrict__ out_len);
 __global__ void dec_finalize_single_kernel(int64_t* err_off, int32_t* status, int64_t* out_len,
                                            const uint8_t* __restrict__ in, int64_t m, uint32_t pad);
 __global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off, int32_t* status);

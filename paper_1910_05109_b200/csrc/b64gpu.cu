@@ -3,4 +3,5 @@
 #include "encode.cu"
 #include "decode.cu"
 #include "group.cu"
+#include "small.cu"
 #include "capi.cu"

@@ -57,6 +57,8 @@ const DevInfo* dev_info() {
     }
     info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
     info.occ_dec_gen = info.occ_dec_gen < 1 ? 1 : info.occ_dec_gen;
+    if (cudaFuncSetAttribute(dec_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        return nullptr;
     g_dev[d] = info;
     g_dev_ready[d] = true;
     return &g_dev[d];
@@ -123,6 +125,16 @@ int enc_depth(int64_t n) {
 int dec_depth(int64_t m) {
     static const int d = depth_env("B64_DEC_DEPTH");
     return d ? d : (m >= (int64_t(256) << 20) ? 2 : 1);
+}
+
+// Largest input (chars) for the single-launch cluster decode (small.cu);
+// B64_SMALL_MAX overrides (0 disables the path).
+int64_t small_max() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("B64_SMALL_MAX");
+        return e ? int64_t(std::atoll(e)) : kSmallMax;
+    }();
+    return v;
 }
 
 // Resident CTAs per SM used by the single-stream kernels: at most 5 (40 warps;
@@ -248,8 +260,30 @@ int b64_decode_ex(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
     if (m % 4) return B64_ELENGTH;
     if (m > 0 && (!d_in || !d_out)) return B64_EINVAL;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (m <= small_max() && (m == 0 || (aligned(d_in, 32) && aligned(d_out, 16)))) {
+        // small input: one cluster launch does init, decode and finalize (small.cu)
+        if (!dev_info()) return B64_ECUDA;
+        const int64_t nchunk = (m / 4) / 256;
+        int64_t r = (nchunk + kSmallThreads / 32 - 1) / (kSmallThreads / 32);
+        r = r < 1 ? 1 : (r > kSmallCluster ? kSmallCluster : r);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(r));
+        cfg.blockDim = dim3(kSmallThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = unsigned(r);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        cudaLaunchKernelEx(&cfg, dec_small_kernel, d_in, m, d_out, dec_tab(a), d_err_off, d_status, d_out_len);
+        return launched();
+    }
     if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), s) != cudaSuccess) return B64_ECUDA;
-    if (m > 0) {
+    {
         const int r = decode_launch(d_in, m, d_out, a, 0, 1, d_err_off, nullptr, s);
         if (r != B64_OK) return r;
     }

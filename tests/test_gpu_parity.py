@@ -562,3 +562,42 @@ def test_group_decode_as_shards(b64):
         assert int(eo.item()) == rerr
         got = torch.cat(outs).cpu().numpy()
         assert np.array_equal(got[: ref.size], ref)
+
+
+def test_decode_fast_path_small_sizes(b64):
+    """b64_decode_ex takes the single-launch cluster kernel up to 512 KiB; the multi-CTA
+    bulk kernel (b64_decode_chunk + finalize) must agree with the oracle on the same sizes."""
+    std = b64.standard()
+    for n in (0, 1, 2, 3, 767, 768, 3 * 1024 + 2, 100_001, 768 * 300 + 1, 3_000_000, 3_200_000):
+        x = synth.data(n, seed=n + 5)
+        text = oracle.encode(x)
+        for trial in range(3):
+            t2 = text.copy()
+            if trial and t2.size:
+                pos, bad = synth.corruption(trial, t2.size, oracle.STANDARD, seed=n + trial)
+                t2[pos] = bad
+            ref, rerr, rst = oracle.decode(t2)
+            dt = to_dev(t2)
+            cell = torch.full((1,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+            out = b64.decode_chunk(dt, 0, True, cell, std)
+            eo = torch.empty(1, dtype=torch.int64, device=DEV)
+            st = torch.zeros(1, dtype=torch.int32, device=DEV)
+            b64.decode_finalize(cell, eo, st)
+            assert (int(eo.item()), int(st.item())) == (rerr, rst), (n, trial)
+            assert np.array_equal(out[: ref.size].cpu().numpy(), ref)
+            assert dec_check(b64, t2, oracle.STANDARD, oracle.PAD, std) == rerr  # small cluster path
+
+
+def test_decode_ex_small_path_many_ctas(b64):
+    """Around the cluster-size and kSmallMax boundaries (16 CTAs x 16 warps x 1024 chars)."""
+    std = b64.standard()
+    for m_chars in (16 * 1024 - 4, 16 * 1024, 256 * 1024, 256 * 1024 + 4096, (512 << 10) - 4, 512 << 10,
+                    (512 << 10) + 4, 4 << 20):
+        n = m_chars // 4 * 3 - 1
+        x = synth.data(n, seed=m_chars)
+        text = oracle.encode(x)
+        dec_check(b64, text, oracle.STANDARD, oracle.PAD, std)
+        for p in (0, text.size // 2, text.size - 3, text.size - 1):
+            t2 = text.copy()
+            t2[p] = ord("#")
+            dec_check(b64, t2, oracle.STANDARD, oracle.PAD, std)
