@@ -63,6 +63,8 @@ def lib():
         L.oracle_encode.restype = I64
         L.oracle_decode.argtypes = [P, I64, P, P, U8, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.oracle_decode.restype = ctypes.c_int
+        L.oracle_decode_unpadded.argtypes = [P, I64, P, P, U8, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.oracle_decode_unpadded.restype = ctypes.c_int
         L.oracle_encode_batch.argtypes = [P, P, I64, P, P, P, U8]
         L.oracle_encode_batch.restype = None
         L.oracle_decode_batch.argtypes = [P, P, I64, P, P, P, U8, P, P, P]
@@ -117,6 +119,24 @@ def decode(text, chars: bytes = STANDARD, pad: int = PAD):
     st = lib().oracle_decode(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
                              ctypes.byref(ol), ctypes.byref(eo))
     return out[: ol.value], eo.value, st
+
+
+def decode_unpadded(text, chars: bytes = STANDARD, pad: int = PAD):
+    """Padding-optional decode (reading R13).  Returns (exact prefix bytes, err_off, status)."""
+    t = _u8(text)
+    out = np.empty(3 * (t.size // 4) + 3, dtype=np.uint8)
+    ol = ctypes.c_int64(0)
+    eo = ctypes.c_int64(0)
+    st = lib().oracle_decode_unpadded(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
+                                      ctypes.byref(ol), ctypes.byref(eo))
+    return out[: ol.value], eo.value, st
+
+
+def encode_unpadded(data, chars: bytes = STANDARD, pad: int = PAD) -> np.ndarray:
+    """encode() with the trailing '=' dropped (the length law without padding)."""
+    t = encode(data, chars, pad)
+    n = _u8(data).size
+    return t[: t.size - (3 - n % 3) % 3]
 
 
 def encode_batch(data, in_off, chars: bytes = STANDARD, pad: int = PAD):

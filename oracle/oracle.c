@@ -184,6 +184,68 @@ int oracle_decode(const uint8_t *in, int64_t m, uint8_t *out,
     return ORACLE_ST_OK;
 }
 
+/* Padding-optional decode (reading R13):
+ * the encoded length law of PAPER.md:84-87 without the '=' ("may be
+ * appended").  m % 4 == 0: exactly oracle_decode.  m % 4 == 1: LENGTH at
+ * m - 1.  m % 4 in {2, 3}: every full quad is interior (all chars in the
+ * alphabet), then the last 2 or 3 chars must be alphabet chars and decode to
+ * 1 or 2 bytes by the same formulas (missing values taken as zero), with the
+ * dropped low bits zero (canonical; NONCANON at m - 1). */
+int oracle_decode_unpadded(const uint8_t *in, int64_t m, uint8_t *out,
+                           const uint8_t chars[64], uint8_t pad,
+                           int64_t *out_len, int64_t *err_off)
+{
+    uint8_t dec[256];
+    int64_t q, nq, r, p;
+    if (m % 4 == 0) return oracle_decode(in, m, out, chars, pad, out_len, err_off);
+    build_decode_table(chars, dec);
+    *out_len = 0;
+    *err_off = -1;
+    r = m % 4;
+    if (r == 1) {
+        *err_off = m - 1;
+        return ORACLE_ST_LENGTH;
+    }
+    nq = m / 4;
+    for (q = 0; q < nq; q++) {
+        const uint8_t *c = in + 4 * q;
+        int j;
+        for (j = 0; j < 4; j++) {
+            if (dec[c[j]] == ORACLE_INVALID) {
+                *err_off = 4 * q + j;
+                *out_len = 3 * q;
+                return ORACLE_ST_BADCHAR;
+            }
+        }
+        {
+            unsigned a = dec[c[0]], b = dec[c[1]], cc = dec[c[2]], d = dec[c[3]];
+            out[3 * q] = (uint8_t)((a * 4) + (b / 16));
+            out[3 * q + 1] = (uint8_t)((b * 16) % 256 + (cc / 4));
+            out[3 * q + 2] = (uint8_t)((cc * 64) % 256 + d);
+        }
+    }
+    p = 4 * nq;
+    for (q = 0; q < r; q++) {
+        if (dec[in[p + q]] == ORACLE_INVALID) {
+            *err_off = p + q;
+            *out_len = 3 * nq;
+            return ORACLE_ST_BADCHAR;
+        }
+    }
+    {
+        unsigned a = dec[in[p]], b = dec[in[p + 1]], cc = (r == 3) ? dec[in[p + 2]] : 0;
+        if ((r == 2 && (b % 16) != 0) || (r == 3 && (cc % 4) != 0)) {
+            *err_off = m - 1;
+            *out_len = 3 * nq;
+            return ORACLE_ST_NONCANON;
+        }
+        out[3 * nq] = (uint8_t)((a * 4) + (b / 16));
+        if (r == 3) out[3 * nq + 1] = (uint8_t)((b * 16) % 256 + (cc / 4));
+        *out_len = 3 * nq + (r - 1);
+    }
+    return ORACLE_ST_OK;
+}
+
 /* Batched forms: the single-stream definitions applied string by string over
  * concatenated buffers with int64 offsets[count + 1] (BASELINE.json
  * configs[3]).  Encode output string i starts at out_off[i]. */

@@ -327,3 +327,47 @@ def test_batch_vs_stdlib(orc):
     assert (st == 0).all() and (err == -1).all() and (olen == L).all()
     for i in range(0, L.size, 7):
         assert out[ooff[i]: ooff[i] + olen[i]].tobytes() == x[off[i]: off[i + 1]].tobytes()
+
+
+# --------------------------------------------------------------------------- padding-optional decode (R13)
+
+def test_unpadded_decode_vs_stdlib(orc):
+    """Unpadded text == stdlib decode of the text with its '=' restored; padded text as strict."""
+    for n in range(0, 600):
+        x = synth.data(n, seed=n + 77)
+        for chars, enc in ((orc.STANDARD, base64.b64encode), (orc.URL, base64.urlsafe_b64encode)):
+            full = enc(x.tobytes())
+            bare = full.rstrip(b"=")
+            out, err, st = orc.decode_unpadded(np.frombuffer(bare, np.uint8), chars)
+            assert err == -1 and st == 0 and out.tobytes() == x.tobytes(), n
+            out, err, st = orc.decode_unpadded(np.frombuffer(full, np.uint8), chars)
+            assert err == -1 and out.tobytes() == x.tobytes(), n
+            assert orc.encode_unpadded(x, chars).tobytes() == bare
+
+
+def test_unpadded_partial_groups_exhaustive(orc):
+    """Every 2- and 3-char final group: accepted <=> re-encoding without '=' reproduces it
+    (canonical), i.e. 256 of 4096 and 65536 of 262144 (as for 'xx==' / 'xxx=')."""
+    a = STD
+    for r, total, want in ((2, 64 ** 2, 256), (3, 64 ** 3, 65536)):
+        i = np.arange(total)
+        grp = np.stack([np.frombuffer(a, np.uint8)[(i // 64 ** (r - 1 - k)) % 64] for k in range(r)], axis=1)
+        acc = 0
+        for g in grp:
+            t = np.concatenate([np.frombuffer(b"QUJD", np.uint8), g])
+            out, err, st = orc.decode_unpadded(t)
+            canon = base64.b64encode(base64.b64decode(t.tobytes() + b"=" * (4 - r))).rstrip(b"=") == t.tobytes()
+            assert (err == -1) == canon
+            if err != -1:
+                assert err == t.size - 1 and st == orc.ST_NONCANON
+            acc += err == -1
+        assert acc == want
+
+
+def test_unpadded_errors(orc):
+    assert orc.decode_unpadded(b"QUJDR")[1:] == (4, orc.ST_LENGTH)
+    assert orc.decode_unpadded(b"QU=")[1:] == (2, orc.ST_BADCHAR)      # '=' only completes a quad
+    assert orc.decode_unpadded(b"Q*JD")[1:] == (1, orc.ST_BADCHAR)
+    assert orc.decode_unpadded(b"QUJDQ!")[1:] == (5, orc.ST_BADCHAR)
+    assert orc.decode_unpadded(b"Zh")[1:] == (1, orc.ST_NONCANON)
+    assert orc.decode_unpadded(b"Zg")[0].tobytes() == b"f"
