@@ -122,6 +122,15 @@ int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alph
                   int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len,
                   b64_stream_t stream);
 
+/* Padding-optional decode (R13; e.g. base64url without '='):
+ * m % 4 == 0 behaves exactly as b64_decode_ex; m % 4 == 1 returns B64_ELENGTH
+ * synchronously; m % 4 in {2, 3}: all full quads must be alphabet chars and
+ * the trailing 2 / 3 chars decode to 1 / 2 bytes with zero dropped bits
+ * (B64_ST_NONCANON at m - 1 otherwise).  Outputs as b64_decode_ex; d_out
+ * capacity >= 3*(m/4) + 2. */
+int b64_decode_unpadded(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a,
+                        int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len, b64_stream_t stream);
+
 /* Shard-aware decode used by the multi-GPU driver.
  * Decodes chars [base_offset, base_offset + m) of a larger stream, m % 4 == 0.
  * Only when is_final_chunk != 0 is the last quad treated as the stream's

@@ -23,7 +23,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
-    "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline", "new_info",
+    "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline", "new_info", "decode_unpadded",
     "encode_group", "decode_group",
     "ERR_NONE",
 ]
@@ -133,6 +133,25 @@ def decode(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Te
     """Validating decode.  Returns (decoded bytes, err_off); err_off = -1 when valid.
     Forces one 24-byte device->host read of (err_off, status, out_len)."""
     out, info = decode_async(t, a, out=out, stream=stream)
+    err, _, olen = info.tolist()
+    return out[:olen], err
+
+
+def decode_unpadded(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
+                    stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, int]:
+    """Padding-optional validating decode (b64_decode_unpadded, R13).
+    Returns (decoded bytes, err_off); err_off = -1 when valid."""
+    _check_u8(t, "t")
+    m = t.numel()
+    if m % 4 == 1:
+        raise B64Error("B64_ELENGTH: text length is 1 more than a multiple of 4")
+    if out is None:
+        out = torch.empty(3 * (m // 4) + 3, dtype=torch.uint8, device=t.device)
+    info = new_info(t.device)
+    ip = info.data_ptr()
+    _lib.check(_lib.lib().b64_decode_unpadded(_ptr(t), m, _ptr(out), _alpha(a), ctypes.c_void_p(ip),
+                                              ctypes.c_void_p(ip + 8), ctypes.c_void_p(ip + 16), _stream(stream)),
+               "b64_decode_unpadded")
     err, _, olen = info.tolist()
     return out[:olen], err
 

@@ -62,6 +62,7 @@ SIGNATURES = [
     ("b64_encode", INT, [P, I64, P, AP, P]),
     ("b64_decode", INT, [P, I64, P, AP, P, P]),
     ("b64_decode_ex", INT, [P, I64, P, AP, P, P, P, P]),
+    ("b64_decode_unpadded", INT, [P, I64, P, AP, P, P, P, P]),
     ("b64_decode_chunk", INT, [P, I64, P, AP, I64, INT, P, P, P]),
     ("b64_decode_finalize", INT, [P, P, P, P]),
     ("b64_encode_group", INT, [P, I64, P]),

@@ -315,6 +315,9 @@ __global__ void dec_small_kernel(const uint8_t* __restrict__ in, int64_t m, uint
                                  int64_t* __restrict__ out_len);
 __global__ void dec_finalize_single_kernel(int64_t* err_off, int32_t* status, int64_t* out_len,
                                            const uint8_t* __restrict__ in, int64_t m, uint32_t pad);
+__global__ void dec_finalize_unpadded_kernel(int64_t* err_off, int32_t* status, int64_t* out_len,
+                                             const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out,
+                                             DecTab tab);
 __global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off, int32_t* status);
 __global__ void dec_batch_init_kernel(int64_t* err, int64_t count);
 __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,

@@ -291,6 +291,23 @@ int b64_decode_ex(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
     return launched();
 }
 
+int b64_decode_unpadded(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a,
+                        int64_t* d_err_off, int32_t* d_status, int64_t* d_out_len, b64_stream_t stream) {
+    if (m < 0 || !alpha_ok(a) || !d_err_off) return B64_EINVAL;
+    if (m % 4 == 1) return B64_ELENGTH;
+    if (m % 4 == 0) return b64_decode_ex(d_in, m, d_out, a, d_err_off, d_status, d_out_len, stream);
+    if (!d_in || !d_out) return B64_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), s) != cudaSuccess) return B64_ECUDA;
+    const int64_t full = m - m % 4;
+    if (full > 0) {  // every full quad is interior (no '=' allowed before the trailing group)
+        const int r = decode_launch(d_in, full, d_out, a, 0, 0, d_err_off, nullptr, s);
+        if (r != B64_OK) return r;
+    }
+    launch(dec_finalize_unpadded_kernel, 1, 1, s, d_err_off, d_status, d_out_len, d_in, m, d_out, dec_tab(a));
+    return launched();
+}
+
 int b64_decode(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t* d_err_off,
                b64_stream_t stream) {
     return b64_decode_ex(d_in, m, d_out, a, d_err_off, nullptr, nullptr, stream);

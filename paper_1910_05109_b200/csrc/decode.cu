@@ -287,6 +287,41 @@ __global__ void dec_finalize_single_kernel(int64_t* err_off, int32_t* status, in
     }
 }
 
+// Padding-optional decode (R13), m % 4 in {2, 3}: the 4*floor(m/4)
+// full quads were decoded as interior quads into the cell; this one thread
+// checks the trailing 2-3 char group (alphabet chars, zero dropped bits),
+// decodes it to 1-2 bytes and writes the API results.
+__global__ void dec_finalize_unpadded_kernel(int64_t* err_off, int32_t* status, int64_t* out_len,
+                                             const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out,
+                                             DecTab tab) {
+    griddep_wait();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(tab.w);
+    const int r = int(m & 3);
+    const int64_t p = m - r;
+    unsigned long long wv = *reinterpret_cast<unsigned long long*>(err_off);
+    const uint32_t a = lut[in[p]], b = lut[in[p + 1]], c = (r == 3) ? lut[in[p + 2]] : 0u;
+    unsigned long long pw = kErrNone;
+    if (a & kInvalid) pw = pack_err(p, kBadChar);
+    else if (b & kInvalid) pw = pack_err(p + 1, kBadChar);
+    else if (r == 3 && (c & kInvalid)) pw = pack_err(p + 2, kBadChar);
+    else if ((r == 2 && (b & 15u)) || (r == 3 && (c & 3u))) pw = pack_err(m - 1, kNonCanon);
+    if (pw == kErrNone) {
+        out[3 * (p >> 2)] = uint8_t((a << 2) | (b >> 4));
+        if (r == 3) out[3 * (p >> 2) + 1] = uint8_t(((b & 15u) << 4) | (c >> 2));
+    }
+    wv = pw < wv ? pw : wv;
+    if (wv >= kErrNone) {
+        *err_off = -1;
+        if (status) *status = kOk;
+        if (out_len) *out_len = 3 * (p >> 2) + (r - 1);
+    } else {
+        const int64_t pos = int64_t(wv >> 3);
+        *err_off = pos;
+        if (status) *status = int32_t(wv & 7);
+        if (out_len) *out_len = 3 * (pos >> 2);
+    }
+}
+
 // Chunk / multi-GPU: packed word -> (err_off, status).
 __global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off, int32_t* status) {
     griddep_wait();

@@ -601,3 +601,35 @@ def test_decode_ex_small_path_many_ctas(b64):
             t2 = text.copy()
             t2[p] = ord("#")
             dec_check(b64, t2, oracle.STANDARD, oracle.PAD, std)
+
+
+# ------------------------------------------------------------------ padding-optional decode (R13)
+
+def test_decode_unpadded_vs_oracle(b64):
+    al = _alphabets(b64)
+    for n in list(range(0, 200)) + [767, 768, 769, 3 * 1024 + 1, 100_001, 1 << 20, (1 << 20) + 1, 3_000_001]:
+        chars, pad, alpha = al[n % len(al)]
+        x = synth.data(n, seed=n + 9)
+        bare = oracle.encode_unpadded(x, chars, pad)
+        variants = [bare, oracle.encode(x, chars, pad)]
+        if bare.size:
+            t2 = bare.copy()
+            pos, bad = synth.corruption(1 + n % 2, t2.size, chars, seed=n, pad=pad)
+            t2[pos] = bad
+            variants.append(t2)
+            t3 = bare.copy()
+            t3[-1] = pad  # '=' inside a partial group is a bad char
+            variants.append(t3)
+            if bare.size % 4 in (2, 3):
+                t4 = bare.copy()
+                t4[-1] = chars[(chars.index(bytes([t4[-1]])) + 1) % 64]  # dirty dropped bits
+                variants.append(t4)
+        for t in variants:
+            if t.size % 4 == 1:
+                with pytest.raises(b64.B64Error, match="ELENGTH"):
+                    b64.decode_unpadded(to_dev(t), alpha)
+                continue
+            ref, rerr, rst = oracle.decode_unpadded(t, chars, pad)
+            out, err = b64.decode_unpadded(to_dev(t), alpha)
+            assert err == rerr, (n, err, rerr)
+            assert np.array_equal(out.cpu().numpy(), ref), n
