@@ -65,6 +65,8 @@ def lib():
         L.oracle_decode.restype = ctypes.c_int
         L.oracle_decode_unpadded.argtypes = [P, I64, P, P, U8, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.oracle_decode_unpadded.restype = ctypes.c_int
+        L.oracle_decode_ws.argtypes = [P, I64, P, P, U8, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.oracle_decode_ws.restype = ctypes.c_int
         L.oracle_encode_batch.argtypes = [P, P, I64, P, P, P, U8]
         L.oracle_encode_batch.restype = None
         L.oracle_decode_batch.argtypes = [P, P, I64, P, P, P, U8, P, P, P]
@@ -129,6 +131,18 @@ def decode_unpadded(text, chars: bytes = STANDARD, pad: int = PAD):
     eo = ctypes.c_int64(0)
     st = lib().oracle_decode_unpadded(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
                                       ctypes.byref(ol), ctypes.byref(eo))
+    return out[: ol.value], eo.value, st
+
+
+def decode_ws(text, chars: bytes = STANDARD, pad: int = PAD):
+    """Whitespace-skipping decode (reading R14).  Returns (exact prefix bytes, err_off in the
+    original text, status)."""
+    t = _u8(text)
+    out = np.empty(3 * (t.size // 4) + 1, dtype=np.uint8)
+    ol = ctypes.c_int64(0)
+    eo = ctypes.c_int64(0)
+    st = lib().oracle_decode_ws(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
+                                ctypes.byref(ol), ctypes.byref(eo))
     return out[: ol.value], eo.value, st
 
 

@@ -34,6 +34,7 @@
  * error injection).  Parity status per function is listed in DESIGN.md.
  */
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #define ORACLE_INVALID 0xFFu /* the paper's "special value" */
@@ -244,6 +245,39 @@ int oracle_decode_unpadded(const uint8_t *in, int64_t m, uint8_t *out,
         *out_len = 3 * nq + (r - 1);
     }
     return ORACLE_ST_OK;
+}
+
+/* Whitespace-skipping decode (reading R14; SURVEY.md Sec. 8(f) f2;
+ * the MIME use of PAPER.md:44): the bytes 0x09-0x0D and 0x20 that are not
+ * alphabet chars are removed, the remaining text is decoded by oracle_decode,
+ * and err_off is mapped back to the position of the offending byte in the
+ * ORIGINAL text (for LENGTH: the first char of the incomplete group). */
+int oracle_decode_ws(const uint8_t *in, int64_t m, uint8_t *out,
+                     const uint8_t chars[64], uint8_t pad,
+                     int64_t *out_len, int64_t *err_off)
+{
+    uint8_t skip[256];
+    uint8_t *txt;
+    int64_t *orig, i, k = 0;
+    int v, st;
+    memset(skip, 0, sizeof skip);
+    for (v = 0x09; v <= 0x0D; v++) skip[v] = 1;
+    skip[0x20] = 1;
+    for (v = 0; v < 64; v++) skip[chars[v]] = 0;
+    txt = (uint8_t *)malloc((size_t)(m > 0 ? m : 1));
+    orig = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m > 0 ? m : 1));
+    for (i = 0; i < m; i++) {
+        if (!skip[in[i]]) {
+            txt[k] = in[i];
+            orig[k] = i;
+            k++;
+        }
+    }
+    st = oracle_decode(txt, k, out, chars, pad, out_len, err_off);
+    if (*err_off >= 0) *err_off = orig[*err_off];
+    free(txt);
+    free(orig);
+    return st;
 }
 
 /* Batched forms: the single-stream definitions applied string by string over

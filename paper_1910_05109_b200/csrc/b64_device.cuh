@@ -306,7 +306,7 @@ __global__ void enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __re
 template <int D>
 __global__ void dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
-                                int64_t* __restrict__ out_len);
+                                int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev);
 __global__ void dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off,
                                    DecTab tab, int64_t base, int is_final_single,
                                    unsigned long long* __restrict__ err_cells, int64_t* __restrict__ out_len_single);

@@ -245,7 +245,8 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
         const int dd = dec_depth(m);
         const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(di->occ_dec_fast[dd]));
         auto k = pick2(dd, dec_fast_kernel<1>, dec_fast_kernel<2>);
-        launch(k, blocks, kThreads, s, d_in, m, d_out, dec_tab(a), base, is_final, c, out_len);
+        launch(k, blocks, kThreads, s, d_in, m, d_out, dec_tab(a), base, is_final, c, out_len,
+               static_cast<const int64_t*>(nullptr));
     } else {
         Offsets off{nullptr, nullptr, 1, m};
         const int64_t blocks = clamp_grid((m / 16 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_gen);

@@ -41,10 +41,12 @@ template <int D>
 __global__ void __launch_bounds__(kThreads)
 dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
-                int64_t* __restrict__ out_len) {
+                int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev) {
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];  // per-warp output staging
     griddep_launch_dependents();
+    griddep_wait();
+    if (m_dev) m = *m_dev;  // length produced on the device by a previous kernel (mime.cu)
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
@@ -62,7 +64,6 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     // (conflict-free STS.64 at a 24 B stride) so the global stores are
     // lane-linear STG.64 writing whole sectors.
     // int32 chunk indices and pointers advanced by the grid stride.
-    griddep_wait();
     const int64_t c0 = gtid >> 5;
     const int32_t C = int32_t(nchunk), W = int32_t(nwarp), c0i = int32_t(c0);
     const int64_t sin = nwarp * 1024, sout = nwarp * 768;

@@ -371,3 +371,55 @@ def test_unpadded_errors(orc):
     assert orc.decode_unpadded(b"QUJDQ!")[1:] == (5, orc.ST_BADCHAR)
     assert orc.decode_unpadded(b"Zh")[1:] == (1, orc.ST_NONCANON)
     assert orc.decode_unpadded(b"Zg")[0].tobytes() == b"f"
+
+
+# --------------------------------------------------------------------------- whitespace-skipping decode (R14)
+
+WS = b" \t\n\r\x0b\x0c"
+
+
+def _sprinkle(text: bytes, seed: int, every: int = 76) -> bytes:
+    """MIME-style CRLF every `every` chars plus a few random whitespace bytes."""
+    lines = [text[i: i + every] for i in range(0, len(text), every)]
+    s = b"\r\n".join(lines)
+    w = synth.words(seed, 11, 0, 8)
+    b = bytearray(s)
+    for k in range(int(w[0] % 5)):
+        p = int(w[1 + k] % (len(b) + 1))
+        b[p:p] = bytes([WS[int(w[7] >> np.uint64(8 * k)) % len(WS)]])
+    return bytes(b)
+
+
+def test_ws_decode_vs_stdlib(orc):
+    """Whitespace inserted into valid text: output == stdlib (non-strict decode ignores it)."""
+    for n in list(range(0, 300, 7)) + [4096, 100_000]:
+        x = synth.data(n, seed=n + 3)
+        text = _sprinkle(base64.b64encode(x.tobytes()), seed=n)
+        out, err, st = orc.decode_ws(text)
+        assert err == -1 and st == 0
+        assert out.tobytes() == base64.b64decode(text) == x.tobytes()
+
+
+def test_ws_decode_errors_map_to_original_positions(orc):
+    for trial in range(300):
+        n = 3 + trial * 5
+        x = synth.data(n, seed=trial)
+        clean = base64.b64encode(x.tobytes())
+        text = bytearray(_sprinkle(clean, seed=trial, every=1 + trial % 20))
+        # inject one non-alphabet, non-whitespace byte at an original position
+        cand = [i for i, c in enumerate(text) if c not in WS]
+        p = cand[int(synth.words(trial, 12, 0, 1)[0] % len(cand))]
+        if p >= cand[-4]:  # keep the injection out of the final quad
+            p = cand[0]
+        text[p] = ord("*")
+        out, err, st = orc.decode_ws(bytes(text))
+        assert err == p and st == orc.ST_BADCHAR
+    # LENGTH: compacted length 5 -> the first char of the incomplete group, original coordinates
+    out, err, st = orc.decode_ws(b" QU\nJD\r\nR ")
+    assert st == orc.ST_LENGTH and err == 8
+    assert orc.decode_ws(b" \r\n\t")[1:] == (-1, 0)
+    # whitespace that is an alphabet char is data, not skipped
+    alpha = orc.STANDARD[:62] + b" \t"
+    t = orc.encode(synth.data(300, seed=1), alpha)
+    out, err, st = orc.decode_ws(t, alpha)
+    assert err == -1 and out.tobytes() == synth.data(300, seed=1).tobytes()
