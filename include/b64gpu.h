@@ -131,6 +131,21 @@ int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alph
 int b64_decode_unpadded(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a,
                         int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len, b64_stream_t stream);
 
+/* Whitespace-skipping decode (MIME line-wrapped text; R14): the
+ * bytes 0x09-0x0D and 0x20 that are not alphabet chars are ignored, the rest
+ * is decoded under the strict rules (length and padding rules apply to the
+ * text without whitespace); *d_err_off is the position of the offending byte
+ * in the ORIGINAL text (for B64_ST_LENGTH: of the first char of the
+ * incomplete group).  *d_out_len is 0 for B64_ST_LENGTH (nothing is
+ * decoded, as in b64_decode_ex), else the exact prefix as in b64_decode_ex.
+ * Needs a device workspace of
+ * b64_decode_ws_workspace_bytes(m) bytes (~m + m/1000 + 17 KiB) and d_out
+ * 16-byte aligned with capacity 3*(m/4).  Asynchronous: count, scan, compact,
+ * decode and finalize kernels on `stream`. */
+int64_t b64_decode_ws_workspace_bytes(int64_t m);
+int b64_decode_ws(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a, uint8_t *d_ws,
+                  int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len, b64_stream_t stream);
+
 /* Shard-aware decode used by the multi-GPU driver.
  * Decodes chars [base_offset, base_offset + m) of a larger stream, m % 4 == 0.
  * Only when is_final_chunk != 0 is the last quad treated as the stream's

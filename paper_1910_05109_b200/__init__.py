@@ -23,7 +23,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
-    "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline", "new_info", "decode_unpadded",
+    "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline", "new_info", "decode_unpadded", "decode_ws",
     "encode_group", "decode_group",
     "ERR_NONE",
 ]
@@ -152,6 +152,27 @@ def decode_unpadded(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional
     _lib.check(_lib.lib().b64_decode_unpadded(_ptr(t), m, _ptr(out), _alpha(a), ctypes.c_void_p(ip),
                                               ctypes.c_void_p(ip + 8), ctypes.c_void_p(ip + 16), _stream(stream)),
                "b64_decode_unpadded")
+    err, _, olen = info.tolist()
+    return out[:olen], err
+
+
+def decode_ws(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
+              workspace: Optional[torch.Tensor] = None,
+              stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, int]:
+    """Whitespace-skipping validating decode (b64_decode_ws, R14): MIME-style line
+    breaks and blanks are ignored; err_off is a position in the ORIGINAL text (-1 = valid)."""
+    _check_u8(t, "t")
+    m = t.numel()
+    if out is None:
+        out = torch.empty(max(3 * (m // 4), 1), dtype=torch.uint8, device=t.device)
+    need = int(_lib.lib().b64_decode_ws_workspace_bytes(m))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=t.device)
+    info = new_info(t.device)
+    ip = info.data_ptr()
+    _lib.check(_lib.lib().b64_decode_ws(_ptr(t), m, _ptr(out), _alpha(a), _ptr(workspace), workspace.numel(),
+                                        ctypes.c_void_p(ip), ctypes.c_void_p(ip + 8), ctypes.c_void_p(ip + 16),
+                                        _stream(stream)), "b64_decode_ws")
     err, _, olen = info.tolist()
     return out[:olen], err
 

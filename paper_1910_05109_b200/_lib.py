@@ -63,6 +63,8 @@ SIGNATURES = [
     ("b64_decode", INT, [P, I64, P, AP, P, P]),
     ("b64_decode_ex", INT, [P, I64, P, AP, P, P, P, P]),
     ("b64_decode_unpadded", INT, [P, I64, P, AP, P, P, P, P]),
+    ("b64_decode_ws_workspace_bytes", I64, [I64]),
+    ("b64_decode_ws", INT, [P, I64, P, AP, P, I64, P, P, P, P]),
     ("b64_decode_chunk", INT, [P, I64, P, AP, I64, INT, P, P, P]),
     ("b64_decode_finalize", INT, [P, P, P, P]),
     ("b64_encode_group", INT, [P, I64, P]),

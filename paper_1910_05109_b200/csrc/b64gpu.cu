@@ -4,4 +4,5 @@
 #include "decode.cu"
 #include "group.cu"
 #include "small.cu"
+#include "mime.cu"
 #include "capi.cu"

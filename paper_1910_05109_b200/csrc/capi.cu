@@ -309,6 +309,76 @@ int b64_decode_unpadded(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b6
     return launched();
 }
 
+// ---------------------------------------------------------------- whitespace-skipping decode (mime.cu)
+namespace {
+struct WsLayout {
+    int64_t nch, ncta, K;
+    int64_t off_counts, off_tot, off_base, off_mc, total;
+};
+int64_t up256(int64_t v) { return (v + 255) / 256 * 256; }
+WsLayout ws_layout(int64_t m) {
+    WsLayout L;
+    L.nch = (m + kWsChunk - 1) / kWsChunk;
+    L.ncta = L.nch < kWsMaxCtas ? (L.nch > 0 ? L.nch : 1) : kWsMaxCtas;
+    L.K = (L.nch + L.ncta - 1) / L.ncta;
+    if (L.K < 1) L.K = 1;
+    L.ncta = (L.nch + L.K - 1) / L.K;
+    if (L.ncta < 1) L.ncta = 1;
+    L.off_counts = up256(m + 64);
+    L.off_tot = L.off_counts + up256(4 * (L.nch + 1));
+    L.off_base = L.off_tot + up256(8 * kWsMaxCtas);
+    L.off_mc = L.off_base + up256(8 * kWsMaxCtas);
+    L.total = L.off_mc + 256 + 256;  // + slack to align the caller's pointer
+    return L;
+}
+}  // namespace
+
+int64_t b64_decode_ws_workspace_bytes(int64_t m) { return m < 0 ? -1 : ws_layout(m).total; }
+
+int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, uint8_t* d_ws,
+                  int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, int64_t* d_out_len, b64_stream_t stream) {
+    if (m < 0 || !alpha_ok(a) || !d_err_off) return B64_EINVAL;
+    if (m > 0 && (!d_in || !d_out || !d_ws)) return B64_EINVAL;
+    if (m > 0 && !aligned(d_out, 16)) return B64_EINVAL;
+    const WsLayout L = ws_layout(m);
+    if (m > 0 && ws_bytes < L.total) return B64_EINVAL;
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), s) != cudaSuccess) return B64_ECUDA;
+    if (m == 0) {
+        launch(dec_finalize_packed_kernel, 1, 1, s, static_cast<const int64_t*>(d_err_off), d_err_off, d_status);
+        if (d_out_len && cudaMemsetAsync(d_out_len, 0, sizeof(int64_t), s) != cudaSuccess) return B64_ECUDA;
+        return launched();
+    }
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
+    uint8_t* comp = base;
+    int32_t* counts = reinterpret_cast<int32_t*>(base + L.off_counts);
+    int64_t* tot = reinterpret_cast<int64_t*>(base + L.off_tot);
+    int64_t* cbase = reinterpret_cast<int64_t*>(base + L.off_base);
+    int64_t* mc = reinterpret_cast<int64_t*>(base + L.off_mc);
+    WsTab wt;
+    uint8_t* wb = reinterpret_cast<uint8_t*>(wt.w);
+    std::memcpy(wb, a->dec, 256);
+    for (int c : {0x09, 0x0A, 0x0B, 0x0C, 0x0D, 0x20})
+        if (wb[c] == 0x80) wb[c] = kSkip;
+    launch(ws_count_kernel, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot);
+    launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc);
+    launch(ws_compact_kernel, L.ncta, kThreads, s, d_in, m, wt, L.K, static_cast<const int32_t*>(counts),
+           static_cast<const int64_t*>(cbase), comp);
+    {  // strict decode of the compacted text; its length m' is read on the device
+        const int64_t blocks = balanced_blocks(m / 1024, int64_t(di->sms) * cap_bps(di->occ_dec_fast[1]));
+        launch(dec_fast_kernel<1>, blocks, kThreads, s, static_cast<const uint8_t*>(comp), m, d_out, dec_tab(a),
+               int64_t(0), 1, reinterpret_cast<unsigned long long*>(d_err_off), static_cast<int64_t*>(nullptr),
+               static_cast<const int64_t*>(mc));
+    }
+    launch(ws_finalize_kernel, 1, 32, s, d_err_off, d_status, d_out_len, static_cast<const int64_t*>(mc), d_in, m,
+           static_cast<const uint8_t*>(comp), wt, uint32_t(a->pad), L.K, int(L.ncta),
+           static_cast<const int32_t*>(counts), static_cast<const int64_t*>(cbase));
+    g_launches.fetch_add(4, std::memory_order_relaxed);
+    return launched();
+}
+
 int b64_decode(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t* d_err_off,
                b64_stream_t stream) {
     return b64_decode_ex(d_in, m, d_out, a, d_err_off, nullptr, nullptr, stream);

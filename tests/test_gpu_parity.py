@@ -633,3 +633,58 @@ def test_decode_unpadded_vs_oracle(b64):
             out, err = b64.decode_unpadded(to_dev(t), alpha)
             assert err == rerr, (n, err, rerr)
             assert np.array_equal(out.cpu().numpy(), ref), n
+
+
+# ------------------------------------------------------------------ whitespace-skipping decode (R14)
+
+_WS = np.frombuffer(b" \t\n\r\x0b\x0c", np.uint8)
+
+
+def _mime(text: np.ndarray, seed: int, every: int = 76, extra: int = 0) -> np.ndarray:
+    """CRLF after every `every` chars plus `extra` random whitespace bytes at seeded positions."""
+    parts = []
+    for i in range(0, text.size, every):
+        parts.append(text[i: i + every])
+        parts.append(np.frombuffer(b"\r\n", np.uint8))
+    out = np.concatenate(parts) if parts else text.copy()
+    if extra:
+        w = synth.words(seed, 13, 0, 2 * extra)
+        pos = np.sort((w[:extra] % np.uint64(out.size + 1)).astype(np.int64))
+        vals = _WS[(w[extra:] % np.uint64(_WS.size)).astype(np.int64)]
+        out = np.insert(out, pos, vals)
+    return out
+
+
+def test_decode_ws_vs_oracle(b64):
+    al = _alphabets(b64)
+    ws_alpha = oracle.STANDARD[:62] + b" \t"  # whitespace chars that are data
+    cases = []
+    for n in (0, 1, 2, 3, 57, 100, 3000, 4096 * 3 + 5, 100_001, 1_000_003, 6_000_000):
+        cases.append(n)
+    for i, n in enumerate(cases):
+        chars, pad, alpha = al[i % len(al)]
+        x = synth.data(n, seed=n + 21)
+        text = oracle.encode(x, chars, pad)
+        variants = [_mime(text, n, every=76, extra=3), _mime(text, n, every=1 + n % 97, extra=50)]
+        if text.size > 8:
+            t2 = _mime(text, n + 1, every=64, extra=5)
+            keep = np.nonzero(~np.isin(t2, _WS))[0]
+            p = int(keep[int(synth.words(n, 14, 0, 1)[0] % max(keep.size - 4, 1))])
+            t2 = t2.copy()
+            t2[p] = ord("*")
+            variants.append(t2)
+            t3 = _mime(text[:-1], n + 2, every=50, extra=2)  # compacted length % 4 != 0
+            variants.append(t3)
+        variants.append(np.frombuffer(b"\r\n \t" * 9, np.uint8).copy())
+        for t in variants:
+            ref, rerr, rst = oracle.decode_ws(t, chars, pad)
+            out, err = b64.decode_ws(to_dev(t), alpha)
+            assert err == rerr, (n, err, rerr, rst)
+            assert np.array_equal(out.cpu().numpy(), ref), n
+    # whitespace that belongs to the alphabet is data
+    a2 = b64.alphabet(ws_alpha)
+    x = synth.data(5000, seed=4)
+    t = oracle.encode(x, ws_alpha)
+    out, err = b64.decode_ws(to_dev(_mime(t, 4, every=33)), a2)
+    ref, rerr, _ = oracle.decode_ws(_mime(t, 4, every=33), ws_alpha)
+    assert err == rerr and np.array_equal(out.cpu().numpy(), ref)
