@@ -23,6 +23,7 @@ namespace b64 {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kThreads = 256;          // threads per CTA for every kernel
+constexpr int kBulkCtasPerSm = 5;      // resident CTAs per SM of the bulk kernels (<= 48 registers)
 constexpr uint32_t kInvalid = 0x80u;   // decode-table sentinel
 
 constexpr unsigned long long kErrNone = 0x7F7F7F7F7F7F7F7FULL;  // B64_ERR_NONE

@@ -1,6 +1,7 @@
 // capi.cu -- the C ABI of include/b64gpu.h: argument checks, alphabet
 // validation, launch configuration and kernel dispatch.  No allocation, no
 // per-call state; every launch goes to the caller's stream.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <climits>
@@ -162,6 +163,30 @@ int64_t balanced_blocks(int64_t units, int64_t max_blocks) {
     const int64_t w = (units + rounds - 1) / rounds;
     const int64_t b = (w + wpb - 1) / wpb;
     return b < 1 ? 1 : (b > max_blocks ? max_blocks : b);
+}
+
+// Warp partition of a grouped launch (warp-partitioned group kernels): stream i
+// with C[i] warp-chunks gets W_i = ceil(C[i] / t) warps, t = the smallest
+// per-warp chunk count with sum W_i <= wmax (the resident warps).  Fills
+// wstart[0..count] (exclusive scan of W_i) and returns the blocks to launch.
+int64_t group_partition(const int64_t* cstart, int count, int64_t wmax, int32_t* wstart) {
+    int64_t cmax = 0;
+    for (int i = 0; i < count; ++i) cmax = std::max(cmax, cstart[i + 1] - cstart[i]);
+    auto need = [&](int64_t t) {
+        int64_t s = 0;
+        for (int i = 0; i < count; ++i) s += (cstart[i + 1] - cstart[i] + t - 1) / t;
+        return s;
+    };
+    int64_t lo = 1, hi = cmax < 1 ? 1 : cmax;  // need(cmax) <= count <= wmax
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (need(mid) <= wmax) hi = mid; else lo = mid + 1;
+    }
+    wstart[0] = 0;
+    for (int i = 0; i < count; ++i) wstart[i + 1] = wstart[i] + int32_t((cstart[i + 1] - cstart[i] + lo - 1) / lo);
+    const int64_t wpb = kThreads / 32;
+    const int64_t b = (int64_t(wstart[count]) + wpb - 1) / wpb;
+    return b < 1 ? 1 : b;
 }
 
 int64_t clamp_grid(int64_t want, int64_t cap) { return want < 1 ? 1 : (want > cap ? cap : want); }
@@ -544,7 +569,8 @@ int b64_encode_group(const b64_encode_item* items, int64_t count, b64_stream_t s
     auto flush = [&]() -> int {
         if (g.count == 0) return B64_OK;
         const int d = enc_depth(bytes);
-        const int64_t blocks = balanced_blocks(g.cstart[g.count], int64_t(di->sms) * di->occ_enc_group[d]);
+        const int64_t wmax = int64_t(di->sms) * cap_bps(di->occ_enc_group[d]) * (kThreads / 32);
+        const int64_t blocks = group_partition(g.cstart, g.count, wmax, g.wstart);
         launch(pick2(d, enc_group_kernel<1>, enc_group_kernel<2>), blocks, kThreads, s, g);
         const int r = launched();
         std::memset(&g, 0, sizeof(g));
@@ -559,7 +585,7 @@ int b64_encode_group(const b64_encode_item* items, int64_t count, b64_stream_t s
             if (r != B64_OK) return r;
             continue;
         }
-        if (it.n / 768 >= int64_t(INT32_MAX) / 2) {  // > 800 GB: too many chunks for a group's int32 cursor
+        if (it.n / 768 >= int64_t(INT32_MAX) / 2) {  // > 800 GB: too many chunks for a group's int32 chunk index
             const int r = b64_encode(it.d_in, it.n, it.d_out, it.a, stream);
             if (r != B64_OK) return r;
             continue;
@@ -602,7 +628,8 @@ int b64_decode_group(const b64_decode_item* items, int64_t count, b64_stream_t s
     auto flush = [&]() -> int {
         if (g.count == 0) return B64_OK;
         const int d = dec_depth(bytes);
-        const int64_t blocks = balanced_blocks(g.cstart[g.count], int64_t(di->sms) * di->occ_dec_group[d]);
+        const int64_t wmax = int64_t(di->sms) * cap_bps(di->occ_dec_group[d]) * (kThreads / 32);
+        const int64_t blocks = group_partition(g.cstart, g.count, wmax, g.wstart);
         launch(pick2(d, dec_group_kernel<1>, dec_group_kernel<2>), blocks, kThreads, s, g);
         const int r = launched();
         std::memset(&g, 0, sizeof(g));
@@ -618,7 +645,7 @@ int b64_decode_group(const b64_decode_item* items, int64_t count, b64_stream_t s
             if (r != B64_OK) return r;
             continue;
         }
-        if (it.m / 1024 >= int64_t(INT32_MAX) / 2) {  // too many chunks for a group's int32 cursor
+        if (it.m / 1024 >= int64_t(INT32_MAX) / 2) {  // too many chunks for a group's int32 chunk index
             const int r = b64_decode_chunk(it.d_in, it.m, it.d_out, it.a, it.base_offset, it.is_final, it.d_err_min,
                                            nullptr, stream);
             if (r != B64_OK) return r;

@@ -536,6 +536,33 @@ def test_group_encode_decode_vs_oracle(b64):
             assert np.array_equal(douts[i][: ref.size].cpu().numpy(), ref), (rep, i)
 
 
+def test_group_unequal_large_streams(b64):
+    """Warp-partitioned groups: streams of very different chunk counts (many warps per
+    large stream, one warp for a tiny one, none for an empty one) vs the oracle."""
+    al = _alphabets(b64)
+    sizes = [40 << 20, (3 << 20) + 5, 1024, 0, (17 << 20) + 2, 768 * 7]
+    xs = [synth.data(n, seed=500 + i) for i, n in enumerate(sizes)]
+    chars_l = [(al[i % len(al)][0], al[i % len(al)][1]) for i in range(len(sizes))]
+    alph_l = [al[i % len(al)][2] for i in range(len(sizes))]
+    outs = b64.encode_group([to_dev(x) for x in xs], alph_l)
+    texts = []
+    for i, x in enumerate(xs):
+        ref = oracle.encode(x, *chars_l[i])
+        assert np.array_equal(outs[i].cpu().numpy(), ref), i
+        t = ref.copy()
+        if i in (0, 4) and t.size > 4:
+            pos, bad = synth.corruption(3, t.size, chars_l[i][0], seed=i, pad=chars_l[i][1])
+            t[pos] = bad
+        texts.append(t)
+    douts, err, st = b64.decode_group([to_dev(t) for t in texts], alph_l)
+    errc, stc = err.cpu().numpy(), st.cpu().numpy()
+    for i, t in enumerate(texts):
+        ref, rerr, rst = oracle.decode(t, *chars_l[i])
+        assert (errc[i], stc[i]) == (rerr, rst), i
+        k = ref.size if rerr < 0 else 3 * (rerr // 4)
+        assert np.array_equal(douts[i][:k].cpu().numpy(), ref[:k]), i
+
+
 def test_group_decode_as_shards(b64):
     """Grouped items as shards of one stream: global bases, only the last is final, one cell."""
     x = synth.data(768 * 500 + 1, seed=3)
