@@ -37,27 +37,30 @@ __device__ __forceinline__ uint32_t scan_first_bad(const uint8_t* p, int nquads,
     return 0xffffffffu;
 }
 
-// The bulk loop of one stream as seen by one warp: chunks c0, c0 + W, ... of
-// the stream's C warp-chunks (1024 chars -> 768 bytes), D of them in flight in
-// registers ahead of the one being translated.  prime() issues the first loads
+// The bulk loop of one stream as seen by one warp of a grouped launch
+// (dec_group_kernel): chunks c0, c0 + W, ... of the stream's C warp-chunks
+// (1024 chars -> 768 bytes), D of them in flight in registers ahead of the one
+// being translated.  prime() issues the first loads
 // (before the table is staged); run() is the steady state.  The 24-byte lane
 // outputs are re-laid through the warp's shared buffer sb (conflict-free
 // STS.64 at a 24 B stride) so the global stores are lane-linear STG.64 writing
-// whole sectors.  Positions reported to `cell` are base + char index.  Shared
-// by dec_fast_kernel (one stream, the whole grid) and dec_group_kernel (each
-// stream its own set of warps).
+// whole sectors.  Positions reported to `cell` are base + char index.  The
+// per-lane work is dec_fast_kernel's; that kernel keeps its own copy of the
+// loop, whose loop-invariant bounds ptxas keeps in uniform registers (the
+// shared struct form measured 3.5 % slower at 1 GiB there, profiles/).
 template <int D>
 struct DecBulk {
     const uint8_t* pin;   // next chunk to load
     const uint8_t* pcur;  // chunk being decoded (rare error rescan)
     uint8_t* pout;        // its output
     int32_t c0, C, W;
+    uint32_t zero;  // 0 at run time, opaque to the compiler (see run())
     int64_t sin, sout;
     uint32_t xr[D][8];
 
     __device__ __forceinline__ void prime(const uint8_t* in, uint8_t* out, int32_t c0_, int32_t C_, int32_t W_,
-                                          int lane) {
-        c0 = c0_; C = C_; W = W_;
+                                          int lane, uint32_t zero_) {
+        c0 = c0_; C = C_; W = W_; zero = zero_;
         sin = int64_t(W) * 1024;
         sout = int64_t(W) * 768;
         pin = in + int64_t(c0) * 1024 + lane * 32;
@@ -77,17 +80,22 @@ struct DecBulk {
             for (int i = 0; i < D; ++i) {
                 const int32_t c = cb + i * W;
                 if (c < C) {
-                    uint32_t y[8];
-                    if (c + D * W < C) {
-                        ld256_stream(pin, y);
-                        pin += sin;
-                    }
                     uint32_t err = 0, v[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(xr[i][q], lb, err);
                     uint32_t o[6];
                     dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
                     dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
+                    // The prefetch is issued once xr[i] is consumed: its address carries a
+                    // dependency on the translated values (err & zero, zero == 0 at run
+                    // time but opaque to ptxas), so it cannot be hoisted above the 32
+                    // lookups (hoisted, it keeps 8 more registers live under the
+                    // 48-register cap: 2.5 % slower on 6 x 1 GiB groups).
+                    uint32_t y[8];
+                    if (c + D * W < C) {
+                        ld256_stream(pin + (err & zero), y);
+                        pin += sin;
+                    }
                     sts64(sb + lane * 24, o[0], o[1]);
                     sts64(sb + lane * 24 + 8, o[2], o[3]);
                     sts64(sb + lane * 24 + 16, o[4], o[5]);
@@ -119,7 +127,7 @@ struct DecBulk {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, kBulkCtasPerSm)
+__global__ void __launch_bounds__(kThreads)
 dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
                 int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev) {
@@ -131,18 +139,80 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t nwarp = gthreads >> 5;
     const int64_t Q = m >> 2;
     const int64_t Qint = (is_final && Q > 0) ? Q - 1 : Q;
     const int64_t nchunk = Qint >> 8;
+    const uint32_t sb = smem_u32(&s_stage[threadIdx.x >> 5][0]);
 
-    // Bulk: grid-stride over warp-chunks, so the whole grid sweeps one
-    // contiguous window of memory at a time.
-    DecBulk<D> bulk;
-    bulk.prime(in, out, int32_t(gtid >> 5), int32_t(nchunk), int32_t(gthreads >> 5), lane);
+    // Bulk: grid-stride over warp-chunks (1024 chars -> 768 bytes), so the
+    // whole grid sweeps one contiguous window of memory at a time.  Software
+    // pipeline: D chunks per warp are in flight ahead of the one being
+    // translated (the first ones are issued before the table is staged).  The
+    // 24-byte lane outputs are re-laid through a per-warp shared buffer
+    // (conflict-free STS.64 at a 24 B stride) so the global stores are
+    // lane-linear STG.64 writing whole sectors.
+    // int32 chunk indices and pointers advanced by the grid stride.
+    const int64_t c0 = gtid >> 5;
+    const int32_t C = int32_t(nchunk), W = int32_t(nwarp), c0i = int32_t(c0);
+    const int64_t sin = nwarp * 1024, sout = nwarp * 768;
+    const uint8_t* pin = in + c0 * 1024 + lane * 32;  // next chunk to load
+    const uint8_t* pcur = in + c0 * 1024 + lane * 32; // chunk being decoded (rare error rescan)
+    uint8_t* pout = out + c0 * 768;                   // its output
+    uint32_t xr[D][8];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        if (c0i + i * W < C) {
+            ld256_stream(pin, xr[i]);
+            pin += sin;
+        }
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
-    bulk.run(smem_u32(s_lut), lut, smem_u32(&s_stage[threadIdx.x >> 5][0]), lane, base, err_cell);
+    const uint32_t lb = smem_u32(s_lut);
+    for (int32_t cb = c0i; cb < C; cb += D * W) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int32_t c = cb + i * W;
+            if (c < C) {
+                uint32_t y[8];
+                if (c + D * W < C) {
+                    ld256_stream(pin, y);
+                    pin += sin;
+                }
+                uint32_t err = 0, v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(xr[i][q], lb, err);
+                uint32_t o[6];
+                dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
+                dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
+                sts64(sb + lane * 24, o[0], o[1]);
+                sts64(sb + lane * 24 + 8, o[2], o[3]);
+                sts64(sb + lane * 24 + 16, o[4], o[5]);
+                __syncwarp();
+                uint8_t* dst = pout + lane * 8;
+                const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8),
+                            s2 = lds64(sb + 512 + lane * 8);
+                st64(dst, s0.x, s0.y);
+                st64(dst + 256, s1.x, s1.y);
+                st64(dst + 512, s2.x, s2.y);
+                __syncwarp();
+                const bool bad = (err & kInvalid) != 0;
+                if (__any_sync(kFull, bad)) {  // rare: locate the first invalid char of the chunk
+                    uint32_t rel = 0xffffffffu;
+                    if (bad) {
+                        rel = scan_first_bad(pcur, 8, lut);
+                        if (rel != 0xffffffffu) rel += lane * 32;
+                    }
+                    warp_report(bad, rel, base + int64_t(c) * 1024, err_cell);
+                }
+                pout += sout;
+                pcur += sin;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) xr[i][j] = y[j];
+            }
+        }
+    }
 
     // leftover interior quads, one per thread
     for (int64_t q = (nchunk << 8) + gtid; q < Qint; q += gthreads) {

@@ -34,14 +34,14 @@ __device__ __forceinline__ void enc_lane_compute(const uint32_t (&w)[6], uint32_
     o[7] = enc_triple_s(__byte_perm(w[5], w[5], 0x1233), lb);
 }
 
-// The bulk loop of one stream as seen by one warp: chunks c0, c0 + W, ... of
+// The bulk loop of one stream as seen by one warp of a grouped launch
+// (enc_group_kernel; enc_fast_kernel keeps its own copy): chunks c0, c0 + W, ... of
 // the stream's C warp-chunks (768 B -> 1024 chars), D of them in flight in
 // registers ahead of the one being encoded.  prime() issues the first loads
 // (before the alphabet is staged, so the table set-up hides under the first
 // DRAM latency); run() is the steady state.  int32 chunk indices (an
 // HBM-resident stream has < 2^31 chunks) and pointers advanced by the stride:
-// no 64-bit index math per chunk.  Shared by enc_fast_kernel (one stream, the
-// whole grid) and enc_group_kernel (each stream its own set of warps).
+// no 64-bit index math per chunk.
 template <int D>
 struct EncBulk {
     const uint8_t* pin;  // next chunk to load
@@ -87,27 +87,61 @@ struct EncBulk {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, kBulkCtasPerSm)
+__global__ void __launch_bounds__(kThreads)
 enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab, uint32_t pad) {
     __shared__ __align__(64) uint32_t s_lut[16];
     griddep_launch_dependents();
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t nwarp = gthreads >> 5;
     const int64_t nchunk = n / 768;
+    const int64_t c0 = gtid >> 5;
 
     // Grid-stride over warp-chunks: at any moment the whole grid works on one
-    // contiguous window of memory (DRAM row locality).
+    // contiguous window of memory (DRAM row locality).  Software pipeline: D
+    // chunks per warp are in flight ahead of the one being encoded.  The first
+    // loads are issued before the alphabet is staged, so the table set-up
+    // hides under the first DRAM latency.
+    // int32 chunk indices (an HBM-resident stream has < 2^31 chunks) and
+    // pointers advanced by the grid stride: no 64-bit index math per chunk.
     griddep_wait();
-    EncBulk<D> bulk;
-    bulk.prime(in, out, int32_t(gtid >> 5), int32_t(nchunk), int32_t(gthreads >> 5), lane);
+    const int32_t C = int32_t(nchunk), W = int32_t(nwarp), c0i = int32_t(c0);
+    const int64_t sin = nwarp * 768, sout = nwarp * 1024;
+    const uint8_t* pin = in + c0 * 768 + lane * 24;  // next chunk to load
+    uint8_t* pout = out + c0 * 1024 + lane * 32;     // next chunk to store
+    uint32_t wv[D][6];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        if (c0i + i * W < C) {
+            enc_lane24(pin, wv[i]);
+            pin += sin;
+        }
     if (threadIdx.x == 0) {  // static indices: the table stays in the constant bank, no stack copy
 #pragma unroll
         for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
     }
     __syncthreads();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
-    bulk.run(smem_u32(s_lut));
+    const uint32_t lb = smem_u32(s_lut);
+    for (int32_t c = c0i; c < C; c += D * W) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int32_t ci = c + i * W;
+            if (ci < C) {
+                uint32_t yv[6], o[8];
+                if (ci + D * W < C) {
+                    enc_lane24(pin, yv);
+                    pin += sin;
+                }
+                enc_lane_compute(wv[i], o, lb);
+                st256(pout, o);
+                pout += sout;
+#pragma unroll
+                for (int j = 0; j < 6; ++j) wv[i][j] = yv[j];
+            }
+        }
+    }
 
     // remainder: output quads [256*nchunk, ceil(n/3)), one per thread
     const int64_t T = n / 3;

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) dec_group_kernel(con
     DecBulk<D> bulk;
     if (it < g.count) {
         bulk.prime(g.in[it], g.out[it], w - g.wstart[it], int32_t(g.cstart[it + 1] - g.cstart[it]),
-                   g.wstart[it + 1] - g.wstart[it], lane);
+                   g.wstart[it + 1] - g.wstart[it], lane, g.pad[it] >> 8);  // pad < 0x80
     }
     for (int t = threadIdx.x; t < g.count * 64; t += blockDim.x) (&s_lut[0][0])[t] = (&g.lut[0][0])[t];
     __syncthreads();
