@@ -194,6 +194,53 @@ int b64_decode_group(const b64_decode_item *items, int64_t count, b64_stream_t s
 int b64_decode_finalize_n(const int64_t *d_err_min, int64_t count, int64_t *d_err_off, int32_t *d_status,
                           b64_stream_t stream);
 
+/* ---- streaming: input in pieces, carry between calls (R15) ------ */
+/* Input arrives in pieces of any length (e.g. network / file reads); the result
+ * is exactly the one-shot b64_encode / b64_decode_ex of the concatenation, with
+ * error positions in its coordinates.  Whole triples / quads are coded as soon
+ * as they are complete; the bytes of an incomplete group are held in d_carry
+ * (device, >= 8 bytes, caller-owned, used only by this stream).  Decode always
+ * holds back the last 1-4 chars, so the stream's final quad (the only place
+ * '=' may appear, R6) is decoded by the end call.  The host struct
+ * carries only lengths: no call waits for the device.  Every call of one
+ * stream must use the same alphabet and the same CUDA stream (or be ordered by
+ * the caller); pieces may be reused / freed once the work queued by the call
+ * has run.  Calls on a finished stream (or the wrong kind) return B64_EINVAL. */
+typedef struct b64_stream {
+    int64_t consumed;   /* input bytes (encode) / chars (decode) accepted so far */
+    int64_t produced;   /* output bytes written so far                           */
+    int32_t held;       /* bytes (0-2) / chars (0-4) currently held in d_carry    */
+    int32_t state;      /* internal: 1 encoding, 2 decoding, 3 finished           */
+    uint8_t *d_carry;   /* device carry buffer (>= 8 bytes)                       */
+    int64_t *d_err_min; /* decode: device packed error word of the stream         */
+} b64_stream;
+
+int b64_encode_stream_begin(b64_stream *st, uint8_t *d_carry);
+/* Encode piece d_in[0..n): writes *n_out = 4*floor((held + n)/3) chars at d_out
+ * (capacity >= that; *n_out is known on return, host-side). */
+int b64_encode_stream_update(b64_stream *st, const uint8_t *d_in, int64_t n, uint8_t *d_out, const b64_alphabet *a,
+                             int64_t *n_out, b64_stream_t stream);
+/* Finish: the 1-2 held bytes -> 4 chars with '=' padding at d_out (*n_out = 4),
+ * or nothing (*n_out = 0).  Total output = b64_encoded_len(consumed). */
+int b64_encode_stream_end(b64_stream *st, uint8_t *d_out, const b64_alphabet *a, int64_t *n_out,
+                          b64_stream_t stream);
+
+/* Decode: d_err_min (device int64) is set to B64_ERR_NONE on `stream` and
+ * lowered by every later call (packed global position << 3 | status). */
+int b64_decode_stream_begin(b64_stream *st, uint8_t *d_carry, int64_t *d_err_min, b64_stream_t stream);
+/* Decode piece d_in[0..m) (any m >= 0): writes *n_out = 3*Q bytes at d_out,
+ * Q = floor((held + m - 1)/4) interior quads (capacity >= *n_out). */
+int b64_decode_stream_update(b64_stream *st, const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a,
+                             int64_t *n_out, b64_stream_t stream);
+/* Finish: total = consumed chars.  total % 4 != 0 -> status B64_ST_LENGTH at
+ * total - total % 4 (as b64_decode_batch); else the held final quad -> 1-3
+ * bytes at d_out (capacity >= 3, *n_out = 3 = the most it may write).  Then
+ * *d_err_off / *d_status / *d_out_len (device; the last two nullable) exactly
+ * as b64_decode_ex for the whole concatenated text (*d_out_len = 0 for
+ * B64_ST_LENGTH). */
+int b64_decode_stream_end(b64_stream *st, uint8_t *d_out, const b64_alphabet *a, int64_t *d_err_off,
+                          int32_t *d_status, int64_t *d_out_len, int64_t *n_out, b64_stream_t stream);
+
 /* ---- host buffers, overlapped (SURVEY.md Sec. 8(f) f3 ingest pipeline) ------ */
 /* Encode / decode HOST buffers (h_*: host pointers, pinned for the copies to be
  * asynchronous) through a caller-owned DEVICE workspace d_ws of ws_bytes.  The

@@ -24,7 +24,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
     "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline", "new_info", "decode_unpadded", "decode_ws",
-    "encode_group", "decode_group",
+    "encode_group", "decode_group", "EncodeStream", "DecodeStream",
     "ERR_NONE",
 ]
 
@@ -246,6 +246,92 @@ def decode_group(ts, alphabets=None, outs=None, cells: Optional[torch.Tensor] = 
     _lib.check(_lib.lib().b64_decode_finalize_n(_ptr(cells), k, _ptr(err), _ptr(st), _stream(stream)),
                "b64_decode_finalize_n")
     return outs, err, st
+
+
+# ------------------------------------------------------------------ streaming (carry between calls)
+
+class EncodeStream:
+    """Encode input that arrives in pieces of any length (b64_encode_stream_*).
+
+    update(x) returns the chars completed so far (a view of a fresh or given buffer);
+    end() returns the padded tail.  The concatenation of every returned piece equals
+    encode(concatenation of the inputs)."""
+
+    def __init__(self, a: Optional[Alphabet] = None, device=None, stream: Optional[torch.cuda.Stream] = None):
+        self.a = _alpha(a)
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.carry = torch.zeros(8, dtype=torch.uint8, device=self.dev)
+        self.st = _lib.Stream()
+        self.stream = stream
+        _lib.check(_lib.lib().b64_encode_stream_begin(ctypes.byref(self.st), _ptr(self.carry)),
+                   "b64_encode_stream_begin")
+
+    def out_len(self, n: int) -> int:
+        return 4 * ((self.st.held + n) // 3)
+
+    def update(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        _check_u8(x, "x")
+        k = self.out_len(x.numel())
+        if out is None:
+            out = torch.empty(max(k, 1), dtype=torch.uint8, device=self.dev)
+        n_out = ctypes.c_int64(0)
+        _lib.check(_lib.lib().b64_encode_stream_update(ctypes.byref(self.st), _ptr(x), x.numel(), _ptr(out),
+                                                       self.a, ctypes.byref(n_out), _stream(self.stream)),
+                   "b64_encode_stream_update")
+        return out[: n_out.value]
+
+    def end(self, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty(4, dtype=torch.uint8, device=self.dev)
+        n_out = ctypes.c_int64(0)
+        _lib.check(_lib.lib().b64_encode_stream_end(ctypes.byref(self.st), _ptr(out), self.a, ctypes.byref(n_out),
+                                                    _stream(self.stream)), "b64_encode_stream_end")
+        return out[: n_out.value]
+
+
+class DecodeStream:
+    """Validating decode of text that arrives in pieces of any length (b64_decode_stream_*).
+
+    update(t) returns the bytes of the quads completed so far (the last 1-4 chars are
+    held back); end() returns (tail bytes tensor, info) with info = int64[3] device tensor
+    (err_off, status, out_len) for the whole concatenated text, exactly as decode_async."""
+
+    def __init__(self, a: Optional[Alphabet] = None, device=None, stream: Optional[torch.cuda.Stream] = None):
+        self.a = _alpha(a)
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.carry = torch.zeros(8, dtype=torch.uint8, device=self.dev)
+        self.cell = torch.empty(1, dtype=torch.int64, device=self.dev)
+        self.st = _lib.Stream()
+        self.stream = stream
+        _lib.check(_lib.lib().b64_decode_stream_begin(ctypes.byref(self.st), _ptr(self.carry), _ptr(self.cell),
+                                                      _stream(stream)), "b64_decode_stream_begin")
+
+    def out_len(self, m: int) -> int:
+        A = self.st.held + m
+        return 3 * ((A - 1) // 4) if A > 0 else 0
+
+    def update(self, t: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        _check_u8(t, "t")
+        k = self.out_len(t.numel())
+        if out is None:
+            out = torch.empty(max(k, 1), dtype=torch.uint8, device=self.dev)
+        n_out = ctypes.c_int64(0)
+        _lib.check(_lib.lib().b64_decode_stream_update(ctypes.byref(self.st), _ptr(t), t.numel(), _ptr(out),
+                                                       self.a, ctypes.byref(n_out), _stream(self.stream)),
+                   "b64_decode_stream_update")
+        return out[: n_out.value]
+
+    def end(self, out: Optional[torch.Tensor] = None):
+        if out is None:
+            out = torch.empty(3, dtype=torch.uint8, device=self.dev)
+        info = new_info(self.dev)
+        ip = info.data_ptr()
+        n_out = ctypes.c_int64(0)
+        _lib.check(_lib.lib().b64_decode_stream_end(ctypes.byref(self.st), _ptr(out), self.a, ctypes.c_void_p(ip),
+                                                    ctypes.c_void_p(ip + 8), ctypes.c_void_p(ip + 16),
+                                                    ctypes.byref(n_out), _stream(self.stream)),
+                   "b64_decode_stream_end")
+        return out[: n_out.value], info
 
 
 # ------------------------------------------------------------------ host buffers (overlapped pipeline)

@@ -53,6 +53,15 @@ class DecodeItem(ctypes.Structure):
                 ("base_offset", ctypes.c_int64), ("is_final", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("d_err_min", ctypes.c_void_p)]
 
+class Stream(ctypes.Structure):
+    """b64_stream (streaming encode / decode state; lengths only, the carry is on the device)."""
+    _fields_ = [("consumed", ctypes.c_int64), ("produced", ctypes.c_int64), ("held", ctypes.c_int32),
+                ("state", ctypes.c_int32), ("d_carry", ctypes.c_void_p), ("d_err_min", ctypes.c_void_p)]
+
+
+SP = ctypes.POINTER(Stream)
+I64P = ctypes.POINTER(ctypes.c_int64)
+
 SIGNATURES = [
     ("b64_alphabet_init", INT, [AP, ctypes.c_char_p, ctypes.c_char, ctypes.POINTER(INT)]),
     ("b64_alphabet_standard", AP, []),
@@ -70,6 +79,12 @@ SIGNATURES = [
     ("b64_encode_group", INT, [P, I64, P]),
     ("b64_decode_group", INT, [P, I64, P]),
     ("b64_decode_finalize_n", INT, [P, I64, P, P, P]),
+    ("b64_encode_stream_begin", INT, [SP, P]),
+    ("b64_encode_stream_update", INT, [SP, P, I64, P, AP, I64P, P]),
+    ("b64_encode_stream_end", INT, [SP, P, AP, I64P, P]),
+    ("b64_decode_stream_begin", INT, [SP, P, P, P]),
+    ("b64_decode_stream_update", INT, [SP, P, I64, P, AP, I64P, P]),
+    ("b64_decode_stream_end", INT, [SP, P, AP, P, P, P, I64P, P]),
     ("b64_host_workspace_bytes", I64, [I64]),
     ("b64_encode_host", INT, [P, I64, P, AP, P, I64, P, P, P]),
     ("b64_decode_host", INT, [P, I64, P, AP, P, I64, P, P, P, P, P]),

@@ -5,4 +5,5 @@
 #include "group.cu"
 #include "small.cu"
 #include "mime.cu"
+#include "stream.cu"
 #include "capi.cu"

@@ -428,6 +428,122 @@ int b64_decode_finalize(const int64_t* d_err_min, int64_t* d_err_off, int32_t* d
     return launched();
 }
 
+// ---------------------------------------------------------------- streaming (stream.cu)
+// The host side of a stream only does length arithmetic (held / consumed /
+// produced are functions of the piece lengths), so no call waits for the
+// device; the held bytes themselves live in the caller's device carry buffer.
+namespace {
+enum { kStIdle = 0, kStEncode = 1, kStDecode = 2, kStDone = 3 };
+}
+
+int b64_encode_stream_begin(b64_stream* st, uint8_t* d_carry) {
+    if (!st || !d_carry) return B64_EINVAL;
+    st->consumed = st->produced = 0;
+    st->held = 0;
+    st->state = kStEncode;
+    st->d_carry = d_carry;
+    st->d_err_min = nullptr;
+    return B64_OK;
+}
+
+int b64_encode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabet* a,
+                             int64_t* n_out, b64_stream_t stream) {
+    if (!st || st->state != kStEncode || n < 0 || !alpha_ok(a) || (n > 0 && !d_in)) return B64_EINVAL;
+    const int64_t H = st->held, A = H + n, T = A / 3;
+    if (T > 0 && !d_out) return B64_EINVAL;
+    if (n_out) *n_out = 4 * T;
+    if (n == 0) return B64_OK;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int join = (H > 0 && T > 0) ? 1 : 0;
+    if (H > 0 || A % 3) {  // a straddling triple and / or bytes to hold
+        launch(enc_stream_join_kernel, 1, 1, s, st->d_carry, int(H), d_in, n, d_out, enc_tab(a));
+        const int r = launched();
+        if (r != B64_OK) return r;
+    }
+    const int64_t skip = join ? 3 - H : 0, tb = T - join;  // whole triples read straight from the piece
+    if (tb > 0) {
+        const int r = b64_encode(d_in + skip, 3 * tb, d_out + 4 * join, a, stream);
+        if (r != B64_OK) return r;
+    }
+    st->held = int32_t(A % 3);
+    st->consumed += n;
+    st->produced += 4 * T;
+    return B64_OK;
+}
+
+int b64_encode_stream_end(b64_stream* st, uint8_t* d_out, const b64_alphabet* a, int64_t* n_out,
+                          b64_stream_t stream) {
+    if (!st || st->state != kStEncode || !alpha_ok(a)) return B64_EINVAL;
+    const int H = st->held;
+    if (H > 0 && !d_out) return B64_EINVAL;
+    if (n_out) *n_out = H > 0 ? 4 : 0;
+    if (H > 0) {
+        launch(enc_stream_end_kernel, 1, 1, reinterpret_cast<cudaStream_t>(stream), st->d_carry, H, d_out, enc_tab(a),
+               uint32_t(a->pad));
+        const int r = launched();
+        if (r != B64_OK) return r;
+        st->produced += 4;
+    }
+    st->held = 0;
+    st->state = kStDone;
+    return B64_OK;
+}
+
+int b64_decode_stream_begin(b64_stream* st, uint8_t* d_carry, int64_t* d_err_min, b64_stream_t stream) {
+    if (!st || !d_carry || !d_err_min) return B64_EINVAL;
+    if (cudaMemsetAsync(d_err_min, 0x7F, sizeof(int64_t), reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return B64_ECUDA;
+    st->consumed = st->produced = 0;
+    st->held = 0;
+    st->state = kStDecode;
+    st->d_carry = d_carry;
+    st->d_err_min = d_err_min;
+    return B64_OK;
+}
+
+int b64_decode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a,
+                             int64_t* n_out, b64_stream_t stream) {
+    if (!st || st->state != kStDecode || m < 0 || !alpha_ok(a) || (m > 0 && !d_in)) return B64_EINVAL;
+    const int64_t H = st->held, A = H + m;
+    const int64_t Q = A > 0 ? (A - 1) / 4 : 0;  // the last 1..4 chars are always held
+    if (Q > 0 && !d_out) return B64_EINVAL;
+    if (n_out) *n_out = 3 * Q;
+    if (m == 0) return B64_OK;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int join = (H > 0 && Q > 0) ? 1 : 0;
+    launch(dec_stream_join_kernel, 1, 1, s, st->d_carry, int(H), d_in, m, d_out, dec_tab(a), st->consumed - H,
+           reinterpret_cast<unsigned long long*>(st->d_err_min));
+    int r = launched();
+    if (r != B64_OK) return r;
+    const int64_t skip = join ? 4 - H : 0, qb = Q - join;  // whole quads read straight from the piece
+    if (qb > 0) {
+        r = b64_decode_chunk(d_in + skip, 4 * qb, d_out + 3 * join, a, st->consumed + skip, 0, st->d_err_min,
+                             nullptr, stream);
+        if (r != B64_OK) return r;
+    }
+    st->held = int32_t(A - 4 * Q);
+    st->consumed += m;
+    st->produced += 3 * Q;
+    return B64_OK;
+}
+
+int b64_decode_stream_end(b64_stream* st, uint8_t* d_out, const b64_alphabet* a, int64_t* d_err_off,
+                          int32_t* d_status, int64_t* d_out_len, int64_t* n_out, b64_stream_t stream) {
+    if (!st || st->state != kStDecode || !alpha_ok(a) || !d_err_off) return B64_EINVAL;
+    const int64_t total = st->consumed;
+    const bool fin = total > 0 && total % 4 == 0;
+    if (fin && !d_out) return B64_EINVAL;
+    launch(dec_stream_end_kernel, 1, 1, reinterpret_cast<cudaStream_t>(stream), st->d_carry, int(st->held), total,
+           d_out, dec_tab(a), reinterpret_cast<const unsigned long long*>(st->d_err_min), d_err_off, d_status,
+           d_out_len);
+    const int r = launched();
+    if (r != B64_OK) return r;
+    if (n_out) *n_out = fin ? 3 : 0;  // bytes of d_out the end call may write (the exact count is in *d_out_len)
+    st->held = 0;
+    st->state = kStDone;
+    return B64_OK;
+}
+
 // ---------------------------------------------------------------- host-buffer pipelines
 // Chunks of the host input are copied H2D on s_h2d, coded on s_comp and copied
 // back D2H on s_d2h through kHostBufs rotating device buffers, so both PCIe

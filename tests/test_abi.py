@@ -94,3 +94,31 @@ def test_no_cpu_fallback_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 s = open(os.path.join(dp, f)).read()
                 assert "oracle" not in s.replace("oracle/", ""), f
+
+
+def test_stream_host_state_machine(L):
+    """Streaming API (b64gpu.h, R15): argument / state errors are synchronous
+    and touch no device; zero-length pieces launch nothing."""
+    from paper_1910_05109_b200 import _lib
+
+    a = L.b64_alphabet_standard()
+    st = _lib.Stream()
+    n_out = ctypes.c_int64(-1)
+    carry = ctypes.c_void_p(0x1000)  # never dereferenced on the host
+    assert L.b64_encode_stream_update(ctypes.byref(st), None, 0, None, a, ctypes.byref(n_out), None) == -1  # not begun
+    assert L.b64_encode_stream_begin(None, carry) == -1
+    assert L.b64_encode_stream_begin(ctypes.byref(st), None) == -1
+    assert L.b64_encode_stream_begin(ctypes.byref(st), carry) == 0
+    assert (st.consumed, st.produced, st.held) == (0, 0, 0)
+    assert L.b64_encode_stream_update(ctypes.byref(st), None, 0, None, a, ctypes.byref(n_out), None) == 0
+    assert n_out.value == 0
+    assert L.b64_encode_stream_update(ctypes.byref(st), None, 5, None, a, ctypes.byref(n_out), None) == -1
+    assert L.b64_encode_stream_update(ctypes.byref(st), None, -1, None, a, ctypes.byref(n_out), None) == -1
+    # a decode call on an encode stream is refused
+    assert L.b64_decode_stream_update(ctypes.byref(st), None, 0, None, a, ctypes.byref(n_out), None) == -1
+    assert L.b64_decode_stream_end(ctypes.byref(st), None, a, ctypes.c_void_p(8), None, None, None, None) == -1
+    # nothing held: ending writes nothing and launches nothing
+    assert L.b64_encode_stream_end(ctypes.byref(st), None, a, ctypes.byref(n_out), None) == 0
+    assert n_out.value == 0
+    assert L.b64_encode_stream_update(ctypes.byref(st), None, 0, None, a, ctypes.byref(n_out), None) == -1  # finished
+    assert L.b64_decode_stream_begin(ctypes.byref(st), carry, None, None) == -1

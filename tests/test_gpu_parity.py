@@ -715,3 +715,104 @@ def test_decode_ws_vs_oracle(b64):
     out, err = b64.decode_ws(to_dev(_mime(t, 4, every=33)), a2)
     ref, rerr, _ = oracle.decode_ws(_mime(t, 4, every=33), ws_alpha)
     assert err == rerr and np.array_equal(out.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------ streaming (carry between calls)
+
+def _splits(total: int, rng, small: bool):
+    """Piece lengths summing to total: tiny pieces (0-9) when small, else a mix of tiny,
+    chunk-sized and odd multi-chunk pieces."""
+    out, left = [], total
+    while left > 0:
+        if small or rng.random() < 0.4:
+            k = int(rng.integers(0, 10))
+        else:
+            k = int(rng.choice([1024, 4096, 3 * 1024 + 1, 100_003, 768 * 50 + 7, 1 << 16]))
+        k = min(k, left)
+        out.append(k)
+        left -= k
+        if rng.random() < 0.05:
+            out.append(0)
+    return out
+
+
+def test_encode_stream_vs_oracle(b64):
+    """Streaming encode (R15): any split of the input gives the one-shot encode."""
+    al = _alphabets(b64)
+    rng = np.random.default_rng(21)
+    for trial, n in enumerate([0, 1, 2, 3, 4, 5, 47, 1000, 100_000, 768 * 300 + 2, 1 << 20]):
+        for small in ((True, False) if n < 5000 else (False,)):
+            chars, pad, alpha = al[trial % len(al)]
+            x = synth.data(n, seed=300 + trial)
+            dx = to_dev(x)
+            es = b64.EncodeStream(alpha)
+            parts, pos = [], 0
+            for k in _splits(n, rng, small):
+                parts.append(es.update(dx[pos: pos + k]).cpu().numpy())
+                pos += k
+            parts.append(es.end().cpu().numpy())
+            got = np.concatenate(parts)
+            assert np.array_equal(got, oracle.encode(x, chars, pad)), (n, small)
+            assert es.st.produced == got.size == b64.encoded_len(n)
+
+
+def _dec_stream(b64, text, alpha, pieces, misalign=0):
+    ds = b64.DecodeStream(alpha)
+    dt = to_dev(text, misalign)
+    parts, pos = [], 0
+    for k in pieces:
+        parts.append(ds.update(dt[pos: pos + k]).cpu().numpy())
+        pos += k
+    tail, info = ds.end()
+    parts.append(tail.cpu().numpy())
+    return np.concatenate(parts), info.tolist()
+
+
+def test_decode_stream_vs_oracle(b64):
+    """Streaming decode: any split gives the one-shot decode -- output, err_off, status and
+    out_len of the whole text -- including errors in straddling quads, in the held-back
+    final quad and the LENGTH rule."""
+    al = _alphabets(b64)
+    rng = np.random.default_rng(22)
+    cases = 0
+    for trial, n in enumerate([0, 1, 2, 3, 4, 30, 31, 32, 1000, 100_000, 768 * 300 + 1, 1 << 20]):
+        chars, pad, alpha = al[trial % len(al)]
+        text = oracle.encode(synth.data(n, seed=400 + trial), chars, pad)
+        variants = [text]
+        if text.size > 8:
+            for j in range(3):  # corrupted copies
+                t2 = text.copy()
+                p_, b_ = synth.corruption(1 + j, text.size, chars, seed=trial * 10 + j, pad=pad)
+                t2[p_] = b_
+                variants.append(t2)
+            t3 = text.copy()  # a pad in the middle; bad final quad forms
+            t3[text.size // 2] = pad
+            variants.append(t3)
+            t4 = text.copy()
+            t4[-1] = ord("*")
+            variants.append(t4)
+            variants.append(text[:-1])  # LENGTH (m % 4 == 3)
+            variants.append(text[:-3])  # LENGTH (m % 4 == 1)
+        for v in variants:
+            ref, rerr, rst = oracle.decode(v, chars, pad)
+            for small in ((True, False) if v.size < 5000 else (False,)):
+                got, (err, st, olen) = _dec_stream(b64, v, alpha, _splits(v.size, rng, small), misalign=trial % 3)
+                assert (err, st) == (rerr, rst), (n, small, err, st, rerr, rst)
+                assert olen == ref.size, (n, olen, ref.size)
+                assert np.array_equal(got[:olen], ref), n
+                cases += 1
+    assert cases > 60
+
+
+def test_decode_stream_error_at_every_boundary_position(b64):
+    """Piece boundary at every offset of a small text x one bad char at every position:
+    the error lands in the join quad, a bulk quad or the held final quad."""
+    text = oracle.encode(synth.data(45, seed=9))  # 60 chars, final quad 'xxxx'
+    std = b64.standard()
+    for cut in range(0, text.size + 1, 3):
+        for p in range(0, text.size, 5):
+            t = text.copy()
+            t[p] = ord("$")
+            _, rerr, rst = oracle.decode(t)
+            got, (err, st, olen) = _dec_stream(b64, t, std, [cut, text.size - cut])
+            assert (err, st) == (rerr, rst) == (p, oracle.ST_BADCHAR), (cut, p)
