@@ -32,11 +32,49 @@ def main():
     p.add_argument("--reps", type=int, default=20)
     p.add_argument("--tag", default=os.environ.get("B64_TAG", ""))
     p.add_argument("--group", type=int, default=0, help="also time k grouped streams of each size (one launch)")
+    p.add_argument("--batch", type=int, default=0, help="time configs[3]-style batches of this many strings instead")
+    p.add_argument("--batch-len", type=int, default=0, help="with --batch: every string this long (else log-uniform)")
     a = p.parse_args()
     dev = torch.device("cuda:0")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     flush_r = torch.zeros(64 << 20, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
+
+    def timed(fn, reps):
+        evs = []
+        for k in range(reps + 3):
+            flush.fill_(k & 255)
+            flush_r.sum()
+            torch.cuda._sleep(200_000)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        return statistics.median([e0.elapsed_time(e1) for e0, e1 in evs[3:]])
+
+    if a.batch:  # log-uniform string lengths in [1, 64 KiB] (configs[3] recipe)
+        import numpy as np
+
+        Ls = (np.full(a.batch, a.batch_len, dtype=np.int64) if a.batch_len
+              else synth.loguniform_lengths(a.batch, seed=0))
+        off = synth.offsets(Ls)
+        x = synth.device_data(int(off[-1]), seed=0)
+        doff = torch.from_numpy(off).to(dev)
+        enc, eoff = b64.encode_batch(x, doff)
+        tot_in, tot_out = int(off[-1]), int(eoff[-1].item())
+        lens = eoff[1:] - eoff[:-1]
+        doo = torch.zeros(len(Ls) + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(3 * torch.div(lens, 4, rounding_mode="floor"), 0, out=doo[1:])
+        dout = torch.empty(int(doo[-1].item()) + 16, dtype=torch.uint8, device=dev)
+        te = timed(lambda: b64.encode_batch(x, doff, out=enc, out_off=eoff), a.reps)
+        td = timed(lambda: b64.decode_batch(enc, eoff, out=dout, out_off=doo), a.reps)
+        print(json.dumps({"tag": a.tag, "batch": a.batch, "len": a.batch_len, "in": tot_in, "b64": tot_out,
+                          "enc": {"us": round(te * 1e3, 1), "traffic_gbs": round((tot_in + tot_out) / te / 1e6, 1)},
+                          "dec": {"us": round(td * 1e3, 1), "traffic_gbs": round((tot_in + tot_out) / td / 1e6, 1)}}),
+              flush=True)
+        return
     for s in a.sizes.split(","):
         n = parse_size(s)
         x = synth.device_data(n, seed=0)
