@@ -67,6 +67,11 @@ def lib():
         L.oracle_decode_unpadded.restype = ctypes.c_int
         L.oracle_decode_ws.argtypes = [P, I64, P, P, U8, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.oracle_decode_ws.restype = ctypes.c_int
+        for nm in ("oracle_decode_lenient", "oracle_decode_unpadded_lenient", "oracle_decode_ws_lenient"):
+            getattr(L, nm).argtypes = [P, I64, P, P, U8, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+            getattr(L, nm).restype = ctypes.c_int
+        L.oracle_decode_batch_opt.argtypes = [P, P, I64, P, P, P, U8, ctypes.c_int, P, P, P]
+        L.oracle_decode_batch_opt.restype = None
         L.oracle_encode_batch.argtypes = [P, P, I64, P, P, P, U8]
         L.oracle_encode_batch.restype = None
         L.oracle_decode_batch.argtypes = [P, P, I64, P, P, P, U8, P, P, P]
@@ -112,36 +117,41 @@ def encode(data, chars: bytes = STANDARD, pad: int = PAD) -> np.ndarray:
     return out[:m]
 
 
-def decode(text, chars: bytes = STANDARD, pad: int = PAD):
-    """Returns (bytes ndarray of the exact prefix, err_off, status)."""
+def decode(text, chars: bytes = STANDARD, pad: int = PAD, lenient: bool = False):
+    """Returns (bytes ndarray of the exact prefix, err_off, status).  lenient: reading R16
+    (non-zero trailing bits before the padding are dropped instead of rejected)."""
     t = _u8(text)
     out = np.empty(3 * (t.size // 4) + 1, dtype=np.uint8)
     ol = ctypes.c_int64(0)
     eo = ctypes.c_int64(0)
-    st = lib().oracle_decode(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
+    f = lib().oracle_decode_lenient if lenient else lib().oracle_decode
+    st = f(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
                              ctypes.byref(ol), ctypes.byref(eo))
     return out[: ol.value], eo.value, st
 
 
-def decode_unpadded(text, chars: bytes = STANDARD, pad: int = PAD):
-    """Padding-optional decode (reading R13).  Returns (exact prefix bytes, err_off, status)."""
+def decode_unpadded(text, chars: bytes = STANDARD, pad: int = PAD, lenient: bool = False):
+    """Padding-optional decode (reading R13; + R16 when lenient).  Returns (exact prefix bytes,
+    err_off, status)."""
     t = _u8(text)
     out = np.empty(3 * (t.size // 4) + 3, dtype=np.uint8)
     ol = ctypes.c_int64(0)
     eo = ctypes.c_int64(0)
-    st = lib().oracle_decode_unpadded(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
+    f = lib().oracle_decode_unpadded_lenient if lenient else lib().oracle_decode_unpadded
+    st = f(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
                                       ctypes.byref(ol), ctypes.byref(eo))
     return out[: ol.value], eo.value, st
 
 
-def decode_ws(text, chars: bytes = STANDARD, pad: int = PAD):
-    """Whitespace-skipping decode (reading R14).  Returns (exact prefix bytes, err_off in the
-    original text, status)."""
+def decode_ws(text, chars: bytes = STANDARD, pad: int = PAD, lenient: bool = False):
+    """Whitespace-skipping decode (reading R14; + R16 when lenient).  Returns (exact prefix
+    bytes, err_off in the original text, status)."""
     t = _u8(text)
     out = np.empty(3 * (t.size // 4) + 1, dtype=np.uint8)
     ol = ctypes.c_int64(0)
     eo = ctypes.c_int64(0)
-    st = lib().oracle_decode_ws(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
+    f = lib().oracle_decode_ws_lenient if lenient else lib().oracle_decode_ws
+    st = f(_ptr(t) if t.size else None, t.size, _ptr(out), _ptr(_alpha(chars)), pad,
                                 ctypes.byref(ol), ctypes.byref(eo))
     return out[: ol.value], eo.value, st
 
@@ -167,7 +177,7 @@ def encode_batch(data, in_off, chars: bytes = STANDARD, pad: int = PAD):
     return out[: out_off[-1]], out_off
 
 
-def decode_batch(text, in_off, chars: bytes = STANDARD, pad: int = PAD):
+def decode_batch(text, in_off, chars: bytes = STANDARD, pad: int = PAD, lenient: bool = False):
     """Returns (out buffer laid out at out_off = scan(3*len//4), out_off, status, err_off, out_len)."""
     t = _u8(text)
     in_off = np.ascontiguousarray(in_off, dtype=np.int64)
@@ -180,6 +190,6 @@ def decode_batch(text, in_off, chars: bytes = STANDARD, pad: int = PAD):
     err = np.zeros(max(count, 1), dtype=np.int64)
     olen = np.zeros(max(count, 1), dtype=np.int64)
     ts = t if t.size else np.zeros(1, np.uint8)
-    lib().oracle_decode_batch(_ptr(ts), _ptr(in_off), count, _ptr(out), _ptr(out_off), _ptr(_alpha(chars)), pad,
-                              _ptr(status), _ptr(err), _ptr(olen))
+    lib().oracle_decode_batch_opt(_ptr(ts), _ptr(in_off), count, _ptr(out), _ptr(out_off), _ptr(_alpha(chars)), pad,
+                                  int(lenient), _ptr(status), _ptr(err), _ptr(olen))
     return out[: out_off[-1]], out_off, status[:count], err[:count], olen[:count]

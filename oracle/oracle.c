@@ -117,10 +117,13 @@ static void build_decode_table(const uint8_t chars[64], uint8_t dec[256])
 }
 
 /* Decode m chars.  Returns the status kind; *out_len and *err_off as in the
- * header comment (err_off = -1 when valid). */
-int oracle_decode(const uint8_t *in, int64_t m, uint8_t *out,
-                  const uint8_t chars[64], uint8_t pad,
-                  int64_t *out_len, int64_t *err_off)
+ * header comment (err_off = -1 when valid).  lenient != 0 (DESIGN.md reading
+ * R16): the canonical-bits check is skipped -- the low bits of the last char
+ * before the padding are dropped, as Python's binascii strict mode and GNU
+ * coreutils do; every other rule is unchanged. */
+static int decode_opt(const uint8_t *in, int64_t m, uint8_t *out,
+                      const uint8_t chars[64], uint8_t pad, int lenient,
+                      int64_t *out_len, int64_t *err_off)
 {
     uint8_t dec[256];
     int64_t q, nq;
@@ -162,8 +165,8 @@ int oracle_decode(const uint8_t *in, int64_t m, uint8_t *out,
             else if (dec[c[2]] == ORACLE_INVALID && !pad2) { bad = p + 2; kind = ORACLE_ST_BADCHAR; }
             else if (dec[c[3]] == ORACLE_INVALID && !pad3) { bad = p + 3; kind = ORACLE_ST_BADCHAR; }
             else if (pad2 && !pad3) { bad = p + 3; kind = ORACLE_ST_BADPAD; }
-            else if (pad2 && pad3 && (dec[c[1]] % 16) != 0) { bad = p + 1; kind = ORACLE_ST_NONCANON; }
-            else if (!pad2 && pad3 && (dec[c[2]] % 4) != 0) { bad = p + 2; kind = ORACLE_ST_NONCANON; }
+            else if (!lenient && pad2 && pad3 && (dec[c[1]] % 16) != 0) { bad = p + 1; kind = ORACLE_ST_NONCANON; }
+            else if (!lenient && !pad2 && pad3 && (dec[c[2]] % 4) != 0) { bad = p + 2; kind = ORACLE_ST_NONCANON; }
             if (kind != ORACLE_ST_OK) {
                 *err_off = bad;
                 *out_len = 3 * q;
@@ -185,6 +188,20 @@ int oracle_decode(const uint8_t *in, int64_t m, uint8_t *out,
     return ORACLE_ST_OK;
 }
 
+int oracle_decode(const uint8_t *in, int64_t m, uint8_t *out,
+                  const uint8_t chars[64], uint8_t pad,
+                  int64_t *out_len, int64_t *err_off)
+{
+    return decode_opt(in, m, out, chars, pad, 0, out_len, err_off);
+}
+
+int oracle_decode_lenient(const uint8_t *in, int64_t m, uint8_t *out,
+                          const uint8_t chars[64], uint8_t pad,
+                          int64_t *out_len, int64_t *err_off)
+{
+    return decode_opt(in, m, out, chars, pad, 1, out_len, err_off);
+}
+
 /* Padding-optional decode (reading R13):
  * the encoded length law of PAPER.md:84-87 without the '=' ("may be
  * appended").  m % 4 == 0: exactly oracle_decode.  m % 4 == 1: LENGTH at
@@ -192,13 +209,13 @@ int oracle_decode(const uint8_t *in, int64_t m, uint8_t *out,
  * alphabet), then the last 2 or 3 chars must be alphabet chars and decode to
  * 1 or 2 bytes by the same formulas (missing values taken as zero), with the
  * dropped low bits zero (canonical; NONCANON at m - 1). */
-int oracle_decode_unpadded(const uint8_t *in, int64_t m, uint8_t *out,
-                           const uint8_t chars[64], uint8_t pad,
-                           int64_t *out_len, int64_t *err_off)
+static int decode_unpadded_opt(const uint8_t *in, int64_t m, uint8_t *out,
+                               const uint8_t chars[64], uint8_t pad, int lenient,
+                               int64_t *out_len, int64_t *err_off)
 {
     uint8_t dec[256];
     int64_t q, nq, r, p;
-    if (m % 4 == 0) return oracle_decode(in, m, out, chars, pad, out_len, err_off);
+    if (m % 4 == 0) return decode_opt(in, m, out, chars, pad, lenient, out_len, err_off);
     build_decode_table(chars, dec);
     *out_len = 0;
     *err_off = -1;
@@ -235,7 +252,7 @@ int oracle_decode_unpadded(const uint8_t *in, int64_t m, uint8_t *out,
     }
     {
         unsigned a = dec[in[p]], b = dec[in[p + 1]], cc = (r == 3) ? dec[in[p + 2]] : 0;
-        if ((r == 2 && (b % 16) != 0) || (r == 3 && (cc % 4) != 0)) {
+        if (!lenient && ((r == 2 && (b % 16) != 0) || (r == 3 && (cc % 4) != 0))) {
             *err_off = m - 1;
             *out_len = 3 * nq;
             return ORACLE_ST_NONCANON;
@@ -247,14 +264,30 @@ int oracle_decode_unpadded(const uint8_t *in, int64_t m, uint8_t *out,
     return ORACLE_ST_OK;
 }
 
+int oracle_decode_unpadded(const uint8_t *in, int64_t m, uint8_t *out,
+                           const uint8_t chars[64], uint8_t pad,
+                           int64_t *out_len, int64_t *err_off)
+{
+    return decode_unpadded_opt(in, m, out, chars, pad, 0, out_len, err_off);
+}
+
+/* Padding-optional AND lenient (R13 + R16): the dropped low bits of a 2/3-char
+ * tail (or of the char before '=') may be non-zero. */
+int oracle_decode_unpadded_lenient(const uint8_t *in, int64_t m, uint8_t *out,
+                                   const uint8_t chars[64], uint8_t pad,
+                                   int64_t *out_len, int64_t *err_off)
+{
+    return decode_unpadded_opt(in, m, out, chars, pad, 1, out_len, err_off);
+}
+
 /* Whitespace-skipping decode (reading R14; SURVEY.md Sec. 8(f) f2;
  * the MIME use of PAPER.md:44): the bytes 0x09-0x0D and 0x20 that are not
  * alphabet chars are removed, the remaining text is decoded by oracle_decode,
  * and err_off is mapped back to the position of the offending byte in the
  * ORIGINAL text (for LENGTH: the first char of the incomplete group). */
-int oracle_decode_ws(const uint8_t *in, int64_t m, uint8_t *out,
-                     const uint8_t chars[64], uint8_t pad,
-                     int64_t *out_len, int64_t *err_off)
+static int decode_ws_opt(const uint8_t *in, int64_t m, uint8_t *out,
+                         const uint8_t chars[64], uint8_t pad, int lenient,
+                         int64_t *out_len, int64_t *err_off)
 {
     uint8_t skip[256];
     uint8_t *txt;
@@ -273,11 +306,25 @@ int oracle_decode_ws(const uint8_t *in, int64_t m, uint8_t *out,
             k++;
         }
     }
-    st = oracle_decode(txt, k, out, chars, pad, out_len, err_off);
+    st = decode_opt(txt, k, out, chars, pad, lenient, out_len, err_off);
     if (*err_off >= 0) *err_off = orig[*err_off];
     free(txt);
     free(orig);
     return st;
+}
+
+int oracle_decode_ws(const uint8_t *in, int64_t m, uint8_t *out,
+                     const uint8_t chars[64], uint8_t pad,
+                     int64_t *out_len, int64_t *err_off)
+{
+    return decode_ws_opt(in, m, out, chars, pad, 0, out_len, err_off);
+}
+
+int oracle_decode_ws_lenient(const uint8_t *in, int64_t m, uint8_t *out,
+                             const uint8_t chars[64], uint8_t pad,
+                             int64_t *out_len, int64_t *err_off)
+{
+    return decode_ws_opt(in, m, out, chars, pad, 1, out_len, err_off);
 }
 
 /* Batched forms: the single-stream definitions applied string by string over
@@ -294,13 +341,21 @@ void oracle_encode_batch(const uint8_t *in, const int64_t *in_off, int64_t count
 
 /* Decode output string i starts at out_off[i]; err_off is relative to the
  * string start, -1 when valid. */
+void oracle_decode_batch_opt(const uint8_t *in, const int64_t *in_off, int64_t count,
+                             uint8_t *out, const int64_t *out_off,
+                             const uint8_t chars[64], uint8_t pad, int lenient,
+                             int32_t *status, int64_t *err_off, int64_t *out_len)
+{
+    int64_t i;
+    for (i = 0; i < count; i++)
+        status[i] = decode_opt(in + in_off[i], in_off[i + 1] - in_off[i], out + out_off[i],
+                               chars, pad, lenient, &out_len[i], &err_off[i]);
+}
+
 void oracle_decode_batch(const uint8_t *in, const int64_t *in_off, int64_t count,
                          uint8_t *out, const int64_t *out_off,
                          const uint8_t chars[64], uint8_t pad,
                          int32_t *status, int64_t *err_off, int64_t *out_len)
 {
-    int64_t i;
-    for (i = 0; i < count; i++)
-        status[i] = oracle_decode(in + in_off[i], in_off[i + 1] - in_off[i], out + out_off[i],
-                                  chars, pad, &out_len[i], &err_off[i]);
+    oracle_decode_batch_opt(in, in_off, count, out, out_off, chars, pad, 0, status, err_off, out_len);
 }

@@ -423,3 +423,73 @@ def test_ws_decode_errors_map_to_original_positions(orc):
     t = orc.encode(synth.data(300, seed=1), alpha)
     out, err, st = orc.decode_ws(t, alpha)
     assert err == -1 and out.tobytes() == synth.data(300, seed=1).tobytes()
+
+
+# --------------------------------------------------------------------------- lenient decode (R16)
+
+def test_lenient_final_quad_vs_stdlib_strict(orc):
+    """Lenient (reading R16) == binascii strict mode on every padded final quad: all
+    4096 'xx==' and 262144 'xxx=' alphabet quads are accepted, with stdlib's bytes
+    (stdlib drops the trailing bits)."""
+    a = STD
+    for i in range(64):
+        for j in range(64):
+            q = bytes([a[i], a[j]]) + b"=="
+            out, err, st = orc.decode(q, lenient=True)
+            assert err == -1 and st == 0
+            assert out.tobytes() == binascii.a2b_base64(q, strict_mode=True)
+    t = _all_quads_text(STD).reshape(-1, 4)[::64].copy()
+    t[:, 3] = ord("=")
+    for q in t:
+        out, err, st = orc.decode(q, lenient=True)
+        assert err == -1 and out.tobytes() == binascii.a2b_base64(q.tobytes(), strict_mode=True)
+
+
+def test_lenient_final_quad_every_byte(orc):
+    """Every byte value at each final-quad position: lenient accepts <=> stdlib strict
+    accepts, same bytes; rejections keep the strict kinds (never NONCANON)."""
+    for base in (b"QUJD", b"QQ==", b"QUI=", b"Zh==", b"Zm9="):
+        for p in range(4):
+            for v in range(256):
+                t = bytearray(b"AAAA" + base)
+                t[4 + p] = v
+                out, err, st = orc.decode(bytes(t), lenient=True)
+                try:
+                    ref = binascii.a2b_base64(bytes(t), strict_mode=True)
+                    ok = True
+                except binascii.Error:
+                    ok = False
+                assert (err == -1) == ok, (base, p, v, err)
+                if ok:
+                    assert out.tobytes() == ref
+                else:
+                    assert st != orc.ST_NONCANON and 4 <= err <= 7
+                    # a rejection is the strict verdict at the same place
+                    assert orc.decode(bytes(t))[1:] == (err, st)
+
+
+def test_lenient_equals_strict_elsewhere(orc):
+    """Lenient differs from strict only on NONCANON verdicts (fuzzed texts, injected errors)."""
+    for trial in range(300):
+        n = trial * 7
+        x = synth.data(n, seed=trial)
+        t = orc.encode(x)
+        if t.size > 8 and trial % 2:
+            pos, bad = synth.corruption(1 + trial % 3, t.size, orc.STANDARD, seed=trial)
+            t[pos] = bad
+        s = orc.decode(t)
+        l = orc.decode(t, lenient=True)
+        if s[2] != orc.ST_NONCANON:
+            assert s[1:] == l[1:] and s[0].tobytes() == l[0].tobytes()
+    # unpadded lenient: the 2/3-char tail's dropped bits may be non-zero (stdlib on re-padded text)
+    for g in (b"Zh", b"Zm9", b"QUJDZh", b"QUJDZm9"):
+        out, err, st = orc.decode_unpadded(g, lenient=True)
+        assert err == -1 and out.tobytes() == binascii.a2b_base64(g + b"=" * (-len(g) % 4), strict_mode=True)
+        assert orc.decode_unpadded(g)[2] == orc.ST_NONCANON
+    assert orc.decode_ws(b"Z h\n==", lenient=True)[0].tobytes() == b"f"
+    assert orc.decode_ws(b"Z h\n==")[1:] == (2, orc.ST_NONCANON)  # original coordinates
+    txt = np.frombuffer(b"QUJDZh==Zg==QQ", np.uint8)
+    out, off, st, err, olen = orc.decode_batch(txt, np.array([0, 8, 12, 14]), lenient=True)
+    assert list(st) == [0, 0, orc.ST_LENGTH] and list(err) == [-1, -1, 0]
+    out, off, st, err, olen = orc.decode_batch(txt, np.array([0, 8, 12, 14]))
+    assert list(st) == [orc.ST_NONCANON, 0, orc.ST_LENGTH] and list(err) == [5, -1, 0]
