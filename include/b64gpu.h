@@ -82,8 +82,16 @@ typedef struct b64_alphabet {
     uint8_t enc[64];
     uint8_t dec[256];
     uint8_t pad;
-    uint8_t reserved[3];
+    uint8_t flags;       /* B64_ALPHA_* decode options; 0 after b64_alphabet_init */
+    uint8_t reserved[2];
 } b64_alphabet;
+
+/* Lenient decode (R16): every strict rule applies except the
+ * canonical-bits check -- the low bits of the char before '=' (or of the last
+ * char of an unpadded 2/3-char tail) are dropped instead of reported as
+ * B64_ST_NONCANON, as Python's binascii strict mode and GNU coreutils do.
+ * Honoured by every decode entry point that takes the alphabet. */
+#define B64_ALPHA_LENIENT 1u
 
 /* Validate `chars` (64 bytes) + `pad` and fill `*a`.  Rules (R4):
  * 64 distinct bytes < 0x80, pad < 0x80 and not among them.  On failure
@@ -91,7 +99,11 @@ typedef struct b64_alphabet {
  * (64 = the pad); *a is then unspecified.  Host only, O(1). */
 int b64_alphabet_init(b64_alphabet *a, const char chars[64], char pad, int *bad_index);
 
-/* Built-in alphabets (static storage, never freed). */
+/* Set the decode options of a validated alphabet (B64_ALPHA_* bits; unknown
+ * bits -> B64_EINVAL).  Host only. */
+int b64_alphabet_set_flags(b64_alphabet *a, unsigned flags);
+
+/* Built-in alphabets (static storage, never freed; strict: flags 0). */
 const b64_alphabet *b64_alphabet_standard(void);
 const b64_alphabet *b64_alphabet_url(void);
 

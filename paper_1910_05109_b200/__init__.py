@@ -22,7 +22,7 @@ from . import _lib
 from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH, ST_NONCANON, ST_OK  # noqa: F401
 
 __all__ = [
-    "Alphabet", "B64Error", "alphabet", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
+    "Alphabet", "B64Error", "alphabet", "lenient_of", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
     "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline", "new_info", "decode_unpadded", "decode_ws",
     "encode_group", "decode_group", "EncodeStream", "DecodeStream",
     "ERR_NONE",
@@ -50,8 +50,9 @@ def _check_i64(t: torch.Tensor, name: str) -> None:
 
 # ------------------------------------------------------------------ alphabets
 
-def alphabet(chars: bytes, pad: bytes = b"=") -> Alphabet:
-    """Validate a 64-char alphabet + pad (R4); returns the by-value table struct."""
+def alphabet(chars: bytes, pad: bytes = b"=", lenient: bool = False) -> Alphabet:
+    """Validate a 64-char alphabet + pad (R4); returns the by-value table struct.
+    lenient=True sets B64_ALPHA_LENIENT (R16) for every decode with it."""
     if len(chars) != 64 or len(pad) != 1:
         raise B64Error("alphabet needs 64 chars and a 1-byte pad")
     a = Alphabet()
@@ -59,7 +60,16 @@ def alphabet(chars: bytes, pad: bytes = b"=") -> Alphabet:
     rc = _lib.lib().b64_alphabet_init(ctypes.byref(a), bytes(chars), pad, ctypes.byref(bad))
     if rc != 0:
         raise B64Error(f"invalid alphabet: {_lib.ERRORS.get(rc, rc)} at index {bad.value}")
-    return a
+    return lenient_of(a) if lenient else a
+
+
+def lenient_of(a: Alphabet) -> Alphabet:
+    """A copy of `a` with B64_ALPHA_LENIENT set (R16: non-zero trailing bits before
+    the padding are dropped instead of rejected)."""
+    b = Alphabet()
+    ctypes.pointer(b)[0] = a
+    _lib.check(_lib.lib().b64_alphabet_set_flags(ctypes.byref(b), _lib.ALPHA_LENIENT), "b64_alphabet_set_flags")
+    return b
 
 
 def standard() -> Alphabet:

@@ -36,9 +36,12 @@ ERRORS = {
 P, I64, I32, INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
 
 
+ALPHA_LENIENT = 1  # B64_ALPHA_LENIENT
+
+
 class Alphabet(ctypes.Structure):
     _fields_ = [("enc", ctypes.c_uint8 * 64), ("dec", ctypes.c_uint8 * 256), ("pad", ctypes.c_uint8),
-                ("reserved", ctypes.c_uint8 * 3)]
+                ("flags", ctypes.c_uint8), ("reserved", ctypes.c_uint8 * 2)]
 
 
 AP = ctypes.POINTER(Alphabet)
@@ -64,6 +67,7 @@ I64P = ctypes.POINTER(ctypes.c_int64)
 
 SIGNATURES = [
     ("b64_alphabet_init", INT, [AP, ctypes.c_char_p, ctypes.c_char, ctypes.POINTER(INT)]),
+    ("b64_alphabet_set_flags", INT, [AP, ctypes.c_uint]),
     ("b64_alphabet_standard", AP, []),
     ("b64_alphabet_url", AP, []),
     ("b64_encoded_len", I64, [I64]),

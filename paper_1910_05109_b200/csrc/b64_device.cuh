@@ -32,7 +32,7 @@ enum : uint32_t { kOk = 0, kBadChar = 1, kBadPad = 2, kNonCanon = 3, kLength = 4
 // Alphabet tables passed BY VALUE as kernel parameters (runtime constants,
 // PAPER.md:240).
 struct EncTab { uint32_t w[16]; };             // enc[64] chars
-struct DecTab { uint32_t w[64]; uint32_t pad; };  // dec[256] + pad char
+struct DecTab { uint32_t w[64]; uint32_t pad; uint32_t lenient; };  // dec[256] + pad char + R16 flag
 
 // Programmatic dependent launch (PDL): kernels are launched so the next
 // kernel on the stream may start its prologue while this one drains; each
@@ -251,9 +251,10 @@ __device__ __forceinline__ int first_bad_in_quad(uint32_t x, const uint8_t* __re
 // The stream's final quad (R6, "final and separate code path",
 // PAPER.md:569).  Returns the error kind (kOk when valid); *bad = 0..3 the
 // offending position within the quad; *k = output bytes (1..3) when valid and
-// *v = the 24-bit value.
+// *v = the 24-bit value.  lenient (R16): non-zero trailing bits are
+// dropped instead of reported as NONCANON.
 __device__ __forceinline__ uint32_t final_quad(uint32_t x, const uint8_t* __restrict__ lut, uint32_t pad,
-                                               int* bad, int* k, uint32_t* v) {
+                                               uint32_t lenient, int* bad, int* k, uint32_t* v) {
     const uint32_t ch0 = x & 0xffu, ch1 = (x >> 8) & 0xffu, ch2 = (x >> 16) & 0xffu, ch3 = x >> 24;
     const uint32_t a = lut[ch0], b = lut[ch1], c = lut[ch2], d = lut[ch3];
     const bool p2 = ch2 == pad, p3 = ch3 == pad;
@@ -264,8 +265,8 @@ __device__ __forceinline__ uint32_t final_quad(uint32_t x, const uint8_t* __rest
     if ((c & kInvalid) && !p2) { *bad = 2; return kBadChar; }
     if ((d & kInvalid) && !p3) { *bad = 3; return kBadChar; }
     if (p2 && !p3) { *bad = 3; return kBadPad; }
-    if (p2 && (b & 15u)) { *bad = 1; return kNonCanon; }
-    if (!p2 && p3 && (c & 3u)) { *bad = 2; return kNonCanon; }
+    if (!lenient && p2 && (b & 15u)) { *bad = 1; return kNonCanon; }
+    if (!lenient && !p2 && p3 && (c & 3u)) { *bad = 2; return kNonCanon; }
     *v = (a << 18) | (b << 12) | ((p2 ? 0u : c) << 6) | (p3 ? 0u : d);
     return kOk;
 }

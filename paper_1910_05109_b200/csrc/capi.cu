@@ -74,6 +74,7 @@ DecTab dec_tab(const b64_alphabet* a) {
     DecTab t;
     std::memcpy(t.w, a->dec, 256);
     t.pad = a->pad;
+    t.lenient = (a->flags & B64_ALPHA_LENIENT) ? 1u : 0u;
     return t;
 }
 
@@ -218,7 +219,14 @@ int b64_alphabet_init(b64_alphabet* a, const char chars[64], char pad, int* bad_
     std::memset(a->dec, 0x80, 256);
     for (int v = 0; v < 64; ++v) a->dec[c[v]] = static_cast<uint8_t>(v);
     a->pad = p;
-    a->reserved[0] = a->reserved[1] = a->reserved[2] = 0;
+    a->flags = 0;
+    a->reserved[0] = a->reserved[1] = 0;
+    return B64_OK;
+}
+
+int b64_alphabet_set_flags(b64_alphabet* a, unsigned flags) {
+    if (!a || (flags & ~unsigned(B64_ALPHA_LENIENT))) return B64_EINVAL;
+    a->flags = static_cast<uint8_t>(flags);
     return B64_OK;
 }
 
@@ -779,6 +787,7 @@ int b64_decode_group(const b64_decode_item* items, int64_t count, b64_stream_t s
         g.cell[k] = reinterpret_cast<unsigned long long*>(it.d_err_min);
         g.is_final[k] = it.is_final ? 1 : 0;
         g.pad[k] = it.a->pad;
+        g.lenient[k] = (it.a->flags & B64_ALPHA_LENIENT) ? 1u : 0u;
         std::memcpy(g.lut[k], it.a->dec, 256);
         const int64_t Q = it.m / 4;
         const int64_t Qint = (it.is_final && Q > 0) ? Q - 1 : Q;

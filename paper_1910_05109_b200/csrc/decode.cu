@@ -228,7 +228,7 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
             const int64_t q = Q - 1;
             int bad, k;
             uint32_t v;
-            const uint32_t kind = final_quad(ld32(in + 4 * q), lut, tab.pad, &bad, &k, &v);
+            const uint32_t kind = final_quad(ld32(in + 4 * q), lut, tab.pad, tab.lenient, &bad, &k, &v);
             if (kind == kOk) store_bytes(out + 3 * q, v, k);
             else atomicMin(err_cell, pack_err(base + 4 * q + bad, kind));
             if (out_len) *out_len = 3 * q + k;
@@ -340,7 +340,7 @@ dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
                 if (fin && j == Qs - 1) {
                     int badj, kk;
                     uint32_t v;
-                    const uint32_t kind = final_quad(x, lut, tab.pad, &badj, &kk, &v);
+                    const uint32_t kind = final_quad(x, lut, tab.pad, tab.lenient, &badj, &kk, &v);
                     if (kind == kOk) store_bytes(o + 3 * j, v, kk);
                     else atomicMin(cell, pack_err(pbase + 4 * j + badj, kind));
                 } else {
@@ -394,7 +394,7 @@ __global__ void dec_finalize_unpadded_kernel(int64_t* err_off, int32_t* status, 
     if (a & kInvalid) pw = pack_err(p, kBadChar);
     else if (b & kInvalid) pw = pack_err(p + 1, kBadChar);
     else if (r == 3 && (c & kInvalid)) pw = pack_err(p + 2, kBadChar);
-    else if ((r == 2 && (b & 15u)) || (r == 3 && (c & 3u))) pw = pack_err(m - 1, kNonCanon);
+    else if (!tab.lenient && ((r == 2 && (b & 15u)) || (r == 3 && (c & 3u)))) pw = pack_err(m - 1, kNonCanon);
     if (pw == kErrNone) {
         out[3 * (p >> 2)] = uint8_t((a << 2) | (b >> 4));
         if (r == 3) out[3 * (p >> 2) + 1] = uint8_t(((b & 15u) << 4) | (c >> 2));

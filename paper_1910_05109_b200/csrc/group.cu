@@ -34,6 +34,7 @@ struct DecGroup {
     int32_t wstart[kGroupMax + 1];
     int32_t is_final[kGroupMax];
     uint32_t pad[kGroupMax];
+    uint32_t lenient[kGroupMax];    // DESIGN.md R16
     uint32_t lut[kGroupMax][64];    // dec[256] per stream
     int count;
 };
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) dec_group_kernel(con
             const int64_t q = Q - 1;
             int bad, k;
             uint32_t v;
-            const uint32_t kind = final_quad(ld32(in + 4 * q), lut, g.pad[is], &bad, &k, &v);
+            const uint32_t kind = final_quad(ld32(in + 4 * q), lut, g.pad[is], g.lenient[is], &bad, &k, &v);
             if (kind == kOk) store_bytes(out + 3 * q, v, k);
             else atomicMin(g.cell[is], pack_err(g.base[is] + 4 * q + bad, kind));
         }

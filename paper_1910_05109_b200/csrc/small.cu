@@ -87,7 +87,7 @@ dec_small_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
         const int64_t q = Q - 1;
         int bad;
         uint32_t v;
-        const uint32_t kind = final_quad(ld32(in + 4 * q), lut, tab.pad, &bad, &k_final, &v);
+        const uint32_t kind = final_quad(ld32(in + 4 * q), lut, tab.pad, tab.lenient, &bad, &k_final, &v);
         if (kind == kOk) store_bytes(out + 3 * q, v, k_final);
         else atomicMin(&s_min, pack_err(4 * q + bad, kind));
     }

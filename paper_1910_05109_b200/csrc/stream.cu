@@ -100,7 +100,7 @@ __global__ void dec_stream_end_kernel(const uint8_t* __restrict__ carry, int H, 
                            (uint32_t(carry[3]) << 24);
         int bad, k;
         uint32_t v;
-        const uint32_t kind = final_quad(x, lut, tab.pad, &bad, &k, &v);
+        const uint32_t kind = final_quad(x, lut, tab.pad, tab.lenient, &bad, &k, &v);
         if (kind == kOk) store_bytes(out, v, k);
         else wv = min(wv, pack_err(total - 4 + bad, kind));
         ol = 3 * (total / 4 - 1) + k;

@@ -816,3 +816,108 @@ def test_decode_stream_error_at_every_boundary_position(b64):
             _, rerr, rst = oracle.decode(t)
             got, (err, st, olen) = _dec_stream(b64, t, std, [cut, text.size - cut])
             assert (err, st) == (rerr, rst) == (p, oracle.ST_BADCHAR), (cut, p)
+
+
+# ------------------------------------------------------------------ lenient decode (R16)
+
+def _noncanonical_texts(chars, pad, n_list=(1, 2, 4, 5, 700, 3000, 200_000, 600_001)):
+    """Valid texts whose final quad is 'xx==' / 'xxx=' with NON-zero trailing bits (strict
+    rejects them as NONCANON at m-3 / m-2; lenient drops the bits), plus their canonical form."""
+    out = []
+    for n in n_list:
+        t = oracle.encode(synth.data(n, seed=n), chars, pad)
+        out.append(t)
+        if n % 3:
+            u = t.copy()
+            k = t.size - (3 if n % 3 == 1 else 2)       # the char before the padding
+            v = chars.index(bytes([u[k]]))
+            u[k] = chars[v | (1 if n % 3 == 2 else 5)]  # set dropped low bits
+            out.append(u)
+    return out
+
+
+def test_lenient_decode_all_paths_vs_oracle(b64):
+    """B64_ALPHA_LENIENT honoured by every decode entry point: single call (small cluster and
+    bulk paths), misaligned generic, chunk API, group, batch, stream, unpadded, whitespace."""
+    al = _alphabets(b64)
+    for ai in (0, 1, 3):
+        chars, pad, strict_a = al[ai]
+        len_a = b64.lenient_of(strict_a)
+        texts = _noncanonical_texts(chars, pad)
+        for t in texts:
+            ref, rerr, rst = oracle.decode(t, chars, pad, lenient=True)
+            sref = oracle.decode(t, chars, pad)
+            for oi, oo in ((0, 0), (1, 3)):
+                assert dec_check_lenient(b64, t, ref, rerr, rst, len_a, oi, oo)
+            # strict alphabet still strict
+            out, info = b64.decode_async(to_dev(t), strict_a)
+            assert tuple(info.tolist()[:2]) == (sref[1], sref[2])
+            # chunk API as 3 shards (+ finalize)
+            if t.size >= 12:
+                cut = (t.size // 3) // 4 * 4
+                dt = to_dev(t)
+                cell = torch.full((1,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+                o = torch.empty(3 * (t.size // 4) + 3, dtype=torch.uint8, device=DEV)
+                b64.decode_chunk(dt[:cut], 0, False, cell, len_a, out=o[: 3 * cut // 4])
+                b64.decode_chunk(dt[cut:], cut, True, cell, len_a, out=o[3 * cut // 4:])
+                eo = torch.empty(1, dtype=torch.int64, device=DEV)
+                b64.decode_finalize(cell, eo)
+                assert int(eo.item()) == rerr
+                if rerr < 0:
+                    assert np.array_equal(o[: ref.size].cpu().numpy(), ref)
+            # streaming
+            got, (err, st, olen) = _dec_stream(b64, t, len_a, [t.size // 2, t.size - t.size // 2])
+            assert (err, st, olen) == (rerr, rst, ref.size) and np.array_equal(got[:olen], ref)
+            # unpadded (the same text with its '=' removed)
+            bare = t[: t.size - int((t[-2:] == pad).sum())] if t.size else t
+            uref = oracle.decode_unpadded(bare, chars, pad, lenient=True)
+            if bare.size % 4 != 1:
+                uo, uerr = b64.decode_unpadded(to_dev(bare), len_a)
+                assert uerr == uref[1] and np.array_equal(uo.cpu().numpy(), uref[0])
+            # whitespace-skipping
+            if t.size:
+                wt = np.concatenate([t[:1], np.frombuffer(b"\r\n", np.uint8), t[1:]])
+                wref = oracle.decode_ws(wt, chars, pad, lenient=True)
+                wo, werr = b64.decode_ws(to_dev(wt), len_a)
+                assert werr == wref[1] and np.array_equal(wo.cpu().numpy(), wref[0])
+        # group and batch over all texts at once
+        douts, err, st = b64.decode_group([to_dev(t) for t in texts], len_a)
+        errc, stc = err.cpu().numpy(), st.cpu().numpy()
+        lens = np.array([t.size for t in texts], dtype=np.int64)
+        in_off = np.zeros(len(texts) + 1, dtype=np.int64)
+        np.cumsum(lens, out=in_off[1:])
+        cat = np.concatenate(texts)
+        bo, boff, bst, berr, bolen = b64.decode_batch(to_dev(cat), torch.from_numpy(in_off).to(DEV), len_a)
+        bst, berr, bolen, boff = bst.cpu().numpy(), berr.cpu().numpy(), bolen.cpu().numpy(), boff.cpu().numpy()
+        bo = bo.cpu().numpy()
+        for i, t in enumerate(texts):
+            ref, rerr, rst = oracle.decode(t, chars, pad, lenient=True)
+            assert (errc[i], stc[i]) == (rerr, rst), i
+            assert np.array_equal(douts[i][: ref.size].cpu().numpy(), ref), i
+            assert (berr[i], bst[i], bolen[i]) == (rerr, rst, ref.size), i
+            assert np.array_equal(bo[boff[i]: boff[i] + ref.size], ref), i
+
+
+def dec_check_lenient(b64, text, ref, rerr, rst, alpha, off_in, off_out):
+    t = to_dev(text, off_in)
+    cap = 3 * (text.size // 4)
+    obuf = torch.empty(cap + off_out + 64, dtype=torch.uint8, device=DEV)
+    out, info = b64.decode_async(t, alpha, out=obuf[off_out: off_out + max(cap, 1)])
+    err, st, olen = info.tolist()
+    assert (err, st, olen) == (rerr, rst, ref.size), (text.size, err, st, rerr, rst)
+    assert np.array_equal(out[:olen].cpu().numpy(), ref)
+    return True
+
+
+def test_lenient_every_byte_final_quad(b64):
+    """Every byte value at each final-quad position of 'xxxx' / 'xx==' / 'xxx=' texts with a
+    lenient alphabet (the single-launch small path) vs the lenient oracle."""
+    len_a = b64.lenient_of(b64.standard())
+    for raw_len in (30, 31, 32):
+        text = oracle.encode(synth.data(raw_len, seed=raw_len))
+        for p in range(text.size - 4, text.size):
+            for v in range(256):
+                t = text.copy()
+                t[p] = v
+                ref, rerr, rst = oracle.decode(t, lenient=True)
+                dec_check_lenient(b64, t, ref, rerr, rst, len_a, 0, 0)
