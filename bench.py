@@ -204,12 +204,26 @@ def run_ours(args):
         dec_calls.append((V(c.text.data_ptr()), c.m, V(c.dec_out.data_ptr()), ap, c.c0, 1 if c.last else 0,
                           V(cells[i:].data_ptr()), None, sp))
         fin_calls.append((V(cells[i:].data_ptr()), V(err_off[i:].data_ptr()), V(status[i:].data_ptr()), sp))
-    allreduce = None
+    # N > 1: the first-error combine (one NCCL all_reduce(MIN) of the 6 packed words) runs on a
+    # side stream as soon as the decodes are done and overlaps the step's encodes (independent
+    # work); the main stream joins it before the step ends.  N = 1: no collective.
+    combine_begin = combine_end = None
     if world > 1:
         import torch.distributed as dist
 
-        def allreduce():
-            dist.all_reduce(cells, op=dist.ReduceOp.MIN)
+        comm = torch.cuda.Stream(device=dev)
+        ev_dec, ev_comm = torch.cuda.Event(), torch.cuda.Event()
+
+        def combine_begin(finalize):
+            ev_dec.record(stream)
+            comm.wait_event(ev_dec)
+            with torch.cuda.stream(comm):
+                dist.all_reduce(cells, op=dist.ReduceOp.MIN)
+                finalize(V(comm.cuda_stream))
+            ev_comm.record(comm)
+
+        def combine_end():
+            stream.wait_event(ev_comm)
 
     enc_g, dec_g, fin_n = L.b64_encode_group, L.b64_decode_group, L.b64_decode_finalize_n
     enc_f, dec_f, fin_f = L.b64_encode, L.b64_decode_chunk, L.b64_decode_finalize
@@ -231,28 +245,37 @@ def run_ours(args):
         return rc
 
     def step_group(rec):
-        """One step, grouped: ONE encode launch for the 6 cases, ONE decode launch, one finalize."""
+        """One step, grouped: ONE decode launch for the 6 cases, ONE encode launch, one finalize
+        (the decodes go first so that at N > 1 the error combine overlaps the encodes)."""
         cells.fill_(b64.ERR_NONE)
-        rc = timed("enc", rec, enc_g, enc_items, k, sp)
-        rc |= timed("dec", rec, dec_g, dec_items, k, sp)
+        rc = timed("dec", rec, dec_g, dec_items, k, sp)
+        if combine_begin is not None:
+            combine_begin(lambda s_: fin_n(cells_p, k, err_p, st_p, s_))
+        rc |= timed("enc", rec, enc_g, enc_items, k, sp)
         if rc:
             raise RuntimeError(f"C ABI returned {rc}")
-        if allreduce is not None:
-            allreduce()
-        fin_n(cells_p, k, err_p, st_p, sp)
+        if combine_end is not None:
+            combine_end()
+        else:
+            fin_n(cells_p, k, err_p, st_p, sp)
 
     def step_per_call(rec):
         """One step, one C-ABI call (one launch) per op."""
         cells.fill_(b64.ERR_NONE)
+        rc = 0
         for i in range(k):
-            rc = timed("enc", rec, enc_f, *enc_calls[i])
             rc |= timed("dec", rec, dec_f, *dec_calls[i])
-            if rc:
-                raise RuntimeError(f"C ABI returned {rc}")
-        if allreduce is not None:
-            allreduce()
+        fins = lambda s_: [fin_f(*(fin_calls[i][:3] + (s_,))) for i in range(k)]  # noqa: E731
+        if combine_begin is not None:
+            combine_begin(fins)
         for i in range(k):
-            fin_f(*fin_calls[i])
+            rc |= timed("enc", rec, enc_f, *enc_calls[i])
+        if rc:
+            raise RuntimeError(f"C ABI returned {rc}")
+        if combine_end is not None:
+            combine_end()
+        else:
+            fins(sp)
 
     def run(step, nsteps, nwarm):
         for i in range(nwarm):
