@@ -382,6 +382,18 @@ def run_ours(args):
             traffic = json.load(open(tp)).get(kname)
         except Exception:  # noqa: BLE001
             traffic = None
+    # context: what a pure streaming kernel with the same read:write mix reaches on B200
+    # (profiles/mix_probe.json, tools/mix_probe.cu) -- writes are the slow side of HBM3e
+    mix_ceiling = None
+    mp = os.path.join(ROOT, "profiles", "mix_probe.json")
+    if os.path.exists(mp):
+        try:
+            best = json.load(open(mp))["best_gbs"]
+            mk = "dec_4_3" if dom == "decode" else "enc_3_4"
+            mix_ceiling = {"mix": mk, "gbs": best[mk], "frac": round(ach / best[mk], 4),
+                           "source": "profiles/mix_probe.json (tools/mix_probe.cu, same-mix pure streaming kernel)"}
+        except Exception:  # noqa: BLE001
+            mix_ceiling = None
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -402,7 +414,7 @@ def run_ours(args):
         "per_call": per_call,
         "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                     "traffic": traffic, "peak_source": peak_src,
+                     "traffic": traffic, "peak_source": peak_src, "mix_ceiling": mix_ceiling,
                      "alg_bytes_per_launch": int(dec_alg if dom == "decode" else enc_alg),
                      "avg_launch_ms": round(dec_avg if dom == "decode" else enc_avg, 5),
                      "other": {"kernel": "enc_group_kernel" if dom == "decode" else "dec_group_kernel",
