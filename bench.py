@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--no-extra", action="store_true", help="skip the configs 1/3/4 side measurements")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (profiling runs)")
     p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-chunk-mib", type=int, default=64, help="host pipeline chunk (MiB of input per chunk)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
     return p.parse_args()
@@ -442,7 +443,7 @@ def e2e(b64, synth, torch, dev, args, cases):
     encodes and decodes each case from host memory with b64.HostPipeline
     (b64_encode_host / b64_decode_host: chunked H2D copy, kernel and D2H copy
     overlapped on three streams), so the PCIe transfers are inside the timing."""
-    pipe = b64.HostPipeline(chunk_bytes=16 << 20)
+    pipe = b64.HostPipeline(chunk_bytes=args.e2e_chunk_mib << 20)
     hx = [torch.empty(c.n, dtype=torch.uint8, pin_memory=True) for c in cases]
     ht = [torch.empty(c.m, dtype=torch.uint8, pin_memory=True) for c in cases]
     hx_out = [torch.empty(c.m, dtype=torch.uint8, pin_memory=True) for c in cases]
@@ -466,11 +467,13 @@ def e2e(b64, synth, torch, dev, args, cases):
             pipe.decode(ht[i], c.alpha, out=ht_out[i], sync=False)
 
     one()
+    pipe.join()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.e2e_steps):
         one()
+    pipe.join()
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.e2e_steps
@@ -503,8 +506,8 @@ def e2e(b64, synth, torch, dev, args, cases):
     return {"value": round(b64_bytes / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
             "link": link,
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "steps": args.e2e_steps,
-            "path": "pinned host buffers -> b64.HostPipeline (b64_encode_host / b64_decode_host: 16 MiB chunks, "
-                    "H2D copy + kernel + D2H copy overlapped on 3 streams)"}
+            "path": f"pinned host buffers -> b64.HostPipeline (b64_encode_host / b64_decode_host: "
+                    f"{args.e2e_chunk_mib} MiB chunks, H2D copy + kernel + D2H copy overlapped on 3 streams)"}
 
 
 def extra_configs(b64, synth, torch, dev, stream, flush, Ev):

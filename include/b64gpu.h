@@ -275,6 +275,19 @@ int b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, const b64_al
 int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, const b64_alphabet *a, uint8_t *d_ws,
                     int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, b64_stream_t s_h2d,
                     b64_stream_t s_comp, b64_stream_t s_d2h);
+/* The same with flags.  B64_HOST_CALLER_ORDERED: the caller guarantees that
+ * no earlier work still uses d_ws (e.g. it alternates two workspaces and makes
+ * s_h2d wait for the end of the call before last that used this one), so the
+ * call does not wait for the work already queued on s_comp / s_d2h -- back-to-
+ * back calls then overlap (one call's last chunks with the next call's first
+ * copies: both PCIe directions stay busy across calls). */
+#define B64_HOST_CALLER_ORDERED 1u
+int b64_encode_host_ex(const uint8_t *h_in, int64_t n, uint8_t *h_out, const b64_alphabet *a, uint8_t *d_ws,
+                       int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h,
+                       unsigned flags);
+int b64_decode_host_ex(const uint8_t *h_in, int64_t m, uint8_t *h_out, const b64_alphabet *a, uint8_t *d_ws,
+                       int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, b64_stream_t s_h2d,
+                       b64_stream_t s_comp, b64_stream_t s_d2h, unsigned flags);
 
 /* ---- batched (BASELINE.json configs[3]) ------------------------------------ */
 /* `count` independent strings concatenated in d_in; string i is

@@ -347,23 +347,51 @@ class DecodeStream:
 # ------------------------------------------------------------------ host buffers (overlapped pipeline)
 
 class HostPipeline:
-    """Device workspace + three streams for b64_encode_host / b64_decode_host.
+    """Device workspaces + three streams for b64_encode_host / b64_decode_host.
 
     Chunks of a host buffer rotate through 3 device buffers: H2D copy, kernel
-    and D2H copy of consecutive chunks overlap (both PCIe directions busy)."""
+    and D2H copy of consecutive chunks overlap (both PCIe directions busy).
+    Calls alternate between two workspaces and are issued with
+    B64_HOST_CALLER_ORDERED: a call only waits (on its H2D stream) for the end
+    of the call before last -- the previous user of its workspace -- so
+    back-to-back sync=False calls overlap each other too.  join() makes the
+    current stream wait for everything issued; sync=True calls join and
+    synchronise."""
 
     def __init__(self, chunk_bytes: int = 16 << 20, device=None):
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.device = dev
         self.ws_bytes = int(_lib.lib().b64_host_workspace_bytes(chunk_bytes))
-        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.ws = [torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.done = [None, None]  # event at the end of the last call on each workspace
+        self.turn = 0
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
         self.info = torch.zeros(2, dtype=torch.int64, device=dev)
 
     def _sp(self):
         return [ctypes.c_void_p(s.cuda_stream) for s in self.streams]
 
-    def _join(self):
+    def _begin(self):
+        """Order a new call: after the caller's queued work, and after the previous user of the
+        workspace it gets.  Returns the workspace."""
+        w = self.turn
+        self.turn ^= 1
+        cur = torch.cuda.current_stream(self.device)
+        for s in self.streams:
+            s.wait_stream(cur)
+        if self.done[w] is not None:
+            self.streams[0].wait_event(self.done[w])
+        return w
+
+    def _end(self, w):
+        # the D2H stream's last copy waited for the kernels, which waited for the H2D copies; it
+        # also waits for the rest of the compute stream (the decode finalize) before the mark
+        self.streams[2].wait_stream(self.streams[1])
+        ev = torch.cuda.Event()
+        ev.record(self.streams[2])
+        self.done[w] = ev
+
+    def join(self):
         cur = torch.cuda.current_stream(self.device)
         for s in self.streams:
             cur.wait_stream(s)
@@ -375,18 +403,20 @@ class HostPipeline:
         m = encoded_len(x.numel())
         if out is None:
             out = torch.empty(m, dtype=torch.uint8, pin_memory=True)
-        for s in self.streams:
-            s.wait_stream(torch.cuda.current_stream(self.device))
-        _lib.check(_lib.lib().b64_encode_host(_ptr(x), x.numel(), _ptr(out), _alpha(a), _ptr(self.ws), self.ws_bytes,
-                                              *self._sp()), "b64_encode_host")
-        self._join()
+        w = self._begin()
+        _lib.check(_lib.lib().b64_encode_host_ex(_ptr(x), x.numel(), _ptr(out), _alpha(a), _ptr(self.ws[w]),
+                                                 self.ws_bytes, *self._sp(), _lib.HOST_CALLER_ORDERED),
+                   "b64_encode_host_ex")
+        self._end(w)
         if sync:
+            self.join()
             torch.cuda.current_stream(self.device).synchronize()
         return out[:m]
 
     def decode(self, t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
-               sync: bool = True):
-        """Returns (host bytes, err_off) when sync, else (host buffer, device info int64[2] = err, status)."""
+               sync: bool = True, info: Optional[torch.Tensor] = None):
+        """Returns (host bytes, err_off) when sync, else (host buffer, device info int64[2] = err, status;
+        a fresh one per call unless `info` is given -- overlapped calls must not share it)."""
         if t.is_cuda or t.dtype != torch.uint8 or not t.is_contiguous():
             raise B64Error("t must be a contiguous uint8 host tensor (pinned for overlap)")
         m = t.numel()
@@ -394,16 +424,20 @@ class HostPipeline:
             raise B64Error("B64_ELENGTH: text length is not a multiple of 4")
         if out is None:
             out = torch.empty(max(3 * (m // 4), 1), dtype=torch.uint8, pin_memory=True)
-        for s in self.streams:
-            s.wait_stream(torch.cuda.current_stream(self.device))
-        self.info[1].zero_()
-        st = self.info[1:2].view(torch.int32)[:1]
-        _lib.check(_lib.lib().b64_decode_host(_ptr(t), m, _ptr(out), _alpha(a), _ptr(self.ws), self.ws_bytes,
-                                              _ptr(self.info[0:1]), _ptr(st), *self._sp()), "b64_decode_host")
-        self._join()
+        if info is None:
+            info = self.info if sync else torch.zeros(2, dtype=torch.int64, device=self.device)
+        w = self._begin()
+        with torch.cuda.stream(self.streams[1]):
+            info[1].zero_()
+        st = info[1:2].view(torch.int32)[:1]
+        _lib.check(_lib.lib().b64_decode_host_ex(_ptr(t), m, _ptr(out), _alpha(a), _ptr(self.ws[w]), self.ws_bytes,
+                                                 _ptr(info[0:1]), _ptr(st), *self._sp(), _lib.HOST_CALLER_ORDERED),
+                   "b64_decode_host_ex")
+        self._end(w)
         if not sync:
-            return out, self.info
-        err = int(self.info[0].item())
+            return out, info
+        self.join()
+        err = int(info[0].item())
         if err < 0:
             pads = (2 if m >= 4 and int(t[m - 2]) == (a or standard()).pad else
                     (1 if m >= 4 and int(t[m - 1]) == (a or standard()).pad else 0))

@@ -37,6 +37,7 @@ P, I64, I32, INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
 
 
 ALPHA_LENIENT = 1  # B64_ALPHA_LENIENT
+HOST_CALLER_ORDERED = 1  # B64_HOST_CALLER_ORDERED
 
 
 class Alphabet(ctypes.Structure):
@@ -92,6 +93,8 @@ SIGNATURES = [
     ("b64_host_workspace_bytes", I64, [I64]),
     ("b64_encode_host", INT, [P, I64, P, AP, P, I64, P, P, P]),
     ("b64_decode_host", INT, [P, I64, P, AP, P, I64, P, P, P, P, P]),
+    ("b64_encode_host_ex", INT, [P, I64, P, AP, P, I64, P, P, P, ctypes.c_uint]),
+    ("b64_decode_host_ex", INT, [P, I64, P, AP, P, I64, P, P, P, P, P, ctypes.c_uint]),
     ("b64_encode_batch", INT, [P, P, I64, P, P, AP, P]),
     ("b64_decode_batch", INT, [P, P, I64, P, P, AP, P, P, P, P]),
     ("b64_launch_count", I64, []),

@@ -599,7 +599,13 @@ int64_t b64_host_workspace_bytes(int64_t chunk_bytes) {
 
 int b64_encode_host(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
                     int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h) {
-    if (n < 0 || !alpha_ok(a)) return B64_EINVAL;
+    return b64_encode_host_ex(h_in, n, h_out, a, d_ws, ws_bytes, s_h2d, s_comp, s_d2h, 0u);
+}
+
+int b64_encode_host_ex(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
+                       int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h,
+                       unsigned flags) {
+    if (n < 0 || !alpha_ok(a) || (flags & ~unsigned(B64_HOST_CALLER_ORDERED))) return B64_EINVAL;
     if (n == 0) return B64_OK;
     if (!h_in || !h_out || !d_ws) return B64_EINVAL;
     // per buffer: C input bytes + 4C/3 output chars; C a multiple of 3072 (= 4 * 768, keeps both aligned)
@@ -610,7 +616,8 @@ int b64_encode_host(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_al
     cudaStream_t sh = reinterpret_cast<cudaStream_t>(s_h2d), sc = reinterpret_cast<cudaStream_t>(s_comp),
                  sd = reinterpret_cast<cudaStream_t>(s_d2h);
     HostPipe pipe;
-    if (!pipe.ok || pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
+    if (!pipe.ok) return B64_ECUDA;
+    if (!(flags & B64_HOST_CALLER_ORDERED) && pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
     const int64_t stride = C + C / 3 * 4 + 512;
     int64_t j = 0;
     for (int64_t off = 0; off < n; off += C, ++j) {
@@ -637,7 +644,13 @@ int b64_encode_host(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_al
 int b64_decode_host(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
                     int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, b64_stream_t s_h2d,
                     b64_stream_t s_comp, b64_stream_t s_d2h) {
-    if (m < 0 || !alpha_ok(a) || !d_err_off) return B64_EINVAL;
+    return b64_decode_host_ex(h_in, m, h_out, a, d_ws, ws_bytes, d_err_off, d_status, s_h2d, s_comp, s_d2h, 0u);
+}
+
+int b64_decode_host_ex(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
+                       int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, b64_stream_t s_h2d,
+                       b64_stream_t s_comp, b64_stream_t s_d2h, unsigned flags) {
+    if (m < 0 || !alpha_ok(a) || !d_err_off || (flags & ~unsigned(B64_HOST_CALLER_ORDERED))) return B64_EINVAL;
     if (m % 4) return B64_ELENGTH;
     if (m > 0 && (!h_in || !h_out || !d_ws)) return B64_EINVAL;
     cudaStream_t sh = reinterpret_cast<cudaStream_t>(s_h2d), sc = reinterpret_cast<cudaStream_t>(s_comp),
@@ -653,7 +666,8 @@ int b64_decode_host(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_al
     if (C <= 0) return B64_EINVAL;
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
     HostPipe pipe;
-    if (!pipe.ok || pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
+    if (!pipe.ok) return B64_ECUDA;
+    if (!(flags & B64_HOST_CALLER_ORDERED) && pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
     if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), sc) != cudaSuccess) return B64_ECUDA;
     const int64_t stride = C + C / 4 * 3 + 512;
     int64_t j = 0;

@@ -446,6 +446,41 @@ def test_host_pipeline_vs_oracle(b64):
                 assert np.array_equal(y.numpy(), rref)
 
 
+def test_host_pipeline_overlapped_calls(b64):
+    """Back-to-back sync=False host calls (two workspaces, B64_HOST_CALLER_ORDERED): calls
+    overlap each other; every output and error word must still match the oracle."""
+    pipe = b64.HostPipeline(chunk_bytes=3072 * 7)
+    jobs = []
+    for i, n in enumerate((100_003, 5, 3072 * 7 * 3 + 11, 64_000, 0, 250_001, 3)):
+        chars, alpha = ((oracle.STANDARD, b64.standard()), (oracle.URL, b64.url()))[i % 2]
+        x = synth.data(n, seed=700 + i)
+        ref = oracle.encode(x, chars)
+        t2 = ref.copy()
+        if ref.size > 8 and i % 2 == 0:
+            pos, bad = synth.corruption(2, ref.size, chars, seed=i)
+            t2[pos] = bad
+        xh = torch.from_numpy(x).pin_memory()
+        th = torch.from_numpy(t2).pin_memory()
+        eo = torch.empty(max(ref.size, 1), dtype=torch.uint8).pin_memory()
+        do = torch.empty(max(3 * (ref.size // 4), 1), dtype=torch.uint8).pin_memory()
+        jobs.append((chars, x, ref, t2, xh, th, eo, do, alpha))
+    results = []
+    for rep in range(2):
+        for chars, x, ref, t2, xh, th, eo, do, alpha in jobs:
+            te = pipe.encode(xh, alpha, out=eo, sync=False)
+            yo, info = pipe.decode(th, alpha, out=do, sync=False)
+            results.append((te, yo, info))
+    pipe.join()
+    torch.cuda.synchronize()
+    for k, (te, yo, info) in enumerate(results):
+        chars, x, ref, t2, *_ = jobs[k % len(jobs)]
+        assert np.array_equal(te.numpy()[: ref.size], ref), k
+        rref, rerr, rst = oracle.decode(t2, chars)
+        err, st = int(info[0].item()), int(info[1:2].view(torch.int32)[0].item())
+        assert (err, st) == (rerr, rst), k
+        assert np.array_equal(yo.numpy()[: rref.size], rref), k
+
+
 # ------------------------------------------------------------------ guard bands (no writes outside the output)
 
 def test_no_writes_outside_outputs(b64):
