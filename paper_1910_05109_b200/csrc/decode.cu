@@ -241,9 +241,76 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
 
 // ---------------------------------------------------------------- generic / batch
 
+// A short string decoded whole by one lane (dec_generic_kernel): interior
+// quads, then the final quad when `fin` (R6 / R16); the first error
+// is reported and ends the string.  Chars are read as naturally aligned
+// 4-byte words + funnel shifts (src has any alignment); output bytes are
+// gathered in a 64-bit register and written as aligned 4-byte words (one
+// store per 4 bytes instead of 3 byte stores per quad), the unaligned head
+// and tail byte by byte.
+#ifndef B64_SHORT_DEC
+#define B64_SHORT_DEC 128
+#endif
+constexpr int64_t kShortDec = B64_SHORT_DEC;  // chars
+__device__ __forceinline__ void dec_short_lane(const uint8_t* __restrict__ src, int64_t L, uint8_t* __restrict__ o,
+                                               const uint8_t* __restrict__ lut, uint32_t pad, uint32_t lenient,
+                                               bool fin, int64_t pbase, unsigned long long* cell) {
+    const int64_t Qs = L >> 2;
+    const uintptr_t su = reinterpret_cast<uintptr_t>(src);
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(su & ~uintptr_t(3));
+    const uint32_t sh = uint32_t(su & 3) * 8;
+    uint32_t w0 = ld32(sw);
+    // output: bytes before the first 4-byte boundary go one by one
+    int64_t pos = 0;                                            // output bytes emitted
+    const int head = int((4 - (reinterpret_cast<uintptr_t>(o) & 3)) & 3);
+    unsigned long long acc = 0;                                 // pending bytes, little-endian
+    int nacc = 0;
+    auto emit = [&](uint32_t v, int k) {                        // k bytes of v in stream order (v>>16, v>>8, v)
+        for (int b = 0; b < k; ++b) {
+            const uint32_t byte = (v >> (16 - 8 * b)) & 0xffu;
+            if (pos < head) {
+                o[pos++] = uint8_t(byte);
+            } else {
+                acc |= (unsigned long long)byte << (8 * nacc);
+                if (++nacc == 4) {
+                    *reinterpret_cast<uint32_t*>(o + pos) = uint32_t(acc);
+                    pos += 4;
+                    acc = 0;
+                    nacc = 0;
+                }
+            }
+        }
+    };
+    int64_t q = 0;
+    for (; q < Qs; ++q) {
+        const uint32_t w1 = (sh || q + 1 < Qs) ? ld32(sw + q + 1) : 0u;  // never past the string's last word
+        const uint32_t x = sh ? __funnelshift_r(w0, w1, sh) : w0;
+        w0 = w1;
+        if (fin && q == Qs - 1) {
+            int bad, k;
+            uint32_t v;
+            const uint32_t kind = final_quad(x, lut, pad, lenient, &bad, &k, &v);
+            if (kind == kOk) emit(v, k);
+            else atomicMin(cell, pack_err(pbase + 4 * q + bad, kind));
+            break;
+        }
+        uint32_t err = 0;
+        const uint32_t v = dec_quad(x, lut, err);
+        if (err & kInvalid) {
+            atomicMin(cell, pack_err(pbase + 4 * q + first_bad_in_quad(x, lut), kBadChar));
+            break;
+        }
+        emit(v, 3);
+    }
+    for (int b = 0; b < nacc; ++b) o[pos + b] = uint8_t(acc >> (8 * b));  // tail bytes
+}
+
 // Batch: err cell per string, positions relative to the string start.
 // Single: one cell, positions base + offset; is_final as given.
-__global__ void __launch_bounds__(kThreads)
+#ifndef B64_GEN_MINB
+#define B64_GEN_MINB 5
+#endif
+__global__ void __launch_bounds__(kThreads, B64_GEN_MINB)
 dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, DecTab tab,
                    int64_t base, int is_final_single, unsigned long long* __restrict__ err_cells,
                    int64_t* __restrict__ out_len_single) {
@@ -277,16 +344,35 @@ dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
     const int64_t hi = first + (total * (w + 1)) / W;
     if (lo >= hi) return;
 
-    for (int64_t s = first_string_ending_after(off, lo); s < off.count; ++s) {
-        const int64_t a = off.in(s);
-        if (a >= hi) break;
-        const int64_t L = off.in(s + 1) - a;
-        if (L <= 0 || (L & 3)) continue;  // empty / LENGTH: settled by the finalize kernel
-        const int64_t ob = off.out(s);
+    // Strings are visited 32 at a time (lane i holds string s0 + i's offsets): a short string
+    // (<= kShortDec chars) is decoded whole by its own lane -- by the warp whose range holds
+    // its first char -- and the longer ones one after the other by the whole warp (every
+    // unit whose first char lies in [lo, hi)).  Empty strings and len % 4 != 0 (LENGTH) are
+    // settled by the finalize kernel.
+    const bool fin = batch ? true : (is_final_single != 0);
+    const int64_t pbase = batch ? 0 : base;  // reported position = pbase + (char index in string)
+    for (int64_t s0 = first_string_ending_after(off, lo); s0 < off.count; s0 += 32) {
+      const int64_t si = s0 + lane;
+      const bool valid = si < off.count;
+      int64_t ai = 0, Li = 0, obi = 0;
+      if (valid) {
+          ai = off.in(si);
+          Li = off.in(si + 1) - ai;
+          obi = off.out(si);
+      }
+      const bool started = valid && ai < hi;  // strings from hi on belong to later warps
+      const bool ok_len = Li > 0 && (Li & 3) == 0;
+      if (started && ok_len && Li <= kShortDec && ai >= lo)
+          dec_short_lane(in + ai, Li, out + obi, lut, tab.pad, tab.lenient, fin, pbase,
+                         batch ? err_cells + si : err_cells);
+      for (uint32_t longs = __ballot_sync(kFull, started && ok_len && Li > kShortDec); longs; longs &= longs - 1) {
+        const int jl = __ffs(longs) - 1;
+        const int64_t s = s0 + jl;
+        const int64_t a = __shfl_sync(kFull, ai, jl);
+        const int64_t L = __shfl_sync(kFull, Li, jl);
+        const int64_t ob = __shfl_sync(kFull, obi, jl);
         uint8_t* o = out + ob;
-        const bool fin = batch ? true : (is_final_single != 0);
         unsigned long long* cell = batch ? err_cells + s : err_cells;
-        const int64_t pbase = batch ? 0 : base;  // reported position = pbase + (char index in string)
         const int64_t Qs = L >> 2;
         const int64_t Qint = fin ? Qs - 1 : Qs;
         // h head quads make the unit outputs 8-byte aligned: 3h == -o (mod 8), 3^-1 == 3 (mod 8)
@@ -351,6 +437,8 @@ dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
                 }
             }
         }
+      }
+      if (__any_sync(kFull, !started)) break;  // a string at or after hi (or the end): done
     }
 }
 

@@ -211,6 +211,37 @@ __device__ __forceinline__ void enc_string_unaligned_out(const uint8_t* __restri
     }
 }
 
+// A short string encoded whole by one lane (enc_generic_kernel): plain triples
+// then the padded tail, 4-byte stores when the output is 4-byte aligned
+// (always, in a batch).
+#ifndef B64_SHORT_ENC
+#define B64_SHORT_ENC 96
+#endif
+constexpr int64_t kShortEnc = B64_SHORT_ENC;  // bytes
+__device__ __forceinline__ void enc_short_lane(const uint8_t* __restrict__ src, int64_t L, uint8_t* __restrict__ o,
+                                               const uint8_t* __restrict__ lut, uint32_t pad) {
+    const int64_t T = L / 3;
+    const int r = int(L - 3 * T);
+    const bool al = (reinterpret_cast<uintptr_t>(o) & 3) == 0;
+    for (int64_t t = 0; t <= T; ++t) {
+        uint32_t word;
+        if (t < T) {
+            word = enc_triple((uint32_t(src[3 * t]) << 24) | (uint32_t(src[3 * t + 1]) << 16) |
+                              (uint32_t(src[3 * t + 2]) << 8), lut);
+        } else if (r) {
+            word = enc_partial(src[3 * t], r == 2 ? src[3 * t + 1] : 0u, r, lut, pad);
+        } else {
+            break;
+        }
+        if (al) {
+            *reinterpret_cast<uint32_t*>(o + 4 * t) = word;
+        } else {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) o[4 * t + b] = uint8_t(word >> (8 * b));
+        }
+    }
+}
+
 // Any alignment, one stream or a batch.  The concatenated input is cut into
 // equal byte ranges, one per warp; a warp owns every work item whose first
 // input byte lies in its range.  Per string with a 4-byte-aligned output
@@ -242,17 +273,31 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
     const int64_t hi = base + (total * (w + 1)) / W;
     if (lo >= hi) return;
 
-    for (int64_t s = first_string_ending_after(off, lo); s < off.count; ++s) {
-        const int64_t a = off.in(s);
-        if (a >= hi) break;
-        const int64_t L = off.in(s + 1) - a;
-        if (L <= 0) continue;
-        const int64_t ob = off.out(s);
+    // Strings are visited 32 at a time (lane i holds string s0 + i's offsets): a short string
+    // (<= kShortEnc bytes) is encoded whole by its own lane -- by the warp whose range holds
+    // its first byte -- and the longer ones one after the other by the whole warp (every
+    // unit whose first byte lies in [lo, hi)).
+    for (int64_t s0 = first_string_ending_after(off, lo); s0 < off.count; s0 += 32) {
+      const int64_t si = s0 + lane;
+      const bool valid = si < off.count;
+      int64_t ai = 0, Li = 0, obi = 0;
+      if (valid) {
+          ai = off.in(si);
+          Li = off.in(si + 1) - ai;
+          obi = off.out(si);
+      }
+      const bool started = valid && ai < hi;  // strings from hi on belong to later warps
+      if (started && Li > 0 && Li <= kShortEnc && ai >= lo) enc_short_lane(in + ai, Li, out + obi, lut, pad);
+      for (uint32_t longs = __ballot_sync(kFull, started && Li > kShortEnc); longs; longs &= longs - 1) {
+        const int jl = __ffs(longs) - 1;
+        const int64_t a = __shfl_sync(kFull, ai, jl);
+        const int64_t L = __shfl_sync(kFull, Li, jl);
+        const int64_t ob = __shfl_sync(kFull, obi, jl);
         uint8_t* o = out + ob;
         const uintptr_t oa = reinterpret_cast<uintptr_t>(o);
         if (oa & 3) {
             enc_string_unaligned_out(in, out, a, L, ob, lo, hi, lane, lut, pad);
-            continue;
+            continue;  // next long string
         }
         const int64_t T = L / 3;
         const int r = int(L - 3 * T);
@@ -285,6 +330,8 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
                 *reinterpret_cast<uint32_t*>(o + 4 * j) = word;
             }
         }
+      }
+      if (__any_sync(kFull, !started)) break;  // a string at or after hi (or the end): done
     }
 }
 
