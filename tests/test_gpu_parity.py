@@ -258,6 +258,42 @@ def test_batch_encode_decode_vs_oracle(b64):
             assert np.array_equal(o[rooff[i]: rooff[i] + rolen[i]], rout[rooff[i]: rooff[i] + rolen[i]]), i
 
 
+def test_batch_many_short_strings(b64):
+    """200k strings of 0..140 bytes (the lane-per-string path and its hand-over to the warp path
+    at the thresholds, strings straddling warp ranges), ~5 % corrupted anywhere (interior and
+    final-quad chars, '=' misplaced), a few LENGTH errors; strict and lenient alphabets."""
+    count = 200_000
+    L = (synth.words(77, 3, 0, count) % np.uint64(141)).astype(np.int64)
+    off = synth.offsets(L)
+    x = synth.data(int(off[-1]), seed=77)
+    doff = torch.from_numpy(off).to(DEV)
+    enc, eoff = b64.encode_batch(to_dev(x, 1), doff)  # misaligned input base too
+    renc, reoff = oracle.encode_batch(x, off)
+    assert np.array_equal(eoff.cpu().numpy(), reoff)
+    assert np.array_equal(enc[: reoff[-1]].cpu().numpy(), renc)
+    text = renc.copy()
+    tl = np.diff(reoff)
+    picks = synth.pick(count, 0.05, seed=78)
+    w = synth.words(79, 3, 0, len(picks))
+    for k, i in enumerate(picks):
+        if tl[i]:
+            p = int(w[k] % np.uint64(tl[i]))
+            text[reoff[i] + p] = (ord("="), ord("*"), 0xC3)[k % 3]
+    din = reoff.copy()
+    for i in range(5, count, 997):  # shift some boundaries: LENGTH errors on both sides
+        if din[i] + 1 <= din[i + 1]:  # offsets stay non-decreasing (the API's precondition)
+            din[i] += 1
+    for alpha, lenient in ((b64.standard(), False), (b64.lenient_of(b64.standard()), True)):
+        out, ooff, st, err, olen = b64.decode_batch(to_dev(text, 3), torch.from_numpy(din).to(DEV), alpha)
+        rout, rooff, rst, rerr, rolen = oracle.decode_batch(text, din, lenient=lenient)
+        assert np.array_equal(st.cpu().numpy(), rst)
+        assert np.array_equal(err.cpu().numpy(), rerr)
+        assert np.array_equal(olen.cpu().numpy(), rolen)
+        o = out.cpu().numpy()
+        for i in np.flatnonzero(rolen):
+            assert np.array_equal(o[rooff[i]: rooff[i] + rolen[i]], rout[rooff[i]: rooff[i] + rolen[i]]), i
+
+
 def test_batch_misaligned_offsets(b64):
     """String starts at every alignment: input offsets shifted by a 1..3 byte prefix gap."""
     for gap in (1, 2, 3):
