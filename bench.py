@@ -51,6 +51,10 @@ def parse():
     p.add_argument("--e2e-chunk-mib", type=int, default=64, help="host pipeline chunk (MiB of input per chunk)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
+    p.add_argument("--combine", choices=("nccl", "peer"), default="nccl",
+                   help="N>1 first-error combine: NCCL all_reduce(MIN) (default) or the one-sided peer-memory "
+                        "kernel (dist.PeerCombine, SURVEY 8(f) f4; 'peer' also runs it at N=1).  Never run "
+                        "'peer' with several ranks on ONE GPU: its kernels wait on each other")
     return p.parse_args()
 
 
@@ -208,23 +212,31 @@ def run_ours(args):
     # N > 1: the first-error combine (one NCCL all_reduce(MIN) of the 6 packed words) runs on a
     # side stream as soon as the decodes are done and overlaps the step's encodes (independent
     # work); the main stream joins it before the step ends.  N = 1: no collective.
-    combine_begin = combine_end = None
-    if world > 1:
-        import torch.distributed as dist
+    # (At N = 1 the side stream still takes the finalize, so it overlaps the encodes too.)
+    import torch.distributed as dist
 
-        comm = torch.cuda.Stream(device=dev)
-        ev_dec, ev_comm = torch.cuda.Event(), torch.cuda.Event()
+    comm = torch.cuda.Stream(device=dev)
+    ev_dec, ev_comm = torch.cuda.Event(), torch.cuda.Event()
+    pc = None
+    if args.combine == "peer":
+        from paper_1910_05109_b200 import dist as b64dist
 
-        def combine_begin(finalize):
-            ev_dec.record(stream)
-            comm.wait_event(ev_dec)
-            with torch.cuda.stream(comm):
-                dist.all_reduce(cells, op=dist.ReduceOp.MIN)
+        pc = b64dist.PeerCombine(len(cases))
+
+    def combine_begin(finalize):
+        ev_dec.record(stream)
+        comm.wait_event(ev_dec)
+        with torch.cuda.stream(comm):
+            if pc is not None:  # one kernel: peer atomics + arrival counters + finalize
+                pc.combine(cells, err_off, status, stream=comm)
+            else:
+                if world > 1:
+                    dist.all_reduce(cells, op=dist.ReduceOp.MIN)
                 finalize(V(comm.cuda_stream))
-            ev_comm.record(comm)
+        ev_comm.record(comm)
 
-        def combine_end():
-            stream.wait_event(ev_comm)
+    def combine_end():
+        stream.wait_event(ev_comm)
 
     enc_g, dec_g, fin_n = L.b64_encode_group, L.b64_decode_group, L.b64_decode_finalize_n
     enc_f, dec_f, fin_f = L.b64_encode, L.b64_decode_chunk, L.b64_decode_finalize
@@ -247,18 +259,14 @@ def run_ours(args):
 
     def step_group(rec):
         """One step, grouped: ONE decode launch for the 6 cases, ONE encode launch, one finalize
-        (the decodes go first so that at N > 1 the error combine overlaps the encodes)."""
+        (the decodes go first so that the error combine / finalize overlaps the encodes)."""
         cells.fill_(b64.ERR_NONE)
         rc = timed("dec", rec, dec_g, dec_items, k, sp)
-        if combine_begin is not None:
-            combine_begin(lambda s_: fin_n(cells_p, k, err_p, st_p, s_))
+        combine_begin(lambda s_: fin_n(cells_p, k, err_p, st_p, s_))
         rc |= timed("enc", rec, enc_g, enc_items, k, sp)
         if rc:
             raise RuntimeError(f"C ABI returned {rc}")
-        if combine_end is not None:
-            combine_end()
-        else:
-            fin_n(cells_p, k, err_p, st_p, sp)
+        combine_end()
 
     def step_per_call(rec):
         """One step, one C-ABI call (one launch) per op."""
@@ -266,17 +274,12 @@ def run_ours(args):
         rc = 0
         for i in range(k):
             rc |= timed("dec", rec, dec_f, *dec_calls[i])
-        fins = lambda s_: [fin_f(*(fin_calls[i][:3] + (s_,))) for i in range(k)]  # noqa: E731
-        if combine_begin is not None:
-            combine_begin(fins)
+        combine_begin(lambda s_: [fin_f(*(fin_calls[i][:3] + (s_,))) for i in range(k)])
         for i in range(k):
             rc |= timed("enc", rec, enc_f, *enc_calls[i])
         if rc:
             raise RuntimeError(f"C ABI returned {rc}")
-        if combine_end is not None:
-            combine_end()
-        else:
-            fins(sp)
+        combine_end()
 
     def run(step, nsteps, nwarm):
         for i in range(nwarm):

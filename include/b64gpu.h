@@ -253,6 +253,44 @@ int b64_decode_stream_update(b64_stream *st, const uint8_t *d_in, int64_t m, uin
 int b64_decode_stream_end(b64_stream *st, uint8_t *d_out, const b64_alphabet *a, int64_t *d_err_off,
                           int32_t *d_status, int64_t *d_out_len, int64_t *n_out, b64_stream_t stream);
 
+/* ---- one-sided cross-GPU error combine ------------ */
+/* The multi-GPU decode's only exchange -- the MIN over ranks of `count` packed
+ * error words -- done by ONE small kernel over peer memory instead of an NCCL
+ * all_reduce: each rank atomicMin's its words into every rank's buffer
+ * (system scope, over NVLink), then arrives on every rank's counter and waits
+ * for all arrivals of the epoch on its own.
+ *   - Every rank owns one buffer of b64_peer_combine_bytes(count) bytes, set
+ *     up once with b64_peer_combine_init, then mapped into every other rank
+ *     (CUDA IPC); d_bufs is a DEVICE array of `world` device pointers, d_bufs[p]
+ *     = rank p's buffer as seen by the caller.  All ranks must have initialised
+ *     their buffers before any rank's first combine (e.g. a host barrier).
+ *   - epoch = number of combines this group already did (0, 1, 2, ... the same
+ *     sequence on every rank); one combine per epoch per rank.
+ *   - Output as b64_decode_finalize_n: d_err_off[k] = -1 or the global first
+ *     error position, d_status[k] (nullable) its kind.  If a peer does not
+ *     arrive within 5 s the kernel gives up: d_err_off[k] = -2, d_status = -1.
+ *   - count <= 4096, world <= 32. */
+int64_t b64_peer_combine_bytes(int64_t count);
+int b64_peer_combine_init(uint8_t *d_buf, int64_t count, b64_stream_t stream);
+int b64_peer_combine(uint8_t *const *d_bufs, int world, int rank, const int64_t *d_local, int64_t count,
+                     uint64_t epoch, int64_t *d_err_off, int32_t *d_status, b64_stream_t stream);
+/* Buffer plumbing for the combine (the one place the library allocates: an IPC
+ * handle needs a cudaMalloc base address).  b64_peer_buffer_alloc: cudaMalloc
+ * `bytes` on the current device and export its 64-byte IPC handle;
+ * b64_peer_buffer_open: map a peer's buffer from its handle (another process,
+ * peer access enabled); b64_peer_buffer_release: cudaFree (opened = 0) or
+ * close the mapping (opened = 1). */
+int b64_peer_buffer_alloc(int64_t bytes, uint8_t **d_buf, uint8_t handle[64]);
+int b64_peer_buffer_open(const uint8_t handle[64], uint8_t **d_buf);
+int b64_peer_buffer_release(uint8_t *d_buf, int opened);
+/* Test hook: `world` ranks emulated on ONE GPU by one cooperative kernel (block
+ * r = rank r; d_bufs = the world buffers on this device) running `epochs`
+ * combines: rank r contributes d_local[(e*world + r)*count + k] in epoch e and
+ * writes the MIN it sees to d_out[(e*world + r)*count + k] (packed words);
+ * *d_ok (device int, caller sets 1) becomes 0 on a timeout. */
+int b64_peer_combine_emulate(uint8_t *const *d_bufs, int world, const int64_t *d_local, int64_t count, int epochs,
+                             int64_t *d_out, int *d_ok, b64_stream_t stream);
+
 /* ---- host buffers, overlapped (SURVEY.md Sec. 8(f) f3 ingest pipeline) ------ */
 /* Encode / decode HOST buffers (h_*: host pointers, pinned for the copies to be
  * asynchronous) through a caller-owned DEVICE workspace d_ws of ws_bytes.  The

@@ -90,6 +90,13 @@ SIGNATURES = [
     ("b64_decode_stream_begin", INT, [SP, P, P, P]),
     ("b64_decode_stream_update", INT, [SP, P, I64, P, AP, I64P, P]),
     ("b64_decode_stream_end", INT, [SP, P, AP, P, P, P, I64P, P]),
+    ("b64_peer_combine_bytes", I64, [I64]),
+    ("b64_peer_combine_init", INT, [P, I64, P]),
+    ("b64_peer_combine", INT, [P, INT, INT, P, I64, ctypes.c_uint64, P, P, P]),
+    ("b64_peer_buffer_alloc", INT, [I64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p]),
+    ("b64_peer_buffer_open", INT, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
+    ("b64_peer_buffer_release", INT, [P, INT]),
+    ("b64_peer_combine_emulate", INT, [P, INT, P, I64, INT, P, P, P]),
     ("b64_host_workspace_bytes", I64, [I64]),
     ("b64_encode_host", INT, [P, I64, P, AP, P, I64, P, P, P]),
     ("b64_decode_host", INT, [P, I64, P, AP, P, I64, P, P, P, P, P]),

@@ -6,4 +6,5 @@
 #include "small.cu"
 #include "mime.cu"
 #include "stream.cu"
+#include "peer.cu"
 #include "capi.cu"

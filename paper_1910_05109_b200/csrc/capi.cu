@@ -552,6 +552,83 @@ int b64_decode_stream_end(b64_stream* st, uint8_t* d_out, const b64_alphabet* a,
     return B64_OK;
 }
 
+// ---------------------------------------------------------------- one-sided peer combine (peer.cu)
+int64_t b64_peer_combine_bytes(int64_t count) { return count < 0 ? -1 : kPeerSlotsOff + 16 * count; }
+
+int b64_peer_combine_init(uint8_t* d_buf, int64_t count, b64_stream_t stream) {
+    if (!d_buf || count < 0) return B64_EINVAL;
+    launch(peer_buffer_init_kernel, 1, kThreads, reinterpret_cast<cudaStream_t>(stream), d_buf, count);
+    return launched();
+}
+
+int b64_peer_combine(uint8_t* const* d_bufs, int world, int rank, const int64_t* d_local, int64_t count,
+                     uint64_t epoch, int64_t* d_err_off, int32_t* d_status, b64_stream_t stream) {
+    if (!d_bufs || world < 1 || world > 32 || rank < 0 || rank >= world || count < 0 || count > 4096 ||
+        (count > 0 && (!d_local || !d_err_off)))
+        return B64_EINVAL;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = size_t(count) * 8;
+    cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaLaunchKernelEx(&cfg, peer_combine_kernel, d_bufs, world, rank,
+                           reinterpret_cast<const unsigned long long*>(d_local), count,
+                           static_cast<unsigned long long>(epoch), d_err_off, d_status) != cudaSuccess)
+        return (cudaGetLastError(), B64_ECUDA);
+    return launched();
+}
+
+int b64_peer_buffer_alloc(int64_t bytes, uint8_t** d_buf, uint8_t handle[64]) {
+    if (bytes <= 0 || !d_buf || !handle) return B64_EINVAL;
+    void* p = nullptr;
+    if (cudaMalloc(&p, size_t(bytes)) != cudaSuccess) return (cudaGetLastError(), B64_ECUDA);
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+        cudaFree(p);
+        return (cudaGetLastError(), B64_ECUDA);
+    }
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle, &h, 64);
+    *d_buf = static_cast<uint8_t*>(p);
+    return B64_OK;
+}
+
+int b64_peer_buffer_open(const uint8_t handle[64], uint8_t** d_buf) {
+    if (!handle || !d_buf) return B64_EINVAL;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return (cudaGetLastError(), B64_ECUDA);
+    *d_buf = static_cast<uint8_t*>(p);
+    return B64_OK;
+}
+
+int b64_peer_buffer_release(uint8_t* d_buf, int opened) {
+    if (!d_buf) return B64_EINVAL;
+    const cudaError_t e = opened ? cudaIpcCloseMemHandle(d_buf) : cudaFree(d_buf);
+    return e == cudaSuccess ? B64_OK : (cudaGetLastError(), B64_ECUDA);
+}
+
+int b64_peer_combine_emulate(uint8_t* const* d_bufs, int world, const int64_t* d_local, int64_t count, int epochs,
+                             int64_t* d_out, int* d_ok, b64_stream_t stream) {
+    if (!d_bufs || world < 1 || world > 32 || count < 0 || epochs < 0 || !d_ok || (count > 0 && (!d_local || !d_out)))
+        return B64_EINVAL;
+    uint8_t* const* b = d_bufs;
+    int w = world;
+    const unsigned long long* l = reinterpret_cast<const unsigned long long*>(d_local);
+    int64_t k = count;
+    int e = epochs;
+    unsigned long long* o = reinterpret_cast<unsigned long long*>(d_out);
+    int* okp = d_ok;
+    void* args[] = {&b, &w, &l, &k, &e, &o, &okp};
+    // all `world` blocks wait on one another: a cooperative launch guarantees they are co-resident
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(peer_combine_emulate_kernel), dim3(world), dim3(32),
+                                    args, 0, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return (cudaGetLastError(), B64_ECUDA);
+    return launched();
+}
+
 // ---------------------------------------------------------------- host-buffer pipelines
 // Chunks of the host input are copied H2D on s_h2d, coded on s_comp and copied
 // back D2H on s_d2h through kHostBufs rotating device buffers, so both PCIe

@@ -17,6 +17,11 @@ decodes on its own, so
 The codec calls go through ``codec`` (default: the CUDA library).  Tests on
 CPU pass their own object with the same two methods to exercise the sharding
 and the MIN combine over gloo.
+
+``PeerCombine`` is the one-sided alternative to the all_reduce (SURVEY.md
+Sec. 8(f) f4): one small kernel per combine that atomicMin's the words into
+every rank's peer-mapped buffer over NVLink and meets the other ranks on
+arrival counters (b64_peer_combine).
 """
 from __future__ import annotations
 
@@ -123,3 +128,78 @@ def decode_sharded(t_local: torch.Tensor, shard: Shard, codec=None, group=None) 
         dist.all_reduce(cell, op=dist.ReduceOp.MIN, group=group)
     err, status = codec.finalize(cell)
     return out, err, status
+
+
+class PeerCombine:
+    """One-sided first-error combine over peer memory (b64_peer_combine).
+
+    Replaces decode_sharded's NCCL all_reduce(MIN) by one small kernel per combine: every
+    rank atomicMin's its packed words into every rank's buffer over NVLink and arrives on
+    every rank's counter.  Each rank allocates its buffer with
+    b64_peer_buffer_alloc, the 64-byte CUDA IPC handles are exchanged once with
+    all_gather_object (the plumbing collective), and every rank maps its peers' buffers.
+    All ranks must construct it together (collective) and then call combine() in the same
+    sequence.  world == 1 needs no IPC."""
+
+    def __init__(self, count: int, group=None, device=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self._lib = _lib
+        L = _lib.lib()
+        self.world, self.rank = _group_info(group)
+        self.count = count
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        nbytes = int(L.b64_peer_combine_bytes(count))
+        own = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        _lib.check(L.b64_peer_buffer_alloc(nbytes, ctypes.byref(own), handle), "b64_peer_buffer_alloc")
+        self._own = own.value
+        self._opened = []
+        _lib.check(L.b64_peer_combine_init(ctypes.c_void_p(self._own), count, None), "b64_peer_combine_init")
+        torch.cuda.synchronize(self.dev)
+        ptrs = [self._own]
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(handle.raw), group=group)
+            ptrs = []
+            for p, h in enumerate(handles):
+                if p == self.rank:
+                    ptrs.append(self._own)
+                    continue
+                q = ctypes.c_void_p()
+                _lib.check(L.b64_peer_buffer_open(h, ctypes.byref(q)), "b64_peer_buffer_open")
+                self._opened.append(q.value)
+                ptrs.append(q.value)
+            dist.barrier(group=group)  # every buffer is initialised before anyone's first combine
+        self.d_bufs = torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
+        self.epoch = 0
+
+    def combine(self, local: torch.Tensor, err_off: torch.Tensor, status: Optional[torch.Tensor] = None,
+                stream: Optional[torch.cuda.Stream] = None) -> None:
+        """local: int64[count] packed words of this rank -> err_off int64[count] (-1 or global first
+        error), status int32[count] (nullable), on `stream` (default: the current stream)."""
+        import ctypes
+
+        s = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        self._lib.check(self._lib.lib().b64_peer_combine(
+            ctypes.c_void_p(self.d_bufs.data_ptr()), self.world, self.rank, ctypes.c_void_p(local.data_ptr()),
+            self.count, self.epoch, ctypes.c_void_p(err_off.data_ptr()),
+            ctypes.c_void_p(status.data_ptr()) if status is not None else None, ctypes.c_void_p(s.cuda_stream)),
+            "b64_peer_combine")
+        self.epoch += 1
+
+    def close(self) -> None:
+        import ctypes
+
+        torch.cuda.synchronize(self.dev)
+        L = self._lib.lib()
+        for q in self._opened:
+            L.b64_peer_buffer_release(ctypes.c_void_p(q), 1)
+        self._opened = []
+        if self._own:
+            L.b64_peer_buffer_release(ctypes.c_void_p(self._own), 0)
+            self._own = None

@@ -992,3 +992,79 @@ def test_lenient_every_byte_final_quad(b64):
                 t[p] = v
                 ref, rerr, rst = oracle.decode(t, lenient=True)
                 dec_check_lenient(b64, t, ref, rerr, rst, len_a, 0, 0)
+
+
+# ------------------------------------------------------------------ one-sided peer combine (f4)
+
+def _packed_words(rng, n, none_frac=0.3):
+    pos = rng.integers(0, 1 << 40, n, dtype=np.int64)
+    kind = rng.integers(1, 4, n, dtype=np.int64)
+    w = (pos << 3) | kind
+    w[rng.random(n) < none_frac] = b64_err_none()
+    return w
+
+
+def b64_err_none():
+    return 0x7F7F7F7F7F7F7F7F
+
+
+def _api_form(words):
+    w = np.asarray(words, dtype=np.int64)
+    none = w >= b64_err_none()
+    return np.where(none, -1, w >> 3), np.where(none, 0, w & 7).astype(np.int32)
+
+
+def test_peer_combine_emulated_ranks(b64):
+    """W ranks emulated on one GPU (one cooperative kernel, block r = rank r) through E
+    back-to-back epochs: every rank sees the MIN over ranks of that epoch's words (the slot
+    parity, counters and slot resets of b64_peer_combine's protocol, real atomics)."""
+    L = b64._lib.lib()
+    rng = np.random.default_rng(5)
+    for world, K, epochs in ((1, 6, 5), (2, 6, 9), (3, 1, 7), (8, 6, 12), (5, 40, 4)):
+        nbytes = int(L.b64_peer_combine_bytes(K))
+        bufs = [torch.empty(nbytes, dtype=torch.uint8, device=DEV) for _ in range(world)]
+        for bb in bufs:
+            b64._lib.check(L.b64_peer_combine_init(ctypes.c_void_p(bb.data_ptr()), K, None), "init")
+        d_bufs = torch.tensor([bb.data_ptr() for bb in bufs], dtype=torch.int64, device=DEV)
+        local = _packed_words(rng, epochs * world * K).reshape(epochs, world, K)
+        local[0, :, 0] = b64_err_none()  # an epoch-0 stream with no error anywhere
+        d_local = torch.from_numpy(local.copy()).to(DEV)
+        d_out = torch.zeros(epochs * world * K, dtype=torch.int64, device=DEV)
+        ok = torch.ones(1, dtype=torch.int32, device=DEV)
+        b64._lib.check(L.b64_peer_combine_emulate(ctypes.c_void_p(d_bufs.data_ptr()), world,
+                                                  ctypes.c_void_p(d_local.data_ptr()), K, epochs,
+                                                  ctypes.c_void_p(d_out.data_ptr()),
+                                                  ctypes.c_void_p(ok.data_ptr()), None), "emulate")
+        torch.cuda.synchronize()
+        assert int(ok.item()) == 1
+        got = d_out.cpu().numpy().reshape(epochs, world, K)
+        want = local.min(axis=1)
+        for r in range(world):
+            assert np.array_equal(got[:, r, :], want), (world, K, r)
+        # after the epochs, each rank's slots are reset (ERR_NONE) and its counter = epochs * world
+        for bb in bufs:
+            raw = bb.cpu().numpy().view(np.int64)
+            assert raw[0] == epochs * world
+            assert np.all(raw[8: 8 + 2 * K] == b64_err_none())
+
+
+def test_peer_combine_world1_api(b64):
+    """dist.PeerCombine at world 1 (the per-rank kernel, IPC-allocated buffer): err_off/status
+    equal b64_decode_finalize_n of the same words, epoch after epoch."""
+    from paper_1910_05109_b200 import dist as b64dist
+
+    rng = np.random.default_rng(6)
+    pc = b64dist.PeerCombine(6)
+    try:
+        for e in range(6):
+            w = _packed_words(rng, 6)
+            cells = torch.from_numpy(w).to(DEV)
+            err = torch.empty(6, dtype=torch.int64, device=DEV)
+            st = torch.empty(6, dtype=torch.int32, device=DEV)
+            pc.combine(cells, err, st)
+            torch.cuda.synchronize()
+            we, ws = _api_form(w)
+            assert np.array_equal(err.cpu().numpy(), we), e
+            assert np.array_equal(st.cpu().numpy(), ws), e
+    finally:
+        pc.close()
