@@ -363,6 +363,32 @@ def test_config2_full(b64):
             assert err == -1 and y.numel() == n and torch.equal(y, xd)
 
 
+def test_config2_bench_step_grouped(b64):
+    """configs[1] in bench.py's launch configuration: the 6 cases (n, n+1, n+2 x std, url) as
+    ONE b64_decode_group launch + ONE b64_encode_group launch + b64_decode_finalize_n, full
+    outputs vs the oracle; three of the decode texts carry seeded corruptions."""
+    cases = [(67108864 + d, chars, pad, alpha) for d in (0, 1, 2)
+             for chars, pad, alpha in ((oracle.STANDARD, oracle.PAD, b64.standard()), (oracle.URL, oracle.PAD, b64.url()))]
+    xs = [synth.data(n, seed=0) for n, *_ in cases]
+    refs = [oracle.encode(x, chars, pad) for x, (n, chars, pad, _) in zip(xs, cases)]
+    texts = []
+    for i, r in enumerate(refs):
+        t = r.copy()
+        if i % 2 == 1:
+            pos, bad = synth.corruption(3 + i, t.size, cases[i][1], seed=40 + i)
+            t[pos] = bad
+        texts.append(t)
+    alph = [a for *_, a in cases]
+    douts, err, st = b64.decode_group([to_dev(t) for t in texts], alph)
+    eouts = b64.encode_group([to_dev(x) for x in xs], alph)
+    errc, stc = err.cpu().numpy(), st.cpu().numpy()
+    for i, (n, chars, pad, _) in enumerate(cases):
+        assert np.array_equal(eouts[i].cpu().numpy(), refs[i]), i
+        ref, rerr, rst = oracle.decode(texts[i], chars, pad)
+        assert (errc[i], stc[i]) == (rerr, rst), i
+        assert np.array_equal(douts[i][: ref.size].cpu().numpy(), ref), i
+
+
 def _windows(total, count, width, seed):
     starts = (synth.words(seed, 7, 0, count) % np.uint64(max(total - width, 1))).astype(np.int64)
     return sorted(set([0, max(total - width, 0)] + starts.tolist()))
