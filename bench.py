@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--e2e-chunk-mib", type=int, default=64, help="host pipeline chunk (MiB of input per chunk)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
+    p.add_argument("--step", choices=("codec", "split"), default="codec",
+                   help="headline step: one b64_codec_group launch (decode + encode CTAs) or two grouped launches")
     p.add_argument("--combine", choices=("nccl", "peer"), default="nccl",
                    help="N>1 first-error combine: NCCL all_reduce(MIN) (default) or the one-sided peer-memory "
                         "kernel (dist.PeerCombine, SURVEY 8(f) f4; 'peer' also runs it at N=1).  Never run "
@@ -239,6 +241,7 @@ def run_ours(args):
         stream.wait_event(ev_comm)
 
     enc_g, dec_g, fin_n = L.b64_encode_group, L.b64_decode_group, L.b64_decode_finalize_n
+    codec_g = L.b64_codec_group
     enc_f, dec_f, fin_f = L.b64_encode, L.b64_decode_chunk, L.b64_decode_finalize
     cells_p, err_p, st_p = V(cells.data_ptr()), V(err_off.data_ptr()), V(status.data_ptr())
     Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -266,6 +269,16 @@ def run_ours(args):
         rc |= timed("enc", rec, enc_g, enc_items, k, sp)
         if rc:
             raise RuntimeError(f"C ABI returned {rc}")
+        combine_end()
+
+    def step_codec(rec):
+        """One step as ONE mixed launch (b64_codec_group: decode CTAs + encode CTAs), the finalize on
+        the side stream once the kernel is done."""
+        cells.fill_(b64.ERR_NONE)
+        rc = timed("codec", rec, codec_g, enc_items, k, dec_items, k, sp)
+        if rc:
+            raise RuntimeError(f"C ABI returned {rc}")
+        combine_begin(lambda s_: fin_n(cells_p, k, err_p, st_p, s_))
         combine_end()
 
     def step_per_call(rec):
@@ -324,9 +337,10 @@ def run_ours(args):
         assert all(e == -1 for e in errs), errs
         for c in cases:
             assert torch.equal(c.enc_out, c.text) and torch.equal(c.dec_out[: c.n], c.x)
-        enc_ms = [a.elapsed_time(b) for kind, a, b in recs if kind == "enc"]
-        dec_ms = [a.elapsed_time(b) for kind, a, b in recs if kind == "dec"]
-        return total_ms, enc_ms, dec_ms, launches, wall, sampler
+        op_ms = {}
+        for kind, a, b in recs:
+            op_ms.setdefault(kind, []).append(a.elapsed_time(b))
+        return total_ms, op_ms, launches, wall, sampler
 
     b64_bytes_rank = sum(2 * c.m for c in cases)
     b64_bytes_all = b64_bytes_rank * world
@@ -335,16 +349,29 @@ def run_ours(args):
                   for c in cases)
     peak, peak_src = peaks()
 
-    total_ms, enc_ms, dec_ms, launches, wall, sampler = run(step_group, args.steps, args.warmup)
+    # headline: the step as ONE mixed launch (default) or as two grouped launches; the other form is
+    # reported beside it ("split" always gives the per-direction rates)
+    head = step_codec if args.step == "codec" else step_group
+    total_ms, op_ms, launches, wall, sampler = run(head, args.steps, args.warmup)
     value = b64_bytes_all * args.steps / (total_ms * 1e-3) / 1e9
-    enc_avg, dec_avg = statistics.mean(enc_ms), statistics.mean(dec_ms)  # one grouped launch each, 6 cases
+    sp_steps = max(10, args.steps // 2)
+    if args.step == "codec":
+        sp_total, sp_ms, _, _, _ = run(step_group, sp_steps, max(3, args.warmup // 2))
+    else:
+        sp_total, sp_ms = total_ms * sp_steps / args.steps, op_ms
+    enc_avg, dec_avg = statistics.mean(sp_ms["enc"]), statistics.mean(sp_ms["dec"])  # one grouped launch each
     enc_gbs = sum(c.m for c in cases) / (enc_avg * 1e-3) / 1e9
     dec_gbs = sum(c.m for c in cases) / (dec_avg * 1e-3) / 1e9
+    split = {"value": round(b64_bytes_all * sp_steps / (sp_total * 1e-3) / 1e9, 2),
+             "ms_per_step": round(sp_total / sp_steps, 5),
+             "dec_group_frac": round(dec_alg / (dec_avg * 1e-3) / 1e9 / peak, 4),
+             "enc_group_frac": round(enc_alg / (enc_avg * 1e-3) / 1e9 / peak, 4),
+             "note": "b64_decode_group + b64_encode_group (2 codec launches per step)"}
 
     # the same step with one launch per op (per-call API), for comparison
     pc_steps = max(10, args.steps // 2)
-    pc_total, pc_enc, pc_dec, _, _, _ = run(step_per_call, pc_steps, max(3, args.warmup // 2))
-    pc_enc_avg, pc_dec_avg = statistics.mean(pc_enc), statistics.mean(pc_dec)
+    pc_total, pc_ms, _, _, _ = run(step_per_call, pc_steps, max(3, args.warmup // 2))
+    pc_enc_avg, pc_dec_avg = statistics.mean(pc_ms["enc"]), statistics.mean(pc_ms["dec"])
     per_call = {"value": round(b64_bytes_all * pc_steps / (pc_total * 1e-3) / 1e9, 2),
                 "ms_per_step": round(pc_total / pc_steps, 5),
                 "encode_gbs": round(statistics.mean(c.m for c in cases) / (pc_enc_avg * 1e-3) / 1e9, 1),
@@ -375,10 +402,15 @@ def run_ours(args):
     memcpy_gbs = cases[0].m / (mc1 * 1e-3) / 1e9  # base64 bytes per second, same convention as the codec
     memcpy6_gbs = sum(c.m for c in cases) / (mc6 * 1e-3) / 1e9
 
-    dom = "decode" if dec_avg >= enc_avg else "encode"
-    ach = (dec_alg / (dec_avg * 1e-3) if dom == "decode" else enc_alg / (enc_avg * 1e-3)) / 1e9
-    oth = (enc_alg / (enc_avg * 1e-3) if dom == "decode" else dec_alg / (dec_avg * 1e-3)) / 1e9
-    kname = "dec_group_kernel" if dom == "decode" else "enc_group_kernel"
+    if args.step == "codec":  # the dominant (only) codec kernel of the step
+        codec_avg = statistics.mean(op_ms["codec"])
+        kname, alg, kavg, mix_key = "codec_group_kernel", enc_alg + dec_alg, codec_avg, "mixed"
+    else:
+        dom = "decode" if dec_avg >= enc_avg else "encode"
+        kname = "dec_group_kernel" if dom == "decode" else "enc_group_kernel"
+        alg, kavg = (dec_alg, dec_avg) if dom == "decode" else (enc_alg, enc_avg)
+        mix_key = "dec_4_3" if dom == "decode" else "enc_3_4"
+    ach = alg / (kavg * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -393,8 +425,12 @@ def run_ours(args):
     if os.path.exists(mp):
         try:
             best = json.load(open(mp))["best_gbs"]
-            mk = "dec_4_3" if dom == "decode" else "enc_3_4"
-            mix_ceiling = {"mix": mk, "gbs": best[mk], "frac": round(ach / best[mk], 4),
+            if mix_key == "mixed":  # equal bytes of both mixes: time-weighted (harmonic) ceiling
+                ceil_gbs = round(2 / (1 / best["enc_3_4"] + 1 / best["dec_4_3"]), 1)
+            else:
+                ceil_gbs = best[mix_key]
+            mix_ceiling = {"mix": mix_key if mix_key != "mixed" else "enc_3_4 + dec_4_3 (equal bytes)",
+                           "gbs": ceil_gbs, "frac": round(ach / ceil_gbs, 4),
                            "source": "profiles/mix_probe.json (tools/mix_probe.cu, same-mix pure streaming kernel)"}
         except Exception:  # noqa: BLE001
             mix_ceiling = None
@@ -406,8 +442,10 @@ def run_ours(args):
         "config": {"workload": "configs[1]: 64 MiB x {n, n+1, n+2} x {standard, base64url} encode + validating decode "
                                "per rank (weak scaling, shards of one stream)",
                    "bytes_per_rank_per_case": N_BYTES, "ops_per_step": 2 * k,
-                   "launches_per_step": "b64_encode_group (6 cases, 1 kernel) + b64_decode_group (1 kernel) + "
-                                        "b64_decode_finalize_n (1 kernel)",
+                   "launches_per_step": ("b64_codec_group (6 decodes + 6 encodes, 1 kernel) + "
+                                         "b64_decode_finalize_n (1 kernel)") if args.step == "codec" else
+                                        ("b64_decode_group (6 cases, 1 kernel) + b64_encode_group (1 kernel) + "
+                                         "b64_decode_finalize_n (1 kernel)"),
                    "l2": "flushed before every step (256 MiB write + 256 MiB read); 1.7 GB of disjoint buffers per step",
                    "parallelism": f"dp{world}", "volume": "base64 bytes (encode output + decode input), GB=1e9"},
         "encode_gbs": round(enc_gbs, 1), "decode_gbs": round(dec_gbs, 1),
@@ -415,14 +453,14 @@ def run_ours(args):
         "codec_vs_memcpy": {"encode_time_ratio": round(enc_avg / mc6, 4), "decode_time_ratio": round(dec_avg / mc6, 4),
                             "note": "grouped op time / time of D2D copies of the same base64 bytes (6 cases); "
                                     "<= 1 beats memcpy"},
+        "split": split,
         "per_call": per_call,
         "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                      "traffic": traffic, "peak_source": peak_src, "mix_ceiling": mix_ceiling,
-                     "alg_bytes_per_launch": int(dec_alg if dom == "decode" else enc_alg),
-                     "avg_launch_ms": round(dec_avg if dom == "decode" else enc_avg, 5),
-                     "other": {"kernel": "enc_group_kernel" if dom == "decode" else "dec_group_kernel",
-                               "achieved": round(oth, 1), "frac": round(oth / peak, 4)}},
+                     "alg_bytes_per_launch": int(alg), "avg_launch_ms": round(kavg, 5),
+                     "units": ("6 decodes (m + 3m/4 - pads bytes each) + 6 encodes (n + 4ceil(n/3)) per launch"
+                               if args.step == "codec" else "6 cases of one direction per launch")},
         "gpu_launches": int(launches), "wall_s_timed_region": round(wall, 3),
         "clocks": sampler.summary(),
     }

@@ -202,6 +202,13 @@ typedef struct b64_decode_item {
 
 int b64_encode_group(const b64_encode_item *items, int64_t count, b64_stream_t stream);
 int b64_decode_group(const b64_decode_item *items, int64_t count, b64_stream_t stream);
+/* A mixed job list: n_enc encodes and n_dec decodes, all independent (no item
+ * may read another's output).  Up to 8 + 8 items run as ONE kernel whose CTAs
+ * take either role (one launch instead of an encode group + a decode group).
+ * Same results as b64_encode_group + b64_decode_group; both lists are checked
+ * before anything is launched. */
+int b64_codec_group(const b64_encode_item *enc, int64_t n_enc, const b64_decode_item *dec, int64_t n_dec,
+                    b64_stream_t stream);
 /* b64_decode_finalize for `count` consecutive packed words. */
 int b64_decode_finalize_n(const int64_t *d_err_min, int64_t count, int64_t *d_err_off, int32_t *d_status,
                           b64_stream_t stream);

@@ -24,7 +24,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "lenient_of", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
     "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline", "new_info", "decode_unpadded", "decode_ws",
-    "encode_group", "decode_group", "EncodeStream", "DecodeStream",
+    "encode_group", "decode_group", "codec_group", "EncodeStream", "DecodeStream",
     "ERR_NONE",
 ]
 
@@ -213,9 +213,7 @@ def decode_finalize(err_cell: torch.Tensor, err_off: torch.Tensor, status: Optio
 
 # ------------------------------------------------------------------ grouped launches
 
-def encode_group(xs, alphabets=None, outs=None, stream: Optional[torch.cuda.Stream] = None):
-    """Encode several independent device buffers with one kernel per group of 8 (b64_encode_group).
-    alphabets: one Alphabet for all, or a list; returns the list of outputs."""
+def _enc_items(xs, alphabets, outs):
     k = len(xs)
     al = alphabets if isinstance(alphabets, (list, tuple)) else [alphabets] * k
     al = [a if a is not None else standard() for a in al]
@@ -226,14 +224,10 @@ def encode_group(xs, alphabets=None, outs=None, stream: Optional[torch.cuda.Stre
         _check_u8(x, "x")
         _check_u8(o, "out")
         items[i] = _lib.EncodeItem(x.data_ptr(), x.numel(), o.data_ptr(), ctypes.pointer(al[i]))
-    _lib.check(_lib.lib().b64_encode_group(items, k, _stream(stream)), "b64_encode_group")
-    return [o[: encoded_len(x.numel())] for x, o in zip(xs, outs)]
+    return items, [o[: encoded_len(x.numel())] for x, o in zip(xs, outs)]
 
 
-def decode_group(ts, alphabets=None, outs=None, cells: Optional[torch.Tensor] = None, bases=None, finals=None,
-                 stream: Optional[torch.cuda.Stream] = None):
-    """Validating decode of several device buffers, one kernel per group of 8 (b64_decode_group).
-    Returns (outs, err_off int64[k] device tensor, status int32[k] device tensor)."""
+def _dec_items(ts, alphabets, outs, cells, bases, finals):
     k = len(ts)
     dev = ts[0].device
     al = alphabets if isinstance(alphabets, (list, tuple)) else [alphabets] * k
@@ -250,12 +244,50 @@ def decode_group(ts, alphabets=None, outs=None, cells: Optional[torch.Tensor] = 
         items[i] = _lib.DecodeItem(t.data_ptr(), t.numel(), o.data_ptr(), ctypes.pointer(al[i]),
                                    0 if bases is None else bases[i], 1 if finals is None else int(finals[i]), 0,
                                    cells[i:].data_ptr())
-    _lib.check(_lib.lib().b64_decode_group(items, k, _stream(stream)), "b64_decode_group")
+    return items, outs, cells
+
+
+def _finalize_n(cells, k, dev, stream):
     err = torch.empty(k, dtype=torch.int64, device=dev)
     st = torch.empty(k, dtype=torch.int32, device=dev)
     _lib.check(_lib.lib().b64_decode_finalize_n(_ptr(cells), k, _ptr(err), _ptr(st), _stream(stream)),
                "b64_decode_finalize_n")
+    return err, st
+
+
+def encode_group(xs, alphabets=None, outs=None, stream: Optional[torch.cuda.Stream] = None):
+    """Encode several independent device buffers with one kernel per group of 8 (b64_encode_group).
+    alphabets: one Alphabet for all, or a list; returns the list of outputs."""
+    items, outs = _enc_items(xs, alphabets, outs)
+    _lib.check(_lib.lib().b64_encode_group(items, len(xs), _stream(stream)), "b64_encode_group")
+    return outs
+
+
+def decode_group(ts, alphabets=None, outs=None, cells: Optional[torch.Tensor] = None, bases=None, finals=None,
+                 stream: Optional[torch.cuda.Stream] = None):
+    """Validating decode of several device buffers, one kernel per group of 8 (b64_decode_group).
+    Returns (outs, err_off int64[k] device tensor, status int32[k] device tensor)."""
+    items, outs, cells = _dec_items(ts, alphabets, outs, cells, bases, finals)
+    _lib.check(_lib.lib().b64_decode_group(items, len(ts), _stream(stream)), "b64_decode_group")
+    err, st = _finalize_n(cells, len(ts), ts[0].device, stream)
     return outs, err, st
+
+
+def codec_group(xs, ts, enc_alphabets=None, dec_alphabets=None, enc_outs=None, dec_outs=None,
+                cells: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None):
+    """Independent encodes of xs and validating decodes of ts, ONE kernel per group of up to 8 + 8
+    (b64_codec_group).  Returns (encoded list, decoded list, err_off int64[len(ts)] or None,
+    status int32[len(ts)] or None)."""
+    eitems, eouts = _enc_items(xs, enc_alphabets, enc_outs)
+    if ts:
+        ditems, douts, cells = _dec_items(ts, dec_alphabets, dec_outs, cells, None, None)
+    else:
+        ditems, douts = (_lib.DecodeItem * 1)(), []
+    _lib.check(_lib.lib().b64_codec_group(eitems, len(xs), ditems, len(ts), _stream(stream)), "b64_codec_group")
+    if not ts:
+        return eouts, douts, None, None
+    err, st = _finalize_n(cells, len(ts), ts[0].device, stream)
+    return eouts, douts, err, st
 
 
 # ------------------------------------------------------------------ streaming (carry between calls)

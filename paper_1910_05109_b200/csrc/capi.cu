@@ -24,13 +24,32 @@ const char kUrlChars[65] = "ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz
 
 struct DevInfo {
     int sms = 0;
-    int occ_enc_group[4] = {0, 0, 0, 0}, occ_dec_group[4] = {0, 0, 0, 0};
+    int occ_group[4] = {0, 0, 0, 0};  // min over the enc / dec / codec group kernels
     int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_enc_gen = 0, occ_dec_gen = 0;
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
 bool g_dev_ready[kMaxDev];
 std::mutex g_dev_mu;
+
+// Resident CTAs per SM of the grouped kernels at depth 1 / 2: the minimum over
+// the decode, encode and mixed kernels (one grid size serves all three).
+cudaError_t group_occupancy(int (&occ)[4]) {
+    for (int d = 1; d <= 2; ++d) {
+        int a = 0, b = 0, c = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &a, d == 1 ? enc_group_kernel<1> : enc_group_kernel<2>, kThreads, 0);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, d == 1 ? dec_group_kernel<1> : dec_group_kernel<2>,
+                                                              kThreads, 0);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &c, d == 1 ? codec_group_kernel<1> : codec_group_kernel<2>, kThreads, 0);
+        if (e != cudaSuccess) return e;
+        occ[d] = std::min(a, std::min(b, c));
+    }
+    return cudaSuccess;
+}
 
 const DevInfo* dev_info() {
     int d = 0;
@@ -43,18 +62,14 @@ const DevInfo* dev_info() {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fast[2], enc_fast_kernel<2>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[1], dec_fast_kernel<1>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[2], dec_fast_kernel<2>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_group[1], enc_group_kernel<1>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_group[2], enc_group_kernel<2>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_group[1], dec_group_kernel<1>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_group[2], dec_group_kernel<2>, kThreads, 0) ||
+        group_occupancy(info.occ_group) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0))
         return nullptr;
     for (int i = 0; i < 4; ++i) {
         info.occ_enc_fast[i] = info.occ_enc_fast[i] < 1 ? 1 : info.occ_enc_fast[i];
         info.occ_dec_fast[i] = info.occ_dec_fast[i] < 1 ? 1 : info.occ_dec_fast[i];
-        info.occ_enc_group[i] = info.occ_enc_group[i] < 1 ? 1 : info.occ_enc_group[i];
-        info.occ_dec_group[i] = info.occ_dec_group[i] < 1 ? 1 : info.occ_dec_group[i];
+        info.occ_group[i] = info.occ_group[i] < 1 ? 1 : info.occ_group[i];
     }
     info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
     info.occ_dec_gen = info.occ_dec_gen < 1 ? 1 : info.occ_dec_gen;
@@ -166,16 +181,16 @@ int64_t balanced_blocks(int64_t units, int64_t max_blocks) {
     return b < 1 ? 1 : (b > max_blocks ? max_blocks : b);
 }
 
-// Warp partition of a grouped launch (warp-partitioned group kernels): stream i
-// with C[i] warp-chunks gets W_i = ceil(C[i] / t) warps, t = the smallest
-// per-warp chunk count with sum W_i <= wmax (the resident warps).  Fills
-// wstart[0..count] (exclusive scan of W_i) and returns the blocks to launch.
-int64_t group_partition(const int64_t* cstart, int count, int64_t wmax, int32_t* wstart) {
+// Warp partition of a grouped launch: stream i with C[i] warp-chunks gets
+// W_i = ceil(C[i] / t) warps, t = the smallest per-warp chunk count with
+// sum W_i <= wmax (the resident warps).  Fills wstart[0..count] (exclusive scan
+// of W_i) and returns the blocks the warps need.
+int64_t group_partition(const int64_t* C, int count, int64_t wmax, int32_t* wstart) {
     int64_t cmax = 0;
-    for (int i = 0; i < count; ++i) cmax = std::max(cmax, cstart[i + 1] - cstart[i]);
+    for (int i = 0; i < count; ++i) cmax = std::max(cmax, C[i]);
     auto need = [&](int64_t t) {
         int64_t s = 0;
-        for (int i = 0; i < count; ++i) s += (cstart[i + 1] - cstart[i] + t - 1) / t;
+        for (int i = 0; i < count; ++i) s += (C[i] + t - 1) / t;
         return s;
     };
     int64_t lo = 1, hi = cmax < 1 ? 1 : cmax;  // need(cmax) <= count <= wmax
@@ -184,7 +199,7 @@ int64_t group_partition(const int64_t* cstart, int count, int64_t wmax, int32_t*
         if (need(mid) <= wmax) hi = mid; else lo = mid + 1;
     }
     wstart[0] = 0;
-    for (int i = 0; i < count; ++i) wstart[i + 1] = wstart[i] + int32_t((cstart[i + 1] - cstart[i] + lo - 1) / lo);
+    for (int i = 0; i < count; ++i) wstart[i + 1] = wstart[i] + int32_t((C[i] + lo - 1) / lo);
     const int64_t wpb = kThreads / 32;
     const int64_t b = (int64_t(wstart[count]) + wpb - 1) / wpb;
     return b < 1 ? 1 : b;
@@ -770,63 +785,117 @@ int b64_decode_host_ex(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64
 }
 
 // ---------------------------------------------------------------- grouped launches
-int b64_encode_group(const b64_encode_item* items, int64_t count, b64_stream_t stream) {
-    if (count < 0 || (count > 0 && !items)) return B64_EINVAL;
-    for (int64_t i = 0; i < count; ++i)
-        if (items[i].n < 0 || !alpha_ok(items[i].a) || (items[i].n > 0 && (!items[i].d_in || !items[i].d_out)))
-            return B64_EINVAL;
-    const DevInfo* di = dev_info();
-    if (!di) return B64_ECUDA;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    EncGroup g;
-    std::memset(&g, 0, sizeof(g));
+// Items are collected into one pending group of up to kGroupMax decodes and
+// kGroupMax encodes; a flush launches dec_group_kernel, enc_group_kernel, or --
+// when both kinds are pending -- ONE codec_group_kernel (decode CTAs + encode
+// CTAs).  Items whose pointers are not fast-path aligned, or whose chunk count
+// does not fit the group's int32 chunk indices, get their own single-stream
+// launch.
+namespace {
+constexpr int64_t kGroupChunkMax = int64_t(INT32_MAX) / 2;
+
+struct GroupBuilder {
+    const DevInfo* di;
+    b64_stream_t stream;
+    CodecGroup g;
     int64_t bytes = 0;
-    auto flush = [&]() -> int {
-        if (g.count == 0) return B64_OK;
-        const int d = enc_depth(bytes);
-        const int64_t wmax = int64_t(di->sms) * cap_bps(di->occ_enc_group[d]) * (kThreads / 32);
-        const int64_t blocks = group_partition(g.cstart, g.count, wmax, g.wstart);
-        launch(pick2(d, enc_group_kernel<1>, enc_group_kernel<2>), blocks, kThreads, s, g);
+
+    GroupBuilder(const DevInfo* d, b64_stream_t st) : di(d), stream(st) { std::memset(&g, 0, sizeof(g)); }
+
+    int flush() {
+        const int nd = g.d.count, ne = g.e.count;
+        if (nd + ne == 0) return B64_OK;
+        cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+        const int dd = enc_depth(bytes);
+        const int64_t wmax = int64_t(di->sms) * cap_bps(di->occ_group[dd]) * (kThreads / 32);
+        int64_t C[2 * kGroupMax];
+        for (int i = 0; i < nd; ++i) C[i] = g.d.cstart[i + 1] - g.d.cstart[i];
+        for (int i = 0; i < ne; ++i) C[nd + i] = g.e.cstart[i + 1] - g.e.cstart[i];
+        if (nd && ne) {
+            // one partition over both kinds (a decode and an encode chunk move the same 1792 B);
+            // each kind's warps are rounded up to whole CTAs, so one CTA of headroom is kept
+            int32_t w[2 * kGroupMax + 1];
+            group_partition(C, nd + ne, wmax - 2 * (kThreads / 32), w);
+            for (int i = 0; i <= nd; ++i) g.d.wstart[i] = w[i];
+            for (int i = 0; i <= ne; ++i) g.e.wstart[i] = w[nd + i] - w[nd];
+            const int64_t wpb = kThreads / 32;
+            g.dec_blocks = std::max<int64_t>(1, (int64_t(w[nd]) + wpb - 1) / wpb);
+            const int64_t eb = std::max<int64_t>(1, (int64_t(w[nd + ne] - w[nd]) + wpb - 1) / wpb);
+            launch(pick2(dd, codec_group_kernel<1>, codec_group_kernel<2>), g.dec_blocks + eb, kThreads, s, g);
+        } else if (nd) {
+            const int64_t blocks = group_partition(C, nd, wmax, g.d.wstart);
+            launch(pick2(dd, dec_group_kernel<1>, dec_group_kernel<2>), blocks, kThreads, s, g.d);
+        } else {
+            const int64_t blocks = group_partition(C, ne, wmax, g.e.wstart);
+            launch(pick2(dd, enc_group_kernel<1>, enc_group_kernel<2>), blocks, kThreads, s, g.e);
+        }
         const int r = launched();
         std::memset(&g, 0, sizeof(g));
         bytes = 0;
         return r;
-    };
-    for (int64_t i = 0; i < count; ++i) {
-        const b64_encode_item& it = items[i];
-        if (it.n == 0) continue;
-        if (!(aligned(it.d_in, 8) && aligned(it.d_out, 32))) {  // not groupable: its own launch
-            const int r = b64_encode(it.d_in, it.n, it.d_out, it.a, stream);
-            if (r != B64_OK) return r;
-            continue;
-        }
-        if (it.n / 768 >= int64_t(INT32_MAX) / 2) {  // > 800 GB: too many chunks for a group's int32 chunk index
-            const int r = b64_encode(it.d_in, it.n, it.d_out, it.a, stream);
-            if (r != B64_OK) return r;
-            continue;
-        }
-        if (g.count && g.cstart[g.count] + it.n / 768 >= int64_t(INT32_MAX) / 2) {
-            const int r = flush();
-            if (r != B64_OK) return r;
-        }
-        const int k = g.count;
-        g.in[k] = it.d_in;
-        g.out[k] = it.d_out;
-        g.n[k] = it.n;
-        g.pad[k] = it.a->pad;
-        std::memcpy(g.lut[k], it.a->enc, 64);
-        g.cstart[k + 1] = g.cstart[k] + it.n / 768;
-        g.count = k + 1;
-        bytes += it.n;
-        if (g.count == kGroupMax) {
-            const int r = flush();
-            if (r != B64_OK) return r;
-        }
     }
-    return flush();
+
+    int add(const b64_encode_item& it) {
+        if (it.n == 0) return B64_OK;
+        const int64_t nc = it.n / 768;
+        if (!(aligned(it.d_in, 8) && aligned(it.d_out, 32)) || nc >= kGroupChunkMax)  // its own launch
+            return b64_encode(it.d_in, it.n, it.d_out, it.a, stream);
+        EncGroup& e = g.e;
+        if (e.count == kGroupMax || e.cstart[e.count] + nc >= kGroupChunkMax) {
+            const int r = flush();
+            if (r != B64_OK) return r;
+        }
+        const int k = e.count;
+        e.in[k] = it.d_in;
+        e.out[k] = it.d_out;
+        e.n[k] = it.n;
+        e.pad[k] = it.a->pad;
+        std::memcpy(e.lut[k], it.a->enc, 64);
+        e.cstart[k + 1] = e.cstart[k] + nc;
+        e.count = k + 1;
+        bytes += it.n;
+        return B64_OK;
+    }
+
+    int add(const b64_decode_item& it) {
+        if (it.m == 0) return B64_OK;
+        const int64_t Q = it.m / 4;
+        const int64_t Qint = (it.is_final && Q > 0) ? Q - 1 : Q;
+        const int64_t nc = Qint / 256;
+        if (!(aligned(it.d_in, 32) && aligned(it.d_out, 16)) || nc >= kGroupChunkMax)
+            return b64_decode_chunk(it.d_in, it.m, it.d_out, it.a, it.base_offset, it.is_final, it.d_err_min,
+                                    nullptr, stream);
+        DecGroup& d = g.d;
+        if (d.count == kGroupMax || d.cstart[d.count] + nc >= kGroupChunkMax) {
+            const int r = flush();
+            if (r != B64_OK) return r;
+        }
+        const int k = d.count;
+        d.in[k] = it.d_in;
+        d.out[k] = it.d_out;
+        d.m[k] = it.m;
+        d.base[k] = it.base_offset;
+        d.cell[k] = reinterpret_cast<unsigned long long*>(it.d_err_min);
+        d.is_final[k] = it.is_final ? 1 : 0;
+        d.pad[k] = it.a->pad;
+        d.lenient[k] = (it.a->flags & B64_ALPHA_LENIENT) ? 1u : 0u;
+        std::memcpy(d.lut[k], it.a->dec, 256);
+        d.cstart[k + 1] = d.cstart[k] + nc;
+        d.count = k + 1;
+        bytes += it.m;
+        return B64_OK;
+    }
+};
+
+int check_enc_items(const b64_encode_item* items, int64_t count) {
+    if (count < 0 || (count > 0 && !items)) return B64_EINVAL;
+    for (int64_t i = 0; i < count; ++i)
+        if (items[i].n < 0 || !alpha_ok(items[i].a) || (items[i].n > 0 && (!items[i].d_in || !items[i].d_out)))
+            return B64_EINVAL;
+    return B64_OK;
 }
 
-int b64_decode_group(const b64_decode_item* items, int64_t count, b64_stream_t stream) {
+int check_dec_items(const b64_decode_item* items, int64_t count) {
     if (count < 0 || (count > 0 && !items)) return B64_EINVAL;
     for (int64_t i = 0; i < count; ++i) {
         const b64_decode_item& it = items[i];
@@ -834,63 +903,32 @@ int b64_decode_group(const b64_decode_item* items, int64_t count, b64_stream_t s
             return B64_EINVAL;
         if (it.m % 4) return B64_ELENGTH;
     }
+    return B64_OK;
+}
+}  // namespace
+
+int b64_codec_group(const b64_encode_item* enc, int64_t n_enc, const b64_decode_item* dec, int64_t n_dec,
+                    b64_stream_t stream) {
+    int r = check_enc_items(enc, n_enc);
+    if (r == B64_OK) r = check_dec_items(dec, n_dec);
+    if (r != B64_OK) return r;
     const DevInfo* di = dev_info();
     if (!di) return B64_ECUDA;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    DecGroup g;
-    std::memset(&g, 0, sizeof(g));
-    int64_t bytes = 0;
-    auto flush = [&]() -> int {
-        if (g.count == 0) return B64_OK;
-        const int d = dec_depth(bytes);
-        const int64_t wmax = int64_t(di->sms) * cap_bps(di->occ_dec_group[d]) * (kThreads / 32);
-        const int64_t blocks = group_partition(g.cstart, g.count, wmax, g.wstart);
-        launch(pick2(d, dec_group_kernel<1>, dec_group_kernel<2>), blocks, kThreads, s, g);
-        const int r = launched();
-        std::memset(&g, 0, sizeof(g));
-        bytes = 0;
-        return r;
-    };
-    for (int64_t i = 0; i < count; ++i) {
-        const b64_decode_item& it = items[i];
-        if (it.m == 0) continue;
-        if (!(aligned(it.d_in, 32) && aligned(it.d_out, 16))) {
-            const int r = b64_decode_chunk(it.d_in, it.m, it.d_out, it.a, it.base_offset, it.is_final, it.d_err_min,
-                                           nullptr, stream);
-            if (r != B64_OK) return r;
-            continue;
-        }
-        if (it.m / 1024 >= int64_t(INT32_MAX) / 2) {  // too many chunks for a group's int32 chunk index
-            const int r = b64_decode_chunk(it.d_in, it.m, it.d_out, it.a, it.base_offset, it.is_final, it.d_err_min,
-                                           nullptr, stream);
-            if (r != B64_OK) return r;
-            continue;
-        }
-        if (g.count && g.cstart[g.count] + it.m / 1024 >= int64_t(INT32_MAX) / 2) {
-            const int r = flush();
-            if (r != B64_OK) return r;
-        }
-        const int k = g.count;
-        g.in[k] = it.d_in;
-        g.out[k] = it.d_out;
-        g.m[k] = it.m;
-        g.base[k] = it.base_offset;
-        g.cell[k] = reinterpret_cast<unsigned long long*>(it.d_err_min);
-        g.is_final[k] = it.is_final ? 1 : 0;
-        g.pad[k] = it.a->pad;
-        g.lenient[k] = (it.a->flags & B64_ALPHA_LENIENT) ? 1u : 0u;
-        std::memcpy(g.lut[k], it.a->dec, 256);
-        const int64_t Q = it.m / 4;
-        const int64_t Qint = (it.is_final && Q > 0) ? Q - 1 : Q;
-        g.cstart[k + 1] = g.cstart[k] + Qint / 256;
-        g.count = k + 1;
-        bytes += it.m;
-        if (g.count == kGroupMax) {
-            const int r = flush();
-            if (r != B64_OK) return r;
-        }
+    GroupBuilder gb(di, stream);
+    // interleaved so that a group pairs decodes with encodes when both lists are long
+    for (int64_t i = 0; i < std::max(n_enc, n_dec); ++i) {
+        if (i < n_dec && (r = gb.add(dec[i])) != B64_OK) return r;
+        if (i < n_enc && (r = gb.add(enc[i])) != B64_OK) return r;
     }
-    return flush();
+    return gb.flush();
+}
+
+int b64_encode_group(const b64_encode_item* items, int64_t count, b64_stream_t stream) {
+    return b64_codec_group(items, count, nullptr, 0, stream);
+}
+
+int b64_decode_group(const b64_decode_item* items, int64_t count, b64_stream_t stream) {
+    return b64_codec_group(nullptr, 0, items, count, stream);
 }
 
 int b64_decode_finalize_n(const int64_t* d_err_min, int64_t count, int64_t* d_err_off, int32_t* d_status,

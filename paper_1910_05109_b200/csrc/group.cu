@@ -55,13 +55,15 @@ __device__ __forceinline__ int warp_stream(const G& g, int32_t w) {
     return it;  // == g.count: an idle warp (no bulk work)
 }
 
+// The grouped encode as run by CTA `bid` of `nblocks` (a whole enc_group_kernel
+// grid, or the encode CTAs of a codec_group_kernel grid).
 template <int D>
-__global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) enc_group_kernel(const __grid_constant__ EncGroup g) {
+__device__ __forceinline__ void enc_group_body(const EncGroup& g, int64_t bid, int64_t nblocks) {
     __shared__ __align__(64) uint32_t s_lut[kGroupMax][16];
     griddep_launch_dependents();
     const int lane = threadIdx.x & 31;
-    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t gtid = bid * blockDim.x + threadIdx.x;
+    const int64_t gthreads = nblocks * blockDim.x;
     const int32_t w = int32_t(gtid >> 5);
     const int it = warp_stream(g, w);
 
@@ -95,14 +97,15 @@ __global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) enc_group_kernel(con
     }
 }
 
+// The grouped decode as run by CTA `bid` of `nblocks`.
 template <int D>
-__global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) dec_group_kernel(const __grid_constant__ DecGroup g) {
+__device__ __forceinline__ void dec_group_body(const DecGroup& g, int64_t bid, int64_t nblocks) {
     __shared__ __align__(256) uint32_t s_lut[kGroupMax][64];
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];
     griddep_launch_dependents();
     const int lane = threadIdx.x & 31;
-    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t gtid = bid * blockDim.x + threadIdx.x;
+    const int64_t gthreads = nblocks * blockDim.x;
     const int32_t w = int32_t(gtid >> 5);
     const int it = warp_stream(g, w);
 
@@ -143,6 +146,33 @@ __global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) dec_group_kernel(con
             else atomicMin(g.cell[is], pack_err(g.base[is] + 4 * q + bad, kind));
         }
     }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) enc_group_kernel(const __grid_constant__ EncGroup g) {
+    enc_group_body<D>(g, blockIdx.x, gridDim.x);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) dec_group_kernel(const __grid_constant__ DecGroup g) {
+    dec_group_body<D>(g, blockIdx.x, gridDim.x);
+}
+
+// Mixed job list in ONE launch: CTAs [0, dec_blocks) run the grouped decode,
+// the rest the grouped encode (each CTA one role, so each role's code, table
+// staging and barrier are exactly the single-role kernel's).  Saves one kernel
+// boundary (launch, ramp, drain) per encode + decode pair of groups.
+struct CodecGroup {
+    DecGroup d;
+    EncGroup e;
+    int64_t dec_blocks;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) codec_group_kernel(const __grid_constant__ CodecGroup g) {
+    const int64_t b = blockIdx.x;
+    if (b < g.dec_blocks) dec_group_body<D>(g.d, b, g.dec_blocks);
+    else enc_group_body<D>(g.e, b - g.dec_blocks, int64_t(gridDim.x) - g.dec_blocks);
 }
 
 // Packed error words -> (err_off, status) for count streams.

@@ -660,6 +660,39 @@ def test_group_unequal_large_streams(b64):
         assert np.array_equal(douts[i][:k].cpu().numpy(), ref[:k]), i
 
 
+def test_codec_group_mixed(b64):
+    """b64_codec_group: encodes and decodes in ONE launch (decode CTAs + encode CTAs), unequal
+    sizes, corrupted texts, several groups (> 8 + 8 items), misaligned items in between."""
+    al = _alphabets(b64)
+    rng = np.random.default_rng(12)
+    sizes = [40 << 20, 5, (3 << 20) + 1, 0, 768 * 9 + 2] + [int(v) for v in rng.integers(0, 400_000, 14)]
+    xs = [synth.data(n, seed=950 + i) for i, n in enumerate(sizes)]
+    chars_l = [al[i % len(al)][:2] for i in range(len(sizes))]
+    alph_l = [al[i % len(al)][2] for i in range(len(sizes))]
+    texts = [oracle.encode(x, *chars_l[i]) for i, x in enumerate(xs)]
+    for i in range(0, len(texts), 3):
+        if texts[i].size > 8:
+            pos, bad = synth.corruption(2, texts[i].size, chars_l[i][0], seed=i, pad=chars_l[i][1])
+            texts[i][pos] = bad
+    dx = [to_dev(x, 1 if i % 7 == 6 else 0) for i, x in enumerate(xs)]
+    order = list(range(len(texts)))[::-1]  # decode list in another order than the encode list
+    dt = [to_dev(texts[i], 2 if i % 6 == 5 else 0) for i in order]
+    eouts, douts, err, st = b64.codec_group(dx, dt, alph_l, [alph_l[i] for i in order])
+    errc, stc = err.cpu().numpy(), st.cpu().numpy()
+    for i, x in enumerate(xs):
+        assert np.array_equal(eouts[i].cpu().numpy(), oracle.encode(x, *chars_l[i])), i
+    for j, i in enumerate(order):
+        ref, rerr, rst = oracle.decode(texts[i], *chars_l[i])
+        assert (errc[j], stc[j]) == (rerr, rst), i
+        k = ref.size if rerr < 0 else 3 * (rerr // 4)
+        assert np.array_equal(douts[j][:k].cpu().numpy(), ref[:k]), i
+    # one kind only
+    eouts, douts, err, st = b64.codec_group(dx[:3], [], alph_l[:3])
+    assert douts == [] and err is None
+    for i in range(3):
+        assert np.array_equal(eouts[i].cpu().numpy(), oracle.encode(xs[i], *chars_l[i])), i
+
+
 def test_group_decode_as_shards(b64):
     """Grouped items as shards of one stream: global bases, only the last is final, one cell."""
     x = synth.data(768 * 500 + 1, seed=3)

@@ -26,9 +26,11 @@ def main():
         xs = [synth.device_data(a.n + d, seed=0) for d in (0, 0, 1, 1, 2, 2)]
         al = [b64.standard(), b64.url()] * 3
         ts = b64.encode_group(xs, al)
-        for _ in range(a.reps):
-            b64.encode_group(xs, al, outs=ts)
+        eo = [torch.empty_like(t) for t in ts]
+        for _ in range(a.reps):  # the bench step's launches: one mixed codec kernel, then the two grouped ones
+            _, outs, err, st = b64.codec_group(xs, ts, al, al, enc_outs=eo)
             outs, err, st = b64.decode_group(ts, al)
+            b64.encode_group(xs, al, outs=eo)
         torch.cuda.synchronize()
         assert (err == -1).all()
         print("ok group")
