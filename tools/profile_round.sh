@@ -11,7 +11,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 echo "launch list rc=$?"
 PG="python tools/prof_case.py --op group --n 67108864 --reps 2"
 $PG > gpurun_out/${T}_pg.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"group_kernel" -s 2 -c 2 -o gpurun_out/${T}_full_group $PG > gpurun_out/${T}_ncu_group.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"group_kernel" -s 1 -c 3 -o gpurun_out/${T}_full_group $PG > gpurun_out/${T}_ncu_group.log 2>&1
 echo "full group rc=$?"
 P64="python tools/prof_case.py --op both --n 67108864 --reps 2"
 $P64 > gpurun_out/${T}_p64.log 2>&1 && \
