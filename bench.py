@@ -51,8 +51,9 @@ def parse():
     p.add_argument("--e2e-chunk-mib", type=int, default=64, help="host pipeline chunk (MiB of input per chunk)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
-    p.add_argument("--step", choices=("codec", "split"), default="codec",
-                   help="headline step: one b64_codec_group launch (decode + encode CTAs) or two grouped launches")
+    p.add_argument("--step", choices=("auto", "codec", "split"), default="auto",
+                   help="headline step: one b64_codec_group launch (decode + encode CTAs) or two grouped launches; "
+                        "auto = codec at N=1, split at N>1 (the error combine then overlaps the encode launch)")
     p.add_argument("--combine", choices=("nccl", "peer"), default="nccl",
                    help="N>1 first-error combine: NCCL all_reduce(MIN) (default) or the one-sided peer-memory "
                         "kernel (dist.PeerCombine, SURVEY 8(f) f4; 'peer' also runs it at N=1).  Never run "
@@ -184,6 +185,10 @@ def run_ours(args):
     import synth
 
     world, rank, local = dist_setup(args)
+    if args.step == "auto":
+        # N > 1: the cross-rank error combine must follow the decodes; with two launches it
+        # overlaps the encode launch, with one codec launch it would be exposed
+        args.step = "codec" if world == 1 or args.combine == "peer" else "split"
     dev = torch.device("cuda", torch.cuda.current_device())
     L = b64._lib.lib()
     stream = torch.cuda.current_stream()
