@@ -17,9 +17,12 @@ namespace b64 {
 
 namespace cg = cooperative_groups;
 
-constexpr int kSmallThreads = 512;
+#ifndef B64_SMALL_THREADS
+#define B64_SMALL_THREADS 512
+#endif
+constexpr int kSmallThreads = B64_SMALL_THREADS;  // 16 warps per CTA (1024 measured slower below 1 MiB)
 constexpr int kSmallCluster = 16;                // CTAs (non-portable cluster size, one per SM)
-constexpr int64_t kSmallMax = int64_t(512) << 10;  // chars handled by the single-launch path (tools/small_sweep.py)
+constexpr int64_t kSmallMax = int64_t(1536) << 10;  // chars handled by the single-launch path (tools/small_sweep.py: beats the 3-op path up to ~1.5 Mi chars)
 
 __global__ void __launch_bounds__(kSmallThreads)
 dec_small_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
@@ -44,10 +47,17 @@ dec_small_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
     const int64_t Qint = Q > 0 ? Q - 1 : 0;
     const int32_t C = int32_t(Qint >> 8);
 
-    for (int32_t c = int32_t(gtid >> 5); c < C; c += W) {
+    // one chunk per warp in flight ahead of the one being translated (the data is
+    // usually L2-resident here: latency, not bandwidth, bounds a 16-SM grid)
+    uint32_t xn[8];
+    int32_t c = int32_t(gtid >> 5);
+    if (c < C) ld256_stream(in + int64_t(c) * 1024 + lane * 32, xn);
+    for (; c < C; c += W) {
         uint32_t x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = xn[j];
         const uint8_t* src = in + int64_t(c) * 1024 + lane * 32;
-        ld256_stream(src, x);
+        if (c + W < C) ld256_stream(src + int64_t(W) * 1024, xn);
         uint32_t err = 0, v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(x[q], lb, err);
