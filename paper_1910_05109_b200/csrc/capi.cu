@@ -326,8 +326,14 @@ int b64_decode_ex(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
         attr[0].val.clusterDim.z = 1;
         attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[1].val.programmaticStreamSerializationAllowed = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        if (r == 1) {  // one CTA: a plain launch (implicit 1-CTA cluster), ~0.6-1 us cheaper than a cluster launch
+            attr[0] = attr[1];
+            cfg.attrs = attr;
+            cfg.numAttrs = pdl_enabled() ? 1 : 0;
+        } else {
+            cfg.attrs = attr;
+            cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        }
         cudaLaunchKernelEx(&cfg, dec_small_kernel, d_in, m, d_out, dec_tab(a), d_err_off, d_status, d_out_len);
         return launched();
     }
