@@ -472,6 +472,10 @@ def run_ours(args):
 
     if rank == 0 and not args.no_extra and world == 1:
         out["extra_configs"] = extra_configs(b64, synth, torch, dev, stream, flush, Ev)
+    if not args.no_extra and world > 1:  # every rank takes part
+        ex = extra_configs_dist(b64, synth, torch, dev, world, rank, flush)
+        if rank == 0:
+            out["extra_configs"] = ex
     if rank == 0:
         out["e2e"] = e2e(b64, synth, torch, dev, args, cases)
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -709,6 +713,82 @@ def config5_one_gpu(b64, synth, torch, dev, timeit):
            "note": "8 dist shards of one stream on one GPU (grouped launches): the strong-scaling N=1 point"}
     del text, out, tparts, oparts
     torch.cuda.empty_cache()
+    return res
+
+
+def extra_configs_dist(b64, synth, torch, dev, world, rank, flush):
+    """N > 1: configs[2] (1 GiB decode-heavy) and configs[4] (16 GiB with 1000 injected errors)
+    sharded over the ranks by paper_1910_05109_b200.dist (strong scaling: the global sizes are
+    fixed).  Each rank encodes its own input shard into its text shard (device-generated data,
+    no exchange), then the timed region is its shard's kernel plus the NCCL all_reduce(MIN) of
+    the error word and the finalize; times are CUDA events, max over ranks."""
+    import numpy as np
+    import torch.distributed as dist
+
+    import oracle
+    from paper_1910_05109_b200 import dist as b64dist
+
+    stream = torch.cuda.current_stream()
+
+    def tmax(ms):
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, reps):
+        kern, full = [], []
+        for j in range(reps + 2):
+            flush(j)
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            fn(e1)
+            e2.record(stream)
+            torch.cuda.synchronize()
+            if j >= 2:
+                kern.append(e0.elapsed_time(e1))
+                full.append(e0.elapsed_time(e2))
+        return tmax(statistics.median(kern)), tmax(statistics.median(full))
+
+    res = {}
+    for name, N, inject in (("config3_1GiB_sharded", 1 << 30, 0), ("config5_16GiB_sharded", 1 << 34, 1000)):
+        m = b64.encoded_len(N)
+        es, ds = b64dist.encode_shard(N, world, rank), b64dist.decode_shard(m, world, rank)
+        x = torch.empty(es.stop - es.start, dtype=torch.uint8, device=dev)
+        synth.device_fill(x, seed=0, offset=es.start)
+        t = torch.empty(ds.stop - ds.start, dtype=torch.uint8, device=dev)
+        assert t.numel() == (b64.encoded_len(x.numel()) if es.is_final else 4 * (x.numel() // 3))
+        te_k, _ = timed(lambda ev: (b64.encode(x, out=t), ev.record(stream)), 5)
+        expected = -1
+        if inject:
+            pos, bad = synth.corruption(inject, m, oracle.STANDARD, seed=0)
+            sel = (pos >= ds.start) & (pos < ds.stop)
+            if sel.any():
+                t[torch.from_numpy(pos[sel] - ds.start).to(dev)] = torch.from_numpy(bad[sel]).to(dev)
+            expected = int(pos.min())
+        out = torch.empty(3 * (t.numel() // 4), dtype=torch.uint8, device=dev)
+        cell = torch.empty(1, dtype=torch.int64, device=dev)
+        eo = torch.empty(1, dtype=torch.int64, device=dev)
+
+        def dec(ev):
+            cell.fill_(b64.ERR_NONE)
+            b64.decode_chunk(t, ds.start, ds.is_final, cell, out=out)
+            ev.record(stream)
+            dist.all_reduce(cell, op=dist.ReduceOp.MIN)
+            b64.decode_finalize(cell, eo)
+
+        td_k, td_full = timed(dec, 5)
+        got = int(eo.item())
+        assert got == expected, (got, expected)
+        res[name] = {"encode_gbs_aggregate": round(m / (te_k * 1e-3) / 1e9, 1),
+                     "decode_gbs_aggregate_kernel": round(m / (td_k * 1e-3) / 1e9, 1),
+                     "decode_gbs_aggregate_with_combine": round(m / (td_full * 1e-3) / 1e9, 1),
+                     "decode_ms_max_kernel": round(td_k, 4), "decode_ms_max_with_combine": round(td_full, 4),
+                     "first_error": got, "injected": inject, "bytes_per_rank": x.numel(),
+                     "note": "strong scaling: global size fixed, max over ranks of CUDA-event times"}
+        del x, t, out
+        torch.cuda.empty_cache()
     return res
 
 
