@@ -463,6 +463,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                      "traffic": traffic, "peak_source": peak_src, "mix_ceiling": mix_ceiling,
+                     "frac_of_nominal_8000": round(ach / 8000.0, 4),  # BASELINE north star's ~8 TB/s (context)
                      "alg_bytes_per_launch": int(alg), "avg_launch_ms": round(kavg, 5),
                      "units": ("6 decodes (m + 3m/4 - pads bytes each) + 6 encodes (n + 4ceil(n/3)) per launch"
                                if args.step == "codec" else "6 cases of one direction per launch")},
