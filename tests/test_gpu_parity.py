@@ -364,9 +364,10 @@ def test_config2_full(b64):
 
 
 def test_config2_bench_step_grouped(b64):
-    """configs[1] in bench.py's launch configuration: the 6 cases (n, n+1, n+2 x std, url) as
-    ONE b64_decode_group launch + ONE b64_encode_group launch + b64_decode_finalize_n, full
-    outputs vs the oracle; three of the decode texts carry seeded corruptions."""
+    """configs[1] in bench.py's launch configurations: the 6 cases (n, n+1, n+2 x std, url) as
+    ONE b64_decode_group launch + ONE b64_encode_group launch (the split step) and as ONE
+    b64_codec_group launch (the headline step), + b64_decode_finalize_n; full outputs vs the
+    oracle; three of the decode texts carry seeded corruptions."""
     cases = [(67108864 + d, chars, pad, alpha) for d in (0, 1, 2)
              for chars, pad, alpha in ((oracle.STANDARD, oracle.PAD, b64.standard()), (oracle.URL, oracle.PAD, b64.url()))]
     xs = [synth.data(n, seed=0) for n, *_ in cases]
@@ -379,8 +380,17 @@ def test_config2_bench_step_grouped(b64):
             t[pos] = bad
         texts.append(t)
     alph = [a for *_, a in cases]
-    douts, err, st = b64.decode_group([to_dev(t) for t in texts], alph)
-    eouts = b64.encode_group([to_dev(x) for x in xs], alph)
+    dxs, dts = [to_dev(x) for x in xs], [to_dev(t) for t in texts]
+    douts, err, st = b64.decode_group(dts, alph)
+    eouts = b64.encode_group(dxs, alph)
+    errc, stc = err.cpu().numpy(), st.cpu().numpy()
+    for i, (n, chars, pad, _) in enumerate(cases):
+        assert np.array_equal(eouts[i].cpu().numpy(), refs[i]), i
+        ref, rerr, rst = oracle.decode(texts[i], chars, pad)
+        assert (errc[i], stc[i]) == (rerr, rst), i
+        assert np.array_equal(douts[i][: ref.size].cpu().numpy(), ref), i
+    # the bench's headline launch: the same 6 + 6 jobs as ONE b64_codec_group kernel
+    eouts, douts, err, st = b64.codec_group(dxs, dts, alph, alph)
     errc, stc = err.cpu().numpy(), st.cpu().numpy()
     for i, (n, chars, pad, _) in enumerate(cases):
         assert np.array_equal(eouts[i].cpu().numpy(), refs[i]), i
@@ -482,6 +492,50 @@ def test_config5_single_gpu_sampled(b64):
     eo = torch.empty(1, dtype=torch.int64, device=DEV)
     b64.decode_finalize(cells.min().reshape(1), eo)
     assert int(eo.item()) == int(pos.min())
+
+
+def test_config5_bench_launch_sampled(b64):
+    """configs[4] as bench.py times it on one GPU: the 16 GiB stream cut into the 8 shards an
+    8-GPU run owns (dist rules), ONE encode_group launch and ONE decode_group launch over the
+    8 shards with one shared error word; sampled text windows vs the oracle, 1000 injected
+    errors, global first error, the exact output prefix before it."""
+    from paper_1910_05109_b200 import dist as b64dist
+
+    N, G = 1 << 34, 8
+    x = synth.device_data(N, seed=0)
+    m = b64.encoded_len(N)
+    text = torch.empty(m, dtype=torch.uint8, device=DEV)
+    es = [b64dist.encode_shard(N, G, r) for r in range(G)]
+    b64.encode_group([x[sh.start: sh.stop] for sh in es],
+                     outs=[text[sh.out_start: sh.out_start + (b64.encoded_len(sh.stop - sh.start) if sh.is_final
+                                                              else 4 * ((sh.stop - sh.start) // 3))] for sh in es])
+    for s0 in _windows(N // 3, 12, 2048, seed=5) + [es[3].start // 3 - 5, (N - 10) // 3]:
+        ref = oracle.encode(synth.data(min(3 * 2048, N - 3 * s0), seed=0, offset=3 * s0))
+        assert np.array_equal(text[4 * s0: 4 * s0 + ref.size].cpu().numpy(), ref), s0
+    pos, bad = synth.corruption(1000, m, oracle.STANDARD, seed=0)
+    text[torch.from_numpy(pos).to(DEV)] = torch.from_numpy(bad).to(DEV)
+    del x
+    torch.cuda.empty_cache()
+    out = torch.empty(3 * (m // 4), dtype=torch.uint8, device=DEV)
+    ds = [b64dist.decode_shard(m, G, r) for r in range(G)]
+    cell = torch.full((1,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+    items = (b64._lib.DecodeItem * G)()
+    std = b64.standard()
+    for r, sh in enumerate(ds):
+        t_r = text[sh.start: sh.stop]
+        o_r = out[sh.out_start: sh.out_start + 3 * ((sh.stop - sh.start) // 4)]
+        items[r] = b64._lib.DecodeItem(t_r.data_ptr(), t_r.numel(), o_r.data_ptr(), ctypes.pointer(std), sh.start,
+                                       int(sh.is_final), 0, cell.data_ptr())
+    b64._lib.check(b64._lib.lib().b64_decode_group(items, G, None), "b64_decode_group")
+    eo = torch.empty(1, dtype=torch.int64, device=DEV)
+    st = torch.zeros(1, dtype=torch.int32, device=DEV)
+    b64.decode_finalize(cell, eo, st)
+    first = int(pos.min())
+    assert (int(eo.item()), int(st.item())) == (first, oracle.ST_BADCHAR)
+    k = 3 * (first // 4)
+    assert np.array_equal(out[:k].cpu().numpy(), synth.data(k, seed=0))
+    del text, out
+    torch.cuda.empty_cache()
 
 
 # ------------------------------------------------------------------ host-buffer pipeline
