@@ -793,10 +793,53 @@ def extra_configs_dist(b64, synth, torch, dev, world, rank, flush):
     return res
 
 
-def cpu_baseline(seconds: float):
-    """The oracle (single-threaded scalar C, never tuned) on a bounded sample of the workload."""
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_step_parallel(cases, threads: int) -> int:
+    """One encode + decode of every (bytes, alphabet) case with the unmodified scalar oracle on
+    `threads` host threads: each case is cut at 3-byte / 4-char boundaries (the GPU shard rule)
+    and the pieces run concurrently (the oracle is C behind ctypes, which releases the GIL).
+    Returns the base64 bytes (encode output + decode input) processed."""
+    from concurrent.futures import ThreadPoolExecutor
+
     import numpy as np
 
+    import oracle
+
+    vol = 0
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for x, chars in cases:
+            n = x.size
+            T = n // 3
+            cuts = [3 * (T * k // threads) for k in range(threads)] + [n]
+            parts = list(ex.map(lambda k: oracle.encode(x[cuts[k]: cuts[k + 1]], chars), range(threads)))
+            t = np.concatenate(parts)
+            m = t.size
+            ccuts = [4 * (cuts[k] // 3) for k in range(threads)] + [m]
+            res = list(ex.map(lambda k: oracle.decode(t[ccuts[k]: ccuts[k + 1]], chars), range(threads)))
+            assert all(r[1] == -1 for r in res) and sum(r[0].size for r in res) == n
+            vol += 2 * m
+    return vol
+
+
+def cpu_baseline(seconds: float):
+    """The oracle (scalar C, never tuned) on a bounded sample of the workload: single-threaded
+    (the headline baseline) and on all host cores (SURVEY.md Sec. 8(d) oracle timing)."""
     import oracle
     import synth
 
@@ -813,8 +856,20 @@ def cpu_baseline(seconds: float):
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
+    cores = host_cores()
+    t1 = time.perf_counter()
+    vol, reps_all = 0, 0
+    while True:
+        vol += oracle_step_parallel([(x, oracle.STANDARD)], cores)
+        reps_all += 1
+        if time.perf_counter() - t1 >= seconds / 2:
+            break
+    dt_all = time.perf_counter() - t1
     return {"value": round(done / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"{reps} x (encode + decode) of the 64 MiB (n, standard) case = {done} base64 bytes in {dt:.1f} s"}
+            "sample": f"{reps} x (encode + decode) of the 64 MiB (n, standard) case = {done} base64 bytes in {dt:.1f} s",
+            "all_cores": {"value": round(vol / dt_all / 1e9, 4), "cores": cores, "cpu_model": cpu_model(),
+                          "sample": f"{reps_all} x the same case cut into {cores} shards at 3-byte / 4-char "
+                                    f"boundaries, one host thread each ({dt_all:.1f} s)"}}
 
 
 # ---------------------------------------------------------------- reference arm (the oracle on host cores)
@@ -830,7 +885,7 @@ def run_reference(args):
     if rank != 0:
         return  # only rank 0 runs and prints; the others exit 0 without work
     budget_s = 90.0
-    rate = 0.8e9  # approx oracle base64 B/s, only to size the per-step sample
+    rate = 0.8e9 * host_cores()  # approx oracle base64 B/s on all cores, only to size the per-step sample
     per_step = budget_s * rate / max(1, args.steps + args.warmup)
     full = 6 * 2 * 89478488
     frac = min(1.0, per_step / full)
@@ -841,14 +896,10 @@ def run_reference(args):
             xs = synth.data(n + d, seed=0)
             cases.append((xs, chars))
 
-    def step():
-        vol = 0
-        for xs, chars in cases:
-            t = oracle.encode(xs, chars)
-            y, err, st = oracle.decode(t, chars)
-            assert err == -1
-            vol += 2 * t.size
-        return vol
+    cores = host_cores()
+
+    def step():  # the unmodified oracle on all host cores (shards cut at 3-byte / 4-char boundaries)
+        return oracle_step_parallel(cases, cores)
 
     for _ in range(args.warmup):
         step()
@@ -859,14 +910,14 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     v = vol / dt / 1e9
     sample = (f"each step: configs[1] cases truncated to {n}(+0/1/2) bytes (fraction {frac:.4f} of the full step), "
-              "6 encodes + 6 decodes")
+              f"6 encodes + 6 decodes, each cut into {cores} shards run on {cores} host threads ({cpu_model()})")
     out = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
            "data": "synthetic (splitmix64 seed 0, uniform bytes)",
            "config": {"workload": "configs[1]: 64 MiB x {n, n+1, n+2} x {standard, base64url} encode + validating "
-                                  "decode (sampled, see cpu_baseline.sample)", "parallelism": "host, 1 thread"},
-           "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+                                  "decode (sampled, see cpu_baseline.sample)", "parallelism": f"host, {cores} threads"},
+           "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
