@@ -22,7 +22,7 @@ namespace cg = cooperative_groups;
 #endif
 constexpr int kSmallThreads = B64_SMALL_THREADS;  // 16 warps per CTA (1024 measured slower below 1 MiB)
 constexpr int kSmallCluster = 16;                // CTAs (non-portable cluster size, one per SM)
-constexpr int64_t kSmallMax = int64_t(1536) << 10;  // chars handled by the single-launch path (tools/small_sweep.py: beats the 3-op path up to ~1.5 Mi chars)
+constexpr int64_t kSmallMax = int64_t(512) << 10;  // chars handled by the single-launch path (tools/small_sweep.py)
 
 __global__ void __launch_bounds__(kSmallThreads)
 dec_small_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,

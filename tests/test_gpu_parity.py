@@ -776,7 +776,7 @@ def test_group_decode_as_shards(b64):
 
 
 def test_decode_fast_path_small_sizes(b64):
-    """b64_decode_ex takes the single-launch cluster kernel up to 1.5 Mi chars; the multi-CTA
+    """b64_decode_ex takes the single-launch cluster kernel up to 512 Ki chars; the multi-CTA
     bulk kernel (b64_decode_chunk + finalize) must agree with the oracle on the same sizes."""
     std = b64.standard()
     for n in (0, 1, 2, 3, 767, 768, 3 * 1024 + 2, 100_001, 768 * 300 + 1, 3_000_000, 3_200_000):
@@ -800,7 +800,7 @@ def test_decode_fast_path_small_sizes(b64):
 
 
 def test_decode_ex_small_path_many_ctas(b64):
-    """Around the cluster-size and kSmallMax boundaries (16 CTAs x 16 warps x 1024 chars; 1.5 Mi chars),
+    """Around the cluster-size and kSmallMax boundaries (16 CTAs x 16 warps x 1024 chars; 512 Ki chars),
     errors at the start, middle and in the final quad (the prefetched chunk loop and its tail)."""
     std = b64.standard()
     for m_chars in (16 * 1024 - 4, 16 * 1024, 256 * 1024, 256 * 1024 + 4096, (512 << 10) - 4, 512 << 10,
