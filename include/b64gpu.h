@@ -335,7 +335,10 @@ int b64_decode_host_ex(const uint8_t *h_in, int64_t m, uint8_t *h_out, const b64
                        b64_stream_t s_comp, b64_stream_t s_d2h, unsigned flags);
 
 /* ---- batched (BASELINE.json configs[3]) ------------------------------------ */
-/* `count` independent strings concatenated in d_in; string i is
+/* (d_in / d_out must be valid device pointers when count > 0, even if every
+ * string is empty -- the library cannot see the total length without reading
+ * the device offsets.)
+ * `count` independent strings concatenated in d_in; string i is
  * d_in[d_in_off[i] .. d_in_off[i+1]) (d_in_off: device int64[count+1],
  * non-decreasing, d_in_off[0] >= 0).  Output string i is written at
  * d_out + d_out_off[i] (device int64[count], caller-computed):

@@ -488,6 +488,8 @@ def encode_batch(x: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = 
     """Per-string padded encode of strings concatenated in x (offsets int64[count+1]).
     Returns (out, out_off) with out_off = exclusive scan of 4*ceil(len/3) (int64[count+1])."""
     _check_u8(x, "x")
+    if x.numel() == 0:  # all strings empty: the C ABI still wants a valid (unread) pointer
+        x = torch.empty(1, dtype=torch.uint8, device=x.device)
     _check_i64(in_off, "in_off")
     count = in_off.numel() - 1
     if out_off is None:
@@ -509,6 +511,8 @@ def decode_batch(t: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = 
     """Per-string validating decode.  Returns (out, out_off, status int32, err_off int64
     (relative, -1 = ok), out_len int64); out_off = exclusive scan of 3*(len//4)."""
     _check_u8(t, "t")
+    if t.numel() == 0:  # all strings empty: the C ABI still wants a valid (unread) pointer
+        t = torch.empty(1, dtype=torch.uint8, device=t.device)
     _check_i64(in_off, "in_off")
     count = in_off.numel() - 1
     dev = t.device

@@ -1,0 +1,140 @@
+"""Property-based GPU fuzzing (hypothesis): random lengths, alignments, alphabets (incl.
+lenient), corruptions and entry points -- every result compared with the oracle, element
+by element.  Seeded (derandomized) so a failure reproduces."""
+
+import numpy as np
+import pytest
+import torch
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+SETTINGS = settings(max_examples=400, deadline=None, derandomize=True,
+                    suppress_health_check=[HealthCheck.function_scoped_fixture, HealthCheck.too_slow])
+
+
+@pytest.fixture(scope="module")
+def b64():
+    import __graft_entry__ as g
+
+    g.build()
+    import paper_1910_05109_b200 as m
+
+    return m
+
+
+def _alpha(b64, kind, seed):
+    if kind == "std":
+        return oracle.STANDARD, oracle.PAD, b64.standard()
+    if kind == "url":
+        return oracle.URL, oracle.PAD, b64.url()
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(127)[:65]
+    chars, pad = bytes(perm[:64].tolist()), int(perm[64])
+    return chars, pad, b64.alphabet(chars, bytes([pad]))
+
+
+def _dev(x, off):
+    buf = torch.empty(x.size + off + 64, dtype=torch.uint8, device=DEV)
+    t = buf[off: off + x.size]
+    if x.size:
+        t.copy_(torch.from_numpy(x))
+    return t
+
+
+lengths = st.one_of(st.integers(0, 40), st.integers(0, 5000), st.integers(760, 800), st.integers(0, 300_000))
+
+
+@SETTINGS
+@given(n=lengths, kind=st.sampled_from(["std", "url", "custom"]), aseed=st.integers(0, 50),
+       off_in=st.sampled_from([0, 0, 1, 3, 8]), off_out=st.sampled_from([0, 0, 1, 2, 16]),
+       lenient=st.booleans(), k_bad=st.integers(0, 3), seed=st.integers(0, 10_000),
+       api=st.sampled_from(["single", "chunk", "group", "codec", "stream", "batch"]))
+def test_fuzz_encode_decode_vs_oracle(b64, n, kind, aseed, off_in, off_out, lenient, k_bad, seed, api):
+    chars, pad, alpha = _alpha(b64, kind, aseed)
+    if lenient:
+        alpha = b64.lenient_of(alpha)
+    x = synth.data(n, seed=seed)
+    ref_t = oracle.encode(x, chars, pad)
+    text = ref_t.copy()
+    if k_bad and text.size:
+        pos, bad = synth.corruption(min(k_bad, text.size), text.size, chars, seed=seed, pad=pad)
+        text[pos] = bad
+        if seed % 5 == 0 and text.size >= 4:
+            text[-4 + seed % 4] = pad  # a misplaced pad in the final quad
+    ref, rerr, rst = oracle.decode(text, chars, pad, lenient=lenient)
+    m = text.size
+    if api == "single":
+        t = b64.encode(_dev(x, off_in), alpha, out=torch.empty(m + off_out + 8, dtype=torch.uint8,
+                                                               device=DEV)[off_out:])
+        assert np.array_equal(t.cpu().numpy(), ref_t)
+        obuf = torch.empty(3 * (m // 4) + off_out + 8, dtype=torch.uint8, device=DEV)
+        out, info = b64.decode_async(_dev(text, off_in), alpha, out=obuf[off_out: off_out + max(3 * (m // 4), 1)])
+        err, stt, olen = info.tolist()
+        got = out[:olen].cpu().numpy()
+    elif api == "chunk":
+        cut = (m // 3) // 4 * 4
+        dt = _dev(text, off_in)
+        cell = torch.full((1,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+        o = torch.empty(3 * (m // 4) + 8, dtype=torch.uint8, device=DEV)
+        if m:
+            b64.decode_chunk(dt[:cut], 0, False, cell, alpha, out=o[: 3 * cut // 4 + 1])
+            b64.decode_chunk(dt[cut:], cut, True, cell, alpha, out=o[3 * cut // 4:])
+        eo = torch.empty(1, dtype=torch.int64, device=DEV)
+        sto = torch.zeros(1, dtype=torch.int32, device=DEV)
+        b64.decode_finalize(cell, eo, sto)
+        err, stt = int(eo.item()), int(sto.item())
+        olen = ref.size if err < 0 else 3 * (err // 4)
+        got = o[:olen].cpu().numpy()
+    elif api in ("group", "codec"):
+        dx, dt = _dev(x, off_in), _dev(text, off_in)
+        if api == "group":
+            (eo,) = b64.encode_group([dx], alpha)
+            (o,), e, s = b64.decode_group([dt], alpha)
+        else:
+            (eo,), (o,), e, s = b64.codec_group([dx], [dt], alpha, alpha)
+        assert np.array_equal(eo.cpu().numpy(), ref_t)
+        err, stt = int(e.item()), int(s.item())
+        olen = ref.size if err < 0 else 3 * (err // 4)
+        got = o[:olen].cpu().numpy()
+    elif api == "stream":
+        es, ds = b64.EncodeStream(alpha), b64.DecodeStream(alpha)
+        dx, dt = _dev(x, off_in), _dev(text, off_in)
+        rng = np.random.default_rng(seed)
+        parts, p = [], 0
+        while p < n:
+            k = int(rng.integers(0, 5000))
+            parts.append(es.update(dx[p: p + k]).cpu().numpy())
+            p += k
+        parts.append(es.end().cpu().numpy())
+        assert np.array_equal(np.concatenate(parts), ref_t)
+        parts, p = [], 0
+        while p < m:
+            k = int(rng.integers(0, 7000))
+            parts.append(ds.update(dt[p: p + k]).cpu().numpy())
+            p += k
+        tail, info = ds.end()
+        parts.append(tail.cpu().numpy())
+        err, stt, olen = info.tolist()
+        got = np.concatenate(parts)[:olen]
+    else:  # batch of the text cut into pieces at random quad boundaries, plus the text itself
+        rng = np.random.default_rng(seed)
+        cuts = sorted(set([0, m] + [int(4 * v) for v in rng.integers(0, m // 4 + 1, 4)]))
+        in_off = np.array(cuts + [m + m], dtype=np.int64)  # last string = the whole text again
+        cat = np.concatenate([text, text])
+        out, ooff, sts, errs, olens = b64.decode_batch(_dev(cat, off_in), torch.from_numpy(in_off).to(DEV), alpha)
+        rout, rooff, rst_, rerr_, rolen = oracle.decode_batch(cat, in_off, chars, pad, lenient=lenient)
+        assert np.array_equal(sts.cpu().numpy(), rst_) and np.array_equal(errs.cpu().numpy(), rerr_)
+        assert np.array_equal(olens.cpu().numpy(), rolen)
+        o = out.cpu().numpy()
+        for i in range(len(rolen)):
+            assert np.array_equal(o[rooff[i]: rooff[i] + rolen[i]], rout[rooff[i]: rooff[i] + rolen[i]]), i
+        return
+    assert (err, stt) == (rerr, rst), (api, n, err, stt, rerr, rst)
+    assert olen == ref.size
+    assert np.array_equal(got, ref)
