@@ -51,9 +51,10 @@ def parse():
     p.add_argument("--e2e-chunk-mib", type=int, default=64, help="host pipeline chunk (MiB of input per chunk)")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to exercise N>1 on one GPU")
-    p.add_argument("--step", choices=("auto", "codec", "split"), default="auto",
-                   help="headline step: one b64_codec_group launch (decode + encode CTAs) or two grouped launches; "
-                        "auto = codec at N=1, split at N>1 (the error combine then overlaps the encode launch)")
+    p.add_argument("--step", choices=("auto", "fused", "codec", "split"), default="auto",
+                   help="headline step: one b64_codec_group_fused launch (decode + encode CTAs, finalize in the "
+                        "kernel), one b64_codec_group launch + finalize, or two grouped launches + finalize; "
+                        "auto = fused at N=1, split at N>1 (the error combine then overlaps the encode launch)")
     p.add_argument("--combine", choices=("nccl", "peer"), default="nccl",
                    help="N>1 first-error combine: NCCL all_reduce(MIN) (default) or the one-sided peer-memory "
                         "kernel (dist.PeerCombine, SURVEY 8(f) f4; 'peer' also runs it at N=1).  Never run "
@@ -188,7 +189,7 @@ def run_ours(args):
     if args.step == "auto":
         # N > 1: the cross-rank error combine must follow the decodes; with two launches it
         # overlaps the encode launch, with one codec launch it would be exposed
-        args.step = "codec" if world == 1 or args.combine == "peer" else "split"
+        args.step = "fused" if world == 1 else ("codec" if args.combine == "peer" else "split")
     dev = torch.device("cuda", torch.cuda.current_device())
     L = b64._lib.lib()
     stream = torch.cuda.current_stream()
@@ -276,6 +277,18 @@ def run_ours(args):
             raise RuntimeError(f"C ABI returned {rc}")
         combine_end()
 
+    ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+    codec_f = L.b64_codec_group_fused
+    ticket_p = V(ticket.data_ptr())
+
+    def step_fused(rec):
+        """One step as ONE launch (b64_codec_group_fused): decode CTAs + encode CTAs, the kernel's last
+        CTA writes err_off/status and leaves the error words at ERR_NONE (and its ticket at 0) for the
+        next step -- no fill, no finalize launch."""
+        rc = timed("codec", rec, codec_f, enc_items, k, dec_items, k, err_p, st_p, ticket_p, sp)
+        if rc:
+            raise RuntimeError(f"C ABI returned {rc}")
+
     def step_codec(rec):
         """One step as ONE mixed launch (b64_codec_group: decode CTAs + encode CTAs), the finalize on
         the side stream once the kernel is done."""
@@ -356,11 +369,13 @@ def run_ours(args):
 
     # headline: the step as ONE mixed launch (default) or as two grouped launches; the other form is
     # reported beside it ("split" always gives the per-direction rates)
-    head = step_codec if args.step == "codec" else step_group
+    head = {"fused": step_fused, "codec": step_codec, "split": step_group}[args.step]
+    cells.fill_(b64.ERR_NONE)  # the fused step keeps them at ERR_NONE itself from here on
+    ticket.zero_()
     total_ms, op_ms, launches, wall, sampler = run(head, args.steps, args.warmup)
     value = b64_bytes_all * args.steps / (total_ms * 1e-3) / 1e9
     sp_steps = max(10, args.steps // 2)
-    if args.step == "codec":
+    if args.step != "split":
         sp_total, sp_ms, _, _, _ = run(step_group, sp_steps, max(3, args.warmup // 2))
     else:
         sp_total, sp_ms = total_ms * sp_steps / args.steps, op_ms
@@ -407,7 +422,7 @@ def run_ours(args):
     memcpy_gbs = cases[0].m / (mc1 * 1e-3) / 1e9  # base64 bytes per second, same convention as the codec
     memcpy6_gbs = sum(c.m for c in cases) / (mc6 * 1e-3) / 1e9
 
-    if args.step == "codec":  # the dominant (only) codec kernel of the step
+    if args.step in ("fused", "codec"):  # the dominant (only) codec kernel of the step
         codec_avg = statistics.mean(op_ms["codec"])
         kname, alg, kavg, mix_key = "codec_group_kernel", enc_alg + dec_alg, codec_avg, "mixed"
     else:
@@ -447,10 +462,11 @@ def run_ours(args):
         "config": {"workload": "configs[1]: 64 MiB x {n, n+1, n+2} x {standard, base64url} encode + validating decode "
                                "per rank (weak scaling, shards of one stream)",
                    "bytes_per_rank_per_case": N_BYTES, "ops_per_step": 2 * k,
-                   "launches_per_step": ("b64_codec_group (6 decodes + 6 encodes, 1 kernel) + "
-                                         "b64_decode_finalize_n (1 kernel)") if args.step == "codec" else
-                                        ("b64_decode_group (6 cases, 1 kernel) + b64_encode_group (1 kernel) + "
-                                         "b64_decode_finalize_n (1 kernel)"),
+                   "launches_per_step": {
+                       "fused": "b64_codec_group_fused (6 decodes + 6 encodes + finalize, 1 kernel)",
+                       "codec": "b64_codec_group (6 decodes + 6 encodes, 1 kernel) + b64_decode_finalize_n (1 kernel)",
+                       "split": "b64_decode_group (6 cases, 1 kernel) + b64_encode_group (1 kernel) + "
+                                "b64_decode_finalize_n (1 kernel)"}[args.step],
                    "l2": "flushed before every step (256 MiB write + 256 MiB read); 1.7 GB of disjoint buffers per step",
                    "parallelism": f"dp{world}", "volume": "base64 bytes (encode output + decode input), GB=1e9"},
         "encode_gbs": round(enc_gbs, 1), "decode_gbs": round(dec_gbs, 1),
@@ -466,7 +482,7 @@ def run_ours(args):
                      "frac_of_nominal_8000": round(ach / 8000.0, 4),  # BASELINE north star's ~8 TB/s (context)
                      "alg_bytes_per_launch": int(alg), "avg_launch_ms": round(kavg, 5),
                      "units": ("6 decodes (m + 3m/4 - pads bytes each) + 6 encodes (n + 4ceil(n/3)) per launch"
-                               if args.step == "codec" else "6 cases of one direction per launch")},
+                               if args.step != "split" else "6 cases of one direction per launch")},
         "gpu_launches": int(launches), "wall_s_timed_region": round(wall, 3),
         "clocks": sampler.summary(),
     }

@@ -209,6 +209,18 @@ int b64_decode_group(const b64_decode_item *items, int64_t count, b64_stream_t s
  * before anything is launched. */
 int b64_codec_group(const b64_encode_item *enc, int64_t n_enc, const b64_decode_item *dec, int64_t n_dec,
                     b64_stream_t stream);
+/* b64_codec_group with the finalize fused into the kernel: ONE launch, no
+ * initialisation and no finalize launch.  Every item must be fast-path aligned
+ * (encode d_in 8 B / d_out 32 B, decode d_in 32 B / d_out 16 B), n_enc <= 8,
+ * n_dec <= 8 (else B64_EINVAL, nothing launched).  Each decode item's
+ * *d_err_min must hold B64_ERR_NONE before the call; d_ticket (device uint32)
+ * must be 0.  The last CTA of the kernel writes d_err_off[i] (-1 or the first
+ * error position, positions base_offset-relative as b64_decode_chunk) and
+ * d_status[i] (nullable) for decode item i, then resets every item's
+ * *d_err_min to B64_ERR_NONE and *d_ticket to 0 -- so back-to-back calls need
+ * no set-up in between.  (Items sharing one error word get the same result.) */
+int b64_codec_group_fused(const b64_encode_item *enc, int64_t n_enc, const b64_decode_item *dec, int64_t n_dec,
+                          int64_t *d_err_off, int32_t *d_status, uint32_t *d_ticket, b64_stream_t stream);
 /* b64_decode_finalize for `count` consecutive packed words. */
 int b64_decode_finalize_n(const int64_t *d_err_min, int64_t count, int64_t *d_err_off, int32_t *d_status,
                           b64_stream_t stream);

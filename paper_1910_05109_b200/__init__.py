@@ -24,7 +24,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "lenient_of", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
     "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "launch_count", "HostPipeline", "new_info", "decode_unpadded", "decode_ws",
-    "encode_group", "decode_group", "codec_group", "EncodeStream", "DecodeStream",
+    "encode_group", "decode_group", "codec_group", "codec_group_fused", "EncodeStream", "DecodeStream",
     "ERR_NONE",
 ]
 
@@ -271,6 +271,30 @@ def decode_group(ts, alphabets=None, outs=None, cells: Optional[torch.Tensor] = 
     _lib.check(_lib.lib().b64_decode_group(items, len(ts), _stream(stream)), "b64_decode_group")
     err, st = _finalize_n(cells, len(ts), ts[0].device, stream)
     return outs, err, st
+
+
+def codec_group_fused(xs, ts, enc_alphabets=None, dec_alphabets=None, enc_outs=None, dec_outs=None,
+                      cells: Optional[torch.Tensor] = None, ticket: Optional[torch.Tensor] = None,
+                      err: Optional[torch.Tensor] = None, status: Optional[torch.Tensor] = None,
+                      stream: Optional[torch.cuda.Stream] = None):
+    """b64_codec_group_fused: up to 8 encodes + 8 decodes (fast-path aligned) in ONE launch whose
+    last CTA also writes err/status and resets `cells` (ERR_NONE) and `ticket` (0) -- pass the
+    same cells/ticket to back-to-back calls and no set-up launch is needed.  Returns
+    (encoded list, decoded list, err_off int64[len(ts)], status int32[len(ts)])."""
+    dev = (xs[0] if xs else ts[0]).device
+    eitems, eouts = _enc_items(xs, enc_alphabets, enc_outs)
+    if ts:
+        ditems, douts, cells = _dec_items(ts, dec_alphabets, dec_outs, cells, None, None)
+    else:
+        ditems, douts = (_lib.DecodeItem * 1)(), []
+    if ticket is None:
+        ticket = torch.zeros(1, dtype=torch.int32, device=dev)
+    k = max(len(ts), 1)
+    err = err if err is not None else torch.empty(k, dtype=torch.int64, device=dev)
+    status = status if status is not None else torch.empty(k, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib().b64_codec_group_fused(eitems, len(xs), ditems, len(ts), _ptr(err), _ptr(status),
+                                                _ptr(ticket), _stream(stream)), "b64_codec_group_fused")
+    return eouts, douts, err[: len(ts)], status[: len(ts)]
 
 
 def codec_group(xs, ts, enc_alphabets=None, dec_alphabets=None, enc_outs=None, dec_outs=None,

@@ -808,16 +808,18 @@ struct GroupBuilder {
 
     GroupBuilder(const DevInfo* d, b64_stream_t st) : di(d), stream(st) { std::memset(&g, 0, sizeof(g)); }
 
+    bool fused = false;  // b64_codec_group_fused: everything in ONE codec launch, nothing else
+
     int flush() {
         const int nd = g.d.count, ne = g.e.count;
-        if (nd + ne == 0) return B64_OK;
+        if (nd + ne == 0 && !fused) return B64_OK;
         cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
         const int dd = enc_depth(bytes);
         const int64_t wmax = int64_t(di->sms) * cap_bps(di->occ_group[dd]) * (kThreads / 32);
         int64_t C[2 * kGroupMax];
         for (int i = 0; i < nd; ++i) C[i] = g.d.cstart[i + 1] - g.d.cstart[i];
         for (int i = 0; i < ne; ++i) C[nd + i] = g.e.cstart[i + 1] - g.e.cstart[i];
-        if (nd && ne) {
+        if ((nd && ne) || fused) {
             // one partition over both kinds (a decode and an encode chunk move the same 1792 B);
             // each kind's warps are rounded up to whole CTAs, so one CTA of headroom is kept
             int32_t w[2 * kGroupMax + 1];
@@ -825,8 +827,9 @@ struct GroupBuilder {
             for (int i = 0; i <= nd; ++i) g.d.wstart[i] = w[i];
             for (int i = 0; i <= ne; ++i) g.e.wstart[i] = w[nd + i] - w[nd];
             const int64_t wpb = kThreads / 32;
-            g.dec_blocks = std::max<int64_t>(1, (int64_t(w[nd]) + wpb - 1) / wpb);
-            const int64_t eb = std::max<int64_t>(1, (int64_t(w[nd + ne] - w[nd]) + wpb - 1) / wpb);
+            g.dec_blocks = nd ? std::max<int64_t>(1, (int64_t(w[nd]) + wpb - 1) / wpb) : 0;
+            const int64_t eb = ne ? std::max<int64_t>(1, (int64_t(w[nd + ne] - w[nd]) + wpb - 1) / wpb) : 0;
+            if (g.dec_blocks + eb == 0) g.dec_blocks = 1;  // fused call with nothing to code: finalize only
             launch(pick2(dd, codec_group_kernel<1>, codec_group_kernel<2>), g.dec_blocks + eb, kThreads, s, g);
         } else if (nd) {
             const int64_t blocks = group_partition(C, nd, wmax, g.d.wstart);
@@ -844,10 +847,13 @@ struct GroupBuilder {
     int add(const b64_encode_item& it) {
         if (it.n == 0) return B64_OK;
         const int64_t nc = it.n / 768;
-        if (!(aligned(it.d_in, 8) && aligned(it.d_out, 32)) || nc >= kGroupChunkMax)  // its own launch
+        if (!(aligned(it.d_in, 8) && aligned(it.d_out, 32)) || nc >= kGroupChunkMax) {  // its own launch
+            if (fused) return B64_EINVAL;
             return b64_encode(it.d_in, it.n, it.d_out, it.a, stream);
+        }
         EncGroup& e = g.e;
         if (e.count == kGroupMax || e.cstart[e.count] + nc >= kGroupChunkMax) {
+            if (fused) return B64_EINVAL;
             const int r = flush();
             if (r != B64_OK) return r;
         }
@@ -863,16 +869,19 @@ struct GroupBuilder {
         return B64_OK;
     }
 
-    int add(const b64_decode_item& it) {
-        if (it.m == 0) return B64_OK;
+    int add(const b64_decode_item& it, int index = 0) {
+        if (it.m == 0 && !fused) return B64_OK;  // (fused: even an empty stream gets its result)
         const int64_t Q = it.m / 4;
         const int64_t Qint = (it.is_final && Q > 0) ? Q - 1 : Q;
         const int64_t nc = Qint / 256;
-        if (!(aligned(it.d_in, 32) && aligned(it.d_out, 16)) || nc >= kGroupChunkMax)
+        if (!(aligned(it.d_in, 32) && aligned(it.d_out, 16)) || nc >= kGroupChunkMax) {
+            if (fused) return B64_EINVAL;
             return b64_decode_chunk(it.d_in, it.m, it.d_out, it.a, it.base_offset, it.is_final, it.d_err_min,
                                     nullptr, stream);
+        }
         DecGroup& d = g.d;
         if (d.count == kGroupMax || d.cstart[d.count] + nc >= kGroupChunkMax) {
+            if (fused) return B64_EINVAL;
             const int r = flush();
             if (r != B64_OK) return r;
         }
@@ -888,6 +897,7 @@ struct GroupBuilder {
         std::memcpy(d.lut[k], it.a->dec, 256);
         d.cstart[k + 1] = d.cstart[k] + nc;
         d.count = k + 1;
+        g.didx[k] = index;
         bytes += it.m;
         return B64_OK;
     }
@@ -926,6 +936,26 @@ int b64_codec_group(const b64_encode_item* enc, int64_t n_enc, const b64_decode_
         if (i < n_dec && (r = gb.add(dec[i])) != B64_OK) return r;
         if (i < n_enc && (r = gb.add(enc[i])) != B64_OK) return r;
     }
+    return gb.flush();
+}
+
+int b64_codec_group_fused(const b64_encode_item* enc, int64_t n_enc, const b64_decode_item* dec, int64_t n_dec,
+                          int64_t* d_err_off, int32_t* d_status, uint32_t* d_ticket, b64_stream_t stream) {
+    int r = check_enc_items(enc, n_enc);
+    if (r == B64_OK) r = check_dec_items(dec, n_dec);
+    if (r != B64_OK) return r;
+    if (n_enc > kGroupMax || n_dec > kGroupMax || !d_ticket || (n_dec > 0 && !d_err_off)) return B64_EINVAL;
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    GroupBuilder gb(di, stream);
+    gb.fused = true;
+    for (int64_t i = 0; i < n_dec; ++i)
+        if ((r = gb.add(dec[i], int(i))) != B64_OK) return r;
+    for (int64_t i = 0; i < n_enc; ++i)
+        if ((r = gb.add(enc[i])) != B64_OK) return r;
+    gb.g.ticket = d_ticket;
+    gb.g.err_off = d_err_off;
+    gb.g.status = d_status;
     return gb.flush();
 }
 

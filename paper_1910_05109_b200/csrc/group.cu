@@ -166,13 +166,51 @@ struct CodecGroup {
     DecGroup d;
     EncGroup e;
     int64_t dec_blocks;
+    // Fused finalize (b64_codec_group_fused; ticket == nullptr: none).  The last CTA to
+    // finish maps every decode stream's error word to (err_off, status) at index didx[k]
+    // and resets the word to kErrNone and the ticket to 0, so the next call needs no
+    // initialisation launch and no finalize launch.
+    unsigned int* ticket;
+    int64_t* err_off;
+    int32_t* status;
+    int32_t didx[kGroupMax];
 };
+
+// "Last block" epilogue of the fused finalize (the classic threadfence reduction):
+// every thread fences its own writes (outputs, error-word atomics), the CTA barriers,
+// one thread takes a ticket; the CTA holding the last ticket sees every other CTA's
+// writes and finalises.
+__device__ __forceinline__ void codec_fused_finalize(const CodecGroup& g) {
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(g.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int k = threadIdx.x;
+    unsigned long long wv = kErrNone;
+    if (k < g.d.count) {
+        wv = atomicMax(g.d.cell[k], 0ull);  // atomic read (L2), never stale
+        if (wv >= kErrNone) {
+            g.err_off[g.didx[k]] = -1;
+            if (g.status) g.status[g.didx[k]] = kOk;
+        } else {
+            g.err_off[g.didx[k]] = int64_t(wv >> 3);
+            if (g.status) g.status[g.didx[k]] = int32_t(wv & 7);
+        }
+    }
+    __syncthreads();  // every word read before any (possibly shared) word is reset
+    if (k < g.d.count) *g.d.cell[k] = kErrNone;
+    if (k == 0) *g.ticket = 0u;
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) codec_group_kernel(const __grid_constant__ CodecGroup g) {
     const int64_t b = blockIdx.x;
     if (b < g.dec_blocks) dec_group_body<D>(g.d, b, g.dec_blocks);
     else enc_group_body<D>(g.e, b - g.dec_blocks, int64_t(gridDim.x) - g.dec_blocks);
+    if (g.ticket) codec_fused_finalize(g);
 }
 
 // Packed error words -> (err_off, status) for count streams.

@@ -55,7 +55,7 @@ def test_our_arm_contract():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    # one codec launch + finalize per step (or decode group + encode group + finalize)
-    assert d["gpu_launches"] in (2 * d["steps"], 3 * d["steps"])
+    # one fused codec launch per step (or codec + finalize, or decode group + encode group + finalize)
+    assert d["gpu_launches"] in (d["steps"], 2 * d["steps"], 3 * d["steps"])
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["cpu_baseline"]["kind"] == "oracle"

@@ -389,14 +389,20 @@ def test_config2_bench_step_grouped(b64):
         ref, rerr, rst = oracle.decode(texts[i], chars, pad)
         assert (errc[i], stc[i]) == (rerr, rst), i
         assert np.array_equal(douts[i][: ref.size].cpu().numpy(), ref), i
-    # the bench's headline launch: the same 6 + 6 jobs as ONE b64_codec_group kernel
-    eouts, douts, err, st = b64.codec_group(dxs, dts, alph, alph)
-    errc, stc = err.cpu().numpy(), st.cpu().numpy()
-    for i, (n, chars, pad, _) in enumerate(cases):
-        assert np.array_equal(eouts[i].cpu().numpy(), refs[i]), i
-        ref, rerr, rst = oracle.decode(texts[i], chars, pad)
-        assert (errc[i], stc[i]) == (rerr, rst), i
-        assert np.array_equal(douts[i][: ref.size].cpu().numpy(), ref), i
+    # the bench's headline launches: the same 6 + 6 jobs as ONE b64_codec_group kernel, and as the
+    # fused one (finalize in the kernel) twice in a row on the same error words
+    results = [b64.codec_group(dxs, dts, alph, alph)]
+    cells = torch.full((6,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+    ticket = torch.zeros(1, dtype=torch.int32, device=DEV)
+    for _ in range(2):
+        results.append(b64.codec_group_fused(dxs, dts, alph, alph, cells=cells, ticket=ticket))
+    for eouts, douts, err, st in results:
+        errc, stc = err.cpu().numpy(), st.cpu().numpy()
+        for i, (n, chars, pad, _) in enumerate(cases):
+            assert np.array_equal(eouts[i].cpu().numpy(), refs[i]), i
+            ref, rerr, rst = oracle.decode(texts[i], chars, pad)
+            assert (errc[i], stc[i]) == (rerr, rst), i
+            assert np.array_equal(douts[i][: ref.size].cpu().numpy(), ref), i
 
 
 def _windows(total, count, width, seed):
@@ -745,6 +751,49 @@ def test_codec_group_mixed(b64):
     assert douts == [] and err is None
     for i in range(3):
         assert np.array_equal(eouts[i].cpu().numpy(), oracle.encode(xs[i], *chars_l[i])), i
+
+
+def test_codec_group_fused(b64):
+    """b64_codec_group_fused: ONE launch whose last CTA finalises and resets the error words and
+    the ticket; back-to-back calls with the same cells / ticket and changing corruptions, empty
+    items, a decode-only and an encode-only call, and the refusal of non-fusable lists."""
+    al = _alphabets(b64)
+    sizes = [3 << 20, 768 * 5 + 1, 0, 100_003, (1 << 20) + 2]
+    xs = [synth.data(n, seed=60 + i) for i, n in enumerate(sizes)]
+    chars_l = [al[i % len(al)][:2] for i in range(len(sizes))]
+    alph_l = [al[i % len(al)][2] for i in range(len(sizes))]
+    refs = [oracle.encode(x, *chars_l[i]) for i, x in enumerate(xs)]
+    dx = [to_dev(x) for x in xs]
+    cells = torch.full((len(sizes),), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+    ticket = torch.zeros(1, dtype=torch.int32, device=DEV)
+    for rep in range(4):
+        texts = []
+        for i, r in enumerate(refs):
+            t = r.copy()
+            if (i + rep) % 2 and t.size > 4:
+                pos, bad = synth.corruption(1 + rep, t.size, chars_l[i][0], seed=10 * rep + i, pad=chars_l[i][1])
+                t[pos] = bad
+            texts.append(t)
+        dt = [to_dev(t) for t in texts]
+        eouts, douts, err, st = b64.codec_group_fused(dx, dt, alph_l, alph_l, cells=cells, ticket=ticket)
+        errc, stc = err.cpu().numpy(), st.cpu().numpy()
+        for i in range(len(sizes)):
+            assert np.array_equal(eouts[i].cpu().numpy(), refs[i]), (rep, i)
+            ref, rerr, rst = oracle.decode(texts[i], *chars_l[i])
+            assert (errc[i], stc[i]) == (rerr, rst), (rep, i)
+            k = ref.size if rerr < 0 else 3 * (rerr // 4)
+            assert np.array_equal(douts[i][:k].cpu().numpy(), ref[:k]), (rep, i)
+        # the kernel left the words and the ticket ready for the next call
+        assert torch.all(cells == b64.ERR_NONE) and int(ticket.item()) == 0
+    _, douts, err, st = b64.codec_group_fused([], [to_dev(refs[0])], dec_alphabets=alph_l[0], cells=cells[:1],
+                                              ticket=ticket)
+    assert int(err.item()) == -1 and torch.equal(douts[0][: xs[0].size], dx[0])
+    eouts, _, _, _ = b64.codec_group_fused(dx[:2], [], alph_l[:2], ticket=ticket)
+    assert np.array_equal(eouts[1].cpu().numpy(), refs[1]) and int(ticket.item()) == 0
+    with pytest.raises(b64.B64Error, match="EINVAL"):  # misaligned item: not fusable
+        b64.codec_group_fused([to_dev(xs[1], 1)], [], alph_l[1], ticket=ticket)
+    with pytest.raises(b64.B64Error, match="EINVAL"):  # more than 8 items
+        b64.codec_group_fused(dx[1:2] * 9, [], alph_l[1], ticket=ticket)
 
 
 def test_group_decode_as_shards(b64):
