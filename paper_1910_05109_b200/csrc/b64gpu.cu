@@ -8,3 +8,4 @@
 #include "stream.cu"
 #include "peer.cu"
 #include "capi.cu"
+#include "capi_ext.cu"

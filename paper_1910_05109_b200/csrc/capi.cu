@@ -1,6 +1,8 @@
 // capi.cu -- the C ABI of include/b64gpu.h: argument checks, alphabet
-// validation, launch configuration and kernel dispatch.  No allocation, no
-// per-call state; every launch goes to the caller's stream.
+// validation, launch configuration and kernel dispatch for the single-stream,
+// decode-variant, grouped and batched entry points (capi_ext.cu: streaming,
+// peer combine, host pipelines).  No allocation, no per-call state; every
+// launch goes to the caller's stream.
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -457,339 +459,6 @@ int b64_decode_finalize(const int64_t* d_err_min, int64_t* d_err_off, int32_t* d
     return launched();
 }
 
-// ---------------------------------------------------------------- streaming (stream.cu)
-// The host side of a stream only does length arithmetic (held / consumed /
-// produced are functions of the piece lengths), so no call waits for the
-// device; the held bytes themselves live in the caller's device carry buffer.
-namespace {
-enum { kStIdle = 0, kStEncode = 1, kStDecode = 2, kStDone = 3 };
-}
-
-int b64_encode_stream_begin(b64_stream* st, uint8_t* d_carry) {
-    if (!st || !d_carry) return B64_EINVAL;
-    st->consumed = st->produced = 0;
-    st->held = 0;
-    st->state = kStEncode;
-    st->d_carry = d_carry;
-    st->d_err_min = nullptr;
-    return B64_OK;
-}
-
-int b64_encode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabet* a,
-                             int64_t* n_out, b64_stream_t stream) {
-    if (!st || st->state != kStEncode || n < 0 || !alpha_ok(a) || (n > 0 && !d_in)) return B64_EINVAL;
-    const int64_t H = st->held, A = H + n, T = A / 3;
-    if (T > 0 && !d_out) return B64_EINVAL;
-    if (n_out) *n_out = 4 * T;
-    if (n == 0) return B64_OK;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int join = (H > 0 && T > 0) ? 1 : 0;
-    if (H > 0 || A % 3) {  // a straddling triple and / or bytes to hold
-        launch(enc_stream_join_kernel, 1, 1, s, st->d_carry, int(H), d_in, n, d_out, enc_tab(a));
-        const int r = launched();
-        if (r != B64_OK) return r;
-    }
-    const int64_t skip = join ? 3 - H : 0, tb = T - join;  // whole triples read straight from the piece
-    if (tb > 0) {
-        const int r = b64_encode(d_in + skip, 3 * tb, d_out + 4 * join, a, stream);
-        if (r != B64_OK) return r;
-    }
-    st->held = int32_t(A % 3);
-    st->consumed += n;
-    st->produced += 4 * T;
-    return B64_OK;
-}
-
-int b64_encode_stream_end(b64_stream* st, uint8_t* d_out, const b64_alphabet* a, int64_t* n_out,
-                          b64_stream_t stream) {
-    if (!st || st->state != kStEncode || !alpha_ok(a)) return B64_EINVAL;
-    const int H = st->held;
-    if (H > 0 && !d_out) return B64_EINVAL;
-    if (n_out) *n_out = H > 0 ? 4 : 0;
-    if (H > 0) {
-        launch(enc_stream_end_kernel, 1, 1, reinterpret_cast<cudaStream_t>(stream), st->d_carry, H, d_out, enc_tab(a),
-               uint32_t(a->pad));
-        const int r = launched();
-        if (r != B64_OK) return r;
-        st->produced += 4;
-    }
-    st->held = 0;
-    st->state = kStDone;
-    return B64_OK;
-}
-
-int b64_decode_stream_begin(b64_stream* st, uint8_t* d_carry, int64_t* d_err_min, b64_stream_t stream) {
-    if (!st || !d_carry || !d_err_min) return B64_EINVAL;
-    if (cudaMemsetAsync(d_err_min, 0x7F, sizeof(int64_t), reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
-        return B64_ECUDA;
-    st->consumed = st->produced = 0;
-    st->held = 0;
-    st->state = kStDecode;
-    st->d_carry = d_carry;
-    st->d_err_min = d_err_min;
-    return B64_OK;
-}
-
-int b64_decode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a,
-                             int64_t* n_out, b64_stream_t stream) {
-    if (!st || st->state != kStDecode || m < 0 || !alpha_ok(a) || (m > 0 && !d_in)) return B64_EINVAL;
-    const int64_t H = st->held, A = H + m;
-    const int64_t Q = A > 0 ? (A - 1) / 4 : 0;  // the last 1..4 chars are always held
-    if (Q > 0 && !d_out) return B64_EINVAL;
-    if (n_out) *n_out = 3 * Q;
-    if (m == 0) return B64_OK;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int join = (H > 0 && Q > 0) ? 1 : 0;
-    launch(dec_stream_join_kernel, 1, 1, s, st->d_carry, int(H), d_in, m, d_out, dec_tab(a), st->consumed - H,
-           reinterpret_cast<unsigned long long*>(st->d_err_min));
-    int r = launched();
-    if (r != B64_OK) return r;
-    const int64_t skip = join ? 4 - H : 0, qb = Q - join;  // whole quads read straight from the piece
-    if (qb > 0) {
-        r = b64_decode_chunk(d_in + skip, 4 * qb, d_out + 3 * join, a, st->consumed + skip, 0, st->d_err_min,
-                             nullptr, stream);
-        if (r != B64_OK) return r;
-    }
-    st->held = int32_t(A - 4 * Q);
-    st->consumed += m;
-    st->produced += 3 * Q;
-    return B64_OK;
-}
-
-int b64_decode_stream_end(b64_stream* st, uint8_t* d_out, const b64_alphabet* a, int64_t* d_err_off,
-                          int32_t* d_status, int64_t* d_out_len, int64_t* n_out, b64_stream_t stream) {
-    if (!st || st->state != kStDecode || !alpha_ok(a) || !d_err_off) return B64_EINVAL;
-    const int64_t total = st->consumed;
-    const bool fin = total > 0 && total % 4 == 0;
-    if (fin && !d_out) return B64_EINVAL;
-    launch(dec_stream_end_kernel, 1, 1, reinterpret_cast<cudaStream_t>(stream), st->d_carry, int(st->held), total,
-           d_out, dec_tab(a), reinterpret_cast<const unsigned long long*>(st->d_err_min), d_err_off, d_status,
-           d_out_len);
-    const int r = launched();
-    if (r != B64_OK) return r;
-    if (n_out) *n_out = fin ? 3 : 0;  // bytes of d_out the end call may write (the exact count is in *d_out_len)
-    st->held = 0;
-    st->state = kStDone;
-    return B64_OK;
-}
-
-// ---------------------------------------------------------------- one-sided peer combine (peer.cu)
-int64_t b64_peer_combine_bytes(int64_t count) { return count < 0 ? -1 : kPeerSlotsOff + 16 * count; }
-
-int b64_peer_combine_init(uint8_t* d_buf, int64_t count, b64_stream_t stream) {
-    if (!d_buf || count < 0) return B64_EINVAL;
-    launch(peer_buffer_init_kernel, 1, kThreads, reinterpret_cast<cudaStream_t>(stream), d_buf, count);
-    return launched();
-}
-
-int b64_peer_combine(uint8_t* const* d_bufs, int world, int rank, const int64_t* d_local, int64_t count,
-                     uint64_t epoch, int64_t* d_err_off, int32_t* d_status, b64_stream_t stream) {
-    if (!d_bufs || world < 1 || world > 32 || rank < 0 || rank >= world || count < 0 || count > 4096 ||
-        (count > 0 && (!d_local || !d_err_off)))
-        return B64_EINVAL;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(1);
-    cfg.blockDim = dim3(32);
-    cfg.dynamicSmemBytes = size_t(count) * 8;
-    cfg.stream = reinterpret_cast<cudaStream_t>(stream);
-    if (cudaLaunchKernelEx(&cfg, peer_combine_kernel, d_bufs, world, rank,
-                           reinterpret_cast<const unsigned long long*>(d_local), count,
-                           static_cast<unsigned long long>(epoch), d_err_off, d_status) != cudaSuccess)
-        return (cudaGetLastError(), B64_ECUDA);
-    return launched();
-}
-
-int b64_peer_buffer_alloc(int64_t bytes, uint8_t** d_buf, uint8_t handle[64]) {
-    if (bytes <= 0 || !d_buf || !handle) return B64_EINVAL;
-    void* p = nullptr;
-    if (cudaMalloc(&p, size_t(bytes)) != cudaSuccess) return (cudaGetLastError(), B64_ECUDA);
-    cudaIpcMemHandle_t h;
-    if (cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
-        cudaFree(p);
-        return (cudaGetLastError(), B64_ECUDA);
-    }
-    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
-    std::memcpy(handle, &h, 64);
-    *d_buf = static_cast<uint8_t*>(p);
-    return B64_OK;
-}
-
-int b64_peer_buffer_open(const uint8_t handle[64], uint8_t** d_buf) {
-    if (!handle || !d_buf) return B64_EINVAL;
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, handle, 64);
-    void* p = nullptr;
-    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
-        return (cudaGetLastError(), B64_ECUDA);
-    *d_buf = static_cast<uint8_t*>(p);
-    return B64_OK;
-}
-
-int b64_peer_buffer_release(uint8_t* d_buf, int opened) {
-    if (!d_buf) return B64_EINVAL;
-    const cudaError_t e = opened ? cudaIpcCloseMemHandle(d_buf) : cudaFree(d_buf);
-    return e == cudaSuccess ? B64_OK : (cudaGetLastError(), B64_ECUDA);
-}
-
-int b64_peer_combine_emulate(uint8_t* const* d_bufs, int world, const int64_t* d_local, int64_t count, int epochs,
-                             int64_t* d_out, int* d_ok, b64_stream_t stream) {
-    if (!d_bufs || world < 1 || world > 32 || count < 0 || epochs < 0 || !d_ok || (count > 0 && (!d_local || !d_out)))
-        return B64_EINVAL;
-    uint8_t* const* b = d_bufs;
-    int w = world;
-    const unsigned long long* l = reinterpret_cast<const unsigned long long*>(d_local);
-    int64_t k = count;
-    int e = epochs;
-    unsigned long long* o = reinterpret_cast<unsigned long long*>(d_out);
-    int* okp = d_ok;
-    void* args[] = {&b, &w, &l, &k, &e, &o, &okp};
-    // all `world` blocks wait on one another: a cooperative launch guarantees they are co-resident
-    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(peer_combine_emulate_kernel), dim3(world), dim3(32),
-                                    args, 0, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
-        return (cudaGetLastError(), B64_ECUDA);
-    return launched();
-}
-
-// ---------------------------------------------------------------- host-buffer pipelines
-// Chunks of the host input are copied H2D on s_h2d, coded on s_comp and copied
-// back D2H on s_d2h through kHostBufs rotating device buffers, so both PCIe
-// directions and the kernels overlap.  Cross-stream order uses events created
-// for the call and released at its end (the library keeps no state).
-namespace {
-constexpr int kHostBufs = 3;
-
-struct HostPipe {
-    cudaEvent_t h2d[kHostBufs], comp[kHostBufs], d2h[kHostBufs];
-    bool ok = true;
-    HostPipe() {
-        for (int i = 0; i < kHostBufs; ++i) {
-            ok &= cudaEventCreateWithFlags(&h2d[i], cudaEventDisableTiming) == cudaSuccess;
-            ok &= cudaEventCreateWithFlags(&comp[i], cudaEventDisableTiming) == cudaSuccess;
-            ok &= cudaEventCreateWithFlags(&d2h[i], cudaEventDisableTiming) == cudaSuccess;
-        }
-    }
-    // The workspace buffers may still be in use by work already queued on the
-    // three streams (a previous call): the first copy of this call waits for it.
-    cudaError_t order_after_previous(cudaStream_t sh, cudaStream_t sc, cudaStream_t sd) {
-        cudaError_t e = cudaEventRecord(comp[0], sc);
-        if (e == cudaSuccess) e = cudaEventRecord(d2h[0], sd);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(sh, comp[0], 0);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(sh, d2h[0], 0);
-        return e;
-    }
-    ~HostPipe() {
-        for (int i = 0; i < kHostBufs; ++i) {
-            cudaEventDestroy(h2d[i]);
-            cudaEventDestroy(comp[i]);
-            cudaEventDestroy(d2h[i]);
-        }
-    }
-};
-
-int64_t align_down(int64_t v, int64_t a) { return v / a * a; }
-}  // namespace
-
-int64_t b64_host_workspace_bytes(int64_t chunk_bytes) {
-    if (chunk_bytes <= 0) return -1;
-    const int64_t c = align_down(chunk_bytes, 3072) > 0 ? align_down(chunk_bytes, 3072) : 3072;
-    return kHostBufs * (c + (c / 3) * 4 + 512) + 256;
-}
-
-int b64_encode_host(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
-                    int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h) {
-    return b64_encode_host_ex(h_in, n, h_out, a, d_ws, ws_bytes, s_h2d, s_comp, s_d2h, 0u);
-}
-
-int b64_encode_host_ex(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
-                       int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h,
-                       unsigned flags) {
-    if (n < 0 || !alpha_ok(a) || (flags & ~unsigned(B64_HOST_CALLER_ORDERED))) return B64_EINVAL;
-    if (n == 0) return B64_OK;
-    if (!h_in || !h_out || !d_ws) return B64_EINVAL;
-    // per buffer: C input bytes + 4C/3 output chars; C a multiple of 3072 (= 4 * 768, keeps both aligned)
-    const int64_t per = (ws_bytes - 256) / kHostBufs - 512;
-    const int64_t C = align_down(per * 3 / 7, 3072);
-    if (C <= 0) return B64_EINVAL;
-    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
-    cudaStream_t sh = reinterpret_cast<cudaStream_t>(s_h2d), sc = reinterpret_cast<cudaStream_t>(s_comp),
-                 sd = reinterpret_cast<cudaStream_t>(s_d2h);
-    HostPipe pipe;
-    if (!pipe.ok) return B64_ECUDA;
-    if (!(flags & B64_HOST_CALLER_ORDERED) && pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
-    const int64_t stride = C + C / 3 * 4 + 512;
-    int64_t j = 0;
-    for (int64_t off = 0; off < n; off += C, ++j) {
-        const int b = int(j % kHostBufs);
-        uint8_t* din = base + b * stride;
-        uint8_t* dout = din + C + 256;
-        const int64_t len = (n - off < C) ? n - off : C;
-        const int64_t olen = b64_encoded_len(len);
-        if (j >= kHostBufs && cudaStreamWaitEvent(sh, pipe.d2h[b], 0) != cudaSuccess) return B64_ECUDA;
-        if (cudaMemcpyAsync(din, h_in + off, size_t(len), cudaMemcpyHostToDevice, sh) != cudaSuccess) return B64_ECUDA;
-        cudaEventRecord(pipe.h2d[b], sh);
-        cudaStreamWaitEvent(sc, pipe.h2d[b], 0);
-        const int r = b64_encode(din, len, dout, a, s_comp);
-        if (r != B64_OK) return r;
-        cudaEventRecord(pipe.comp[b], sc);
-        cudaStreamWaitEvent(sd, pipe.comp[b], 0);
-        if (cudaMemcpyAsync(h_out + off / 3 * 4, dout, size_t(olen), cudaMemcpyDeviceToHost, sd) != cudaSuccess)
-            return B64_ECUDA;
-        cudaEventRecord(pipe.d2h[b], sd);
-    }
-    return cudaPeekAtLastError() == cudaSuccess ? B64_OK : (cudaGetLastError(), B64_ECUDA);
-}
-
-int b64_decode_host(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
-                    int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, b64_stream_t s_h2d,
-                    b64_stream_t s_comp, b64_stream_t s_d2h) {
-    return b64_decode_host_ex(h_in, m, h_out, a, d_ws, ws_bytes, d_err_off, d_status, s_h2d, s_comp, s_d2h, 0u);
-}
-
-int b64_decode_host_ex(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
-                       int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, b64_stream_t s_h2d,
-                       b64_stream_t s_comp, b64_stream_t s_d2h, unsigned flags) {
-    if (m < 0 || !alpha_ok(a) || !d_err_off || (flags & ~unsigned(B64_HOST_CALLER_ORDERED))) return B64_EINVAL;
-    if (m % 4) return B64_ELENGTH;
-    if (m > 0 && (!h_in || !h_out || !d_ws)) return B64_EINVAL;
-    cudaStream_t sh = reinterpret_cast<cudaStream_t>(s_h2d), sc = reinterpret_cast<cudaStream_t>(s_comp),
-                 sd = reinterpret_cast<cudaStream_t>(s_d2h);
-    if (m == 0) {
-        if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), sc) != cudaSuccess) return B64_ECUDA;
-        return b64_decode_finalize(d_err_off, d_err_off, d_status, s_comp);
-    }
-    if (!d_ws) return B64_EINVAL;
-    // per buffer: C chars + 3C/4 bytes; C a multiple of 4096 (= 4 * 1024)
-    const int64_t per = (ws_bytes - 256) / kHostBufs - 512;
-    const int64_t C = align_down(per * 4 / 7, 4096);
-    if (C <= 0) return B64_EINVAL;
-    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
-    HostPipe pipe;
-    if (!pipe.ok) return B64_ECUDA;
-    if (!(flags & B64_HOST_CALLER_ORDERED) && pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
-    if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), sc) != cudaSuccess) return B64_ECUDA;
-    const int64_t stride = C + C / 4 * 3 + 512;
-    int64_t j = 0;
-    for (int64_t off = 0; off < m; off += C, ++j) {
-        const int b = int(j % kHostBufs);
-        uint8_t* din = base + b * stride;
-        uint8_t* dout = din + C + 256;
-        const int64_t len = (m - off < C) ? m - off : C;
-        const bool fin = off + len == m;
-        if (j >= kHostBufs && cudaStreamWaitEvent(sh, pipe.d2h[b], 0) != cudaSuccess) return B64_ECUDA;
-        if (cudaMemcpyAsync(din, h_in + off, size_t(len), cudaMemcpyHostToDevice, sh) != cudaSuccess) return B64_ECUDA;
-        cudaEventRecord(pipe.h2d[b], sh);
-        cudaStreamWaitEvent(sc, pipe.h2d[b], 0);
-        const int r = b64_decode_chunk(din, len, dout, a, off, fin ? 1 : 0, d_err_off, nullptr, s_comp);
-        if (r != B64_OK) return r;
-        cudaEventRecord(pipe.comp[b], sc);
-        cudaStreamWaitEvent(sd, pipe.comp[b], 0);
-        if (cudaMemcpyAsync(h_out + off / 4 * 3, dout, size_t(len / 4 * 3), cudaMemcpyDeviceToHost, sd) != cudaSuccess)
-            return B64_ECUDA;
-        cudaEventRecord(pipe.d2h[b], sd);
-    }
-    return b64_decode_finalize(d_err_off, d_err_off, d_status, s_comp);
-}
-
 // ---------------------------------------------------------------- grouped launches
 // Items are collected into one pending group of up to kGroupMax decodes and
 // kGroupMax encodes; a flush launches dec_group_kernel, enc_group_kernel, or --
@@ -1006,11 +675,11 @@ int b64_decode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count
     Offsets off{d_in_off, d_out_off, count, 0};
     const int64_t blocks = int64_t(di->sms) * di->occ_dec_gen;
     launch(dec_generic_kernel, blocks, kThreads, s, d_in, d_out, off, dec_tab(a), 0, 1,
-                                                             reinterpret_cast<unsigned long long*>(d_err_off), nullptr);
+           reinterpret_cast<unsigned long long*>(d_err_off), nullptr);
     r = launched();
     if (r != B64_OK) return r;
     launch(dec_batch_finalize_kernel, small, kThreads, s, d_in, d_in_off, count, a->pad, d_status,
-                                                                   d_err_off, d_out_len);
+           d_err_off, d_out_len);
     return launched();
 }
 
@@ -1020,7 +689,8 @@ const char* b64_build_info(void) {
 #define B64_STR2(x) #x
 #define B64_STR(x) B64_STR2(x)
     return "b64gpu sm_100a, nvcc " B64_STR(__CUDACC_VER_MAJOR__) "." B64_STR(__CUDACC_VER_MINOR__)
-           "; kernels enc_fast enc_generic dec_fast dec_generic dec_finalize_* dec_batch_*";
+           "; kernels enc_fast dec_fast enc_generic dec_generic {enc,dec,codec}_group dec_small ws_* "
+           "{enc,dec}_stream_* peer_combine dec_finalize_* dec_batch_*";
 }
 
 }  // extern "C"
