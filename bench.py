@@ -56,9 +56,9 @@ def parse():
                         "kernel), one b64_codec_group launch + finalize, or two grouped launches + finalize; "
                         "auto = fused at N=1, split at N>1 (the error combine then overlaps the encode launch)")
     p.add_argument("--combine", choices=("nccl", "peer"), default="nccl",
-                   help="N>1 first-error combine: NCCL all_reduce(MIN) (default) or the one-sided peer-memory "
-                        "kernel (dist.PeerCombine, SURVEY 8(f) f4; 'peer' also runs it at N=1).  Never run "
-                        "'peer' with several ranks on ONE GPU: its kernels wait on each other")
+                   help="N>1 first-error combine: NCCL all_reduce(MIN) (default) or over peer memory inside the "
+                        "fused codec kernel (dist.PeerCombine, SURVEY 8(f) f4; 'peer' also runs it at N=1).  Never "
+                        "run 'peer' with several ranks on ONE GPU: its kernels wait on each other")
     return p.parse_args()
 
 
@@ -189,7 +189,7 @@ def run_ours(args):
     if args.step == "auto":
         # N > 1: the cross-rank error combine must follow the decodes; with two launches it
         # overlaps the encode launch, with one codec launch it would be exposed
-        args.step = "fused" if world == 1 else ("codec" if args.combine == "peer" else "split")
+        args.step = "fused" if world == 1 or args.combine == "peer" else "split"
     dev = torch.device("cuda", torch.cuda.current_device())
     L = b64._lib.lib()
     stream = torch.cuda.current_stream()
@@ -289,6 +289,14 @@ def run_ours(args):
         if rc:
             raise RuntimeError(f"C ABI returned {rc}")
 
+    def step_fused_peer(rec):
+        """One step as ONE launch whose last CTA also takes the cross-rank MIN over peer memory
+        (b64_codec_group_fused_peer; --combine peer)."""
+        rc = timed("codec", rec, lambda: pc.codec_fused(enc_items, k, dec_items, err_off, status, ticket,
+                                                          stream=stream) or 0)
+        if rc:
+            raise RuntimeError(f"C ABI returned {rc}")
+
     def step_codec(rec):
         """One step as ONE mixed launch (b64_codec_group: decode CTAs + encode CTAs), the finalize on
         the side stream once the kernel is done."""
@@ -369,7 +377,9 @@ def run_ours(args):
 
     # headline: the step as ONE mixed launch (default) or as two grouped launches; the other form is
     # reported beside it ("split" always gives the per-direction rates)
-    head = {"fused": step_fused, "codec": step_codec, "split": step_group}[args.step]
+    if args.combine == "peer" and args.step in ("fused", "codec"):
+        args.step = "fused_peer"
+    head = {"fused": step_fused, "fused_peer": step_fused_peer, "codec": step_codec, "split": step_group}[args.step]
     cells.fill_(b64.ERR_NONE)  # the fused step keeps them at ERR_NONE itself from here on
     ticket.zero_()
     total_ms, op_ms, launches, wall, sampler = run(head, args.steps, args.warmup)
@@ -422,7 +432,7 @@ def run_ours(args):
     memcpy_gbs = cases[0].m / (mc1 * 1e-3) / 1e9  # base64 bytes per second, same convention as the codec
     memcpy6_gbs = sum(c.m for c in cases) / (mc6 * 1e-3) / 1e9
 
-    if args.step in ("fused", "codec"):  # the dominant (only) codec kernel of the step
+    if args.step != "split":  # the dominant (only) codec kernel of the step
         codec_avg = statistics.mean(op_ms["codec"])
         kname, alg, kavg, mix_key = "codec_group_kernel", enc_alg + dec_alg, codec_avg, "mixed"
     else:
@@ -464,6 +474,8 @@ def run_ours(args):
                    "bytes_per_rank_per_case": N_BYTES, "ops_per_step": 2 * k,
                    "launches_per_step": {
                        "fused": "b64_codec_group_fused (6 decodes + 6 encodes + finalize, 1 kernel)",
+                       "fused_peer": "b64_codec_group_fused_peer (6 decodes + 6 encodes + cross-rank MIN over "
+                                     "peer memory + finalize, 1 kernel)",
                        "codec": "b64_codec_group (6 decodes + 6 encodes, 1 kernel) + b64_decode_finalize_n (1 kernel)",
                        "split": "b64_decode_group (6 cases, 1 kernel) + b64_encode_group (1 kernel) + "
                                 "b64_decode_finalize_n (1 kernel)"}[args.step],

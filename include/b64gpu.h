@@ -221,6 +221,18 @@ int b64_codec_group(const b64_encode_item *enc, int64_t n_enc, const b64_decode_
  * no set-up in between.  (Items sharing one error word get the same result.) */
 int b64_codec_group_fused(const b64_encode_item *enc, int64_t n_enc, const b64_decode_item *dec, int64_t n_dec,
                           int64_t *d_err_off, int32_t *d_status, uint32_t *d_ticket, b64_stream_t stream);
+/* b64_codec_group_fused for one rank of a multi-GPU job:
+ * the kernel's last CTA also combines the error words with every rank's over
+ * peer memory (the b64_peer_combine protocol below: d_peer_bufs / world / rank /
+ * epoch exactly as for b64_peer_combine, buffers sized
+ * b64_peer_combine_bytes(n_dec)) before it finalises, so d_err_off / d_status
+ * hold the GLOBAL first error -- decode, collective and finalize in ONE
+ * kernel.  Every rank must make the call with the same n_dec and epoch; on a
+ * peer timeout d_err_off[i] = -2, d_status[i] = -1.  d_peer_bufs == NULL is
+ * b64_codec_group_fused. */
+int b64_codec_group_fused_peer(const b64_encode_item *enc, int64_t n_enc, const b64_decode_item *dec, int64_t n_dec,
+                               int64_t *d_err_off, int32_t *d_status, uint32_t *d_ticket, uint8_t *const *d_peer_bufs,
+                               int world, int rank, uint64_t epoch, b64_stream_t stream);
 /* b64_decode_finalize for `count` consecutive packed words. */
 int b64_decode_finalize_n(const int64_t *d_err_min, int64_t count, int64_t *d_err_off, int32_t *d_status,
                           b64_stream_t stream);

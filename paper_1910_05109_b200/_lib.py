@@ -85,6 +85,7 @@ SIGNATURES = [
     ("b64_decode_group", INT, [P, I64, P]),
     ("b64_codec_group", INT, [P, I64, P, I64, P]),
     ("b64_codec_group_fused", INT, [P, I64, P, I64, P, P, P, P]),
+    ("b64_codec_group_fused_peer", INT, [P, I64, P, I64, P, P, P, P, INT, INT, ctypes.c_uint64, P]),
     ("b64_decode_finalize_n", INT, [P, I64, P, P, P]),
     ("b64_encode_stream_begin", INT, [SP, P]),
     ("b64_encode_stream_update", INT, [SP, P, I64, P, AP, I64P, P]),

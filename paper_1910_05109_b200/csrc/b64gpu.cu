@@ -2,10 +2,10 @@
 // compilation: the templated kernels are instantiated and launched in one TU).
 #include "encode.cu"
 #include "decode.cu"
+#include "peer.cu"
 #include "group.cu"
 #include "small.cu"
 #include "mime.cu"
 #include "stream.cu"
-#include "peer.cu"
 #include "capi.cu"
 #include "capi_ext.cu"

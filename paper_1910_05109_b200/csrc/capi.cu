@@ -610,6 +610,13 @@ int b64_codec_group(const b64_encode_item* enc, int64_t n_enc, const b64_decode_
 
 int b64_codec_group_fused(const b64_encode_item* enc, int64_t n_enc, const b64_decode_item* dec, int64_t n_dec,
                           int64_t* d_err_off, int32_t* d_status, uint32_t* d_ticket, b64_stream_t stream) {
+    return b64_codec_group_fused_peer(enc, n_enc, dec, n_dec, d_err_off, d_status, d_ticket, nullptr, 1, 0, 0, stream);
+}
+
+int b64_codec_group_fused_peer(const b64_encode_item* enc, int64_t n_enc, const b64_decode_item* dec, int64_t n_dec,
+                               int64_t* d_err_off, int32_t* d_status, uint32_t* d_ticket, uint8_t* const* d_peer_bufs,
+                               int world, int rank, uint64_t epoch, b64_stream_t stream) {
+    if (d_peer_bufs && (world < 1 || world > 32 || rank < 0 || rank >= world)) return B64_EINVAL;
     int r = check_enc_items(enc, n_enc);
     if (r == B64_OK) r = check_dec_items(dec, n_dec);
     if (r != B64_OK) return r;
@@ -625,6 +632,10 @@ int b64_codec_group_fused(const b64_encode_item* enc, int64_t n_enc, const b64_d
     gb.g.ticket = d_ticket;
     gb.g.err_off = d_err_off;
     gb.g.status = d_status;
+    gb.g.peer_bufs = d_peer_bufs;
+    gb.g.world = world;
+    gb.g.rank = rank;
+    gb.g.epoch = static_cast<unsigned long long>(epoch);
     return gb.flush();
 }
 

@@ -174,6 +174,12 @@ struct CodecGroup {
     int64_t* err_off;
     int32_t* status;
     int32_t didx[kGroupMax];
+    // Fused cross-rank MIN (b64_codec_group_fused_peer; peer_bufs == nullptr: none): the last
+    // CTA combines the error words with every rank's over peer memory (peer.cu) before it
+    // finalises -- the decode, the collective and the finalize in ONE kernel.
+    uint8_t* const* peer_bufs;
+    int32_t world, rank;
+    unsigned long long epoch;
 };
 
 // "Last block" epilogue of the fused finalize (the classic threadfence reduction):
@@ -188,11 +194,27 @@ __device__ __forceinline__ void codec_fused_finalize(const CodecGroup& g) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    __shared__ unsigned long long s_w[kGroupMax], s_g[kGroupMax];
+    __shared__ bool s_ok;
     const int k = threadIdx.x;
-    unsigned long long wv = kErrNone;
+    if (k < g.d.count) s_w[k] = atomicMax(g.d.cell[k], 0ull);  // atomic read (L2), never stale
+    if (k == 0) s_ok = true;
+    __syncthreads();
+    if (g.peer_bufs) {  // one warp: MIN with every rank's words over peer memory
+        if (k < 32) {
+            const bool ok = peer_min_epoch(g.peer_bufs, g.world, g.rank, s_w, g.d.count, g.epoch, s_g);
+            if (k == 0) s_ok = ok;
+        }
+    } else if (k < g.d.count) {
+        s_g[k] = s_w[k];
+    }
+    __syncthreads();
     if (k < g.d.count) {
-        wv = atomicMax(g.d.cell[k], 0ull);  // atomic read (L2), never stale
-        if (wv >= kErrNone) {
+        const unsigned long long wv = s_g[k];
+        if (!s_ok) {  // a peer never arrived (peer.cu timeout)
+            g.err_off[g.didx[k]] = -2;
+            if (g.status) g.status[g.didx[k]] = -1;
+        } else if (wv >= kErrNone) {
             g.err_off[g.didx[k]] = -1;
             if (g.status) g.status[g.didx[k]] = kOk;
         } else {

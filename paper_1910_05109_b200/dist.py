@@ -192,6 +192,21 @@ class PeerCombine:
             "b64_peer_combine")
         self.epoch += 1
 
+    def codec_fused(self, enc_items, n_enc: int, dec_items, err_off: torch.Tensor, status: Optional[torch.Tensor],
+                    ticket: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """b64_codec_group_fused_peer: this rank's encodes + decodes in ONE kernel whose last CTA
+        also takes the global MIN of the `count` error words over peer memory and finalises
+        (err_off / status = the global first errors).  One epoch per call, as combine()."""
+        import ctypes
+
+        s = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        self._lib.check(self._lib.lib().b64_codec_group_fused_peer(
+            enc_items, n_enc, dec_items, self.count, ctypes.c_void_p(err_off.data_ptr()),
+            ctypes.c_void_p(status.data_ptr()) if status is not None else None, ctypes.c_void_p(ticket.data_ptr()),
+            ctypes.c_void_p(self.d_bufs.data_ptr()), self.world, self.rank, self.epoch,
+            ctypes.c_void_p(s.cuda_stream)), "b64_codec_group_fused_peer")
+        self.epoch += 1
+
     def close(self) -> None:
         import ctypes
 

@@ -1211,6 +1211,41 @@ def test_peer_combine_emulated_ranks(b64):
             assert np.all(raw[8: 8 + 2 * K] == b64_err_none())
 
 
+def test_codec_fused_peer_world1(b64):
+    """b64_codec_group_fused_peer at world 1 (dist.PeerCombine.codec_fused): the codec kernel's
+    last CTA runs the peer-memory MIN protocol before it finalises; results equal the oracle,
+    epoch after epoch, and the error words / ticket are left ready."""
+    from paper_1910_05109_b200 import dist as b64dist
+
+    xs = [synth.data(n, seed=80 + n) for n in (1 << 20, 768 * 7 + 2, 3)]
+    refs = [oracle.encode(x) for x in xs]
+    dx = [to_dev(x) for x in xs]
+    pc = b64dist.PeerCombine(len(xs))
+    try:
+        cells = torch.full((len(xs),), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+        ticket = torch.zeros(1, dtype=torch.int32, device=DEV)
+        for e in range(5):
+            texts = [r.copy() for r in refs]
+            if e % 2:
+                texts[0][1000 + e] = ord("!")
+                texts[2][-1] = ord("?")
+            dt = [to_dev(t) for t in texts]
+            eitems, eouts = b64._enc_items(dx, None, None)
+            ditems, douts, _ = b64._dec_items(dt, None, None, cells, None, None)
+            err = torch.empty(len(xs), dtype=torch.int64, device=DEV)
+            st = torch.empty(len(xs), dtype=torch.int32, device=DEV)
+            pc.codec_fused(eitems, len(xs), ditems, err, st, ticket)
+            torch.cuda.synchronize()
+            for i in range(len(xs)):
+                assert np.array_equal(eouts[i].cpu().numpy(), refs[i]), (e, i)
+                ref, rerr, rst = oracle.decode(texts[i])
+                assert (int(err[i].item()), int(st[i].item())) == (rerr, rst), (e, i)
+                assert np.array_equal(douts[i][: ref.size].cpu().numpy(), ref), (e, i)
+            assert torch.all(cells == b64.ERR_NONE) and int(ticket.item()) == 0
+    finally:
+        pc.close()
+
+
 def test_peer_combine_world1_api(b64):
     """dist.PeerCombine at world 1 (the per-rank kernel, IPC-allocated buffer): err_off/status
     equal b64_decode_finalize_n of the same words, epoch after epoch."""
