@@ -687,6 +687,7 @@ def extra_configs(b64, synth, torch, dev, stream, flush, Ev):
     del x, enc, eoff, dout, doff
     torch.cuda.empty_cache()
     res["config5_16GiB_1gpu"] = config5_one_gpu(b64, synth, torch, dev, timeit)
+    res["next_rows_1GiB"] = next_rows(b64, synth, torch, dev, timeit)
     return res
 
 
@@ -742,6 +743,105 @@ def config5_one_gpu(b64, synth, torch, dev, timeit):
            "note": "8 dist shards of one stream on one GPU (grouped launches): the strong-scaling N=1 point"}
     del text, out, tparts, oparts
     torch.cuda.empty_cache()
+    return res
+
+
+def next_rows(b64, synth, torch, dev, timeit):
+    """SURVEY.md Sec. 8(f) rows measured on the configs[2] text (1 GiB of data): padding-optional,
+    whitespace-skipping (MIME, CRLF every 76 chars), lenient and streaming (64 MiB pieces) decode,
+    against the plain strict decode of the same bytes; plus the peer-combine kernel at world 1.
+    Direct C-ABI calls (no host syncs inside the timing); L2 flushed between reps."""
+    L = b64._lib.lib()
+    V = ctypes.c_void_p
+    sp = V(torch.cuda.current_stream().cuda_stream)
+    n = 1 << 30
+    x = synth.device_data(n, seed=0)
+    t = b64.encode(x)                      # strict text, m = 1,431,655,768 chars ('==' at the end)
+    m = t.numel()
+    out = torch.empty(3 * (m // 4) + 8, dtype=torch.uint8, device=dev)
+    info = b64.new_info(dev)
+    ip = info.data_ptr()
+    std, url = b64.standard(), b64.url()
+    res = {}
+
+    def rate(ms, in_bytes, out_bytes):
+        return {"ms": round(ms, 4), "input_gbs": round(in_bytes / (ms * 1e-3) / 1e9, 1),
+                "traffic_gbs": round((in_bytes + out_bytes) / (ms * 1e-3) / 1e9, 1)}
+
+    def ex(tt, mm, a):
+        b64._lib.check(L.b64_decode_ex(V(tt.data_ptr()), mm, V(out.data_ptr()), ctypes.byref(a), V(ip), V(ip + 8),
+                                       V(ip + 16), sp), "b64_decode_ex")
+
+    for _ in range(3):  # warm-up: the first launches after the big configs[4] buffers are freed run slow
+        ex(t, m, std)
+    ms = timeit(lambda: ex(t, m, std), reps=10)
+    res["strict"] = rate(ms, m, n)
+    lenient = b64.lenient_of(std)
+    ms = timeit(lambda: ex(t, m, lenient), reps=10)
+    res["lenient"] = rate(ms, m, n)
+    assert int(info[0].item()) == -1
+    # padding-optional: the base64url text without its '=' (m - 2 chars)
+    tu = b64.encode(x, url)[: m - 2]
+
+    def unp():
+        b64._lib.check(L.b64_decode_unpadded(V(tu.data_ptr()), m - 2, V(out.data_ptr()), ctypes.byref(url), V(ip),
+                                             V(ip + 8), V(ip + 16), sp), "b64_decode_unpadded")
+
+    ms = timeit(unp, reps=10)
+    assert int(info[0].item()) == -1 and int(info[2].item()) == n
+    res["unpadded"] = rate(ms, m - 2, n)
+    # whitespace-skipping: MIME lines of 76 chars + CRLF
+    lines = m // 76
+    body = t[: lines * 76].view(lines, 76)
+    crlf = torch.tensor([13, 10], dtype=torch.uint8, device=dev).expand(lines, 2)
+    tw = torch.cat([torch.cat([body, crlf], 1).reshape(-1), t[lines * 76:]])
+    mw = tw.numel()
+    del body, crlf
+    ws = torch.empty(int(L.b64_decode_ws_workspace_bytes(mw)), dtype=torch.uint8, device=dev)
+
+    def wsd():
+        b64._lib.check(L.b64_decode_ws(V(tw.data_ptr()), mw, V(out.data_ptr()), ctypes.byref(std), V(ws.data_ptr()),
+                                       ws.numel(), V(ip), V(ip + 8), V(ip + 16), sp), "b64_decode_ws")
+
+    ms = timeit(wsd, reps=5)
+    assert int(info[0].item()) == -1 and int(info[2].item()) == n
+    res["whitespace_mime76"] = dict(rate(ms, mw, n), note="input = text incl. CRLF; kernels move ~4.75 B per char "
+                                                          "(count, compact, decode) against 1.75 algorithmic")
+    del tw, ws
+    # streaming: the strict text in 64 MiB pieces (plus the carry joins and the end call)
+    carry = torch.zeros(8, dtype=torch.uint8, device=dev)
+    cell = torch.empty(1, dtype=torch.int64, device=dev)
+    piece = 64 << 20
+
+    def streamed():
+        stt = b64._lib.Stream()
+        L.b64_decode_stream_begin(ctypes.byref(stt), V(carry.data_ptr()), V(cell.data_ptr()), sp)
+        o, p_ = 0, 0
+        n_out = ctypes.c_int64(0)
+        while p_ < m:
+            k_ = min(piece + 3, m - p_)  # odd piece sizes: every piece boundary needs a join
+            b64._lib.check(L.b64_decode_stream_update(ctypes.byref(stt), V(t.data_ptr() + p_), k_,
+                                                      V(out.data_ptr() + o), ctypes.byref(std), ctypes.byref(n_out),
+                                                      sp), "stream_update")
+            o += n_out.value
+            p_ += k_
+        b64._lib.check(L.b64_decode_stream_end(ctypes.byref(stt), V(out.data_ptr() + o), ctypes.byref(std), V(ip),
+                                               V(ip + 8), V(ip + 16), ctypes.byref(n_out), sp), "stream_end")
+
+    ms = timeit(streamed, reps=5)
+    assert int(info[0].item()) == -1 and int(info[2].item()) == n
+    res["streaming_64MiB_pieces"] = rate(ms, m, n)
+    del x, t, tu, out
+    torch.cuda.empty_cache()
+    # one-sided peer combine, world 1 (per-combine kernel latency)
+    from paper_1910_05109_b200 import dist as b64dist
+
+    pc = b64dist.PeerCombine(6)
+    cells = torch.full((6,), b64.ERR_NONE, dtype=torch.int64, device=dev)
+    eo = torch.empty(6, dtype=torch.int64, device=dev)
+    ms = timeit(lambda: pc.combine(cells, eo), reps=20, do_flush=False)
+    pc.close()
+    res["peer_combine_world1_us"] = round(ms * 1e3, 2)
     return res
 
 

@@ -59,6 +59,11 @@ __device__ __forceinline__ uint2 ld64_l1(const void* p) {
     asm("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
+__device__ __forceinline__ uint4 ld128_nc(const void* p) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
 __device__ __forceinline__ uint32_t ld32(const void* p) {
     uint32_t r;
     asm("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
