@@ -55,10 +55,12 @@ def parse():
                    help="headline step: one b64_codec_group_fused launch (decode + encode CTAs, finalize in the "
                         "kernel), one b64_codec_group launch + finalize, or two grouped launches + finalize; "
                         "auto = fused at N=1, split at N>1 (the error combine then overlaps the encode launch)")
-    p.add_argument("--combine", choices=("nccl", "peer"), default="nccl",
-                   help="N>1 first-error combine: NCCL all_reduce(MIN) (default) or over peer memory inside the "
-                        "fused codec kernel (dist.PeerCombine, SURVEY 8(f) f4; 'peer' also runs it at N=1).  Never "
-                        "run 'peer' with several ranks on ONE GPU: its kernels wait on each other")
+    p.add_argument("--combine", choices=("auto", "nccl", "peer"), default="auto",
+                   help="N>1 first-error combine: over peer memory inside the fused codec kernel "
+                        "(dist.PeerCombine, SURVEY 8(f) f4; 'peer' also runs it at N=1) or NCCL all_reduce(MIN) "
+                        "overlapped with the encode launch; auto = peer at N>1 when its collective self-test "
+                        "passes on every rank, else nccl.  Never run 'peer' with several ranks on ONE GPU "
+                        "(--dist-backend gloo): its kernels wait on each other")
     return p.parse_args()
 
 
@@ -186,10 +188,6 @@ def run_ours(args):
     import synth
 
     world, rank, local = dist_setup(args)
-    if args.step == "auto":
-        # N > 1: the cross-rank error combine must follow the decodes; with two launches it
-        # overlaps the encode launch, with one codec launch it would be exposed
-        args.step = "fused" if world == 1 or args.combine == "peer" else "split"
     dev = torch.device("cuda", torch.cuda.current_device())
     L = b64._lib.lib()
     stream = torch.cuda.current_stream()
@@ -226,10 +224,30 @@ def run_ours(args):
     comm = torch.cuda.Stream(device=dev)
     ev_dec, ev_comm = torch.cuda.Event(), torch.cuda.Event()
     pc = None
-    if args.combine == "peer":
+    if args.combine == "auto":
+        args.combine = "nccl"
+        if world > 1 and args.dist_backend == "nccl":
+            from paper_1910_05109_b200 import dist as b64dist
+
+            try:  # collective: every rank reaches the same verdict
+                pc = b64dist.PeerCombine(len(cases))
+                if pc.validate():
+                    args.combine = "peer"
+                else:
+                    pc.close()
+                    pc = None
+            except RuntimeError as e:
+                print(f"peer combine unavailable ({e}); using NCCL", file=sys.stderr)
+                pc = None
+    elif args.combine == "peer":
         from paper_1910_05109_b200 import dist as b64dist
 
         pc = b64dist.PeerCombine(len(cases))
+    if args.step == "auto":
+        # N > 1: the cross-rank error combine must follow the decodes.  Over peer memory it runs
+        # inside the one codec launch (its last CTA); over NCCL it is a separate collective, which
+        # with two launches overlaps the encode launch and with one codec launch would be exposed
+        args.step = "fused" if world == 1 or args.combine == "peer" else "split"
 
     def combine_begin(finalize):
         ev_dec.record(stream)
@@ -480,7 +498,12 @@ def run_ours(args):
                        "split": "b64_decode_group (6 cases, 1 kernel) + b64_encode_group (1 kernel) + "
                                 "b64_decode_finalize_n (1 kernel)"}[args.step],
                    "l2": "flushed before every step (256 MiB write + 256 MiB read); 1.7 GB of disjoint buffers per step",
-                   "parallelism": f"dp{world}", "volume": "base64 bytes (encode output + decode input), GB=1e9"},
+                   "parallelism": f"dp{world}",
+                   "error_combine": ("none (N=1)" if world == 1 else
+                                     "peer memory, inside the codec kernel" if args.step == "fused_peer" else
+                                     "peer memory, 1 kernel" if args.combine == "peer" else
+                                     "NCCL all_reduce(MIN), overlapped with the encode launch"),
+                   "volume": "base64 bytes (encode output + decode input), GB=1e9"},
         "encode_gbs": round(enc_gbs, 1), "decode_gbs": round(dec_gbs, 1),
         "memcpy_d2d_gbs": round(memcpy_gbs, 1), "memcpy_d2d_6cases_gbs": round(memcpy6_gbs, 1),
         "codec_vs_memcpy": {"encode_time_ratio": round(enc_avg / mc6, 4), "decode_time_ratio": round(dec_avg / mc6, 4),

@@ -165,18 +165,48 @@ class PeerCombine:
         if self.world > 1:
             handles = [None] * self.world
             dist.all_gather_object(handles, bytes(handle.raw), group=group)
-            ptrs = []
+            ptrs, ok = [], True
             for p, h in enumerate(handles):
                 if p == self.rank:
                     ptrs.append(self._own)
                     continue
                 q = ctypes.c_void_p()
-                _lib.check(L.b64_peer_buffer_open(h, ctypes.byref(q)), "b64_peer_buffer_open")
-                self._opened.append(q.value)
-                ptrs.append(q.value)
-            dist.barrier(group=group)  # every buffer is initialised before anyone's first combine
+                if ok and L.b64_peer_buffer_open(h, ctypes.byref(q)) == 0:
+                    self._opened.append(q.value)
+                    ptrs.append(q.value)
+                else:
+                    ok = False
+                    ptrs.append(0)
+            # every rank learns whether every rank mapped every peer (and all buffers are
+            # initialised before anyone's first combine): a MIN over the ranks, not a barrier,
+            # so a rank that failed cannot leave the others waiting
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                                device=self.dev if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            if int(flag.item()) != 1:
+                self.close()
+                raise RuntimeError("PeerCombine: a rank could not map its peers' buffers (CUDA IPC)")
         self.d_bufs = torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
         self.epoch = 0
+
+    def validate(self, group=None) -> bool:
+        """Collective self-test: one combine of rank-specific words against the MIN every rank
+        expects (also a timeout check).  Returns the same verdict on every rank."""
+        import torch.distributed as dist
+
+        words = torch.tensor([((self.rank * 7 + k * 3) % (2 * self.world + 1)) << 3 | 1 for k in range(self.count)],
+                             dtype=torch.int64, device=self.dev)
+        expect = [min(((r * 7 + k * 3) % (2 * self.world + 1)) for r in range(self.world)) for k in range(self.count)]
+        err = torch.empty(self.count, dtype=torch.int64, device=self.dev)
+        self.combine(words, err)
+        torch.cuda.synchronize(self.dev)
+        ok = err.tolist() == expect
+        if self.world > 1:
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                                device=self.dev if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            ok = int(flag.item()) == 1
+        return ok
 
     def combine(self, local: torch.Tensor, err_off: torch.Tensor, status: Optional[torch.Tensor] = None,
                 stream: Optional[torch.cuda.Stream] = None) -> None:

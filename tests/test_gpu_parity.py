@@ -1264,5 +1264,6 @@ def test_peer_combine_world1_api(b64):
             we, ws = _api_form(w)
             assert np.array_equal(err.cpu().numpy(), we), e
             assert np.array_equal(st.cpu().numpy(), ws), e
+        assert pc.validate()  # the bench's collective self-test (world 1: the own buffer only)
     finally:
         pc.close()
