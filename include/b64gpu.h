@@ -214,7 +214,8 @@ int b64_codec_group(const b64_encode_item *enc, int64_t n_enc, const b64_decode_
  * (encode d_in 8 B / d_out 32 B, decode d_in 32 B / d_out 16 B), n_enc <= 8,
  * n_dec <= 8 (else B64_EINVAL, nothing launched).  Each decode item's
  * *d_err_min must hold B64_ERR_NONE before the call; d_ticket (device uint32)
- * must be 0.  The last CTA of the kernel writes d_err_off[i] (-1 or the first
+ * must be 0.  The last decode CTA to finish (encode CTAs may still be running;
+ * with n_dec == 0 one idle decode CTA is launched) writes d_err_off[i] (-1 or the first
  * error position, positions base_offset-relative as b64_decode_chunk) and
  * d_status[i] (nullable) for decode item i, then resets every item's
  * *d_err_min to B64_ERR_NONE and *d_ticket to 0 -- so back-to-back calls need
@@ -222,7 +223,7 @@ int b64_codec_group(const b64_encode_item *enc, int64_t n_enc, const b64_decode_
 int b64_codec_group_fused(const b64_encode_item *enc, int64_t n_enc, const b64_decode_item *dec, int64_t n_dec,
                           int64_t *d_err_off, int32_t *d_status, uint32_t *d_ticket, b64_stream_t stream);
 /* b64_codec_group_fused for one rank of a multi-GPU job:
- * the kernel's last CTA also combines the error words with every rank's over
+ * that last decode CTA also combines the error words with every rank's over
  * peer memory (the b64_peer_combine protocol below: d_peer_bufs / world / rank /
  * epoch exactly as for b64_peer_combine, buffers sized
  * b64_peer_combine_bytes(n_dec)) before it finalises, so d_err_off / d_status
@@ -287,9 +288,10 @@ int b64_decode_stream_end(b64_stream *st, uint8_t *d_out, const b64_alphabet *a,
 /* ---- one-sided cross-GPU error combine ------------ */
 /* The multi-GPU decode's only exchange -- the MIN over ranks of `count` packed
  * error words -- done by ONE small kernel over peer memory instead of an NCCL
- * all_reduce: each rank atomicMin's its words into every rank's buffer
- * (system scope, over NVLink), then arrives on every rank's counter and waits
- * for all arrivals of the epoch on its own.
+ * all_reduce: each rank stores its words into every rank's buffer (system
+ * scope, over NVLink) as 64-bit cells tagged with the epoch, then polls its
+ * own buffer until every rank's cells of the epoch are there and takes their
+ * MIN -- no fence, no atomics.
  *   - Every rank owns one buffer of b64_peer_combine_bytes(count) bytes, set
  *     up once with b64_peer_combine_init, then mapped into every other rank
  *     (CUDA IPC); d_bufs is a DEVICE array of `world` device pointers, d_bufs[p]

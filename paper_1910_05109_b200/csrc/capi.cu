@@ -498,7 +498,7 @@ struct GroupBuilder {
             const int64_t wpb = kThreads / 32;
             g.dec_blocks = nd ? std::max<int64_t>(1, (int64_t(w[nd]) + wpb - 1) / wpb) : 0;
             const int64_t eb = ne ? std::max<int64_t>(1, (int64_t(w[nd + ne] - w[nd]) + wpb - 1) / wpb) : 0;
-            if (g.dec_blocks + eb == 0) g.dec_blocks = 1;  // fused call with nothing to code: finalize only
+            if (fused && g.dec_blocks == 0) g.dec_blocks = 1;  // the finalizing (peer-meeting) CTA, no decodes
             launch(pick2(dd, codec_group_kernel<1>, codec_group_kernel<2>), g.dec_blocks + eb, kThreads, s, g);
         } else if (nd) {
             const int64_t blocks = group_partition(C, nd, wmax, g.d.wstart);

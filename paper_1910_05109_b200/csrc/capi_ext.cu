@@ -121,7 +121,9 @@ int b64_decode_stream_end(b64_stream* st, uint8_t* d_out, const b64_alphabet* a,
 }
 
 // ---------------------------------------------------------------- one-sided peer combine (peer.cu)
-int64_t b64_peer_combine_bytes(int64_t count) { return count < 0 ? -1 : kPeerSlotsOff + 16 * count; }
+int64_t b64_peer_combine_bytes(int64_t count) {
+    return count < 0 ? -1 : std::max<int64_t>(64, 2ll * kPeerMaxWorld * count * 16);
+}
 
 int b64_peer_combine_init(uint8_t* d_buf, int64_t count, b64_stream_t stream) {
     if (!d_buf || count < 0) return B64_EINVAL;

@@ -166,8 +166,8 @@ struct CodecGroup {
     DecGroup d;
     EncGroup e;
     int64_t dec_blocks;
-    // Fused finalize (b64_codec_group_fused; ticket == nullptr: none).  The last CTA to
-    // finish maps every decode stream's error word to (err_off, status) at index didx[k]
+    // Fused finalize (b64_codec_group_fused; ticket == nullptr: none).  The last DECODE CTA
+    // to finish (dec_blocks >= 1 whenever a ticket is given) maps every decode stream's error word to (err_off, status) at index didx[k]
     // and resets the word to kErrNone and the ticket to 0, so the next call needs no
     // initialisation launch and no finalize launch.
     unsigned int* ticket;
@@ -190,7 +190,7 @@ __device__ __forceinline__ void codec_fused_finalize(const CodecGroup& g) {
     __shared__ bool s_last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(g.ticket, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) s_last = atomicAdd(g.ticket, 1u) == unsigned(g.dec_blocks) - 1u;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -230,9 +230,14 @@ __device__ __forceinline__ void codec_fused_finalize(const CodecGroup& g) {
 template <int D>
 __global__ void __launch_bounds__(kThreads, kBulkCtasPerSm) codec_group_kernel(const __grid_constant__ CodecGroup g) {
     const int64_t b = blockIdx.x;
-    if (b < g.dec_blocks) dec_group_body<D>(g.d, b, g.dec_blocks);
-    else enc_group_body<D>(g.e, b - g.dec_blocks, int64_t(gridDim.x) - g.dec_blocks);
-    if (g.ticket) codec_fused_finalize(g);
+    if (b < g.dec_blocks) {
+        dec_group_body<D>(g.d, b, g.dec_blocks);
+        // only the decode CTAs take a ticket: the last of them finalises (and, multi-GPU, meets
+        // the other ranks) while encode CTAs may still be running, off the kernel's tail
+        if (g.ticket) codec_fused_finalize(g);
+    } else {
+        enc_group_body<D>(g.e, b - g.dec_blocks, int64_t(gridDim.x) - g.dec_blocks);
+    }
 }
 
 // Packed error words -> (err_off, status) for count streams.

@@ -2,24 +2,28 @@
 // (DESIGN.md "Multi-GPU").
 //
 // The multi-GPU decode's only exchange is a MIN over ranks of K packed error
-// words (pos << 3 | kind).  Instead of an NCCL all_reduce, every rank writes
-// its words straight into every rank's buffer with system-scope atomicMin
-// over NVLink (peer pointers from CUDA IPC), then signals arrival on every
-// rank's counter; a rank whose counter shows all arrivals of this epoch holds
-// the global MIN in its own buffer.  One tiny kernel, no NCCL launch.
+// words (pos << 3 | kind).  Instead of an NCCL all_reduce, every rank PUSHES
+// its words straight into every rank's buffer over NVLink (peer pointers from
+// CUDA IPC) and then reads the world x K words that arrived in its own buffer
+// and takes their MIN.  There is no fence, no atomic and no separate arrival
+// flag: every word travels as two 64-bit cells {32-bit half, 32-bit epoch
+// tag}, and a single aligned 64-bit store is single-copy atomic, so a reader
+// polling a cell sees either the old cell or the whole new one -- the tag
+// says which (the low-latency protocol NCCL calls LL).  One NVLink one-way
+// latency per combine instead of a round trip for a fence plus the arrival.
 //
-// Per-rank buffer (b64_peer_combine_bytes): two slots of K words + an arrival
-// counter.  Epoch e uses slot e & 1; after reading its slot a rank resets it
-// for epoch e + 2.  Safe because a peer can only write that slot in epoch
-// e + 2 after passing the barrier of epoch e + 1, which needs this rank's
-// arrival in e + 1, issued after the reset.  Counters only grow (epoch e is
-// complete when the counter reaches (e + 1) * world).
+// Per-rank buffer (b64_peer_combine_bytes): two parity slots x kPeerMaxWorld
+// ranks x K words x 2 cells.  Epoch e uses slot e & 1 and tag e + 1.  Rank p
+// overwrites slot e & 1 of another rank's buffer next in epoch e + 2, which it
+// only reaches after epoch e + 1 completed for it -- and that needs this
+// rank's words of epoch e + 1, pushed after this rank finished reading epoch
+// e.  Tags only grow (mod 2^32; a slot is rewritten every other epoch, so a
+// stale tag can never equal the awaited one); the buffer starts zeroed.
 #include "b64_device.cuh"
 
 namespace b64 {
 
-constexpr int64_t kPeerCounterOff = 0;  // uint64 arrival counter, then the two slots (64-byte aligned)
-constexpr int64_t kPeerSlotsOff = 64;
+constexpr int kPeerMaxWorld = 32;
 constexpr unsigned long long kSpinTimeoutNs = 5ull * 1000 * 1000 * 1000;  // 5 s: a peer never arrived
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -28,50 +32,56 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
+__device__ __forceinline__ void st_relaxed_sys_v2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ void ld_relaxed_sys_v2(const unsigned long long* p, unsigned long long& a,
+                                                  unsigned long long& b) {
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+// Cell pair of word k from rank p in parity slot `par` of a buffer.
+__device__ __forceinline__ unsigned long long* peer_cells(uint8_t* buf, int par, int p, int64_t K, int64_t k) {
+    return reinterpret_cast<unsigned long long*>(buf) + ((int64_t(par) * kPeerMaxWorld + p) * K + k) * 2;
 }
 
 // One rank's side of epoch `epoch`, executed by one warp.  bufs[p] is rank p's
 // buffer (peer-mapped), local[0..K) this rank's words.  Writes the global MIN
-// to out[0..K) (packed words); returns false on timeout.
+// to out[0..K) (packed words; shared or global memory); returns false on
+// timeout (a peer's words did not arrive within kSpinTimeoutNs).
 __device__ bool peer_min_epoch(uint8_t* const* bufs, int world, int rank, const unsigned long long* local, int64_t K,
                                unsigned long long epoch, unsigned long long* out) {
     const int lane = threadIdx.x & 31;
-    const int64_t slot = int64_t(epoch & 1) * K;
-    // 1. contribute to every rank's slot (system-scope atomics over NVLink)
+    const int par = int(epoch & 1);
+    const unsigned long long tag = (epoch + 1) << 32;  // low 32 bits of the tag, in the cells' high half
+    // 1. push this rank's words into every rank's buffer (own one included)
     for (int64_t i = lane; i < int64_t(world) * K; i += 32) {
         const int p = int(i / K);
         const int64_t k = i - int64_t(p) * K;
-        auto* cells = reinterpret_cast<unsigned long long*>(bufs[p] + kPeerSlotsOff);
-        atomicMin_system(cells + slot + k, local[k]);
+        const unsigned long long v = local[k];
+        st_relaxed_sys_v2(peer_cells(bufs[p], par, rank, K, k), tag | (v & 0xffffffffull), tag | (v >> 32));
     }
-    __threadfence_system();
+    for (int64_t k = lane; k < K; k += 32) out[k] = ~0ull;
     __syncwarp();
-    // 2. arrive on every rank's counter
-    if (lane < world) atomicAdd_system(reinterpret_cast<unsigned long long*>(bufs[lane] + kPeerCounterOff), 1ull);
-    // 3. wait for all arrivals of this epoch on the own counter
-    const auto* ctr = reinterpret_cast<const unsigned long long*>(bufs[rank] + kPeerCounterOff);
-    const unsigned long long want = (epoch + 1) * (unsigned long long)world;
+    // 2. wait for every rank's words in the own buffer, MIN per stream
     bool ok = true;
-    if (lane == 0) {
-        const unsigned long long t0 = globaltimer_ns();
-        while (ld_acquire_sys(ctr) < want) {
+    const unsigned long long t0 = globaltimer_ns();
+    for (int64_t i = lane; i < int64_t(world) * K; i += 32) {
+        const int p = int(i / K);
+        const int64_t k = i - int64_t(p) * K;
+        const unsigned long long* c = peer_cells(bufs[rank], par, p, K, k);
+        unsigned long long lo, hi;
+        for (;;) {
+            ld_relaxed_sys_v2(c, lo, hi);
+            if ((lo >> 32) == (tag >> 32) && (hi >> 32) == (tag >> 32)) break;
             if (globaltimer_ns() - t0 > kSpinTimeoutNs) { ok = false; break; }
-            __nanosleep(64);
         }
+        if (!ok) break;
+        atomicMin(out + k, (hi << 32) | (lo & 0xffffffffull));
     }
-    ok = __shfl_sync(kFull, ok ? 1 : 0, 0) != 0;
+    ok = __all_sync(kFull, ok);
     __syncwarp();
-    // 4. the own slot now holds the MIN over all ranks; 5. reset it for epoch + 2
-    auto* mine = reinterpret_cast<unsigned long long*>(bufs[rank] + kPeerSlotsOff) + slot;
-    for (int64_t k = lane; k < K; k += 32) {
-        out[k] = ok ? atomicMax_system(mine + k, 0ull) : 0ull;  // atomic read at system scope
-        mine[k] = kErrNone;
-    }
-    __threadfence_system();
     return ok;
 }
 
@@ -120,8 +130,8 @@ __global__ void peer_combine_emulate_kernel(uint8_t* const* __restrict__ bufs, i
 __global__ void peer_buffer_init_kernel(uint8_t* buf, int64_t K) {
     griddep_wait();
     auto* p = reinterpret_cast<unsigned long long*>(buf);
-    const int64_t words = (kPeerSlotsOff / 8) + 2 * K;
-    for (int64_t i = threadIdx.x; i < words; i += blockDim.x) p[i] = (i < kPeerSlotsOff / 8) ? 0ull : kErrNone;
+    const int64_t cells = 2ll * kPeerMaxWorld * K * 2;
+    for (int64_t i = threadIdx.x; i < cells; i += blockDim.x) p[i] = 0ull;  // tag 0: no epoch yet
 }
 
 }  // namespace b64

@@ -19,9 +19,9 @@ CPU pass their own object with the same two methods to exercise the sharding
 and the MIN combine over gloo.
 
 ``PeerCombine`` is the one-sided alternative to the all_reduce (SURVEY.md
-Sec. 8(f) f4): one small kernel per combine that atomicMin's the words into
-every rank's peer-mapped buffer over NVLink and meets the other ranks on
-arrival counters (b64_peer_combine).
+Sec. 8(f) f4): one small kernel per combine that stores the words, tagged with
+the epoch, into every rank's peer-mapped buffer over NVLink and polls its own
+buffer for everyone's (b64_peer_combine).
 """
 from __future__ import annotations
 
@@ -134,8 +134,9 @@ class PeerCombine:
     """One-sided first-error combine over peer memory (b64_peer_combine).
 
     Replaces decode_sharded's NCCL all_reduce(MIN) by one small kernel per combine: every
-    rank atomicMin's its packed words into every rank's buffer over NVLink and arrives on
-    every rank's counter.  Each rank allocates its buffer with
+    rank stores its packed words (epoch-tagged 64-bit cells) into every rank's buffer over
+    NVLink and polls its own buffer until every rank's words of the epoch arrived
+    (DESIGN.md "Multi-GPU").  Each rank allocates its buffer with
     b64_peer_buffer_alloc, the 64-byte CUDA IPC handles are exchanged once with
     all_gather_object (the plumbing collective), and every rank maps its peers' buffers.
     All ranks must construct it together (collective) and then call combine() in the same

@@ -1180,7 +1180,7 @@ def _api_form(words):
 def test_peer_combine_emulated_ranks(b64):
     """W ranks emulated on one GPU (one cooperative kernel, block r = rank r) through E
     back-to-back epochs: every rank sees the MIN over ranks of that epoch's words (the slot
-    parity, counters and slot resets of b64_peer_combine's protocol, real atomics)."""
+    parity and epoch tags of b64_peer_combine's push protocol, real system-scope stores)."""
     L = b64._lib.lib()
     rng = np.random.default_rng(5)
     for world, K, epochs in ((1, 6, 5), (2, 6, 9), (3, 1, 7), (8, 6, 12), (5, 40, 4)):
@@ -1204,11 +1204,15 @@ def test_peer_combine_emulated_ranks(b64):
         want = local.min(axis=1)
         for r in range(world):
             assert np.array_equal(got[:, r, :], want), (world, K, r)
-        # after the epochs, each rank's slots are reset (ERR_NONE) and its counter = epochs * world
+        # after the epochs, slot e & 1 of every rank's buffer holds epoch e's words of every rank
+        # as cells {low / high 32-bit half, tag e + 1} (e = the last two epochs)
         for bb in bufs:
-            raw = bb.cpu().numpy().view(np.int64)
-            assert raw[0] == epochs * world
-            assert np.all(raw[8: 8 + 2 * K] == b64_err_none())
+            raw = bb.cpu().numpy().view(np.uint64).reshape(2, 32, K, 2)
+            for e in range(max(0, epochs - 2), epochs):
+                cells = raw[e & 1, :world]
+                assert np.all(cells >> np.uint64(32) == np.uint64(e + 1)), (world, K, e)
+                words = (cells[..., 1] << np.uint64(32)) | (cells[..., 0] & np.uint64(0xFFFFFFFF))
+                assert np.array_equal(words.view(np.int64), local[e]), (world, K, e)
 
 
 def test_codec_fused_peer_world1(b64):

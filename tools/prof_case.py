@@ -18,7 +18,7 @@ import synth  # noqa: E402
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--op", choices=("enc", "dec", "both", "batch", "group"), default="both")
+    p.add_argument("--op", choices=("enc", "dec", "both", "batch", "group", "peer"), default="both")
     p.add_argument("--n", type=int, default=1 << 30)
     p.add_argument("--reps", type=int, default=3)
     a = p.parse_args()
@@ -36,6 +36,28 @@ def main():
         torch.cuda.synchronize()
         assert (err == -1).all()
         print("ok group")
+        return
+    if a.op == "peer":  # configs[1] fused step without / with the (world 1) peer combine, alternating
+        from paper_1910_05109_b200 import dist as b64dist
+
+        xs = [synth.device_data(a.n + d, seed=0) for d in (0, 0, 1, 1, 2, 2)]
+        al = [b64.standard(), b64.url()] * 3
+        ts = b64.encode_group(xs, al)
+        eo = [torch.empty_like(t) for t in ts]
+        cells = torch.full((6,), b64.ERR_NONE, dtype=torch.int64, device="cuda")
+        ticket = torch.zeros(1, dtype=torch.int32, device="cuda")
+        err = torch.empty(6, dtype=torch.int64, device="cuda")
+        st = torch.empty(6, dtype=torch.int32, device="cuda")
+        eitems, _ = b64._enc_items(xs, al, eo)
+        ditems, douts, cells = b64._dec_items(ts, al, None, cells, None, None)
+        pc = b64dist.PeerCombine(6)
+        for _ in range(a.reps):
+            b64.codec_group_fused(xs, ts, al, al, enc_outs=eo, cells=cells, ticket=ticket)
+            pc.codec_fused(eitems, 6, ditems, err, st, ticket)
+        torch.cuda.synchronize()
+        assert (err == -1).all()
+        pc.close()
+        print("ok peer")
         return
     if a.op == "batch":
         Ls = synth.loguniform_lengths(1_000_000, seed=0)
