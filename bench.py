@@ -979,6 +979,46 @@ def extra_configs_dist(b64, synth, torch, dev, world, rank, flush):
                      "note": "strong scaling: global size fixed, max over ranks of CUDA-event times"}
         del x, t, out
         torch.cuda.empty_cache()
+    # configs[3]: the 10^6-string batch cut by cumulative bytes (dist.batch_shard); each rank
+    # generates its strings' bytes, encodes them, corrupts its share of 1 % of the strings and
+    # decodes; the global first failing string is one all_reduce(MIN) (b64_decode_batch_ex)
+    Ls = synth.loguniform_lengths(1_000_000, seed=0)
+    off = synth.offsets(Ls)
+    sh = b64dist.batch_shard(off, world, rank)
+    x = torch.empty(max(sh.byte_stop - sh.byte_start, 1), dtype=torch.uint8, device=dev)
+    synth.device_fill(x, seed=0, offset=sh.byte_start)
+    doff = torch.from_numpy(off[sh.start: sh.stop + 1] - sh.byte_start).to(dev)
+    enc, eoff = b64.encode_batch(x, doff)
+    te_k, _ = timed(lambda ev: (b64.encode_batch(x, doff, out=enc, out_off=eoff), ev.record(stream)), 3)
+    picks = synth.pick(len(Ls), 0.01, seed=0)
+    mine = picks[(picks >= sh.start) & (picks < sh.stop)]
+    if mine.size:
+        enc[eoff[torch.from_numpy(mine - sh.start).to(dev)]] = ord("*")
+    tot_out = torch.tensor([int(eoff[-1].item())], dtype=torch.int64, device=dev)
+    lens = eoff[1:] - eoff[:-1]
+    doo = torch.zeros(lens.numel() + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(3 * torch.div(lens, 4, rounding_mode="floor"), 0, out=doo[1:])
+    dout = torch.empty(max(int(doo[-1].item()), 1), dtype=torch.uint8, device=dev)
+    first = torch.empty(1, dtype=torch.int64, device=dev)
+
+    def decb(ev):
+        first.fill_(b64.ERR_NONE)
+        b64.decode_batch(enc, eoff, out=dout, out_off=doo, index_base=sh.start, first_bad=first)
+        ev.record(stream)
+        dist.all_reduce(first, op=dist.ReduceOp.MIN)
+
+    td_k, td_full = timed(decb, 3)
+    got = int(first.item())
+    assert got == int(picks.min()), (got, int(picks.min()))
+    dist.all_reduce(tot_out)
+    B = int(tot_out.item())
+    res["config4_batch_1e6_sharded"] = {
+        "encode_gbs_aggregate": round(B / (te_k * 1e-3) / 1e9, 1),
+        "decode_gbs_aggregate_kernel": round(B / (td_k * 1e-3) / 1e9, 1),
+        "decode_gbs_aggregate_with_combine": round(B / (td_full * 1e-3) / 1e9, 1),
+        "first_failing_string": got, "corrupted_strings": int(picks.size), "base64_bytes": B,
+        "strings_rank0": sh.stop - sh.start,
+        "note": "strong scaling, strings cut by cumulative bytes; max over ranks of CUDA-event times"}
     return res
 
 

@@ -382,6 +382,17 @@ int b64_decode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t count
                      uint8_t *d_out, const int64_t *d_out_off, const b64_alphabet *a,
                      int32_t *d_status, int64_t *d_err_off, int64_t *d_out_len,
                      b64_stream_t stream);
+/* b64_decode_batch that also lowers *d_first_bad (device int64, nullable,
+ * caller-initialised, e.g. to B64_ERR_NONE) to the index of the batch's first
+ * failing string, counted from index_base (>= 0): MIN over i with
+ * d_status[i] != B64_ST_OK of index_base + i, taken inside the finalize kernel
+ * (no extra launch).  A multi-GPU batch sharded by cumulative bytes (DESIGN.md
+ * "Multi-GPU") passes its first string's global index and
+ * all_reduce(MIN)s the word to get the global first failing string. */
+int b64_decode_batch_ex(const uint8_t *d_in, const int64_t *d_in_off, int64_t count,
+                        uint8_t *d_out, const int64_t *d_out_off, const b64_alphabet *a,
+                        int32_t *d_status, int64_t *d_err_off, int64_t *d_out_len,
+                        int64_t index_base, int64_t *d_first_bad, b64_stream_t stream);
 
 /* ---- introspection ---------------------------------------------------------- */
 /* Number of kernels the library launched on this process so far (all calls),

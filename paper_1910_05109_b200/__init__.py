@@ -531,9 +531,12 @@ def encode_batch(x: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = 
 
 def decode_batch(t: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = None,
                  out: Optional[torch.Tensor] = None, out_off: Optional[torch.Tensor] = None,
-                 total_out: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None):
+                 total_out: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None,
+                 index_base: int = 0, first_bad: Optional[torch.Tensor] = None):
     """Per-string validating decode.  Returns (out, out_off, status int32, err_off int64
-    (relative, -1 = ok), out_len int64); out_off = exclusive scan of 3*(len//4)."""
+    (relative, -1 = ok), out_len int64); out_off = exclusive scan of 3*(len//4).
+    first_bad (device int64[1], caller-initialised, e.g. ERR_NONE): lowered to index_base + the
+    index of the first failing string (b64_decode_batch_ex)."""
     _check_u8(t, "t")
     if t.numel() == 0:  # all strings empty: the C ABI still wants a valid (unread) pointer
         t = torch.empty(1, dtype=torch.uint8, device=t.device)
@@ -551,9 +554,12 @@ def decode_batch(t: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = 
     status = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
     err = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
     olen = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
-    _lib.check(_lib.lib().b64_decode_batch(_ptr(t), _ptr(in_off), count, _ptr(out), _ptr(out_off), _alpha(a),
-                                           _ptr(status), _ptr(err), _ptr(olen), _stream(stream)),
-               "b64_decode_batch")
+    if first_bad is not None:
+        _check_i64(first_bad, "first_bad")
+    _lib.check(_lib.lib().b64_decode_batch_ex(_ptr(t), _ptr(in_off), count, _ptr(out), _ptr(out_off), _alpha(a),
+                                              _ptr(status), _ptr(err), _ptr(olen), index_base,
+                                              _ptr(first_bad) if first_bad is not None else None, _stream(stream)),
+               "b64_decode_batch_ex")
     return out, out_off, status[:count], err[:count], olen[:count]
 
 

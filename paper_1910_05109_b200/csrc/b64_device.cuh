@@ -329,6 +329,6 @@ __global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off
 __global__ void dec_batch_init_kernel(int64_t* err, int64_t count);
 __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
                                           int64_t count, uint32_t pad, int32_t* status, int64_t* err,
-                                          int64_t* out_len);
+                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad);
 
 }  // namespace b64

@@ -673,7 +673,15 @@ int b64_encode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count
 int b64_decode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count, uint8_t* d_out,
                      const int64_t* d_out_off, const b64_alphabet* a, int32_t* d_status, int64_t* d_err_off,
                      int64_t* d_out_len, b64_stream_t stream) {
-    if (count < 0 || !alpha_ok(a)) return B64_EINVAL;
+    return b64_decode_batch_ex(d_in, d_in_off, count, d_out, d_out_off, a, d_status, d_err_off, d_out_len, 0, nullptr,
+                               stream);
+}
+
+int b64_decode_batch_ex(const uint8_t* d_in, const int64_t* d_in_off, int64_t count, uint8_t* d_out,
+                        const int64_t* d_out_off, const b64_alphabet* a, int32_t* d_status, int64_t* d_err_off,
+                        int64_t* d_out_len, int64_t index_base, int64_t* d_first_bad, b64_stream_t stream) {
+    if (count < 0 || !alpha_ok(a) || index_base < 0 || (d_first_bad && count > INT64_MAX - index_base))
+        return B64_EINVAL;
     if (count == 0) return B64_OK;
     if (!d_in || !d_in_off || !d_out || !d_out_off || !d_err_off) return B64_EINVAL;
     const DevInfo* di = dev_info();
@@ -690,7 +698,7 @@ int b64_decode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count
     r = launched();
     if (r != B64_OK) return r;
     launch(dec_batch_finalize_kernel, small, kThreads, s, d_in, d_in_off, count, a->pad, d_status,
-           d_err_off, d_out_len);
+           d_err_off, d_out_len, index_base, reinterpret_cast<unsigned long long*>(d_first_bad));
     return launched();
 }
 

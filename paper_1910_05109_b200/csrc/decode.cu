@@ -521,8 +521,9 @@ __global__ void dec_batch_init_kernel(int64_t* err, int64_t count) {
 
 __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
                                           int64_t count, uint32_t pad, int32_t* status, int64_t* err,
-                                          int64_t* out_len) {
+                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad) {
     griddep_wait();
+    int64_t bad = INT64_MAX;  // this thread's first failing string (index_base + i)
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t a = in_off[i], L = in_off[i + 1] - a;
         const unsigned long long wv = static_cast<unsigned long long>(err[i]);
@@ -539,6 +540,13 @@ __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const 
         err[i] = e;
         if (status) status[i] = st;
         if (out_len) out_len[i] = ol;
+        if (st != kOk && bad == INT64_MAX) bad = index_base + i;  // i only grows per thread
+    }
+    if (first_bad) {  // the batch's first failing string: warp MIN, one atomic per warp
+        const unsigned long long b = static_cast<unsigned long long>(bad);
+        const unsigned hi = __reduce_min_sync(kFull, unsigned(b >> 32));
+        const unsigned lo_min = __reduce_min_sync(kFull, unsigned(b >> 32) == hi ? unsigned(b) : ~0u);
+        if ((threadIdx.x & 31) == 0 && hi != 0x7FFFFFFFu) atomicMin(first_bad, (static_cast<unsigned long long>(hi) << 32) | lo_min);
     }
 }
 

@@ -32,6 +32,7 @@ import torch
 
 ENC_UNIT = 768   # bytes per warp-chunk (256 triples)
 DEC_UNIT = 1024  # chars per warp-chunk (256 quads)
+ERR_NONE = 0x7F7F7F7F7F7F7F7F  # b64gpu.h B64_ERR_NONE: "no error" packed word
 
 
 @dataclass(frozen=True)
@@ -89,6 +90,16 @@ class CudaCodec:
 
         return decode_chunk(t, base, is_final, cell, self.alphabet)
 
+    def encode_batch(self, x: torch.Tensor, off: torch.Tensor):
+        from . import encode_batch
+
+        return encode_batch(x, off, self.alphabet)
+
+    def decode_batch(self, t: torch.Tensor, off: torch.Tensor, index_base: int, first_bad: torch.Tensor):
+        from . import decode_batch
+
+        return decode_batch(t, off, self.alphabet, index_base=index_base, first_bad=first_bad)
+
     def finalize(self, cell: torch.Tensor) -> Tuple[int, int]:
         from . import decode_finalize
 
@@ -128,6 +139,65 @@ def decode_sharded(t_local: torch.Tensor, shard: Shard, codec=None, group=None) 
         dist.all_reduce(cell, op=dist.ReduceOp.MIN, group=group)
     err, status = codec.finalize(cell)
     return out, err, status
+
+
+@dataclass(frozen=True)
+class BatchShard:
+    start: int        # first string of this rank
+    stop: int         # one past its last string
+    byte_start: int   # in_off[start]: where its strings begin in the concatenated input
+    byte_stop: int    # in_off[stop]
+
+
+def batch_shard(in_off, world: int, rank: int) -> BatchShard:
+    """Rank's strings of a batch (SURVEY.md Sec. 8(e) "Batch (C4)"): the string index range is
+    cut by CUMULATIVE BYTES, not by count -- rank r owns the strings whose start offset lies in
+    [in_off[0] + r*T/world, in_off[0] + (r+1)*T/world), T the total length, so every rank gets
+    about T/world bytes (within one string) whatever the length mix.  in_off: host int64
+    offsets [count+1] (numpy array, list or CPU tensor; non-decreasing)."""
+    import numpy as np
+
+    off = np.asarray(in_off.numpy() if isinstance(in_off, torch.Tensor) else in_off, dtype=np.int64)
+    count = off.size - 1
+    if count < 0 or world < 1 or not 0 <= rank < world:
+        raise ValueError("bad batch / world / rank")
+    total = int(off[-1] - off[0])
+    starts = off[:-1]
+
+    def cut(r):
+        if r == 0:
+            return 0
+        if r == world:
+            return count
+        return int(np.searchsorted(starts, off[0] + (r * total) // world, side="left"))
+
+    s0, s1 = cut(rank), cut(rank + 1)
+    return BatchShard(s0, s1, int(off[s0]), int(off[s1]))
+
+
+def encode_batch_sharded(x_local: torch.Tensor, off_local: torch.Tensor, codec=None):
+    """Encode this rank's strings (their bytes and offsets [count_local+1], any base).  No
+    collective: outputs stay local.  Returns (out, out_off)."""
+    codec = codec or CudaCodec()
+    return codec.encode_batch(x_local, off_local)
+
+
+def decode_batch_sharded(t_local: torch.Tensor, off_local: torch.Tensor, shard: BatchShard, codec=None,
+                         group=None):
+    """Decode this rank's strings; per-string status / err_off / out_len stay local.  The one
+    exchange is optional in the paper's terms and done here: the global index of the batch's
+    first failing string, one all_reduce(MIN) of an int64 (-1 if every string decoded).
+    Returns (out, out_off, status, err_off, out_len, first_bad)."""
+    import torch.distributed as dist
+
+    codec = codec or CudaCodec()
+    cell = codec.new_cell(t_local.device)
+    out, out_off, status, err, olen = codec.decode_batch(t_local, off_local, shard.start, cell)
+    world, _ = _group_info(group)
+    if world > 1:
+        dist.all_reduce(cell, op=dist.ReduceOp.MIN, group=group)
+    v = int(cell.item())
+    return out, out_off, status, err, olen, (-1 if v >= ERR_NONE else v)
 
 
 class PeerCombine:

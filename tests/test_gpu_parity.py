@@ -258,6 +258,52 @@ def test_batch_encode_decode_vs_oracle(b64):
             assert np.array_equal(o[rooff[i]: rooff[i] + rolen[i]], rout[rooff[i]: rooff[i] + rolen[i]]), i
 
 
+def test_batch_sharded_single_gpu(b64):
+    """configs[3]'s multi-GPU form on one GPU: the batch cut into W shards by cumulative bytes
+    (dist.batch_shard), each decoded through b64_decode_batch_ex with offsets that are a SLICE of
+    the whole batch's (first offset > 0, same buffer) and its global first string index; the
+    shards' first-failing words MIN-combined equal the whole batch's first failing string, and
+    every per-string result equals the oracle's."""
+    from paper_1910_05109_b200 import dist as b64dist
+
+    count = 30_000
+    L, off, x = _batch_case(count, 65536, 11)
+    renc, reoff = oracle.encode_batch(x, off)
+    text = renc.copy()
+    tl = np.diff(reoff)
+    picks = synth.pick(count, 0.01, seed=12)
+    for i in picks:
+        if tl[i]:
+            pos, bad = synth.corruption(1, int(tl[i]), oracle.STANDARD, seed=int(i))
+            text[reoff[i] + pos] = bad
+    rout, rooff, rst, rerr, rolen = oracle.decode_batch(text, reoff)
+    want_first = int(np.flatnonzero(rst)[0]) if np.any(rst) else -1
+    dt, dx = to_dev(text), to_dev(x)
+    doff_t, doff_x = torch.from_numpy(reoff).to(DEV), torch.from_numpy(off).to(DEV)
+    for W in (1, 2, 3, 8):
+        cells = torch.full((W,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+        for r in range(W):
+            es = b64dist.batch_shard(off, W, r)
+            eo, eoo = b64.encode_batch(dx, doff_x[es.start: es.stop + 1])
+            assert np.array_equal(eo[: int(eoo[-1])].cpu().numpy(), renc[reoff[es.start]: reoff[es.stop]]), (W, r)
+            ds = b64dist.batch_shard(reoff, W, r)
+            out, ooff, st, err, olen = b64.decode_batch(dt, doff_t[ds.start: ds.stop + 1], index_base=ds.start,
+                                                        first_bad=cells[r:r + 1])
+            assert np.array_equal(st.cpu().numpy(), rst[ds.start: ds.stop]), (W, r)
+            assert np.array_equal(err.cpu().numpy(), rerr[ds.start: ds.stop]), (W, r)
+            assert np.array_equal(olen.cpu().numpy(), rolen[ds.start: ds.stop]), (W, r)
+            o, oo = out.cpu().numpy(), ooff.cpu().numpy()
+            for j in range(0, ds.stop - ds.start, 97):
+                i = ds.start + j
+                assert np.array_equal(o[oo[j]: oo[j] + rolen[i]], rout[rooff[i]: rooff[i] + rolen[i]]), (W, i)
+        v = int(cells.min().item())
+        assert (v if v < b64.ERR_NONE else -1) == want_first, W
+    # no failing string: the word stays untouched
+    clean = torch.full((1,), b64.ERR_NONE, dtype=torch.int64, device=DEV)
+    b64.decode_batch(to_dev(renc), torch.from_numpy(reoff).to(DEV), index_base=5, first_bad=clean)
+    assert int(clean.item()) == b64.ERR_NONE
+
+
 def test_batch_many_short_strings(b64):
     """200k strings of 0..140 bytes (the lane-per-string path and its hand-over to the warp path
     at the thresholds, strings straddling warp ranges), ~5 % corrupted anywhere (interior and
