@@ -83,6 +83,16 @@ def test_sizes_and_sync_errors(L):
     assert L.b64_decode_chunk(None, 6, None, a, 0, 1, ctypes.c_void_p(8), None, None) == -2
     assert L.b64_encode_batch(None, None, -1, None, None, a, None) == -1
     assert L.b64_encode_batch(None, None, 0, None, None, a, None) == 0
+    # b64_decode_batch_ex: negative index base, index overflow with a first-bad word
+    V = ctypes.c_void_p
+    assert L.b64_decode_batch_ex(V(8), V(8), 1, V(8), V(8), a, None, V(8), None, -1, None, None) == -1
+    assert L.b64_decode_batch_ex(V(8), V(8), 2, V(8), V(8), a, None, V(8), None, (1 << 63) - 1, V(8), None) == -1
+    assert L.b64_decode_batch_ex(None, None, 0, None, None, a, None, None, None, 0, V(8), None) == 0
+    # fused peer codec: world / rank out of range (nothing launched)
+    assert L.b64_codec_group_fused_peer(None, 0, None, 0, V(8), None, V(8), V(8), 33, 0, 0, None) == -1
+    assert L.b64_codec_group_fused_peer(None, 0, None, 0, V(8), None, V(8), V(8), 2, 2, 0, None) == -1
+    assert L.b64_peer_combine_bytes(-1) == -1 and L.b64_peer_combine_bytes(0) == 64
+    assert L.b64_peer_combine_bytes(6) == 2 * 32 * 6 * 16
     assert b"sm_100a" in L.b64_build_info()
 
 
