@@ -989,12 +989,61 @@ def test_decode_ws_vs_oracle(b64):
             assert err == rerr, (n, err, rerr, rst)
             assert np.array_equal(out.cpu().numpy(), ref), n
     # whitespace that belongs to the alphabet is data
+    _decode_ws_adversarial(b64)
     a2 = b64.alphabet(ws_alpha)
     x = synth.data(5000, seed=4)
     t = oracle.encode(x, ws_alpha)
     out, err = b64.decode_ws(to_dev(_mime(t, 4, every=33)), a2)
     ref, rerr, _ = oracle.decode_ws(_mime(t, 4, every=33), ws_alpha)
     assert err == rerr and np.array_equal(out.cpu().numpy(), ref)
+
+
+def _decode_ws_adversarial(b64):
+    """Whitespace layouts around the 4 KiB chunks of the fused decode: long runs spanning
+    chunks, chunks holding 0-3 kept chars, quads (and the final quad) split across chunks by
+    whitespace, errors in the look-ahead chars and in a split final quad, '=' misplaced,
+    unaligned input (byte path), lenient alphabet."""
+    x = synth.data(30_000, seed=91)
+    text = oracle.encode(x)  # 40000 chars, no padding
+    xp = synth.data(30_001, seed=92)
+    textp = oracle.encode(xp)  # ends 'xx=='
+    sp = lambda k: np.full(k, ord(" "), np.uint8)  # noqa: E731
+    cat = lambda *a: np.concatenate(a)  # noqa: E731
+    cases = [
+        cat(text[:5000], sp(10_000), text[5000:]),                          # run over 2+ chunks
+        cat(*[cat(text[i: i + 1], sp(1500)) for i in range(12)], text[12:]),  # chunks with 1-3 kept chars
+        cat(textp[:-2], sp(5000), textp[-2:]),                              # final quad split by 5000 blanks
+        cat(textp[:-1], sp(4096), textp[-1:], np.frombuffer(b"\r\n\r\n", np.uint8)),  # trailing CRLFs
+        cat(text[:4095], sp(1), text[4095:]),                               # a quad split at the chunk edge
+        cat(sp(4093), text),                                                # G % 4 != 0 everywhere
+    ]
+    bad = []
+    for t in cases[:3]:
+        t = t.copy()
+        keep = np.nonzero(t != ord(" "))[0]
+        t[keep[4097 if keep.size > 4097 else 1]] = ord("*")  # a char read by the look-ahead
+        bad.append(t)
+        t2 = t.copy()
+        t2[keep[keep.size // 2]] = ord("=")                  # '=' in the middle
+        bad.append(t2)
+    t = cases[2].copy()
+    t[np.nonzero(t != ord(" "))[0][-3]] = ord("A")          # final quad 'xA==' non-canonical
+    bad.append(t)
+    t = cases[2].copy()
+    t[np.nonzero(t != ord(" "))[0][-2]] = ord("A")          # 'xxA=': not canonical or bad bits
+    bad.append(t)
+    t = cases[2].copy()
+    t[np.nonzero(t != ord(" "))[0][-1]] = ord("A")          # 'xx=A': data after padding
+    bad.append(t)
+    for i, t in enumerate(cases + bad):
+        ref, rerr, rst = oracle.decode_ws(t)
+        for off in (0, 1):
+            out, err = b64.decode_ws(to_dev(t, off))
+            assert err == rerr, (i, off, err, rerr, rst)
+            assert np.array_equal(out.cpu().numpy(), ref), (i, off)
+        refl, rerrl, _ = oracle.decode_ws(t, lenient=True)
+        out, err = b64.decode_ws(to_dev(t), b64.lenient_of(b64.standard()))
+        assert err == rerrl and np.array_equal(out.cpu().numpy(), refl), i
 
 
 # ------------------------------------------------------------------ streaming (carry between calls)

@@ -1,0 +1,55 @@
+#!/usr/bin/env python3
+"""Whitespace-skipping decode timing: 1 GiB of data (or argv[1] bytes) as MIME text (76-char
+lines + CRLF), CUDA events, L2 flushed, median of 10."""
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1910_05109_b200 as b64  # noqa: E402
+import synth  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 30
+    dev = torch.device("cuda:0")
+    x = synth.device_data(n, seed=0)
+    t = b64.encode(x)
+    m = t.numel()
+    rows = (m + 75) // 76
+    mime = torch.empty(rows * 78, dtype=torch.uint8, device=dev)
+    full = rows * 76
+    tp = torch.full((full,), ord("A"), dtype=torch.uint8, device=dev)
+    tp[:m] = t
+    v = mime.view(rows, 78)
+    v[:, :76] = tp.view(rows, 76)
+    v[:, 76] = 13
+    v[:, 77] = 10
+    mime = mime[: (m // 76) * 78 + (m % 76) + (2 if m % 76 else 0)]
+    if m % 76:
+        mime[-2:] = torch.tensor([13, 10], dtype=torch.uint8, device=dev)
+    out = torch.empty(3 * (m // 4), dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(b64._lib.lib().b64_decode_ws_workspace_bytes(mime.numel())), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    res = {"n": n, "text": mime.numel()}
+    o, err = b64.decode_ws(mime, out=out, workspace=ws)
+    assert err == -1 and torch.equal(o[:n], x)
+    ts = []
+    for k in range(13):
+        flush.fill_(k)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b64.decode_ws(mime, out=out, workspace=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        if k >= 3:
+            ts.append(e0.elapsed_time(e1))
+    res["ms"] = round(statistics.median(ts), 4)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
