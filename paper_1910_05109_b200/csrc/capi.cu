@@ -418,9 +418,11 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
     std::memcpy(wb, a->dec, 256);
     for (int c : {0x09, 0x0A, 0x0B, 0x0C, 0x0D, 0x20})
         if (wb[c] == 0x80) wb[c] = kSkip;
-    launch(ws_count_kernel, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot);
+    bool sw = true;  // no whitespace char is data: the arithmetic whitespace test applies
+    for (int c : {0x09, 0x0A, 0x0B, 0x0C, 0x0D, 0x20}) sw = sw && a->dec[c] >= 64;
+    launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot);
     launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc);
-    launch(ws_compact_kernel, L.ncta, kThreads, s, d_in, m, wt, L.K, static_cast<const int32_t*>(counts),
+    launch(sw ? ws_compact_kernel<true> : ws_compact_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, static_cast<const int32_t*>(counts),
            static_cast<const int64_t*>(cbase), comp);
     {  // strict decode of the compacted text; its length m' is read on the device
         const int64_t blocks = balanced_blocks(m / 1024, int64_t(di->sms) * cap_bps(di->occ_dec_fast[1]));

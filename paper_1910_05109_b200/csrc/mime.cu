@@ -26,10 +26,12 @@
 //                         text: CTA (binary search) -> chunk -> byte.
 // Traffic: read m (count) + read m, write m' (compact) + read m', write 3m'/4
 // (decode), i.e. ~4.75 B per char against 1.75 for the strict decode.
-// Measured (1 GiB of data as MIME lines of 76 chars + CRLF): count 0.33 ms,
-// compact 1.1 ms, decode 0.42 ms -- the compaction (table look-up + shared
-// byte store per char) is the cost; the byte-at-a-time first version took
-// 3.7 ms in all.
+// Measured (1 GiB of data as MIME lines of 76 chars + CRLF): 1.67 ms in all;
+// per 256 MiB (ncu): count 72 us, compact 238 us, decode ~100 us.  The
+// compaction (shared byte store per char) is issue-bound; with an alphabet
+// that has no whitespace chars the keep masks come from an arithmetic
+// per-byte test (ws_bits) instead of table look-ups (count 88 -> 72 us,
+// compact 285 -> 238 us).  The byte-at-a-time first version took 3.7 ms.
 #include "b64_device.cuh"
 
 namespace b64 {
@@ -50,6 +52,30 @@ __device__ __forceinline__ uint32_t ws_keep4(const uint8_t* lut, uint32_t x) {
     return mask;
 }
 
+// Arithmetic whitespace test for alphabets without whitespace chars (host
+// checked; the table path handles the others): 0x80 in every byte of x that is
+// 0x09-0x0D or 0x20, exact per byte (no carries: each byte is masked to 7 bits
+// first), ~7 instructions per 4 bytes instead of 4 table look-ups.
+__device__ __forceinline__ uint32_t ws_bits(uint32_t x) {
+    const uint32_t y = x & 0x7F7F7F7Fu;
+    const uint32_t z = y ^ 0x20202020u;
+    const uint32_t nz = (z + 0x7F7F7F7Fu) | z;   // bit 7: byte != 0x20
+    const uint32_t ge9 = y + 0x77777777u;        // bit 7: byte >= 0x09
+    const uint32_t ge14 = y + 0x72727272u;       // bit 7: byte >= 0x0E
+    return (~nz | (ge9 & ~ge14)) & ~x & 0x80808080u;
+}
+
+// keep-mask of the 4 bytes of x (bit b = byte b kept), either way
+template <bool SW>
+__device__ __forceinline__ uint32_t keep4(const uint8_t* lut, uint32_t x) {
+    if (SW) {
+        const uint32_t k = ~ws_bits(x) & 0x80808080u;
+        return ((k >> 7) | (k >> 14) | (k >> 21) | (k >> 28)) & 0xFu;
+    }
+    return ws_keep4(lut, x);
+}
+
+template <bool SW>
 __global__ void __launch_bounds__(kThreads)
 ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K, int32_t* __restrict__ counts,
                 int64_t* __restrict__ cta_tot) {
@@ -78,10 +104,16 @@ ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K,
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
                 const uint32_t wv[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+                if (SW) {  // the 16 whitespace flags at distinct bits, one popcount
+                    const uint32_t f = (ws_bits(wv[0]) >> 7) | (ws_bits(wv[1]) >> 6) | (ws_bits(wv[2]) >> 5) |
+                                       (ws_bits(wv[3]) >> 4);
+                    cnt += 16u - __popc(f);
+                } else {
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                    for (int q = 0; q < 4; ++q)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) cnt += ws_keep(lut, (wv[q] >> (8 * b)) & 0xffu) ? 1u : 0u;
+                        for (int b = 0; b < 4; ++b) cnt += ws_keep(lut, (wv[q] >> (8 * b)) & 0xffu) ? 1u : 0u;
+                }
             }
         } else {
             for (int64_t i = lane; i < len; i += 32) cnt += ws_keep(lut, in[b0 + i]) ? 1u : 0u;
@@ -128,6 +160,7 @@ __global__ void __launch_bounds__(1024) ws_scan_kernel(const int64_t* __restrict
     if (t == 0) *m_out = s_warp[31];
 }
 
+template <bool SW>
 __global__ void __launch_bounds__(kThreads)
 ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K, const int32_t* __restrict__ counts,
                   const int64_t* __restrict__ cta_base, uint8_t* __restrict__ dst) {
@@ -185,7 +218,7 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
                 const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
                 uint32_t mask = 0;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) mask |= ws_keep4(lut, wv[q]) << (4 * q);
+                for (int q = 0; q < 4; ++q) mask |= keep4<SW>(lut, wv[q]) << (4 * q);
                 const int cnt = __popc(mask);
                 int incl = cnt;
 #pragma unroll
