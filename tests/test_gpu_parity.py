@@ -1035,6 +1035,15 @@ def _decode_ws_adversarial(b64):
     t = cases[2].copy()
     t[np.nonzero(t != ord(" "))[0][-1]] = ord("A")          # 'xx=A': data after padding
     bad.append(t)
+    # near misses of the whitespace set (the kernels' arithmetic test must not skip them): each
+    # is an invalid char at its position; and every whitespace byte at every lane offset
+    for k, nb in enumerate((0x08, 0x0E, 0x1F, 0x21, 0x89, 0x8A, 0x8D, 0xA0, 0x00, 0x7F, 0xC9)):
+        t = cat(text[:3000], np.frombuffer(b"\r\n", np.uint8), text[3000:]).copy()
+        t[1000 + 37 * k] = nb
+        bad.append(t)
+    allws = np.frombuffer(b" \t\n\r\x0b\x0c", np.uint8)
+    t = np.concatenate([cat(text[i: i + 5], allws[i % 6: i % 6 + 1 + (i % 3)]) for i in range(0, 8000, 5)])
+    bad.append(cat(t, text[8000:]))
     for i, t in enumerate(cases + bad):
         ref, rerr, rst = oracle.decode_ws(t)
         for off in (0, 1):
