@@ -54,7 +54,7 @@ lengths = st.one_of(st.integers(0, 40), st.integers(0, 5000), st.integers(760, 8
 @given(n=lengths, kind=st.sampled_from(["std", "url", "custom"]), aseed=st.integers(0, 50),
        off_in=st.sampled_from([0, 0, 1, 3, 8]), off_out=st.sampled_from([0, 0, 1, 2, 16]),
        lenient=st.booleans(), k_bad=st.integers(0, 3), seed=st.integers(0, 10_000),
-       api=st.sampled_from(["single", "chunk", "group", "codec", "stream", "batch"]))
+       api=st.sampled_from(["single", "chunk", "group", "codec", "stream", "batch", "unpadded", "ws"]))
 def test_fuzz_encode_decode_vs_oracle(b64, n, kind, aseed, off_in, off_out, lenient, k_bad, seed, api):
     chars, pad, alpha = _alpha(b64, kind, aseed)
     if lenient:
@@ -122,6 +122,28 @@ def test_fuzz_encode_decode_vs_oracle(b64, n, kind, aseed, off_in, off_out, leni
         parts.append(tail.cpu().numpy())
         err, stt, olen = info.tolist()
         got = np.concatenate(parts)[:olen]
+    elif api == "unpadded":  # the same text with its '=' stripped (R13), one call
+        t_u = text[: text.size - int(np.sum(text[-2:] == pad))] if text.size >= 4 else text
+        if t_u.size % 4 == 1:
+            return
+        ref, rerr, rst = oracle.decode_unpadded(t_u, chars, pad, lenient=lenient)
+        out, err = b64.decode_unpadded(_dev(t_u, off_in), alpha)
+        assert err == rerr, (api, n, err, rerr, rst)
+        assert np.array_equal(out.cpu().numpy(), ref)
+        return
+    elif api == "ws":  # the text with seeded whitespace runs inserted (R14)
+        rng = np.random.default_rng(seed)
+        k = int(rng.integers(0, 1 + text.size // 8))
+        pos = np.sort(rng.integers(0, text.size + 1, k))
+        ws = np.frombuffer(b" \t\n\r\x0b\x0c", np.uint8)
+        t_w = np.insert(text, pos, ws[rng.integers(0, 6, k)]) if k else text
+        if chars.translate(None, bytes(ws)) != chars:  # a whitespace char is data here: keep it simple
+            return
+        ref, rerr, rst = oracle.decode_ws(t_w, chars, pad, lenient=lenient)
+        out, err = b64.decode_ws(_dev(t_w, off_in), alpha)
+        assert err == rerr, (api, n, err, rerr, rst)
+        assert np.array_equal(out.cpu().numpy(), ref)
+        return
     else:  # batch of the text cut into pieces at random quad boundaries, plus the text itself
         rng = np.random.default_rng(seed)
         cuts = sorted(set([0, m] + [int(4 * v) for v in rng.integers(0, m // 4 + 1, 4)]))
