@@ -673,12 +673,17 @@ def extra_configs(b64, synth, torch, dev, stream, flush, Ev):
     t = b64.encode(x)
     o = torch.empty(1048578, dtype=torch.uint8, device=dev)
     info = torch.zeros(3, dtype=torch.int64, device=dev)
+    ctx = b64.DecodeContext()
     te = timeit(lambda: b64.encode(x, out=t), do_flush=False)
     td = timeit(lambda: b64.decode_async(t, out=o, info=info), do_flush=False)
+    tf = timeit(lambda: b64.decode_async(t, out=o, info=info, ctx=ctx), do_flush=False)
+    assert info.tolist() == [-1, 0, 1048576]
     res["config1_1MiB"] = {"encode_us": round(te * 1e3, 2), "decode_us": round(td * 1e3, 2),
+                           "decode_fused_us": round(tf * 1e3, 2),
                            "encode_gbs": round(t.numel() / (te * 1e-3) / 1e9, 1),
                            "decode_gbs": round(t.numel() / (td * 1e-3) / 1e9, 1), "l2": "resident (not flushed)",
-                           "decode_path": "b64_decode_ex (memset + kernel + finalize)",
+                           "decode_path": "b64_decode_ex (memset + kernel + finalize); decode_fused: "
+                                          "b64_decode_fused (one launch, self-resetting context)",
                            "timing": "events around one call after a GPU sleep (device time incl. launch gaps)"}
     del x, t, o
     # the paper's Table 3 sizes (random bytes stand in for the files):
@@ -690,27 +695,33 @@ def extra_configs(b64, synth, torch, dev, stream, flush, Ev):
         ts = b64.encode(xs)
         os_ = torch.empty(3 * (ts.numel() // 4), dtype=torch.uint8, device=dev)
         inf = b64.new_info(dev)
-        g = torch.cuda.CUDAGraph()
-        sg = torch.cuda.Stream()
-        sg.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(sg):
-            b64.decode_async(ts, out=os_, info=inf)
+        row = {"bytes": n}
+        for tag, use_ctx in (("", False), ("_fused", True)):
+            g = torch.cuda.CUDAGraph()
+            sg = torch.cuda.Stream()
+            sg.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(sg):
+                gctx = b64.DecodeContext(stream=sg) if use_ctx else None
+                b64.decode_async(ts, out=os_, info=inf, ctx=gctx)
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=sg):
+                    for _ in range(100):
+                        b64.decode_async(ts, out=os_, info=inf, ctx=gctx)
+            torch.cuda.current_stream().wait_stream(sg)
+            g.replay()
             torch.cuda.synchronize()
-            with torch.cuda.graph(g, stream=sg):
-                for _ in range(100):
-                    b64.decode_async(ts, out=os_, info=inf)
-        torch.cuda.current_stream().wait_stream(sg)
-        g.replay()
-        torch.cuda.synchronize()
-        a0, a1 = Ev(), Ev()
-        a0.record(stream)
-        g.replay()
-        a1.record(stream)
-        torch.cuda.synchronize()
-        us = a0.elapsed_time(a1) * 1e3 / 100
-        assert int(inf[0].item()) == -1
-        t3[name] = {"bytes": n, "decode_us": round(us, 2), "decode_gbs": round(ts.numel() / us / 1e3, 2)}
-        del xs, ts, os_, g
+            a0, a1 = Ev(), Ev()
+            a0.record(stream)
+            g.replay()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            us = a0.elapsed_time(a1) * 1e3 / 100
+            assert int(inf[0].item()) == -1 and int(inf[2].item()) == n
+            row["decode" + tag + "_us"] = round(us, 2)
+            row["decode" + tag + "_gbs"] = round(ts.numel() / us / 1e3, 2)
+            del g
+        t3[name] = row
+        del xs, ts, os_
     res["table3_sizes_decode"] = t3
     # configs[2]: 1 GiB -> 1.43 GB text, decode on 1 GPU
     x = synth.device_data(1 << 30, seed=0)

@@ -234,6 +234,20 @@ int b64_codec_group_fused(const b64_encode_item *enc, int64_t n_enc, const b64_d
 int b64_codec_group_fused_peer(const b64_encode_item *enc, int64_t n_enc, const b64_decode_item *dec, int64_t n_dec,
                                int64_t *d_err_off, int32_t *d_status, uint32_t *d_ticket, uint8_t *const *d_peer_bufs,
                                int world, int rank, uint64_t epoch, b64_stream_t stream);
+/* Single-launch validating decode with a caller-owned, self-resetting context
+ * (the fixed-overhead regime of PAPER.md:582, 613):
+ * the same results as b64_decode_ex (d_err_off required; d_status, d_out_len
+ * nullable) from ONE kernel -- no initialisation and no finalize launch.
+ * d_ctx: a device buffer of B64_DECODE_CTX_BYTES bytes, set up once with
+ * b64_decode_ctx_init; every call leaves it ready for the next, so calls that
+ * share a context must be ordered (the same stream, or events); use one
+ * context per stream.  Inputs up to the single-launch cluster size, and
+ * inputs that are not fast-path aligned (d_in 32 B, d_out 16 B), take
+ * b64_decode_ex's own path (the context is not touched). */
+#define B64_DECODE_CTX_BYTES 16
+int b64_decode_ctx_init(uint8_t *d_ctx, b64_stream_t stream);
+int b64_decode_fused(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a, int64_t *d_err_off,
+                     int32_t *d_status, int64_t *d_out_len, uint8_t *d_ctx, b64_stream_t stream);
 /* b64_decode_finalize for `count` consecutive packed words. */
 int b64_decode_finalize_n(const int64_t *d_err_min, int64_t count, int64_t *d_err_off, int32_t *d_status,
                           b64_stream_t stream);

@@ -115,10 +115,21 @@ def new_info(device=None) -> torch.Tensor:
     return torch.zeros(3, dtype=torch.int64, device=device if device is not None else "cuda")
 
 
+class DecodeContext:
+    """Device context of b64_decode_fused (B64_DECODE_CTX_BYTES): with it, decode_async is ONE
+    kernel launch (no initialisation, no finalize launch).  Calls sharing a context must be
+    ordered (one context per stream)."""
+
+    def __init__(self, device=None, stream: Optional[torch.cuda.Stream] = None):
+        self.buf = torch.empty(16, dtype=torch.uint8, device=device if device is not None else "cuda")
+        _lib.check(_lib.lib().b64_decode_ctx_init(_ptr(self.buf), _stream(stream)), "b64_decode_ctx_init")
+
+
 def decode_async(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
-                 info: Optional[torch.Tensor] = None,
-                 stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, torch.Tensor]:
-    """Validating decode (b64_decode_ex) without a host sync.
+                 info: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None,
+                 ctx: Optional[DecodeContext] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Validating decode (b64_decode_ex, or b64_decode_fused with a DecodeContext) without a
+    host sync.
 
     Returns (out, info) where info is a device int64[3]: (err_off, status, out_len).
     A caller-provided info must come from new_info() (the status is written as an
@@ -132,6 +143,11 @@ def decode_async(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[to
     if info is None:
         info = new_info(t.device)
     ip = info.data_ptr()
+    if ctx is not None:
+        _lib.check(_lib.lib().b64_decode_fused(_ptr(t), m, _ptr(out), _alpha(a), ctypes.c_void_p(ip),
+                                               ctypes.c_void_p(ip + 8), ctypes.c_void_p(ip + 16), _ptr(ctx.buf),
+                                               _stream(stream)), "b64_decode_fused")
+        return out, info
     _lib.check(_lib.lib().b64_decode_ex(_ptr(t), m, _ptr(out), _alpha(a), ctypes.c_void_p(ip),
                                         ctypes.c_void_p(ip + 8), ctypes.c_void_p(ip + 16), _stream(stream)),
                "b64_decode_ex")
@@ -139,10 +155,10 @@ def decode_async(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[to
 
 
 def decode(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
-           stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, int]:
+           stream: Optional[torch.cuda.Stream] = None, ctx: Optional[DecodeContext] = None) -> Tuple[torch.Tensor, int]:
     """Validating decode.  Returns (decoded bytes, err_off); err_off = -1 when valid.
     Forces one 24-byte device->host read of (err_off, status, out_len)."""
-    out, info = decode_async(t, a, out=out, stream=stream)
+    out, info = decode_async(t, a, out=out, stream=stream, ctx=ctx)
     err, _, olen = info.tolist()
     return out[:olen], err
 

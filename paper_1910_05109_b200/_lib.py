@@ -108,6 +108,8 @@ SIGNATURES = [
     ("b64_encode_batch", INT, [P, P, I64, P, P, AP, P]),
     ("b64_decode_batch", INT, [P, P, I64, P, P, AP, P, P, P, P]),
     ("b64_decode_batch_ex", INT, [P, P, I64, P, P, AP, P, P, P, I64, P, P]),
+    ("b64_decode_ctx_init", INT, [P, P]),
+    ("b64_decode_fused", INT, [P, I64, P, AP, P, P, P, P, P]),
     ("b64_launch_count", I64, []),
     ("b64_build_info", ctypes.c_char_p, []),
 ]

@@ -641,6 +641,36 @@ int b64_codec_group_fused_peer(const b64_encode_item* enc, int64_t n_enc, const 
     return gb.flush();
 }
 
+int b64_decode_ctx_init(uint8_t* d_ctx, b64_stream_t stream) {
+    if (!d_ctx) return B64_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(d_ctx, 0x7F, 8, s) != cudaSuccess || cudaMemsetAsync(d_ctx + 8, 0, 8, s) != cudaSuccess)
+        return (cudaGetLastError(), B64_ECUDA);
+    return B64_OK;
+}
+
+int b64_decode_fused(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t* d_err_off,
+                     int32_t* d_status, int64_t* d_out_len, uint8_t* d_ctx, b64_stream_t stream) {
+    if (m < 0 || !alpha_ok(a) || !d_err_off || !d_ctx) return B64_EINVAL;
+    if (m % 4) return B64_ELENGTH;
+    if (m > 0 && (!d_in || !d_out)) return B64_EINVAL;
+    // small inputs: the single-launch cluster kernel needs no context; unaligned: the 3-op path
+    if (m <= small_max() || !aligned(d_in, 32) || !aligned(d_out, 16))
+        return b64_decode_ex(d_in, m, d_out, a, d_err_off, d_status, d_out_len, stream);
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    b64_decode_item it = {d_in, m, d_out, a, 0, 1, 0, reinterpret_cast<int64_t*>(d_ctx)};
+    GroupBuilder gb(di, stream);
+    gb.fused = true;
+    const int r = gb.add(it, 0);
+    if (r != B64_OK) return r;
+    gb.g.ticket = reinterpret_cast<unsigned int*>(d_ctx + 8);
+    gb.g.err_off = d_err_off;
+    gb.g.status = d_status;
+    gb.g.out_len = d_out_len;
+    return gb.flush();
+}
+
 int b64_encode_group(const b64_encode_item* items, int64_t count, b64_stream_t stream) {
     return b64_codec_group(items, count, nullptr, 0, stream);
 }

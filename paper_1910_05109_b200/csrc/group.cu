@@ -172,6 +172,7 @@ struct CodecGroup {
     // initialisation launch and no finalize launch.
     unsigned int* ticket;
     int64_t* err_off;
+    int64_t* out_len;  // nullable: exact output bytes per decode item (as b64_decode_ex)
     int32_t* status;
     int32_t didx[kGroupMax];
     // Fused cross-rank MIN (b64_codec_group_fused_peer; peer_bufs == nullptr: none): the last
@@ -214,12 +215,24 @@ __device__ __forceinline__ void codec_fused_finalize(const CodecGroup& g) {
         if (!s_ok) {  // a peer never arrived (peer.cu timeout)
             g.err_off[g.didx[k]] = -2;
             if (g.status) g.status[g.didx[k]] = -1;
+            if (g.out_len) g.out_len[g.didx[k]] = 0;
         } else if (wv >= kErrNone) {
             g.err_off[g.didx[k]] = -1;
             if (g.status) g.status[g.didx[k]] = kOk;
+            if (g.out_len) {
+                const int64_t m = g.d.m[k];
+                const uint32_t pad = g.d.pad[k] & 0xffu;
+                int64_t ol = 3 * (m >> 2);
+                if (g.d.is_final[k] && m >= 4) ol -= (g.d.in[k][m - 2] == pad) ? 2 : (g.d.in[k][m - 1] == pad ? 1 : 0);
+                g.out_len[g.didx[k]] = ol;
+            }
         } else {
             g.err_off[g.didx[k]] = int64_t(wv >> 3);
             if (g.status) g.status[g.didx[k]] = int32_t(wv & 7);
+            if (g.out_len) {
+                const int64_t rel = int64_t(wv >> 3) - g.d.base[k];
+                g.out_len[g.didx[k]] = rel > 0 ? 3 * (rel >> 2) : 0;
+            }
         }
     }
     __syncthreads();  // every word read before any (possibly shared) word is reset

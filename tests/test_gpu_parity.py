@@ -998,6 +998,59 @@ def test_decode_ws_vs_oracle(b64):
     assert err == rerr and np.array_equal(out.cpu().numpy(), ref)
 
 
+def test_decode_fused_ctx(b64):
+    """b64_decode_fused (one launch, self-resetting DecodeContext) equals b64_decode_ex / the oracle
+    -- err_off, status, out_len, bytes -- call after call on the same context with valid and
+    corrupted texts (interior and final-quad errors), strict and lenient alphabets, sizes below
+    and above the cluster threshold, unaligned buffers (3-op path), and replayed from a graph."""
+    al = _alphabets(b64)
+    ctx = b64.DecodeContext()
+    rng = np.random.default_rng(31)
+    for trial, n in enumerate([0, 1, 5, 400_000, 1 << 20, (1 << 20) + 1, 3_000_002, 25_000_001]):
+        chars, pad, alpha = al[trial % len(al)]
+        ref_t = oracle.encode(synth.data(n, seed=500 + trial), chars, pad)
+        for rep in range(4):
+            text = ref_t.copy()
+            if rep % 2 and text.size:
+                k = int(rng.integers(1, 4))
+                pos, bad = synth.corruption(k, text.size, chars, seed=trial * 10 + rep, pad=pad)
+                text[pos] = bad
+            if rep == 3 and text.size >= 4 and ref_t[-1] == pad:
+                text[-2] = chars[1]  # 'x?b=' or 'xb==' -> a final-quad error of some kind
+            for lenient in (False, True):
+                a = b64.lenient_of(alpha) if lenient else alpha
+                ref, rerr, rst = oracle.decode(text, chars, pad, lenient=lenient)
+                out, info = b64.decode_async(to_dev(text), a, ctx=ctx)
+                err, stt, olen = info.tolist()
+                assert (err, stt) == (rerr, rst), (n, rep, lenient, err, stt, rerr, rst)
+                assert olen == (ref.size if rerr < 0 else 3 * (rerr // 4)), (n, rep, olen)
+                assert np.array_equal(out[:olen].cpu().numpy(), ref[:olen]), (n, rep)
+        # unaligned input: falls back to the 3-op path, same results
+        out, err = b64.decode(to_dev(ref_t, 1), alpha, ctx=ctx)
+        assert err == -1 and out.numel() == b64.decoded_len_max(ref_t.size) - int(np.sum(ref_t[-2:] == pad))
+    # graph replay of a fused decode: every replay gives the result
+    x = synth.data(3_000_000, seed=9)
+    t = to_dev(oracle.encode(x))
+    info = b64.new_info()
+    o = torch.empty(b64.decoded_len_max(t.numel()), dtype=torch.uint8, device=DEV)
+    g, sg = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+    sg.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(sg):
+        gctx = b64.DecodeContext(stream=sg)
+        b64.decode_async(t, out=o, info=info, ctx=gctx)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=sg):
+            for _ in range(3):
+                b64.decode_async(t, out=o, info=info, ctx=gctx)
+    torch.cuda.current_stream().wait_stream(sg)
+    for _ in range(3):
+        info.zero_()
+        o.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert info.tolist() == [-1, 0, x.size] and np.array_equal(o[: x.size].cpu().numpy(), x)
+
+
 def _decode_ws_adversarial(b64):
     """Whitespace layouts around the 4 KiB chunks of the fused decode: long runs spanning
     chunks, chunks holding 0-3 kept chars, quads (and the final quad) split across chunks by
