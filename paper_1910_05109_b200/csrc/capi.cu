@@ -420,10 +420,17 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
         if (wb[c] == 0x80) wb[c] = kSkip;
     bool sw = true;  // no whitespace char is data: the arithmetic whitespace test applies
     for (int c : {0x09, 0x0A, 0x0B, 0x0C, 0x0D, 0x20}) sw = sw && a->dec[c] >= 64;
-    launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot);
-    launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc);
+    // line-structured text (MIME / PEM) is decoded in one pass by ws_line_kernel; the general
+    // path's kernels then return at once (they run when the probe or the line kernel clears
+    // the mode)
+    WsLine* li = reinterpret_cast<WsLine*>(base + L.off_mc + 64);
+    const WsLine* lic = li;
+    launch(ws_line_probe_kernel, 1, 32, s, d_in, m, wt, li, mc);
+    launch(ws_line_kernel, int64_t(di->sms) * B64_LINE_MINB, kThreads, s, d_in, m, wt, li, d_out);
+    launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot, lic);
+    launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc, lic);
     launch(sw ? ws_compact_kernel<true> : ws_compact_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, static_cast<const int32_t*>(counts),
-           static_cast<const int64_t*>(cbase), comp);
+           static_cast<const int64_t*>(cbase), comp, lic);
     {  // strict decode of the compacted text; its length m' is read on the device
         const int64_t blocks = balanced_blocks(m / 1024, int64_t(di->sms) * cap_bps(di->occ_dec_fast[1]));
         launch(dec_fast_kernel<1>, blocks, kThreads, s, static_cast<const uint8_t*>(comp), m, d_out, dec_tab(a),
@@ -432,8 +439,9 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
     }
     launch(ws_finalize_kernel, 1, 32, s, d_err_off, d_status, d_out_len, static_cast<const int64_t*>(mc), d_in, m,
            static_cast<const uint8_t*>(comp), wt, uint32_t(a->pad), L.K, int(L.ncta),
-           static_cast<const int32_t*>(counts), static_cast<const int64_t*>(cbase));
-    g_launches.fetch_add(4, std::memory_order_relaxed);
+           static_cast<const int32_t*>(counts), static_cast<const int64_t*>(cbase), lic, d_out,
+           uint32_t((a->flags & B64_ALPHA_LENIENT) ? 1 : 0));
+    g_launches.fetch_add(6, std::memory_order_relaxed);
     return launched();
 }
 

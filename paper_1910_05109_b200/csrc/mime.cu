@@ -26,12 +26,16 @@
 //                         text: CTA (binary search) -> chunk -> byte.
 // Traffic: read m (count) + read m, write m' (compact) + read m', write 3m'/4
 // (decode), i.e. ~4.75 B per char against 1.75 for the strict decode.
-// Measured (1 GiB of data as MIME lines of 76 chars + CRLF): 1.67 ms in all;
-// per 256 MiB (ncu): count 72 us, compact 238 us, decode ~100 us.  The
-// compaction (shared byte store per char) is issue-bound; with an alphabet
-// that has no whitespace chars the keep masks come from an arithmetic
-// per-byte test (ws_bits) instead of table look-ups (count 88 -> 72 us,
-// compact 285 -> 238 us).  The byte-at-a-time first version took 3.7 ms.
+// Line-structured text (MIME / PEM: every line L >= 32 chars, L % 4 == 0,
+// then the same 1-2 whitespace bytes) skips all of that: ws_line_probe_kernel
+// guesses the layout, ws_line_kernel decodes straight from the text in one
+// pass and verifies every byte; the general kernels above then return at once
+// (they run when the layout does not hold).  Measured (1 GiB of data as MIME
+// lines of 76 chars + CRLF): 0.83 ms (line kernel 210 us per 256 MiB, ALU-
+// bound); the general path 1.67 ms (per 256 MiB: count 72 us, compact 238
+// us, decode ~100 us; the compaction is issue-bound; alphabets without
+// whitespace chars use an arithmetic per-byte test, ws_bits, for the keep
+// masks).  The byte-at-a-time first version took 3.7 ms.
 #include "b64_device.cuh"
 
 namespace b64 {
@@ -75,10 +79,227 @@ __device__ __forceinline__ uint32_t keep4(const uint8_t* lut, uint32_t x) {
     return ws_keep4(lut, x);
 }
 
+// ---------------------------------------------------------------- line-structured text
+// MIME / PEM text is lines of L chars (L % 4 == 0) each followed by the same
+// 1-2 whitespace bytes, the last line possibly shorter.  Then kept char e sits
+// at orig(e) = (e / L) * P + e % L (P = L + s): no compaction is needed.  A
+// one-warp probe guesses (L, s, separator) from the first whitespace byte and
+// the text's end; ws_line_kernel decodes straight from the text AND verifies
+// every byte (chars non-whitespace, separators exact); any deviation clears
+// `mode` and the general path (count / scan / compact / decode, which exit
+// at once in line mode) runs instead.  Traffic: read m + write 3m'/4, one pass.
+struct WsLine {
+    int32_t mode;             // 1: line-structured (ws_line_kernel decodes), 0: general path
+    int32_t L, s, sep;        // chars per full line, separator bytes (0-2) and their values (LE)
+    int64_t nfull, r, mc;     // full lines, chars of the last partial line, kept chars
+    unsigned long long cell;  // first interior error, packed (kept index << 3 | kind)
+};
+constexpr int64_t kLineProbe = 65536;  // bytes searched for the first whitespace byte
+constexpr int kLineBlk = 2048;         // kept chars per warp step (two 32-char units per lane)
+constexpr int kLineStage = 2256;       // per-warp stage: kLineBlk chars + separators (L >= 32) + alignment
+
+__device__ __forceinline__ int64_t line_orig(int64_t e, int64_t L, int64_t P) { return (e / L) * P + e % L; }
+
+__global__ void __launch_bounds__(32)
+ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li,
+                     int64_t* __restrict__ mc_general) {
+    __shared__ __align__(256) uint32_t s_lut[64];
+    griddep_launch_dependents();
+    const int lane = threadIdx.x;
+    s_lut[lane] = tab.w[lane];
+    s_lut[lane + 32] = tab.w[lane + 32];
+    griddep_wait();
+    __syncwarp();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const int64_t lim = min(m, kLineProbe);
+    int64_t p = -1;
+    for (int64_t i0 = 0; i0 < lim && p < 0; i0 += 32) {
+        const int64_t i = i0 + lane;
+        const uint32_t bal = __ballot_sync(kFull, i < lim && lut[in[i]] == kSkip);
+        if (bal) p = i0 + __ffs(bal) - 1;
+    }
+    if (lane) return;
+    WsLine w;
+    w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.cell = kErrNone;
+    *mc_general = 0;  // the general path's decode does nothing unless its scan runs
+    if (m > 0 && p < 0) {  // no whitespace seen: one line (ws_line_kernel checks the rest)
+        w.mode = 1; w.r = m; w.mc = m;
+        w.L = int32_t(min(int64_t(1) << 30, (m + 4) & ~int64_t(3)));  // any multiple of 4 above m
+    } else if (p >= 32 && (p & 3) == 0 && p < (int64_t(1) << 30)) {  // (shorter lines: general path)
+        int s = 0;
+        while (s < 3 && p + s < m && lut[in[p + s]] == kSkip) ++s;
+        if (s <= 2) {
+            const int64_t L = p, P = p + s;
+            const int64_t nfull = m / P, rem = m - nfull * P;
+            int64_t r = -1;
+            if (rem == 0) {
+                r = 0;
+            } else if (lut[in[m - 1]] == kSkip) {  // a separator after a shorter last line
+                bool same = rem > s;
+                for (int b = 0; b < s && same; ++b) same = in[m - s + b] == in[p + b];
+                if (same) r = rem - s;
+            } else if (rem <= L) {
+                r = rem;
+            }
+            if (r >= 0) {
+                w.mode = 1; w.L = int32_t(L); w.s = s; w.nfull = nfull; w.r = r; w.mc = nfull * L + r;
+                w.sep = int32_t(s > 0 ? in[p] : 0) | int32_t(s > 1 ? in[p + 1] : 0) << 8;
+            }
+        }
+    }
+    *li = w;
+}
+
+// Decode + verify in line mode.  A warp takes 1024 kept chars at a time: it
+// stages their text span (chars + separators) in shared memory with
+// lane-linear 16-byte loads, then lane l decodes kept chars [32l, 32l + 32)
+// (8 quads, gathered from the stage: a quad never crosses a line since
+// L % 4 == 0) and checks the separator of every line it ends.  Output: 24
+// bytes per lane at out + 3e/4 (3 x STG.64; byte stores in a partial unit).
+// The final quad is left to ws_finalize_kernel; when mc % 4 != 0 (LENGTH)
+// nothing is written, but the structure is still verified.
+// x / d for 0 <= x < 2^31 and 32 <= d <= 2^30 without an integer division: a float estimate
+// (relative error ~1e-7, so off by at most one here) corrected either way
+__device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, float inv) {
+    int32_t q = __float2int_rz(__int2float_rn(x) * inv);
+    if (int64_t(q) * d > x) --q;
+    else if (int64_t(q + 1) * d <= x) ++q;
+    return q;
+}
+
+#ifndef B64_LINE_MINB
+#define B64_LINE_MINB 4
+#endif
+__global__ void __launch_bounds__(kThreads, B64_LINE_MINB)
+ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li,
+               uint8_t* __restrict__ out) {
+    __shared__ __align__(256) uint32_t s_lut[64];
+    __shared__ __align__(16) uint8_t s_stage[kThreads / 32][kLineStage];
+    griddep_launch_dependents();
+    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    griddep_wait();
+    __syncthreads();
+    if (__ldcg(&li->mode) != 1) return;
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
+    const int lane = threadIdx.x & 31;
+    uint8_t* stg = &s_stage[threadIdx.x >> 5][0];
+    const int32_t L = li->L, S = li->s;             // L >= 32: a 32-char unit crosses <= 1 line end
+    const float invL = 1.0f / float(L);
+    const int64_t P = int64_t(L) + S, nfull = li->nfull, mc = li->mc;
+    const uint32_t sep = uint32_t(li->sep);
+    const bool dec = (mc & 3) == 0;
+    const int64_t qfin = dec ? (mc >> 2) - 1 : -1;  // the final quad (ws_finalize_kernel)
+    const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    int64_t it = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    // line / column of the warp's first kept char, advanced per grid-stride step without division
+    int64_t line0 = (it * kLineBlk) / L;
+    int32_t col0 = int32_t(it * kLineBlk - line0 * L);
+    const int64_t step_lines = (W * kLineBlk) / L;
+    const int32_t step_col = int32_t(W * kLineBlk - step_lines * L);
+    bool irregular = false;
+    int64_t bad = INT64_MAX;  // first invalid kept index seen by this lane
+    for (; it * kLineBlk < mc; it += W) {
+        const int64_t K0 = it * kLineBlk, K1 = min(K0 + kLineBlk, mc);
+        const int32_t rl = int32_t(K1 - 1 - K0) + col0;  // last char, relative to line0's start
+        const int32_t dll = div_small(rl, L, invL);
+        const int64_t o0 = line0 * P + col0;
+        const int64_t o1 = min(m, o0 + int64_t(dll) * P + (rl - dll * L - col0) + 1 + S);
+        const int64_t b0 = o0 - int64_t(reinterpret_cast<uintptr_t>(in + o0) & 15);
+        const int nch = int((o1 - b0 + 15) >> 4);
+        for (int c = lane; c < nch; c += 32)
+            *reinterpret_cast<uint4*>(stg + 16 * c) = ld128_nc(in + b0 + 16 * c);
+        __syncwarp();
+        const int32_t sb = int32_t(o0 - b0) - col0;  // stage offset of line0's first char
+#pragma unroll 1
+        for (int u = 0; u < kLineBlk / 1024; ++u) {
+            const int32_t ru = 32 * (lane + 32 * u);     // unit's first char, relative to K0
+            const int64_t e = K0 + ru;
+            if (e >= K1) break;
+            const int32_t re = col0 + ru;
+            const int32_t dl = div_small(re, L, invL), col = re - dl * L;
+            const int32_t so0 = dl * int32_t(P) + col + sb;
+            const int32_t left = L - col;               // chars before this line's end (>= 4)
+            const int qs = left >= 32 ? 8 : (left >> 2);  // quads before the line end
+            const int nq = int(min(int64_t(8), (K1 - e) >> 2));
+            const int64_t q0 = e >> 2;
+            // the unit's chars: 10 aligned stage words; quads [qs, 8) sit S bytes further on
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(stg + (so0 & ~3));
+            uint32_t w[10];
+#pragma unroll
+            for (int k = 0; k < 10; ++k) w[k] = sw[k];
+            const uint32_t sh0 = uint32_t(so0 & 3) * 8;
+            const int t1 = (so0 & 3) + S;
+            const bool c1 = t1 >= 4;
+            const uint32_t sh1 = uint32_t(t1 & 3) * 8;
+            uint32_t x[8], v[8], err = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                x[q] = q < qs ? __funnelshift_r(w[q], w[q + 1], sh0)
+                              : __funnelshift_r(c1 ? w[q + 1] : w[q], c1 ? w[q + 2] : w[q + 1], sh1);
+                uint32_t eq = 0;
+                v[q] = dec_quad_s(x[q], lb, eq);
+                if (q < nq) err |= eq;
+            }
+            if (left <= 32 && line0 + dl < nfull && left <= int32_t(K1 - e)) {
+                // this unit ends a full line: its separator must follow
+                const int32_t sp = so0 + left;
+                for (int b = 0; b < S; ++b) irregular |= stg[sp + b] != ((sep >> (8 * b)) & 0xffu);
+            }
+            irregular |= (err & kSkip) != 0;
+            const bool tail = nq < 8 || q0 + 7 >= qfin;  // a partial unit or the final quad's
+            if ((err & kInvalid) || tail) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (q < nq && q0 + q != qfin && bad == INT64_MAX) {
+                        const int j = first_bad_in_quad(x[q], lut);
+                        if (j < 4) bad = 4 * (q0 + q) + j;
+                    }
+                }
+            }
+            if (!dec) {
+                // LENGTH: verify the chars of the incomplete group too, write nothing
+                if (nq < 8 && K1 == mc) {
+                    for (int32_t k = 4 * nq; k < int32_t(min(int64_t(32), K1 - e)); ++k) {
+                        const int32_t rk = re + k, dk = div_small(rk, L, invL);
+                        irregular |= lut[stg[dk * int32_t(P) + (rk - dk * L) + sb]] == kSkip;
+                    }
+                }
+            } else {
+                uint32_t ov[6];
+                dec_pack12(v[0], v[1], v[2], v[3], ov[0], ov[1], ov[2]);
+                dec_pack12(v[4], v[5], v[6], v[7], ov[3], ov[4], ov[5]);
+                uint8_t* o = out + 3 * q0;
+                if (!tail) {
+                    st64(o, ov[0], ov[1]);
+                    st64(o + 8, ov[2], ov[3]);
+                    st64(o + 16, ov[4], ov[5]);
+                } else {
+                    const int nst = int(min(int64_t(nq), qfin - q0)) * 3;  // bytes before the final quad
+#pragma unroll
+                    for (int b = 0; b < 24; ++b)
+                        if (b < nst) o[b] = uint8_t(ov[b >> 2] >> (8 * (b & 3)));
+                }
+            }
+        }
+        __syncwarp();
+        line0 += step_lines;
+        col0 += step_col;
+        if (col0 >= L) {
+            col0 -= L;
+            ++line0;
+        }
+    }
+    if (__any_sync(kFull, irregular) && lane == 0) atomicExch(&li->mode, 0);
+    const unsigned hi = __reduce_min_sync(kFull, unsigned(uint64_t(bad) >> 32));
+    const unsigned lo = __reduce_min_sync(kFull, unsigned(uint64_t(bad) >> 32) == hi ? unsigned(bad) : ~0u);
+    if (lane == 0 && hi != 0x7FFFFFFFu) atomicMin(&li->cell, pack_err(int64_t((uint64_t(hi) << 32) | lo), kBadChar));
+}
+
 template <bool SW>
 __global__ void __launch_bounds__(kThreads)
 ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K, int32_t* __restrict__ counts,
-                int64_t* __restrict__ cta_tot) {
+                int64_t* __restrict__ cta_tot, const WsLine* __restrict__ li) {
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ unsigned long long s_tot;
     griddep_launch_dependents();
@@ -86,6 +307,7 @@ ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K,
     if (threadIdx.x == 0) s_tot = 0;
     griddep_wait();
     __syncthreads();
+    if (__ldcg(&li->mode) == 1) return;  // line mode: ws_line_kernel did it all
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
@@ -131,10 +353,12 @@ ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K,
 
 // One CTA: exclusive scan of n (<= 1024) CTA totals -> cta_base; *m_out = sum.
 __global__ void __launch_bounds__(1024) ws_scan_kernel(const int64_t* __restrict__ cta_tot, int n,
-                                                       int64_t* __restrict__ cta_base, int64_t* __restrict__ m_out) {
+                                                       int64_t* __restrict__ cta_base, int64_t* __restrict__ m_out,
+                                                       const WsLine* __restrict__ li) {
     __shared__ int64_t s_warp[32];
     griddep_launch_dependents();
     griddep_wait();
+    if (__ldcg(&li->mode) == 1) return;
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int64_t v = t < n ? cta_tot[t] : 0;
     int64_t x = v;  // inclusive warp scan
@@ -163,13 +387,14 @@ __global__ void __launch_bounds__(1024) ws_scan_kernel(const int64_t* __restrict
 template <bool SW>
 __global__ void __launch_bounds__(kThreads)
 ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K, const int32_t* __restrict__ counts,
-                  const int64_t* __restrict__ cta_base, uint8_t* __restrict__ dst) {
+                  const int64_t* __restrict__ cta_base, uint8_t* __restrict__ dst, const WsLine* __restrict__ li) {
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(16) uint8_t s_buf[kThreads / 32][kWsChunk + 16];
     __shared__ int64_t s_pref[kThreads];   // per-thread partial sums of the CTA's chunk counts
     griddep_launch_dependents();
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     griddep_wait();
+    if (__ldcg(&li->mode) == 1) return;
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
@@ -279,7 +504,8 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
 __global__ void __launch_bounds__(32)
 ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const int64_t* __restrict__ m_c,
                    const uint8_t* __restrict__ in, int64_t m, const uint8_t* __restrict__ comp, WsTab tab, uint32_t pad,
-                   int64_t K, int ncta, const int32_t* __restrict__ counts, const int64_t* __restrict__ cta_base) {
+                   int64_t K, int ncta, const int32_t* __restrict__ counts, const int64_t* __restrict__ cta_base,
+                   const WsLine* __restrict__ li, uint8_t* __restrict__ out, uint32_t lenient) {
     __shared__ __align__(256) uint32_t s_lut[64];
     griddep_wait();
     const int lane = threadIdx.x;
@@ -287,6 +513,35 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
     s_lut[lane + 32] = tab.w[lane + 32];
     __syncwarp();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    if (__ldcg(&li->mode) == 1) {  // line mode: kept index -> text position in closed form
+        if (lane) return;
+        const int64_t L = li->L, P = L + li->s, mcl = li->mc;
+        unsigned long long w = __ldcg(&li->cell);
+        int64_t e = -1, ol = 0;
+        int32_t kind = kOk;
+        if (mcl & 3) {
+            e = mcl - (mcl & 3);
+            kind = kLength;
+        } else {
+            uint32_t x = 0;
+            for (int b = 0; b < 4; ++b) x |= uint32_t(in[line_orig(mcl - 4 + b, L, P)]) << (8 * b);
+            int fb = 0, k = 0;
+            uint32_t v = 0;
+            const uint32_t fk = final_quad(x, lut, pad, lenient, &fb, &k, &v);
+            if (fk != kOk) w = min(w, pack_err(mcl - 4 + fb, fk));
+            if (w < kErrNone) {
+                e = int64_t(w >> 3);
+                kind = int32_t(w & 7);
+            } else {
+                ol = 3 * (mcl >> 2) - 3 + k;
+                store_bytes(out + 3 * ((mcl >> 2) - 1), v, k);
+            }
+        }
+        *err_off = e < 0 ? -1 : line_orig(e, L, P);
+        if (status) *status = kind;
+        if (out_len) *out_len = e < 0 ? ol : (kind == kLength ? 0 : 3 * (e >> 2));
+        return;
+    }
     const int64_t mc = *m_c;
     const unsigned long long wv = *reinterpret_cast<unsigned long long*>(err_off);
     int64_t e = -1;

@@ -1051,6 +1051,55 @@ def test_decode_fused_ctx(b64):
         assert info.tolist() == [-1, 0, x.size] and np.array_equal(o[: x.size].cpu().numpy(), x)
 
 
+def test_decode_ws_line_structured(b64):
+    """MIME / PEM line layouts (the one-pass line path of b64_decode_ws) and their near misses
+    (which take the general path): every result equals the oracle's -- bytes, err_off in the
+    ORIGINAL text, status."""
+    def lines(t, L, sep=b"\r\n", trail=True):
+        parts = []
+        for i in range(0, t.size, L):
+            parts.append(t[i: i + L])
+            if trail or i + L < t.size:
+                parts.append(np.frombuffer(sep, np.uint8))
+        return np.concatenate(parts) if parts else t.copy()
+
+    al = _alphabets(b64)
+    cases = []
+    for n in (1, 2, 3, 54, 57, 58, 1000, 4096 * 3 + 1, 100_000, 1_000_002):
+        for L, sep, trail in ((76, b"\r\n", True), (76, b"\r\n", False), (64, b"\n", True), (64, b"\n", False),
+                              (4, b"\r\n", True), (72, b" ", False)):
+            t = oracle.encode(synth.data(n, seed=n + L))
+            cases.append(lines(t, L, sep, trail))
+    t = oracle.encode(synth.data(100_000, seed=5))
+    mime = lines(t, 76)
+    k = mime.size // 2
+    variants = []
+    for pos, val in ((k, ord("*")), (k, ord("=")), (77, ord("A")), (76, ord("A")), (78 * 5 + 3, ord("\n")),
+                     (mime.size - 3, ord("A")), (mime.size - 4, ord("A")), (mime.size - 1, ord("x"))):
+        v = mime.copy()
+        v[pos] = val
+        variants.append(v)  # bad char / '=' / a separator byte replaced / a whitespace byte inside a line
+    variants.append(np.concatenate([mime, np.frombuffer(b"\r\n", np.uint8)]))      # a blank line at the end
+    variants.append(lines(t, 75))                                                   # L % 4 != 0
+    variants.append(np.concatenate([lines(t[:7600], 76), lines(t[7600:], 64)]))    # line length changes
+    variants.append(lines(t[:-1], 76))                                              # kept chars % 4 != 0
+    variants.append(lines(t[:-3], 76, trail=False))
+    variants.append(np.frombuffer(b"\r\n", np.uint8).copy())
+    variants.append(lines(oracle.encode(synth.data(57, seed=1)), 76)[:-1])           # separator cut short
+    for i, c in enumerate(cases + variants):
+        chars, pad, alpha = al[i % len(al)] if i < len(cases) else al[0]
+        if i < len(cases) and (chars, pad) != (oracle.STANDARD, oracle.PAD):
+            c = oracle.encode(oracle.decode_ws(c)[0], chars, pad)  # re-encode in this alphabet, same layout
+            c = lines(c, [76, 76, 64, 64, 4, 72][i % 6], [b"\r\n", b"\r\n", b"\n", b"\n", b"\r\n", b" "][i % 6],
+                      [True, False, True, False, True, False][i % 6])
+        for lenient in (False, True):
+            ref, rerr, rst = oracle.decode_ws(c, chars, pad, lenient=lenient)
+            a = b64.lenient_of(alpha) if lenient else alpha
+            out, err = b64.decode_ws(to_dev(c, i % 3), a)
+            assert err == rerr, (i, lenient, err, rerr, rst)
+            assert np.array_equal(out.cpu().numpy(), ref), (i, lenient)
+
+
 def _decode_ws_adversarial(b64):
     """Whitespace layouts around the 4 KiB chunks of the fused decode: long runs spanning
     chunks, chunks holding 0-3 kept chars, quads (and the final quad) split across chunks by
