@@ -879,8 +879,17 @@ def next_rows(b64, synth, torch, dev, timeit):
 
     ms = timeit(wsd, reps=5)
     assert int(info[0].item()) == -1 and int(info[2].item()) == n
-    res["whitespace_mime76"] = dict(rate(ms, mw, n), note="input = text incl. CRLF; kernels move ~4.75 B per char "
-                                                          "(count, compact, decode) against 1.75 algorithmic")
+    res["whitespace_mime76"] = dict(rate(ms, mw, n), note="input = text incl. CRLF; line-structured: one pass "
+                                                          "(ws_line_kernel) that decodes and verifies the layout")
+    # the same text with ONE extra blank in the middle: the layout check fails, so the line pass
+    # is wasted and the general path (count / scan / compact / decode) runs -- the worst case
+    tw = torch.cat([tw[: mw // 2], torch.tensor([32], dtype=torch.uint8, device=dev), tw[mw // 2:]])
+    mw = tw.numel()
+    ws = torch.empty(int(L.b64_decode_ws_workspace_bytes(mw)), dtype=torch.uint8, device=dev)
+    ms = timeit(wsd, reps=5)
+    assert int(info[0].item()) == -1 and int(info[2].item()) == n
+    res["whitespace_irregular"] = dict(rate(ms, mw, n), note="MIME text + one stray blank: line pass, then the "
+                                                             "general path (~4.75 B per char moved)")
     del tw, ws
     # streaming: the strict text in 64 MiB pieces (plus the carry joins and the end call)
     carry = torch.zeros(8, dtype=torch.uint8, device=dev)

@@ -282,7 +282,12 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
                 }
             }
         }
-        __syncwarp();
+        // the layout broke here or anywhere else: stop at once (the general path redoes it all)
+        if (__any_sync(kFull, irregular)) {
+            if (lane == 0) atomicExch(&li->mode, 0);
+            break;
+        }
+        if (__ldcg(&li->mode) != 1) break;
         line0 += step_lines;
         col0 += step_col;
         if (col0 >= L) {
@@ -290,7 +295,6 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
             ++line0;
         }
     }
-    if (__any_sync(kFull, irregular) && lane == 0) atomicExch(&li->mode, 0);
     const unsigned hi = __reduce_min_sync(kFull, unsigned(uint64_t(bad) >> 32));
     const unsigned lo = __reduce_min_sync(kFull, unsigned(uint64_t(bad) >> 32) == hi ? unsigned(bad) : ~0u);
     if (lane == 0 && hi != 0x7FFFFFFFu) atomicMin(&li->cell, pack_err(int64_t((uint64_t(hi) << 32) | lo), kBadChar));
