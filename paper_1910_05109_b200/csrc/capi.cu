@@ -426,7 +426,7 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
     WsLine* li = reinterpret_cast<WsLine*>(base + L.off_mc + 64);
     const WsLine* lic = li;
     launch(ws_line_probe_kernel, 1, 32, s, d_in, m, wt, li, mc);
-    launch(ws_line_kernel, int64_t(di->sms) * B64_LINE_MINB, kThreads, s, d_in, m, wt, li, d_out);
+    launch(ws_line_kernel, int64_t(di->sms) * B64_LINE_MINB, kLineThreads, s, d_in, m, wt, li, d_out);
     launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot, lic);
     launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc, lic);
     launch(sw ? ws_compact_kernel<true> : ws_compact_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, static_cast<const int32_t*>(counts),

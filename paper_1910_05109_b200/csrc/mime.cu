@@ -31,7 +31,7 @@
 // guesses the layout, ws_line_kernel decodes straight from the text in one
 // pass and verifies every byte; the general kernels above then return at once
 // (they run when the layout does not hold).  Measured (1 GiB of data as MIME
-// lines of 76 chars + CRLF): 0.83 ms (line kernel 210 us per 256 MiB, ALU-
+// lines of 76 chars + CRLF): 0.70 ms (line kernel ~175 us per 256 MiB, issue-
 // bound); the general path 1.67 ms (per 256 MiB: count 72 us, compact 238
 // us, decode ~100 us; the compaction is issue-bound; alphabets without
 // whitespace chars use an arithmetic per-byte test, ws_bits, for the keep
@@ -95,8 +95,15 @@ struct WsLine {
     unsigned long long cell;  // first interior error, packed (kept index << 3 | kind)
 };
 constexpr int64_t kLineProbe = 65536;  // bytes searched for the first whitespace byte
-constexpr int kLineBlk = 2048;         // kept chars per warp step (two 32-char units per lane)
-constexpr int kLineStage = 2256;       // per-warp stage: kLineBlk chars + separators (L >= 32) + alignment
+#ifndef B64_LINE_BLK
+#define B64_LINE_BLK 4096
+#endif
+#ifndef B64_LINE_THREADS
+#define B64_LINE_THREADS 128
+#endif
+constexpr int kLineThreads = B64_LINE_THREADS;
+constexpr int kLineBlk = B64_LINE_BLK;  // kept chars per warp step (kLineBlk / 1024 units per lane)
+constexpr int kLineStage = kLineBlk + kLineBlk / 16 + 80;  // + separators (L >= 32: <= 2 per 32) + slop
 
 __device__ __forceinline__ int64_t line_orig(int64_t e, int64_t L, int64_t P) { return (e / L) * P + e % L; }
 
@@ -150,14 +157,15 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
     *li = w;
 }
 
-// Decode + verify in line mode.  A warp takes 1024 kept chars at a time: it
-// stages their text span (chars + separators) in shared memory with
-// lane-linear 16-byte loads, then lane l decodes kept chars [32l, 32l + 32)
-// (8 quads, gathered from the stage: a quad never crosses a line since
-// L % 4 == 0) and checks the separator of every line it ends.  Output: 24
-// bytes per lane at out + 3e/4 (3 x STG.64; byte stores in a partial unit).
-// The final quad is left to ws_finalize_kernel; when mc % 4 != 0 (LENGTH)
-// nothing is written, but the structure is still verified.
+// Decode + verify in line mode.  A warp takes kLineBlk kept chars at a time:
+// it stages their text span (chars + separators) in shared memory with
+// lane-linear 16-byte loads; lane j copies line piece j of the span (whole
+// words, funnel-shifted: col0 and L are multiples of 4) into a compact buffer
+// and checks the separator after it; then lane l decodes 32 compacted chars
+// per unit exactly as the fast kernels do (two LDS.128, 32 table look-ups,
+// 3 x STG.64).  Any whitespace among the chars or a wrong separator flags the
+// layout as broken.  The final quad is left to ws_finalize_kernel; when
+// mc % 4 != 0 (LENGTH) nothing is written, but the layout is still verified.
 // x / d for 0 <= x < 2^31 and 32 <= d <= 2^30 without an integer division: a float estimate
 // (relative error ~1e-7, so off by at most one here) corrected either way
 __device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, float inv) {
@@ -168,13 +176,14 @@ __device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, float inv) {
 }
 
 #ifndef B64_LINE_MINB
-#define B64_LINE_MINB 4
+#define B64_LINE_MINB 6
 #endif
-__global__ void __launch_bounds__(kThreads, B64_LINE_MINB)
+__global__ void __launch_bounds__(kLineThreads, B64_LINE_MINB)
 ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li,
                uint8_t* __restrict__ out) {
     __shared__ __align__(256) uint32_t s_lut[64];
-    __shared__ __align__(16) uint8_t s_stage[kThreads / 32][kLineStage];
+    __shared__ __align__(16) uint8_t s_stage[kLineThreads / 32][kLineStage];
+    __shared__ __align__(16) uint8_t s_comp[kLineThreads / 32][kLineBlk + 48];
     griddep_launch_dependents();
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     griddep_wait();
@@ -188,6 +197,7 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
     const float invL = 1.0f / float(L);
     const int64_t P = int64_t(L) + S, nfull = li->nfull, mc = li->mc;
     const uint32_t sep = uint32_t(li->sep);
+    const uint32_t sep_mask = S == 2 ? 0xffffu : (S == 1 ? 0xffu : 0u);
     const bool dec = (mc & 3) == 0;
     const int64_t qfin = dec ? (mc >> 2) - 1 : -1;  // the final quad (ws_finalize_kernel)
     const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -211,59 +221,66 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
             *reinterpret_cast<uint4*>(stg + 16 * c) = ld128_nc(in + b0 + 16 * c);
         __syncwarp();
         const int32_t sb = int32_t(o0 - b0) - col0;  // stage offset of line0's first char
+        const int32_t krel = int32_t(K1 - K0);         // kept chars in this step
+        // 1. separators out: lane j copies line piece j of the step (whole aligned words;
+        //    col0 and L are multiples of 4) into the compact buffer and checks the separator
+        //    after it (full lines ending inside the step)
+        uint32_t* cw = reinterpret_cast<uint32_t*>(&s_comp[threadIdx.x >> 5][0]);
+        const int32_t npieces = div_small(col0 + krel - 1, L, invL) + 1;
+        for (int32_t jp = lane; jp < npieces; jp += 32) {
+            const int32_t c_beg = jp == 0 ? col0 : 0;                         // first col of the piece
+            const int32_t d_beg = jp == 0 ? 0 : jp * L - col0;                // its compact offset
+            const int32_t c_end = min(L, col0 + krel - jp * L);               // one past its last col
+            const int32_t so = jp * int32_t(P) + c_beg + sb;                  // stage offset of c_beg
+            const uint32_t* sw = reinterpret_cast<const uint32_t*>(stg + (so & ~3));
+            const uint32_t sh = uint32_t(so & 3) * 8;
+            uint32_t lo = sw[0];
+            const int nw = (c_end - c_beg + 3) >> 2;
+            for (int k = 0; k < nw; ++k) {
+                const uint32_t hi = sw[k + 1];
+                cw[(d_beg >> 2) + k] = __funnelshift_r(lo, hi, sh);
+                lo = hi;
+            }
+            if (c_end == L && line0 + jp < nfull) {
+                const int32_t sp = so + (c_end - c_beg);
+                const uint32_t got = uint32_t(stg[sp]) | (uint32_t(stg[sp + 1]) << 8);
+                irregular |= ((got ^ sep) & sep_mask) != 0;
+            }
+        }
+        __syncwarp();
+        // 2. decode the compacted chars, 32 per lane and unit (the fast kernels' per-lane code)
 #pragma unroll 1
         for (int u = 0; u < kLineBlk / 1024; ++u) {
             const int32_t ru = 32 * (lane + 32 * u);     // unit's first char, relative to K0
-            const int64_t e = K0 + ru;
-            if (e >= K1) break;
-            const int32_t re = col0 + ru;
-            const int32_t dl = div_small(re, L, invL), col = re - dl * L;
-            const int32_t so0 = dl * int32_t(P) + col + sb;
-            const int32_t left = L - col;               // chars before this line's end (>= 4)
-            const int qs = left >= 32 ? 8 : (left >> 2);  // quads before the line end
-            const int nq = int(min(int64_t(8), (K1 - e) >> 2));
-            const int64_t q0 = e >> 2;
-            // the unit's chars: 10 aligned stage words; quads [qs, 8) sit S bytes further on
-            const uint32_t* sw = reinterpret_cast<const uint32_t*>(stg + (so0 & ~3));
-            uint32_t w[10];
-#pragma unroll
-            for (int k = 0; k < 10; ++k) w[k] = sw[k];
-            const uint32_t sh0 = uint32_t(so0 & 3) * 8;
-            const int t1 = (so0 & 3) + S;
-            const bool c1 = t1 >= 4;
-            const uint32_t sh1 = uint32_t(t1 & 3) * 8;
-            uint32_t x[8], v[8], err = 0;
+            if (ru >= krel) break;
+            const int nq = min(8, (krel - ru) >> 2);
+            const int64_t q0 = (K0 + ru) >> 2;
+            const uint4 a0 = *reinterpret_cast<const uint4*>(cw + (ru >> 2));
+            const uint4 a1 = *reinterpret_cast<const uint4*>(cw + (ru >> 2) + 4);
+            const uint32_t x[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            uint32_t v[8], err = 0;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                x[q] = q < qs ? __funnelshift_r(w[q], w[q + 1], sh0)
-                              : __funnelshift_r(c1 ? w[q + 1] : w[q], c1 ? w[q + 2] : w[q + 1], sh1);
                 uint32_t eq = 0;
                 v[q] = dec_quad_s(x[q], lb, eq);
-                if (q < nq) err |= eq;
-            }
-            if (left <= 32 && line0 + dl < nfull && left <= int32_t(K1 - e)) {
-                // this unit ends a full line: its separator must follow
-                const int32_t sp = so0 + left;
-                for (int b = 0; b < S; ++b) irregular |= stg[sp + b] != ((sep >> (8 * b)) & 0xffu);
+                if (q < nq) err |= eq;  // (the final quad's '=' is sorted out below)
             }
             irregular |= (err & kSkip) != 0;
             const bool tail = nq < 8 || q0 + 7 >= qfin;  // a partial unit or the final quad's
-            if ((err & kInvalid) || tail) {
+            if (err & kInvalid) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     if (q < nq && q0 + q != qfin && bad == INT64_MAX) {
-                        const int j = first_bad_in_quad(x[q], lut);
-                        if (j < 4) bad = 4 * (q0 + q) + j;
+                        const int jb = first_bad_in_quad(x[q], lut);
+                        if (jb < 4) bad = 4 * (q0 + q) + jb;
                     }
                 }
             }
             if (!dec) {
-                // LENGTH: verify the chars of the incomplete group too, write nothing
+                // LENGTH: the chars of the incomplete group must not be whitespace either
                 if (nq < 8 && K1 == mc) {
-                    for (int32_t k = 4 * nq; k < int32_t(min(int64_t(32), K1 - e)); ++k) {
-                        const int32_t rk = re + k, dk = div_small(rk, L, invL);
-                        irregular |= lut[stg[dk * int32_t(P) + (rk - dk * L) + sb]] == kSkip;
-                    }
+                    const uint8_t* cb = reinterpret_cast<const uint8_t*>(cw);
+                    for (int32_t k = ru + 4 * nq; k < min(ru + 32, krel); ++k) irregular |= lut[cb[k]] == kSkip;
                 }
             } else {
                 uint32_t ov[6];
@@ -282,6 +299,7 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
                 }
             }
         }
+        __syncwarp();
         // the layout broke here or anywhere else: stop at once (the general path redoes it all)
         if (__any_sync(kFull, irregular)) {
             if (lane == 0) atomicExch(&li->mode, 0);
