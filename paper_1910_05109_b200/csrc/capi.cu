@@ -749,7 +749,7 @@ const char* b64_build_info(void) {
 #define B64_STR(x) B64_STR2(x)
     return "b64gpu sm_100a, nvcc " B64_STR(__CUDACC_VER_MAJOR__) "." B64_STR(__CUDACC_VER_MINOR__)
            "; kernels enc_fast dec_fast enc_generic dec_generic {enc,dec,codec}_group dec_small ws_* "
-           "{enc,dec}_stream_* peer_combine dec_finalize_* dec_batch_*";
+           "{enc,dec}_stream_* peer_combine ws_line_* dec_finalize_* dec_batch_*";
 }
 
 }  // extern "C"

@@ -1051,6 +1051,40 @@ def test_decode_fused_ctx(b64):
         assert info.tolist() == [-1, 0, x.size] and np.array_equal(o[: x.size].cpu().numpy(), x)
 
 
+def test_concurrent_streams_and_contexts(b64):
+    """Decodes (fused single-launch with one context per stream, plain, MIME) and encodes issued
+    on 4 streams at once, twice over, with no host sync in between: every result equals the
+    oracle's (contexts and workspaces are per call / per stream; the library keeps no per-call
+    state)."""
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    ctxs = [b64.DecodeContext(stream=s_) for s_ in streams]
+    torch.cuda.synchronize()
+    data = [synth.data(n, seed=40 + i) for i, n in enumerate((2_000_003, 700_001, 5_000_000, 1_500_002))]
+    texts = [oracle.encode(x) for x in data]
+    bad = [t.copy() for t in texts]
+    for i, t in enumerate(bad):
+        t[(i + 1) * 10_007] = ord("*")
+    dts, dbad = [to_dev(t) for t in texts], [to_dev(t) for t in bad]
+    dxs = [to_dev(x) for x in data]
+    res = []
+    for rep in range(2):
+        for i, s_ in enumerate(streams):
+            with torch.cuda.stream(s_):
+                src = dbad[i] if (i + rep) % 2 else dts[i]
+                res.append((i, rep, b64.decode_async(src, ctx=ctxs[i]), b64.decode_async(src),
+                            b64.encode(dxs[i])))
+    torch.cuda.synchronize()
+    for i, rep, (o1, inf1), (o2, inf2), e in res:
+        t = bad[i] if (i + rep) % 2 else texts[i]
+        ref, rerr, rst = oracle.decode(t)
+        for o, inf in ((o1, inf1), (o2, inf2)):
+            err, stt, olen = inf.tolist()
+            assert (err, stt) == (rerr, rst), (i, rep, err, rerr)
+            k = ref.size if rerr < 0 else 3 * (rerr // 4)
+            assert olen == k and np.array_equal(o[:k].cpu().numpy(), ref[:k]), (i, rep)
+        assert np.array_equal(e.cpu().numpy(), texts[i]), (i, rep)
+
+
 def test_decode_ws_line_structured(b64):
     """MIME / PEM line layouts (the one-pass line path of b64_decode_ws) and their near misses
     (which take the general path): every result equals the oracle's -- bytes, err_off in the
