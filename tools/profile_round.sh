@@ -25,7 +25,7 @@ PB="python tools/prof_case.py --op batch --reps 1"
 $PB > gpurun_out/${T}_pb.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"generic" -s 2 -c 2 -o gpurun_out/${T}_full_batch $PB > gpurun_out/${T}_ncu_batch.log 2>&1
 echo "full batch rc=$?"
-PW="python tools/ws_probe.py 268435456"
+PW="python tools/ws_probe.py 268435456"   # MIME text: probe + line kernel (+ the general kernels exiting at once)
 $PW > gpurun_out/${T}_pw.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"ws_" -s 4 -c 4 -o gpurun_out/${T}_full_ws $PW > gpurun_out/${T}_ncu_ws.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"ws_" -s 7 -c 7 -o gpurun_out/${T}_full_ws $PW > gpurun_out/${T}_ncu_ws.log 2>&1
 echo "full ws rc=$?"
