@@ -54,7 +54,7 @@ lengths = st.one_of(st.integers(0, 40), st.integers(0, 5000), st.integers(760, 8
 @given(n=lengths, kind=st.sampled_from(["std", "url", "custom"]), aseed=st.integers(0, 50),
        off_in=st.sampled_from([0, 0, 1, 3, 8]), off_out=st.sampled_from([0, 0, 1, 2, 16]),
        lenient=st.booleans(), k_bad=st.integers(0, 3), seed=st.integers(0, 10_000),
-       api=st.sampled_from(["single", "chunk", "group", "codec", "stream", "batch", "unpadded", "ws"]))
+       api=st.sampled_from(["single", "ctx", "chunk", "group", "codec", "stream", "batch", "unpadded", "ws"]))
 def test_fuzz_encode_decode_vs_oracle(b64, n, kind, aseed, off_in, off_out, lenient, k_bad, seed, api):
     chars, pad, alpha = _alpha(b64, kind, aseed)
     if lenient:
@@ -69,7 +69,21 @@ def test_fuzz_encode_decode_vs_oracle(b64, n, kind, aseed, off_in, off_out, leni
             text[-4 + seed % 4] = pad  # a misplaced pad in the final quad
     ref, rerr, rst = oracle.decode(text, chars, pad, lenient=lenient)
     m = text.size
-    if api == "single":
+    if api == "ctx":  # one-launch decode with a self-resetting context (b64_decode_fused)
+        if not hasattr(b64, "_fuzz_ctx"):
+            b64._fuzz_ctx = b64.DecodeContext()
+        # a valid unpadded prefix (n % 3 == 0) takes the text past the single-cluster size, so
+        # the fused kernel runs; the expected result is the oracle's on the concatenation
+        pre = oracle.encode(synth.data(3 * (200_000 + seed), seed=seed + 1), chars, pad)
+        text = np.concatenate([pre, text])
+        ref, rerr, rst = oracle.decode(text, chars, pad, lenient=lenient)
+        m = text.size
+        obuf = torch.empty(3 * (m // 4) + off_out + 8, dtype=torch.uint8, device=DEV)
+        out, info = b64.decode_async(_dev(text, off_in), alpha, out=obuf[off_out: off_out + max(3 * (m // 4), 1)],
+                                     ctx=b64._fuzz_ctx)
+        err, stt, olen = info.tolist()
+        got = out[:olen].cpu().numpy()
+    elif api == "single":
         t = b64.encode(_dev(x, off_in), alpha, out=torch.empty(m + off_out + 8, dtype=torch.uint8,
                                                                device=DEV)[off_out:])
         assert np.array_equal(t.cpu().numpy(), ref_t)
