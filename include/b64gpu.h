@@ -152,8 +152,10 @@ int b64_decode_unpadded(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b6
  * decoded, as in b64_decode_ex), else the exact prefix as in b64_decode_ex.
  * Needs a device workspace of
  * b64_decode_ws_workspace_bytes(m) bytes (~m + m/1000 + 17 KiB) and d_out
- * 16-byte aligned with capacity 3*(m/4).  Asynchronous: count, scan, compact,
- * decode and finalize kernels on `stream`. */
+ * 16-byte aligned with capacity 3*(m/4).  Asynchronous on `stream`: texts up
+ * to 512 KiB are one cluster launch; larger line-structured text (MIME / PEM)
+ * is decoded in one pass; anything else goes through count, scan, compact,
+ * decode and finalize kernels. */
 int64_t b64_decode_ws_workspace_bytes(int64_t m);
 int b64_decode_ws(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a, uint8_t *d_ws,
                   int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len, b64_stream_t stream);

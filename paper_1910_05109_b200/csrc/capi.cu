@@ -75,7 +75,8 @@ const DevInfo* dev_info() {
     }
     info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
     info.occ_dec_gen = info.occ_dec_gen < 1 ? 1 : info.occ_dec_gen;
-    if (cudaFuncSetAttribute(dec_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    if (cudaFuncSetAttribute(dec_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaFuncSetAttribute(ws_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         return nullptr;
     g_dev[d] = info;
     g_dev_ready[d] = true;
@@ -401,6 +402,35 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
     const DevInfo* di = dev_info();
     if (!di) return B64_ECUDA;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (m > 0 && m <= std::min(small_max(), kWsSmallMax)) {
+        // small text: the whole decode is ONE cluster launch (mime.cu ws_small_kernel)
+        uint8_t* comp = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
+        WsTab wt;
+        uint8_t* wb = reinterpret_cast<uint8_t*>(wt.w);
+        std::memcpy(wb, a->dec, 256);
+        for (int c : {0x09, 0x0A, 0x0B, 0x0C, 0x0D, 0x20})
+            if (wb[c] == 0x80) wb[c] = kSkip;
+        int64_t r = (m + 8191) / 8192;  // one 512-byte step per warp and CTA at 8 KiB
+        r = r < 1 ? 1 : (r > kSmallCluster ? kSmallCluster : r);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(r));
+        cfg.blockDim = dim3(kWsSmallThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = unsigned(r);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl_enabled() ? 2 : 1;
+        if (cudaLaunchKernelEx(&cfg, ws_small_kernel, d_in, m, wt, uint32_t(a->pad),
+                               uint32_t((a->flags & B64_ALPHA_LENIENT) ? 1 : 0), comp, d_out, d_err_off, d_status,
+                               d_out_len) != cudaSuccess)
+            return (cudaGetLastError(), B64_ECUDA);
+        return launched();
+    }
     if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), s) != cudaSuccess) return B64_ECUDA;
     if (m == 0) {
         launch(dec_finalize_packed_kernel, 1, 1, s, static_cast<const int64_t*>(d_err_off), d_err_off, d_status);

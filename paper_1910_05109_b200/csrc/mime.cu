@@ -26,6 +26,8 @@
 //                         text: CTA (binary search) -> chunk -> byte.
 // Traffic: read m (count) + read m, write m' (compact) + read m', write 3m'/4
 // (decode), i.e. ~4.75 B per char against 1.75 for the strict decode.
+// Texts up to 512 KiB take ONE cluster launch instead (ws_small_kernel: the
+// same steps separated by cluster barriers).
 // Line-structured text (MIME / PEM: every line L >= 32 chars, L % 4 == 0,
 // then the same 1-2 whitespace bytes) skips all of that: ws_line_probe_kernel
 // guesses the layout, ws_line_kernel decodes straight from the text in one
@@ -517,6 +519,195 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
         if (lane < n_kept - tail0) d[tail0 + lane] = buf[tail0 + lane];
         __syncwarp();
     }
+}
+
+// ---------------------------------------------------------------- small texts: one launch
+// For texts up to the single-launch size the whole whitespace-skipping decode
+// is ONE cluster launch (the general path's steps, cluster-synchronised instead
+// of separate kernels): every warp counts the kept chars of its slice; CTA and
+// cluster prefix sums through shared memory and DSMEM; every warp writes its
+// kept chars to the workspace at their compacted positions; cluster barrier;
+// the interior quads are decoded by all threads, the final quad by the last
+// one; CTA 0 maps the first error back to the original text.
+constexpr int kWsSmallThreads = 512;
+constexpr int kWsSmallWarps = kWsSmallThreads / 32;
+constexpr int64_t kWsSmallMax = int64_t(16) * kWsSmallWarps * 4 * 512;  // 16 CTAs x warps x 4 steps of 512 B
+
+__global__ void __launch_bounds__(kWsSmallThreads)
+ws_small_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, uint32_t pad, uint32_t lenient,
+                uint8_t* __restrict__ comp, uint8_t* __restrict__ out, int64_t* __restrict__ err_off,
+                int32_t* __restrict__ status, int64_t* __restrict__ out_len) {
+    __shared__ __align__(256) uint32_t s_lut[64];
+    __shared__ int32_t s_wcnt[kWsSmallWarps], s_wpre[kWsSmallWarps];
+    __shared__ int64_t s_tot, s_base, s_mc;
+    __shared__ int32_t s_kfin;
+    __shared__ unsigned long long s_min;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    if (threadIdx.x == 0) {
+        s_min = kErrNone;
+        s_kfin = 3;
+    }
+    griddep_wait();
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const int R = int(gridDim.x);  // the grid is one cluster
+    const int64_t C = (((m + R - 1) / R) + 8191) & ~int64_t(8191);  // bytes per CTA (512 per warp-step)
+    const int64_t Cw = C / kWsSmallWarps;
+    const int64_t wb = min(m, int64_t(blockIdx.x) * C + w * Cw), we = min(m, wb + Cw);
+    const bool vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    // keep mask of lane's 16 bytes at i (bytes past `we` dropped)
+    auto keep16 = [&](int64_t i, uint4& v) -> uint32_t {
+        uint32_t mask = 0;
+        if (vec && i + 16 <= we) {
+            v = ld128_nc(in + i);
+            const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mask |= ws_keep4(lut, wv[q]) << (4 * q);
+        } else {
+            uint32_t wv[4] = {0, 0, 0, 0};
+            for (int b = 0; b < 16; ++b) {
+                if (i + b < we) {
+                    const uint32_t c = in[i + b];
+                    wv[b >> 2] |= c << (8 * (b & 3));
+                    if (lut[c] != kSkip) mask |= 1u << b;
+                }
+            }
+            v = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+        return mask;
+    };
+    // 1. kept chars per warp slice, CTA prefix, cluster prefix (DSMEM)
+    int32_t cnt = 0;
+    for (int64_t i0 = wb; i0 < we; i0 += 512) {
+        uint4 v;
+        const int64_t i = i0 + 16 * lane;
+        cnt += i < we ? __popc(keep16(i, v)) : 0;
+    }
+    cnt = __reduce_add_sync(kFull, cnt);
+    if (lane == 0) s_wcnt[w] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t run = 0;
+        for (int k = 0; k < kWsSmallWarps; ++k) {
+            s_wpre[k] = run;
+            run += s_wcnt[k];
+        }
+        s_tot = run;
+    }
+    cluster.sync();
+    if (threadIdx.x == 0) {
+        int64_t base = 0, mc = 0;
+        for (int q = 0; q < R; ++q) {
+            const int64_t t = *cluster.map_shared_rank(&s_tot, q);
+            if (q < int(blockIdx.x)) base += t;
+            mc += t;
+        }
+        s_base = base;
+        s_mc = mc;
+    }
+    __syncthreads();
+    // 2. kept chars to their compacted positions (workspace)
+    int64_t dst = s_base + s_wpre[w];
+    for (int64_t i0 = wb; i0 < we; i0 += 512) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        const int64_t i = i0 + 16 * lane;
+        const uint32_t mask = i < we ? keep16(i, v) : 0u;
+        const int k = __popc(mask);
+        int incl = k;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += y;
+        }
+        int64_t pos = dst + incl - k;
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int b = 0; b < 16; ++b)
+            if (mask & (1u << b)) comp[pos++] = uint8_t(wv[b >> 2] >> (8 * (b & 3)));
+        dst += __shfl_sync(kFull, incl, 31);
+    }
+    cluster.sync();  // every CTA's compacted chars are visible cluster-wide
+    // 3. strict decode of the compacted text (interior quads by all threads, the final one last)
+    const int64_t mc = s_mc;
+    if ((mc & 3) == 0 && mc > 0) {
+        const int64_t Q = mc >> 2;
+        const int64_t gthreads = int64_t(R) * kWsSmallThreads;
+        const int64_t gtid = int64_t(blockIdx.x) * kWsSmallThreads + threadIdx.x;
+        for (int64_t q = gtid; q < Q - 1; q += gthreads) {
+            const uint32_t x = ld32(comp + 4 * q);
+            uint32_t e = 0;
+            const uint32_t v = dec_quad(x, lut, e);
+            store_bytes(out + 3 * q, v, 3);
+            if (e & kInvalid) atomicMin(&s_min, pack_err(4 * q + first_bad_in_quad(x, lut), kBadChar));
+        }
+        if (gtid == gthreads - 1) {
+            int bad, k;
+            uint32_t v;
+            const uint32_t kind = final_quad(ld32(comp + 4 * (Q - 1)), lut, pad, lenient, &bad, &k, &v);
+            if (kind == kOk) {
+                store_bytes(out + 3 * (Q - 1), v, k);
+                s_kfin = k;
+            } else {
+                atomicMin(&s_min, pack_err(4 * (Q - 1) + bad, kind));
+            }
+        }
+    }
+    cluster.sync();
+    // 4. CTA 0, warp 0: results; the first error's kept index back to the text
+    if (blockIdx.x == 0 && w == 0) {
+        unsigned long long mn = kErrNone;
+        for (int q = 0; q < R; ++q) {
+            const unsigned long long v = *cluster.map_shared_rank(&s_min, q);
+            mn = v < mn ? v : mn;
+        }
+        int64_t e = -1, ol = 0;
+        int32_t kind = kOk;
+        if (mc & 3) {
+            e = mc - (mc & 3);
+            kind = kLength;
+        } else if (mn < kErrNone) {
+            e = int64_t(mn >> 3);
+            kind = int32_t(mn & 7);
+        } else if (mc > 0) {
+            ol = 3 * (mc >> 2) - 3 + *cluster.map_shared_rank(&s_kfin, R - 1);
+        }
+        int64_t pos = -1;
+        if (e >= 0) {
+            // the CTA, then the warp slice holding kept index e, then the byte
+            int q = 0;
+            int64_t base = 0;
+            for (; q < R - 1; ++q) {
+                const int64_t t = *cluster.map_shared_rank(&s_tot, q);
+                if (base + t > e) break;
+                base += t;
+            }
+            const int32_t* wpre = cluster.map_shared_rank(s_wpre, q);
+            int ww = kWsSmallWarps - 1;
+            while (ww > 0 && base + wpre[ww] > e) --ww;
+            int64_t want = e - base - wpre[ww];
+            const int64_t b0 = min(m, int64_t(q) * C + ww * Cw), b1 = min(m, b0 + Cw);
+            for (int64_t i0 = b0; i0 < b1 && pos < 0; i0 += 32) {
+                const int64_t i = i0 + lane;
+                const uint32_t bal = __ballot_sync(kFull, i < b1 && lut[in[i]] != kSkip);
+                const int k = __popc(bal);
+                if (want < k) {
+                    uint32_t b = bal;
+                    for (int64_t t = 0; t < want; ++t) b &= b - 1;
+                    pos = i0 + (__ffs(b) - 1);
+                } else {
+                    want -= k;
+                }
+            }
+        }
+        if (lane == 0) {
+            *err_off = pos;
+            if (status) *status = kind;
+            if (out_len) *out_len = e < 0 ? ol : (kind == kLength ? 0 : 3 * (e >> 2));
+        }
+    }
+    cluster.sync();  // keep every CTA's shared memory alive until CTA 0 has read it
 }
 
 // One warp.  Finalises a whitespace-skipping decode: the strict decode of the

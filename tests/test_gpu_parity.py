@@ -1085,6 +1085,40 @@ def test_concurrent_streams_and_contexts(b64):
         assert np.array_equal(e.cpu().numpy(), texts[i]), (i, rep)
 
 
+def test_decode_ws_small_single_launch(b64):
+    """Texts up to the single-launch size (one cluster: 1-16 CTAs of 16 warps, 8 KiB per CTA step):
+    sizes around the CTA and warp-slice boundaries, random whitespace, an error in every CTA's
+    slice in turn, the LENGTH rule, all-whitespace text, unaligned input, lenient alphabet --
+    bytes, err_off (original coordinates) and status equal the oracle's."""
+    rng = np.random.default_rng(17)
+    ws = np.frombuffer(b" \t\n\r\x0b\x0c", np.uint8)
+    for target in (5, 511, 512, 513, 8191, 8192, 8193, 3 * 8192 + 7, 100_000, 400_000, 524_288):
+        n = max(1, (target * 3) // 4 - target // 40)
+        t = oracle.encode(synth.data(n, seed=target))
+        k = max(0, target - t.size)
+        pos = np.sort(rng.integers(0, t.size + 1, k))
+        text = np.insert(t, pos, ws[rng.integers(0, 6, k)])[:target] if k else t[:target]
+        variants = [text]
+        R = min(16, max(1, (text.size + 8191) // 8192))
+        C = (((text.size + R - 1) // R) + 8191) // 8192 * 8192
+        for r in range(R):  # one bad char in each CTA's slice
+            keep = np.nonzero(~np.isin(text, ws))[0]
+            cand = keep[(keep >= r * C) & (keep < (r + 1) * C)]
+            if cand.size:
+                v = text.copy()
+                v[cand[cand.size // 2]] = ord("*")
+                variants.append(v)
+        variants.append(np.concatenate([text, np.frombuffer(b"A", np.uint8)]))  # kept % 4 != 0 (usually)
+        variants.append(np.full(min(target, 3000), ord(" "), np.uint8))          # whitespace only
+        for i, v in enumerate(variants):
+            for lenient in (False, True):
+                ref, rerr, rst = oracle.decode_ws(v, lenient=lenient)
+                a = b64.lenient_of(b64.standard()) if lenient else b64.standard()
+                out, err = b64.decode_ws(to_dev(v, i % 2), a)
+                assert err == rerr, (target, i, lenient, err, rerr, rst)
+                assert np.array_equal(out.cpu().numpy(), ref), (target, i, lenient)
+
+
 def test_decode_ws_line_structured(b64):
     """MIME / PEM line layouts (the one-pass line path of b64_decode_ws) and their near misses
     (which take the general path): every result equals the oracle's -- bytes, err_off in the
