@@ -187,6 +187,34 @@ __device__ __forceinline__ void ld_unaligned64(const uint8_t* p, uint32_t (&w)[N
     }
 }
 __device__ __forceinline__ void ld24_unaligned(const uint8_t* p, uint32_t (&w)[6]) { ld_unaligned64<6>(p, w); }
+// NW words at any alignment from 2-3 aligned 16-byte loads (L1-allocating: a neighbouring
+// lane's unit shares the edge blocks) -- fewer L1 wavefronts than LDG.64 for the batch
+// decode, whose 32-char units sit at a 32-byte lane stride (tools/ab_batch.sh: configs[3]
+// decode +0.6 %, 64 KiB strings +2.6 %; the 24-byte encode units measured 11 % slower).
+__device__ __forceinline__ uint4 ld128_l1(const void* p) {
+    uint4 r;
+    asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+template <int NW>
+__device__ __forceinline__ void ld_unaligned128(const uint8_t* p, uint32_t (&x)[NW]) {
+    const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+    const uint4* pa = reinterpret_cast<const uint4*>(u & ~uintptr_t(15));
+    const uint32_t sb = uint32_t(u & 15);
+    const uint4 a = ld128_l1(pa), b = ld128_l1(pa + 1);
+    const uint4 c = (4 * NW + sb > 32) ? ld128_l1(pa + 2) : make_uint4(0, 0, 0, 0);
+    const uint32_t v[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+    const int ws = int(sb >> 2);
+    const uint32_t sh = (sb & 3) * 8;
+    uint32_t wsel[NW + 1];
+#pragma unroll
+    for (int i = 0; i <= NW; ++i)
+        wsel[i] = ws == 0 ? v[i] : ws == 1 ? v[i + 1] : ws == 2 ? v[i + 2] : v[i + 3 < 12 ? i + 3 : 11];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) x[i] = __funnelshift_r(wsel[i], wsel[i + 1], sh);
+}
+__device__ __forceinline__ void ld32_unaligned128(const uint8_t* p, uint32_t (&x)[8]) { ld_unaligned128<8>(p, x); }
+
 __device__ __forceinline__ void ld32_unaligned(const uint8_t* p, uint32_t (&w)[8]) { ld_unaligned64<8>(p, w); }
 
 // ----------------------------------------------------------------- encode

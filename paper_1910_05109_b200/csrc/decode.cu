@@ -387,7 +387,7 @@ dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
             uint32_t err = 0;
             if (act) {
                 uint32_t x[8], v[8], ov[6];
-                ld32_unaligned(in + ua + 32 * k, x);
+                ld32_unaligned128(in + ua + 32 * k, x);
 #pragma unroll
                 for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(x[q], lb, err);
                 dec_pack12(v[0], v[1], v[2], v[3], ov[0], ov[1], ov[2]);

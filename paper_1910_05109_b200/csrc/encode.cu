@@ -308,7 +308,7 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
         const int64_t ke = min(U, (hi - ua + 23) / 24);
         for (int64_t k = kb + lane; k < ke; k += 32) {
             uint32_t wv[6], ov[8];
-            ld24_unaligned(in + ua + 24 * k, wv);
+            ld24_unaligned(in + ua + 24 * k, wv);  // (2-3 LDG.128 instead: configs[3] encode -11 %)
             enc_lane_compute(wv, ov, lb);
             st256(o + 4 * h + 32 * k, ov);
         }
