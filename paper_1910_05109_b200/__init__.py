@@ -154,10 +154,26 @@ def decode_async(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[to
     return out, info
 
 
+_CTX_CACHE = {}  # (device index, stream handle) -> DecodeContext, for the synchronous decode()
+
+
+def _stream_ctx(dev: torch.device, stream: Optional[torch.cuda.Stream]) -> DecodeContext:
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    key = (dev.index, s.cuda_stream)
+    ctx = _CTX_CACHE.get(key)
+    if ctx is None:
+        ctx = _CTX_CACHE[key] = DecodeContext(dev, stream=s)
+    return ctx
+
+
 def decode(t: torch.Tensor, a: Optional[Alphabet] = None, out: Optional[torch.Tensor] = None,
            stream: Optional[torch.cuda.Stream] = None, ctx: Optional[DecodeContext] = None) -> Tuple[torch.Tensor, int]:
     """Validating decode.  Returns (decoded bytes, err_off); err_off = -1 when valid.
-    Forces one 24-byte device->host read of (err_off, status, out_len)."""
+    Forces one 24-byte device->host read of (err_off, status, out_len).  One kernel launch:
+    the call is synchronous, so a context cached per (device, stream) can serve every call
+    on that stream (b64_decode_fused)."""
+    if ctx is None:
+        ctx = _stream_ctx(t.device, stream)
     out, info = decode_async(t, a, out=out, stream=stream, ctx=ctx)
     err, _, olen = info.tolist()
     return out[:olen], err
