@@ -83,7 +83,8 @@ __device__ __forceinline__ uint32_t keep4(const uint8_t* lut, uint32_t x) {
 
 // ---------------------------------------------------------------- line-structured text
 // MIME / PEM text is lines of L chars (L % 4 == 0) each followed by the same
-// 1-2 whitespace bytes, the last line possibly shorter.  Then kept char e sits
+// 1-2 whitespace bytes, the last line possibly shorter (and any whitespace
+// after it, e.g. blank lines at the end of a mail part).  Then kept char e sits
 // at orig(e) = (e / L) * P + e % L (P = L + s): no compaction is needed.  A
 // one-warp probe guesses (L, s, separator) from the first whitespace byte and
 // the text's end; ws_line_kernel decodes straight from the text AND verifies
@@ -120,7 +121,16 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
     griddep_wait();
     __syncwarp();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
-    const int64_t lim = min(m, kLineProbe);
+    // trailing whitespace (a final line break, blank lines, blanks) is skipped anyway: the
+    // layout is read on [0, me), me = one past the last non-whitespace byte (searched in the
+    // last kLineProbe bytes)
+    int64_t me = -1;
+    for (int64_t j0 = m; j0 > 0 && m - j0 < kLineProbe && me < 0; j0 -= 32) {
+        const int64_t i = j0 - 1 - lane;
+        const uint32_t bal = __ballot_sync(kFull, i >= 0 && lut[in[i]] != kSkip);
+        if (bal) me = j0 - (__ffs(bal) - 1);
+    }
+    const int64_t lim = min(me, kLineProbe);
     int64_t p = -1;
     for (int64_t i0 = 0; i0 < lim && p < 0; i0 += 32) {
         const int64_t i = i0 + lane;
@@ -131,26 +141,19 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
     WsLine w;
     w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.cell = kErrNone;
     *mc_general = 0;  // the general path's decode does nothing unless its scan runs
-    if (m > 0 && p < 0) {  // no whitespace seen: one line (ws_line_kernel checks the rest)
-        w.mode = 1; w.r = m; w.mc = m;
-        w.L = int32_t(min(int64_t(1) << 30, (m + 4) & ~int64_t(3)));  // any multiple of 4 above m
+    if (me <= 0) {
+        // whitespace only, or a trailing run longer than the probe: the general path
+    } else if (p < 0) {  // no whitespace before the trailing run (in the probe window): one line
+        w.mode = 1; w.r = me; w.mc = me;
+        w.L = int32_t(min(int64_t(1) << 30, (me + 4) & ~int64_t(3)));  // any multiple of 4 above me
     } else if (p >= 32 && (p & 3) == 0 && p < (int64_t(1) << 30)) {  // (shorter lines: general path)
         int s = 0;
-        while (s < 3 && p + s < m && lut[in[p + s]] == kSkip) ++s;
+        while (s < 3 && p + s < me && lut[in[p + s]] == kSkip) ++s;
         if (s <= 2) {
+            // full lines each followed by the separator, then a last line of 1..L chars
             const int64_t L = p, P = p + s;
-            const int64_t nfull = m / P, rem = m - nfull * P;
-            int64_t r = -1;
-            if (rem == 0) {
-                r = 0;
-            } else if (lut[in[m - 1]] == kSkip) {  // a separator after a shorter last line
-                bool same = rem > s;
-                for (int b = 0; b < s && same; ++b) same = in[m - s + b] == in[p + b];
-                if (same) r = rem - s;
-            } else if (rem <= L) {
-                r = rem;
-            }
-            if (r >= 0) {
+            const int64_t nfull = (me - 1) / P, r = me - nfull * P;
+            if (r >= 1 && r <= L) {
                 w.mode = 1; w.L = int32_t(L); w.s = s; w.nfull = nfull; w.r = r; w.mc = nfull * L + r;
                 w.sep = int32_t(s > 0 ? in[p] : 0) | int32_t(s > 1 ? in[p + 1] : 0) << 8;
             }

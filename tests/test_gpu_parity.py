@@ -1148,6 +1148,9 @@ def test_decode_ws_line_structured(b64):
         v[pos] = val
         variants.append(v)  # bad char / '=' / a separator byte replaced / a whitespace byte inside a line
     variants.append(np.concatenate([mime, np.frombuffer(b"\r\n", np.uint8)]))      # a blank line at the end
+    variants.append(np.concatenate([mime, np.frombuffer(b"\r\n\r\n  \t\n", np.uint8)]))  # trailing blanks
+    variants.append(np.concatenate([mime[:-2], np.full(70_000, ord(" "), np.uint8)]))  # past the probe window
+    variants.append(np.concatenate([lines(t, 76, trail=False), np.frombuffer(b"   ", np.uint8)]))
     variants.append(lines(t, 75))                                                   # L % 4 != 0
     variants.append(np.concatenate([lines(t[:7600], 76), lines(t[7600:], 64)]))    # line length changes
     variants.append(lines(t[:-1], 76))                                              # kept chars % 4 != 0

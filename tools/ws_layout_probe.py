@@ -15,8 +15,12 @@ crlf = torch.tensor([13, 10], dtype=torch.uint8, device=dev).expand(lines, 2)
 tw = torch.cat([torch.cat([body, crlf], 1).reshape(-1), t[lines * 76:]])
 out = torch.empty(3 * (m // 4) + 8, dtype=torch.uint8, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-for tag, pos in (("regular", None), ("stray_at_1KiB", 1024), ("stray_mid", tw.numel() // 2), ("stray_end", tw.numel() - 100)):
-    tt = tw if pos is None else torch.cat([tw[:pos], torch.tensor([32], dtype=torch.uint8, device=dev), tw[pos:]])
+for tag, pos in (("regular", None), ("stray_at_1KiB", 1024), ("stray_mid", tw.numel() // 2),
+                 ("stray_end", tw.numel() - 100), ("trailing_blank_lines", -1)):
+    if pos == -1:
+        tt = torch.cat([tw, torch.tensor([13, 10, 13, 10], dtype=torch.uint8, device=dev)])
+    else:
+        tt = tw if pos is None else torch.cat([tw[:pos], torch.tensor([32], dtype=torch.uint8, device=dev), tw[pos:]])
     ws = torch.empty(int(b64._lib.lib().b64_decode_ws_workspace_bytes(tt.numel())), dtype=torch.uint8, device=dev)
     o, err = b64.decode_ws(tt, out=out, workspace=ws)
     assert err == -1 and torch.equal(o, x)
