@@ -96,6 +96,7 @@ struct WsLine {
     int32_t L, s, sep;        // chars per full line, separator bytes (0-2) and their values (LE)
     int64_t nfull, r, mc;     // full lines, chars of the last partial line, kept chars
     unsigned long long cell;  // first interior error, packed (kept index << 3 | kind)
+    int64_t off;              // leading whitespace bytes (the first line starts here)
 };
 constexpr int64_t kLineProbe = 65536;  // bytes searched for the first whitespace byte
 #ifndef B64_LINE_BLK
@@ -130,31 +131,40 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
         const uint32_t bal = __ballot_sync(kFull, i >= 0 && lut[in[i]] != kSkip);
         if (bal) me = j0 - (__ffs(bal) - 1);
     }
-    const int64_t lim = min(me, kLineProbe);
+    // leading whitespace likewise: the first line starts at ms (searched in the first
+    // kLineProbe bytes); p = the first whitespace byte after it
+    int64_t ms = -1;
+    for (int64_t i0 = 0; i0 < min(me, kLineProbe) && ms < 0; i0 += 32) {
+        const int64_t i = i0 + lane;
+        const uint32_t bal = __ballot_sync(kFull, i < me && lut[in[i]] != kSkip);
+        if (bal) ms = i0 + __ffs(bal) - 1;
+    }
+    const int64_t lim = ms < 0 ? 0 : min(me, ms + kLineProbe);
     int64_t p = -1;
-    for (int64_t i0 = 0; i0 < lim && p < 0; i0 += 32) {
+    for (int64_t i0 = ms; i0 >= 0 && i0 < lim && p < 0; i0 += 32) {
         const int64_t i = i0 + lane;
         const uint32_t bal = __ballot_sync(kFull, i < lim && lut[in[i]] == kSkip);
         if (bal) p = i0 + __ffs(bal) - 1;
     }
     if (lane) return;
     WsLine w;
-    w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.cell = kErrNone;
+    w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.cell = kErrNone; w.off = 0;
     *mc_general = 0;  // the general path's decode does nothing unless its scan runs
-    if (me <= 0) {
-        // whitespace only, or a trailing run longer than the probe: the general path
-    } else if (p < 0) {  // no whitespace before the trailing run (in the probe window): one line
-        w.mode = 1; w.r = me; w.mc = me;
-        w.L = int32_t(min(int64_t(1) << 30, (me + 4) & ~int64_t(3)));  // any multiple of 4 above me
-    } else if (p >= 32 && (p & 3) == 0 && p < (int64_t(1) << 30)) {  // (shorter lines: general path)
+    if (me <= 0 || ms < 0) {
+        // whitespace only, or a leading / trailing run longer than the probe: the general path
+    } else if (p < 0) {  // no whitespace between ms and the trailing run (probe window): one line
+        const int64_t n1 = me - ms;
+        w.mode = 1; w.r = n1; w.mc = n1; w.off = ms;
+        w.L = int32_t(min(int64_t(1) << 30, (n1 + 4) & ~int64_t(3)));  // any multiple of 4 above n1
+    } else if (p - ms >= 32 && ((p - ms) & 3) == 0 && p - ms < (int64_t(1) << 30)) {  // (else: general)
         int s = 0;
         while (s < 3 && p + s < me && lut[in[p + s]] == kSkip) ++s;
         if (s <= 2) {
             // full lines each followed by the separator, then a last line of 1..L chars
-            const int64_t L = p, P = p + s;
-            const int64_t nfull = (me - 1) / P, r = me - nfull * P;
+            const int64_t L = p - ms, P = L + s, n1 = me - ms;
+            const int64_t nfull = (n1 - 1) / P, r = n1 - nfull * P;
             if (r >= 1 && r <= L) {
-                w.mode = 1; w.L = int32_t(L); w.s = s; w.nfull = nfull; w.r = r; w.mc = nfull * L + r;
+                w.mode = 1; w.L = int32_t(L); w.s = s; w.nfull = nfull; w.r = r; w.mc = nfull * L + r; w.off = ms;
                 w.sep = int32_t(s > 0 ? in[p] : 0) | int32_t(s > 1 ? in[p + 1] : 0) << 8;
             }
         }
@@ -200,7 +210,7 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
     uint8_t* stg = &s_stage[threadIdx.x >> 5][0];
     const int32_t L = li->L, S = li->s;             // L >= 32: a 32-char unit crosses <= 1 line end
     const float invL = 1.0f / float(L);
-    const int64_t P = int64_t(L) + S, nfull = li->nfull, mc = li->mc;
+    const int64_t P = int64_t(L) + S, nfull = li->nfull, mc = li->mc, li_off = li->off;
     const uint32_t sep = uint32_t(li->sep);
     const uint32_t sep_mask = S == 2 ? 0xffffu : (S == 1 ? 0xffu : 0u);
     const bool dec = (mc & 3) == 0;
@@ -218,7 +228,7 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
         const int64_t K0 = it * kLineBlk, K1 = min(K0 + kLineBlk, mc);
         const int32_t rl = int32_t(K1 - 1 - K0) + col0;  // last char, relative to line0's start
         const int32_t dll = div_small(rl, L, invL);
-        const int64_t o0 = line0 * P + col0;
+        const int64_t o0 = li_off + line0 * P + col0;
         const int64_t o1 = min(m, o0 + int64_t(dll) * P + (rl - dll * L - col0) + 1 + S);
         const int64_t b0 = o0 - int64_t(reinterpret_cast<uintptr_t>(in + o0) & 15);
         const int nch = int((o1 - b0 + 15) >> 4);
@@ -740,7 +750,7 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
             kind = kLength;
         } else {
             uint32_t x = 0;
-            for (int b = 0; b < 4; ++b) x |= uint32_t(in[line_orig(mcl - 4 + b, L, P)]) << (8 * b);
+            for (int b = 0; b < 4; ++b) x |= uint32_t(in[li->off + line_orig(mcl - 4 + b, L, P)]) << (8 * b);
             int fb = 0, k = 0;
             uint32_t v = 0;
             const uint32_t fk = final_quad(x, lut, pad, lenient, &fb, &k, &v);
@@ -753,7 +763,7 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
                 store_bytes(out + 3 * ((mcl >> 2) - 1), v, k);
             }
         }
-        *err_off = e < 0 ? -1 : line_orig(e, L, P);
+        *err_off = e < 0 ? -1 : li->off + line_orig(e, L, P);
         if (status) *status = kind;
         if (out_len) *out_len = e < 0 ? ol : (kind == kLength ? 0 : 3 * (e >> 2));
         return;

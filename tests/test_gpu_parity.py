@@ -1151,6 +1151,11 @@ def test_decode_ws_line_structured(b64):
     variants.append(np.concatenate([mime, np.frombuffer(b"\r\n\r\n  \t\n", np.uint8)]))  # trailing blanks
     variants.append(np.concatenate([mime[:-2], np.full(70_000, ord(" "), np.uint8)]))  # past the probe window
     variants.append(np.concatenate([lines(t, 76, trail=False), np.frombuffer(b"   ", np.uint8)]))
+    variants.append(np.concatenate([np.frombuffer(b"\r\n \t", np.uint8), mime]))          # leading blanks
+    variants.append(np.concatenate([np.full(70_001, ord("\n"), np.uint8), mime]))        # past the probe window
+    v = np.concatenate([np.frombuffer(b"\n\n", np.uint8), mime]).copy()
+    v[2 + 78 * 3 + 10] = ord("*")                                                      # offset + bad char
+    variants.append(v)
     variants.append(lines(t, 75))                                                   # L % 4 != 0
     variants.append(np.concatenate([lines(t[:7600], 76), lines(t[7600:], 64)]))    # line length changes
     variants.append(lines(t[:-1], 76))                                              # kept chars % 4 != 0
