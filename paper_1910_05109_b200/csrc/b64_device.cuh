@@ -338,10 +338,22 @@ __global__ void enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8
                                 uint32_t pad);
 __global__ void enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab,
                                    uint32_t pad);
+// A streaming decode's join (stream.cu): the quad made of the H held chars and the piece's
+// first 4 - H chars, and the carry update (the piece's last R chars), folded into the piece's
+// bulk kernel when that is dec_fast (active = 0: nothing to do).
+struct StreamJoin {
+    uint8_t* carry;
+    const uint8_t* in;   // the piece
+    uint8_t* out;        // the piece's output (the join quad's 3 bytes go first)
+    int64_t m;           // piece chars
+    int64_t base;        // stream position of the join quad (consumed - H)
+    int32_t H;           // held chars before the piece
+    int32_t active;
+};
 template <int D>
 __global__ void dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
-                                int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev);
+                                int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev, StreamJoin join);
 __global__ void dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off,
                                    DecTab tab, int64_t base, int is_final_single,
                                    unsigned long long* __restrict__ err_cells, int64_t* __restrict__ out_len_single);

@@ -287,17 +287,24 @@ int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabe
 }
 
 static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t base,
-                         int is_final, int64_t* cell, int64_t* out_len, cudaStream_t s) {
+                         int is_final, int64_t* cell, int64_t* out_len, cudaStream_t s,
+                         const StreamJoin* join = nullptr, bool* joined = nullptr) {
     const DevInfo* di = dev_info();
     if (!di) return B64_ECUDA;
     unsigned long long* c = reinterpret_cast<unsigned long long*>(cell);
+    if (joined) *joined = false;
     if (aligned(d_in, 32) && aligned(d_out, 16)) {
         const int64_t nchunk = (m / 4) / 256;
         const int dd = dec_depth(m);
         const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(di->occ_dec_fast[dd]));
         auto k = pick2(dd, dec_fast_kernel<1>, dec_fast_kernel<2>);
+        StreamJoin sj = {};
+        if (join && joined) {  // the stream join rides along (its last thread)
+            sj = *join;
+            *joined = true;
+        }
         launch(k, blocks, kThreads, s, d_in, m, d_out, dec_tab(a), base, is_final, c, out_len,
-               static_cast<const int64_t*>(nullptr));
+               static_cast<const int64_t*>(nullptr), sj);
     } else {
         Offsets off{nullptr, nullptr, 1, m};
         const int64_t blocks = clamp_grid((m / 16 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_gen);
@@ -465,7 +472,7 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
         const int64_t blocks = balanced_blocks(m / 1024, int64_t(di->sms) * cap_bps(di->occ_dec_fast[1]));
         launch(dec_fast_kernel<1>, blocks, kThreads, s, static_cast<const uint8_t*>(comp), m, d_out, dec_tab(a),
                int64_t(0), 1, reinterpret_cast<unsigned long long*>(d_err_off), static_cast<int64_t*>(nullptr),
-               static_cast<const int64_t*>(mc));
+               static_cast<const int64_t*>(mc), StreamJoin{});
     }
     launch(ws_finalize_kernel, 1, 32, s, d_err_off, d_status, d_out_len, static_cast<const int64_t*>(mc), d_in, m,
            static_cast<const uint8_t*>(comp), wt, uint32_t(a->pad), L.K, int(L.ncta),

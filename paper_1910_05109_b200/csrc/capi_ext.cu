@@ -87,14 +87,21 @@ int b64_decode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t m, uin
     if (m == 0) return B64_OK;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int join = (H > 0 && Q > 0) ? 1 : 0;
-    launch(dec_stream_join_kernel, 1, 1, s, st->d_carry, int(H), d_in, m, d_out, dec_tab(a), st->consumed - H,
-           reinterpret_cast<unsigned long long*>(st->d_err_min));
-    int r = launched();
-    if (r != B64_OK) return r;
     const int64_t skip = join ? 4 - H : 0, qb = Q - join;  // whole quads read straight from the piece
+    // the join (held chars + the piece's head, and the new carry) rides along with the piece's
+    // bulk kernel when that is the fast one; otherwise it is a one-thread kernel of its own
+    const StreamJoin sj = {st->d_carry, d_in, d_out, m, st->consumed - H, int32_t(H), 1};
+    bool joined = false;
+    int r = B64_OK;
     if (qb > 0) {
-        r = b64_decode_chunk(d_in + skip, 4 * qb, d_out + 3 * join, a, st->consumed + skip, 0, st->d_err_min,
-                             nullptr, stream);
+        r = decode_launch(d_in + skip, 4 * qb, d_out + 3 * join, a, st->consumed + skip, 0, st->d_err_min, nullptr,
+                          s, &sj, &joined);
+        if (r != B64_OK) return r;
+    }
+    if (!joined) {
+        launch(dec_stream_join_kernel, 1, 1, s, st->d_carry, int(H), d_in, m, d_out, dec_tab(a), st->consumed - H,
+               reinterpret_cast<unsigned long long*>(st->d_err_min));
+        r = launched();
         if (r != B64_OK) return r;
     }
     st->held = int32_t(A - 4 * Q);

@@ -126,11 +126,33 @@ struct DecBulk {
     }
 };
 
+// The join of a streaming decode (stream.cu, R15), one thread: the held chars
+// + the piece's head -> one quad, and the piece's last R chars -> the carry.
+__device__ __forceinline__ void stream_join(uint8_t* carry, int H, const uint8_t* in, int64_t m, uint8_t* out,
+                                            const uint8_t* lut, int64_t base, unsigned long long* cell) {
+    uint8_t c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = carry[k];
+    auto at = [&](int64_t i) -> uint32_t { return i < H ? c[i] : in[i - H]; };
+    const int64_t A = H + m;
+    if (A == 0) return;
+    const int64_t Q = (A - 1) / 4;
+    const int R = int(A - 4 * Q);
+    if (H > 0 && Q >= 1) {
+        const uint32_t x = at(0) | (at(1) << 8) | (at(2) << 16) | (at(3) << 24);
+        uint32_t err = 0;
+        const uint32_t v = dec_quad(x, lut, err);
+        store_bytes(out, v, 3);
+        if (err & kInvalid) atomicMin(cell, pack_err(base + first_bad_in_quad(x, lut), kBadChar));
+    }
+    for (int k = 0; k < R; ++k) carry[k] = uint8_t(at(A - R + k));
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads)
 dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
-                int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev) {
+                int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev, StreamJoin join) {
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];  // per-warp output staging
     griddep_launch_dependents();
@@ -235,6 +257,7 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
         } else if (out_len) {
             *out_len = 3 * Q;
         }
+        if (join.active) stream_join(join.carry, join.H, join.in, join.m, join.out, lut, join.base, err_cell);
     }
 }
 

@@ -61,23 +61,7 @@ __global__ void dec_stream_join_kernel(uint8_t* __restrict__ carry, int H, const
                                        uint8_t* __restrict__ out, DecTab tab, int64_t base,
                                        unsigned long long* __restrict__ cell) {
     griddep_wait();
-    const uint8_t* lut = reinterpret_cast<const uint8_t*>(tab.w);
-    uint8_t c[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) c[k] = carry[k];
-    auto at = [&](int64_t i) -> uint32_t { return i < H ? c[i] : in[i - H]; };
-    const int64_t A = H + m;
-    if (A == 0) return;
-    const int64_t Q = (A - 1) / 4;
-    const int R = int(A - 4 * Q);
-    if (H > 0 && Q >= 1) {
-        const uint32_t x = at(0) | (at(1) << 8) | (at(2) << 16) | (at(3) << 24);
-        uint32_t err = 0;
-        const uint32_t v = dec_quad(x, lut, err);
-        store_bytes(out, v, 3);
-        if (err & kInvalid) atomicMin(cell, pack_err(base + first_bad_in_quad(x, lut), kBadChar));
-    }
-    for (int k = 0; k < R; ++k) carry[k] = uint8_t(at(A - R + k));
+    stream_join(carry, H, in, m, out, reinterpret_cast<const uint8_t*>(tab.w), base, cell);
 }
 
 // The end of a decode stream of `total` chars: carry[0..H) holds its last
