@@ -502,7 +502,7 @@ def run_ours(args):
                    "error_combine": ("none (N=1)" if world == 1 else
                                      "peer memory, inside the codec kernel" if args.step == "fused_peer" else
                                      "peer memory, 1 kernel" if args.combine == "peer" else
-                                     "NCCL all_reduce(MIN), overlapped with the encode launch"),
+                                     f"{args.dist_backend.upper()} all_reduce(MIN), overlapped with the encode launch"),
                    "volume": "base64 bytes (encode output + decode input), GB=1e9"},
         "encode_gbs": round(enc_gbs, 1), "decode_gbs": round(dec_gbs, 1),
         "memcpy_d2d_gbs": round(memcpy_gbs, 1), "memcpy_d2d_6cases_gbs": round(memcpy6_gbs, 1),
