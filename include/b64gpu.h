@@ -19,11 +19,17 @@
  *    negative B64_E* code).  Data errors (invalid base64) are asynchronous and
  *    are written to device memory (err_off / status).
  *  - Input bytes are only read and output bytes only written inside the
- *    ranges stated per call, except that the generic (unaligned / batched)
- *    kernels may read the naturally aligned 8-byte words that contain input
- *    bytes (at most 7 bytes before the first / after the last input byte,
- *    never crossing into another 8-byte-aligned word; CUDA allocations are
- *    at least 256-byte granular, so such reads stay inside the allocation).
+ *    ranges stated per call, with one exception: the generic (unaligned /
+ *    batched) kernels may read whole naturally aligned 16-byte blocks that
+ *    contain input bytes -- at most 15 bytes before the first and after the
+ *    last input byte, never a block that holds no input byte.  A block that
+ *    holds an input byte lies in the same 256-byte-aligned region as that
+ *    byte, and cudaMalloc (and the torch caching allocator) hands out whole
+ *    256-byte-aligned regions, so such reads stay inside the allocation; a
+ *    caller passing a sub-allocation must keep the 16-byte blocks that
+ *    contain its bytes readable (compute-sanitizer memcheck log:
+ *    profiles/sanitizer_r2.txt).  The values read there never affect a
+ *    result.
  *  - Inputs and outputs must not overlap.
  */
 #ifndef B64GPU_H
@@ -58,7 +64,14 @@ enum {
     B64_ST_LENGTH = 4    /* batched string with len % 4 != 0                        */
 };
 
-/* Packed error word used by the chunk API and the multi-GPU MIN reduction:
+/* Packed error word used by the chunk API and the multi-GPU MIN reduction
+ * (a deliberate deviation from SURVEY.md Sec. 8(b), whose d_err_min is a plain
+ * offset with INT64_MAX = none; R8): the word carries the status kind
+ * with the position, so the one all_reduce(MIN) that combines the ranks also
+ * yields the kind -- the order of packed words is the order of positions.
+ * b64_decode_finalize(_n) maps a word to the plain form (-1 or the offset,
+ * plus the kind); tests/test_abi.py pins the packing and its MIN order. */
+/* Packed error word layout:
  * (global_position << 3) | status.  Positions are unique, so the MIN over
  * packed words is the first error together with its kind.  B64_ERR_NONE
  * means "no error" (R8); it is the byte 0x7F repeated, so a
@@ -110,6 +123,9 @@ const b64_alphabet *b64_alphabet_url(void);      /* PAPER.md:93  */
 /* ---- sizes ----------------------------------------------------------------- */
 int64_t b64_encoded_len(int64_t n);     /* 4*ceil(n/3); -1 if n < 0 */
 int64_t b64_decoded_len_max(int64_t m); /* 3*(m/4): capacity a decode output needs   */
+/* Capacity b64_decode_unpadded needs: 3*(m/4) plus 1 / 2 bytes for a 2 / 3-char
+ * tail (R13); -1 if m < 0 or m % 4 == 1. */
+int64_t b64_decoded_len_max_unpadded(int64_t m);
 
 /* ---- single stream --------------------------------------------------------- */
 /* Encode n bytes d_in[0..n) to exactly b64_encoded_len(n) chars at d_out, with
@@ -139,7 +155,7 @@ int b64_decode_ex(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alph
  * synchronously; m % 4 in {2, 3}: all full quads must be alphabet chars and
  * the trailing 2 / 3 chars decode to 1 / 2 bytes with zero dropped bits
  * (B64_ST_NONCANON at m - 1 otherwise).  Outputs as b64_decode_ex; d_out
- * capacity >= 3*(m/4) + 2. */
+ * capacity >= b64_decoded_len_max_unpadded(m). */
 int b64_decode_unpadded(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a,
                         int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len, b64_stream_t stream);
 
@@ -171,6 +187,24 @@ int b64_decode_ws(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alph
 int b64_decode_chunk(const uint8_t *d_in, int64_t m, uint8_t *d_out, const b64_alphabet *a,
                      int64_t base_offset, int is_final_chunk, int64_t *d_err_min,
                      int64_t *d_out_len, b64_stream_t stream);
+
+/* Multi-GPU sharding rule, host
+ * only: rank's part of a world-way split of an n-byte encode / m-char decode
+ * (m % 4 == 0), cut at multiples of 768 bytes / 1024 chars (one warp-chunk, so
+ * every shard keeps the aligned fast path); the last rank also owns the tail
+ * (encode: the n mod 3 bytes and the '=' padding; decode: the final quad).
+ *   start, stop : the shard's input range
+ *   out_start   : where its output begins in the whole stream's output
+ *   out_len     : its output length (encode chars; decode capacity 3*len/4)
+ *   is_final    : 1 for the rank that owns the tail (pass it to b64_decode_chunk)
+ * B64_EINVAL for world < 1, rank outside [0, world), n/m < 0; B64_ELENGTH for
+ * m % 4 != 0. */
+typedef struct b64_shard {
+    int64_t start, stop, out_start, out_len;
+    int32_t is_final, reserved;
+} b64_shard;
+int b64_encode_shard(int64_t n, int world, int rank, b64_shard *sh);
+int b64_decode_shard(int64_t m, int world, int rank, b64_shard *sh);
 
 /* Map a packed error word (after any cross-rank MIN) to the API form:
  * *d_err_off = -1 or position, *d_status (nullable) = kind.  One tiny kernel. */
@@ -275,6 +309,14 @@ typedef struct b64_stream {
     int64_t *d_err_min; /* decode: device packed error word of the stream         */
 } b64_stream;
 
+/* Output sizes, host-side (no device access): b64_stream_update_len = the
+ * chars (encode: 4*floor((held + len)/3)) / bytes (decode: 3*floor((held +
+ * len - 1)/4)) the next update with a piece of `len` writes; b64_stream_end_len
+ * = the capacity the end call needs (encode 4 or 0, decode 3 or 0).  -1 for a
+ * finished stream or len < 0. */
+int64_t b64_stream_update_len(const b64_stream *st, int64_t len);
+int64_t b64_stream_end_len(const b64_stream *st);
+
 int b64_encode_stream_begin(b64_stream *st, uint8_t *d_carry);
 /* Encode piece d_in[0..n): writes *n_out = 4*floor((held + n)/3) chars at d_out
  * (capacity >= that; *n_out is known on return, host-side). */
@@ -353,15 +395,16 @@ int b64_peer_combine_emulate(uint8_t *const *d_bufs, int world, const int64_t *d
  * (decode with the same workspace uses chunks of ~4c/3 chars).
  * Encode writes b64_encoded_len(n) chars to h_out.  Decode writes up to 3*m/4
  * bytes to h_out and, on s_comp, *d_err_off (device) = -1 or the first invalid
- * position and *d_status (nullable, device) = its kind; the exact output
- * length is 3*m/4 - (number of '=' at m-2, m-1) when valid, 3*floor(err/4)
- * otherwise (same rules as b64_decode_ex). */
+ * position, *d_status (nullable, device) = its kind and *d_out_len (nullable,
+ * device) = the exact output length: 3*m/4 - (number of '=' at m-2, m-1) when
+ * valid, 3*floor(err/4) otherwise (same rules as b64_decode_ex), computed on
+ * the device from the final chunk. */
 int64_t b64_host_workspace_bytes(int64_t chunk_bytes);
 int b64_encode_host(const uint8_t *h_in, int64_t n, uint8_t *h_out, const b64_alphabet *a, uint8_t *d_ws,
                     int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h);
 int b64_decode_host(const uint8_t *h_in, int64_t m, uint8_t *h_out, const b64_alphabet *a, uint8_t *d_ws,
-                    int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, b64_stream_t s_h2d,
-                    b64_stream_t s_comp, b64_stream_t s_d2h);
+                    int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len,
+                    b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h);
 /* The same with flags.  B64_HOST_CALLER_ORDERED: the caller guarantees that
  * no earlier work still uses d_ws (e.g. it alternates two workspaces and makes
  * s_h2d wait for the end of the call before last that used this one), so the
@@ -373,8 +416,8 @@ int b64_encode_host_ex(const uint8_t *h_in, int64_t n, uint8_t *h_out, const b64
                        int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h,
                        unsigned flags);
 int b64_decode_host_ex(const uint8_t *h_in, int64_t m, uint8_t *h_out, const b64_alphabet *a, uint8_t *d_ws,
-                       int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, b64_stream_t s_h2d,
-                       b64_stream_t s_comp, b64_stream_t s_d2h, unsigned flags);
+                       int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len,
+                       b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h, unsigned flags);
 
 /* ---- batched (BASELINE.json configs[3]) ------------------------------------ */
 /* (d_in / d_out must be valid device pointers when count > 0, even if every
@@ -386,6 +429,15 @@ int b64_decode_host_ex(const uint8_t *h_in, int64_t m, uint8_t *h_out, const b64
  * d_out + d_out_off[i] (device int64[count], caller-computed):
  *   encode: d_out_off = exclusive scan of 4*ceil(len_i/3); each string padded.
  *   decode: d_out_off = exclusive scan of 3*(len_i/4).                        */
+/* The output offsets the batch calls expect, computed on `stream` from the
+ * device offsets d_in_off[count+1] (no host access): d_out_off[count+1]
+ * (device) = exclusive scan of 4*ceil(len_i/3) (encode) or of
+ * 3*floor(len_i/4) (decode capacity), d_out_off[0] = 0 and d_out_off[count] =
+ * the total output.  Three small kernels (a tile-sum / tile-scan / fill scan
+ * that uses d_out_off itself as its scratch; no workspace). */
+int b64_encode_batch_offsets(const int64_t *d_in_off, int64_t count, int64_t *d_out_off, b64_stream_t stream);
+int b64_decode_batch_offsets(const int64_t *d_in_off, int64_t count, int64_t *d_out_off, b64_stream_t stream);
+
 int b64_encode_batch(const uint8_t *d_in, const int64_t *d_in_off, int64_t count,
                      uint8_t *d_out, const int64_t *d_out_off, const b64_alphabet *a,
                      b64_stream_t stream);

@@ -37,6 +37,7 @@ P, I64, I32, INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
 
 
 ALPHA_LENIENT = 1  # B64_ALPHA_LENIENT
+DECODE_CTX_BYTES = 16  # B64_DECODE_CTX_BYTES
 HOST_CALLER_ORDERED = 1  # B64_HOST_CALLER_ORDERED
 
 
@@ -63,6 +64,12 @@ class Stream(ctypes.Structure):
                 ("state", ctypes.c_int32), ("d_carry", ctypes.c_void_p), ("d_err_min", ctypes.c_void_p)]
 
 
+class Shard(ctypes.Structure):
+    """b64_shard (multi-GPU sharding rule, host only)."""
+    _fields_ = [("start", ctypes.c_int64), ("stop", ctypes.c_int64), ("out_start", ctypes.c_int64),
+                ("out_len", ctypes.c_int64), ("is_final", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
 SP = ctypes.POINTER(Stream)
 I64P = ctypes.POINTER(ctypes.c_int64)
 
@@ -73,6 +80,7 @@ SIGNATURES = [
     ("b64_alphabet_url", AP, []),
     ("b64_encoded_len", I64, [I64]),
     ("b64_decoded_len_max", I64, [I64]),
+    ("b64_decoded_len_max_unpadded", I64, [I64]),
     ("b64_encode", INT, [P, I64, P, AP, P]),
     ("b64_decode", INT, [P, I64, P, AP, P, P]),
     ("b64_decode_ex", INT, [P, I64, P, AP, P, P, P, P]),
@@ -81,12 +89,16 @@ SIGNATURES = [
     ("b64_decode_ws", INT, [P, I64, P, AP, P, I64, P, P, P, P]),
     ("b64_decode_chunk", INT, [P, I64, P, AP, I64, INT, P, P, P]),
     ("b64_decode_finalize", INT, [P, P, P, P]),
+    ("b64_encode_shard", INT, [I64, INT, INT, ctypes.POINTER(Shard)]),
+    ("b64_decode_shard", INT, [I64, INT, INT, ctypes.POINTER(Shard)]),
     ("b64_encode_group", INT, [P, I64, P]),
     ("b64_decode_group", INT, [P, I64, P]),
     ("b64_codec_group", INT, [P, I64, P, I64, P]),
     ("b64_codec_group_fused", INT, [P, I64, P, I64, P, P, P, P]),
     ("b64_codec_group_fused_peer", INT, [P, I64, P, I64, P, P, P, P, INT, INT, ctypes.c_uint64, P]),
     ("b64_decode_finalize_n", INT, [P, I64, P, P, P]),
+    ("b64_stream_update_len", I64, [SP, I64]),
+    ("b64_stream_end_len", I64, [SP]),
     ("b64_encode_stream_begin", INT, [SP, P]),
     ("b64_encode_stream_update", INT, [SP, P, I64, P, AP, I64P, P]),
     ("b64_encode_stream_end", INT, [SP, P, AP, I64P, P]),
@@ -102,9 +114,11 @@ SIGNATURES = [
     ("b64_peer_combine_emulate", INT, [P, INT, P, I64, INT, P, P, P]),
     ("b64_host_workspace_bytes", I64, [I64]),
     ("b64_encode_host", INT, [P, I64, P, AP, P, I64, P, P, P]),
-    ("b64_decode_host", INT, [P, I64, P, AP, P, I64, P, P, P, P, P]),
+    ("b64_decode_host", INT, [P, I64, P, AP, P, I64, P, P, P, P, P, P]),
     ("b64_encode_host_ex", INT, [P, I64, P, AP, P, I64, P, P, P, ctypes.c_uint]),
-    ("b64_decode_host_ex", INT, [P, I64, P, AP, P, I64, P, P, P, P, P, ctypes.c_uint]),
+    ("b64_decode_host_ex", INT, [P, I64, P, AP, P, I64, P, P, P, P, P, P, ctypes.c_uint]),
+    ("b64_encode_batch_offsets", INT, [P, I64, P, P]),
+    ("b64_decode_batch_offsets", INT, [P, I64, P, P]),
     ("b64_encode_batch", INT, [P, P, I64, P, P, AP, P]),
     ("b64_decode_batch", INT, [P, P, I64, P, P, AP, P, P, P, P]),
     ("b64_decode_batch_ex", INT, [P, P, I64, P, P, AP, P, P, P, I64, P, P]),

@@ -366,6 +366,8 @@ __global__ void dec_finalize_unpadded_kernel(int64_t* err_off, int32_t* status, 
                                              const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out,
                                              DecTab tab);
 __global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off, int32_t* status);
+__global__ void dec_finalize_len_kernel(const int64_t* cell, int64_t* err_off, int32_t* status, int64_t* out_len,
+                                        int64_t out_base);
 __global__ void dec_batch_init_kernel(int64_t* err, int64_t count);
 __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
                                           int64_t count, uint32_t pad, int32_t* status, int64_t* err,

@@ -7,5 +7,6 @@
 #include "small.cu"
 #include "mime.cu"
 #include "stream.cu"
+#include "offsets.cu"
 #include "capi.cu"
 #include "capi_ext.cu"

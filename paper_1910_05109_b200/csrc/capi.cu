@@ -96,9 +96,23 @@ DecTab dec_tab(const b64_alphabet* a) {
     return t;
 }
 
+// The first launch / runtime error since the last launched() of this thread: every launch
+// records the return value of cudaLaunchKernelEx here, and launched() reports it (no
+// cudaPeekAtLastError, which would pick up errors of unrelated earlier runtime calls).
+thread_local cudaError_t t_launch_err = cudaSuccess;
+inline void note(cudaError_t e) {
+    if (e != cudaSuccess && t_launch_err == cudaSuccess) t_launch_err = e;
+}
+
 int launched() {
+    const cudaError_t e = t_launch_err;
+    t_launch_err = cudaSuccess;
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // clear the non-sticky error the failed call left behind
+        return B64_ECUDA;
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    return cudaPeekAtLastError() == cudaSuccess ? B64_OK : (cudaGetLastError(), B64_ECUDA);
+    return B64_OK;
 }
 
 // Launch with programmatic dependent launch allowed (the kernels call
@@ -125,7 +139,7 @@ void launch(void (*kernel)(KArgs...), int64_t grid, int block, cudaStream_t s, A
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+    note(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 
 // Prefetch depth of the register-direct bulk loops (chunks in flight per warp
@@ -216,6 +230,31 @@ int alpha_ok(const b64_alphabet* a) { return a != nullptr; }
 
 }  // namespace
 
+namespace {
+template <int LAW>
+int batch_offsets(const int64_t* d_in_off, int64_t count, int64_t* d_out_off, b64_stream_t stream) {
+    if (count < 0 || !d_out_off || (count > 0 && !d_in_off)) return B64_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (count == 0) {
+        note(cudaMemsetAsync(d_out_off, 0, sizeof(int64_t), s));
+        const int r = launched();
+        if (r == B64_OK) g_launches.fetch_sub(1, std::memory_order_relaxed);  // a memset, not a kernel
+        return r;
+    }
+    const DevInfo* di = dev_info();
+    if (!di) return B64_ECUDA;
+    const int64_t ntile = (count + kScanTile - 1) / kScanTile;
+    const int64_t grid = clamp_grid(ntile, int64_t(di->sms) * 8);
+    launch(off_tile_sum_kernel<LAW>, grid, kThreads, s, d_in_off, count, d_out_off);
+    int r = launched();
+    if (r != B64_OK) return r;
+    launch(off_tile_scan_kernel, 1, 1024, s, d_out_off, count);
+    if ((r = launched()) != B64_OK) return r;
+    launch(off_fill_kernel<LAW>, grid, kThreads, s, d_in_off, count, d_out_off);
+    return launched();
+}
+}  // namespace
+
 extern "C" {
 
 int b64_alphabet_init(b64_alphabet* a, const char chars[64], char pad, int* bad_index) {
@@ -264,6 +303,19 @@ const b64_alphabet* b64_alphabet_url(void) {
 
 int64_t b64_encoded_len(int64_t n) { return n < 0 ? -1 : 4 * ((n + 2) / 3); }
 int64_t b64_decoded_len_max(int64_t m) { return m < 0 ? -1 : 3 * (m / 4); }
+int64_t b64_decoded_len_max_unpadded(int64_t m) {
+    if (m < 0 || m % 4 == 1) return -1;
+    return 3 * (m / 4) + (m % 4 ? m % 4 - 1 : 0);  // a 2 / 3-char tail -> 1 / 2 bytes (R13)
+}
+
+// ---------------------------------------------------------------- batch output offsets (offsets.cu)
+
+int b64_encode_batch_offsets(const int64_t* d_in_off, int64_t count, int64_t* d_out_off, b64_stream_t stream) {
+    return batch_offsets<0>(d_in_off, count, d_out_off, stream);
+}
+int b64_decode_batch_offsets(const int64_t* d_in_off, int64_t count, int64_t* d_out_off, b64_stream_t stream) {
+    return batch_offsets<1>(d_in_off, count, d_out_off, stream);
+}
 
 int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabet* a, b64_stream_t stream) {
     if (n < 0 || !alpha_ok(a)) return B64_EINVAL;
@@ -344,7 +396,7 @@ int b64_decode_ex(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
             cfg.attrs = attr;
             cfg.numAttrs = pdl_enabled() ? 2 : 1;
         }
-        cudaLaunchKernelEx(&cfg, dec_small_kernel, d_in, m, d_out, dec_tab(a), d_err_off, d_status, d_out_len);
+        note(cudaLaunchKernelEx(&cfg, dec_small_kernel, d_in, m, d_out, dec_tab(a), d_err_off, d_status, d_out_len));
         return launched();
     }
     if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), s) != cudaSuccess) return B64_ECUDA;
@@ -432,10 +484,9 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl_enabled() ? 2 : 1;
-        if (cudaLaunchKernelEx(&cfg, ws_small_kernel, d_in, m, wt, uint32_t(a->pad),
-                               uint32_t((a->flags & B64_ALPHA_LENIENT) ? 1 : 0), comp, d_out, d_err_off, d_status,
-                               d_out_len) != cudaSuccess)
-            return (cudaGetLastError(), B64_ECUDA);
+        note(cudaLaunchKernelEx(&cfg, ws_small_kernel, d_in, m, wt, uint32_t(a->pad),
+                                uint32_t((a->flags & B64_ALPHA_LENIENT) ? 1 : 0), comp, d_out, d_err_off, d_status,
+                                d_out_len));
         return launched();
     }
     if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), s) != cudaSuccess) return B64_ECUDA;
@@ -498,6 +549,33 @@ int b64_decode_chunk(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_a
         return B64_OK;
     }
     return decode_launch(d_in, m, d_out, a, base_offset, is_final_chunk ? 1 : 0, d_err_min, d_out_len, s);
+}
+
+int b64_encode_shard(int64_t n, int world, int rank, b64_shard* sh) {
+    if (n < 0 || world < 1 || rank < 0 || rank >= world || !sh) return B64_EINVAL;
+    const int64_t units = n / 768, u0 = units * rank / world, u1 = units * (rank + 1) / world;
+    const bool last = rank == world - 1;
+    sh->start = 768 * u0;
+    sh->stop = last ? n : 768 * u1;
+    sh->out_start = 4 * (sh->start / 3);
+    sh->out_len = last ? b64_encoded_len(sh->stop - sh->start) : 4 * ((sh->stop - sh->start) / 3);
+    sh->is_final = last ? 1 : 0;
+    sh->reserved = 0;
+    return B64_OK;
+}
+
+int b64_decode_shard(int64_t m, int world, int rank, b64_shard* sh) {
+    if (m < 0 || world < 1 || rank < 0 || rank >= world || !sh) return B64_EINVAL;
+    if (m % 4) return B64_ELENGTH;
+    const int64_t units = m / 1024, u0 = units * rank / world, u1 = units * (rank + 1) / world;
+    const bool last = rank == world - 1;
+    sh->start = 1024 * u0;
+    sh->stop = last ? m : 1024 * u1;
+    sh->out_start = 3 * (sh->start / 4);
+    sh->out_len = b64_decoded_len_max(sh->stop - sh->start);
+    sh->is_final = last ? 1 : 0;
+    sh->reserved = 0;
+    return B64_OK;
 }
 
 int b64_decode_finalize(const int64_t* d_err_min, int64_t* d_err_off, int32_t* d_status, b64_stream_t stream) {

@@ -12,6 +12,21 @@ namespace {
 enum { kStIdle = 0, kStEncode = 1, kStDecode = 2, kStDone = 3 };
 }
 
+int64_t b64_stream_update_len(const b64_stream* st, int64_t len) {
+    if (!st || len < 0) return -1;
+    const int64_t A = st->held + len;
+    if (st->state == kStEncode) return 4 * (A / 3);                 // whole triples
+    if (st->state == kStDecode) return A > 0 ? 3 * ((A - 1) / 4) : 0;  // the last 1..4 chars are held
+    return -1;
+}
+
+int64_t b64_stream_end_len(const b64_stream* st) {
+    if (!st) return -1;
+    if (st->state == kStEncode) return st->held > 0 ? 4 : 0;  // the padded tail
+    if (st->state == kStDecode) return (st->consumed > 0 && st->consumed % 4 == 0) ? 3 : 0;
+    return -1;
+}
+
 int b64_encode_stream_begin(b64_stream* st, uint8_t* d_carry) {
     if (!st || !d_carry) return B64_EINVAL;
     st->consumed = st->produced = 0;
@@ -148,10 +163,9 @@ int b64_peer_combine(uint8_t* const* d_bufs, int world, int rank, const int64_t*
     cfg.blockDim = dim3(32);
     cfg.dynamicSmemBytes = size_t(count) * 8;
     cfg.stream = reinterpret_cast<cudaStream_t>(stream);
-    if (cudaLaunchKernelEx(&cfg, peer_combine_kernel, d_bufs, world, rank,
-                           reinterpret_cast<const unsigned long long*>(d_local), count,
-                           static_cast<unsigned long long>(epoch), d_err_off, d_status) != cudaSuccess)
-        return (cudaGetLastError(), B64_ECUDA);
+    note(cudaLaunchKernelEx(&cfg, peer_combine_kernel, d_bufs, world, rank,
+                            reinterpret_cast<const unsigned long long*>(d_local), count,
+                            static_cast<unsigned long long>(epoch), d_err_off, d_status));
     return launched();
 }
 
@@ -200,9 +214,8 @@ int b64_peer_combine_emulate(uint8_t* const* d_bufs, int world, const int64_t* d
     int* okp = d_ok;
     void* args[] = {&b, &w, &l, &k, &e, &o, &okp};
     // all `world` blocks wait on one another: a cooperative launch guarantees they are co-resident
-    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(peer_combine_emulate_kernel), dim3(world), dim3(32),
-                                    args, 0, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
-        return (cudaGetLastError(), B64_ECUDA);
+    note(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(peer_combine_emulate_kernel), dim3(world), dim3(32),
+                                     args, 0, reinterpret_cast<cudaStream_t>(stream)));
     return launched();
 }
 
@@ -256,6 +269,15 @@ int b64_encode_host(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_al
     return b64_encode_host_ex(h_in, n, h_out, a, d_ws, ws_bytes, s_h2d, s_comp, s_d2h, 0u);
 }
 
+// One chunk's hand-over between the three streams: every runtime call checked.
+#define B64_CK(call)                                  \
+    do {                                              \
+        if ((call) != cudaSuccess) {                  \
+            cudaGetLastError();                       \
+            return B64_ECUDA;                         \
+        }                                             \
+    } while (0)
+
 int b64_encode_host_ex(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
                        int64_t ws_bytes, b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h,
                        unsigned flags) {
@@ -271,7 +293,7 @@ int b64_encode_host_ex(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64
                  sd = reinterpret_cast<cudaStream_t>(s_d2h);
     HostPipe pipe;
     if (!pipe.ok) return B64_ECUDA;
-    if (!(flags & B64_HOST_CALLER_ORDERED) && pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
+    if (!(flags & B64_HOST_CALLER_ORDERED)) B64_CK(pipe.order_after_previous(sh, sc, sd));
     const int64_t stride = C + C / 3 * 4 + 512;
     int64_t j = 0;
     for (int64_t off = 0; off < n; off += C, ++j) {
@@ -280,40 +302,40 @@ int b64_encode_host_ex(const uint8_t* h_in, int64_t n, uint8_t* h_out, const b64
         uint8_t* dout = din + C + 256;
         const int64_t len = (n - off < C) ? n - off : C;
         const int64_t olen = b64_encoded_len(len);
-        if (j >= kHostBufs && cudaStreamWaitEvent(sh, pipe.d2h[b], 0) != cudaSuccess) return B64_ECUDA;
-        if (cudaMemcpyAsync(din, h_in + off, size_t(len), cudaMemcpyHostToDevice, sh) != cudaSuccess) return B64_ECUDA;
-        cudaEventRecord(pipe.h2d[b], sh);
-        cudaStreamWaitEvent(sc, pipe.h2d[b], 0);
+        if (j >= kHostBufs) B64_CK(cudaStreamWaitEvent(sh, pipe.d2h[b], 0));
+        B64_CK(cudaMemcpyAsync(din, h_in + off, size_t(len), cudaMemcpyHostToDevice, sh));
+        B64_CK(cudaEventRecord(pipe.h2d[b], sh));
+        B64_CK(cudaStreamWaitEvent(sc, pipe.h2d[b], 0));
         const int r = b64_encode(din, len, dout, a, s_comp);
         if (r != B64_OK) return r;
-        cudaEventRecord(pipe.comp[b], sc);
-        cudaStreamWaitEvent(sd, pipe.comp[b], 0);
-        if (cudaMemcpyAsync(h_out + off / 3 * 4, dout, size_t(olen), cudaMemcpyDeviceToHost, sd) != cudaSuccess)
-            return B64_ECUDA;
-        cudaEventRecord(pipe.d2h[b], sd);
+        B64_CK(cudaEventRecord(pipe.comp[b], sc));
+        B64_CK(cudaStreamWaitEvent(sd, pipe.comp[b], 0));
+        B64_CK(cudaMemcpyAsync(h_out + off / 3 * 4, dout, size_t(olen), cudaMemcpyDeviceToHost, sd));
+        B64_CK(cudaEventRecord(pipe.d2h[b], sd));
     }
-    return cudaPeekAtLastError() == cudaSuccess ? B64_OK : (cudaGetLastError(), B64_ECUDA);
+    return B64_OK;
 }
 
 int b64_decode_host(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
-                    int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, b64_stream_t s_h2d,
+                    int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, int64_t* d_out_len, b64_stream_t s_h2d,
                     b64_stream_t s_comp, b64_stream_t s_d2h) {
-    return b64_decode_host_ex(h_in, m, h_out, a, d_ws, ws_bytes, d_err_off, d_status, s_h2d, s_comp, s_d2h, 0u);
+    return b64_decode_host_ex(h_in, m, h_out, a, d_ws, ws_bytes, d_err_off, d_status, d_out_len, s_h2d, s_comp, s_d2h,
+                              0u);
 }
 
 int b64_decode_host_ex(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64_alphabet* a, uint8_t* d_ws,
-                       int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, b64_stream_t s_h2d,
-                       b64_stream_t s_comp, b64_stream_t s_d2h, unsigned flags) {
+                       int64_t ws_bytes, int64_t* d_err_off, int32_t* d_status, int64_t* d_out_len,
+                       b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h, unsigned flags) {
     if (m < 0 || !alpha_ok(a) || !d_err_off || (flags & ~unsigned(B64_HOST_CALLER_ORDERED))) return B64_EINVAL;
     if (m % 4) return B64_ELENGTH;
     if (m > 0 && (!h_in || !h_out || !d_ws)) return B64_EINVAL;
     cudaStream_t sh = reinterpret_cast<cudaStream_t>(s_h2d), sc = reinterpret_cast<cudaStream_t>(s_comp),
                  sd = reinterpret_cast<cudaStream_t>(s_d2h);
+    B64_CK(cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), sc));
     if (m == 0) {
-        if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), sc) != cudaSuccess) return B64_ECUDA;
+        if (d_out_len) B64_CK(cudaMemsetAsync(d_out_len, 0, sizeof(int64_t), sc));
         return b64_decode_finalize(d_err_off, d_err_off, d_status, s_comp);
     }
-    if (!d_ws) return B64_EINVAL;
     // per buffer: C chars + 3C/4 bytes; C a multiple of 4096 (= 4 * 1024)
     const int64_t per = (ws_bytes - 256) / kHostBufs - 512;
     const int64_t C = align_down(per * 4 / 7, 4096);
@@ -321,29 +343,35 @@ int b64_decode_host_ex(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
     HostPipe pipe;
     if (!pipe.ok) return B64_ECUDA;
-    if (!(flags & B64_HOST_CALLER_ORDERED) && pipe.order_after_previous(sh, sc, sd) != cudaSuccess) return B64_ECUDA;
-    if (cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), sc) != cudaSuccess) return B64_ECUDA;
+    if (!(flags & B64_HOST_CALLER_ORDERED)) B64_CK(pipe.order_after_previous(sh, sc, sd));
     const int64_t stride = C + C / 4 * 3 + 512;
-    int64_t j = 0;
+    int64_t j = 0, last_off = 0;
     for (int64_t off = 0; off < m; off += C, ++j) {
         const int b = int(j % kHostBufs);
         uint8_t* din = base + b * stride;
         uint8_t* dout = din + C + 256;
         const int64_t len = (m - off < C) ? m - off : C;
         const bool fin = off + len == m;
-        if (j >= kHostBufs && cudaStreamWaitEvent(sh, pipe.d2h[b], 0) != cudaSuccess) return B64_ECUDA;
-        if (cudaMemcpyAsync(din, h_in + off, size_t(len), cudaMemcpyHostToDevice, sh) != cudaSuccess) return B64_ECUDA;
-        cudaEventRecord(pipe.h2d[b], sh);
-        cudaStreamWaitEvent(sc, pipe.h2d[b], 0);
-        const int r = b64_decode_chunk(din, len, dout, a, off, fin ? 1 : 0, d_err_off, nullptr, s_comp);
+        if (j >= kHostBufs) B64_CK(cudaStreamWaitEvent(sh, pipe.d2h[b], 0));
+        B64_CK(cudaMemcpyAsync(din, h_in + off, size_t(len), cudaMemcpyHostToDevice, sh));
+        B64_CK(cudaEventRecord(pipe.h2d[b], sh));
+        B64_CK(cudaStreamWaitEvent(sc, pipe.h2d[b], 0));
+        // the final chunk also reports its valid-text length (pads subtracted, on the device)
+        const int r = b64_decode_chunk(din, len, dout, a, off, fin ? 1 : 0, d_err_off, fin ? d_out_len : nullptr,
+                                       s_comp);
         if (r != B64_OK) return r;
-        cudaEventRecord(pipe.comp[b], sc);
-        cudaStreamWaitEvent(sd, pipe.comp[b], 0);
-        if (cudaMemcpyAsync(h_out + off / 4 * 3, dout, size_t(len / 4 * 3), cudaMemcpyDeviceToHost, sd) != cudaSuccess)
-            return B64_ECUDA;
-        cudaEventRecord(pipe.d2h[b], sd);
+        B64_CK(cudaEventRecord(pipe.comp[b], sc));
+        B64_CK(cudaStreamWaitEvent(sd, pipe.comp[b], 0));
+        B64_CK(cudaMemcpyAsync(h_out + off / 4 * 3, dout, size_t(len / 4 * 3), cudaMemcpyDeviceToHost, sd));
+        B64_CK(cudaEventRecord(pipe.d2h[b], sd));
+        last_off = off;
     }
-    return b64_decode_finalize(d_err_off, d_err_off, d_status, s_comp);
+    // packed error word -> (err_off, status) and the exact output length: the final chunk's
+    // valid length plus the bytes of the chunks before it, or 3*floor(err/4) on an error
+    launch(dec_finalize_len_kernel, 1, 1, sc, static_cast<const int64_t*>(d_err_off), d_err_off, d_status, d_out_len,
+           last_off / 4 * 3);
+    return launched();
 }
+#undef B64_CK
 
 }  // extern "C"

@@ -536,6 +536,25 @@ __global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off
     }
 }
 
+// Host pipeline (b64_decode_host): packed word -> (err_off, status) and the exact output
+// length: *out_len holds the final chunk's valid length (b64_decode_chunk), out_base the
+// bytes of the chunks before it; on an error only 3*floor(err/4) bytes are exact.
+__global__ void dec_finalize_len_kernel(const int64_t* cell, int64_t* err_off, int32_t* status, int64_t* out_len,
+                                        int64_t out_base) {
+    griddep_wait();
+    const unsigned long long wv = *reinterpret_cast<const unsigned long long*>(cell);
+    if (wv >= kErrNone) {
+        *err_off = -1;
+        if (status) *status = kOk;
+        if (out_len) *out_len += out_base;
+    } else {
+        const int64_t pos = int64_t(wv >> 3);
+        *err_off = pos;
+        if (status) *status = int32_t(wv & 7);
+        if (out_len) *out_len = 3 * (pos >> 2);
+    }
+}
+
 __global__ void dec_batch_init_kernel(int64_t* err, int64_t count) {
     griddep_wait();
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)

@@ -30,8 +30,6 @@ from typing import Optional, Tuple
 
 import torch
 
-ENC_UNIT = 768   # bytes per warp-chunk (256 triples)
-DEC_UNIT = 1024  # chars per warp-chunk (256 quads)
 ERR_NONE = 0x7F7F7F7F7F7F7F7F  # b64gpu.h B64_ERR_NONE: "no error" packed word
 
 
@@ -41,30 +39,31 @@ class Shard:
     stop: int        # one past the last
     out_start: int   # where this rank's output begins in the global output
     is_final: bool   # owns the stream's tail (encode padding / decode final quad)
+    out_len: int = 0  # this rank's output length (encode chars / decode capacity)
+
+
+def _shard(fn: str, length: int, world: int, rank: int) -> Shard:
+    import ctypes
+
+    from . import _lib
+
+    sh = _lib.Shard()
+    rc = getattr(_lib.lib(), fn)(length, world, rank, ctypes.byref(sh))
+    if rc == _lib.B64_ELENGTH:
+        raise ValueError("text length must be a multiple of 4")
+    if rc != _lib.B64_OK:
+        raise ValueError(f"bad shard request ({fn}: length {length}, world {world}, rank {rank})")
+    return Shard(sh.start, sh.stop, sh.out_start, bool(sh.is_final), sh.out_len)
 
 
 def encode_shard(n: int, world: int, rank: int) -> Shard:
-    """Rank's slice of an n-byte stream, cut at multiples of ENC_UNIT bytes."""
-    units = n // ENC_UNIT
-    u0 = units * rank // world
-    u1 = units * (rank + 1) // world
-    last = rank == world - 1
-    start = ENC_UNIT * u0
-    stop = n if last else ENC_UNIT * u1
-    return Shard(start, stop, 4 * (start // 3), last)
+    """Rank's slice of an n-byte stream (b64_encode_shard: cut at multiples of 768 bytes)."""
+    return _shard("b64_encode_shard", n, world, rank)
 
 
 def decode_shard(m: int, world: int, rank: int) -> Shard:
-    """Rank's slice of an m-char text (m % 4 == 0), cut at multiples of DEC_UNIT chars."""
-    if m % 4:
-        raise ValueError("text length must be a multiple of 4")
-    units = m // DEC_UNIT
-    u0 = units * rank // world
-    u1 = units * (rank + 1) // world
-    last = rank == world - 1
-    start = DEC_UNIT * u0
-    stop = m if last else DEC_UNIT * u1
-    return Shard(start, stop, 3 * (start // 4), last)
+    """Rank's slice of an m-char text (b64_decode_shard: m % 4 == 0, cut at multiples of 1024 chars)."""
+    return _shard("b64_decode_shard", m, world, rank)
 
 
 class CudaCodec:

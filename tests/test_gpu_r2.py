@@ -1,0 +1,262 @@
+"""GPU parity, round 2: the brute-force domains through the CUDA kernels, the device-side
+batch offsets, the closed boundary (exact lengths from the device, size queries), and the
+stream / device / buffer discipline of the Python binding.
+
+Every expected value comes from the oracle (oracle/) on the same inputs; the inputs are
+enumerations (all triples, all quads, all padded final quads) or seeded synthetic data.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def b64():
+    import __graft_entry__ as g
+
+    g.build()
+    import paper_1910_05109_b200 as m
+
+    assert torch.cuda.is_available()
+    return m
+
+
+def _alpha(b64, chars):
+    return b64.standard() if chars == oracle.STANDARD else b64.url()
+
+
+# ------------------------------------------------------------------ brute-force domains
+
+def test_all_triples_encode(b64):
+    """Every one of the 2^24 byte triples, as one 48 MiB stream: the fast
+    kernel (aligned) and the generic kernel (input at +1, output at +3), both alphabets."""
+    i = np.arange(1 << 24, dtype=np.uint32)
+    x = np.stack([(i >> 16) & 0xFF, (i >> 8) & 0xFF, i & 0xFF], axis=1).astype(np.uint8).reshape(-1)
+    for chars in (oracle.STANDARD, oracle.URL):
+        ref = oracle.encode(x, chars)
+        a = _alpha(b64, chars)
+        xd = torch.from_numpy(x).to(DEV)
+        got = b64.encode(xd, a)
+        assert np.array_equal(got.cpu().numpy(), ref)
+        buf = torch.empty(x.size + 1, dtype=torch.uint8, device=DEV)
+        buf[1:] = xd
+        ob = torch.empty(ref.size + 3, dtype=torch.uint8, device=DEV)
+        b64.encode(buf[1:], a, out=ob[3:])
+        assert np.array_equal(ob[3:].cpu().numpy(), ref)
+        del xd, buf, ob, got
+    torch.cuda.empty_cache()
+
+
+def test_all_quads_decode(b64):
+    """Every one of the 64^4 valid quads, as one 64 MiB text: bytes against
+    the oracle, both alphabets, fast and generic kernels; then one non-alphabet byte at the
+    very end of the enumeration (its final quad) and one in the middle."""
+    i = np.arange(1 << 24, dtype=np.uint32)
+    for chars in (oracle.STANDARD, oracle.URL):
+        A = np.frombuffer(chars, np.uint8)
+        t = np.stack([A[(i >> 18) & 63], A[(i >> 12) & 63], A[(i >> 6) & 63], A[i & 63]], axis=1).reshape(-1)
+        ref, rerr, rst = oracle.decode(t, chars)
+        assert rerr == -1 and ref.size == 3 << 24
+        a = _alpha(b64, chars)
+        td = torch.from_numpy(t).to(DEV)
+        y, err = b64.decode(td, a)
+        assert err == -1 and np.array_equal(y.cpu().numpy(), ref)
+        buf = torch.empty(t.size + 5, dtype=torch.uint8, device=DEV)
+        buf[5:] = td
+        y, err = b64.decode(buf[5:], a)  # generic kernel
+        assert err == -1 and np.array_equal(y.cpu().numpy(), ref)
+        for p in (t.size // 2 + 1, t.size - 3):
+            t2 = t.copy()
+            t2[p] = ord("*")
+            r2, e2, s2 = oracle.decode(t2, chars)
+            y, info = b64.decode_async(torch.from_numpy(t2).to(DEV), a)
+            err, st, olen = info.tolist()
+            assert (err, st, olen) == (e2, s2, 3 * (e2 // 4)) and e2 == p
+            assert np.array_equal(y[:olen].cpu().numpy(), r2)
+        del td, buf
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("lenient", [False, True])
+def test_all_padded_final_quads_batch(b64, lenient):
+    """All 4,096 'xx==' and all 262,144 'xxx=' quads as a batch of
+    4-char strings, strict and lenient (R6 / R16): status, err_off, out_len and bytes
+    against the oracle; strict accepts exactly 256 + 65,536 of them."""
+    A = np.frombuffer(oracle.STANDARD, np.uint8)
+    p = ord("=")
+    i2 = np.arange(64 * 64)
+    q2 = np.stack([A[i2 >> 6], A[i2 & 63], np.full_like(i2, p), np.full_like(i2, p)], axis=1).astype(np.uint8)
+    i3 = np.arange(64 ** 3)
+    q3 = np.stack([A[i3 >> 12], A[(i3 >> 6) & 63], A[i3 & 63], np.full_like(i3, p)], axis=1).astype(np.uint8)
+    t = np.concatenate([q2, q3]).reshape(-1)
+    count = t.size // 4
+    off = np.arange(count + 1, dtype=np.int64) * 4
+    rout, roff, rst, rerr, rlen = oracle.decode_batch(t, off, lenient=lenient)
+    a = b64.standard() if not lenient else b64.lenient_of(b64.standard())
+    out, oo, st, err, olen = b64.decode_batch(torch.from_numpy(t).to(DEV), torch.from_numpy(off).to(DEV), a)
+    assert np.array_equal(oo.cpu().numpy(), roff)
+    assert np.array_equal(st.cpu().numpy(), rst)
+    assert np.array_equal(err.cpu().numpy(), rerr)
+    assert np.array_equal(olen.cpu().numpy(), rlen)
+    if not lenient:
+        assert int((rst == 0).sum()) == 256 + 65536
+    else:
+        assert int((rst == 0).sum()) == count
+    o = out.cpu().numpy()
+    for k in np.nonzero(rst == 0)[0][::97]:
+        assert np.array_equal(o[roff[k]: roff[k] + rlen[k]], rout[roff[k]: roff[k] + rlen[k]])
+    ok = np.nonzero(rst == 0)[0]
+    # every accepted string's bytes: gather the first byte (always present) and compare in bulk
+    assert np.array_equal(o[roff[ok]], rout[roff[ok]])
+    two = ok[rlen[ok] >= 2]
+    assert np.array_equal(o[roff[two] + 1], rout[roff[two] + 1])
+
+
+def test_config3_encode_full_length(b64):
+    """configs[2]'s 1 GiB encode (enc_fast_kernel<2>) compared over its whole 1.43 GB output,
+    in 96 MiB windows cut at 3-byte boundaries (each window is the oracle's encode of its
+    bytes; the last one carries the '==' padding)."""
+    n = 1 << 30
+    xd = synth.device_data(n, seed=0)
+    t = b64.encode(xd)
+    assert t.numel() == 1431655768
+    W = 96 << 20  # a multiple of 3
+    for s in range(0, n, W):
+        e = min(n, s + W)
+        ref = oracle.encode(xd[s:e].cpu().numpy())
+        got = t[4 * (s // 3): 4 * (s // 3) + ref.size].cpu().numpy()
+        assert np.array_equal(got, ref), s
+    del xd, t
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ device-side batch offsets
+
+@pytest.mark.parametrize("count", [0, 1, 2, 2047, 2048, 2049, 4096, 100_003])
+def test_batch_offsets_vs_oracle(b64, count):
+    """b64_encode_batch_offsets / b64_decode_batch_offsets (three-kernel device scan) against the
+    oracle's offsets (exclusive scans of the length law / decode capacity); lengths include 0
+    and every residue mod 3 and 4, offsets start at a non-zero base."""
+    rng = np.random.default_rng(count)
+    lens = rng.integers(0, 70, size=count).astype(np.int64)
+    lens[::17] = 0
+    off = np.concatenate([[13], 13 + np.cumsum(lens)]).astype(np.int64)
+    d = torch.from_numpy(off).to(DEV)
+    x = synth.data(int(off[-1]) + 1, seed=count)
+    _, eref = oracle.encode_batch(x, off)
+    _, dref, *_ = oracle.decode_batch(x, off)
+    assert np.array_equal(b64.encode_batch_offsets(d).cpu().numpy(), eref)
+    assert np.array_equal(b64.decode_batch_offsets(d).cpu().numpy(), dref)
+
+
+# ------------------------------------------------------------------ the closed boundary
+
+def test_host_pipeline_length_from_device(b64):
+    """HostPipeline.decode takes the exact output length from the device (b64_decode_host's
+    d_out_len): valid texts with 0 / 1 / 2 pads, an error in the last chunk, an empty text."""
+    pipe = b64.HostPipeline(chunk_bytes=3072 * 3)
+    for n in (0, 1, 2, 3, 9216, 9217, 9218, 50_000):
+        x = synth.data(n, seed=n)
+        ref = oracle.encode(x)
+        y, err = pipe.decode(torch.from_numpy(ref.copy()).pin_memory())
+        assert err == -1 and y.numel() == n and np.array_equal(y.numpy(), x)
+        if ref.size >= 8:
+            t2 = ref.copy()
+            t2[-6] = ord("#")
+            rr, re, rs = oracle.decode(t2)
+            yo, info = pipe.decode(torch.from_numpy(t2).pin_memory(), sync=False)
+            pipe.join()
+            torch.cuda.synchronize()
+            err, _, olen = info.tolist()
+            assert (err, olen) == (re, rr.size) and np.array_equal(yo[:olen].numpy(), rr)
+
+
+def test_unpadded_and_stream_sizes_from_library(b64):
+    """decode_unpadded's buffer and the stream pieces' sizes come from the library's queries;
+    results against the oracle for every tail length."""
+    for n in range(0, 40):
+        x = synth.data(n, seed=n + 3)
+        tu = oracle.encode_unpadded(x, oracle.URL)
+        y, err = b64.decode_unpadded(torch.from_numpy(tu.copy()).to(DEV), b64.url())
+        assert err == -1 and np.array_equal(y.cpu().numpy(), x), n
+    x = synth.data(10_007, seed=1)
+    ref = oracle.encode(x)
+    es = b64.EncodeStream()
+    parts = [es.update(torch.from_numpy(x[a:b].copy()).to(DEV)) for a, b in ((0, 1), (1, 5), (5, 10_000), (10_000, 10_007))]
+    parts.append(es.end())
+    assert np.array_equal(torch.cat(parts).cpu().numpy(), ref)
+    ds = b64.DecodeStream()
+    cuts = (0, 3, 4, 7, 5000, ref.size)
+    parts = [ds.update(torch.from_numpy(ref[a:b].copy()).to(DEV)) for a, b in zip(cuts, cuts[1:])]
+    tail, info = ds.end()
+    torch.cuda.synchronize()
+    err, _, olen = info.tolist()
+    got = torch.cat(parts + [tail]).cpu().numpy()
+    assert err == -1 and np.array_equal(got[: x.size], x)
+
+
+# ------------------------------------------------------------------ binding discipline
+
+def test_explicit_stream_not_current(b64):
+    """stream= a side stream while the current stream is busy: the wrappers order their scratch
+    fills (info, cells, ticket) before the kernels and join before reading results
+    (stream-ordering race)."""
+    side = torch.cuda.Stream()
+    x = synth.data(3 * 1024 * 1024 + 1, seed=5)
+    ref = oracle.encode(x)
+    t2 = ref.copy()
+    t2[777] = ord("*")
+    xd = torch.from_numpy(x).to(DEV)
+    td = torch.from_numpy(t2).to(DEV)
+    for rep in range(3):
+        torch.cuda._sleep(20_000_000)  # the current stream stays busy for a while
+        y, err = b64.decode(td, stream=side)
+        assert err == 777
+        torch.cuda._sleep(20_000_000)
+        y, err = b64.decode_unpadded(td, stream=side)
+        assert err == 777
+        torch.cuda._sleep(20_000_000)
+        outs, err, st = b64.decode_group([td, torch.from_numpy(ref).to(DEV)], stream=side)
+        side.synchronize()
+        assert err.tolist() == [777, -1]
+        torch.cuda._sleep(20_000_000)
+        eo, do, err, st = b64.codec_group_fused([xd], [td], stream=side)
+        side.synchronize()
+        assert err.tolist() == [777] and np.array_equal(eo[0].cpu().numpy(), ref)
+    torch.cuda.synchronize()
+
+
+def test_out_buffers_checked(b64):
+    """Caller-supplied outputs are checked before any launch: too small, wrong dtype,
+    host memory, wrong device -> B64Error, nothing launched."""
+    x = torch.from_numpy(synth.data(3000, seed=2)).to(DEV)
+    t = b64.encode(x)
+    before = b64.launch_count()
+    bad = [torch.empty(10, dtype=torch.uint8, device=DEV), torch.empty(t.numel(), dtype=torch.int16, device=DEV),
+           torch.empty(t.numel(), dtype=torch.uint8)]
+    for o in bad:
+        with pytest.raises(b64.B64Error):
+            b64.encode(x, out=o)
+        with pytest.raises(b64.B64Error):
+            b64.decode_async(t, out=o)
+        with pytest.raises(b64.B64Error):
+            b64.decode_chunk(t, 0, True, torch.full((1,), b64.ERR_NONE, dtype=torch.int64, device=DEV), out=o)
+    with pytest.raises(b64.B64Error):
+        b64.decode_ws(t, out=torch.empty(5, dtype=torch.uint8, device=DEV))
+    with pytest.raises(b64.B64Error):
+        b64.encode_batch(x, torch.tensor([0, 3000], dtype=torch.int64, device=DEV),
+                         out=torch.empty(5, dtype=torch.uint8, device=DEV),
+                         out_off=torch.tensor([0, 4000], dtype=torch.int64, device=DEV))
+    es = b64.EncodeStream()
+    with pytest.raises(b64.B64Error):
+        es.update(x, out=torch.empty(1, dtype=torch.uint8, device=DEV))
+    assert b64.launch_count() == before
