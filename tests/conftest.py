@@ -11,6 +11,7 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a); run with -m gpu")
     config.addinivalue_line("markers", "slow: longer CPU test")
+    config.addinivalue_line("markers", "sanitize: small-size run of every entry point for compute-sanitizer")
 
 
 @pytest.fixture(scope="session")
