@@ -335,8 +335,15 @@ def decode_finalize(err_cell: torch.Tensor, err_off: torch.Tensor, status: Optio
 
 # ------------------------------------------------------------------ grouped launches
 
-def _enc_items(xs, alphabets, outs, dev, on):
+class _NoOn:
+    def owns(self, *ts) -> None:
+        pass
+
+
+def _enc_items(xs, alphabets, outs, dev=None, on=None):
     k = len(xs)
+    dev = dev if dev is not None else (xs[0].device if xs else None)
+    on = on if on is not None else _NoOn()
     al = alphabets if isinstance(alphabets, (list, tuple)) else [alphabets] * k
     al = [a if a is not None else standard() for a in al]
     lens = [encoded_len(x.numel()) for x in xs]
@@ -351,8 +358,10 @@ def _enc_items(xs, alphabets, outs, dev, on):
     return items, [o[:m] for m, o in zip(lens, outs)]
 
 
-def _dec_items(ts, alphabets, outs, cells, bases, finals, dev, on):
+def _dec_items(ts, alphabets, outs, cells, bases, finals, dev=None, on=None):
     k = len(ts)
+    dev = dev if dev is not None else ts[0].device
+    on = on if on is not None else _NoOn()
     al = alphabets if isinstance(alphabets, (list, tuple)) else [alphabets] * k
     al = [a if a is not None else standard() for a in al]
     caps = [decoded_len_max(t.numel()) for t in ts]

@@ -59,3 +59,42 @@ def test_our_arm_contract():
     assert d["gpu_launches"] in (d["steps"], 2 * d["steps"], 3 * d["steps"])
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_reference_arm_gpus_flag_without_torchrun():
+    """`bench.py --impl reference --gpus 2` (no torchrun) reports the N asked for."""
+    lines = _json_lines(_run(["bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0"]))
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2
+
+
+@pytest.mark.gpu
+def test_our_arm_spawns_ranks():
+    """`bench.py --gpus 2` started without torchrun spawns 2 ranks itself and prints ONE line
+    with n_gpus 2 (on a 1-GPU box the ranks share it over gloo and the line says so)."""
+    lines = _json_lines(_run(["bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-extra",
+                              "--cpu-seconds", "1", "--e2e-steps", "1"], timeout=900))
+    assert len(lines) == 1
+    d = lines[0]
+    assert BASE_KEYS <= set(d) and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["ranks"] == 2 and d["cpu_baseline"]["kind"] == "oracle"
+    assert "error_combine" in d["config"]
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        assert "shared_gpus" in d["config"]
+
+
+@pytest.mark.gpu
+def test_multi_gpu_rows_real_ranks():
+    """With >= 2 visible GPUs: the strong-scaling rows over 2 real ranks (NCCL and the peer
+    combine side by side), first error found across ranks."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    lines = _json_lines(_run(["bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--cpu-seconds", "1",
+                              "--e2e-steps", "1"], timeout=1800))
+    d = lines[0]
+    r = d["rows"]["configs[4]"]
+    assert r["first_error"] == r["first_error"] and r["injected"] == 1000
+    assert r["decode_ms_with_combine_peer"] is not None
