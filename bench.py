@@ -629,6 +629,7 @@ def scale_rows(b64, synth, torch, dev, world, rank, flush, args, peak):
             barrier()
             torch.cuda.synchronize()
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            torch.cuda._sleep(1_000_000)  # the host enqueues the op while the GPU sleeps: no launch gap timed
             e0.record(stream)
             fn(e1)
             e2.record(stream)
@@ -743,6 +744,7 @@ def batch_row(b64, synth, torch, dev, world, rank, flush, args, peak):
                 dist.barrier()
             torch.cuda.synchronize()
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            torch.cuda._sleep(1_000_000)  # the host enqueues the op while the GPU sleeps: no launch gap timed
             e0.record(stream)
             fn(e1)
             e2.record(stream)

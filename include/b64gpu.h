@@ -462,6 +462,30 @@ int b64_decode_batch_ex(const uint8_t *d_in, const int64_t *d_in_off, int64_t co
                         int32_t *d_status, int64_t *d_err_off, int64_t *d_out_len,
                         int64_t index_base, int64_t *d_first_bad, b64_stream_t stream);
 
+/* b64_decode_batch_ex with a caller-owned context that enables the
+ * concatenation path: when every string length is
+ * a multiple of 4, d_out_off[i] - d_out_off[0] = 3*(d_in_off[i] - d_in_off[0])/4
+ * (the b64_decode_batch_offsets layout), d_in + d_in_off[0] is 32-byte and
+ * d_out + d_out_off[0] 16-byte aligned, the bulk of the batch is decoded as
+ * ONE stream (the single-stream fast kernel over the concatenated text) and
+ * only the strings' final quads get a per-string pass; otherwise -- or when a
+ * '=' sits anywhere but the last two chars of its string -- the per-string
+ * kernel of b64_decode_batch_ex runs.  The results (d_status, d_err_off,
+ * d_out_len, d_first_bad, and the bytes up to each string's out_len) are
+ * those of b64_decode_batch_ex; the bytes of a string's slot after its
+ * out_len may be overwritten.  The eligibility is decided on the device (no
+ * host sync).  d_ctx: B64_BATCH_CTX_BYTES of device memory set up once with
+ * b64_batch_ctx_init; every call leaves it ready for the next, so calls that
+ * share a context must be ordered (one context per stream).  d_ctx == NULL is
+ * b64_decode_batch_ex.  Five launches (the per-string kernel returns at once
+ * when the concatenation path did the work). */
+#define B64_BATCH_CTX_BYTES 32
+int b64_batch_ctx_init(uint8_t *d_ctx, b64_stream_t stream);
+int b64_decode_batch_fast(const uint8_t *d_in, const int64_t *d_in_off, int64_t count,
+                          uint8_t *d_out, const int64_t *d_out_off, const b64_alphabet *a,
+                          int32_t *d_status, int64_t *d_err_off, int64_t *d_out_len,
+                          int64_t index_base, int64_t *d_first_bad, uint8_t *d_ctx, b64_stream_t stream);
+
 /* ---- introspection ---------------------------------------------------------- */
 /* Number of kernels the library launched on this process so far (all calls),
  * counted on the host at each launch -- used by bench.py's gpu_launches. */

@@ -24,7 +24,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "lenient_of", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
     "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "encode_batch_offsets",
-    "decode_batch_offsets", "launch_count", "HostPipeline", "new_info", "decode_unpadded", "decode_ws",
+    "decode_batch_offsets", "BatchContext", "DecodeContext", "launch_count", "HostPipeline", "new_info", "decode_unpadded", "decode_ws",
     "encode_group", "decode_group", "codec_group", "codec_group_fused", "EncodeStream", "DecodeStream",
     "ERR_NONE",
 ]
@@ -62,10 +62,10 @@ class _On:
     """Device guard + stream order for one call on `stream` (default: the current stream).
 
     The library launches on `stream`; the wrappers allocate and initialise their scratch on the
-    current stream.  When the two differ, `stream` first waits for the current stream (so those
-    fills -- and the caller's producers -- are done before the kernels run), internally allocated
-    tensors are marked as used on `stream`, and join() makes the current stream wait for
-    `stream` before a host read of a result."""
+    current stream.  When the two differ, `stream` waits for the current stream right before
+    every launch (reading `sp`), so those fills -- and the caller's producers -- are done before
+    the kernels run; internally allocated tensors are marked as used on `stream` (owns), and
+    join() makes the current stream wait for `stream` before a host read of a result."""
 
     def __init__(self, device, stream: Optional[torch.cuda.Stream] = None):
         self.dev = torch.device(device)
@@ -77,12 +77,13 @@ class _On:
         self.cur = torch.cuda.current_stream(self.dev)
         self.s = self.stream if self.stream is not None else self.cur
         self.other = self.s.cuda_stream != self.cur.cuda_stream
-        if self.other:
-            self.s.wait_stream(self.cur)
         return self
 
     @property
     def sp(self):
+        """The launch stream handle, ordered after everything queued on the current stream."""
+        if self.other:
+            self.s.wait_stream(self.cur)
         return ctypes.c_void_p(self.s.cuda_stream)
 
     def owns(self, *ts) -> None:
@@ -703,6 +704,29 @@ def decode_batch_offsets(in_off: torch.Tensor, stream: Optional[torch.cuda.Strea
     return out_off
 
 
+class BatchContext:
+    """Device context of b64_decode_batch_fast (B64_BATCH_CTX_BYTES): enables the batched decode's
+    concatenation path.  Self-resetting; calls sharing a context must be ordered (one per stream)."""
+
+    def __init__(self, device=None, stream: Optional[torch.cuda.Stream] = None):
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        with _On(dev, stream) as on:
+            self.buf = torch.empty(_lib.BATCH_CTX_BYTES, dtype=torch.uint8, device=dev)
+            on.owns(self.buf)
+            _lib.check(_lib.lib().b64_batch_ctx_init(_ptr(self.buf), on.sp), "b64_batch_ctx_init")
+
+
+_BATCH_CTX_CACHE = {}  # (device index, stream handle) -> BatchContext
+
+
+def _batch_ctx(dev: torch.device, s: torch.cuda.Stream) -> BatchContext:
+    key = (dev.index, s.cuda_stream)
+    ctx = _BATCH_CTX_CACHE.get(key)
+    if ctx is None:
+        ctx = _BATCH_CTX_CACHE[key] = BatchContext(dev, stream=s)
+    return ctx
+
+
 def _batch_total(out_off: torch.Tensor, on: "_On") -> int:
     on.join()
     return int(out_off[-1].item())
@@ -742,11 +766,15 @@ def encode_batch(x: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = 
 def decode_batch(t: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = None,
                  out: Optional[torch.Tensor] = None, out_off: Optional[torch.Tensor] = None,
                  total_out: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None,
-                 index_base: int = 0, first_bad: Optional[torch.Tensor] = None):
+                 index_base: int = 0, first_bad: Optional[torch.Tensor] = None,
+                 ctx: Optional[BatchContext] = None, fast: bool = True):
     """Per-string validating decode.  Returns (out, out_off, status int32, err_off int64
     (relative, -1 = ok), out_len int64); out_off = exclusive scan of 3*(len//4).
     first_bad (device int64[1], caller-initialised, e.g. ERR_NONE): lowered to index_base + the
-    index of the first failing string (b64_decode_batch_ex)."""
+    index of the first failing string.  fast (default): b64_decode_batch_fast with `ctx` (or
+    a context cached per device and stream) -- the concatenation path when the batch is
+    eligible; fast=False: b64_decode_batch_ex (the per-string kernel only).  Bytes of a
+    string's slot after its out_len are unspecified."""
     _check_u8(t, "t")
     dev = t.device
     _check_i64(in_off, "in_off", dev, 1)
@@ -772,10 +800,14 @@ def decode_batch(t: torch.Tensor, in_off: torch.Tensor, a: Optional[Alphabet] = 
         err = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
         olen = torch.empty(max(count, 1), dtype=torch.int64, device=dev)
         on.owns(status, err, olen)
-        _lib.check(_lib.lib().b64_decode_batch_ex(_ptr(t), _ptr(in_off), count, _ptr(out), _ptr(out_off), _alpha(a),
-                                                  _ptr(status), _ptr(err), _ptr(olen), index_base,
-                                                  _ptr(first_bad) if first_bad is not None else None, on.sp),
-                   "b64_decode_batch_ex")
+        cbuf = None
+        if fast:
+            cbuf = (ctx if ctx is not None else _batch_ctx(dev, on.s)).buf
+            _check_u8(cbuf, "ctx", dev)
+        _lib.check(_lib.lib().b64_decode_batch_fast(_ptr(t), _ptr(in_off), count, _ptr(out), _ptr(out_off), _alpha(a),
+                                                    _ptr(status), _ptr(err), _ptr(olen), index_base,
+                                                    _ptr(first_bad) if first_bad is not None else None, _ptr(cbuf),
+                                                    on.sp), "b64_decode_batch_fast")
     return out, out_off, status[:count], err[:count], olen[:count]
 
 

@@ -38,6 +38,7 @@ P, I64, I32, INT = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int
 
 ALPHA_LENIENT = 1  # B64_ALPHA_LENIENT
 DECODE_CTX_BYTES = 16  # B64_DECODE_CTX_BYTES
+BATCH_CTX_BYTES = 32  # B64_BATCH_CTX_BYTES
 HOST_CALLER_ORDERED = 1  # B64_HOST_CALLER_ORDERED
 
 
@@ -123,6 +124,8 @@ SIGNATURES = [
     ("b64_decode_batch", INT, [P, P, I64, P, P, AP, P, P, P, P]),
     ("b64_decode_batch_ex", INT, [P, P, I64, P, P, AP, P, P, P, I64, P, P]),
     ("b64_decode_ctx_init", INT, [P, P]),
+    ("b64_batch_ctx_init", INT, [P, P]),
+    ("b64_decode_batch_fast", INT, [P, P, I64, P, P, AP, P, P, P, I64, P, P, P]),
     ("b64_decode_fused", INT, [P, I64, P, AP, P, P, P, P, P]),
     ("b64_launch_count", I64, []),
     ("b64_build_info", ctypes.c_char_p, []),

@@ -332,6 +332,17 @@ __device__ __forceinline__ int64_t first_string_ending_after(const Offsets& off,
     return lo;
 }
 
+// Context of the batched decode's concatenation path (batch.cu): caller-owned,
+// self-resetting (B64_BATCH_CTX_BYTES = 32, all zero initially).
+struct BatchCtx {
+    uint32_t generic;          // 1: the per-string generic kernel must run
+    uint32_t ticket;           // strfinal's last-CTA ticket
+    unsigned long long eq;     // pad chars the bulk pass saw
+    unsigned long long legit;  // pad chars at positions len-2 / len-1 of the strings
+    uint32_t reserved[2];
+};
+static_assert(sizeof(BatchCtx) == 32, "B64_BATCH_CTX_BYTES");
+
 // Kernel entry points (defined in encode.cu / decode.cu, launched by capi.cu).
 template <int D>
 __global__ void enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab,
@@ -356,7 +367,8 @@ __global__ void dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8
                                 int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev, StreamJoin join);
 __global__ void dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off,
                                    DecTab tab, int64_t base, int is_final_single,
-                                   unsigned long long* __restrict__ err_cells, int64_t* __restrict__ out_len_single);
+                                   unsigned long long* __restrict__ err_cells, int64_t* __restrict__ out_len_single,
+                                   const BatchCtx* gate);
 __global__ void dec_small_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                                  int64_t* __restrict__ err_off, int32_t* __restrict__ status,
                                  int64_t* __restrict__ out_len);
@@ -371,6 +383,7 @@ __global__ void dec_finalize_len_kernel(const int64_t* cell, int64_t* err_off, i
 __global__ void dec_batch_init_kernel(int64_t* err, int64_t count);
 __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
                                           int64_t count, uint32_t pad, int32_t* status, int64_t* err,
-                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad);
+                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad,
+                                          BatchCtx* reset);
 
 }  // namespace b64

@@ -8,5 +8,6 @@
 #include "mime.cu"
 #include "stream.cu"
 #include "offsets.cu"
+#include "batch.cu"
 #include "capi.cu"
 #include "capi_ext.cu"

@@ -1,0 +1,227 @@
+// batch.cu -- the batched decode's concatenation path (BASELINE.json configs[3];
+// b64_decode_batch_fast).
+//
+// When every string length is a multiple of 4 and the output offsets are the
+// scan of 3*len/4 (the layout b64_decode_batch_offsets produces), the batch's
+// output is laid out exactly like the decode of the concatenated text: quad q
+// of the concatenation lands at out + 3q whatever string it belongs to
+// (every quad decodes on its own).  So the bulk of the batch
+// runs the single-stream dec_fast loop (one LDG.256 per lane, shared-memory
+// re-layout, lane-linear stores) over the concatenation, and only the strings'
+// final quads -- the one place padding may appear (DESIGN.md
+// R6) -- get a per-string pass.  Five launches:
+//   1. dec_batch_prep_kernel   err[i] = none; checks the layout (len % 4, the
+//                              offsets, alignment) -> ctx->generic = 1 if not.
+//   2. dec_batch_bulk_kernel   the concatenation, every quad as interior, with
+//                              the pad char classified as 0x40 (a "deferred pad
+//                              candidate", PAPER.md:305-313's deferred check):
+//                              0x80 chars are reported per string, the '='
+//                              seen are counted.
+//   3. dec_batch_strfinal_kernel  per string: the final quad under R6 / R16
+//                              (bytes rewritten, errors reported) and the
+//                              count of '=' at len-2 / len-1; the last CTA
+//                              compares: more '=' seen than at final
+//                              positions -> a pad is misplaced somewhere ->
+//                              ctx->generic = 1.
+//   4. dec_generic_kernel      only when ctx->generic: the exact per-string
+//                              decode (not eligible, or a misplaced '=').
+//   5. dec_batch_finalize_kernel  status / err_off / out_len per string; resets
+//                              the context for the next call.
+// Every position reported in steps 2-4 is a genuinely bad position under the
+// rules, so the per-string MIN is the first error whichever steps ran.
+#include "b64_device.cuh"
+
+namespace b64 {
+
+constexpr uint32_t kPadCand = 0x40u;  // table value of the pad char in the bulk pass
+
+__global__ void __launch_bounds__(kThreads)
+dec_batch_prep_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off, const uint8_t* out,
+                      const int64_t* __restrict__ out_off, int64_t count, int64_t* __restrict__ err, BatchCtx* ctx) {
+    griddep_launch_dependents();
+    griddep_wait();
+    const int64_t g0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x, gs = int64_t(gridDim.x) * blockDim.x;
+    const int64_t a0 = in_off[0], o0 = out_off[0];
+    bool bad = g0 == 0 && (((reinterpret_cast<uintptr_t>(in + a0) & 31) != 0) ||
+                           ((reinterpret_cast<uintptr_t>(out + o0) & 15) != 0));
+    for (int64_t i = g0; i < count; i += gs) {
+        err[i] = int64_t(kErrNone);
+        const int64_t a = in_off[i], L = in_off[i + 1] - a;
+        bad |= (L & 3) != 0 || L < 0 || out_off[i] - o0 != 3 * ((a - a0) >> 2);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) ctx->generic = 1u;
+}
+
+// First string s with in_off[s + 1] > pos (pos absolute, in the concatenated input).
+__device__ __forceinline__ int64_t string_of(const int64_t* __restrict__ in_off, int64_t count, int64_t pos) {
+    int64_t lo = 0, hi = count - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (in_off[mid + 1] > pos) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+
+// Rare path: every string with a non-alphabet char among the nchar chars at p (absolute
+// input position P) gets its first such char (within the window) reported, relative to
+// the string's start.  The pad char is not reported here (step 3 / 4 decide it).
+__device__ __noinline__ void report_window(const uint8_t* p, int64_t P, int nchar, const uint8_t* __restrict__ lut,
+                                           const int64_t* __restrict__ in_off, int64_t count,
+                                           unsigned long long* __restrict__ cells) {
+    int64_t send = INT64_MIN;
+    for (int c = 0; c < nchar; ++c) {
+        if (!(lut[p[c]] & kInvalid)) continue;
+        const int64_t pos = P + c;
+        if (pos < send) continue;  // a later bad char of a string already reported
+        const int64_t s = string_of(in_off, count, pos);
+        const int64_t a = in_off[s];
+        send = in_off[s + 1];
+        atomicMin(&cells[s], pack_err(pos - a, kBadChar));
+    }
+}
+
+__device__ __forceinline__ uint32_t count_pads(const uint32_t (&x)[8], uint32_t pad4) {
+    uint32_t k = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) k += __popc(__vcmpeq4(x[q], pad4));
+    return k >> 3;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+dec_batch_bulk_kernel(const uint8_t* __restrict__ in_base, const int64_t* __restrict__ in_off,
+                      uint8_t* __restrict__ out_base, const int64_t* __restrict__ out_off, int64_t count, DecTab tab,
+                      unsigned long long* __restrict__ cells, BatchCtx* ctx) {
+    __shared__ __align__(256) uint32_t s_lut[64];
+    __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];
+    griddep_launch_dependents();
+    griddep_wait();
+    if (ctx->generic) return;  // the layout is not the concatenation's: step 4 does it all
+    const int lane = threadIdx.x & 31;
+    const int64_t a0 = in_off[0];
+    const int64_t m = in_off[count] - a0;
+    const uint8_t* in = in_base + a0;
+    uint8_t* out = out_base + out_off[0];
+    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t nwarp = gthreads >> 5;
+    const int64_t Q = m >> 2;
+    const int64_t nchunk = Q >> 8;
+    const uint32_t sb = smem_u32(&s_stage[threadIdx.x >> 5][0]);
+    const uint32_t pad4 = tab.pad * 0x01010101u;
+
+    // the dec_fast_kernel loop (decode.cu) over the concatenation, every quad interior
+    const int64_t c0 = gtid >> 5;
+    const int32_t C = int32_t(nchunk), W = int32_t(nwarp), c0i = int32_t(c0);
+    const int64_t sin = nwarp * 1024, sout = nwarp * 768;
+    const uint8_t* pin = in + c0 * 1024 + lane * 32;
+    const uint8_t* pcur = pin;
+    uint8_t* pout = out + c0 * 768;
+    uint32_t xr[D][8];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        if (c0i + i * W < C) {
+            ld256_stream(pin, xr[i]);
+            pin += sin;
+        }
+    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
+    uint32_t npad = 0;
+    for (int32_t cb = c0i; cb < C; cb += D * W) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int32_t c = cb + i * W;
+            if (c < C) {
+                uint32_t y[8];
+                if (c + D * W < C) {
+                    ld256_stream(pin, y);
+                    pin += sin;
+                }
+                uint32_t err = 0, v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(xr[i][q], lb, err);
+                uint32_t o[6];
+                dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
+                dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
+                sts64(sb + lane * 24, o[0], o[1]);
+                sts64(sb + lane * 24 + 8, o[2], o[3]);
+                sts64(sb + lane * 24 + 16, o[4], o[5]);
+                __syncwarp();
+                uint8_t* dst = pout + lane * 8;
+                const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8),
+                            s2 = lds64(sb + 512 + lane * 8);
+                st64(dst, s0.x, s0.y);
+                st64(dst + 256, s1.x, s1.y);
+                st64(dst + 512, s2.x, s2.y);
+                __syncwarp();
+                if (err & (kInvalid | kPadCand)) {  // rare: a bad char or a pad candidate in my 32 chars
+                    if (err & kPadCand) npad += count_pads(xr[i], pad4);
+                    if (err & kInvalid)
+                        report_window(pcur, a0 + int64_t(c) * 1024 + lane * 32, 32, lut, in_off, count, cells);
+                }
+                pout += sout;
+                pcur += sin;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) xr[i][j] = y[j];
+            }
+        }
+    }
+    // leftover quads, one per thread
+    for (int64_t q = (nchunk << 8) + gtid; q < Q; q += gthreads) {
+        const uint32_t x = ld32(in + 4 * q);
+        uint32_t err = 0;
+        const uint32_t v = dec_quad(x, lut, err);
+        store_bytes(out + 3 * q, v, 3);
+        if (err & kPadCand) npad += __popc(__vcmpeq4(x, pad4)) >> 3;
+        if (err & kInvalid) report_window(in + 4 * q, a0 + 4 * q, 4, lut, in_off, count, cells);
+    }
+    npad = __reduce_add_sync(kFull, npad);
+    if (lane == 0 && npad) atomicAdd(&ctx->eq, static_cast<unsigned long long>(npad));
+}
+
+__global__ void __launch_bounds__(kThreads)
+dec_batch_strfinal_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off, uint8_t* __restrict__ out,
+                          const int64_t* __restrict__ out_off, int64_t count, DecTab tab,
+                          unsigned long long* __restrict__ cells, BatchCtx* ctx) {
+    __shared__ __align__(256) uint32_t s_lut[64];
+    __shared__ unsigned long long s_sum[kThreads / 32];
+    __shared__ bool s_last;
+    griddep_launch_dependents();
+    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __syncthreads();
+    griddep_wait();
+    if (ctx->generic) return;
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    unsigned long long legit = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t a = in_off[i], L = in_off[i + 1] - a;
+        if (L < 4) continue;
+        const uint32_t x = ld32(in + a + L - 4);  // 4-byte aligned: the layout check passed
+        legit += uint32_t(((x >> 16) & 0xffu) == tab.pad) + uint32_t((x >> 24) == tab.pad);
+        int bad, k;
+        uint32_t v;
+        const uint32_t kind = final_quad(x, lut, tab.pad, tab.lenient, &bad, &k, &v);
+        if (kind == kOk) store_bytes(out + out_off[i] + 3 * ((L >> 2) - 1), v, k);
+        else atomicMin(&cells[i], pack_err(L - 4 + bad, kind));
+    }
+    legit = __reduce_add_sync(kFull, unsigned(legit));  // < 2^32 per warp
+    if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = legit;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long b = 0;
+        for (int w = 0; w < kThreads / 32; ++w) b += s_sum[w];
+        if (b) atomicAdd(&ctx->legit, b);
+        __threadfence();
+        s_last = atomicAdd(&ctx->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        const unsigned long long eq = atomicAdd(&ctx->eq, 0ull), lg = atomicAdd(&ctx->legit, 0ull);
+        if (eq != lg) ctx->generic = 1u;  // a pad char outside the final two positions of its string
+    }
+}
+
+}  // namespace b64

@@ -336,7 +336,7 @@ __device__ __forceinline__ void dec_short_lane(const uint8_t* __restrict__ src, 
 __global__ void __launch_bounds__(kThreads, B64_GEN_MINB)
 dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, DecTab tab,
                    int64_t base, int is_final_single, unsigned long long* __restrict__ err_cells,
-                   int64_t* __restrict__ out_len_single) {
+                   int64_t* __restrict__ out_len_single, const BatchCtx* gate) {
     __shared__ __align__(256) uint32_t s_lut[64];
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     __syncthreads();
@@ -344,6 +344,7 @@ dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
     const uint32_t lb = smem_u32(s_lut);
     const bool batch = off.in_off != nullptr;
     griddep_wait();
+    if (gate && !gate->generic) return;  // the batch's concatenation path did it all (batch.cu)
 
     const int lane = threadIdx.x & 31;
     const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -563,8 +564,11 @@ __global__ void dec_batch_init_kernel(int64_t* err, int64_t count) {
 
 __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
                                           int64_t count, uint32_t pad, int32_t* status, int64_t* err,
-                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad) {
+                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad,
+                                          BatchCtx* reset) {
     griddep_wait();
+    if (reset && blockIdx.x == 0 && threadIdx.x < sizeof(BatchCtx) / 4)
+        reinterpret_cast<uint32_t*>(reset)[threadIdx.x] = 0;  // ready for the next call
     int64_t bad = INT64_MAX;  // this thread's first failing string (index_base + i)
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t a = in_off[i], L = in_off[i + 1] - a;

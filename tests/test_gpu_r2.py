@@ -260,3 +260,103 @@ def test_out_buffers_checked(b64):
     with pytest.raises(b64.B64Error):
         es.update(x, out=torch.empty(1, dtype=torch.uint8, device=DEV))
     assert b64.launch_count() == before
+
+
+# ------------------------------------------------------------------ batched decode: concatenation path
+
+def _batch_case(count, seed, hi=3000):
+    Ls = synth.loguniform_lengths(count, hi=hi, seed=seed)
+    off = synth.offsets(Ls)
+    x = synth.data(int(off[-1]), seed=seed)
+    text, toff = oracle.encode_batch(x, off)
+    return text, toff
+
+
+@pytest.mark.parametrize("lenient", [False, True])
+def test_batch_fast_path_vs_oracle(b64, lenient):
+    """b64_decode_batch_fast: eligible batches (every length a
+    multiple of 4) with corruptions of every kind -- non-alphabet bytes, '=' in the middle of a
+    string (the pad-count mismatch -> per-string fallback), '=' at len-3, data after '=',
+    non-canonical final quads -- against the oracle, strict and lenient; and the same batch
+    through the generic path (fast=False) gives identical results."""
+    a = b64.standard() if not lenient else b64.lenient_of(b64.standard())
+    text, toff = _batch_case(4000, seed=21)
+    count = toff.size - 1
+    rng = np.random.default_rng(21)
+    variants = {"clean": text.copy()}
+    t = text.copy()
+    for s in rng.choice(count, 40, replace=False):  # non-alphabet bytes anywhere
+        L = toff[s + 1] - toff[s]
+        t[toff[s] + rng.integers(0, L)] = ord("*")
+    variants["badchar"] = t
+    t = text.copy()
+    for s in rng.choice(count, 7, replace=False):  # '=' inside a string: misplaced pad
+        L = toff[s + 1] - toff[s]
+        if L >= 8:
+            t[toff[s] + rng.integers(0, L - 4)] = ord("=")
+    variants["pad_inside"] = t
+    t = text.copy()
+    for s in rng.choice(count, 60, replace=False):  # final-quad forms: x=yy, xx=y, non-canonical
+        e = toff[s + 1]
+        k = int(rng.integers(0, 3))
+        if k == 0:
+            t[e - 3] = ord("=")
+        elif k == 1:
+            t[e - 2] = ord("=")
+        else:
+            t[e - 2], t[e - 1] = ord("B"), ord("=")  # 'xxB=': non-canonical (B = 1)
+    variants["final_forms"] = t
+    toff_d = torch.from_numpy(toff).to(DEV)
+    for name, tv in variants.items():
+        rout, roff, rst, rerr, rlen = oracle.decode_batch(tv, toff, lenient=lenient)
+        td = torch.from_numpy(tv).to(DEV)
+        res = {}
+        for fast in (True, False):
+            out, oo, st, err, olen = b64.decode_batch(td, toff_d, a, fast=fast)
+            res[fast] = (st.cpu().numpy(), err.cpu().numpy(), olen.cpu().numpy(), out.cpu().numpy())
+            assert np.array_equal(res[fast][0], rst), (name, fast)
+            assert np.array_equal(res[fast][1], rerr), (name, fast)
+            assert np.array_equal(res[fast][2], rlen), (name, fast)
+            o = res[fast][3]
+            ok = np.nonzero(rlen > 0)[0]
+            for s in ok[::13]:
+                assert np.array_equal(o[roff[s]: roff[s] + rlen[s]], rout[roff[s]: roff[s] + rlen[s]]), (name, s)
+            # every string's exact bytes, gathered: the first and the last exact byte
+            assert np.array_equal(o[roff[ok]], rout[roff[ok]]), name
+            assert np.array_equal(o[roff[ok] + rlen[ok] - 1], rout[roff[ok] + rlen[ok] - 1]), name
+
+
+def test_batch_fast_path_ineligible_layouts(b64):
+    """Layouts the concatenation path must refuse (the per-string kernel runs): a length not a
+    multiple of 4, a gap in the output offsets, a misaligned first string; empty strings and a
+    batch of only empty strings; repeated calls reuse the cached context."""
+    text, toff = _batch_case(3000, seed=22)
+    cases = []
+    t2 = np.concatenate([text[: toff[100]], np.frombuffer(b"QUJD", np.uint8)[:3], text[toff[100]:]])
+    o2 = np.concatenate([toff[:101], toff[100:] + 3])
+    cases.append(("len%4", t2, o2, None))
+    _, doff, *_ = oracle.decode_batch(text, toff)
+    gap = doff.copy()
+    gap[1500:] += 16
+    cases.append(("gap", text, toff, gap))
+    t3 = np.concatenate([np.zeros(4, np.uint8), text])
+    cases.append(("misaligned", t3, toff + 4, None))
+    Lz = np.diff(toff).copy()
+    Lz[::5] = 0
+    tz = np.concatenate([text[toff[i]: toff[i] + Lz[i]] for i in range(Lz.size)])
+    cases.append(("empties", tz, synth.offsets(Lz), None))
+    cases.append(("all_empty", np.zeros(0, np.uint8), np.zeros(11, np.int64), None))
+    for name, tv, off, oo in cases:
+        rout, roff, rst, rerr, rlen = oracle.decode_batch(tv, off)
+        for rep in range(2):
+            kw = {}
+            if oo is not None:
+                kw = dict(out_off=torch.from_numpy(oo).to(DEV), total_out=int(oo[-1]) + 64)
+            out, ooo, st, err, olen = b64.decode_batch(torch.from_numpy(tv).to(DEV), torch.from_numpy(off).to(DEV), **kw)
+            assert np.array_equal(st.cpu().numpy(), rst), name
+            assert np.array_equal(err.cpu().numpy(), rerr), name
+            assert np.array_equal(olen.cpu().numpy(), rlen), name
+            o = out.cpu().numpy()
+            base = oo if oo is not None else roff
+            for s in np.nonzero(rlen > 0)[0][::29]:
+                assert np.array_equal(o[base[s]: base[s] + rlen[s]], rout[roff[s]: roff[s] + rlen[s]]), (name, s)
