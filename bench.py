@@ -685,6 +685,9 @@ def scale_rows(b64, synth, torch, dev, world, rank, flush, args, peak):
         td_k, td_full = timed(dec, reps)
         got = int(eo.item())
         assert got == expected, (got, expected)
+        cp = torch.empty_like(t)  # the paper's yardstick: a D2D copy of the same base64 bytes
+        tm_k, _ = timed(lambda ev: (cp.copy_(t), ev.record(stream)), reps)
+        del cp
         out_bytes = int(olen.item()) if expected < 0 else ds.out_len  # bytes the kernel wrote
         row = {"n_bytes": N, "base64_bytes": m, "n_gpus": world, "bytes_per_rank": x.numel(),
                "encode_gbs": round(m / (te_k * 1e-3) / 1e9, 1),
@@ -693,6 +696,8 @@ def scale_rows(b64, synth, torch, dev, world, rank, flush, args, peak):
                "encode_ms": round(te_k, 4), "decode_ms_kernel": round(td_k, 4),
                "decode_ms_with_combine_nccl": round(td_full, 4),
                "first_error": got, "injected": inject,
+               "memcpy_d2d_ms": round(tm_k, 4), "decode_time_vs_memcpy": round(td_k / tm_k, 4),
+               "encode_time_vs_memcpy": round(te_k / tm_k, 4),
                "roofline_encode": roof("enc_fast_kernel<2>", x.numel() + t.numel(), te_k),
                "roofline_decode": roof("dec_fast_kernel<2>", t.numel() + out_bytes, td_k),
                "combine": ("none (1 rank)" if dist is None else

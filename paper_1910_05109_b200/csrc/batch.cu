@@ -9,7 +9,7 @@
 // runs the single-stream dec_fast loop (one LDG.256 per lane, shared-memory
 // re-layout, lane-linear stores) over the concatenation, and only the strings'
 // final quads -- the one place padding may appear (DESIGN.md
-// R6) -- get a per-string pass.  Five launches:
+// R6) -- get a per-string pass.  Six launches, three of them gated:
 //   1. dec_batch_prep_kernel   err[i] = none; checks the layout (len % 4, the
 //                              offsets, alignment) -> ctx->generic = 1 if not.
 //   2. dec_batch_bulk_kernel   the concatenation, every quad as interior, with
@@ -18,17 +18,19 @@
 //                              0x80 chars are reported per string, the '='
 //                              seen are counted.
 //   3. dec_batch_strfinal_kernel  per string: the final quad under R6 / R16
-//                              (bytes rewritten, errors reported) and the
-//                              count of '=' at len-2 / len-1; the last CTA
-//                              compares: more '=' seen than at final
+//                              (bytes rewritten), then status / err_off /
+//                              out_len / first failing string in final form;
+//                              and the count of '=' at len-2 / len-1.  The
+//                              last CTA compares: more '=' seen than at final
 //                              positions -> a pad is misplaced somewhere ->
-//                              ctx->generic = 1.
-//   4. dec_generic_kernel      only when ctx->generic: the exact per-string
-//                              decode (not eligible, or a misplaced '=').
-//   5. dec_batch_finalize_kernel  status / err_off / out_len per string; resets
-//                              the context for the next call.
-// Every position reported in steps 2-4 is a genuinely bad position under the
-// rules, so the per-string MIN is the first error whichever steps ran.
+//                              ctx->generic = 1 and the results are redone:
+//   4-6. dec_batch_init / dec_generic / dec_batch_finalize, each gated on
+//                              ctx->generic (they return at once otherwise):
+//                              the exact per-string decode of
+//                              b64_decode_batch_ex.  The finalize's last CTA
+//                              resets the context for the next call.
+// Every position reported in steps 2-3 is a genuinely bad position under the
+// rules, so the per-string MIN is the first error.
 #include "b64_device.cuh"
 
 namespace b64 {
@@ -65,7 +67,7 @@ __device__ __forceinline__ int64_t string_of(const int64_t* __restrict__ in_off,
 // Rare path: every string with a non-alphabet char among the nchar chars at p (absolute
 // input position P) gets its first such char (within the window) reported, relative to
 // the string's start.  The pad char is not reported here (step 3 / 4 decide it).
-__device__ __noinline__ void report_window(const uint8_t* p, int64_t P, int nchar, const uint8_t* __restrict__ lut,
+__device__ __forceinline__ void report_window(const uint8_t* p, int64_t P, int nchar, const uint8_t* __restrict__ lut,
                                            const int64_t* __restrict__ in_off, int64_t count,
                                            unsigned long long* __restrict__ cells) {
     int64_t send = INT64_MIN;
@@ -88,7 +90,7 @@ __device__ __forceinline__ uint32_t count_pads(const uint32_t (&x)[8], uint32_t 
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kBulkCtasPerSm)
 dec_batch_bulk_kernel(const uint8_t* __restrict__ in_base, const int64_t* __restrict__ in_off,
                       uint8_t* __restrict__ out_base, const int64_t* __restrict__ out_off, int64_t count, DecTab tab,
                       unsigned long long* __restrict__ cells, BatchCtx* ctx) {
@@ -181,10 +183,18 @@ dec_batch_bulk_kernel(const uint8_t* __restrict__ in_base, const int64_t* __rest
     if (lane == 0 && npad) atomicAdd(&ctx->eq, static_cast<unsigned long long>(npad));
 }
 
+// Step 3: one thread per string.  The final quad under R6 / R16 (valid: its 1-3 bytes
+// rewritten -- the bulk pass decoded it with the pad as a candidate value), then the
+// string's results in their final form: the first error is the MIN of what the bulk pass
+// reported and the final quad's verdict, out_len follows (b64_decode_ex rules), and the
+// batch's first failing string is folded in.  The last CTA compares the pad counts: a pad
+// anywhere but the last two chars of its string makes all of this provisional, and the
+// gated kernels after this one redo the batch per string.
 __global__ void __launch_bounds__(kThreads)
 dec_batch_strfinal_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off, uint8_t* __restrict__ out,
-                          const int64_t* __restrict__ out_off, int64_t count, DecTab tab,
-                          unsigned long long* __restrict__ cells, BatchCtx* ctx) {
+                          const int64_t* __restrict__ out_off, int64_t count, DecTab tab, int64_t* __restrict__ err,
+                          int32_t* __restrict__ status, int64_t* __restrict__ out_len, int64_t index_base,
+                          unsigned long long* first_bad, BatchCtx* ctx) {
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ unsigned long long s_sum[kThreads / 32];
     __shared__ bool s_last;
@@ -192,21 +202,48 @@ dec_batch_strfinal_kernel(const uint8_t* __restrict__ in, const int64_t* __restr
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     __syncthreads();
     griddep_wait();
-    if (ctx->generic) return;
+    if (ctx->generic) return;  // not eligible: the gated kernels do the batch
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
-    unsigned long long legit = 0;
+    uint32_t legit = 0;
+    int64_t bad_idx = INT64_MAX;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t a = in_off[i], L = in_off[i + 1] - a;
-        if (L < 4) continue;
-        const uint32_t x = ld32(in + a + L - 4);  // 4-byte aligned: the layout check passed
-        legit += uint32_t(((x >> 16) & 0xffu) == tab.pad) + uint32_t((x >> 24) == tab.pad);
-        int bad, k;
-        uint32_t v;
-        const uint32_t kind = final_quad(x, lut, tab.pad, tab.lenient, &bad, &k, &v);
-        if (kind == kOk) store_bytes(out + out_off[i] + 3 * ((L >> 2) - 1), v, k);
-        else atomicMin(&cells[i], pack_err(L - 4 + bad, kind));
+        unsigned long long w = static_cast<unsigned long long>(err[i]);  // the bulk pass's packed word
+        int64_t ol = 0;
+        if (L >= 4) {
+            const uint32_t x = ld32(in + a + L - 4);  // 4-byte aligned: the layout check passed
+            legit += uint32_t(((x >> 16) & 0xffu) == tab.pad) + uint32_t((x >> 24) == tab.pad);
+            int bad, k;
+            uint32_t v;
+            const uint32_t kind = final_quad(x, lut, tab.pad, tab.lenient, &bad, &k, &v);
+            if (kind == kOk) {
+                store_bytes(out + out_off[i] + 3 * ((L >> 2) - 1), v, k);
+                ol = 3 * ((L >> 2) - 1) + k;
+            } else {
+                const unsigned long long fw = pack_err(L - 4 + bad, kind);
+                w = fw < w ? fw : w;
+            }
+        }
+        int32_t st;
+        int64_t e;
+        if (w >= kErrNone) {
+            st = kOk; e = -1;
+        } else {
+            e = int64_t(w >> 3); st = int32_t(w & 7); ol = 3 * (e >> 2);
+            if (bad_idx == INT64_MAX) bad_idx = index_base + i;  // i only grows per thread
+        }
+        err[i] = e;
+        if (status) status[i] = st;
+        if (out_len) out_len[i] = ol;
     }
-    legit = __reduce_add_sync(kFull, unsigned(legit));  // < 2^32 per warp
+    if (first_bad) {  // the batch's first failing string: warp MIN, one atomic per warp
+        const unsigned long long b = static_cast<unsigned long long>(bad_idx);
+        const unsigned hi = __reduce_min_sync(kFull, unsigned(b >> 32));
+        const unsigned lo_min = __reduce_min_sync(kFull, unsigned(b >> 32) == hi ? unsigned(b) : ~0u);
+        if ((threadIdx.x & 31) == 0 && hi != 0x7FFFFFFFu)
+            atomicMin(first_bad, (static_cast<unsigned long long>(hi) << 32) | lo_min);
+    }
+    legit = __reduce_add_sync(kFull, legit);  // < 2^32 per warp
     if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = legit;
     __syncthreads();
     if (threadIdx.x == 0) {

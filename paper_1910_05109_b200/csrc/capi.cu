@@ -877,13 +877,15 @@ int b64_decode_batch_fast(const uint8_t* d_in, const int64_t* d_in_off, int64_t 
         launch(dec_batch_bulk_kernel<2>, int64_t(di->sms) * cap_bps(di->occ_batch_bulk), kThreads, s, d_in, d_in_off,
                d_out, d_out_off, count, bt, cells, ctx);
         if ((r = launched()) != B64_OK) return r;
-        launch(dec_batch_strfinal_kernel, small, kThreads, s, d_in, d_in_off, d_out, d_out_off, count, dec_tab(a),
-               cells, ctx);
-        if ((r = launched()) != B64_OK) return r;
-    } else {
-        launch(dec_batch_init_kernel, small, kThreads, s, d_err_off, count);
+        const int64_t per = clamp_grid((count + kThreads - 1) / kThreads, INT32_MAX);  // one string per thread
+        launch(dec_batch_strfinal_kernel, per, kThreads, s, d_in, d_in_off, d_out, d_out_off, count, dec_tab(a),
+               d_err_off, d_status, d_out_len, index_base, reinterpret_cast<unsigned long long*>(d_first_bad), ctx);
         if ((r = launched()) != B64_OK) return r;
     }
+    // the per-string path (b64_decode_batch_ex); with a context every kernel is gated on
+    // ctx->generic and returns at once when the concatenation path finished the batch
+    launch(dec_batch_init_kernel, small, kThreads, s, d_err_off, count, static_cast<const BatchCtx*>(ctx));
+    if ((r = launched()) != B64_OK) return r;
     Offsets off{d_in_off, d_out_off, count, 0};
     const int64_t blocks = int64_t(di->sms) * di->occ_dec_gen;
     launch(dec_generic_kernel, blocks, kThreads, s, d_in, d_out, off, dec_tab(a), 0, 1, cells, nullptr,

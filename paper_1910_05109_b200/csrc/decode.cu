@@ -556,8 +556,9 @@ __global__ void dec_finalize_len_kernel(const int64_t* cell, int64_t* err_off, i
     }
 }
 
-__global__ void dec_batch_init_kernel(int64_t* err, int64_t count) {
+__global__ void dec_batch_init_kernel(int64_t* err, int64_t count, const BatchCtx* gate) {
     griddep_wait();
+    if (gate && !gate->generic) return;  // the concatenation path finished the batch (batch.cu)
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
         err[i] = int64_t(kErrNone);
 }
@@ -565,10 +566,20 @@ __global__ void dec_batch_init_kernel(int64_t* err, int64_t count) {
 __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
                                           int64_t count, uint32_t pad, int32_t* status, int64_t* err,
                                           int64_t* out_len, int64_t index_base, unsigned long long* first_bad,
-                                          BatchCtx* reset) {
+                                          BatchCtx* ctx) {
     griddep_wait();
-    if (reset && blockIdx.x == 0 && threadIdx.x < sizeof(BatchCtx) / 4)
-        reinterpret_cast<uint32_t*>(reset)[threadIdx.x] = 0;  // ready for the next call
+    if (ctx) {  // gated (batch.cu): only after the generic kernel ran; the last CTA resets the context
+        __shared__ bool s_last;
+        const bool run = ctx->generic != 0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&ctx->reserved[0], 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last && threadIdx.x < sizeof(BatchCtx) / 4) reinterpret_cast<uint32_t*>(ctx)[threadIdx.x] = 0;
+        if (!run) return;
+    }
     int64_t bad = INT64_MAX;  // this thread's first failing string (index_base + i)
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t a = in_off[i], L = in_off[i + 1] - a;
