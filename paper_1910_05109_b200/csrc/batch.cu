@@ -183,7 +183,7 @@ dec_batch_bulk_kernel(const uint8_t* __restrict__ in_base, const int64_t* __rest
     if (lane == 0 && npad) atomicAdd(&ctx->eq, static_cast<unsigned long long>(npad));
 }
 
-// Step 3: one thread per string.  The final quad under R6 / R16 (valid: its 1-3 bytes
+// Step 3: one thread per string.  The final quad under R6 / R16 (lenient: its 1-3 bytes
 // rewritten -- the bulk pass decoded it with the pad as a candidate value), then the
 // string's results in their final form: the first error is the MIN of what the bulk pass
 // reported and the final quad's verdict, out_len follows (b64_decode_ex rules), and the
@@ -217,7 +217,10 @@ dec_batch_strfinal_kernel(const uint8_t* __restrict__ in, const int64_t* __restr
             uint32_t v;
             const uint32_t kind = final_quad(x, lut, tab.pad, tab.lenient, &bad, &k, &v);
             if (kind == kOk) {
-                store_bytes(out + out_off[i] + 3 * ((L >> 2) - 1), v, k);
+                // strict: the bulk pass already wrote the exact bytes -- a canonical final quad's
+                // dropped bits are zero, so the pad candidate (0x40 = 1 << 6) only sets a bit of
+                // a discarded byte; lenient: non-zero dropped bits can carry into a kept byte
+                if (tab.lenient) store_bytes(out + out_off[i] + 3 * ((L >> 2) - 1), v, k);
                 ol = 3 * ((L >> 2) - 1) + k;
             } else {
                 const unsigned long long fw = pack_err(L - 4 + bad, kind);

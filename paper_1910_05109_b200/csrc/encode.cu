@@ -242,18 +242,62 @@ __device__ __forceinline__ void enc_short_lane(const uint8_t* __restrict__ src, 
     }
 }
 
+// Per-warp work lists of enc_generic_kernel (one 32-string batch at a time): the
+// 24-byte units of the batch's long strings, flattened into one index space so the
+// warp's lanes stay busy across string boundaries and the next unit's loads are in
+// flight while the current one is encoded; then the scalar triples (heads, tails and
+// padded partial triples) flattened the same way.
+struct EncWarpList {
+    int64_t pre[33];  // exclusive prefix of per-string item counts; pre[32] = total
+    int64_t src[32];  // units: input offset of the string's first unit in range; scalars: string start
+    int64_t dst[32];  // units: its output offset;  scalars: output offset of the string
+    int32_t h[32];    // scalars: head triples, then the first tail triple and T (packed below)
+    int32_t t0[32];
+    int32_t T[32];
+};
+
+// Last i in [0, 32) with pre[i] <= j (the owner of item j; empty strings are skipped).
+__device__ __forceinline__ int owner_of(const int64_t* pre, int64_t j) {
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1)
+        if (pre[lo + step] <= j) lo += step;
+    return lo;
+}
+
+__device__ __forceinline__ int64_t warp_exclusive_scan(int64_t v, int lane, int64_t* total) {
+    int64_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int64_t y = __shfl_up_sync(kFull, x, d);
+        if (lane >= d) x += y;
+    }
+    *total = __shfl_sync(kFull, x, 31);
+    return x - v;
+}
+
 // Any alignment, one stream or a batch.  The concatenated input is cut into
 // equal byte ranges, one per warp; a warp owns every work item whose first
-// input byte lies in its range.  Per string with a 4-byte-aligned output
-// (always the case for batches, whose output offsets are multiples of 4):
-//   * h < 8 head triples, one per lane, bring the output to a 32-byte boundary;
-//   * then units of 8 triples (24 bytes, read at any alignment as 8-byte-aligned
-//     LDG.64 + funnel shifts) -> 32 chars, one lane-linear-ish STG.256 each, the
-//     same per-lane code as enc_fast_kernel;
-//   * the < 8 leftover triples and the padded tail, one per lane.
-__global__ void __launch_bounds__(kThreads)
+// input byte lies in its range.  Strings are visited 32 at a time (lane i
+// holds string s0 + i's offsets):
+//   * a short string (<= kShortEnc bytes) is encoded whole by its own lane;
+//   * the long ones (output 4-byte aligned: always in a batch, whose output
+//     offsets are multiples of 4) are split into h < 8 head triples that
+//     bring the output to a 32-byte boundary, units of 8 triples (24 bytes,
+//     read at any alignment as 8-byte-aligned LDG.64 + funnel shifts) -> 32
+//     chars with one STG.256 (the same per-lane code as enc_fast_kernel), and
+//     the < 8 tail triples + the padded partial triple; the units of all the
+//     batch's long strings form ONE flattened list the warp sweeps with a
+//     one-unit-ahead prefetch, the scalar triples a second one;
+//   * a long string with a misaligned output (single-stream API only) takes
+//     the byte-store path.
+#ifndef B64_ENC_GEN_MINB
+#define B64_ENC_GEN_MINB 5
+#endif
+__global__ void __launch_bounds__(kThreads, B64_ENC_GEN_MINB)
 enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab, uint32_t pad) {
     __shared__ __align__(64) uint32_t s_lut[16];
+    __shared__ EncWarpList s_list[kThreads / 32];
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
@@ -264,6 +308,7 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
     const uint32_t lb = smem_u32(s_lut);
 
     const int lane = threadIdx.x & 31;
+    EncWarpList& wl = s_list[threadIdx.x >> 5];
     const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
     const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t base = off.in(0);
@@ -273,65 +318,108 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
     const int64_t hi = base + (total * (w + 1)) / W;
     if (lo >= hi) return;
 
-    // Strings are visited 32 at a time (lane i holds string s0 + i's offsets): a short string
-    // (<= kShortEnc bytes) is encoded whole by its own lane -- by the warp whose range holds
-    // its first byte -- and the longer ones one after the other by the whole warp (every
-    // unit whose first byte lies in [lo, hi)).
     for (int64_t s0 = first_string_ending_after(off, lo); s0 < off.count; s0 += 32) {
-      const int64_t si = s0 + lane;
-      const bool valid = si < off.count;
-      int64_t ai = 0, Li = 0, obi = 0;
-      if (valid) {
-          ai = off.in(si);
-          Li = off.in(si + 1) - ai;
-          obi = off.out(si);
-      }
-      const bool started = valid && ai < hi;  // strings from hi on belong to later warps
-      if (started && Li > 0 && Li <= kShortEnc && ai >= lo) enc_short_lane(in + ai, Li, out + obi, lut, pad);
-      for (uint32_t longs = __ballot_sync(kFull, started && Li > kShortEnc); longs; longs &= longs - 1) {
-        const int jl = __ffs(longs) - 1;
-        const int64_t a = __shfl_sync(kFull, ai, jl);
-        const int64_t L = __shfl_sync(kFull, Li, jl);
-        const int64_t ob = __shfl_sync(kFull, obi, jl);
-        uint8_t* o = out + ob;
-        const uintptr_t oa = reinterpret_cast<uintptr_t>(o);
-        if (oa & 3) {
-            enc_string_unaligned_out(in, out, a, L, ob, lo, hi, lane, lut, pad);
-            continue;  // next long string
+        const int64_t si = s0 + lane;
+        const bool valid = si < off.count;
+        int64_t ai = 0, Li = 0, obi = 0;
+        if (valid) {
+            ai = off.in(si);
+            Li = off.in(si + 1) - ai;
+            obi = off.out(si);
         }
-        const int64_t T = L / 3;
-        const int r = int(L - 3 * T);
-        const int64_t h = min(T, int64_t(((32 - (oa & 31)) & 31) >> 2));
-        const int64_t U = (T - h) >> 3;
-        const int64_t ua = a + 3 * h;
-        const int64_t kb = lo > ua ? (lo - ua + 23) / 24 : 0;
-        const int64_t ke = min(U, (hi - ua + 23) / 24);
-        for (int64_t k = kb + lane; k < ke; k += 32) {
+        const bool started = valid && ai < hi;  // strings from hi on belong to later warps
+        if (started && Li > 0 && Li <= kShortEnc && ai >= lo) enc_short_lane(in + ai, Li, out + obi, lut, pad);
+        const bool lng = started && Li > kShortEnc;
+        const bool lng_al = lng && ((reinterpret_cast<uintptr_t>(out + obi) & 3) == 0);
+        // this lane's long string: units [kb, ke) whose first byte lies in [lo, hi)
+        int64_t nu = 0, src = 0, dst = 0, ns = 0;
+        int32_t h = 0, t0 = 0, T = 0;
+        if (lng_al) {
+            const uintptr_t oa = reinterpret_cast<uintptr_t>(out + obi);
+            T = int32_t(Li / 3);
+            const int r = int(Li - 3 * int64_t(T));
+            h = int32_t(min(int64_t(T), int64_t(((32 - (oa & 31)) & 31) >> 2)));
+            const int64_t U = (T - h) >> 3;
+            const int64_t ua = ai + 3 * h;
+            const int64_t kb = lo > ua ? (lo - ua + 23) / 24 : 0;
+            const int64_t ke = min(U, (hi - ua + 23) / 24);
+            nu = ke > kb ? ke - kb : 0;
+            src = ua + 24 * kb;
+            dst = obi + 4 * h + 32 * kb;
+            t0 = int32_t(h + 8 * U);
+            ns = h + (T - t0) + (r > 0 ? 1 : 0);  // scalar triples (range-checked per item)
+        }
+        int64_t nu_all;
+        const int64_t pre = warp_exclusive_scan(nu, lane, &nu_all);
+        wl.pre[lane] = pre;
+        wl.src[lane] = src;
+        wl.dst[lane] = dst;
+        if (lane == 31) wl.pre[32] = nu_all;
+        __syncwarp();
+        // flattened units of the batch's long strings, one unit ahead in flight
+        int64_t j = lane;
+        uint32_t nx[6];
+        int64_t ndst = 0;
+        if (j < nu_all) {
+            const int o = owner_of(wl.pre, j);
+            ld24_unaligned(in + wl.src[o] + 24 * (j - wl.pre[o]), nx);
+            ndst = wl.dst[o] + 32 * (j - wl.pre[o]);
+        }
+        for (; j < nu_all; j += 32) {
             uint32_t wv[6], ov[8];
-            ld24_unaligned(in + ua + 24 * k, wv);  // (2-3 LDG.128 instead: configs[3] encode -11 %)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) wv[q] = nx[q];
+            const int64_t cdst = ndst;
+            const int64_t jn = j + 32;
+            if (jn < nu_all) {
+                const int o = owner_of(wl.pre, jn);
+                ld24_unaligned(in + wl.src[o] + 24 * (jn - wl.pre[o]), nx);
+                ndst = wl.dst[o] + 32 * (jn - wl.pre[o]);
+            }
             enc_lane_compute(wv, ov, lb);
-            st256(o + 4 * h + 32 * k, ov);
+            st256(out + cdst, ov);
         }
-        // scalar triples: head [0, h), tail [h + 8U, T), and the padded partial triple T
-        const int64_t t0 = h + 8 * U;
-        const int nsc = int(h + (T - t0) + (r > 0 ? 1 : 0));
-        if (lane < nsc) {
-            const int64_t j = lane < h ? int64_t(lane) : t0 + (lane - h);
-            const int64_t p = a + 3 * j;
+        __syncwarp();
+        // flattened scalar triples: head [0, h), tail [t0, T), and the padded partial triple T
+        int64_t ns_all;
+        const int64_t spre = warp_exclusive_scan(ns, lane, &ns_all);
+        wl.pre[lane] = spre;
+        wl.src[lane] = ai;
+        wl.dst[lane] = obi;
+        wl.h[lane] = h;
+        wl.t0[lane] = t0;
+        wl.T[lane] = T;
+        if (lane == 31) wl.pre[32] = ns_all;
+        __syncwarp();
+        for (int64_t k = lane; k < ns_all; k += 32) {
+            const int o = owner_of(wl.pre, k);
+            const int32_t t = int32_t(k - wl.pre[o]);
+            const int32_t ho = wl.h[o], To = wl.T[o];
+            const int64_t tri = t < ho ? t : int64_t(wl.t0[o]) + (t - ho);  // == To for the partial triple
+            const int64_t p = wl.src[o] + 3 * tri;
             if (p >= lo && p < hi) {
-                const uint8_t* src = in + p;
+                const uint8_t* sp = in + p;
                 uint32_t word;
-                if (j < T) {
-                    word = enc_triple((uint32_t(src[0]) << 24) | (uint32_t(src[1]) << 16) | (uint32_t(src[2]) << 8),
-                                      lut);
+                if (tri < To) {
+                    word = enc_triple((uint32_t(sp[0]) << 24) | (uint32_t(sp[1]) << 16) | (uint32_t(sp[2]) << 8), lut);
                 } else {
-                    word = enc_partial(src[0], r == 2 ? src[1] : 0u, r, lut, pad);
+                    const int64_t L = off.in(s0 + o + 1) - wl.src[o];
+                    const int r = int(L - 3 * int64_t(To));
+                    word = enc_partial(sp[0], r == 2 ? sp[1] : 0u, r, lut, pad);
                 }
-                *reinterpret_cast<uint32_t*>(o + 4 * j) = word;
+                *reinterpret_cast<uint32_t*>(out + wl.dst[o] + 4 * tri) = word;
             }
         }
-      }
-      if (__any_sync(kFull, !started)) break;  // a string at or after hi (or the end): done
+        __syncwarp();
+        // long strings with a misaligned output (single-stream API): byte-granular path
+        for (uint32_t mis = __ballot_sync(kFull, lng && !lng_al); mis; mis &= mis - 1) {
+            const int jl = __ffs(mis) - 1;
+            const int64_t a = __shfl_sync(kFull, ai, jl);
+            const int64_t L = __shfl_sync(kFull, Li, jl);
+            const int64_t ob = __shfl_sync(kFull, obi, jl);
+            enc_string_unaligned_out(in, out, a, L, ob, lo, hi, lane, lut, pad);
+        }
+        if (__any_sync(kFull, !started)) break;  // a string at or after hi (or the end): done
     }
 }
 
