@@ -256,13 +256,27 @@ struct EncWarpList {
     int32_t T[32];
 };
 
-// Last i in [0, 32) with pre[i] <= j (the owner of item j; empty strings are skipped).
-__device__ __forceinline__ int owner_of(const int64_t* pre, int64_t j) {
-    int lo = 0;
+// The loads of one 24-byte unit at any alignment (the LDG.64 half of ld24_unaligned),
+// kept raw so they can be issued one unit ahead; fix24 does the select / funnel half.
+struct Raw24 {
+    uint2 a, b, c, d;
+    uint32_t sb;
+};
+__device__ __forceinline__ void ld24_raw(const uint8_t* p, Raw24& r) {
+    const uintptr_t u = reinterpret_cast<uintptr_t>(p);
+    const uint2* pa = reinterpret_cast<const uint2*>(u & ~uintptr_t(7));
+    r.sb = uint32_t(u & 7);
+    r.a = ld64_l1(pa);
+    r.b = ld64_l1(pa + 1);
+    r.c = ld64_l1(pa + 2);
+    r.d = r.sb ? ld64_l1(pa + 3) : make_uint2(0u, 0u);
+}
+__device__ __forceinline__ void fix24(const Raw24& r, uint32_t (&w)[6]) {
+    const uint32_t v[8] = {r.a.x, r.a.y, r.b.x, r.b.y, r.c.x, r.c.y, r.d.x, r.d.y};
+    const bool ws = r.sb >= 4;
+    const uint32_t sh = (r.sb & 3) * 8;
 #pragma unroll
-    for (int step = 16; step >= 1; step >>= 1)
-        if (pre[lo + step] <= j) lo += step;
-    return lo;
+    for (int i = 0; i < 6; ++i) w[i] = __funnelshift_r(ws ? v[i + 1] : v[i], ws ? v[i + 2] : v[i + 1], sh);
 }
 
 __device__ __forceinline__ int64_t warp_exclusive_scan(int64_t v, int lane, int64_t* total) {
@@ -356,26 +370,28 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
         wl.dst[lane] = dst;
         if (lane == 31) wl.pre[32] = nu_all;
         __syncwarp();
-        // flattened units of the batch's long strings, one unit ahead in flight
+        // flattened units of the batch's long strings, one unit ahead in flight; each lane's
+        // owner string only moves forward (j grows), so it is tracked, not searched
         int64_t j = lane;
-        uint32_t nx[6];
+        int o = 0;
+        Raw24 nr;
         int64_t ndst = 0;
         if (j < nu_all) {
-            const int o = owner_of(wl.pre, j);
-            ld24_unaligned(in + wl.src[o] + 24 * (j - wl.pre[o]), nx);
+            while (wl.pre[o + 1] <= j) ++o;
+            ld24_raw(in + wl.src[o] + 24 * (j - wl.pre[o]), nr);
             ndst = wl.dst[o] + 32 * (j - wl.pre[o]);
         }
         for (; j < nu_all; j += 32) {
-            uint32_t wv[6], ov[8];
-#pragma unroll
-            for (int q = 0; q < 6; ++q) wv[q] = nx[q];
+            const Raw24 cr = nr;
             const int64_t cdst = ndst;
             const int64_t jn = j + 32;
             if (jn < nu_all) {
-                const int o = owner_of(wl.pre, jn);
-                ld24_unaligned(in + wl.src[o] + 24 * (jn - wl.pre[o]), nx);
+                while (wl.pre[o + 1] <= jn) ++o;
+                ld24_raw(in + wl.src[o] + 24 * (jn - wl.pre[o]), nr);
                 ndst = wl.dst[o] + 32 * (jn - wl.pre[o]);
             }
+            uint32_t wv[6], ov[8];
+            fix24(cr, wv);
             enc_lane_compute(wv, ov, lb);
             st256(out + cdst, ov);
         }
@@ -391,8 +407,10 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
         wl.T[lane] = T;
         if (lane == 31) wl.pre[32] = ns_all;
         __syncwarp();
+        int os = 0;
         for (int64_t k = lane; k < ns_all; k += 32) {
-            const int o = owner_of(wl.pre, k);
+            while (wl.pre[os + 1] <= k) ++os;
+            const int o = os;
             const int32_t t = int32_t(k - wl.pre[o]);
             const int32_t ho = wl.h[o], To = wl.T[o];
             const int64_t tri = t < ho ? t : int64_t(wl.t0[o]) + (t - ho);  // == To for the partial triple
