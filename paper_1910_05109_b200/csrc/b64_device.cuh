@@ -339,7 +339,7 @@ struct BatchCtx {
     uint32_t ticket;           // strfinal's last-CTA ticket
     unsigned long long eq;     // pad chars the bulk pass saw
     unsigned long long legit;  // pad chars at positions len-2 / len-1 of the strings
-    uint32_t reserved[2];      // [0]: the fallback kernel's last-CTA ticket
+    uint32_t reserved[2];      // [0]: the gated finalize's last-CTA ticket
 };
 static_assert(sizeof(BatchCtx) == 32, "B64_BATCH_CTX_BYTES");
 
@@ -367,7 +367,8 @@ __global__ void dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8
                                 int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev, StreamJoin join);
 __global__ void dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off,
                                    DecTab tab, int64_t base, int is_final_single,
-                                   unsigned long long* __restrict__ err_cells, int64_t* __restrict__ out_len_single);
+                                   unsigned long long* __restrict__ err_cells, int64_t* __restrict__ out_len_single,
+                                   const BatchCtx* gate);
 __global__ void dec_small_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                                  int64_t* __restrict__ err_off, int32_t* __restrict__ status,
                                  int64_t* __restrict__ out_len);
@@ -379,9 +380,10 @@ __global__ void dec_finalize_unpadded_kernel(int64_t* err_off, int32_t* status, 
 __global__ void dec_finalize_packed_kernel(const int64_t* cell, int64_t* err_off, int32_t* status);
 __global__ void dec_finalize_len_kernel(const int64_t* cell, int64_t* err_off, int32_t* status, int64_t* out_len,
                                         int64_t out_base);
-__global__ void dec_batch_init_kernel(int64_t* err, int64_t count);
+__global__ void dec_batch_init_kernel(int64_t* err, int64_t count, const BatchCtx* gate);
 __global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
                                           int64_t count, uint32_t pad, int32_t* status, int64_t* err,
-                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad);
+                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad,
+                                          BatchCtx* ctx);
 
 }  // namespace b64

@@ -28,7 +28,7 @@ struct DevInfo {
     int sms = 0;
     int occ_group[4] = {0, 0, 0, 0};  // min over the enc / dec / codec group kernels
     int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_enc_gen = 0, occ_dec_gen = 0;
-    int occ_batch_main = 0, occ_batch_fb = 0;
+    int occ_batch_bulk = 0;
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -68,8 +68,7 @@ const DevInfo* dev_info() {
         group_occupancy(info.occ_group) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_batch_main, dec_batch_main_kernel<2>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_batch_fb, dec_batch_fallback_kernel, kThreads, 0))
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_batch_bulk, dec_batch_bulk_kernel<2>, kThreads, 0))
         return nullptr;
     for (int i = 0; i < 4; ++i) {
         info.occ_enc_fast[i] = info.occ_enc_fast[i] < 1 ? 1 : info.occ_enc_fast[i];
@@ -78,8 +77,7 @@ const DevInfo* dev_info() {
     }
     info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
     info.occ_dec_gen = info.occ_dec_gen < 1 ? 1 : info.occ_dec_gen;
-    info.occ_batch_main = info.occ_batch_main < 1 ? 1 : info.occ_batch_main;
-    info.occ_batch_fb = info.occ_batch_fb < 1 ? 1 : info.occ_batch_fb;
+    info.occ_batch_bulk = info.occ_batch_bulk < 1 ? 1 : info.occ_batch_bulk;
     if (cudaFuncSetAttribute(dec_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
         cudaFuncSetAttribute(ws_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         return nullptr;
@@ -144,25 +142,6 @@ void launch(void (*kernel)(KArgs...), int64_t grid, int block, cudaStream_t s, A
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    note(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
-}
-
-// A cooperative launch (every CTA co-resident; the kernel synchronises its grid with
-// cooperative_groups grid barriers), PDL allowed as for launch().
-template <typename... KArgs, typename... Args>
-void launch_coop(void (*kernel)(KArgs...), int64_t grid, int block, cudaStream_t s, Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(unsigned(block));
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     note(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
 }
 
@@ -384,7 +363,8 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
     } else {
         Offsets off{nullptr, nullptr, 1, m};
         const int64_t blocks = clamp_grid((m / 16 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_gen);
-        launch(dec_generic_kernel, blocks, kThreads, s, d_in, d_out, off, dec_tab(a), base, is_final, c, out_len);
+        launch(dec_generic_kernel, blocks, kThreads, s, d_in, d_out, off, dec_tab(a), base, is_final, c, out_len,
+               static_cast<const BatchCtx*>(nullptr));
     }
     return launched();
 }
@@ -887,27 +867,32 @@ int b64_decode_batch_fast(const uint8_t* d_in, const int64_t* d_in_off, int64_t 
     const int64_t small = clamp_grid((count + kThreads - 1) / kThreads, int64_t(di->sms) * 8);
     int r;
     if (ctx) {
-        // the concatenation path (batch.cu): two cooperative launches, every CTA resident
+        // the concatenation path (batch.cu): layout check, bulk, final quads; the generic
+        // kernel below then only runs when the layout is not eligible or a pad is misplaced
+        launch(dec_batch_prep_kernel, small, kThreads, s, d_in, d_in_off, static_cast<const uint8_t*>(d_out),
+               d_out_off, count, d_err_off, ctx);
+        if ((r = launched()) != B64_OK) return r;
         DecTab bt = dec_tab(a);
         reinterpret_cast<uint8_t*>(bt.w)[a->pad] = uint8_t(kPadCand);
-        launch_coop(dec_batch_main_kernel<2>, int64_t(di->sms) * di->occ_batch_main, kThreads, s, d_in, d_in_off,
-                    d_out, d_out_off, count, bt, dec_tab(a), d_err_off, d_status, d_out_len, index_base,
-                    reinterpret_cast<unsigned long long*>(d_first_bad), ctx);
+        launch(dec_batch_bulk_kernel<2>, int64_t(di->sms) * cap_bps(di->occ_batch_bulk), kThreads, s, d_in, d_in_off,
+               d_out, d_out_off, count, bt, cells, ctx);
         if ((r = launched()) != B64_OK) return r;
-        launch_coop(dec_batch_fallback_kernel, int64_t(di->sms) * di->occ_batch_fb, kThreads, s, d_in, d_in_off,
-                    d_out, d_out_off, count, dec_tab(a), d_err_off, d_status, d_out_len, index_base,
-                    reinterpret_cast<unsigned long long*>(d_first_bad), ctx);
-        return launched();
+        const int64_t per = clamp_grid((count + kThreads - 1) / kThreads, INT32_MAX);  // one string per thread
+        launch(dec_batch_strfinal_kernel, per, kThreads, s, d_in, d_in_off, d_out, d_out_off, count, dec_tab(a),
+               d_err_off, d_status, d_out_len, index_base, reinterpret_cast<unsigned long long*>(d_first_bad), ctx);
+        if ((r = launched()) != B64_OK) return r;
     }
-    // the per-string path (b64_decode_batch_ex)
-    launch(dec_batch_init_kernel, small, kThreads, s, d_err_off, count);
+    // the per-string path (b64_decode_batch_ex); with a context every kernel is gated on
+    // ctx->generic and returns at once when the concatenation path finished the batch
+    launch(dec_batch_init_kernel, small, kThreads, s, d_err_off, count, static_cast<const BatchCtx*>(ctx));
     if ((r = launched()) != B64_OK) return r;
     Offsets off{d_in_off, d_out_off, count, 0};
     const int64_t blocks = int64_t(di->sms) * di->occ_dec_gen;
-    launch(dec_generic_kernel, blocks, kThreads, s, d_in, d_out, off, dec_tab(a), 0, 1, cells, nullptr);
+    launch(dec_generic_kernel, blocks, kThreads, s, d_in, d_out, off, dec_tab(a), 0, 1, cells, nullptr,
+           static_cast<const BatchCtx*>(ctx));
     if ((r = launched()) != B64_OK) return r;
     launch(dec_batch_finalize_kernel, small, kThreads, s, d_in, d_in_off, count, a->pad, d_status,
-           d_err_off, d_out_len, index_base, reinterpret_cast<unsigned long long*>(d_first_bad));
+           d_err_off, d_out_len, index_base, reinterpret_cast<unsigned long long*>(d_first_bad), ctx);
     return launched();
 }
 

@@ -333,15 +333,22 @@ __device__ __forceinline__ void dec_short_lane(const uint8_t* __restrict__ src, 
 #ifndef B64_GEN_MINB
 #define B64_GEN_MINB 5
 #endif
-// The body of dec_generic_kernel as run by warp w of W (also inlined into the batch's
-// cooperative fallback kernel, batch.cu); lut / lb: the CTA's shared copy of tab.
-__device__ __forceinline__ void dec_generic_body(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
-                                                 const Offsets& off, const DecTab& tab, const uint8_t* lut,
-                                                 uint32_t lb, int64_t base, int is_final_single,
-                                                 unsigned long long* __restrict__ err_cells,
-                                                 int64_t* __restrict__ out_len_single, int64_t w, int64_t W) {
+__global__ void __launch_bounds__(kThreads, B64_GEN_MINB)
+dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, DecTab tab,
+                   int64_t base, int is_final_single, unsigned long long* __restrict__ err_cells,
+                   int64_t* __restrict__ out_len_single, const BatchCtx* gate) {
+    __shared__ __align__(256) uint32_t s_lut[64];
+    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
     const bool batch = off.in_off != nullptr;
+    griddep_wait();
+    if (gate && !gate->generic) return;  // the batch's concatenation path did it all (batch.cu)
+
     const int lane = threadIdx.x & 31;
+    const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
 
     if (!batch && out_len_single && w == 0 && lane == 0) {
         // bytes written assuming the chunk is valid
@@ -459,19 +466,6 @@ __device__ __forceinline__ void dec_generic_body(const uint8_t* __restrict__ in,
     }
 }
 
-__global__ void __launch_bounds__(kThreads, B64_GEN_MINB)
-dec_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, DecTab tab,
-                   int64_t base, int is_final_single, unsigned long long* __restrict__ err_cells,
-                   int64_t* __restrict__ out_len_single) {
-    __shared__ __align__(256) uint32_t s_lut[64];
-    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
-    __syncthreads();
-    griddep_wait();
-    dec_generic_body(in, out, off, tab, reinterpret_cast<const uint8_t*>(s_lut), smem_u32(s_lut), base,
-                     is_final_single, err_cells, out_len_single,
-                     (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5, (int64_t(gridDim.x) * blockDim.x) >> 5);
-}
-
 // ---------------------------------------------------------------- finalize
 
 // Single stream: the cell IS *err_off (initialised to kErrNone by memset).
@@ -562,21 +556,32 @@ __global__ void dec_finalize_len_kernel(const int64_t* cell, int64_t* err_off, i
     }
 }
 
-__global__ void dec_batch_init_kernel(int64_t* err, int64_t count) {
+__global__ void dec_batch_init_kernel(int64_t* err, int64_t count, const BatchCtx* gate) {
     griddep_wait();
+    if (gate && !gate->generic) return;  // the concatenation path finished the batch (batch.cu)
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
         err[i] = int64_t(kErrNone);
 }
 
-// Per-string results from the error cells (b64_decode_ex rules; R12 LENGTH) and the batch's
-// first failing string, for threads gtid of gthreads (also inlined into batch.cu's fallback).
-__device__ __forceinline__ void dec_batch_finalize_body(const uint8_t* __restrict__ in,
-                                                        const int64_t* __restrict__ in_off, int64_t count,
-                                                        uint32_t pad, int32_t* status, int64_t* err, int64_t* out_len,
-                                                        int64_t index_base, unsigned long long* first_bad,
-                                                        int64_t gtid, int64_t gthreads) {
+__global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
+                                          int64_t count, uint32_t pad, int32_t* status, int64_t* err,
+                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad,
+                                          BatchCtx* ctx) {
+    griddep_wait();
+    if (ctx) {  // gated (batch.cu): only after the generic kernel ran; the last CTA resets the context
+        __shared__ bool s_last;
+        const bool run = ctx->generic != 0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&ctx->reserved[0], 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last && threadIdx.x < sizeof(BatchCtx) / 4) reinterpret_cast<uint32_t*>(ctx)[threadIdx.x] = 0;
+        if (!run) return;
+    }
     int64_t bad = INT64_MAX;  // this thread's first failing string (index_base + i)
-    for (int64_t i = gtid; i < count; i += gthreads) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t a = in_off[i], L = in_off[i + 1] - a;
         const unsigned long long wv = static_cast<unsigned long long>(err[i]);
         int32_t st;
@@ -600,14 +605,6 @@ __device__ __forceinline__ void dec_batch_finalize_body(const uint8_t* __restric
         const unsigned lo_min = __reduce_min_sync(kFull, unsigned(b >> 32) == hi ? unsigned(b) : ~0u);
         if ((threadIdx.x & 31) == 0 && hi != 0x7FFFFFFFu) atomicMin(first_bad, (static_cast<unsigned long long>(hi) << 32) | lo_min);
     }
-}
-
-__global__ void dec_batch_finalize_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off,
-                                          int64_t count, uint32_t pad, int32_t* status, int64_t* err,
-                                          int64_t* out_len, int64_t index_base, unsigned long long* first_bad) {
-    griddep_wait();
-    dec_batch_finalize_body(in, in_off, count, pad, status, err, out_len, index_base, first_bad,
-                            int64_t(blockIdx.x) * blockDim.x + threadIdx.x, int64_t(gridDim.x) * blockDim.x);
 }
 
 }  // namespace b64
