@@ -2,6 +2,7 @@
 // compilation: the templated kernels are instantiated and launched in one TU).
 #include "encode.cu"
 #include "decode.cu"
+#include "unaligned.cu"
 #include "peer.cu"
 #include "group.cu"
 #include "small.cu"

@@ -360,3 +360,85 @@ def test_batch_fast_path_ineligible_layouts(b64):
             base = oo if oo is not None else roff
             for s in np.nonzero(rlen > 0)[0][::29]:
                 assert np.array_equal(o[base[s]: base[s] + rlen[s]], rout[roff[s]: roff[s] + rlen[s]]), (name, s)
+
+
+# ------------------------------------------------------------------ misaligned bulk decode (unaligned.cu)
+
+@pytest.mark.parametrize("ioff", [1, 2, 3, 4, 5, 13, 31])
+def test_decode_misaligned_fast_kernel(b64, ioff):
+    """dec_fastu_kernel (any alignment, inputs of >= 64 Ki chars): every input offset mod 4 and
+    several mod 32, output offsets mod 8, lengths with head / tail / final quads, valid and
+    with a non-alphabet byte in the head, the bulk, the tail and the final quad -- against the
+    oracle, exact bytes and out_len."""
+    rng = np.random.default_rng(ioff)
+    for n in (49_152 + 7, 200_003, 1_000_000):
+        x = synth.data(n, seed=n + ioff)
+        ref = oracle.encode(x)
+        m = ref.size
+        for ooff in (0, 1, 3, 5, 8):
+            buf = torch.empty(m + 64, dtype=torch.uint8, device=DEV)
+            tin = buf[ioff: ioff + m]
+            tin.copy_(torch.from_numpy(ref).to(DEV))
+            obuf = torch.empty(3 * (m // 4) + 64, dtype=torch.uint8, device=DEV)
+            out = obuf[ooff: ooff + 3 * (m // 4)]
+            y, info = b64.decode_async(tin, out=out)
+            err, st, olen = info.tolist()
+            assert err == -1 and olen == n and np.array_equal(y[:n].cpu().numpy(), x), (n, ooff)
+        for p in (1, 9, 30, m // 2 + 3, m - 700, m - 6, m - 1):
+            t2 = ref.copy()
+            t2[p] = ord("!") if rng.random() < 0.5 else 0xC3
+            r2, e2, s2 = oracle.decode(t2)
+            buf = torch.empty(m + 64, dtype=torch.uint8, device=DEV)
+            tin = buf[ioff: ioff + m]
+            tin.copy_(torch.from_numpy(t2).to(DEV))
+            obuf = torch.empty(3 * (m // 4) + 64, dtype=torch.uint8, device=DEV)
+            out = obuf[3: 3 + 3 * (m // 4)]
+            y, info = b64.decode_async(tin, out=out)
+            err, st, olen = info.tolist()
+            assert (err, st, olen) == (e2, s2, r2.size), (n, p)
+            assert np.array_equal(y[:olen].cpu().numpy(), r2), (n, p)
+
+
+def test_decode_misaligned_no_stray_writes(b64):
+    """dec_fastu_kernel writes exactly [out, out + out_len): canary bytes before and after the
+    output (and every byte of the partial 8-byte words at chunk edges) stay intact."""
+    for n in (300_001, 1 << 20):
+        x = synth.data(n, seed=n)
+        ref = oracle.encode(x)
+        m = ref.size
+        for ioff, ooff in ((1, 1), (2, 7), (3, 4), (6, 3)):
+            tb = torch.empty(m + 32, dtype=torch.uint8, device=DEV)
+            tb[ioff: ioff + m] = torch.from_numpy(ref).to(DEV)
+            ob = torch.full((3 * (m // 4) + 2 * 256,), 0xA5, dtype=torch.uint8, device=DEV)
+            out = ob[256 + ooff: 256 + ooff + 3 * (m // 4)]
+            y, info = b64.decode_async(tb[ioff: ioff + m], out=out)
+            err, st, olen = info.tolist()
+            assert err == -1 and olen == n
+            h = ob.cpu().numpy()
+            assert (h[: 256 + ooff] == 0xA5).all() and (h[256 + ooff + n:] == 0xA5).all(), (n, ioff, ooff)
+            assert np.array_equal(h[256 + ooff: 256 + ooff + n], x)
+
+
+def test_stream_pieces_take_fast_kernel(b64):
+    """A streaming decode in large odd-sized pieces (every piece's quads misaligned): the result
+    equals the oracle's one-shot decode, and the pieces' bulk runs through dec_fastu_kernel (one
+    launch per piece: the join rides along)."""
+    x = synth.data(3_000_001, seed=4)
+    ref = oracle.encode(x)
+    td = torch.from_numpy(ref).to(DEV)
+    for piece in (65_539, 300_001):
+        ds = b64.DecodeStream()
+        before = b64.launch_count()
+        parts, p = [], 0
+        while p < ref.size:
+            k = min(piece, ref.size - p)
+            parts.append(ds.update(td[p: p + k]))
+            p += k
+        npieces = len(parts)
+        tail, info = ds.end()
+        torch.cuda.synchronize()
+        launches = b64.launch_count() - before
+        err, st, olen = info.tolist()
+        got = torch.cat(parts + [tail]).cpu().numpy()
+        assert err == -1 and olen == x.size and np.array_equal(got[: x.size], x)
+        assert launches <= npieces + 1, (launches, npieces)

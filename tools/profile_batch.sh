@@ -10,6 +10,6 @@ $PB > gpurun_out/${T}_pb.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/${T}_batch_launches.csv $PB > gpurun_out/${T}_ncu_batch_launches.log 2>&1
 echo "launch list rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"enc_generic|dec_batch_bulk|dec_generic" -s 1 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"enc_generic|dec_batch_bulk|dec_batch_strfinal" -s 1 -c 3 \
     -o gpurun_out/${T}_full_batch $PB > gpurun_out/${T}_ncu_batch.log 2>&1
 echo "full batch rc=$?"
