@@ -20,7 +20,7 @@
 // lane's first word with one SHFL), so shared byte i is global byte
 // (out_c & ~7) + i: the 96 (or 95) whole 8-byte words go out as lane-linear
 // STG.64 exactly as in dec_fast_kernel, the two partial boundary words (shared
-// with the neighbouring chunks) byte by byte.
+// with the neighbouring chunks) as aligned 1 / 2 / 4-byte stores.
 #include "b64_device.cuh"
 
 namespace b64 {
@@ -35,6 +35,18 @@ struct UnalignedBulk {
 
 __device__ __forceinline__ uint32_t ld_u8x4(const uint8_t* p) {  // 4 bytes at any alignment
     return uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
+}
+
+// Bytes [lo, hi) of the aligned 8-byte word at g (value wv, little-endian) as aligned
+// 1 / 2 / 4-byte stores: the edge words a chunk shares with its neighbours.
+__device__ __forceinline__ void partial_store(uint8_t* g, uint2 wv, uint32_t lo, uint32_t hi) {
+    const unsigned long long v = (static_cast<unsigned long long>(wv.y) << 32) | wv.x;
+    uint32_t t = lo;
+    if ((t & 1) && t < hi) { g[t] = uint8_t(v >> (8 * t)); t += 1; }
+    if ((t & 2) && t + 2 <= hi) { *reinterpret_cast<uint16_t*>(g + t) = uint16_t(v >> (8 * t)); t += 2; }
+    if ((t & 3) == 0 && t + 4 <= hi) { *reinterpret_cast<uint32_t*>(g + t) = uint32_t(v >> (8 * t)); t += 4; }
+    if ((t & 1) == 0 && t + 2 <= hi) { *reinterpret_cast<uint16_t*>(g + t) = uint16_t(v >> (8 * t)); t += 2; }
+    if (t < hi) g[t] = uint8_t(v >> (8 * t));
 }
 
 template <int D>
@@ -86,12 +98,17 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
                     pin += sin;
                 }
                 // the lane's 8 quads: bytes [b, b + 32) of its block and the next one
-                const uint32_t nx = __shfl_down_sync(kFull, xr[i][0], 1);
-                const uint32_t w8 = lane == 31 ? xe[i] : nx;
                 uint32_t err = 0, v[8];
+                if (bsh) {
+                    const uint32_t nx = __shfl_down_sync(kFull, xr[i][0], 1);
+                    const uint32_t w8 = lane == 31 ? xe[i] : nx;
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    v[q] = dec_quad_s(__funnelshift_r(xr[i][q], q < 7 ? xr[i][q + 1] : w8, bsh), lb, err);
+                    for (int q = 0; q < 8; ++q)
+                        v[q] = dec_quad_s(__funnelshift_r(xr[i][q], q < 7 ? xr[i][q + 1] : w8, bsh), lb, err);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(xr[i][q], lb, err);
+                }
                 uint32_t o[6];
                 dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
                 dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
@@ -104,8 +121,16 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
                 const uint32_t spill = __shfl_up_sync(kFull, s[6], 1);
                 if (lane > 0) s[0] |= spill;
                 const uint32_t wa = sbase + (os >> 2) * 4 + lane * 24;
-#pragma unroll
-                for (int k = 0; k < 6; ++k) asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa + 4 * k), "r"(s[k]) : "memory");
+                if (os < 4) {  // 8-byte aligned lane slots: three STS.64 (as dec_fast_kernel)
+                    sts64(wa, s[0], s[1]);
+                    sts64(wa + 8, s[2], s[3]);
+                    sts64(wa + 16, s[4], s[5]);
+                } else {
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(s[0]) : "memory");
+                    sts64(wa + 4, s[1], s[2]);
+                    sts64(wa + 12, s[3], s[4]);
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa + 20), "r"(s[5]) : "memory");
+                }
                 if (lane == 31) asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa + 24), "r"(s[6]) : "memory");
                 __syncwarp();
                 // global: word k of the chunk's aligned window = shared bytes [8k, 8k + 8)
@@ -116,12 +141,15 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
                     const uint2 wv = lds64(sbase + 8 * k);
                     if (k > 0 || os == 0) st64(g + 8 * k, wv.x, wv.y);
                 }
-                if (os) {  // the two partial words at the chunk's edges, shared with its neighbours
-                    const uint8_t* sb = reinterpret_cast<const uint8_t*>(&s_stage[threadIdx.x >> 5][0]);
-                    if (lane == 0)
-                        for (uint32_t t = os; t < 8; ++t) g[t] = sb[t];
-                    if (lane == 31)
-                        for (uint32_t t = 0; t < os; ++t) g[768 + t] = sb[768 + t];
+                if (os) {  // the two partial words at the chunk's edges, shared with its neighbours:
+                           // bytes [os, 8) of word 0 and [0, os) of word 96, in 1 / 2 / 4-byte stores
+                    if (lane == 0) {
+                        const uint2 wv = lds64(sbase);
+                        partial_store(g, wv, os, 8);
+                    } else if (lane == 31) {
+                        const uint2 wv = lds64(sbase + 768);
+                        partial_store(g + 768, wv, 0, os);
+                    }
                 }
                 __syncwarp();
                 const bool bad = (err & kInvalid) != 0;

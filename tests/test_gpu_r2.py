@@ -426,7 +426,7 @@ def test_stream_pieces_take_fast_kernel(b64):
     x = synth.data(3_000_001, seed=4)
     ref = oracle.encode(x)
     td = torch.from_numpy(ref).to(DEV)
-    for piece in (65_539, 300_001):
+    for piece in (100_003, 300_001):  # (pieces' bulk >= 64 Ki chars: the unaligned fast kernel)
         ds = b64.DecodeStream()
         before = b64.launch_count()
         parts, p = [], 0

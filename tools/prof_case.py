@@ -18,7 +18,7 @@ import synth  # noqa: E402
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--op", choices=("enc", "dec", "both", "batch", "group", "peer"), default="both")
+    p.add_argument("--op", choices=("enc", "dec", "both", "batch", "group", "peer", "decu"), default="both")
     p.add_argument("--n", type=int, default=1 << 30)
     p.add_argument("--reps", type=int, default=3)
     a = p.parse_args()
@@ -70,6 +70,24 @@ def main():
             b64.decode_batch(enc, eoff)
         torch.cuda.synchronize()
         print("ok batch")
+        return
+    if a.op == "decu":  # misaligned input (+1) and output (+3): dec_fast vs dec_fastu, alternating
+        x = synth.device_data(a.n, seed=0)
+        t = b64.encode(x)
+        tb = torch.empty(t.numel() + 64, dtype=torch.uint8, device="cuda")
+        tb[1: 1 + t.numel()] = t
+        tu = tb[1: 1 + t.numel()]
+        ob = torch.empty(3 * (t.numel() // 4) + 64, dtype=torch.uint8, device="cuda")
+        out = ob[: 3 * (t.numel() // 4)]
+        outu = ob[3: 3 + 3 * (t.numel() // 4)]
+        cell = torch.empty(1, dtype=torch.int64, device="cuda")
+        for _ in range(a.reps):
+            cell.fill_(b64.ERR_NONE)
+            b64.decode_chunk(t, 0, True, cell, out=out)
+            b64.decode_chunk(tu, 0, True, cell, out=outu)
+        torch.cuda.synchronize()
+        assert int(cell.item()) == b64.ERR_NONE
+        print("ok decu")
         return
     x = synth.device_data(a.n, seed=0)
     t = b64.encode(x)
