@@ -28,7 +28,7 @@ struct DevInfo {
     int sms = 0;
     int occ_group[4] = {0, 0, 0, 0};  // min over the enc / dec / codec group kernels
     int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_enc_gen = 0, occ_dec_gen = 0;
-    int occ_batch_bulk = 0, occ_fastu[4] = {0, 0, 0, 0};
+    int occ_batch_bulk = 0, occ_fastu[3][8] = {};
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -68,9 +68,7 @@ const DevInfo* dev_info() {
         group_occupancy(info.occ_group) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_batch_bulk, dec_batch_bulk_kernel<2>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_fastu[1], dec_fastu_kernel<1>, kThreads, 0) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_fastu[2], dec_fastu_kernel<2>, kThreads, 0))
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_batch_bulk, dec_batch_bulk_kernel<2>, kThreads, 0))
         return nullptr;
     for (int i = 0; i < 4; ++i) {
         info.occ_enc_fast[i] = info.occ_enc_fast[i] < 1 ? 1 : info.occ_enc_fast[i];
@@ -80,7 +78,14 @@ const DevInfo* dev_info() {
     info.occ_enc_gen = info.occ_enc_gen < 1 ? 1 : info.occ_enc_gen;
     info.occ_dec_gen = info.occ_dec_gen < 1 ? 1 : info.occ_dec_gen;
     info.occ_batch_bulk = info.occ_batch_bulk < 1 ? 1 : info.occ_batch_bulk;
-    for (int i = 0; i < 4; ++i) info.occ_fastu[i] = info.occ_fastu[i] < 1 ? 1 : info.occ_fastu[i];
+    for (int d = 1; d <= 2; ++d)
+        for (int w = 0; w < 8; ++w) {
+            int o = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, d == 2 ? dec_fastu_pick<2>(w) : dec_fastu_pick<1>(w),
+                                                              kThreads, 0) != cudaSuccess)
+                return nullptr;
+            info.occ_fastu[d][w] = o < 1 ? 1 : o;
+        }
     if (cudaFuncSetAttribute(dec_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
         cudaFuncSetAttribute(ws_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         return nullptr;
@@ -376,24 +381,24 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
     } else if (m >= unaligned_min()) {
         // any alignment, the fast loop over aligned 32-byte blocks (unaligned.cu)
         const int64_t Q = m / 4, Qint = is_final ? Q - 1 : Q;
-        const uintptr_t u = reinterpret_cast<uintptr_t>(d_in);
-        const uintptr_t b = u & 3;
-        const uintptr_t a0 = ((u - b) + 31) & ~uintptr_t(31);
+        const uintptr_t ou = reinterpret_cast<uintptr_t>(d_out);
         UnalignedBulk ub;
-        ub.b = uint32_t(b);
-        ub.q0 = std::min<int64_t>(int64_t(a0 - (u - b)) / 4, Qint);
-        ub.nchunk = int32_t((Qint - ub.q0) / 256);
-        ub.A0 = reinterpret_cast<const uint8_t*>(a0);
+        ub.q0 = std::min<int64_t>(int64_t(((8 - (ou & 7)) * 3) & 7), Qint);  // out + 3 q0 is 8-byte aligned
+        const uintptr_t s0 = reinterpret_cast<uintptr_t>(d_in) + 4 * uintptr_t(ub.q0);
+        ub.b = uint32_t(s0 & 3);
+        ub.A0 = reinterpret_cast<const uint8_t*>(s0 & ~uintptr_t(31));
         ub.out0 = d_out + 3 * ub.q0;
+        ub.nchunk = int32_t((Qint - ub.q0) / 256);
+        const int ws = int((s0 & 31) >> 2);
         const int dd = dec_depth(m);
-        const int64_t blocks = balanced_blocks(ub.nchunk, int64_t(di->sms) * cap_bps(di->occ_fastu[dd]));
+        const int64_t blocks = balanced_blocks(ub.nchunk, int64_t(di->sms) * cap_bps(di->occ_fastu[dd][ws]));
         StreamJoin sj = {};
         if (join && joined) {
             sj = *join;
             *joined = true;
         }
-        launch(pick2(dd, dec_fastu_kernel<1>, dec_fastu_kernel<2>), blocks, kThreads, s, d_in, m, d_out, dec_tab(a),
-               base, is_final, c, out_len, ub, sj);
+        launch(dd == 2 ? dec_fastu_pick<2>(ws) : dec_fastu_pick<1>(ws), blocks, kThreads, s, d_in, m, d_out,
+               dec_tab(a), base, is_final, c, out_len, ub, sj);
     } else {
         Offsets off{nullptr, nullptr, 1, m};
         const int64_t blocks = clamp_grid((m / 16 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_dec_gen);

@@ -3,32 +3,26 @@
 // of a streaming decode, whose quads start wherever the previous piece left off
 // (R15) -- before, all of those took the per-unit generic kernel.
 //
-// Input.  The quads start at in + 4k, b = in & 3.  An aligned 32-byte block A
-// holds the first bytes of exactly 8 quads (those starting at A + b + 4j), the
-// last of which runs b bytes into the next block.  So the bulk is cut into
-// aligned 1024-byte warp-chunks starting at A0 = align_up(in - b, 32): lane l
-// loads its block with ONE LDG.256 exactly as dec_fast_kernel, takes the next
-// lane's first word with one SHFL (lane 31 loads it: one extra LDG.32 per
-// chunk, only when b != 0) and funnel-shifts the 8 quads out of the 9 words.
-// The h < 8 quads before A0 + b, the < 256 after the last full chunk and the
-// final quad (R6) are done one per thread with byte loads.
-//
-// Output.  A chunk's 768 bytes land at out_c = out + 3*(quad index), whose
-// alignment os = out_c & 7 is the same for every chunk (768 = 96 * 8).  The
-// lanes' 24-byte results are re-laid through the warp's shared buffer shifted
-// by os bytes (funnel shifts; each lane's spill word is merged into the next
-// lane's first word with one SHFL), so shared byte i is global byte
-// (out_c & ~7) + i: the 96 (or 95) whole 8-byte words go out as lane-linear
-// STG.64 exactly as in dec_fast_kernel, the two partial boundary words (shared
-// with the neighbouring chunks) as aligned 1 / 2 / 4-byte stores.
+// Quad k of the text is at in + 4k, its 3 bytes at out + 3k.  The bulk starts at
+// the first quad q0 whose OUTPUT is 8-byte aligned (q0 = 3 * (-out mod 8) mod 8
+// < 8), so the chunks' 768-byte outputs are 8-byte aligned and go out exactly as
+// in dec_fast_kernel (per-warp shared re-layout, lane-linear STG.64).  On the
+// input side chunk c's 1024 chars start at in + 4 q0 + 1024 c, i.e. at word WS
+// and byte b of an aligned 32-byte block (WS, b the same for every chunk): lane l
+// loads its aligned block with ONE LDG.256, takes the next lane's first WS + 1
+// words by SHFL (lane 31 loads the next block itself) and funnel-shifts its 8
+// quads out of words WS .. WS + 8.  WS is a template parameter (8 kernels per
+// prefetch depth; no dynamic register indexing), b a runtime shift.  The < 8
+// quads before q0, the < 256 after the last full chunk and the final quad (R6)
+// are done one per thread with byte loads.
 #include "b64_device.cuh"
 
 namespace b64 {
 
 struct UnalignedBulk {
-    const uint8_t* A0;  // first aligned block of the bulk
-    uint8_t* out0;      // output of the first bulk quad
-    int64_t q0;         // stream quad index of the first bulk quad (= head quads h)
+    const uint8_t* A0;  // aligned 32-byte block holding the first bulk quad's first byte
+    uint8_t* out0;      // output of the first bulk quad (8-byte aligned)
+    int64_t q0;         // quad index of the first bulk quad (= head quads, < 8)
     int32_t nchunk;     // full 256-quad chunks
     uint32_t b;         // in & 3
 };
@@ -37,25 +31,13 @@ __device__ __forceinline__ uint32_t ld_u8x4(const uint8_t* p) {  // 4 bytes at a
     return uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
 }
 
-// Bytes [lo, hi) of the aligned 8-byte word at g (value wv, little-endian) as aligned
-// 1 / 2 / 4-byte stores: the edge words a chunk shares with its neighbours.
-__device__ __forceinline__ void partial_store(uint8_t* g, uint2 wv, uint32_t lo, uint32_t hi) {
-    const unsigned long long v = (static_cast<unsigned long long>(wv.y) << 32) | wv.x;
-    uint32_t t = lo;
-    if ((t & 1) && t < hi) { g[t] = uint8_t(v >> (8 * t)); t += 1; }
-    if ((t & 2) && t + 2 <= hi) { *reinterpret_cast<uint16_t*>(g + t) = uint16_t(v >> (8 * t)); t += 2; }
-    if ((t & 3) == 0 && t + 4 <= hi) { *reinterpret_cast<uint32_t*>(g + t) = uint32_t(v >> (8 * t)); t += 4; }
-    if ((t & 1) == 0 && t + 2 <= hi) { *reinterpret_cast<uint16_t*>(g + t) = uint16_t(v >> (8 * t)); t += 2; }
-    if (t < hi) g[t] = uint8_t(v >> (8 * t));
-}
-
-template <int D>
-__global__ void __launch_bounds__(kThreads)
+template <int D, int WS>
+__global__ void __launch_bounds__(kThreads, D == 1 ? 5 : 4)
 dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab, int64_t base,
                  int is_final, unsigned long long* __restrict__ err_cell, int64_t* __restrict__ out_len,
                  UnalignedBulk ub, StreamJoin join) {
     __shared__ __align__(256) uint32_t s_lut[64];
-    __shared__ __align__(128) uint32_t s_stage[kThreads / 32][776 / 4];
+    __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];
     griddep_launch_dependents();
     griddep_wait();
     const int lane = threadIdx.x & 31;
@@ -64,22 +46,23 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
     const int64_t nwarp = gthreads >> 5;
     const int64_t Q = m >> 2;
     const int64_t Qint = (is_final && Q > 0) ? Q - 1 : Q;
-    const uint32_t sbase = smem_u32(&s_stage[threadIdx.x >> 5][0]);
+    const uint32_t sb = smem_u32(&s_stage[threadIdx.x >> 5][0]);
     const uint32_t bsh = ub.b * 8;
-    const uint32_t os = uint32_t(reinterpret_cast<uintptr_t>(ub.out0) & 7);
-    const uint32_t osr = (os & 3) * 8;
+    const bool need_next = (WS > 0) || (ub.b != 0);  // the last quad of a lane runs into the next block
 
     const int64_t c0 = gtid >> 5;
     const int32_t C = ub.nchunk, W = int32_t(nwarp), c0i = int32_t(c0);
     const int64_t sin = nwarp * 1024, sout = nwarp * 768;
     const uint8_t* pin = ub.A0 + c0 * 1024 + lane * 32;  // next block to load
+    uint8_t* pout = ub.out0 + c0 * 768;
     int64_t cur = c0;                                    // chunk being decoded
-    uint32_t xr[D][8], xe[D];
+    uint32_t xr[D][8], xe[D][WS + 1];
 #pragma unroll
     for (int i = 0; i < D; ++i)
         if (c0i + i * W < C) {
             ld256_stream(pin, xr[i]);
-            xe[i] = (bsh && lane == 31) ? ld32(pin + 32) : 0u;
+#pragma unroll
+            for (int k = 0; k <= WS; ++k) xe[i][k] = (need_next && lane == 31) ? ld32(pin + 32 + 4 * k) : 0u;
             pin += sin;
         }
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
@@ -91,82 +74,57 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
         for (int i = 0; i < D; ++i) {
             const int32_t c = cb + i * W;
             if (c < C) {
-                uint32_t y[8], ye = 0;
+                uint32_t y[8], ye[WS + 1];
                 if (c + D * W < C) {
                     ld256_stream(pin, y);
-                    ye = (bsh && lane == 31) ? ld32(pin + 32) : 0u;
+#pragma unroll
+                    for (int k = 0; k <= WS; ++k) ye[k] = (need_next && lane == 31) ? ld32(pin + 32 + 4 * k) : 0u;
                     pin += sin;
                 }
-                // the lane's 8 quads: bytes [b, b + 32) of its block and the next one
+                // the lane's 8 quads: words WS .. WS + 8 of its block and the next one, shifted by b
+                uint32_t nx[WS + 1];
+#pragma unroll
+                for (int k = 0; k <= WS; ++k) {
+                    const uint32_t t = __shfl_down_sync(kFull, xr[i][k], 1);
+                    nx[k] = lane == 31 ? xe[i][k] : t;
+                }
                 uint32_t err = 0, v[8];
-                if (bsh) {
-                    const uint32_t nx = __shfl_down_sync(kFull, xr[i][0], 1);
-                    const uint32_t w8 = lane == 31 ? xe[i] : nx;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        v[q] = dec_quad_s(__funnelshift_r(xr[i][q], q < 7 ? xr[i][q + 1] : w8, bsh), lb, err);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(xr[i][q], lb, err);
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t lo = (WS + q < 8) ? xr[i][(WS + q) & 7] : nx[(WS + q - 8) & 7];
+                    const uint32_t hi = (WS + q + 1 < 8) ? xr[i][(WS + q + 1) & 7] : nx[(WS + q + 1 - 8) & 7];
+                    v[q] = dec_quad_s(__funnelshift_r(lo, hi, bsh), lb, err);
                 }
                 uint32_t o[6];
                 dec_pack12(v[0], v[1], v[2], v[3], o[0], o[1], o[2]);
                 dec_pack12(v[4], v[5], v[6], v[7], o[3], o[4], o[5]);
-                // shared byte os + 24 lane + j <- output byte j of this lane (a shift by os)
-                uint32_t s[7];
-                s[0] = __funnelshift_l(0u, o[0], osr);
-#pragma unroll
-                for (int k = 1; k < 6; ++k) s[k] = __funnelshift_l(o[k - 1], o[k], osr);
-                s[6] = __funnelshift_l(o[5], 0u, osr);
-                const uint32_t spill = __shfl_up_sync(kFull, s[6], 1);
-                if (lane > 0) s[0] |= spill;
-                const uint32_t wa = sbase + (os >> 2) * 4 + lane * 24;
-                if (os < 4) {  // 8-byte aligned lane slots: three STS.64 (as dec_fast_kernel)
-                    sts64(wa, s[0], s[1]);
-                    sts64(wa + 8, s[2], s[3]);
-                    sts64(wa + 16, s[4], s[5]);
-                } else {
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa), "r"(s[0]) : "memory");
-                    sts64(wa + 4, s[1], s[2]);
-                    sts64(wa + 12, s[3], s[4]);
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa + 20), "r"(s[5]) : "memory");
-                }
-                if (lane == 31) asm volatile("st.shared.u32 [%0], %1;" ::"r"(wa + 24), "r"(s[6]) : "memory");
+                sts64(sb + lane * 24, o[0], o[1]);
+                sts64(sb + lane * 24 + 8, o[2], o[3]);
+                sts64(sb + lane * 24 + 16, o[4], o[5]);
                 __syncwarp();
-                // global: word k of the chunk's aligned window = shared bytes [8k, 8k + 8)
-                uint8_t* g = ub.out0 + cur * 768 - os;  // 8-byte aligned
-#pragma unroll
-                for (int j = 0; j < 3; ++j) {
-                    const int k = lane + 32 * j;
-                    const uint2 wv = lds64(sbase + 8 * k);
-                    if (k > 0 || os == 0) st64(g + 8 * k, wv.x, wv.y);
-                }
-                if (os) {  // the two partial words at the chunk's edges, shared with its neighbours:
-                           // bytes [os, 8) of word 0 and [0, os) of word 96, in 1 / 2 / 4-byte stores
-                    if (lane == 0) {
-                        const uint2 wv = lds64(sbase);
-                        partial_store(g, wv, os, 8);
-                    } else if (lane == 31) {
-                        const uint2 wv = lds64(sbase + 768);
-                        partial_store(g + 768, wv, 0, os);
-                    }
-                }
+                uint8_t* dst = pout + lane * 8;
+                const uint2 s0 = lds64(sb + lane * 8), s1 = lds64(sb + 256 + lane * 8), s2 = lds64(sb + 512 + lane * 8);
+                st64(dst, s0.x, s0.y);
+                st64(dst + 256, s1.x, s1.y);
+                st64(dst + 512, s2.x, s2.y);
                 __syncwarp();
                 const bool bad = (err & kInvalid) != 0;
                 if (__any_sync(kFull, bad)) {  // rare: locate the first invalid char of the chunk
                     uint32_t rel = 0xffffffffu;
                     if (bad) {
-                        const uint8_t* p = ub.A0 + cur * 1024 + lane * 32 + ub.b;
+                        const uint8_t* p = in + 4 * (ub.q0 + cur * 256) + lane * 32;
                         for (int t = 0; t < 32; ++t)
                             if (lut[p[t]] & kInvalid) { rel = uint32_t(lane * 32 + t); break; }
                     }
                     const uint32_t r = __reduce_min_sync(kFull, rel);
                     if (lane == 0) atomicMin(err_cell, pack_err(base + 4 * (ub.q0 + cur * 256) + int64_t(r), kBadChar));
                 }
+                pout += sout;
                 cur += W;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) xr[i][j] = y[j];
-                xe[i] = ye;
+#pragma unroll
+                for (int k = 0; k <= WS; ++k) xe[i][k] = ye[k];
             }
         }
     }
@@ -196,6 +154,23 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
             *out_len = 3 * Q;
         }
         if (join.active) stream_join(join.carry, join.H, join.in, join.m, join.out, lut, join.base, err_cell);
+    }
+}
+
+// (D, WS) -> kernel
+using DecFastuFn = void (*)(const uint8_t*, int64_t, uint8_t*, DecTab, int64_t, int, unsigned long long*, int64_t*,
+                            UnalignedBulk, StreamJoin);
+template <int D>
+DecFastuFn dec_fastu_pick(int ws) {
+    switch (ws) {
+        case 0: return dec_fastu_kernel<D, 0>;
+        case 1: return dec_fastu_kernel<D, 1>;
+        case 2: return dec_fastu_kernel<D, 2>;
+        case 3: return dec_fastu_kernel<D, 3>;
+        case 4: return dec_fastu_kernel<D, 4>;
+        case 5: return dec_fastu_kernel<D, 5>;
+        case 6: return dec_fastu_kernel<D, 6>;
+        default: return dec_fastu_kernel<D, 7>;
     }
 }
 

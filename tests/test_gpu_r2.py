@@ -442,3 +442,25 @@ def test_stream_pieces_take_fast_kernel(b64):
         got = torch.cat(parts + [tail]).cpu().numpy()
         assert err == -1 and olen == x.size and np.array_equal(got[: x.size], x)
         assert launches <= npieces + 1, (launches, npieces)
+
+
+def test_decode_misaligned_every_phase(b64):
+    """Every input offset mod 32 x every output offset mod 8 (all 8 word shifts x 4 byte shifts
+    of dec_fastu_kernel, and every head-quad count) at one size, against the oracle."""
+    n = 150_001
+    x = synth.data(n, seed=11)
+    ref = oracle.encode(x)
+    m = ref.size
+    src = torch.from_numpy(ref).to(DEV)
+    tb = torch.empty(m + 64, dtype=torch.uint8, device=DEV)
+    ob = torch.empty(3 * (m // 4) + 64, dtype=torch.uint8, device=DEV)
+    xd = torch.from_numpy(x).to(DEV)
+    for ioff in range(32):
+        tin = tb[ioff: ioff + m]
+        tin.copy_(src)
+        for ooff in range(8):
+            out = ob[ooff: ooff + 3 * (m // 4)]
+            y, info = b64.decode_async(tin, out=out)
+            err, st, olen = info.tolist()
+            assert err == -1 and olen == n, (ioff, ooff)
+            assert torch.equal(y[:n], xd), (ioff, ooff)
