@@ -64,6 +64,11 @@ __device__ __forceinline__ uint4 ld128_nc(const void* p) {
     asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     return r;
 }
+__device__ __forceinline__ uint32_t ld32_nc(const void* p) {  // streamed once: no L1 allocation
+    uint32_t r;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
 __device__ __forceinline__ uint32_t ld32(const void* p) {
     uint32_t r;
     asm("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));

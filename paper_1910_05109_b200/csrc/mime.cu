@@ -428,8 +428,16 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(16) uint8_t s_buf[kThreads / 32][kWsChunk + 16];
     __shared__ int64_t s_pref[kThreads];   // per-thread partial sums of the CTA's chunk counts
+    __shared__ uint32_t s_sel[16];         // PRMT selector packing the kept bytes of a 4-bit mask
     griddep_launch_dependents();
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+    if (threadIdx.x < 16) {
+        uint32_t sel = 0x4444u;  // unused positions read the zero operand
+        int k = 0;
+        for (int b = 0; b < 4; ++b)
+            if (threadIdx.x & (1 << b)) sel = (sel & ~(0xFu << (4 * k))) | (uint32_t(b) << (4 * k)), ++k;
+        s_sel[threadIdx.x] = sel;
+    }
     griddep_wait();
     if (__ldcg(&li->mode) == 1) return;
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
@@ -469,39 +477,47 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
         const int len = int(min(int64_t(kWsChunk), m - b0));
         int n_kept = 0;
         if (vec && len == kWsChunk) {
-            // the whole 4 KiB chunk in flight at once (8 x lane-linear LDG.128 per lane), then per
-            // 512 B: a 16-bit keep mask per lane (table look-ups), ONE warp prefix sum of the
-            // per-lane counts, and the kept bytes stored at their compacted positions
-            uint4 v[8];
+            // 32 rows of 128 B, lane l holding word l of a row (lane-linear LDG.32, 8 rows in
+            // flight): a lane's kept bytes go to consecutive positions ~4 bytes after the
+            // previous lane's, so the byte stores of a row hit distinct banks (the 16-byte-per-
+            // lane layout put lanes 8 apart on one bank: 4-way conflicts on every byte store).
+            // Per row: a 4-bit keep mask, the kept bytes packed by one PRMT (selector table in
+            // shared memory), their count; the counts of 4 rows ride in one word (8 bits each,
+            // <= 128) so ONE warp scan serves 4 rows.
+#pragma unroll 1
+            for (int g = 0; g < kWsChunk / 1024; ++g) {
+                uint32_t w[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = ld128_nc(in + b0 + u * 512 + lane * 16);
+                for (int r = 0; r < 8; ++r) w[r] = ld32_nc(in + b0 + (g * 8 + r) * 128 + lane * 4);
+                uint32_t km[8], pc[2] = {0u, 0u};
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t wv[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-                uint32_t mask = 0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) mask |= keep4<SW>(lut, wv[q]) << (4 * q);
-                const int cnt = __popc(mask);
-                int incl = cnt;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int y = __shfl_up_sync(kFull, incl, d);
-                    if (lane >= d) incl += y;
+                for (int r = 0; r < 8; ++r) {
+                    km[r] = keep4<SW>(lut, w[r]);
+                    pc[r >> 2] |= uint32_t(__popc(km[r])) << (8 * (r & 3));
                 }
-                int pos = n_kept + incl - cnt;
-                if (mask == 0xffffu) {  // nothing skipped in this lane's 16 bytes
+                uint32_t ex[2], tot[2];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t x = pc[h];
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) buf[pos + 4 * q + b] = uint8_t(wv[q] >> (8 * b));
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-#pragma unroll
-                        for (int b = 0; b < 4; ++b)
-                            if (mask & (1u << (4 * q + b))) buf[pos++] = uint8_t(wv[q] >> (8 * b));
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(kFull, x, d);
+                        if (lane >= d) x += y;
+                    }
+                    tot[h] = __shfl_sync(kFull, x, 31);
+                    ex[h] = x - pc[h];
                 }
-                n_kept += __shfl_sync(kFull, incl, 31);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int pos = n_kept + int((ex[r >> 2] >> (8 * (r & 3))) & 0xffu);
+                    const uint32_t cw = __byte_perm(w[r], 0u, s_sel[km[r]]);
+                    const int cnt = __popc(km[r]);
+                    if (cnt > 0) buf[pos] = uint8_t(cw);
+                    if (cnt > 1) buf[pos + 1] = uint8_t(cw >> 8);
+                    if (cnt > 2) buf[pos + 2] = uint8_t(cw >> 16);
+                    if (cnt > 3) buf[pos + 3] = uint8_t(cw >> 24);
+                    n_kept += int((tot[r >> 2] >> (8 * (r & 3))) & 0xffu);
+                }
             }
         } else {
             for (int i0 = 0; i0 < len; i0 += 32) {

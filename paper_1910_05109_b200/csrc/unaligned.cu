@@ -31,6 +31,21 @@ __device__ __forceinline__ uint32_t ld_u8x4(const uint8_t* p) {  // 4 bytes at a
     return uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
 }
 
+// The first NX words of the next aligned block, loaded only where `pred` (lane 31).
+template <int NX>
+__device__ __forceinline__ void ld_next_block(const uint8_t* p, bool pred, uint32_t (&w)[NX]) {
+    if (NX == 8) {
+        uint32_t t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (pred) ld256_stream(p, t);
+#pragma unroll
+        for (int k = 0; k < NX; ++k) w[k] = t[k & 7];
+    } else {
+        uint4 t = make_uint4(0, 0, 0, 0);
+        if (pred) t = ld128_nc(p);
+        w[0] = t.x; w[1 & (NX - 1)] = t.y; w[2 & (NX - 1)] = t.z; w[3 & (NX - 1)] = t.w;
+    }
+}
+
 template <int D, int WS>
 __global__ void __launch_bounds__(kThreads, D == 1 ? 5 : 4)
 dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab, int64_t base,
@@ -56,13 +71,15 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
     const uint8_t* pin = ub.A0 + c0 * 1024 + lane * 32;  // next block to load
     uint8_t* pout = ub.out0 + c0 * 768;
     int64_t cur = c0;                                    // chunk being decoded
-    uint32_t xr[D][8], xe[D][WS + 1];
+    // lane 31 also loads the next aligned block (the next chunk's first), in ONE LDG.128 / LDG.256
+    constexpr int NX = WS < 4 ? 4 : 8;
+    const bool ld_next = need_next && lane == 31;
+    uint32_t xr[D][8], xe[D][NX];
 #pragma unroll
     for (int i = 0; i < D; ++i)
         if (c0i + i * W < C) {
             ld256_stream(pin, xr[i]);
-#pragma unroll
-            for (int k = 0; k <= WS; ++k) xe[i][k] = (need_next && lane == 31) ? ld32(pin + 32 + 4 * k) : 0u;
+            ld_next_block<NX>(pin + 32, ld_next, xe[i]);
             pin += sin;
         }
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
@@ -74,11 +91,10 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
         for (int i = 0; i < D; ++i) {
             const int32_t c = cb + i * W;
             if (c < C) {
-                uint32_t y[8], ye[WS + 1];
+                uint32_t y[8], ye[NX];
                 if (c + D * W < C) {
                     ld256_stream(pin, y);
-#pragma unroll
-                    for (int k = 0; k <= WS; ++k) ye[k] = (need_next && lane == 31) ? ld32(pin + 32 + 4 * k) : 0u;
+                    ld_next_block<NX>(pin + 32, ld_next, ye);
                     pin += sin;
                 }
                 // the lane's 8 quads: words WS .. WS + 8 of its block and the next one, shifted by b
@@ -124,7 +140,7 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
 #pragma unroll
                 for (int j = 0; j < 8; ++j) xr[i][j] = y[j];
 #pragma unroll
-                for (int k = 0; k <= WS; ++k) xe[i][k] = ye[k];
+                for (int k = 0; k < NX; ++k) xe[i][k] = ye[k];
             }
         }
     }

@@ -464,3 +464,40 @@ def test_decode_misaligned_every_phase(b64):
             err, st, olen = info.tolist()
             assert err == -1 and olen == n, (ioff, ooff)
             assert torch.equal(y[:n], xd), (ioff, ooff)
+
+
+# ------------------------------------------------------------------ whitespace decode, general path (large)
+
+def _wrap(text, every, seed, extra_ws=b"\r\n"):
+    rng = np.random.default_rng(seed)
+    parts, i = [], 0
+    while i < text.size:
+        k = int(rng.integers(1, 2 * every))
+        parts.append(text[i: i + k])
+        parts.append(np.frombuffer(extra_ws[: int(rng.integers(1, len(extra_ws) + 1))], np.uint8))
+        i += k
+    return np.concatenate(parts)
+
+
+@pytest.mark.parametrize("alpha_kind", ["std", "ws_data"])
+def test_decode_ws_general_path_large(b64, alpha_kind):
+    """Texts above the single-launch size with irregular whitespace runs: the general path
+    (count / scan / compaction / decode / finalize), with the arithmetic whitespace test (std)
+    and with the table test (an alphabet in which ' ' and TAB are data chars); valid, with an
+    error, and with a compacted length that is not a multiple of 4."""
+    if alpha_kind == "std":
+        chars, alpha, ws = oracle.STANDARD, b64.standard(), b"\r\n\t \x0b\x0c"
+    else:
+        chars = oracle.STANDARD[:62] + b" \t"
+        alpha, ws = b64.alphabet(chars), b"\r\n\x0b\x0c"
+    for n in (700_001, 3_000_000):
+        x = synth.data(n, seed=n)
+        text = oracle.encode(x, chars)
+        for v, t in enumerate((_wrap(text, 60, n, ws), _wrap(text, 7, n + 1, ws), _wrap(text[:-1], 30, n + 2, ws))):
+            if v == 0:
+                t = t.copy()
+                t[t.size // 3] = ord("*")
+            ref, rerr, rst = oracle.decode_ws(t, chars)
+            out, err = b64.decode_ws(torch.from_numpy(t).to(DEV), alpha)
+            assert err == rerr, (n, v, err, rerr)
+            assert np.array_equal(out.cpu().numpy(), ref), (n, v)
