@@ -1,6 +1,8 @@
 #!/usr/bin/env python3
 """Whitespace-skipping decode timing: 1 GiB of data (or argv[1] bytes) as MIME text (76-char
-lines + CRLF), CUDA events, L2 flushed, median of 10."""
+lines + CRLF), CUDA events, L2 flushed, median of 10.  argv[2]: "mime" (default, the line
+path), "irregular" (one stray blank in the middle: line pass, then the general path) or
+"start" (a stray blank after the first line: the general path almost at once)."""
 import json
 import os
 import statistics
@@ -31,10 +33,14 @@ def main():
     mime = mime[: (m // 76) * 78 + (m % 76) + (2 if m % 76 else 0)]
     if m % 76:
         mime[-2:] = torch.tensor([13, 10], dtype=torch.uint8, device=dev)
-    out = torch.empty(3 * (m // 4), dtype=torch.uint8, device=dev)
+    mode = sys.argv[2] if len(sys.argv) > 2 else "mime"
+    if mode != "mime":
+        at = mime.numel() // 2 if mode == "irregular" else 100
+        mime = torch.cat([mime[:at], torch.tensor([32], dtype=torch.uint8, device=dev), mime[at:]])
+    out = torch.empty(b64.decoded_len_max(mime.numel()), dtype=torch.uint8, device=dev)
     ws = torch.empty(int(b64._lib.lib().b64_decode_ws_workspace_bytes(mime.numel())), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    res = {"n": n, "text": mime.numel()}
+    res = {"n": n, "text": mime.numel(), "mode": mode}
     o, err = b64.decode_ws(mime, out=out, workspace=ws)
     assert err == -1 and torch.equal(o[:n], x)
     ts = []
