@@ -157,7 +157,13 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];  // per-warp output staging
     griddep_launch_dependents();
     griddep_wait();
-    if (m_dev) m = *m_dev;  // length produced on the device by a previous kernel (mime.cu)
+    if (m_dev) {  // the compacted text of mime.cu: its length and the kept index its suffix starts at
+        const int64_t k0 = m_dev[1];
+        m = m_dev[0] - k0;
+        in += k0;
+        out += 3 * (k0 >> 2);
+        base += k0;
+    }
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;

@@ -92,13 +92,20 @@ __device__ __forceinline__ uint32_t keep4(const uint8_t* lut, uint32_t x) {
 // `mode` and the general path (count / scan / compact / decode, which exit
 // at once in line mode) runs instead.  Traffic: read m + write 3m'/4, one pass.
 struct WsLine {
-    int32_t mode;             // 1: line-structured (ws_line_kernel decodes), 0: general path
+    int32_t mode;             // 1: a line segment is active (ws_line_kernel decodes it); 2: line segments
+                              // decoded the whole text; 0: the general path decodes the suffix that
+                              // starts at text position `off`, kept index k0
     int32_t L, s, sep;        // chars per full line, separator bytes (0-2) and their values (LE)
-    int64_t nfull, r, mc;     // full lines, chars of the last partial line, kept chars
-    unsigned long long cell;  // first interior error, packed (kept index << 3 | kind)
-    int64_t off;              // leading whitespace bytes (the first line starts here)
+    int64_t nfull, r, mc;     // the segment's full lines, chars of its last partial line, kept chars
+    unsigned long long cell;  // the segment's first interior error, packed (GLOBAL kept index << 3 | kind)
+    int64_t off;              // text position of the segment's first kept char (leading whitespace skipped)
+    int64_t k0;               // kept index of the segment's first char (a multiple of kLineBlk)
+    long long fail;           // first block of the segment whose layout check failed (LLONG_MAX: none)
+    unsigned long long errk;  // first error of the finished segments, packed (kept index << 3 | kind)
+    int64_t errt;             // its text position
 };
 constexpr int64_t kLineProbe = 65536;  // bytes searched for the first whitespace byte
+constexpr int kLineSegs = 3;           // line segments per call (b64_decode_ws): 2 layout breaks at line speed
 #ifndef B64_LINE_BLK
 #define B64_LINE_BLK 4096
 #endif
@@ -111,30 +118,21 @@ constexpr int kLineStage = kLineBlk + kLineBlk / 16 + 80;  // + separators (L >=
 
 __device__ __forceinline__ int64_t line_orig(int64_t e, int64_t L, int64_t P) { return (e / L) * P + e % L; }
 
-__global__ void __launch_bounds__(32)
-ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li,
-                     int64_t* __restrict__ mc_general) {
-    __shared__ __align__(256) uint32_t s_lut[64];
-    griddep_launch_dependents();
-    const int lane = threadIdx.x;
-    s_lut[lane] = tab.w[lane];
-    s_lut[lane + 32] = tab.w[lane + 32];
-    griddep_wait();
-    __syncwarp();
-    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
-    // trailing whitespace (a final line break, blank lines, blanks) is skipped anyway: the
-    // layout is read on [0, me), me = one past the last non-whitespace byte (searched in the
-    // last kLineProbe bytes)
+// The layout of the text [start, m) (lane 0's w; w.mode 1 = line-structured, 0 = not).
+// Trailing whitespace (a final line break, blank lines, blanks) is skipped: the layout is
+// read on [ms, me), me = one past the last non-whitespace byte (searched in the last
+// kLineProbe bytes), ms = the first non-whitespace byte at or after start (searched in
+// kLineProbe bytes); p = the first whitespace byte after ms gives the line length.
+__device__ void probe_layout(const uint8_t* __restrict__ in, int64_t start, int64_t m, const uint8_t* lut,
+                             int lane, WsLine& w) {
     int64_t me = -1;
-    for (int64_t j0 = m; j0 > 0 && m - j0 < kLineProbe && me < 0; j0 -= 32) {
+    for (int64_t j0 = m; j0 > start && m - j0 < kLineProbe && me < 0; j0 -= 32) {
         const int64_t i = j0 - 1 - lane;
-        const uint32_t bal = __ballot_sync(kFull, i >= 0 && lut[in[i]] != kSkip);
+        const uint32_t bal = __ballot_sync(kFull, i >= start && lut[in[i]] != kSkip);
         if (bal) me = j0 - (__ffs(bal) - 1);
     }
-    // leading whitespace likewise: the first line starts at ms (searched in the first
-    // kLineProbe bytes); p = the first whitespace byte after it
     int64_t ms = -1;
-    for (int64_t i0 = 0; i0 < min(me, kLineProbe) && ms < 0; i0 += 32) {
+    for (int64_t i0 = start; i0 < min(me, start + kLineProbe) && ms < 0; i0 += 32) {
         const int64_t i = i0 + lane;
         const uint32_t bal = __ballot_sync(kFull, i < me && lut[in[i]] != kSkip);
         if (bal) ms = i0 + __ffs(bal) - 1;
@@ -146,11 +144,8 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
         const uint32_t bal = __ballot_sync(kFull, i < lim && lut[in[i]] == kSkip);
         if (bal) p = i0 + __ffs(bal) - 1;
     }
-    if (lane) return;
-    WsLine w;
-    w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.cell = kErrNone; w.off = 0;
-    *mc_general = 0;  // the general path's decode does nothing unless its scan runs
-    if (me <= 0 || ms < 0) {
+    w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.off = start;
+    if (me <= start || ms < 0) {
         // whitespace only, or a leading / trailing run longer than the probe: the general path
     } else if (p < 0) {  // no whitespace between ms and the trailing run (probe window): one line
         const int64_t n1 = me - ms;
@@ -169,6 +164,68 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(32)
+ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li,
+                     int64_t* __restrict__ mc_general) {
+    __shared__ __align__(256) uint32_t s_lut[64];
+    griddep_launch_dependents();
+    const int lane = threadIdx.x;
+    s_lut[lane] = tab.w[lane];
+    s_lut[lane + 32] = tab.w[lane + 32];
+    griddep_wait();
+    __syncwarp();
+    WsLine w;
+    probe_layout(in, 0, m, reinterpret_cast<const uint8_t*>(s_lut), lane, w);
+    if (lane) return;
+    w.cell = kErrNone; w.k0 = 0; w.fail = LLONG_MAX; w.errk = kErrNone; w.errt = -1;
+    mc_general[0] = 0;  // the general path's decode does nothing unless its scan runs
+    mc_general[1] = 0;
+    *li = w;
+}
+
+// After a line segment (one warp): if its layout held everywhere, the line path is done
+// (mode 2).  Otherwise the blocks before the first failing one are verified and decoded:
+// their first error (if any) is kept with its text position (errk / errt), and the rest of
+// the text -- from the failing block's first kept char, whose text position the verified
+// layout gives -- becomes the next segment: probed again (mode 1, decoded by the next line
+// kernel) or, when it has no line layout or this is the last segment, left to the general
+// path (mode 0: suffix [off, m) from kept index k0).  (A stray byte in MIME text thus costs
+// one more probe and the line pass over the rest, not the general path over everything.)
+__global__ void __launch_bounds__(32)
+ws_line_reprobe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li, int last) {
+    __shared__ __align__(256) uint32_t s_lut[64];
+    griddep_launch_dependents();
+    const int lane = threadIdx.x;
+    s_lut[lane] = tab.w[lane];
+    s_lut[lane + 32] = tab.w[lane + 32];
+    griddep_wait();
+    __syncwarp();
+    if (__ldcg(&li->mode) != 1) return;
+    WsLine cur = *li;
+    if (cur.fail == LLONG_MAX) {
+        if (lane == 0) li->mode = 2;
+        return;
+    }
+    const int64_t L = cur.L, P = L + cur.s;
+    const int64_t kb = int64_t(cur.fail) * kLineBlk;  // segment-relative kept index of the failing block
+    unsigned long long errk = cur.errk;
+    int64_t errt = cur.errt;
+    if (cur.cell < kErrNone && int64_t(cur.cell >> 3) - cur.k0 < kb && cur.cell < errk) {
+        errk = cur.cell;  // a verified block's error: keep it, with its text position
+        errt = cur.off + line_orig(int64_t(cur.cell >> 3) - cur.k0, L, P);
+    }
+    const int64_t p0 = cur.off + line_orig(kb, L, P), k0 = cur.k0 + kb;
+    WsLine w;
+    if (last) {
+        w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.off = p0;
+    } else {
+        probe_layout(in, p0, m, reinterpret_cast<const uint8_t*>(s_lut), lane, w);
+        if (w.mode == 0) w.off = p0;
+    }
+    if (lane) return;
+    w.cell = kErrNone; w.k0 = k0; w.fail = LLONG_MAX; w.errk = errk; w.errt = errt;
     *li = w;
 }
 
@@ -208,6 +265,8 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
     const uint32_t lb = smem_u32(s_lut);
     const int lane = threadIdx.x & 31;
     uint8_t* stg = &s_stage[threadIdx.x >> 5][0];
+    const int64_t kseg = li->k0;  // the segment's first kept index (a multiple of kLineBlk)
+    out += 3 * (kseg >> 2);
     const int32_t L = li->L, S = li->s;             // L >= 32: a 32-char unit crosses <= 1 line end
     const float invL = 1.0f / float(L);
     const int64_t P = int64_t(L) + S, nfull = li->nfull, mc = li->mc, li_off = li->off;
@@ -225,6 +284,7 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
     bool irregular = false;
     int64_t bad = INT64_MAX;  // first invalid kept index seen by this lane
     for (; it * kLineBlk < mc; it += W) {
+        if (it >= __ldcg(&li->fail)) break;  // a block before this one broke the layout
         const int64_t K0 = it * kLineBlk, K1 = min(K0 + kLineBlk, mc);
         const int32_t rl = int32_t(K1 - 1 - K0) + col0;  // last char, relative to line0's start
         const int32_t dll = div_small(rl, L, invL);
@@ -315,12 +375,12 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
             }
         }
         __syncwarp();
-        // the layout broke here or anywhere else: stop at once (the general path redoes it all)
+        // the layout broke in this block: record it (the blocks before it stay valid; the
+        // segment is cut here and the rest probed again, ws_line_reprobe_kernel) and stop
         if (__any_sync(kFull, irregular)) {
-            if (lane == 0) atomicExch(&li->mode, 0);
+            if (lane == 0) atomicMin(&li->fail, static_cast<long long>(it));
             break;
         }
-        if (__ldcg(&li->mode) != 1) break;
         line0 += step_lines;
         col0 += step_col;
         if (col0 >= L) {
@@ -330,7 +390,21 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
     }
     const unsigned hi = __reduce_min_sync(kFull, unsigned(uint64_t(bad) >> 32));
     const unsigned lo = __reduce_min_sync(kFull, unsigned(uint64_t(bad) >> 32) == hi ? unsigned(bad) : ~0u);
-    if (lane == 0 && hi != 0x7FFFFFFFu) atomicMin(&li->cell, pack_err(int64_t((uint64_t(hi) << 32) | lo), kBadChar));
+    if (lane == 0 && hi != 0x7FFFFFFFu)
+        atomicMin(&li->cell, pack_err(kseg + int64_t((uint64_t(hi) << 32) | lo), kBadChar));
+}
+
+// The general path decodes the suffix [li->off, m) of the text (all of it unless line
+// segments decoded a prefix): its kernels see the text from A = li->off rounded down to a
+// 16-byte-aligned address (not below 0), the first `excl` = off - A bytes excluded.
+struct WsSuffix {
+    int64_t A, excl;
+};
+__device__ __forceinline__ WsSuffix ws_suffix(const uint8_t* in, const WsLine* li) {
+    const int64_t off = __ldcg(&li->off);
+    int64_t A = off - int64_t((reinterpret_cast<uintptr_t>(in) + off) & 15);
+    if (A < 0) A = 0;
+    return WsSuffix{A, off - A};
 }
 
 template <bool SW>
@@ -344,7 +418,10 @@ ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K,
     if (threadIdx.x == 0) s_tot = 0;
     griddep_wait();
     __syncthreads();
-    if (__ldcg(&li->mode) == 1) return;  // line mode: ws_line_kernel did it all
+    if (__ldcg(&li->mode) != 0) return;  // line mode: ws_line_kernel did it all
+    const WsSuffix sx = ws_suffix(in, li);
+    in += sx.A;
+    m -= sx.A;
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
@@ -355,7 +432,7 @@ ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K,
         const int64_t b0 = c * kWsChunk;
         const int64_t len = min(int64_t(kWsChunk), m - b0);
         uint32_t cnt = 0;
-        if (vec && len == kWsChunk) {
+        if (vec && len == kWsChunk && b0 >= sx.excl) {
             // 8 x 16 B per lane, lane-linear (whole sectors), all in flight before the look-ups
             uint4 v[8];
 #pragma unroll
@@ -375,7 +452,7 @@ ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K,
                 }
             }
         } else {
-            for (int64_t i = lane; i < len; i += 32) cnt += ws_keep(lut, in[b0 + i]) ? 1u : 0u;
+            for (int64_t i = lane; i < len; i += 32) cnt += (b0 + i >= sx.excl && ws_keep(lut, in[b0 + i])) ? 1u : 0u;
         }
         cnt = __reduce_add_sync(kFull, cnt);
         if (lane == 0) {
@@ -395,7 +472,8 @@ __global__ void __launch_bounds__(1024) ws_scan_kernel(const int64_t* __restrict
     __shared__ int64_t s_warp[32];
     griddep_launch_dependents();
     griddep_wait();
-    if (__ldcg(&li->mode) == 1) return;
+    if (__ldcg(&li->mode) != 0) return;
+    const int64_t k0 = __ldcg(&li->k0);  // kept chars the line segments decoded before the suffix
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int64_t v = t < n ? cta_tot[t] : 0;
     int64_t x = v;  // inclusive warp scan
@@ -417,8 +495,11 @@ __global__ void __launch_bounds__(1024) ws_scan_kernel(const int64_t* __restrict
     }
     __syncthreads();
     const int64_t before = (w ? s_warp[w - 1] : 0) + x - v;
-    if (t < n) cta_base[t] = before;
-    if (t == 0) *m_out = s_warp[31];
+    if (t < n) cta_base[t] = k0 + before;
+    if (t == 0) {
+        m_out[0] = k0 + s_warp[31];  // the total kept count
+        m_out[1] = k0;               // where the suffix starts in the compacted text (dec_fast_kernel)
+    }
 }
 
 template <bool SW>
@@ -439,7 +520,10 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
         s_sel[threadIdx.x] = sel;
     }
     griddep_wait();
-    if (__ldcg(&li->mode) == 1) return;
+    if (__ldcg(&li->mode) != 0) return;
+    const WsSuffix sx = ws_suffix(in, li);
+    in += sx.A;
+    m -= sx.A;
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
@@ -476,7 +560,7 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
         const int64_t b0 = (c_lo + j) * kWsChunk;
         const int len = int(min(int64_t(kWsChunk), m - b0));
         int n_kept = 0;
-        if (vec && len == kWsChunk) {
+        if (vec && len == kWsChunk && b0 >= sx.excl) {
             // 32 rows of 128 B, lane l holding word l of a row (lane-linear LDG.32, 8 rows in
             // flight): a lane's kept bytes go to consecutive positions ~4 bytes after the
             // previous lane's, so the byte stores of a row hit distinct banks (the 16-byte-per-
@@ -523,7 +607,7 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
             for (int i0 = 0; i0 < len; i0 += 32) {
                 const int i = i0 + lane;
                 const uint32_t c = i < len ? in[b0 + i] : 0u;
-                const bool keep = i < len && ws_keep(lut, c);
+                const bool keep = i < len && b0 + i >= sx.excl && ws_keep(lut, c);
                 const uint32_t bal = __ballot_sync(kFull, keep);
                 if (keep) buf[n_kept + __popc(bal & ((1u << lane) - 1u))] = uint8_t(c);
                 n_kept += __popc(bal);
@@ -755,14 +839,18 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
     s_lut[lane + 32] = tab.w[lane + 32];
     __syncwarp();
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
-    if (__ldcg(&li->mode) == 1) {  // line mode: kept index -> text position in closed form
+    // the first error of the segments decoded by the line path before (kept index + text position)
+    const unsigned long long errk = __ldcg(&li->errk);
+    const int64_t errt = __ldcg(&li->errt);
+    if (__ldcg(&li->mode) == 2) {  // line segments did it all: kept index -> text position in closed form
         if (lane) return;
-        const int64_t L = li->L, P = L + li->s, mcl = li->mc;
-        unsigned long long w = __ldcg(&li->cell);
-        int64_t e = -1, ol = 0;
+        const int64_t L = li->L, P = L + li->s, mcl = li->mc, k0 = li->k0, mtot = k0 + mcl;
+        unsigned long long w = __ldcg(&li->cell);  // the last segment's first interior error
+        int64_t e = -1, et = -1, ol = 0;
         int32_t kind = kOk;
-        if (mcl & 3) {
-            e = mcl - (mcl & 3);
+        if (mtot & 3) {  // LENGTH (R14 / R6): the first char of the incomplete group
+            e = mtot - (mtot & 3);
+            et = li->off + line_orig(e - k0, L, P);
             kind = kLength;
         } else {
             uint32_t x = 0;
@@ -770,20 +858,27 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
             int fb = 0, k = 0;
             uint32_t v = 0;
             const uint32_t fk = final_quad(x, lut, pad, lenient, &fb, &k, &v);
-            if (fk != kOk) w = min(w, pack_err(mcl - 4 + fb, fk));
-            if (w < kErrNone) {
+            if (fk != kOk) w = min(w, pack_err(mtot - 4 + fb, fk));
+            if (errk < w) {  // an earlier segment's error comes first
+                e = int64_t(errk >> 3);
+                et = errt;
+                kind = int32_t(errk & 7);
+            } else if (w < kErrNone) {
                 e = int64_t(w >> 3);
+                et = li->off + line_orig(e - k0, L, P);
                 kind = int32_t(w & 7);
             } else {
-                ol = 3 * (mcl >> 2) - 3 + k;
-                store_bytes(out + 3 * ((mcl >> 2) - 1), v, k);
+                ol = 3 * (mtot >> 2) - 3 + k;
+                store_bytes(out + 3 * ((mtot >> 2) - 1), v, k);
             }
         }
-        *err_off = e < 0 ? -1 : li->off + line_orig(e, L, P);
+        *err_off = e < 0 ? -1 : et;
         if (status) *status = kind;
         if (out_len) *out_len = e < 0 ? ol : (kind == kLength ? 0 : 3 * (e >> 2));
         return;
     }
+    // the general path decoded the suffix [li->off, m) (kept indices from li->k0 on)
+    const WsSuffix sx = ws_suffix(in, li);
     const int64_t mc = *m_c;
     const unsigned long long wv = *reinterpret_cast<unsigned long long*>(err_off);
     int64_t e = -1;
@@ -791,6 +886,13 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
     if (mc & 3) {
         e = mc - (mc & 3);
         kind = kLength;
+    } else if (errk < kErrNone && errk < wv) {  // a line segment's error comes first
+        if (lane == 0) {
+            *err_off = errt;
+            if (status) *status = int32_t(errk & 7);
+            if (out_len) *out_len = 3 * (int64_t(errk >> 3) >> 2);
+        }
+        return;
     } else if (wv < kErrNone) {
         e = int64_t(wv >> 3);
         kind = int32_t(wv & 7);
@@ -807,6 +909,8 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
         }
         return;
     }
+    in += sx.A;
+    m -= sx.A;
     // CTA holding compacted index e: the last b with cta_base[b] <= e
     int lo = 0, hi = ncta - 1;
     while (lo < hi) {
@@ -846,7 +950,7 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
     int64_t pos = -1;
     for (int i0 = 0; i0 < len && pos < 0; i0 += 32) {
         const int i = i0 + lane;
-        const bool keep = i < len && ws_keep(lut, in[b0 + i]);
+        const bool keep = i < len && b0 + i >= sx.excl && ws_keep(lut, in[b0 + i]);
         const uint32_t bal = __ballot_sync(kFull, keep);
         const int k = __popc(bal);
         if (want < k) {
@@ -858,7 +962,7 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
         }
     }
     if (lane == 0) {
-        *err_off = pos;
+        *err_off = sx.A + pos;
         if (status) *status = kind;
         if (out_len) *out_len = kind == kLength ? 0 : 3 * (e >> 2);  // LENGTH: nothing decoded (R6)
     }

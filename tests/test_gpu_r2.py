@@ -501,3 +501,57 @@ def test_decode_ws_general_path_large(b64, alpha_kind):
             out, err = b64.decode_ws(torch.from_numpy(t).to(DEV), alpha)
             assert err == rerr, (n, v, err, rerr)
             assert np.array_equal(out.cpu().numpy(), ref), (n, v)
+
+
+# ------------------------------------------------------------------ whitespace decode: line segments
+
+def _mime_lines(text, L, sep=b"\r\n"):
+    lines = [text[i: i + L] for i in range(0, text.size, L)]
+    out = []
+    for ln in lines:
+        out.append(ln)
+        out.append(np.frombuffer(sep, np.uint8))
+    return np.concatenate(out)
+
+
+def _insert(t, pos, b):
+    return np.concatenate([t[:pos], np.frombuffer(b, np.uint8), t[pos:]])
+
+
+def test_decode_ws_line_segments(b64):
+    """Line-structured text whose layout breaks (a stray blank, a missing or doubled line break,
+    a change of line length): the line pass keeps the verified blocks, probes the rest again
+    (up to 3 segments) and hands what is left to the general path -- every variant against
+    the oracle (error offset in the ORIGINAL text, status, exact bytes), with errors before,
+    inside and after the break and LENGTH texts."""
+    n = 2_000_000
+    x = synth.data(n, seed=33)
+    t = oracle.encode(x)
+    mime = _mime_lines(t, 76)
+    M = mime.size
+    cases = {
+        "blank_middle": _insert(mime, M // 2, b" "),
+        "blank_start": _insert(mime, 200, b" "),
+        "blank_end": _insert(mime, M - 5000, b" "),
+        "two_blanks": _insert(_insert(mime, M // 3, b" "), 2 * M // 3, b"\t"),
+        "four_blanks": _insert(_insert(_insert(_insert(mime, M // 5, b" "), 2 * M // 5, b" "), 3 * M // 5, b" "),
+                               4 * M // 5, b" "),
+        "missing_crlf": np.concatenate([mime[: 78 * 9000 + 76], mime[78 * 9000 + 78:]]),
+        "double_crlf": _insert(mime, 78 * 12000, b"\r\n"),
+        "relayout": np.concatenate([_mime_lines(t[: 76 * 10000], 76), _mime_lines(t[76 * 10000:], 64, b"\n")]),
+        "block_boundary": _insert(mime, (4096 // 76) * 78 * 3, b" "),
+    }
+    for name, tv in list(cases.items()):
+        cases[name + "+err_before"] = tv.copy()
+        cases[name + "+err_before"][1000] = ord("*")
+        c2 = tv.copy()
+        c2[tv.size - 3000] = ord("#")
+        cases[name + "+err_after"] = c2
+    cases["blank_middle+length"] = _insert(_mime_lines(t[:-1], 76), M // 2, b" ")
+    cases["blank_middle+err_at_blank"] = _insert(mime, M // 2, b"*")
+    for name, tv in cases.items():
+        ref, rerr, rst = oracle.decode_ws(tv)
+        out, info = None, None
+        o, err = b64.decode_ws(torch.from_numpy(tv).to(DEV))
+        assert err == rerr, (name, err, rerr)
+        assert np.array_equal(o.cpu().numpy(), ref), name
