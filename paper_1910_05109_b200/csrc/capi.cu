@@ -561,7 +561,7 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
     // there and the rest probed again; after the last one the general path takes the rest
     for (int seg = 0; seg < kLineSegs; ++seg) {
         launch(ws_line_kernel, int64_t(di->sms) * B64_LINE_MINB, kLineThreads, s, d_in, m, wt, li, d_out);
-        launch(ws_line_reprobe_kernel, 1, 32, s, d_in, m, wt, li, seg == kLineSegs - 1 ? 1 : 0);
+        launch(ws_line_reprobe_kernel, 1, kPatchThreads, s, d_in, m, wt, li, d_out, seg == kLineSegs - 1 ? 1 : 0);
     }
     launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot, lic);
     launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc, lic);

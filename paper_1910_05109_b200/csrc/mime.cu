@@ -96,9 +96,12 @@ struct WsLine {
                               // decoded the whole text; 0: the general path decodes the suffix that
                               // starts at text position `off`, kept index k0
     int32_t L, s, sep;        // chars per full line, separator bytes (0-2) and their values (LE)
-    int64_t nfull, r, mc;     // the segment's full lines, chars of its last partial line, kept chars
+    int32_t v0;               // chars the segment's first line lacks (it may start mid-line): kept char e
+                              // of the segment sits at off + line_orig(e + v0) -- lines counted virtually
+    int64_t nfull, r, mc;     // the segment's full (virtual) lines, chars of its last line, kept chars
     unsigned long long cell;  // the segment's first interior error, packed (GLOBAL kept index << 3 | kind)
-    int64_t off;              // text position of the segment's first kept char (leading whitespace skipped)
+    int64_t off;              // modes 1 / 2: the segment's virtual text base (its first kept char is at
+                              // off + v0); mode 0: where the general path's suffix starts
     int64_t k0;               // kept index of the segment's first char (a multiple of kLineBlk)
     long long fail;           // first block of the segment whose layout check failed (LLONG_MAX: none)
     unsigned long long errk;  // first error of the finished segments, packed (kept index << 3 | kind)
@@ -138,29 +141,42 @@ __device__ void probe_layout(const uint8_t* __restrict__ in, int64_t start, int6
         if (bal) ms = i0 + __ffs(bal) - 1;
     }
     const int64_t lim = ms < 0 ? 0 : min(me, ms + kLineProbe);
-    int64_t p = -1;
+    int64_t p = -1;  // the first whitespace byte after ms: the end of the (maybe partial) first line
     for (int64_t i0 = ms; i0 >= 0 && i0 < lim && p < 0; i0 += 32) {
         const int64_t i = i0 + lane;
         const uint32_t bal = __ballot_sync(kFull, i < lim && lut[in[i]] == kSkip);
         if (bal) p = i0 + __ffs(bal) - 1;
     }
-    w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.off = start;
+    int s = 0;  // separator bytes after it
+    if (p >= 0)
+        while (s < 3 && p + s < me && lut[in[p + s]] == kSkip) ++s;
+    const int64_t q = p + s;  // the second line's first char
+    const int64_t lim2 = (p >= 0 && s <= 2) ? min(me, q + kLineProbe) : 0;
+    int64_t p2 = -1;  // the end of the second line
+    for (int64_t i0 = q; p >= 0 && s <= 2 && i0 < lim2 && p2 < 0; i0 += 32) {
+        const int64_t i = i0 + lane;
+        const uint32_t bal = __ballot_sync(kFull, i < lim2 && lut[in[i]] == kSkip);
+        if (bal) p2 = i0 + __ffs(bal) - 1;
+    }
+    w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.v0 = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.off = start;
     if (me <= start || ms < 0) {
         // whitespace only, or a leading / trailing run longer than the probe: the general path
     } else if (p < 0) {  // no whitespace between ms and the trailing run (probe window): one line
         const int64_t n1 = me - ms;
         w.mode = 1; w.r = n1; w.mc = n1; w.off = ms;
         w.L = int32_t(min(int64_t(1) << 30, (n1 + 4) & ~int64_t(3)));  // any multiple of 4 above n1
-    } else if (p - ms >= 32 && ((p - ms) & 3) == 0 && p - ms < (int64_t(1) << 30)) {  // (else: general)
-        int s = 0;
-        while (s < 3 && p + s < me && lut[in[p + s]] == kSkip) ++s;
-        if (s <= 2) {
-            // full lines each followed by the separator, then a last line of 1..L chars
-            const int64_t L = p - ms, P = L + s, n1 = me - ms;
+    } else if (s >= 1 && s <= 2) {
+        // lines of L chars each followed by the separator; the first may be partial (L0 chars,
+        // the segment starting mid-line), the last has 1..L chars
+        const int64_t L0 = p - ms;
+        const int64_t L = p2 >= 0 ? p2 - q : L0;  // (two lines only: the first one's length)
+        if (L >= 32 && (L & 3) == 0 && L < (int64_t(1) << 30) && L0 >= 1 && L0 <= L && (L0 & 3) == 0) {
+            const int64_t v0 = L - L0, P = L + s, n1 = me - ms + v0;
             const int64_t nfull = (n1 - 1) / P, r = n1 - nfull * P;
             if (r >= 1 && r <= L) {
-                w.mode = 1; w.L = int32_t(L); w.s = s; w.nfull = nfull; w.r = r; w.mc = nfull * L + r; w.off = ms;
-                w.sep = int32_t(s > 0 ? in[p] : 0) | int32_t(s > 1 ? in[p + 1] : 0) << 8;
+                w.mode = 1; w.L = int32_t(L); w.s = s; w.v0 = int32_t(v0); w.nfull = nfull; w.r = r;
+                w.mc = nfull * L + r - v0; w.off = ms - v0;
+                w.sep = int32_t(in[p]) | int32_t(s > 1 ? in[p + 1] : 0) << 8;
             }
         }
     }
@@ -185,47 +201,167 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
     *li = w;
 }
 
-// After a line segment (one warp): if its layout held everywhere, the line path is done
-// (mode 2).  Otherwise the blocks before the first failing one are verified and decoded:
-// their first error (if any) is kept with its text position (errk / errt), and the rest of
-// the text -- from the failing block's first kept char, whose text position the verified
-// layout gives -- becomes the next segment: probed again (mode 1, decoded by the next line
-// kernel) or, when it has no line layout or this is the last segment, left to the general
-// path (mode 0: suffix [off, m) from kept index k0).  (A stray byte in MIME text thus costs
-// one more probe and the line pass over the rest, not the general path over everything.)
-__global__ void __launch_bounds__(32)
-ws_line_reprobe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li, int last) {
+// After a line segment: if its layout held everywhere, the line path is done (mode 2).
+// Otherwise the blocks before the first failing one are verified and decoded: their first
+// error (if any) is kept with its text position (errk / errt).  The failing block itself --
+// its first kLineBlk kept chars, wherever the irregularity sits among them -- is decoded
+// here by one CTA (stage ~8 KiB of text in shared memory, compact the kept chars with a
+// block-wide prefix sum, decode the 1024 interior quads), and the rest of the text after its
+// last kept char becomes the next segment: probed again (mode 1, the next line kernel) or,
+// without a line layout, left to the general path (mode 0: suffix [off, m) from kept index
+// k0).  After the last segment (`last`) the general path takes the rest from the failing
+// block on.  So a stray byte in MIME text costs one probe, one 4 KiB block and the line pass
+// over the rest -- not the general path over everything.
+constexpr int kPatchThreads = 256;
+constexpr int kPatchWin = 8192;  // text bytes staged: the block's 4096 kept chars and at least one more
+
+__global__ void __launch_bounds__(kPatchThreads)
+ws_line_reprobe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li,
+                       uint8_t* __restrict__ out, int last) {
     __shared__ __align__(256) uint32_t s_lut[64];
+    __shared__ __align__(16) uint8_t s_win[kPatchWin];
+    __shared__ __align__(16) uint8_t s_comp[kLineBlk];
+    __shared__ int32_t s_wsum[kPatchThreads / 32];
+    __shared__ int32_t s_plan, s_end, s_bad, s_badpos;
+    __shared__ int64_t s_p0, s_k0;
+    __shared__ unsigned long long s_errk;
+    __shared__ int64_t s_errt;
     griddep_launch_dependents();
-    const int lane = threadIdx.x;
-    s_lut[lane] = tab.w[lane];
-    s_lut[lane + 32] = tab.w[lane + 32];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    if (t < 64) s_lut[t] = tab.w[t];
     griddep_wait();
-    __syncwarp();
+    __syncthreads();
     if (__ldcg(&li->mode) != 1) return;
-    WsLine cur = *li;
-    if (cur.fail == LLONG_MAX) {
-        if (lane == 0) li->mode = 2;
-        return;
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    if (t == 0) {
+        const WsLine cur = *li;
+        s_plan = 0;
+        if (cur.fail == LLONG_MAX) {
+            li->mode = 2;  // the whole segment verified: the line path decoded everything
+        } else {
+            const int64_t L = cur.L, P = L + cur.s;
+            const int64_t kb = int64_t(cur.fail) * kLineBlk;  // segment-relative kept index of the failing block
+            unsigned long long errk = cur.errk;
+            int64_t errt = cur.errt;
+            if (cur.cell < kErrNone && int64_t(cur.cell >> 3) - cur.k0 < kb && cur.cell < errk) {
+                errk = cur.cell;  // a verified block's error: keep it, with its text position
+                errt = cur.off + line_orig(int64_t(cur.cell >> 3) - cur.k0 + cur.v0, L, P);
+            }
+            s_p0 = cur.off + line_orig(kb + cur.v0, L, P);
+            s_k0 = cur.k0 + kb;
+            s_errk = errk;
+            s_errt = errt;
+            s_plan = last ? 2 : 1;
+        }
+        s_bad = INT32_MAX;
     }
-    const int64_t L = cur.L, P = L + cur.s;
-    const int64_t kb = int64_t(cur.fail) * kLineBlk;  // segment-relative kept index of the failing block
-    unsigned long long errk = cur.errk;
-    int64_t errt = cur.errt;
-    if (cur.cell < kErrNone && int64_t(cur.cell >> 3) - cur.k0 < kb && cur.cell < errk) {
-        errk = cur.cell;  // a verified block's error: keep it, with its text position
-        errt = cur.off + line_orig(int64_t(cur.cell >> 3) - cur.k0, L, P);
+    __syncthreads();
+    if (s_plan == 0) return;
+    const int64_t p0 = s_p0, k0 = s_k0;
+    int32_t general = s_plan == 2;
+    int64_t p1 = -1;
+    if (!general) {
+        // ---- stage the text from p0 (16-byte aligned loads when the address allows)
+        int64_t A = p0 - int64_t((reinterpret_cast<uintptr_t>(in) + p0) & 15);
+        if (A < 0) A = 0;
+        const int skip = int(p0 - A);
+        const int nb = int(min(int64_t(kPatchWin), m - A));
+        if (((reinterpret_cast<uintptr_t>(in) + A) & 15) == 0) {
+            for (int c = t; c < nb / 16; c += kPatchThreads)
+                *reinterpret_cast<uint4*>(s_win + 16 * c) = ld128_nc(in + A + 16 * c);
+            for (int i = (nb / 16) * 16 + t; i < nb; i += kPatchThreads) s_win[i] = in[A + i];
+        } else {
+            for (int i = t; i < nb; i += kPatchThreads) s_win[i] = in[A + i];
+        }
+        __syncthreads();
+        // ---- keep flags of this thread's 32 window bytes, block-wide exclusive prefix
+        uint32_t mask = 0;
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+            const int i = 32 * t + j;
+            if (i >= skip && i < nb && lut[s_win[i]] != kSkip) mask |= 1u << j;
+        }
+        const int cnt = __popc(mask);
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += y;
+        }
+        if (lane == 31) s_wsum[wid] = incl;
+        __syncthreads();
+        int wpre = 0, total = 0;
+        for (int w = 0; w < kPatchThreads / 32; ++w) {
+            if (w < wid) wpre += s_wsum[w];
+            total += s_wsum[w];
+        }
+        const int pre = wpre + incl - cnt;
+        // the block's kLineBlk kept chars must all be interior: at least one more kept char
+        // must follow in the window (else: the general path takes the rest, it is short or
+        // whitespace-heavy)
+        general = total <= kLineBlk;
+        if (!general) {
+            int k = pre;
+            for (uint32_t mm = mask; mm; mm &= mm - 1) {
+                const int j = __ffs(mm) - 1;
+                if (k < kLineBlk) s_comp[k] = s_win[32 * t + j];
+                if (k == kLineBlk - 1) s_end = 32 * t + j;
+                ++k;
+            }
+            __syncthreads();
+            // ---- decode the 1024 interior quads: thread t -> quads 4t .. 4t+3 (12 bytes)
+            const uint4 xv = *reinterpret_cast<const uint4*>(s_comp + 16 * t);
+            const uint32_t x[4] = {xv.x, xv.y, xv.z, xv.w};
+            uint32_t err = 0, v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = dec_quad(x[q], lut, err);
+            if (err & (kInvalid | kSkip)) {
+                for (int q = 0; q < 4; ++q) {
+                    const int jb = first_bad_in_quad(x[q], lut);
+                    if (jb < 4) { atomicMin(&s_bad, 16 * t + 4 * q + jb); break; }
+                }
+            }
+            uint32_t o0, o1, o2;
+            dec_pack12(v[0], v[1], v[2], v[3], o0, o1, o2);
+            uint32_t* ow = reinterpret_cast<uint32_t*>(out + 3 * (k0 >> 2) + 12 * t);  // 4-byte aligned
+            ow[0] = o0;
+            ow[1] = o1;
+            ow[2] = o2;
+            __syncthreads();
+            // ---- the first bad char's text position (the thread whose window bytes hold it)
+            const int bad = s_bad;
+            if (bad != INT32_MAX && bad >= pre && bad < pre + cnt) {
+                uint32_t mm = mask;
+                for (int r = bad - pre; r > 0; --r) mm &= mm - 1;
+                s_badpos = 32 * t + __ffs(mm) - 1;
+            }
+            __syncthreads();
+            if (t == 0) {
+                if (bad != INT32_MAX && pack_err(k0 + bad, kBadChar) < s_errk) {
+                    s_errk = pack_err(k0 + bad, kBadChar);
+                    s_errt = A + s_badpos;
+                }
+                s_p0 = A + s_end + 1;  // the next segment starts after the block's last kept char
+            }
+            __syncthreads();
+            p1 = s_p0;
+        }
     }
-    const int64_t p0 = cur.off + line_orig(kb, L, P), k0 = cur.k0 + kb;
+    // ---- the next segment: probe the rest (warp 0) or hand it to the general path
+    if (wid) return;
     WsLine w;
-    if (last) {
-        w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.off = p0;
-    } else {
-        probe_layout(in, p0, m, reinterpret_cast<const uint8_t*>(s_lut), lane, w);
-        if (w.mode == 0) w.off = p0;
+    if (!general) {
+        probe_layout(in, p1, m, lut, lane, w);
+        if (w.mode == 0) w.off = p1;
     }
     if (lane) return;
-    w.cell = kErrNone; w.k0 = k0; w.fail = LLONG_MAX; w.errk = errk; w.errt = errt;
+    if (general) {
+        w.mode = 0; w.L = 0; w.s = 0; w.sep = 0; w.v0 = 0; w.nfull = 0; w.r = 0; w.mc = 0; w.off = p0;
+        w.k0 = k0;
+    } else {
+        w.k0 = k0 + kLineBlk;
+    }
+    w.cell = kErrNone; w.fail = LLONG_MAX; w.errk = s_errk; w.errt = s_errt;
     *li = w;
 }
 
@@ -277,8 +413,9 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
     const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
     int64_t it = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     // line / column of the warp's first kept char, advanced per grid-stride step without division
-    int64_t line0 = (it * kLineBlk) / L;
-    int32_t col0 = int32_t(it * kLineBlk - line0 * L);
+    const int64_t v0 = li->v0;  // virtual line coordinates: kept char K sits at line / col of K + v0
+    int64_t line0 = (it * kLineBlk + v0) / L;
+    int32_t col0 = int32_t(it * kLineBlk + v0 - line0 * L);
     const int64_t step_lines = (W * kLineBlk) / L;
     const int32_t step_col = int32_t(W * kLineBlk - step_lines * L);
     bool irregular = false;
@@ -844,17 +981,17 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
     const int64_t errt = __ldcg(&li->errt);
     if (__ldcg(&li->mode) == 2) {  // line segments did it all: kept index -> text position in closed form
         if (lane) return;
-        const int64_t L = li->L, P = L + li->s, mcl = li->mc, k0 = li->k0, mtot = k0 + mcl;
+        const int64_t L = li->L, P = L + li->s, mcl = li->mc, k0 = li->k0, mtot = k0 + mcl, v0 = li->v0;
         unsigned long long w = __ldcg(&li->cell);  // the last segment's first interior error
         int64_t e = -1, et = -1, ol = 0;
         int32_t kind = kOk;
         if (mtot & 3) {  // LENGTH (R14 / R6): the first char of the incomplete group
             e = mtot - (mtot & 3);
-            et = li->off + line_orig(e - k0, L, P);
+            et = li->off + line_orig(e - k0 + v0, L, P);
             kind = kLength;
         } else {
             uint32_t x = 0;
-            for (int b = 0; b < 4; ++b) x |= uint32_t(in[li->off + line_orig(mcl - 4 + b, L, P)]) << (8 * b);
+            for (int b = 0; b < 4; ++b) x |= uint32_t(in[li->off + line_orig(mcl - 4 + b + v0, L, P)]) << (8 * b);
             int fb = 0, k = 0;
             uint32_t v = 0;
             const uint32_t fk = final_quad(x, lut, pad, lenient, &fb, &k, &v);
@@ -865,7 +1002,7 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
                 kind = int32_t(errk & 7);
             } else if (w < kErrNone) {
                 e = int64_t(w >> 3);
-                et = li->off + line_orig(e - k0, L, P);
+                et = li->off + line_orig(e - k0 + v0, L, P);
                 kind = int32_t(w & 7);
             } else {
                 ol = 3 * (mtot >> 2) - 3 + k;
