@@ -557,11 +557,17 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
     WsLine* li = reinterpret_cast<WsLine*>(base + L.off_mc + 64);
     const WsLine* lic = li;
     launch(ws_line_probe_kernel, 1, 32, s, d_in, m, wt, li, mc);
-    // up to kLineSegs line segments: a text whose layout breaks somewhere (a stray byte) is cut
-    // there and the rest probed again; after the last one the general path takes the rest
-    for (int seg = 0; seg < kLineSegs; ++seg) {
+    // up to kLineSegs line segments (B64_WS_SEGS overrides, >= 1): a text whose layout breaks
+    // somewhere (a stray byte) is cut there and the rest probed again; after the last one the
+    // general path takes the rest
+    static const int nseg = [] {
+        const char* e = std::getenv("B64_WS_SEGS");
+        const int v = e ? std::atoi(e) : kLineSegs;
+        return v < 1 ? 1 : v;
+    }();
+    for (int seg = 0; seg < nseg; ++seg) {
         launch(ws_line_kernel, int64_t(di->sms) * B64_LINE_MINB, kLineThreads, s, d_in, m, wt, li, d_out);
-        launch(ws_line_reprobe_kernel, 1, kPatchThreads, s, d_in, m, wt, li, d_out, seg == kLineSegs - 1 ? 1 : 0);
+        launch(ws_line_reprobe_kernel, 1, kPatchThreads, s, d_in, m, wt, li, d_out, seg == nseg - 1 ? 1 : 0);
     }
     launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot, lic);
     launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc, lic);
@@ -577,7 +583,7 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
            static_cast<const uint8_t*>(comp), wt, uint32_t(a->pad), L.K, int(L.ncta),
            static_cast<const int32_t*>(counts), static_cast<const int64_t*>(cbase), lic, d_out,
            uint32_t((a->flags & B64_ALPHA_LENIENT) ? 1 : 0));
-    g_launches.fetch_add(5 + 2 * kLineSegs, std::memory_order_relaxed);
+    g_launches.fetch_add(5 + 2 * nseg, std::memory_order_relaxed);
     return launched();
 }
 

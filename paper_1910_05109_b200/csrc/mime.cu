@@ -168,8 +168,11 @@ __device__ void probe_layout(const uint8_t* __restrict__ in, int64_t start, int6
     } else if (s >= 1 && s <= 2) {
         // lines of L chars each followed by the separator; the first may be partial (L0 chars,
         // the segment starting mid-line), the last has 1..L chars
+        // L = the second line's length when it is at least the first's (the first is then
+        // partial: a segment starting mid-line), else the first's (the second is the last line,
+        // or holds the irregularity the line kernel will find)
         const int64_t L0 = p - ms;
-        const int64_t L = p2 >= 0 ? p2 - q : L0;  // (two lines only: the first one's length)
+        const int64_t L = (p2 >= 0 && p2 - q >= L0) ? p2 - q : L0;
         if (L >= 32 && (L & 3) == 0 && L < (int64_t(1) << 30) && L0 >= 1 && L0 <= L && (L0 & 3) == 0) {
             const int64_t v0 = L - L0, P = L + s, n1 = me - ms + v0;
             const int64_t nfull = (n1 - 1) / P, r = n1 - nfull * P;
@@ -373,7 +376,7 @@ ws_line_reprobe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsL
 // per unit exactly as the fast kernels do (two LDS.128, 32 table look-ups,
 // 3 x STG.64).  Any whitespace among the chars or a wrong separator flags the
 // layout as broken.  The final quad is left to ws_finalize_kernel; when
-// mc % 4 != 0 (LENGTH) nothing is written, but the layout is still verified.
+// mc % 4 != 0 (LENGTH) the full quads are decoded as interior ones.
 // x / d for 0 <= x < 2^31 and 32 <= d <= 2^30 without an integer division: a float estimate
 // (relative error ~1e-7, so off by at most one here) corrected either way
 __device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, float inv) {
@@ -409,7 +412,10 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
     const uint32_t sep = uint32_t(li->sep);
     const uint32_t sep_mask = S == 2 ? 0xffffu : (S == 1 ? 0xffu : 0u);
     const bool dec = (mc & 3) == 0;
-    const int64_t qfin = dec ? (mc >> 2) - 1 : -1;  // the final quad (ws_finalize_kernel)
+    // the final quad (ws_finalize_kernel); with mc % 4 != 0 (LENGTH -- or a layout guess that a
+    // later block disproves) every full quad is interior and decoded: a segment's verified
+    // blocks must be complete whatever its length turns out to be
+    const int64_t qfin = dec ? (mc >> 2) - 1 : (mc >> 2);
     const int64_t W = (int64_t(gridDim.x) * blockDim.x) >> 5;
     int64_t it = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     // line / column of the warp's first kept char, advanced per grid-stride step without division
@@ -488,13 +494,12 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
                     }
                 }
             }
-            if (!dec) {
+            if (!dec && nq < 8 && K1 == mc) {
                 // LENGTH: the chars of the incomplete group must not be whitespace either
-                if (nq < 8 && K1 == mc) {
-                    const uint8_t* cb = reinterpret_cast<const uint8_t*>(cw);
-                    for (int32_t k = ru + 4 * nq; k < min(ru + 32, krel); ++k) irregular |= lut[cb[k]] == kSkip;
-                }
-            } else {
+                const uint8_t* cb = reinterpret_cast<const uint8_t*>(cw);
+                for (int32_t k = ru + 4 * nq; k < min(ru + 32, krel); ++k) irregular |= lut[cb[k]] == kSkip;
+            }
+            {
                 uint32_t ov[6];
                 dec_pack12(v[0], v[1], v[2], v[3], ov[0], ov[1], ov[2]);
                 dec_pack12(v[4], v[5], v[6], v[7], ov[3], ov[4], ov[5]);
