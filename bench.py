@@ -577,6 +577,15 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from profiles/ncu_traffic.json (an ncu
+    --set full capture of the same workload on one GPU), or None."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(kernel)
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def _tmax(torch, dev, world, ms, args):
     """Max over ranks of a time (the contract's clock: every multi-GPU number is the slowest rank)."""
     if world == 1:
@@ -645,7 +654,7 @@ def scale_rows(b64, synth, torch, dev, world, rank, flush, args, peak):
         ach = alg / (ms * 1e-3) / 1e9
         return {"bound": "hbm", "kernel": kernel, "alg_bytes_all_ranks": alg, "max_rank_ms": round(ms, 4),
                 "achieved": round(ach, 1), "peak": round(peak * world, 1), "unit": "GB/s",
-                "frac": round(ach / (peak * world), 4)}
+                "frac": round(ach / (peak * world), 4), "traffic": ncu_traffic(kernel) if world == 1 else None}
 
     rows = {}
     for name, N, inject, reps in (("configs[2]", 1 << 30, 0, 10), ("configs[4]", 1 << 34, 1000, 5)):
@@ -805,7 +814,7 @@ def batch_row(b64, synth, torch, dev, world, rank, flush, args, peak):
         ach = alg / (ms * 1e-3) / 1e9
         return {"bound": "hbm", "kernel": kernel, "alg_bytes_all_ranks": alg, "max_rank_ms": round(ms, 4),
                 "achieved": round(ach, 1), "peak": round(peak * world, 1), "unit": "GB/s",
-                "frac": round(ach / (peak * world), 4)}
+                "frac": round(ach / (peak * world), 4), "traffic": ncu_traffic(kernel) if world == 1 else None}
 
     return {"strings": len(Ls), "input_bytes": IN, "base64_bytes": B, "n_gpus": world,
             "encode_gbs": round(B / (te_k * 1e-3) / 1e9, 1),
@@ -813,7 +822,7 @@ def batch_row(b64, synth, torch, dev, world, rank, flush, args, peak):
             "decode_gbs_with_combine": round(B / (td_full * 1e-3) / 1e9, 1),
             "encode_ms": round(te_k, 4), "decode_ms_kernel": round(td_k, 4), "decode_ms_with_combine": round(td_full, 4),
             "roofline_encode": roof("enc_generic_kernel", int(sh.byte_stop - sh.byte_start) + out_rank, te_k),
-            "roofline_decode": roof("dec_batch kernels (b64_decode_batch_ex)", out_rank + dec_bytes, td_k),
+            "roofline_decode": roof("dec_batch_bulk_kernel<2>", out_rank + dec_bytes, td_k),
             "first_failing_string": got, "corrupted_strings": int(picks.size),
             "strings_rank0": sh.stop - sh.start,
             "scaling": "strong; strings cut by cumulative bytes" if world > 1 else "1 GPU"}
