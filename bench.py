@@ -948,12 +948,12 @@ def extra_configs(b64, synth, torch, dev, stream, flush, Ev):
     """Side measurements of configs[0], [2], [3] (not the headline)."""
     res = {}
 
-    def timeit(fn, reps=20, do_flush=True):
+    def timeit(fn, reps=20, do_flush=True, sleep=200_000):
         ts = []
         for k in range(reps):
             if do_flush:
                 flush(k)
-            torch.cuda._sleep(200_000)
+            torch.cuda._sleep(sleep)
             a, b = Ev(), Ev()
             a.record(stream)
             fn()
@@ -1057,6 +1057,38 @@ def next_rows(b64, synth, torch, dev, timeit):
     ms = timeit(lambda: ex(t, m, lenient), reps=10)
     res["lenient"] = rate(ms, m, n)
     assert int(info[0].item()) == -1
+    # decode -> consumer: the decoded bytes reduced by a consumer (a byte sum)
+    # chunk by chunk while they sit in an L2-resident 16 MiB ring (b64_decode_consume), against
+    # decoding to HBM and summing the output afterwards
+    ring = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    rbase = ring.data_ptr()
+
+    def _consume(d_chunk, k, off, user, s_):
+        c = int(d_chunk) - rbase
+        acc.add_(ring[c: c + k].sum(dtype=torch.int64))
+
+    cb = b64._lib.CONSUMER_FN(_consume)
+
+    def fused_sum():
+        acc.zero_()
+        b64._lib.check(L.b64_decode_consume(V(t.data_ptr()), m, V(ring.data_ptr()), ring.numel(), ctypes.byref(std),
+                                            cb, None, V(ip), V(ip + 8), V(ip + 16), sp), "b64_decode_consume")
+
+    def separate_sum():
+        acc.zero_()
+        ex(t, m, std)
+        acc.add_(out[:n].sum(dtype=torch.int64))
+
+    want = int(x.sum(dtype=torch.int64).item())
+    for name, fn in (("decode_then_sum", separate_sum), ("decode_consume_sum", fused_sum)):
+        fn()
+        ms = timeit(fn, reps=7, sleep=10_000_000)
+        assert int(info[0].item()) == -1 and int(acc.item()) == want, name
+        res[name] = dict(rate(ms, m, n), note="decode + a consumer reducing the decoded bytes" +
+                         (": decoded to HBM, then summed" if name == "decode_then_sum" else
+                          ": chunks of 21.8 Mi chars through a 16 MiB ring, each summed while in L2"))
+    del ring
     # padding-optional: the base64url text without its '=' (m - 2 chars)
     tu = b64.encode(x, url)[: m - 2]
 

@@ -419,6 +419,28 @@ int b64_decode_host_ex(const uint8_t *h_in, int64_t m, uint8_t *h_out, const b64
                        int64_t ws_bytes, int64_t *d_err_off, int32_t *d_status, int64_t *d_out_len,
                        b64_stream_t s_h2d, b64_stream_t s_comp, b64_stream_t s_d2h, unsigned flags);
 
+/* ---- decode -> consumer through an L2-resident ring ---- */
+/* "process large files in small parts that fit in cache" (the simdjson hand-off,
+ * PAPER.md:642): the text d_in[0..m) (m % 4 == 0, else B64_ELENGTH) is decoded in chunks of C
+ * chars into the caller's device ring d_ring (ring_bytes, 16-byte aligned; C =
+ * b64_consume_chunk_chars(ring_bytes), a multiple of 4096) and after each chunk `consumer` is
+ * called on the host with the chunk's decoded bytes (d_chunk = d_ring, len = 3*C/4 bytes or
+ * fewer for the last chunk, out_offset = their offset in the whole output) and `stream`: it
+ * enqueues its own work on `stream`, which then reads the bytes while they are still in L2,
+ * before the next chunk's decode overwrites the ring -- the decoded text never makes the HBM
+ * round trip.  All work is queued on `stream`; the call returns when every chunk has been
+ * handed over (not when the device finished).  Results as b64_decode_ex: *d_err_off (device,
+ * required) = -1 or the first invalid position, *d_status / *d_out_len (nullable); the last
+ * chunk's exact length is *d_out_len - its out_offset.  Bytes of quads at or after the first
+ * error are unspecified (the consumer still sees every chunk).  Ring sizes of 8-32 MiB keep a
+ * chunk and its consumer in the 126 MB L2. */
+typedef void (*b64_consumer_fn)(const uint8_t *d_chunk, int64_t len, int64_t out_offset, void *user,
+                                b64_stream_t stream);
+int64_t b64_consume_chunk_chars(int64_t ring_bytes);
+int b64_decode_consume(const uint8_t *d_in, int64_t m, uint8_t *d_ring, int64_t ring_bytes, const b64_alphabet *a,
+                       b64_consumer_fn consumer, void *user, int64_t *d_err_off, int32_t *d_status,
+                       int64_t *d_out_len, b64_stream_t stream);
+
 /* ---- batched (BASELINE.json configs[3]) ------------------------------------ */
 /* (d_in / d_out must be valid device pointers when count > 0, even if every
  * string is empty -- the library cannot see the total length without reading

@@ -24,7 +24,7 @@ from ._lib import Alphabet, B64Error, ERR_NONE, ST_BADCHAR, ST_BADPAD, ST_LENGTH
 __all__ = [
     "Alphabet", "B64Error", "alphabet", "lenient_of", "standard", "url", "encoded_len", "decoded_len_max", "encode", "decode",
     "decode_async", "decode_chunk", "decode_finalize", "encode_batch", "decode_batch", "encode_batch_offsets",
-    "decode_batch_offsets", "BatchContext", "DecodeContext", "launch_count", "HostPipeline", "new_info", "decode_unpadded", "decode_ws",
+    "decode_batch_offsets", "BatchContext", "DecodeContext", "decode_consume", "launch_count", "HostPipeline", "new_info", "decode_unpadded", "decode_ws",
     "encode_group", "decode_group", "codec_group", "codec_group_fused", "EncodeStream", "DecodeStream",
     "ERR_NONE",
 ]
@@ -468,6 +468,48 @@ def codec_group(xs, ts, enc_alphabets=None, dec_alphabets=None, enc_outs=None, d
             return eouts, douts, None, None
         err, st = _finalize_n(cells, len(ts), dev, on)
     return eouts, douts, err, st
+
+
+# ------------------------------------------------------------------ decode -> consumer (L2-resident ring)
+
+def decode_consume(t: torch.Tensor, consumer, a: Optional[Alphabet] = None, ring_bytes: int = 16 << 20,
+                   ring: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None):
+    """b64_decode_consume: decode `t` chunk by chunk into an L2-sized device ring and call
+    consumer(chunk, out_offset) after each chunk -- chunk is a uint8 view of the ring holding
+    that chunk's decoded bytes, out_offset their position in the whole output; the consumer
+    queues its own GPU work on the current stream, which reads the bytes while they are in L2
+    (SURVEY.md Sec. 8(f) f3).  Returns (err_off, out_len) after the device finished."""
+    _check_u8(t, "t")
+    dev = t.device
+    with _On(dev, stream) as on:
+        if ring is None:
+            ring = torch.empty(ring_bytes, dtype=torch.uint8, device=dev)
+            on.owns(ring)
+        else:
+            _check_u8(ring, "ring", dev)
+        info = new_info(dev)
+        on.owns(info)
+        base = ring.data_ptr()
+        errors = []
+
+        def _cb(d_chunk, n, off, user, s_):
+            try:
+                k = int(d_chunk) - base
+                with torch.cuda.stream(on.s):
+                    consumer(ring[k: k + n], off)
+            except Exception as e:  # noqa: BLE001 -- re-raised after the C loop returns
+                errors.append(e)
+
+        cb = _lib.CONSUMER_FN(_cb)
+        ip = info.data_ptr()
+        _lib.check(_lib.lib().b64_decode_consume(_ptr(t), t.numel(), _ptr(ring), ring.numel(), _alpha(a), cb, None,
+                                                 ctypes.c_void_p(ip), ctypes.c_void_p(ip + 8),
+                                                 ctypes.c_void_p(ip + 16), on.sp), "b64_decode_consume")
+        if errors:
+            raise errors[0]
+        on.join()
+        err, _, olen = info.tolist()
+    return err, olen
 
 
 # ------------------------------------------------------------------ streaming (carry between calls)

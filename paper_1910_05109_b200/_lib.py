@@ -72,6 +72,8 @@ class Shard(ctypes.Structure):
 
 
 SP = ctypes.POINTER(Stream)
+# b64_consumer_fn: (const uint8_t* d_chunk, int64 len, int64 out_offset, void* user, stream)
+CONSUMER_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p)
 I64P = ctypes.POINTER(ctypes.c_int64)
 
 SIGNATURES = [
@@ -119,6 +121,8 @@ SIGNATURES = [
     ("b64_encode_host_ex", INT, [P, I64, P, AP, P, I64, P, P, P, ctypes.c_uint]),
     ("b64_decode_host_ex", INT, [P, I64, P, AP, P, I64, P, P, P, P, P, P, ctypes.c_uint]),
     ("b64_encode_batch_offsets", INT, [P, I64, P, P]),
+    ("b64_consume_chunk_chars", I64, [I64]),
+    ("b64_decode_consume", INT, [P, I64, P, I64, AP, CONSUMER_FN, P, P, P, P, P]),
     ("b64_decode_batch_offsets", INT, [P, I64, P, P]),
     ("b64_encode_batch", INT, [P, P, I64, P, P, AP, P]),
     ("b64_decode_batch", INT, [P, P, I64, P, P, AP, P, P, P, P]),

@@ -374,4 +374,42 @@ int b64_decode_host_ex(const uint8_t* h_in, int64_t m, uint8_t* h_out, const b64
 }
 #undef B64_CK
 
+// ---------------------------------------------------------------- decode -> consumer (f3)
+int64_t b64_consume_chunk_chars(int64_t ring_bytes) {
+    if (ring_bytes < 3072) return -1;
+    return ring_bytes / 3 * 4 / 4096 * 4096;  // 3C/4 decoded bytes fit the ring; C % 4096 == 0
+}
+
+int b64_decode_consume(const uint8_t* d_in, int64_t m, uint8_t* d_ring, int64_t ring_bytes, const b64_alphabet* a,
+                       b64_consumer_fn consumer, void* user, int64_t* d_err_off, int32_t* d_status,
+                       int64_t* d_out_len, b64_stream_t stream) {
+    if (m < 0 || !alpha_ok(a) || !d_err_off || !consumer) return B64_EINVAL;
+    if (m % 4) return B64_ELENGTH;
+    if (m > 0 && (!d_in || !d_ring)) return B64_EINVAL;
+    const int64_t C = b64_consume_chunk_chars(ring_bytes);
+    if (m > 0 && C <= 0) return B64_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    note(cudaMemsetAsync(d_err_off, 0x7F, sizeof(int64_t), s));
+    if (m == 0) {
+        if (d_out_len) note(cudaMemsetAsync(d_out_len, 0, sizeof(int64_t), s));
+        int r = launched();
+        if (r != B64_OK) return r;
+        g_launches.fetch_sub(1, std::memory_order_relaxed);  // memsets, not kernels
+        return b64_decode_finalize(d_err_off, d_err_off, d_status, stream);
+    }
+    int64_t last_off = 0;
+    for (int64_t off = 0; off < m; off += C) {
+        const int64_t len = (m - off < C) ? m - off : C;
+        const bool fin = off + len == m;
+        const int r = b64_decode_chunk(d_in + off, len, d_ring, a, off, fin ? 1 : 0, d_err_off,
+                                       fin ? d_out_len : nullptr, stream);
+        if (r != B64_OK) return r;
+        consumer(d_ring, len / 4 * 3, off / 4 * 3, user, stream);  // reads the chunk while it is in L2
+        last_off = off;
+    }
+    launch(dec_finalize_len_kernel, 1, 1, s, static_cast<const int64_t*>(d_err_off), d_err_off, d_status, d_out_len,
+           last_off / 4 * 3);
+    return launched();
+}
+
 }  // extern "C"

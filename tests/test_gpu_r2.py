@@ -555,3 +555,41 @@ def test_decode_ws_line_segments(b64):
         o, err = b64.decode_ws(torch.from_numpy(tv).to(DEV))
         assert err == rerr, (name, err, rerr)
         assert np.array_equal(o.cpu().numpy(), ref), name
+
+
+# ------------------------------------------------------------------ decode -> consumer (f3)
+
+def test_decode_consume_vs_oracle(b64):
+    """b64_decode_consume: chunks decoded into a small ring and handed to a consumer that copies
+    them out -- the reassembled output, err_off and out_len equal the oracle's (valid text with
+    every pad count, an error in the middle chunk, a text shorter than one chunk)."""
+    for n, bad_at in ((3_000_001, None), (3_000_002, 1_500_003), (1_234, None), (3_000_000, None)):
+        x = synth.data(n, seed=n)
+        t = oracle.encode(x)
+        if bad_at is not None:
+            t = t.copy()
+            t[bad_at] = ord("!")
+        ref, rerr, _ = oracle.decode(t)
+        full = torch.zeros(b64.decoded_len_max(t.size), dtype=torch.uint8, device=DEV)
+        seen = []
+
+        def consumer(chunk, off):
+            full[off: off + chunk.numel()].copy_(chunk)
+            seen.append((off, chunk.numel()))
+
+        err, olen = b64.decode_consume(torch.from_numpy(t).to(DEV), consumer, ring_bytes=1 << 20)
+        assert err == rerr and olen == ref.size, (n, err, rerr, olen)
+        assert np.array_equal(full[:olen].cpu().numpy(), ref), n
+        assert sum(k for _, k in seen) == full.numel() and [o for o, _ in seen] == sorted(o for o, _ in seen)
+
+
+def test_decode_consume_sum(b64):
+    """A reducing consumer (the decoded bytes never leave L2): the per-chunk sums add up to the
+    sum of the oracle's decode."""
+    x = synth.data(20_000_004, seed=9)  # n % 3 == 0: no padding, every decoded byte is data
+    x = x[:20_000_004 - 20_000_004 % 3]
+    t = torch.from_numpy(oracle.encode(x)).to(DEV)
+    acc = torch.zeros(1, dtype=torch.int64, device=DEV)
+    err, olen = b64.decode_consume(t, lambda c, off: acc.add_(c.sum(dtype=torch.int64)), ring_bytes=8 << 20)
+    assert err == -1 and olen == x.size
+    assert int(acc.item()) == int(x.sum(dtype=np.int64))
