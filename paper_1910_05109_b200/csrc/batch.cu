@@ -46,10 +46,21 @@ dec_batch_prep_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict_
     const int64_t a0 = in_off[0], o0 = out_off[0];
     bool bad = g0 == 0 && (((reinterpret_cast<uintptr_t>(in + a0) & 31) != 0) ||
                            ((reinterpret_cast<uintptr_t>(out + o0) & 15) != 0));
-    for (int64_t i = g0; i < count; i += gs) {
-        err[i] = int64_t(kErrNone);
-        const int64_t a = in_off[i], L = in_off[i + 1] - a;
-        bad |= (L & 3) != 0 || L < 0 || out_off[i] - o0 != 3 * ((a - a0) >> 2);
+    // 4 consecutive strings per thread per step, every load of a step issued before its checks
+    for (int64_t i0 = 4 * g0; i0 < count; i0 += 4 * gs) {
+        int64_t a[5], o[4];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) a[j] = i0 + j <= count ? in_off[i0 + j] : 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = i0 + j < count ? out_off[i0 + j] : 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (i0 + j < count) {
+                err[i0 + j] = int64_t(kErrNone);
+                const int64_t L = a[j + 1] - a[j];
+                bad |= (L & 3) != 0 || L < 0 || o[j] - o0 != 3 * ((a[j] - a0) >> 2);
+            }
+        }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) ctx->generic = 1u;
 }
@@ -206,38 +217,57 @@ dec_batch_strfinal_kernel(const uint8_t* __restrict__ in, const int64_t* __restr
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     uint32_t legit = 0;
     int64_t bad_idx = INT64_MAX;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t a = in_off[i], L = in_off[i + 1] - a;
-        unsigned long long w = static_cast<unsigned long long>(err[i]);  // the bulk pass's packed word
-        int64_t ol = 0;
-        if (L >= 4) {
-            const uint32_t x = ld32(in + a + L - 4);  // 4-byte aligned: the layout check passed
-            legit += uint32_t(((x >> 16) & 0xffu) == tab.pad) + uint32_t((x >> 24) == tab.pad);
-            int bad, k;
-            uint32_t v;
-            const uint32_t kind = final_quad(x, lut, tab.pad, tab.lenient, &bad, &k, &v);
-            if (kind == kOk) {
-                // strict: the bulk pass already wrote the exact bytes -- a canonical final quad's
-                // dropped bits are zero, so the pad candidate (0x40 = 1 << 6) only sets a bit of
-                // a discarded byte; lenient: non-zero dropped bits can carry into a kept byte
-                if (tab.lenient) store_bytes(out + out_off[i] + 3 * ((L >> 2) - 1), v, k);
-                ol = 3 * ((L >> 2) - 1) + k;
-            } else {
-                const unsigned long long fw = pack_err(L - 4 + bad, kind);
-                w = fw < w ? fw : w;
+    // 4 consecutive strings per thread per step: their offsets and words, then their final
+    // quads, are loaded together (two dependent DRAM round trips per step, not per string)
+    const int64_t gs = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i0 = 4 * (int64_t(blockIdx.x) * blockDim.x + threadIdx.x); i0 < count; i0 += 4 * gs) {
+        int64_t a[5];
+        unsigned long long wv[4];
+        uint32_t x[4];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) a[j] = i0 + j <= count ? in_off[i0 + j] : 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) wv[j] = i0 + j < count ? static_cast<unsigned long long>(err[i0 + j]) : kErrNone;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t L = a[j + 1] - a[j];
+            x[j] = (i0 + j < count && L >= 4) ? ld32(in + a[j] + L - 4) : 0u;  // 4-byte aligned: layout checked
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = i0 + j;
+            if (i >= count) break;
+            const int64_t L = a[j + 1] - a[j];
+            unsigned long long w = wv[j];  // the bulk pass's packed word
+            int64_t ol = 0;
+            if (L >= 4) {
+                legit += uint32_t(((x[j] >> 16) & 0xffu) == tab.pad) + uint32_t((x[j] >> 24) == tab.pad);
+                int bad, k;
+                uint32_t v;
+                const uint32_t kind = final_quad(x[j], lut, tab.pad, tab.lenient, &bad, &k, &v);
+                if (kind == kOk) {
+                    // strict: the bulk pass already wrote the exact bytes -- a canonical final quad's
+                    // dropped bits are zero, so the pad candidate (0x40 = 1 << 6) only sets a bit of
+                    // a discarded byte; lenient: non-zero dropped bits can carry into a kept byte
+                    if (tab.lenient) store_bytes(out + out_off[i] + 3 * ((L >> 2) - 1), v, k);
+                    ol = 3 * ((L >> 2) - 1) + k;
+                } else {
+                    const unsigned long long fw = pack_err(L - 4 + bad, kind);
+                    w = fw < w ? fw : w;
+                }
             }
+            int32_t st;
+            int64_t e;
+            if (w >= kErrNone) {
+                st = kOk; e = -1;
+            } else {
+                e = int64_t(w >> 3); st = int32_t(w & 7); ol = 3 * (e >> 2);
+                if (bad_idx == INT64_MAX) bad_idx = index_base + i;  // i only grows per thread
+            }
+            err[i] = e;
+            if (status) status[i] = st;
+            if (out_len) out_len[i] = ol;
         }
-        int32_t st;
-        int64_t e;
-        if (w >= kErrNone) {
-            st = kOk; e = -1;
-        } else {
-            e = int64_t(w >> 3); st = int32_t(w & 7); ol = 3 * (e >> 2);
-            if (bad_idx == INT64_MAX) bad_idx = index_base + i;  // i only grows per thread
-        }
-        err[i] = e;
-        if (status) status[i] = st;
-        if (out_len) out_len[i] = ol;
     }
     if (first_bad) {  // the batch's first failing string: warp MIN, one atomic per warp
         const unsigned long long b = static_cast<unsigned long long>(bad_idx);

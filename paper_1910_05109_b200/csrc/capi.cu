@@ -927,7 +927,7 @@ int b64_decode_batch_fast(const uint8_t* d_in, const int64_t* d_in_off, int64_t 
         launch(dec_batch_bulk_kernel<2>, int64_t(di->sms) * cap_bps(di->occ_batch_bulk), kThreads, s, d_in, d_in_off,
                d_out, d_out_off, count, bt, cells, ctx);
         if ((r = launched()) != B64_OK) return r;
-        const int64_t per = clamp_grid((count + kThreads - 1) / kThreads, INT32_MAX);  // one string per thread
+        const int64_t per = clamp_grid((count + 4 * kThreads - 1) / (4 * kThreads), INT32_MAX);  // 4 strings per thread
         launch(dec_batch_strfinal_kernel, per, kThreads, s, d_in, d_in_off, d_out, d_out_off, count, dec_tab(a),
                d_err_off, d_status, d_out_len, index_base, reinterpret_cast<unsigned long long*>(d_first_bad), ctx);
         if ((r = launched()) != B64_OK) return r;
