@@ -36,6 +36,7 @@
 namespace b64 {
 
 constexpr uint32_t kPadCand = 0x40u;  // table value of the pad char in the bulk pass
+constexpr uint32_t kBadSlots = 64;    // per warp: 32-char windows with a bad char noted for after the loop
 
 __global__ void __launch_bounds__(kThreads)
 dec_batch_prep_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict__ in_off, const uint8_t* out,
@@ -107,7 +108,10 @@ dec_batch_bulk_kernel(const uint8_t* __restrict__ in_base, const int64_t* __rest
                       unsigned long long* __restrict__ cells, BatchCtx* ctx) {
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];
+    __shared__ unsigned long long s_badw[kThreads / 32][kBadSlots];  // windows with a bad char: chunk << 5 | lane
+    __shared__ uint32_t s_nbad[kThreads / 32];
     griddep_launch_dependents();
+    if (threadIdx.x < kThreads / 32) s_nbad[threadIdx.x] = 0;
     griddep_wait();
     if (ctx->generic) return;  // the layout is not the concatenation's: step 4 does it all
     const int lane = threadIdx.x & 31;
@@ -171,8 +175,11 @@ dec_batch_bulk_kernel(const uint8_t* __restrict__ in_base, const int64_t* __rest
                 __syncwarp();
                 if (err & (kInvalid | kPadCand)) {  // rare: a bad char or a pad candidate in my 32 chars
                     if (err & kPadCand) npad += count_pads(xr[i], pad4);
-                    if (err & kInvalid)
-                        report_window(pcur, a0 + int64_t(c) * 1024 + lane * 32, 32, lut, in_off, count, cells);
+                    if (err & kInvalid) {  // noted here, reported after the loop (keeps the loop's registers few)
+                        const uint32_t slot = atomicAdd(&s_nbad[threadIdx.x >> 5], 1u);
+                        if (slot < kBadSlots)
+                            s_badw[threadIdx.x >> 5][slot] = (static_cast<unsigned long long>(c) << 5) | lane;
+                    }
                 }
                 pout += sout;
                 pcur += sin;
@@ -192,6 +199,18 @@ dec_batch_bulk_kernel(const uint8_t* __restrict__ in_base, const int64_t* __rest
     }
     npad = __reduce_add_sync(kFull, npad);
     if (lane == 0 && npad) atomicAdd(&ctx->eq, static_cast<unsigned long long>(npad));
+    // the noted windows: every string with a non-alphabet char there gets its first one
+    __syncwarp();
+    const uint32_t nb = s_nbad[threadIdx.x >> 5];
+    if (nb > kBadSlots) {  // more than the notes hold: the per-string fallback redoes the batch exactly
+        if (lane == 0) ctx->generic = 1u;
+    } else {
+        for (uint32_t k = lane; k < nb; k += 32) {
+            const unsigned long long wv = s_badw[threadIdx.x >> 5][k];
+            const int64_t p = int64_t(wv >> 5) * 1024 + int64_t(wv & 31) * 32;
+            report_window(in + p, a0 + p, 32, lut, in_off, count, cells);
+        }
+    }
 }
 
 // Step 3: one thread per string.  The final quad under R6 / R16 (lenient: its 1-3 bytes

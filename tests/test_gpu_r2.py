@@ -593,3 +593,23 @@ def test_decode_consume_sum(b64):
     err, olen = b64.decode_consume(t, lambda c, off: acc.add_(c.sum(dtype=torch.int64)), ring_bytes=8 << 20)
     assert err == -1 and olen == x.size
     assert int(acc.item()) == int(x.sum(dtype=np.int64))
+
+
+def test_batch_fast_path_many_errors(b64):
+    """So many corrupted windows that a warp's note list of the bulk pass overflows (the per-string
+    fallback then redoes the batch): results still equal the oracle's; and a moderately corrupted
+    batch (reported from the notes) too."""
+    text, toff = _batch_case(20000, seed=23, hi=600)
+    count = toff.size - 1
+    rng = np.random.default_rng(23)
+    for frac in (0.02, 0.6):
+        t = text.copy()
+        for s in rng.choice(count, int(frac * count), replace=False):
+            L = toff[s + 1] - toff[s]
+            for _ in range(3):
+                t[toff[s] + rng.integers(0, L)] = ord("!")
+        rout, roff, rst, rerr, rlen = oracle.decode_batch(t, toff)
+        out, oo, st, err, olen = b64.decode_batch(torch.from_numpy(t).to(DEV), torch.from_numpy(toff).to(DEV))
+        assert np.array_equal(st.cpu().numpy(), rst), frac
+        assert np.array_equal(err.cpu().numpy(), rerr), frac
+        assert np.array_equal(olen.cpu().numpy(), rlen), frac
