@@ -240,3 +240,32 @@ int main(void) {
     from paper_1910_05109_b200 import _lib
 
     assert _lib.ERR_NONE == 0x7F7F7F7F7F7F7F7F
+
+
+def test_consume_and_shard_host_logic(L):
+    """b64_decode_consume / b64_consume_chunk_chars / b64_*_shard: synchronous argument errors and
+    the host-only sizes (no device touched)."""
+    from paper_1910_05109_b200 import _lib
+
+    V = ctypes.c_void_p
+    a = L.b64_alphabet_standard()
+    assert L.b64_consume_chunk_chars(3071) == -1
+    assert L.b64_consume_chunk_chars(3 << 20) == (4 << 20)
+    assert L.b64_consume_chunk_chars(16 << 20) % 4096 == 0
+    assert 3 * L.b64_consume_chunk_chars(16 << 20) // 4 <= (16 << 20)
+    cb = _lib.CONSUMER_FN(lambda *args: None)
+    assert L.b64_decode_consume(V(8), 6, V(8), 1 << 20, a, cb, None, V(8), None, None, None) == -2  # m % 4
+    assert L.b64_decode_consume(V(8), 8, V(8), 1 << 20, a, cb, None, None, None, None, None) == -1  # no err_off
+    assert L.b64_decode_consume(V(8), 8, V(8), 100, a, cb, None, V(8), None, None, None) == -1     # ring too small
+    sh = _lib.Shard()
+    assert L.b64_encode_shard(10, 0, 0, ctypes.byref(sh)) == -1
+    assert L.b64_decode_shard(10, 2, 0, ctypes.byref(sh)) == -2
+    assert L.b64_decode_shard(4096, 2, 2, ctypes.byref(sh)) == -1
+    # the cut rule: 768-byte / 1024-char multiples, the last rank owns the tail
+    total = 0
+    for r in range(3):
+        assert L.b64_encode_shard(768 * 10 + 5, 3, r, ctypes.byref(sh)) == 0
+        assert sh.start % 768 == 0 and sh.out_start == 4 * (sh.start // 3)
+        assert sh.is_final == (r == 2)
+        total += sh.stop - sh.start
+    assert total == 768 * 10 + 5 and sh.out_len == L.b64_encoded_len(sh.stop - sh.start)
