@@ -54,7 +54,8 @@ lengths = st.one_of(st.integers(0, 40), st.integers(0, 5000), st.integers(760, 8
 @given(n=lengths, kind=st.sampled_from(["std", "url", "custom"]), aseed=st.integers(0, 50),
        off_in=st.sampled_from([0, 0, 1, 3, 8]), off_out=st.sampled_from([0, 0, 1, 2, 16]),
        lenient=st.booleans(), k_bad=st.integers(0, 3), seed=st.integers(0, 10_000),
-       api=st.sampled_from(["single", "ctx", "chunk", "group", "codec", "stream", "batch", "unpadded", "ws"]))
+       api=st.sampled_from(["single", "ctx", "chunk", "group", "codec", "stream", "batch", "unpadded", "ws",
+                            "ws_lines", "consume"]))
 def test_fuzz_encode_decode_vs_oracle(b64, n, kind, aseed, off_in, off_out, lenient, k_bad, seed, api):
     chars, pad, alpha = _alpha(b64, kind, aseed)
     if lenient:
@@ -157,6 +158,36 @@ def test_fuzz_encode_decode_vs_oracle(b64, n, kind, aseed, off_in, off_out, leni
         out, err = b64.decode_ws(_dev(t_w, off_in), alpha)
         assert err == rerr, (api, n, err, rerr, rst)
         assert np.array_equal(out.cpu().numpy(), ref)
+        return
+    elif api == "ws_lines":  # MIME-structured text above the one-launch size, with stray bytes (line segments)
+        if chars.translate(None, b" \t\n\r\x0b\x0c") != chars:
+            return
+        rng = np.random.default_rng(seed)
+        pre = oracle.encode(synth.data(3 * (150_000 + seed), seed=seed + 2), chars, pad)
+        big = np.concatenate([pre, text])
+        L = int(rng.choice([64, 76, 128]))
+        sep = [b"\r\n", b"\n", b" "][seed % 3]
+        lines = [big[i: i + L] for i in range(0, big.size, L)]
+        t_l = np.concatenate([np.concatenate([ln, np.frombuffer(sep, np.uint8)]) for ln in lines])
+        for _ in range(int(rng.integers(0, 5))):  # stray whitespace bytes / a doubled separator
+            at = int(rng.integers(0, t_l.size))
+            t_l = np.insert(t_l, at, np.frombuffer([b" ", b"\t", b"\n", b"\r\n"][int(rng.integers(0, 4))], np.uint8))
+        ref, rerr, rst = oracle.decode_ws(t_l, chars, pad, lenient=lenient)
+        out, err = b64.decode_ws(_dev(t_l, off_in), alpha)
+        assert err == rerr, (api, n, err, rerr, rst, L, sep)
+        assert np.array_equal(out.cpu().numpy(), ref), (api, n, L, sep)
+        return
+    elif api == "consume":  # decode -> consumer through a small ring, reassembled by the consumer
+        full = torch.zeros(3 * (m // 4) + 8, dtype=torch.uint8, device=DEV)
+
+        def consumer(chunk, off):
+            full[off: off + chunk.numel()].copy_(chunk)
+
+        ring = 3072 * (1 + seed % 7)
+        err, olen = b64.decode_consume(_dev(text, off_in), consumer, alpha, ring_bytes=ring)
+        assert err == rerr and (err >= 0 or olen == ref.size), (api, n, err, rerr)
+        assert np.array_equal(full[: (olen if err < 0 else 3 * (err // 4))].cpu().numpy(),
+                              ref[: (olen if err < 0 else 3 * (err // 4))])
         return
     else:  # batch of the text cut into pieces at random quad boundaries, plus the text itself
         rng = np.random.default_rng(seed)
