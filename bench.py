@@ -1136,9 +1136,10 @@ def next_rows(b64, synth, torch, dev, timeit):
     cell = torch.empty(1, dtype=torch.int64, device=dev)
     piece = 64 << 20
 
-    def streamed():
+    def streamed(flags=0):
         stt = b64._lib.Stream()
-        L.b64_decode_stream_begin(ctypes.byref(stt), V(carry.data_ptr()), V(cell.data_ptr()), sp)
+        b64._lib.check(L.b64_decode_stream_begin_ex(ctypes.byref(stt), V(carry.data_ptr()), V(cell.data_ptr()),
+                                                    flags, sp), "stream_begin")
         o, p_ = 0, 0
         n_out = ctypes.c_int64(0)
         while p_ < m:
@@ -1154,6 +1155,12 @@ def next_rows(b64, synth, torch, dev, timeit):
     ms = timeit(streamed, reps=5)
     assert int(info[0].item()) == -1 and int(info[2].item()) == n
     res["streaming_64MiB_pieces"] = rate(ms, m, n)
+    # the same with B64_STREAM_OVERLAP (the text is resident: each piece's bulk overlaps the drain
+    # of the previous piece's kernel)
+    ms = timeit(lambda: streamed(b64._lib.STREAM_OVERLAP), reps=5)
+    assert int(info[0].item()) == -1 and int(info[2].item()) == n
+    res["streaming_64MiB_pieces_overlap"] = dict(rate(ms, m, n), note="b64_decode_stream_begin_ex("
+                                                 "B64_STREAM_OVERLAP): resident text, pieces overlap")
     del x, t, tu, out
     torch.cuda.empty_cache()
     # one-sided peer combine, world 1 (per-combine kernel latency)

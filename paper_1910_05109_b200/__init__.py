@@ -580,16 +580,24 @@ class DecodeStream(_StreamBase):
     update(t) returns the bytes of the quads completed so far (the last 1-4 chars are
     held back); end() returns (tail bytes tensor, info) with info = int64[3] device tensor
     (err_off, status, out_len) for the whole concatenated text, exactly as decode_async.
-    All calls run on the CUDA stream fixed at construction."""
+    All calls run on the CUDA stream fixed at construction.
 
-    def __init__(self, a: Optional[Alphabet] = None, device=None, stream: Optional[torch.cuda.Stream] = None):
+    overlap=True: b64_decode_stream_begin_ex with B64_STREAM_OVERLAP -- each piece's
+    bulk starts while the previous piece drains; the caller guarantees every piece's
+    input is written before construction, nothing else on the stream writes any
+    piece's input or output until end(), and inputs do not overlap outputs
+    (include/b64gpu.h)."""
+
+    def __init__(self, a: Optional[Alphabet] = None, device=None, stream: Optional[torch.cuda.Stream] = None,
+                 overlap: bool = False):
         super().__init__(a, device, stream)
         with _On(self.dev, self.stream) as on:
             self.carry = torch.zeros(8, dtype=torch.uint8, device=self.dev)
             self.cell = torch.empty(1, dtype=torch.int64, device=self.dev)
             on.owns(self.carry, self.cell)
-            _lib.check(_lib.lib().b64_decode_stream_begin(ctypes.byref(self.st), _ptr(self.carry), _ptr(self.cell),
-                                                          on.sp), "b64_decode_stream_begin")
+            _lib.check(_lib.lib().b64_decode_stream_begin_ex(ctypes.byref(self.st), _ptr(self.carry), _ptr(self.cell),
+                                                             _lib.STREAM_OVERLAP if overlap else 0, on.sp),
+                       "b64_decode_stream_begin_ex")
 
     def update(self, t: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         _check_u8(t, "t", self.dev)

@@ -72,6 +72,7 @@ class Shard(ctypes.Structure):
 
 
 SP = ctypes.POINTER(Stream)
+STREAM_OVERLAP = 1  # B64_STREAM_OVERLAP
 # b64_consumer_fn: (const uint8_t* d_chunk, int64 len, int64 out_offset, void* user, stream)
 CONSUMER_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p)
 I64P = ctypes.POINTER(ctypes.c_int64)
@@ -106,6 +107,7 @@ SIGNATURES = [
     ("b64_encode_stream_update", INT, [SP, P, I64, P, AP, I64P, P]),
     ("b64_encode_stream_end", INT, [SP, P, AP, I64P, P]),
     ("b64_decode_stream_begin", INT, [SP, P, P, P]),
+    ("b64_decode_stream_begin_ex", INT, [SP, P, P, ctypes.c_uint32, P]),
     ("b64_decode_stream_update", INT, [SP, P, I64, P, AP, I64P, P]),
     ("b64_decode_stream_end", INT, [SP, P, AP, P, P, P, I64P, P]),
     ("b64_peer_combine_bytes", I64, [I64]),

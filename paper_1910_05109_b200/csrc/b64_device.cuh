@@ -39,6 +39,15 @@ struct DecTab { uint32_t w[64]; uint32_t pad; uint32_t lenient; };  // dec[256] 
 // kernel waits for its predecessor's memory before touching global memory.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+// A pointer whose value is (re)defined by an asm volatile placed after griddep_wait(): no load
+// through it -- not even an LDG.CONSTANT of a `const __restrict__` parameter, which the
+// compiler treats as invariant and may hoist -- can be scheduled before the wait, where it
+// would read the predecessor grid's output before it is written (tools/check_pdl_order.py).
+template <class T>
+__device__ __forceinline__ T* after_wait(T* p) {
+    asm volatile("" : "+l"(p));
+    return p;
+}
 
 __device__ __forceinline__ unsigned long long pack_err(int64_t pos, uint32_t kind) {
     return ((unsigned long long)pos << 3) | kind;
@@ -106,6 +115,37 @@ __device__ __forceinline__ uint2 lds64(uint32_t a) {
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
     return v;
+}
+
+// mbarrier + bulk async copy (TMA, non-tensor form) for the staged batch encode:
+// one elected lane arms the barrier with the byte count and issues the copies;
+// every lane waits on the phase parity before reading the stage.
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// global -> shared bulk copy: src / dst 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 v;
@@ -352,6 +392,7 @@ static_assert(sizeof(BatchCtx) == 32, "B64_BATCH_CTX_BYTES");
 template <int D>
 __global__ void enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab,
                                 uint32_t pad);
+template <int TMA>
 __global__ void enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab,
                                    uint32_t pad);
 // A streaming decode's join (stream.cu): the quad made of the H held chars and the piece's
@@ -366,7 +407,7 @@ struct StreamJoin {
     int32_t H;           // held chars before the piece
     int32_t active;
 };
-template <int D>
+template <int D, bool EARLY = false>
 __global__ void dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
                                 int64_t* __restrict__ out_len, const int64_t* __restrict__ m_dev, StreamJoin join);

@@ -43,6 +43,8 @@ dec_batch_prep_kernel(const uint8_t* __restrict__ in, const int64_t* __restrict_
                       const int64_t* __restrict__ out_off, int64_t count, int64_t* __restrict__ err, BatchCtx* ctx) {
     griddep_launch_dependents();
     griddep_wait();
+    in_off = after_wait(in_off);  // the offsets may come from the kernel before (batch_offsets)
+    out_off = after_wait(out_off);
     const int64_t g0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x, gs = int64_t(gridDim.x) * blockDim.x;
     const int64_t a0 = in_off[0], o0 = out_off[0];
     bool bad = g0 == 0 && (((reinterpret_cast<uintptr_t>(in + a0) & 31) != 0) ||

@@ -54,6 +54,17 @@ cudaError_t group_occupancy(int (&occ)[4]) {
     return cudaSuccess;
 }
 
+// The batch / misaligned encode: the TMA-staged loop (enc_generic_kernel<1>) unless
+// B64_ENC_TMA=0 selects the direct-load one (kept for A/B measurement).
+using EncGenericFn = void (*)(const uint8_t*, uint8_t*, Offsets, EncTab, uint32_t);
+EncGenericFn enc_generic_fn() {
+    static const EncGenericFn f = [] {
+        const char* e = std::getenv("B64_ENC_TMA");
+        return (e && e[0] == '0') ? EncGenericFn(enc_generic_kernel<0>) : EncGenericFn(enc_generic_kernel<1>);
+    }();
+    return f;
+}
+
 const DevInfo* dev_info() {
     int d = 0;
     if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) return nullptr;
@@ -66,7 +77,7 @@ const DevInfo* dev_info() {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[1], dec_fast_kernel<1>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[2], dec_fast_kernel<2>, kThreads, 0) ||
         group_occupancy(info.occ_group) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_fn(), kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_batch_bulk, dec_batch_bulk_kernel<2>, kThreads, 0))
         return nullptr;
@@ -354,14 +365,14 @@ int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabe
     } else {
         Offsets off{nullptr, nullptr, 1, n};
         const int64_t blocks = clamp_grid((n / 12 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_gen);
-        launch(enc_generic_kernel, blocks, kThreads, s, d_in, d_out, off, enc_tab(a), a->pad);
+        launch(enc_generic_fn(), blocks, kThreads, s, d_in, d_out, off, enc_tab(a), a->pad);
     }
     return launched();
 }
 
 static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t base,
                          int is_final, int64_t* cell, int64_t* out_len, cudaStream_t s,
-                         const StreamJoin* join = nullptr, bool* joined = nullptr) {
+                         const StreamJoin* join = nullptr, bool* joined = nullptr, bool early = false) {
     const DevInfo* di = dev_info();
     if (!di) return B64_ECUDA;
     unsigned long long* c = reinterpret_cast<unsigned long long*>(cell);
@@ -370,7 +381,8 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
         const int64_t nchunk = (m / 4) / 256;
         const int dd = dec_depth(m);
         const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(di->occ_dec_fast[dd]));
-        auto k = pick2(dd, dec_fast_kernel<1>, dec_fast_kernel<2>);
+        auto k = early ? pick2(dd, dec_fast_kernel<1, true>, dec_fast_kernel<2, true>)
+                       : pick2(dd, dec_fast_kernel<1>, dec_fast_kernel<2>);
         StreamJoin sj = {};
         if (join && joined) {  // the stream join rides along (its last thread)
             sj = *join;
@@ -397,7 +409,9 @@ static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b
             sj = *join;
             *joined = true;
         }
-        launch(dd == 2 ? dec_fastu_pick<2>(ws) : dec_fastu_pick<1>(ws), blocks, kThreads, s, d_in, m, d_out,
+        const DecFastuFn kf = early ? (dd == 2 ? dec_fastu_pick<2, true>(ws) : dec_fastu_pick<1, true>(ws))
+                                    : (dd == 2 ? dec_fastu_pick<2>(ws) : dec_fastu_pick<1>(ws));
+        launch(kf, blocks, kThreads, s, d_in, m, d_out,
                dec_tab(a), base, is_final, c, out_len, ub, sj);
     } else {
         Offsets off{nullptr, nullptr, 1, m};
@@ -875,7 +889,7 @@ int b64_encode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count
     if (!di) return B64_ECUDA;
     Offsets off{d_in_off, d_out_off, count, 0};
     const int64_t blocks = int64_t(di->sms) * di->occ_enc_gen;
-    launch(enc_generic_kernel, blocks, kThreads, reinterpret_cast<cudaStream_t>(stream), d_in, d_out, off, enc_tab(a), a->pad);
+    launch(enc_generic_fn(), blocks, kThreads, reinterpret_cast<cudaStream_t>(stream), d_in, d_out, off, enc_tab(a), a->pad);
     return launched();
 }
 

@@ -10,20 +10,22 @@ extern "C" {
 // device; the held bytes themselves live in the caller's device carry buffer.
 namespace {
 enum { kStIdle = 0, kStEncode = 1, kStDecode = 2, kStDone = 3 };
+constexpr int32_t kStOverlap = 0x100;  // decode state bit: B64_STREAM_OVERLAP
+inline int32_t st_kind(const b64_stream* st) { return st->state & 0xff; }
 }
 
 int64_t b64_stream_update_len(const b64_stream* st, int64_t len) {
     if (!st || len < 0) return -1;
     const int64_t A = st->held + len;
-    if (st->state == kStEncode) return 4 * (A / 3);                 // whole triples
-    if (st->state == kStDecode) return A > 0 ? 3 * ((A - 1) / 4) : 0;  // the last 1..4 chars are held
+    if (st_kind(st) == kStEncode) return 4 * (A / 3);                 // whole triples
+    if (st_kind(st) == kStDecode) return A > 0 ? 3 * ((A - 1) / 4) : 0;  // the last 1..4 chars are held
     return -1;
 }
 
 int64_t b64_stream_end_len(const b64_stream* st) {
     if (!st) return -1;
-    if (st->state == kStEncode) return st->held > 0 ? 4 : 0;  // the padded tail
-    if (st->state == kStDecode) return (st->consumed > 0 && st->consumed % 4 == 0) ? 3 : 0;
+    if (st_kind(st) == kStEncode) return st->held > 0 ? 4 : 0;  // the padded tail
+    if (st_kind(st) == kStDecode) return (st->consumed > 0 && st->consumed % 4 == 0) ? 3 : 0;
     return -1;
 }
 
@@ -80,21 +82,28 @@ int b64_encode_stream_end(b64_stream* st, uint8_t* d_out, const b64_alphabet* a,
     return B64_OK;
 }
 
-int b64_decode_stream_begin(b64_stream* st, uint8_t* d_carry, int64_t* d_err_min, b64_stream_t stream) {
-    if (!st || !d_carry || !d_err_min) return B64_EINVAL;
+int b64_decode_stream_begin_ex(b64_stream* st, uint8_t* d_carry, int64_t* d_err_min, uint32_t flags,
+                                b64_stream_t stream) {
+    if (!st || !d_carry || !d_err_min || (flags & ~B64_STREAM_OVERLAP)) return B64_EINVAL;
+    // a memset, not a kernel: the first piece is fully ordered after everything before the begin
+    // call (no programmatic edge crosses it), which the overlap mode relies on
     if (cudaMemsetAsync(d_err_min, 0x7F, sizeof(int64_t), reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
         return B64_ECUDA;
     st->consumed = st->produced = 0;
     st->held = 0;
-    st->state = kStDecode;
+    st->state = kStDecode | ((flags & B64_STREAM_OVERLAP) ? kStOverlap : 0);
     st->d_carry = d_carry;
     st->d_err_min = d_err_min;
     return B64_OK;
 }
 
+int b64_decode_stream_begin(b64_stream* st, uint8_t* d_carry, int64_t* d_err_min, b64_stream_t stream) {
+    return b64_decode_stream_begin_ex(st, d_carry, d_err_min, 0u, stream);
+}
+
 int b64_decode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a,
                              int64_t* n_out, b64_stream_t stream) {
-    if (!st || st->state != kStDecode || m < 0 || !alpha_ok(a) || (m > 0 && !d_in)) return B64_EINVAL;
+    if (!st || st_kind(st) != kStDecode || m < 0 || !alpha_ok(a) || (m > 0 && !d_in)) return B64_EINVAL;
     const int64_t H = st->held, A = H + m;
     const int64_t Q = A > 0 ? (A - 1) / 4 : 0;  // the last 1..4 chars are always held
     if (Q > 0 && !d_out) return B64_EINVAL;
@@ -105,12 +114,15 @@ int b64_decode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t m, uin
     const int64_t skip = join ? 4 - H : 0, qb = Q - join;  // whole quads read straight from the piece
     // the join (held chars + the piece's head, and the new carry) rides along with the piece's
     // bulk kernel when that is the fast one; otherwise it is a one-thread kernel of its own
+    // overlap mode (B64_STREAM_OVERLAP): from the second piece on, the bulk runs before
+    // griddepcontrol.wait, i.e. while the previous piece's kernel drains (R15)
+    const bool early = (st->state & kStOverlap) && st->consumed > 0;
     const StreamJoin sj = {st->d_carry, d_in, d_out, m, st->consumed - H, int32_t(H), 1};
     bool joined = false;
     int r = B64_OK;
     if (qb > 0) {
         r = decode_launch(d_in + skip, 4 * qb, d_out + 3 * join, a, st->consumed + skip, 0, st->d_err_min, nullptr,
-                          s, &sj, &joined);
+                          s, &sj, &joined, early);
         if (r != B64_OK) return r;
     }
     if (!joined) {
@@ -127,7 +139,7 @@ int b64_decode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t m, uin
 
 int b64_decode_stream_end(b64_stream* st, uint8_t* d_out, const b64_alphabet* a, int64_t* d_err_off,
                           int32_t* d_status, int64_t* d_out_len, int64_t* n_out, b64_stream_t stream) {
-    if (!st || st->state != kStDecode || !alpha_ok(a) || !d_err_off) return B64_EINVAL;
+    if (!st || st_kind(st) != kStDecode || !alpha_ok(a) || !d_err_off) return B64_EINVAL;
     const int64_t total = st->consumed;
     const bool fin = total > 0 && total % 4 == 0;
     if (fin && !d_out) return B64_EINVAL;

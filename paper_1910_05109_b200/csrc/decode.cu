@@ -148,7 +148,7 @@ __device__ __forceinline__ void stream_join(uint8_t* carry, int H, const uint8_t
     for (int k = 0; k < R; ++k) carry[k] = uint8_t(at(A - R + k));
 }
 
-template <int D>
+template <int D, bool EARLY>
 __global__ void __launch_bounds__(kThreads)
 dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
                 int64_t base, int is_final, unsigned long long* __restrict__ err_cell,
@@ -156,7 +156,11 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];  // per-warp output staging
     griddep_launch_dependents();
-    griddep_wait();
+    if (!EARLY) {  // (EARLY: a B64_STREAM_OVERLAP piece -- the bulk runs before the wait)
+        griddep_wait();
+        in = after_wait(in);
+        m_dev = after_wait(m_dev);
+    }
     if (m_dev) {  // the compacted text of mime.cu: its length and the kept index its suffix starts at
         const int64_t k0 = m_dev[1];
         m = m_dev[0] - k0;
@@ -232,6 +236,7 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
                         rel = scan_first_bad(pcur, 8, lut);
                         if (rel != 0xffffffffu) rel += lane * 32;
                     }
+                    if (EARLY) griddep_wait();
                     warp_report(bad, rel, base + int64_t(c) * 1024, err_cell);
                 }
                 pout += sout;
@@ -242,6 +247,7 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
         }
     }
 
+    if (EARLY) griddep_wait();  // the previous piece done: the rest touches shared state
     // leftover interior quads, one per thread
     for (int64_t q = (nchunk << 8) + gtid; q < Qint; q += gthreads) {
         const uint32_t x = ld32(in + 4 * q);

@@ -1063,8 +1063,8 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
     int64_t run = cta_base[lo];
     int64_t c = int64_t(lo) * K;
     const int64_t c_end = min(c + K, nch);
-    // chunk: walk the CTA's counts 32 at a time
-    for (;;) {
+    // chunk: walk the CTA's counts 32 at a time (bounded: e lies in CTA lo's chunks)
+    for (; c < c_end;) {
         const int64_t ci = c + lane;
         const int64_t v = ci < c_end ? counts[ci] : 0;
         int64_t incl = v;

@@ -45,6 +45,7 @@ __global__ void enc_stream_join_kernel(uint8_t* __restrict__ carry, int H, const
 __global__ void enc_stream_end_kernel(const uint8_t* __restrict__ carry, int H, uint8_t* __restrict__ out, EncTab tab,
                                       uint32_t pad) {
     griddep_wait();
+    carry = after_wait(carry);  // written by the previous piece's kernel
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(tab.w);
     const uint32_t v = enc_partial(carry[0], H == 2 ? carry[1] : 0u, H, lut, pad);
 #pragma unroll

@@ -46,7 +46,7 @@ __device__ __forceinline__ void ld_next_block(const uint8_t* p, bool pred, uint3
     }
 }
 
-template <int D, int WS>
+template <int D, int WS, bool EARLY>
 __global__ void __launch_bounds__(kThreads, D == 1 ? 5 : 4)
 dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab, int64_t base,
                  int is_final, unsigned long long* __restrict__ err_cell, int64_t* __restrict__ out_len,
@@ -54,7 +54,11 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];
     griddep_launch_dependents();
-    griddep_wait();
+    if (!EARLY) {  // (EARLY: a B64_STREAM_OVERLAP piece -- the bulk runs before the wait)
+        griddep_wait();
+        in = after_wait(in);
+        ub.A0 = after_wait(ub.A0);
+    }
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
@@ -133,6 +137,7 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
                             if (lut[p[t]] & kInvalid) { rel = uint32_t(lane * 32 + t); break; }
                     }
                     const uint32_t r = __reduce_min_sync(kFull, rel);
+                    if (EARLY) griddep_wait();
                     if (lane == 0) atomicMin(err_cell, pack_err(base + 4 * (ub.q0 + cur * 256) + int64_t(r), kBadChar));
                 }
                 pout += sout;
@@ -145,6 +150,7 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
         }
     }
 
+    if (EARLY) griddep_wait();  // the previous piece done: the rest touches shared state
     // the head quads [0, q0), the quads after the last full chunk, one per thread (byte loads)
     const int64_t qt = ub.q0 + int64_t(C) * 256;
     const int64_t nh = ub.q0, nrest = nh + (Qint - qt);
@@ -176,17 +182,17 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
 // (D, WS) -> kernel
 using DecFastuFn = void (*)(const uint8_t*, int64_t, uint8_t*, DecTab, int64_t, int, unsigned long long*, int64_t*,
                             UnalignedBulk, StreamJoin);
-template <int D>
+template <int D, bool EARLY = false>
 DecFastuFn dec_fastu_pick(int ws) {
     switch (ws) {
-        case 0: return dec_fastu_kernel<D, 0>;
-        case 1: return dec_fastu_kernel<D, 1>;
-        case 2: return dec_fastu_kernel<D, 2>;
-        case 3: return dec_fastu_kernel<D, 3>;
-        case 4: return dec_fastu_kernel<D, 4>;
-        case 5: return dec_fastu_kernel<D, 5>;
-        case 6: return dec_fastu_kernel<D, 6>;
-        default: return dec_fastu_kernel<D, 7>;
+        case 0: return dec_fastu_kernel<D, 0, EARLY>;
+        case 1: return dec_fastu_kernel<D, 1, EARLY>;
+        case 2: return dec_fastu_kernel<D, 2, EARLY>;
+        case 3: return dec_fastu_kernel<D, 3, EARLY>;
+        case 4: return dec_fastu_kernel<D, 4, EARLY>;
+        case 5: return dec_fastu_kernel<D, 5, EARLY>;
+        case 6: return dec_fastu_kernel<D, 6, EARLY>;
+        default: return dec_fastu_kernel<D, 7, EARLY>;
     }
 }
 

@@ -132,6 +132,11 @@ def test_stream_host_state_machine(L):
     assert n_out.value == 0
     assert L.b64_encode_stream_update(ctypes.byref(st), None, 0, None, a, ctypes.byref(n_out), None) == -1  # finished
     assert L.b64_decode_stream_begin(ctypes.byref(st), carry, None, None) == -1
+    # begin_ex: unknown flag bits and missing buffers are refused before any device work
+    cell = ctypes.c_void_p(0x2000)
+    assert L.b64_decode_stream_begin_ex(ctypes.byref(st), carry, cell, 2, None) == -1
+    assert L.b64_decode_stream_begin_ex(ctypes.byref(st), carry, None, _lib.STREAM_OVERLAP, None) == -1
+    assert L.b64_decode_stream_begin_ex(None, carry, cell, 0, None) == -1
 
 
 def test_binding_is_marshalling_only():

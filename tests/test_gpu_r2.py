@@ -613,3 +613,61 @@ def test_batch_fast_path_many_errors(b64):
         assert np.array_equal(st.cpu().numpy(), rst), frac
         assert np.array_equal(err.cpu().numpy(), rerr), frac
         assert np.array_equal(olen.cpu().numpy(), rlen), frac
+
+
+def _stream_into(b64, dt, alpha, pieces, overlap):
+    """Decode dt in the given pieces into ONE preallocated buffer (no host sync and no other
+    launch between the updates, so the overlap mode really overlaps)."""
+    ds = b64.DecodeStream(alpha, overlap=overlap)
+    buf = torch.full((3 * (dt.numel() // 4) + 16,), 0xA5, dtype=torch.uint8, device=DEV)
+    o = p = 0
+    for k in pieces:
+        n = ds.out_len(k)
+        got = ds.update(dt[p: p + k], out=buf[o: o + max(n, 1)])
+        assert got.numel() == n
+        o += n
+        p += k
+    tail, info = ds.end(out=buf[o: o + max(ds.end_len(), 1)])
+    return buf, info.tolist()
+
+
+@pytest.mark.parametrize("ai", [0, 1, 3, 4])
+def test_stream_overlap_vs_oracle(b64, ai):
+    """B64_STREAM_OVERLAP (each piece's bulk runs while the previous piece drains): for large
+    pieces of odd and aligned sizes, texts with bad chars in several pieces (the first one is the
+    error), a bad final quad and a LENGTH tail, the result equals the oracle's one-shot decode and
+    the default mode's, bit for bit; repeated to give a race a chance."""
+    perm = np.random.default_rng(7).permutation(127)[:65]
+    al = [(oracle.STANDARD, oracle.PAD, b64.standard()), (oracle.URL, oracle.PAD, b64.url()), None,
+          (bytes(perm[:64].tolist()), int(perm[64]), b64.alphabet(bytes(perm[:64].tolist()), bytes([int(perm[64])]))),
+          (oracle.STANDARD, oracle.PAD, b64.lenient_of(b64.standard()))]
+    chars, pad, alpha = al[ai]
+    rng = np.random.default_rng(70 + ai)
+    x = synth.data(6_000_001 + ai, seed=70 + ai)
+    text = oracle.encode(x, chars, pad)
+    variants = [text]
+    t2 = text.copy()
+    for p_ in sorted(rng.choice(text.size - 8, 3, replace=False))[::-1]:  # bad chars in 3 places
+        t2[p_] = ord("*")
+    variants.append(t2)
+    t3 = text.copy()
+    t3[-1] = ord("!")
+    variants.append(t3)
+    variants.append(text[:-2])  # LENGTH
+    for v in variants:
+        ref, rerr, rst = oracle.decode(v, chars, pad, lenient=(ai == 4))
+        dt = torch.from_numpy(v).to(DEV)
+        for pieces in ([(1 << 20) + 3] * (v.size // ((1 << 20) + 3)) + [v.size % ((1 << 20) + 3)],
+                       [1 << 20] * (v.size // (1 << 20)) + [v.size % (1 << 20)],
+                       None):
+            if pieces is None:
+                cuts = np.sort(rng.choice(np.arange(70_000, v.size - 70_000), 5, replace=False))
+                pieces = np.diff(np.concatenate([[0], cuts, [v.size]])).tolist()
+            base, binfo = _stream_into(b64, dt, alpha, pieces, overlap=False)
+            for rep in range(3):
+                got, info = _stream_into(b64, dt, alpha, pieces, overlap=True)
+                err, st, olen = info
+                assert (err, st) == (rerr, rst) and info == binfo, (ai, rep, info, binfo, rerr, rst)
+                assert torch.equal(got, base)
+                if err < 0:
+                    assert olen == ref.size and np.array_equal(got[:olen].cpu().numpy(), ref)

@@ -47,9 +47,9 @@ def main():
             b64._lib.check(L.b64_decode_chunk(V(t.data_ptr() + p), k, V(out.data_ptr() + p // 4 * 3), ctypes.byref(std),
                                               p, 1 if p + k == m else 0, V(cell.data_ptr()), None, sp), "chunk")
 
-    def streamed():
+    def streamed(flags=0):
         st = b64._lib.Stream()
-        L.b64_decode_stream_begin(ctypes.byref(st), V(carry.data_ptr()), V(cell.data_ptr()), sp)
+        L.b64_decode_stream_begin_ex(ctypes.byref(st), V(carry.data_ptr()), V(cell.data_ptr()), flags, sp)
         o, p = 0, 0
         n_out = ctypes.c_int64(0)
         while p < m:
@@ -75,7 +75,8 @@ def main():
         return statistics.median(ts)
 
     res = {}
-    for name, fn in (("one_call", one), ("chunks", chunks), ("stream", streamed)):
+    for name, fn in (("one_call", one), ("chunks", chunks), ("stream", streamed),
+                     ("stream_overlap", lambda: streamed(b64._lib.STREAM_OVERLAP))):
         fn()
         torch.cuda.synchronize()
         res[name + "_sleep100us"] = timeit(fn, 200_000)
