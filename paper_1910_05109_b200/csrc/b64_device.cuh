@@ -56,6 +56,14 @@ __device__ __forceinline__ unsigned long long pack_err(int64_t pos, uint32_t kin
 // ----------------------------------------------------------------- memory ops
 // 256-bit lane-linear load, no L1 allocation (streamed once).
 __device__ __forceinline__ void ld256_stream(const void* p, uint32_t (&r)[8]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+        : "l"(p));
+}
+// The same load as a plain (non-volatile) asm: ptxas may move it within the loop (where to
+// is measured per kernel: dec_fast_kernel<2> is 5 % faster with it).  Only for loads issued
+// after griddepcontrol.wait in program order; tests/test_pdl_order.py checks the SASS.
+__device__ __forceinline__ void ld256_stream_nv(const void* p, uint32_t (&r)[8]) {
     asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
         : "l"(p));
@@ -65,22 +73,22 @@ __device__ __forceinline__ void ld256_stream(const void* p, uint32_t (&r)[8]) {
 // L1 and the next two hit there (DRAM reads each byte once).
 __device__ __forceinline__ uint2 ld64_l1(const void* p) {
     uint2 r;
-    asm("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
 __device__ __forceinline__ uint4 ld128_nc(const void* p) {
     uint4 r;
-    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     return r;
 }
 __device__ __forceinline__ uint32_t ld32_nc(const void* p) {  // streamed once: no L1 allocation
     uint32_t r;
-    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
 __device__ __forceinline__ uint32_t ld32(const void* p) {
     uint32_t r;
-    asm("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
 __device__ __forceinline__ void st256(void* p, const uint32_t (&v)[8]) {
@@ -115,37 +123,6 @@ __device__ __forceinline__ uint2 lds64(uint32_t a) {
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
     return v;
-}
-
-// mbarrier + bulk async copy (TMA, non-tensor form) for the staged batch encode:
-// one elected lane arms the barrier with the byte count and issues the copies;
-// every lane waits on the phase parity before reading the stage.
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_init_fence() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    do {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-                     : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
-    } while (!ok);
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-// global -> shared bulk copy: src / dst 16-byte aligned, bytes a multiple of 16
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 v;
@@ -238,7 +215,7 @@ __device__ __forceinline__ void ld24_unaligned(const uint8_t* p, uint32_t (&w)[6
 // decode +0.6 %, 64 KiB strings +2.6 %; the 24-byte encode units measured 11 % slower).
 __device__ __forceinline__ uint4 ld128_l1(const void* p) {
     uint4 r;
-    asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     return r;
 }
 template <int NW>
@@ -392,7 +369,6 @@ static_assert(sizeof(BatchCtx) == 32, "B64_BATCH_CTX_BYTES");
 template <int D>
 __global__ void enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab,
                                 uint32_t pad);
-template <int TMA>
 __global__ void enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab,
                                    uint32_t pad);
 // A streaming decode's join (stream.cu): the quad made of the H held chars and the piece's

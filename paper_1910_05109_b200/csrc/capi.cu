@@ -54,17 +54,6 @@ cudaError_t group_occupancy(int (&occ)[4]) {
     return cudaSuccess;
 }
 
-// The batch / misaligned encode: the TMA-staged loop (enc_generic_kernel<1>) unless
-// B64_ENC_TMA=0 selects the direct-load one (kept for A/B measurement).
-using EncGenericFn = void (*)(const uint8_t*, uint8_t*, Offsets, EncTab, uint32_t);
-EncGenericFn enc_generic_fn() {
-    static const EncGenericFn f = [] {
-        const char* e = std::getenv("B64_ENC_TMA");
-        return (e && e[0] == '0') ? EncGenericFn(enc_generic_kernel<0>) : EncGenericFn(enc_generic_kernel<1>);
-    }();
-    return f;
-}
-
 const DevInfo* dev_info() {
     int d = 0;
     if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) return nullptr;
@@ -77,7 +66,7 @@ const DevInfo* dev_info() {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[1], dec_fast_kernel<1>, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_fast[2], dec_fast_kernel<2>, kThreads, 0) ||
         group_occupancy(info.occ_group) ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_fn(), kThreads, 0) ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_gen, enc_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_dec_gen, dec_generic_kernel, kThreads, 0) ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_batch_bulk, dec_batch_bulk_kernel<2>, kThreads, 0))
         return nullptr;
@@ -365,7 +354,7 @@ int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabe
     } else {
         Offsets off{nullptr, nullptr, 1, n};
         const int64_t blocks = clamp_grid((n / 12 + kThreads - 1) / kThreads, int64_t(di->sms) * di->occ_enc_gen);
-        launch(enc_generic_fn(), blocks, kThreads, s, d_in, d_out, off, enc_tab(a), a->pad);
+        launch(enc_generic_kernel, blocks, kThreads, s, d_in, d_out, off, enc_tab(a), a->pad);
     }
     return launched();
 }
@@ -889,7 +878,7 @@ int b64_encode_batch(const uint8_t* d_in, const int64_t* d_in_off, int64_t count
     if (!di) return B64_ECUDA;
     Offsets off{d_in_off, d_out_off, count, 0};
     const int64_t blocks = int64_t(di->sms) * di->occ_enc_gen;
-    launch(enc_generic_fn(), blocks, kThreads, reinterpret_cast<cudaStream_t>(stream), d_in, d_out, off, enc_tab(a), a->pad);
+    launch(enc_generic_kernel, blocks, kThreads, reinterpret_cast<cudaStream_t>(stream), d_in, d_out, off, enc_tab(a), a->pad);
     return launched();
 }
 

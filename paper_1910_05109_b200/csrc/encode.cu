@@ -308,44 +308,16 @@ __device__ __forceinline__ int64_t warp_exclusive_scan(int64_t v, int lane, int6
 #ifndef B64_ENC_GEN_MINB
 #define B64_ENC_GEN_MINB 5
 #endif
-// TMA = 1: the units' input bytes are staged per warp in shared memory by bulk async
-// copies (cp.async.bulk, one or two contiguous segments per 32-unit iteration, issued
-// kEncAhead iterations ahead on an mbarrier ring) and read back with conflict-free
-// LDS.64 at the 24-byte lane stride, instead of four L1-allocating LDG.64 per lane:
-// the loads leave the LSU pipe, which the per-char table look-ups keep busy
-// (enc_generic).
-constexpr int kEncStages = 3, kEncAhead = 2;
-constexpr int kEncStageBytes = 896;  // <= 2 segments of 32 units: 768 + 2 x 30 (16-byte rounding) + 32 read slack
-struct EncStageRef {
-    const uint8_t* A;  // the lane's unit input (fallback iterations: loaded directly)
-    int64_t dst;       // its output offset
-    uint32_t saddr;    // its bytes in the stage (shared address)
-    uint32_t flags;    // bit 0: valid unit, bit 1: staged (TMA)
-};
-#ifndef B64_ENC_TMA_MINB
-#define B64_ENC_TMA_MINB 4
-#endif
-template <int TMA>
-__global__ void __launch_bounds__(kThreads, TMA ? B64_ENC_TMA_MINB : B64_ENC_GEN_MINB)
+__global__ void __launch_bounds__(kThreads, B64_ENC_GEN_MINB)
 enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Offsets off, EncTab tab, uint32_t pad) {
     __shared__ __align__(64) uint32_t s_lut[16];
     __shared__ EncWarpList s_list[kThreads / 32];
-    __shared__ __align__(128) uint8_t s_stage[TMA ? kThreads / 32 : 1][TMA ? kEncStages : 1][TMA ? kEncStageBytes : 16];
-    __shared__ __align__(8) uint64_t s_bar[TMA ? kThreads / 32 : 1][kEncStages];
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
     }
-    if (TMA && (threadIdx.x & 31) == 0) {
-#pragma unroll
-        for (int i = 0; i < kEncStages; ++i) mbar_init(smem_u32(&s_bar[threadIdx.x >> 5][i]), 1);
-        mbar_init_fence();
-    }
     __syncthreads();
     griddep_wait();
-    const uint32_t bar0 = TMA ? smem_u32(&s_bar[(threadIdx.x >> 5) % (TMA ? kThreads / 32 : 1)][0]) : 0;
-    const uint32_t stage0 = TMA ? smem_u32(&s_stage[(threadIdx.x >> 5) % (TMA ? kThreads / 32 : 1)][0][0]) : 0;
-    uint32_t g_issue = 0, g_cons = 0;  // the warp's ring positions (continue across string batches)
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const uint32_t lb = smem_u32(s_lut);
 
@@ -398,102 +370,30 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
         wl.dst[lane] = dst;
         if (lane == 31) wl.pre[32] = nu_all;
         __syncwarp();
-        if (TMA) {
-            // flattened units of the batch's long strings, 32 per iteration, kEncAhead
-            // iterations staged ahead; each lane's owner string only moves forward
-            const int64_t nit = (nu_all + 31) >> 5;
-            int oi = 0;
-            auto issue = [&](int64_t it, EncStageRef& r) {
-                const int64_t j = (it << 5) + lane;
-                const bool v = j < nu_all;
-                if (v)
-                    while (wl.pre[oi + 1] <= j) ++oi;
-                const int64_t k_in = v ? j - wl.pre[oi] : 0;
-                r.A = v ? in + wl.src[oi] + 24 * k_in : in;
-                r.dst = v ? wl.dst[oi] + 32 * k_in : 0;
-                const int nv = int(min(int64_t(32), nu_all - (it << 5)));
-                const int po = __shfl_up_sync(kFull, oi, 1);
-                const uint32_t chg = __ballot_sync(kFull, v && lane > 0 && oi != po);
-                const uint32_t st = g_issue % kEncStages;
-                const uint32_t bar = bar0 + 8 * st, sb = stage0 + st * kEncStageBytes;
-                ++g_issue;
-                if (__popc(chg) <= 1) {  // one or two contiguous segments: bulk copies
-                    const int k = chg ? __ffs(chg) - 1 : nv;
-                    const unsigned long long a = reinterpret_cast<unsigned long long>(r.A);
-                    const unsigned long long a0 = __shfl_sync(kFull, a, 0), ak1 = __shfl_sync(kFull, a, k - 1);
-                    const unsigned long long ak = __shfl_sync(kFull, a, k & 31), al = __shfl_sync(kFull, a, nv - 1);
-                    const unsigned long long S0 = a0 & ~15ull, E0 = (ak1 + 24 + 15) & ~15ull;
-                    const unsigned long long S1 = ak & ~15ull, E1 = (al + 24 + 15) & ~15ull;
-                    const uint32_t b0 = uint32_t(E0 - S0), b1 = k < nv ? uint32_t(E1 - S1) : 0u;
-                    r.saddr = sb + (lane < k ? uint32_t(a - S0) : b0 + uint32_t(a - S1));
-                    r.flags = (v ? 1u : 0u) | 2u;
-                    if (lane == 0) {
-                        fence_proxy_async_smem();
-                        mbar_expect_tx(bar, b0 + b1);
-                        bulk_g2s(sb, reinterpret_cast<const void*>(S0), b0, bar);
-                        if (b1) bulk_g2s(sb + b0, reinterpret_cast<const void*>(S1), b1, bar);
-                    }
-                } else {  // many short strings in one iteration: direct loads at consumption
-                    r.saddr = 0;
-                    r.flags = v ? 1u : 0u;
-                    if (lane == 0) mbar_arrive(bar);
-                }
-            };
-            EncStageRef r0 = {}, r1 = {};
-            if (nit > 0) issue(0, r0);
-            if (nit > 1) issue(1, r1);
-            for (int64_t it = 0; it < nit; ++it) {
-                const EncStageRef cur = r0;
-                r0 = r1;
-                __syncwarp();  // every lane is done with the stage issue() refills
-                if (it + kEncAhead < nit) issue(it + kEncAhead, r1);
-                const uint32_t st = g_cons % kEncStages;
-                mbar_wait(bar0 + 8 * st, (g_cons / kEncStages) & 1);
-                ++g_cons;
-                if (cur.flags & 1u) {
-                    Raw24 cr;
-                    if (cur.flags & 2u) {
-                        const uint32_t d = cur.saddr & ~7u;
-                        cr.sb = cur.saddr & 7u;
-                        cr.a = lds64(d);
-                        cr.b = lds64(d + 8);
-                        cr.c = lds64(d + 16);
-                        cr.d = cr.sb ? lds64(d + 24) : make_uint2(0u, 0u);
-                    } else {
-                        ld24_raw(cur.A, cr);
-                    }
-                    uint32_t wv[6], ov[8];
-                    fix24(cr, wv);
-                    enc_lane_compute(wv, ov, lb);
-                    st256(out + cur.dst, ov);
-                }
+        // flattened units of the batch's long strings, one unit ahead in flight; each lane's
+        // owner string only moves forward (j grows), so it is tracked, not searched
+        int64_t j = lane;
+        int o = 0;
+        Raw24 nr;
+        int64_t ndst = 0;
+        if (j < nu_all) {
+            while (wl.pre[o + 1] <= j) ++o;
+            ld24_raw(in + wl.src[o] + 24 * (j - wl.pre[o]), nr);
+            ndst = wl.dst[o] + 32 * (j - wl.pre[o]);
+        }
+        for (; j < nu_all; j += 32) {
+            const Raw24 cr = nr;
+            const int64_t cdst = ndst;
+            const int64_t jn = j + 32;
+            if (jn < nu_all) {
+                while (wl.pre[o + 1] <= jn) ++o;
+                ld24_raw(in + wl.src[o] + 24 * (jn - wl.pre[o]), nr);
+                ndst = wl.dst[o] + 32 * (jn - wl.pre[o]);
             }
-        } else {
-            // flattened units of the batch's long strings, one unit ahead in flight; each lane's
-            // owner string only moves forward (j grows), so it is tracked, not searched
-            int64_t j = lane;
-            int o = 0;
-            Raw24 nr;
-            int64_t ndst = 0;
-            if (j < nu_all) {
-                while (wl.pre[o + 1] <= j) ++o;
-                ld24_raw(in + wl.src[o] + 24 * (j - wl.pre[o]), nr);
-                ndst = wl.dst[o] + 32 * (j - wl.pre[o]);
-            }
-            for (; j < nu_all; j += 32) {
-                const Raw24 cr = nr;
-                const int64_t cdst = ndst;
-                const int64_t jn = j + 32;
-                if (jn < nu_all) {
-                    while (wl.pre[o + 1] <= jn) ++o;
-                    ld24_raw(in + wl.src[o] + 24 * (jn - wl.pre[o]), nr);
-                    ndst = wl.dst[o] + 32 * (jn - wl.pre[o]);
-                }
-                uint32_t wv[6], ov[8];
-                fix24(cr, wv);
-                enc_lane_compute(wv, ov, lb);
-                st256(out + cdst, ov);
-            }
+            uint32_t wv[6], ov[8];
+            fix24(cr, wv);
+            enc_lane_compute(wv, ov, lb);
+            st256(out + cdst, ov);
         }
         __syncwarp();
         // flattened scalar triples: head [0, h), tail [t0, T), and the padded partial triple T

@@ -54,11 +54,7 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(128) uint32_t s_stage[kThreads / 32][768 / 4];
     griddep_launch_dependents();
-    if (!EARLY) {  // (EARLY: a B64_STREAM_OVERLAP piece -- the bulk runs before the wait)
-        griddep_wait();
-        in = after_wait(in);
-        ub.A0 = after_wait(ub.A0);
-    }
+    if (!EARLY) griddep_wait();  // (EARLY: a B64_STREAM_OVERLAP piece -- the bulk runs before the wait)
     const int lane = threadIdx.x & 31;
     const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;

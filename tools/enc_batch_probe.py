@@ -17,6 +17,12 @@ import synth  # noqa: E402
 
 
 def main():
+    if os.environ.get("B64_LIB_PATH"):  # another build of the library (A/B)
+        import ctypes
+        path = os.environ["B64_LIB_PATH"]
+        probe = ctypes.CDLL(path)
+        b64._lib.LIB_PATH = path
+        b64._lib.SIGNATURES = [sg for sg in b64._lib.SIGNATURES if hasattr(probe, sg[0])]
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 7
     Ls = synth.loguniform_lengths(1_000_000, seed=0)
     off = synth.offsets(Ls)
@@ -39,7 +45,7 @@ def main():
     ck = int((w * torch.arange(1, w.numel() + 1, device="cuda", dtype=torch.int64)).sum().item())
     ms = statistics.median(ts)
     alg = off[-1] + enc.numel()
-    print({"tma": os.environ.get("B64_ENC_TMA", "default"), "ms": round(ms, 4), "min_ms": round(min(ts), 4),
+    print({"lib": os.path.basename(b64._lib.LIB_PATH), "tma": os.environ.get("B64_ENC_TMA", "default"), "ms": round(ms, 4), "min_ms": round(min(ts), 4),
            "alg_gbs": round(alg / ms / 1e6, 1), "checksum": ck})
 
 

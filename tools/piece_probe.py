@@ -19,6 +19,11 @@ import synth  # noqa: E402
 
 
 def main():
+    if os.environ.get("B64_LIB_PATH"):  # another build of the library (A/B)
+        path = os.environ["B64_LIB_PATH"]
+        probe = ctypes.CDLL(path)
+        b64._lib.LIB_PATH = path
+        b64._lib.SIGNATURES = [sg for sg in b64._lib.SIGNATURES if hasattr(probe, sg[0])]
     piece = (int(sys.argv[1]) if len(sys.argv) > 1 else 64) << 20
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 7
     L = b64._lib.lib()
@@ -49,7 +54,10 @@ def main():
 
     def streamed(flags=0):
         st = b64._lib.Stream()
-        L.b64_decode_stream_begin_ex(ctypes.byref(st), V(carry.data_ptr()), V(cell.data_ptr()), flags, sp)
+        if flags:
+            L.b64_decode_stream_begin_ex(ctypes.byref(st), V(carry.data_ptr()), V(cell.data_ptr()), flags, sp)
+        else:
+            L.b64_decode_stream_begin(ctypes.byref(st), V(carry.data_ptr()), V(cell.data_ptr()), sp)
         o, p = 0, 0
         n_out = ctypes.c_int64(0)
         while p < m:
@@ -75,8 +83,10 @@ def main():
         return statistics.median(ts)
 
     res = {}
-    for name, fn in (("one_call", one), ("chunks", chunks), ("stream", streamed),
-                     ("stream_overlap", lambda: streamed(b64._lib.STREAM_OVERLAP))):
+    modes = [("one_call", one), ("chunks", chunks), ("stream", streamed)]
+    if hasattr(L, "b64_decode_stream_begin_ex"):
+        modes.append(("stream_overlap", lambda: streamed(b64._lib.STREAM_OVERLAP)))
+    for name, fn in modes:
         fn()
         torch.cuda.synchronize()
         res[name + "_sleep100us"] = timeit(fn, 200_000)
