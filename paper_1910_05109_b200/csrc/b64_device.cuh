@@ -56,14 +56,6 @@ __device__ __forceinline__ unsigned long long pack_err(int64_t pos, uint32_t kin
 // ----------------------------------------------------------------- memory ops
 // 256-bit lane-linear load, no L1 allocation (streamed once).
 __device__ __forceinline__ void ld256_stream(const void* p, uint32_t (&r)[8]) {
-    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-        : "l"(p));
-}
-// The same load as a plain (non-volatile) asm: ptxas may move it within the loop (where to
-// is measured per kernel: dec_fast_kernel<2> is 5 % faster with it).  Only for loads issued
-// after griddepcontrol.wait in program order; tests/test_pdl_order.py checks the SASS.
-__device__ __forceinline__ void ld256_stream_nv(const void* p, uint32_t (&r)[8]) {
     asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
         : "l"(p));
@@ -73,22 +65,22 @@ __device__ __forceinline__ void ld256_stream_nv(const void* p, uint32_t (&r)[8])
 // L1 and the next two hit there (DRAM reads each byte once).
 __device__ __forceinline__ uint2 ld64_l1(const void* p) {
     uint2 r;
-    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    asm("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
 __device__ __forceinline__ uint4 ld128_nc(const void* p) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     return r;
 }
 __device__ __forceinline__ uint32_t ld32_nc(const void* p) {  // streamed once: no L1 allocation
     uint32_t r;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
 __device__ __forceinline__ uint32_t ld32(const void* p) {
     uint32_t r;
-    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm("ld.global.nc.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
 __device__ __forceinline__ void st256(void* p, const uint32_t (&v)[8]) {
@@ -215,7 +207,7 @@ __device__ __forceinline__ void ld24_unaligned(const uint8_t* p, uint32_t (&w)[6
 // decode +0.6 %, 64 KiB strings +2.6 %; the 24-byte encode units measured 11 % slower).
 __device__ __forceinline__ uint4 ld128_l1(const void* p) {
     uint4 r;
-    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
     return r;
 }
 template <int NW>

@@ -148,14 +148,6 @@ __device__ __forceinline__ void stream_join(uint8_t* carry, int H, const uint8_t
     for (int k = 0; k < R; ++k) carry[k] = uint8_t(at(A - R + k));
 }
 
-// dec_fast_kernel's chunk loads: volatile at D = 1 (kept in program order: 64 MiB pieces
-// 0.51 -> 0.46 ms per GiB), free for ptxas to schedule at D = 2 (1 GiB 0.418 -> 0.393 ms).
-template <int D>
-__device__ __forceinline__ void ld256_fast(const void* p, uint32_t (&r)[8]) {
-    if (D == 1) ld256_stream(p, r);
-    else ld256_stream_nv(p, r);
-}
-
 template <int D, bool EARLY>
 __global__ void __launch_bounds__(kThreads)
 dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__ out, DecTab tab,
@@ -166,7 +158,11 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
     griddep_launch_dependents();
     if (!EARLY) {  // (EARLY: a B64_STREAM_OVERLAP piece -- the bulk runs before the wait)
         griddep_wait();
-        m_dev = after_wait(m_dev);  // (the asm loads of `in` are volatile: ordered after the wait)
+        // D = 1 (the launches of <= 64 MiB): the laundered m_dev makes the stream's pointers
+        // per-thread values, which ptxas schedules better here -- measured 64 MiB pieces 0.51 ->
+        // 0.46 ms per GiB; at D = 2 (1 GiB) the uniform-register version is 6 % faster
+        // (0.393 vs 0.418 ms).  Either way m_dev is read after the wait (test_pdl_order.py).
+        if (D == 1) m_dev = after_wait(m_dev);
     }
     if (m_dev) {  // the compacted text of mime.cu: its length and the kept index its suffix starts at
         const int64_t k0 = m_dev[1];
@@ -202,7 +198,7 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
 #pragma unroll
     for (int i = 0; i < D; ++i)
         if (c0i + i * W < C) {
-            ld256_fast<D>(pin, xr[i]);
+            ld256_stream(pin, xr[i]);
             pin += sin;
         }
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
@@ -216,7 +212,7 @@ dec_fast_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict__
             if (c < C) {
                 uint32_t y[8];
                 if (c + D * W < C) {
-                    ld256_fast<D>(pin, y);
+                    ld256_stream(pin, y);
                     pin += sin;
                 }
                 uint32_t err = 0, v[8];
