@@ -1058,9 +1058,9 @@ def next_rows(b64, synth, torch, dev, timeit):
     res["lenient"] = rate(ms, m, n)
     assert int(info[0].item()) == -1
     # decode -> consumer: the decoded bytes reduced by a consumer (a byte sum)
-    # chunk by chunk while they sit in an L2-resident 16 MiB ring (b64_decode_consume), against
+    # chunk by chunk while they sit in an L2-resident 64 MiB ring (b64_decode_consume), against
     # decoding to HBM and summing the output afterwards
-    ring = torch.empty(16 << 20, dtype=torch.uint8, device=dev)
+    ring = torch.empty(64 << 20, dtype=torch.uint8, device=dev)
     acc = torch.zeros(1, dtype=torch.int64, device=dev)
     rbase = ring.data_ptr()
 
@@ -1092,7 +1092,7 @@ def next_rows(b64, synth, torch, dev, timeit):
         assert int(info[0].item()) == -1 and int(acc.item()) == want, name
         res[name] = dict(rate(ms, m, n), note="decode + a consumer checksumming the decoded bytes (64-bit word sum)" +
                          (": decoded to HBM, then summed" if name == "decode_then_sum" else
-                          ": chunks of 21.8 Mi chars through a 16 MiB ring, each summed while in L2"))
+                          ": chunks of 87 Mi chars through a 64 MiB ring, each summed while in L2"))
     del ring
     # padding-optional: the base64url text without its '=' (m - 2 chars)
     tu = b64.encode(x, url)[: m - 2]

@@ -447,8 +447,11 @@ int b64_decode_host_ex(const uint8_t *h_in, int64_t m, uint8_t *h_out, const b64
  * handed over (not when the device finished).  Results as b64_decode_ex: *d_err_off (device,
  * required) = -1 or the first invalid position, *d_status / *d_out_len (nullable); the last
  * chunk's exact length is *d_out_len - its out_offset.  Bytes of quads at or after the first
- * error are unspecified (the consumer still sees every chunk).  Ring sizes of 8-32 MiB keep a
- * chunk and its consumer in the 126 MB L2. */
+ * error are unspecified (the consumer still sees every chunk).  Every chunk costs one decode
+ * launch plus the consumer's launches, so the ring should be as large as L2 allows: measured
+ * on 1 GiB with a 3-launch checksum consumer, 16 MiB 1.27 ms, 32 MiB 0.88, 64 MiB 0.67, 96 MiB
+ * 0.60 -- against 0.46 ms for decode-to-HBM then the same checksum (tools/consume_probe.py): a
+ * consumer this light gains less from L2 than the extra launches cost. */
 typedef void (*b64_consumer_fn)(const uint8_t *d_chunk, int64_t len, int64_t out_offset, void *user,
                                 b64_stream_t stream);
 int64_t b64_consume_chunk_chars(int64_t ring_bytes);

@@ -472,7 +472,7 @@ def codec_group(xs, ts, enc_alphabets=None, dec_alphabets=None, enc_outs=None, d
 
 # ------------------------------------------------------------------ decode -> consumer (L2-resident ring)
 
-def decode_consume(t: torch.Tensor, consumer, a: Optional[Alphabet] = None, ring_bytes: int = 16 << 20,
+def decode_consume(t: torch.Tensor, consumer, a: Optional[Alphabet] = None, ring_bytes: int = 64 << 20,
                    ring: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None):
     """b64_decode_consume: decode `t` chunk by chunk into an L2-sized device ring and call
     consumer(chunk, out_offset) after each chunk -- chunk is a uint8 view of the ring holding
