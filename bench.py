@@ -1161,6 +1161,28 @@ def next_rows(b64, synth, torch, dev, timeit):
     assert int(info[0].item()) == -1 and int(info[2].item()) == n
     res["streaming_64MiB_pieces_overlap"] = dict(rate(ms, m, n), note="b64_decode_stream_begin_ex("
                                                  "B64_STREAM_OVERLAP): resident text, pieces overlap")
+    # streaming ENCODE of the same 1 GiB in 64 MiB + 1 pieces (every piece after the first
+    # misaligned: enc_fastu_kernel), into t (its content is encode(x) again: checked)
+    tref = t.clone()
+    epiece = (64 << 20) + 1
+
+    def enc_streamed(overlap):
+        es = b64.EncodeStream(overlap=overlap)
+        o, p_ = 0, 0
+        while p_ < n:
+            k_ = min(epiece, n - p_)
+            c_ = es.out_len(k_)
+            es.update(x[p_: p_ + k_], out=t[o: o + max(c_, 1)])
+            o += c_
+            p_ += k_
+        es.end(out=t[o: o + max(es.end_len(), 1)])
+
+    for name, ov in (("streaming_encode_64MiB_pieces", False), ("streaming_encode_64MiB_pieces_overlap", True)):
+        ms = timeit(lambda: enc_streamed(ov), reps=5)
+        assert torch.equal(t, tref), name
+        res[name] = dict(rate(ms, n, m), note="input = bytes; " + ("b64_encode_stream_begin_ex(B64_STREAM_OVERLAP)"
+                                                                   if ov else "default mode"))
+    del tref
     del x, t, tu, out
     torch.cuda.empty_cache()
     # one-sided peer combine, world 1 (per-combine kernel latency)

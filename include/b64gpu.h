@@ -308,6 +308,7 @@ typedef struct b64_stream {
     uint8_t *d_carry;   /* device carry buffer (>= 8 bytes)                       */
     int64_t *d_err_min; /* decode: device packed error word of the stream         */
 } b64_stream;
+#define B64_STREAM_OVERLAP 1u /* b64_{encode,decode}_stream_begin_ex flag: overlapped pieces (below) */
 
 /* Output sizes, host-side (no device access): b64_stream_update_len = the
  * chars (encode: 4*floor((held + len)/3)) / bytes (decode: 3*floor((held +
@@ -318,6 +319,13 @@ int64_t b64_stream_update_len(const b64_stream *st, int64_t len);
 int64_t b64_stream_end_len(const b64_stream *st);
 
 int b64_encode_stream_begin(b64_stream *st, uint8_t *d_carry);
+/* b64_encode_stream_begin with flags (0: the same, no device work).  B64_STREAM_OVERLAP
+ * (defined with b64_decode_stream_begin_ex below; same contract): d_carry is zeroed on
+ * `stream` (8 bytes) as the ordering point, and from the second piece on each update of at
+ * least 64 Ki bytes runs its bulk while the previous piece's kernel drains, with the join
+ * (straddling triple, new carry) at the kernel's end after the wait -- ONE launch per piece.
+ * Every later call of the stream must use the same `stream`.  Unknown flags -> B64_EINVAL. */
+int b64_encode_stream_begin_ex(b64_stream *st, uint8_t *d_carry, uint32_t flags, b64_stream_t stream);
 /* Encode piece d_in[0..n): writes *n_out = 4*floor((held + n)/3) chars at d_out
  * (capacity >= that; *n_out is known on return, host-side). */
 int b64_encode_stream_update(b64_stream *st, const uint8_t *d_in, int64_t n, uint8_t *d_out, const b64_alphabet *a,
@@ -342,7 +350,6 @@ int b64_decode_stream_begin(b64_stream *st, uint8_t *d_carry, int64_t *d_err_min
  * output; no piece's input overlaps any piece's output.  Results, as without
  * the flag, are complete once later work on the stream runs.  Unknown flag bits
  * -> B64_EINVAL. */
-#define B64_STREAM_OVERLAP 1u
 int b64_decode_stream_begin_ex(b64_stream *st, uint8_t *d_carry, int64_t *d_err_min, uint32_t flags,
                                b64_stream_t stream);
 /* Decode piece d_in[0..m) (any m >= 0): writes *n_out = 3*Q bytes at d_out,

@@ -545,15 +545,21 @@ class EncodeStream(_StreamBase):
     update(x) returns the chars completed so far (a view of a fresh or given buffer);
     end() returns the padded tail.  The concatenation of every returned piece equals
     encode(concatenation of the inputs).  All calls run on the CUDA stream fixed at
-    construction (default: the current stream then)."""
+    construction (default: the current stream then).
 
-    def __init__(self, a: Optional[Alphabet] = None, device=None, stream: Optional[torch.cuda.Stream] = None):
+    overlap=True: b64_encode_stream_begin_ex with B64_STREAM_OVERLAP (contract as
+    DecodeStream's: every piece's input written before construction, nothing else on the
+    stream writes a piece's input or output until end(), inputs and outputs disjoint)."""
+
+    def __init__(self, a: Optional[Alphabet] = None, device=None, stream: Optional[torch.cuda.Stream] = None,
+                 overlap: bool = False):
         super().__init__(a, device, stream)
         with _On(self.dev, self.stream) as on:
             self.carry = torch.zeros(8, dtype=torch.uint8, device=self.dev)
             on.owns(self.carry)
-        _lib.check(_lib.lib().b64_encode_stream_begin(ctypes.byref(self.st), _ptr(self.carry)),
-                   "b64_encode_stream_begin")
+            _lib.check(_lib.lib().b64_encode_stream_begin_ex(ctypes.byref(self.st), _ptr(self.carry),
+                                                             _lib.STREAM_OVERLAP if overlap else 0, on.sp),
+                       "b64_encode_stream_begin_ex")
 
     def update(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         _check_u8(x, "x", self.dev)

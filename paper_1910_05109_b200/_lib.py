@@ -104,6 +104,7 @@ SIGNATURES = [
     ("b64_stream_update_len", I64, [SP, I64]),
     ("b64_stream_end_len", I64, [SP]),
     ("b64_encode_stream_begin", INT, [SP, P]),
+    ("b64_encode_stream_begin_ex", INT, [SP, P, ctypes.c_uint32, P]),
     ("b64_encode_stream_update", INT, [SP, P, I64, P, AP, I64P, P]),
     ("b64_encode_stream_end", INT, [SP, P, AP, I64P, P]),
     ("b64_decode_stream_begin", INT, [SP, P, P, P]),

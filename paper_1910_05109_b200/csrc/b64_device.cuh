@@ -366,6 +366,16 @@ __global__ void enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __re
 // A streaming decode's join (stream.cu): the quad made of the H held chars and the piece's
 // first 4 - H chars, and the carry update (the piece's last R chars), folded into the piece's
 // bulk kernel when that is dec_fast (active = 0: nothing to do).
+// A streaming encode's join riding along with an overlapped piece's enc_fastu_kernel<true>
+// (its last thread, after the wait).
+struct EncJoin {
+    uint8_t* carry;
+    const uint8_t* in;   // the piece
+    uint8_t* out;        // the piece's output (the straddling triple's 4 chars go first)
+    int64_t n;           // piece bytes
+    int32_t H;           // held bytes before the piece
+    int32_t active;
+};
 struct StreamJoin {
     uint8_t* carry;
     const uint8_t* in;   // the piece

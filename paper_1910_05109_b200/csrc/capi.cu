@@ -28,7 +28,7 @@ struct DevInfo {
     int sms = 0;
     int occ_group[4] = {0, 0, 0, 0};  // min over the enc / dec / codec group kernels
     int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_enc_gen = 0, occ_dec_gen = 0;
-    int occ_batch_bulk = 0, occ_fastu[3][8] = {};
+    int occ_batch_bulk = 0, occ_fastu[3][8] = {}, occ_enc_fastu = 0;
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -86,6 +86,10 @@ const DevInfo* dev_info() {
                 return nullptr;
             info.occ_fastu[d][w] = o < 1 ? 1 : o;
         }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_enc_fastu, enc_fastu_kernel<1, false>, kThreads, 0) !=
+        cudaSuccess)
+        return nullptr;
+    info.occ_enc_fastu = info.occ_enc_fastu < 1 ? 1 : info.occ_enc_fastu;
     if (cudaFuncSetAttribute(dec_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
         cudaFuncSetAttribute(ws_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         return nullptr;
@@ -338,14 +342,26 @@ int b64_decode_batch_offsets(const int64_t* d_in_off, int64_t count, int64_t* d_
     return batch_offsets<1>(d_in_off, count, d_out_off, stream);
 }
 
-int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabet* a, b64_stream_t stream) {
-    if (n < 0 || !alpha_ok(a)) return B64_EINVAL;
-    if (n == 0) return B64_OK;
-    if (!d_in || !d_out) return B64_EINVAL;
+// The single-stream encode launch (fast, misaligned-fast or generic kernel by alignment).
+// `early` (an overlapped streaming piece, caller-checked: n >= unaligned_min(), d_out 4-byte
+// aligned): enc_fastu_kernel<1, true> whatever the alignment, with `join` riding along.
+static int encode_launch(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabet* a, cudaStream_t s,
+                         bool early = false, const EncJoin* join = nullptr) {
     const DevInfo* di = dev_info();
     if (!di) return B64_ECUDA;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (aligned(d_in, 8) && aligned(d_out, 32)) {
+    if (early || (!aligned(d_in, 8) || !aligned(d_out, 32)) && aligned(d_out, 4) && n >= unaligned_min()) {
+        // any input alignment, 4-byte aligned output: enc_fast's loop with a uniform byte
+        // shift, from the first triple whose output is 32-byte aligned (unaligned.cu)
+        const int64_t T = n / 3;
+        const uintptr_t ou = reinterpret_cast<uintptr_t>(d_out);
+        const int64_t q0 = std::min<int64_t>(int64_t(((32 - (ou & 31)) & 31) >> 2), T);
+        const int64_t nchunk = (T - q0) / 256;
+        // (one chunk in flight per warp at every size: two measured 3 % slower at 1 GiB)
+        const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(di->occ_enc_fastu));
+        const EncJoin ej = join ? *join : EncJoin{};
+        launch(early ? enc_fastu_kernel<1, true> : enc_fastu_kernel<1, false>, blocks, kThreads, s, d_in, n, d_out,
+               enc_tab(a), a->pad, q0, int32_t(nchunk), ej);
+    } else if (aligned(d_in, 8) && aligned(d_out, 32)) {
         const int64_t nchunk = n / 768;
         const int dd = enc_depth(n);
         const int64_t blocks = balanced_blocks(nchunk, int64_t(di->sms) * cap_bps(di->occ_enc_fast[dd]));
@@ -357,6 +373,13 @@ int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabe
         launch(enc_generic_kernel, blocks, kThreads, s, d_in, d_out, off, enc_tab(a), a->pad);
     }
     return launched();
+}
+
+int b64_encode(const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabet* a, b64_stream_t stream) {
+    if (n < 0 || !alpha_ok(a)) return B64_EINVAL;
+    if (n == 0) return B64_OK;
+    if (!d_in || !d_out) return B64_EINVAL;
+    return encode_launch(d_in, n, d_out, a, reinterpret_cast<cudaStream_t>(stream));
 }
 
 static int decode_launch(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alphabet* a, int64_t base,

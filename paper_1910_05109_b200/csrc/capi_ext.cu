@@ -10,7 +10,7 @@ extern "C" {
 // device; the held bytes themselves live in the caller's device carry buffer.
 namespace {
 enum { kStIdle = 0, kStEncode = 1, kStDecode = 2, kStDone = 3 };
-constexpr int32_t kStOverlap = 0x100;  // decode state bit: B64_STREAM_OVERLAP
+constexpr int32_t kStOverlap = 0x100;  // state bit: B64_STREAM_OVERLAP
 inline int32_t st_kind(const b64_stream* st) { return st->state & 0xff; }
 }
 
@@ -39,23 +39,49 @@ int b64_encode_stream_begin(b64_stream* st, uint8_t* d_carry) {
     return B64_OK;
 }
 
+int b64_encode_stream_begin_ex(b64_stream* st, uint8_t* d_carry, uint32_t flags, b64_stream_t stream) {
+    if (!st || !d_carry || (flags & ~B64_STREAM_OVERLAP)) return B64_EINVAL;
+    if (flags & B64_STREAM_OVERLAP) {
+        // a memset, not a kernel: the first piece is fully ordered after everything before the
+        // begin call (no programmatic edge crosses it), which the overlap mode relies on
+        if (cudaMemsetAsync(d_carry, 0, 8, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess) return B64_ECUDA;
+    }
+    const int r = b64_encode_stream_begin(st, d_carry);
+    if (r == B64_OK && (flags & B64_STREAM_OVERLAP)) st->state |= kStOverlap;
+    return r;
+}
+
 int b64_encode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t n, uint8_t* d_out, const b64_alphabet* a,
                              int64_t* n_out, b64_stream_t stream) {
-    if (!st || st->state != kStEncode || n < 0 || !alpha_ok(a) || (n > 0 && !d_in)) return B64_EINVAL;
+    if (!st || st_kind(st) != kStEncode || n < 0 || !alpha_ok(a) || (n > 0 && !d_in)) return B64_EINVAL;
     const int64_t H = st->held, A = H + n, T = A / 3;
     if (T > 0 && !d_out) return B64_EINVAL;
     if (n_out) *n_out = 4 * T;
     if (n == 0) return B64_OK;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int join = (H > 0 && T > 0) ? 1 : 0;
-    if (H > 0 || A % 3) {  // a straddling triple and / or bytes to hold
+    const int64_t skip = join ? 3 - H : 0, tb = T - join;  // whole triples read straight from the piece
+    if ((st->state & kStOverlap) && st->consumed > 0 && 3 * tb >= unaligned_min() &&
+        aligned(d_out + 4 * join, 4)) {
+        // overlap mode (B64_STREAM_OVERLAP), from the second piece on: the bulk runs while the
+        // previous piece drains, the join (reading the carry it writes) at its end, after the wait
+        const EncJoin ej = {st->d_carry, d_in, d_out, n, int32_t(H), (H > 0 || A % 3) ? 1 : 0};
+        const int r = encode_launch(d_in + skip, 3 * tb, d_out + 4 * join, a, s, true, &ej);
+        if (r != B64_OK) return r;
+        st->held = int32_t(A % 3);
+        st->consumed += n;
+        st->produced += 4 * T;
+        return B64_OK;
+    }
+    if (H > 0 || A % 3) {  // a straddling triple and / or bytes to hold: one thread, before the bulk
+        // (riding along with enc_fastu_kernel, first or last thread, measured 4 % slower on
+        // 64 MiB pieces: its dependent loads sit on the piece's critical path)
         launch(enc_stream_join_kernel, 1, 1, s, st->d_carry, int(H), d_in, n, d_out, enc_tab(a));
         const int r = launched();
         if (r != B64_OK) return r;
     }
-    const int64_t skip = join ? 3 - H : 0, tb = T - join;  // whole triples read straight from the piece
     if (tb > 0) {
-        const int r = b64_encode(d_in + skip, 3 * tb, d_out + 4 * join, a, stream);
+        const int r = encode_launch(d_in + skip, 3 * tb, d_out + 4 * join, a, s);
         if (r != B64_OK) return r;
     }
     st->held = int32_t(A % 3);
@@ -66,7 +92,7 @@ int b64_encode_stream_update(b64_stream* st, const uint8_t* d_in, int64_t n, uin
 
 int b64_encode_stream_end(b64_stream* st, uint8_t* d_out, const b64_alphabet* a, int64_t* n_out,
                           b64_stream_t stream) {
-    if (!st || st->state != kStEncode || !alpha_ok(a)) return B64_EINVAL;
+    if (!st || st_kind(st) != kStEncode || !alpha_ok(a)) return B64_EINVAL;
     const int H = st->held;
     if (H > 0 && !d_out) return B64_EINVAL;
     if (n_out) *n_out = H > 0 ? 4 : 0;

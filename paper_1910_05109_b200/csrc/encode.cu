@@ -160,6 +160,24 @@ enc_fast_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__
     }
 }
 
+// The join of a streaming encode (stream.cu, R15), one thread: carry[0..H) are
+// held input bytes (H <= 2), in[0..n) the new piece.  If H > 0 and H + n >= 3 the straddling
+// triple carry ++ in[0 .. 3-H) is encoded to out[0..4).  The new carry is the last
+// (H + n) % 3 bytes of carry ++ in (read before the old carry is overwritten).
+__device__ __forceinline__ void enc_stream_join(uint8_t* carry, int H, const uint8_t* in, int64_t n, uint8_t* out,
+                                                const uint8_t* lut) {
+    const uint8_t c0 = carry[0], c1 = carry[1];
+    auto at = [&](int64_t i) -> uint32_t { return i < H ? (i == 0 ? c0 : c1) : in[i - H]; };
+    const int64_t A = H + n;
+    const int R = int(A % 3);
+    if (H > 0 && A >= 3) {
+        const uint32_t v = enc_triple((at(0) << 24) | (at(1) << 16) | (at(2) << 8), lut);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) out[k] = uint8_t(v >> (8 * k));
+    }
+    for (int k = 0; k < R; ++k) carry[k] = uint8_t(at(A - R + k));
+}
+
 // ---------------------------------------------------------------- generic / batch
 
 __device__ __forceinline__ void store16(uint8_t* dst, const uint32_t (&o)[4]) {

@@ -20,24 +20,13 @@
 
 namespace b64 {
 
-// carry[0..H) are held input bytes (H <= 2); in[0..n) is the new piece.
-// If H > 0 and H + n >= 3 the straddling triple carry ++ in[0 .. 3-H) is
-// encoded to out[0..4).  The new carry is the last (H + n) % 3 bytes of
-// carry ++ in (read before the old carry is overwritten).
+// The join of a streaming encode on its own (enc_stream_join, encode.cu), when it cannot ride
+// along with the piece's bulk kernel.
 __global__ void enc_stream_join_kernel(uint8_t* __restrict__ carry, int H, const uint8_t* __restrict__ in, int64_t n,
                                        uint8_t* __restrict__ out, EncTab tab) {
     griddep_wait();
-    const uint8_t* lut = reinterpret_cast<const uint8_t*>(tab.w);
-    const uint8_t c0 = carry[0], c1 = carry[1];
-    auto at = [&](int64_t i) -> uint32_t { return i < H ? (i == 0 ? c0 : c1) : in[i - H]; };
-    const int64_t A = H + n;
-    const int R = int(A % 3);
-    if (H > 0 && A >= 3) {
-        const uint32_t v = enc_triple((at(0) << 24) | (at(1) << 16) | (at(2) << 8), lut);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) out[k] = uint8_t(v >> (8 * k));
-    }
-    for (int k = 0; k < R; ++k) carry[k] = uint8_t(at(A - R + k));
+    carry = after_wait(carry);  // written by the previous piece's kernel
+    enc_stream_join(carry, H, in, n, out, reinterpret_cast<const uint8_t*>(tab.w));
 }
 
 // The end of an encode stream: the H (1 or 2) held bytes -> 4 chars with '='

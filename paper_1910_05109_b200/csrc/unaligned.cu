@@ -175,6 +175,105 @@ dec_fastu_kernel(const uint8_t* __restrict__ in, int64_t m, uint8_t* __restrict_
     }
 }
 
+// ---------------------------------------------------------------- encode at any input alignment
+// enc_fastu_kernel: the encode of a stream whose input is not 8-byte aligned or whose output
+// is 4- but not 32-byte aligned (misaligned single calls, shards, and above all the pieces of
+// a streaming encode, whose triples start wherever the previous piece left off).  The bulk
+// starts at the first triple q0 whose output is 32-byte aligned (q0 = (-out mod 32) / 4 < 8),
+// so the chunks' 1024-char outputs go out as in enc_fast_kernel (one lane-linear STG.256 per
+// lane).  Lane l's 24 input bytes of chunk c start at in + 3 q0 + 768 c + 24 l: the same
+// offset sb within an 8-byte word for EVERY lane and chunk (768 and 24 are multiples of 8),
+// so the loads are enc_fast's three LDG.64 at a 24-byte lane stride from the word-aligned
+// base plus a fourth when sb != 0, and one warp-uniform funnel shift realigns them.  The < 8
+// head triples, the < 256 after the last full chunk and the padded partial triple go one per
+// thread.
+// EARLY (an overlapped streaming piece, B64_STREAM_OVERLAP): the bulk runs before
+// griddepcontrol.wait; after it, the rest and the join with the held bytes (`join`, which
+// reads the carry the previous piece writes) by the last thread.
+template <int D, bool EARLY>
+__global__ void __launch_bounds__(kThreads)
+enc_fastu_kernel(const uint8_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, EncTab tab, uint32_t pad,
+                 int64_t q0, int32_t nchunk, EncJoin join) {
+    __shared__ __align__(64) uint32_t s_lut[16];
+    griddep_launch_dependents();
+    if (!EARLY) griddep_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t gtid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gthreads = int64_t(gridDim.x) * blockDim.x;
+    const int64_t nwarp = gthreads >> 5;
+    const uintptr_t ib = reinterpret_cast<uintptr_t>(in) + 3 * uintptr_t(q0);
+    const uint32_t sb = uint32_t(ib & 7);
+    const bool wsh = sb >= 4;
+    const uint32_t sh = (sb & 3) * 8;
+    const int32_t C = nchunk, W = int32_t(nwarp), c0i = int32_t(gtid >> 5);
+    const int64_t sin = nwarp * 768, sout = nwarp * 1024;
+    const uint8_t* pin = reinterpret_cast<const uint8_t*>(ib & ~uintptr_t(7)) + int64_t(c0i) * 768 + lane * 24;
+    uint8_t* pout = out + 4 * q0 + int64_t(c0i) * 1024 + lane * 32;
+    uint2 xr[D][4];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+        if (c0i + i * W < C) {
+            xr[i][0] = ld64_l1(pin);
+            xr[i][1] = ld64_l1(pin + 8);
+            xr[i][2] = ld64_l1(pin + 16);
+            xr[i][3] = sb ? ld64_l1(pin + 24) : make_uint2(0u, 0u);
+            pin += sin;
+        }
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s_lut[i] = tab.w[i];
+    }
+    __syncthreads();
+    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
+    const uint32_t lb = smem_u32(s_lut);
+    for (int32_t cb = c0i; cb < C; cb += D * W) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            const int32_t c = cb + i * W;
+            if (c < C) {
+                uint2 y[4];
+                if (c + D * W < C) {
+                    y[0] = ld64_l1(pin);
+                    y[1] = ld64_l1(pin + 8);
+                    y[2] = ld64_l1(pin + 16);
+                    y[3] = sb ? ld64_l1(pin + 24) : make_uint2(0u, 0u);
+                    pin += sin;
+                }
+                const uint32_t v[8] = {xr[i][0].x, xr[i][0].y, xr[i][1].x, xr[i][1].y,
+                                       xr[i][2].x, xr[i][2].y, xr[i][3].x, xr[i][3].y};
+                uint32_t w[6], o[8];
+#pragma unroll
+                for (int k = 0; k < 6; ++k) w[k] = __funnelshift_r(wsh ? v[k + 1] : v[k], wsh ? v[k + 2] : v[k + 1], sh);
+                enc_lane_compute(w, o, lb);
+                st256(pout, o);
+                pout += sout;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) xr[i][k] = y[k];
+            }
+        }
+    }
+    if (EARLY) griddep_wait();  // the previous piece done: its carry is written
+    // the head triples [0, q0), the triples after the last full chunk and the padded partial
+    // triple, one output word per thread (out 4-byte aligned)
+    const int64_t T = n / 3, Q = (n + 2) / 3;
+    const int64_t qt = q0 + int64_t(C) * 256;
+    const int64_t nrest = q0 + (Q - qt);
+    for (int64_t t = gtid; t < nrest; t += gthreads) {
+        const int64_t q = t < q0 ? t : qt + (t - q0);
+        const uint8_t* sp = in + 3 * q;
+        uint32_t word;
+        if (q < T) {
+            word = enc_triple((uint32_t(sp[0]) << 24) | (uint32_t(sp[1]) << 16) | (uint32_t(sp[2]) << 8), lut);
+        } else {
+            const int r = int(n - 3 * q);
+            word = enc_partial(sp[0], r == 2 ? sp[1] : 0u, r, lut, pad);
+        }
+        *reinterpret_cast<uint32_t*>(out + 4 * q) = word;
+    }
+    if (EARLY && join.active && gtid == gthreads - 1)
+        enc_stream_join(join.carry, join.H, join.in, join.n, join.out, lut);
+}
+
 // (D, WS) -> kernel
 using DecFastuFn = void (*)(const uint8_t*, int64_t, uint8_t*, DecTab, int64_t, int, unsigned long long*, int64_t*,
                             UnalignedBulk, StreamJoin);

@@ -137,6 +137,10 @@ def test_stream_host_state_machine(L):
     assert L.b64_decode_stream_begin_ex(ctypes.byref(st), carry, cell, 2, None) == -1
     assert L.b64_decode_stream_begin_ex(ctypes.byref(st), carry, None, _lib.STREAM_OVERLAP, None) == -1
     assert L.b64_decode_stream_begin_ex(None, carry, cell, 0, None) == -1
+    assert L.b64_encode_stream_begin_ex(ctypes.byref(st), carry, 2, None) == -1
+    assert L.b64_encode_stream_begin_ex(ctypes.byref(st), None, 0, None) == -1
+    assert L.b64_encode_stream_begin_ex(ctypes.byref(st), carry, 0, None) == 0  # no flags: no device work
+    assert (st.consumed, st.produced, st.held) == (0, 0, 0)
 
 
 def test_binding_is_marshalling_only():

@@ -671,3 +671,83 @@ def test_stream_overlap_vs_oracle(b64, ai):
                 assert torch.equal(got, base)
                 if err < 0:
                     assert olen == ref.size and np.array_equal(got[:olen].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("n", [150_000, 150_001, 150_002, 1_000_003])
+def test_encode_misaligned_every_phase(b64, n):
+    """Every input offset mod 8 x every 4-byte-aligned output offset mod 32 (all shifts of
+    enc_fastu_kernel and every head-triple count q0 = 0..7), plus an output that is not 4-byte
+    aligned (the byte-store generic path), against the oracle; the bytes around the output
+    are untouched."""
+    x = synth.data(n, seed=n)
+    ref = oracle.encode(x)
+    m = ref.size
+    xb = torch.empty(n + 64, dtype=torch.uint8, device=DEV)
+    ob = torch.empty(m + 128, dtype=torch.uint8, device=DEV)
+    xd = torch.from_numpy(x).to(DEV)
+    for ioff in range(8):
+        xin = xb[ioff: ioff + n]
+        xin.copy_(xd)
+        for ooff in list(range(0, 32, 4)) + [3]:
+            ob.fill_(0xA5)
+            out = b64.encode(xin, out=ob[32 + ooff: 32 + ooff + m])
+            assert out.numel() == m
+            h = ob.cpu().numpy()
+            assert (h[: 32 + ooff] == 0xA5).all() and (h[32 + ooff + m:] == 0xA5).all(), (ioff, ooff)
+            assert np.array_equal(h[32 + ooff: 32 + ooff + m], ref), (n, ioff, ooff)
+
+
+def test_encode_stream_large_pieces(b64):
+    """A streaming encode in large pieces of odd and aligned sizes (the pieces' bulk through
+    enc_fastu_kernel when misaligned, enc_fast_kernel when aligned, with 0-2 held bytes at the
+    boundaries): the concatenation equals the oracle's one-shot encode."""
+    x = synth.data(3_000_001, seed=5)
+    ref = oracle.encode(x)
+    xd = torch.from_numpy(x).to(DEV)
+    for piece in (100_001, 300_002, 262_144, 65_536 * 3):
+        es = b64.EncodeStream()
+        parts, p = [], 0
+        while p < x.size:
+            k = min(piece, x.size - p)
+            parts.append(es.update(xd[p: p + k]))
+            p += k
+        parts.append(es.end())
+        got = torch.cat(parts).cpu().numpy()
+        assert np.array_equal(got, ref), piece
+
+
+@pytest.mark.parametrize("ai", [0, 1, 3])
+def test_encode_stream_overlap_vs_oracle(b64, ai):
+    """B64_STREAM_OVERLAP for the streaming encode (each piece's bulk runs while the previous
+    piece drains; the join with the held bytes at the kernel's end): pieces of odd, aligned and
+    random sizes, written into ONE buffer with no launch in between, equal the oracle's one-shot
+    encode and the default mode's output, repeated to give a race a chance."""
+    perm = np.random.default_rng(7).permutation(127)[:65]
+    al = [(oracle.STANDARD, oracle.PAD, b64.standard()), (oracle.URL, oracle.PAD, b64.url()), None,
+          (bytes(perm[:64].tolist()), int(perm[64]), b64.alphabet(bytes(perm[:64].tolist()), bytes([int(perm[64])])))]
+    chars, pad, alpha = al[ai]
+    rng = np.random.default_rng(90 + ai)
+    x = synth.data(5_000_002 + ai, seed=90 + ai)
+    ref = oracle.encode(x, chars, pad)
+    xd = torch.from_numpy(x).to(DEV)
+    cuts = np.sort(rng.choice(np.arange(70_000, x.size - 70_000), 5, replace=False))
+    for pieces in ([(1 << 20) + 1] * (x.size // ((1 << 20) + 1)) + [x.size % ((1 << 20) + 1)],
+                   [3 << 18] * (x.size // (3 << 18)) + [x.size % (3 << 18)],
+                   np.diff(np.concatenate([[0], cuts, [x.size]])).tolist()):
+        outs = []
+        for overlap in (False, True, True, True):
+            es = b64.EncodeStream(alpha, overlap=overlap)
+            buf = torch.full((ref.size + 16,), 0xA5, dtype=torch.uint8, device=DEV)
+            o = p = 0
+            for k in pieces:
+                c = es.out_len(k)
+                got = es.update(xd[p: p + k], out=buf[o: o + max(c, 1)])
+                assert got.numel() == c
+                o += c
+                p += k
+            es.end(out=buf[o: o + max(es.end_len(), 1)])
+            outs.append(buf)
+        for b in outs:
+            assert torch.equal(b, outs[0])
+        h = outs[0].cpu().numpy()
+        assert np.array_equal(h[: ref.size], ref) and (h[ref.size:] == 0xA5).all(), (ai, pieces[:2])

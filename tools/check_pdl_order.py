@@ -16,7 +16,7 @@ import sys
 LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1910_05109_b200/libb64gpu.so"
 GLOBAL = re.compile(r"\b(LDG|STG|ATOMG|RED|LD\.E|ST\.E|UBLKCP|LDGSTS)\b")
 # B64_STREAM_OVERLAP pieces: the EARLY = true instantiations run their bulk before the wait
-ALLOW = ("dec_fast_kernel", "dec_fastu_kernel")
+ALLOW = ("dec_fast_kernel", "dec_fastu_kernel", "enc_fastu_kernel")
 
 
 def offenders(lib=LIB):
