@@ -18,7 +18,7 @@ import synth  # noqa: E402
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--op", choices=("enc", "dec", "both", "batch", "group", "peer", "decu"), default="both")
+    p.add_argument("--op", choices=("enc", "dec", "both", "batch", "group", "peer", "decu", "encu"), default="both")
     p.add_argument("--n", type=int, default=1 << 30)
     p.add_argument("--reps", type=int, default=3)
     a = p.parse_args()
@@ -88,6 +88,19 @@ def main():
         torch.cuda.synchronize()
         assert int(cell.item()) == b64.ERR_NONE
         print("ok decu")
+        return
+    if a.op == "encu":  # misaligned input (+1) and output (+4): enc_fast vs enc_fastu, alternating
+        xb = torch.empty(a.n + 64, dtype=torch.uint8, device="cuda")
+        synth.device_fill(xb, seed=0, offset=0)
+        x, xu = xb[: a.n], xb[1: 1 + a.n]
+        m = b64.encoded_len(a.n)
+        ob = torch.empty(m + 64, dtype=torch.uint8, device="cuda")
+        for _ in range(a.reps):
+            b64.encode(x, out=ob[:m])
+            b64.encode(xu, out=ob[4: 4 + m])
+        torch.cuda.synchronize()
+        assert torch.equal(ob[4: 4 + m], b64.encode(xu))
+        print("ok encu")
         return
     x = synth.device_data(a.n, seed=0)
     t = b64.encode(x)
