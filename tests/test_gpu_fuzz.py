@@ -55,7 +55,7 @@ lengths = st.one_of(st.integers(0, 40), st.integers(0, 5000), st.integers(760, 8
        off_in=st.sampled_from([0, 0, 1, 3, 8]), off_out=st.sampled_from([0, 0, 1, 2, 16]),
        lenient=st.booleans(), k_bad=st.integers(0, 3), seed=st.integers(0, 10_000),
        api=st.sampled_from(["single", "ctx", "chunk", "group", "codec", "stream", "batch", "unpadded", "ws",
-                            "ws_lines", "consume"]))
+                            "ws_lines", "consume", "stream_overlap"]))
 def test_fuzz_encode_decode_vs_oracle(b64, n, kind, aseed, off_in, off_out, lenient, k_bad, seed, api):
     chars, pad, alpha = _alpha(b64, kind, aseed)
     if lenient:
@@ -137,6 +137,39 @@ def test_fuzz_encode_decode_vs_oracle(b64, n, kind, aseed, off_in, off_out, leni
         parts.append(tail.cpu().numpy())
         err, stt, olen = info.tolist()
         got = np.concatenate(parts)[:olen]
+    elif api == "stream_overlap":  # B64_STREAM_OVERLAP: large random pieces into one buffer, no sync between
+        rng = np.random.default_rng(seed)
+        pre = synth.data(3 * (100_000 + seed), seed=seed + 3)  # a prefix so that pieces reach the fast kernels
+        x2 = np.concatenate([pre, x])
+        ref_t2 = oracle.encode(x2, chars, pad)
+        text = np.concatenate([oracle.encode(pre, chars, pad), text])
+        ref, rerr, rst = oracle.decode(text, chars, pad, lenient=lenient)
+        m = text.size
+        es = b64.EncodeStream(alpha, overlap=True)
+        dx = _dev(x2, off_in)
+        eb = torch.full((ref_t2.size + 8,), 0xA5, dtype=torch.uint8, device=DEV)
+        o = p = 0
+        while p < x2.size:
+            k = int(rng.integers(1, 200_000))
+            c = es.out_len(k if p + k <= x2.size else x2.size - p)
+            es.update(dx[p: p + k], out=eb[o: o + max(c, 1)])
+            o += c
+            p += k
+        es.end(out=eb[o: o + max(es.end_len(), 1)])
+        assert np.array_equal(eb[: ref_t2.size].cpu().numpy(), ref_t2), (api, n, seed)
+        ds = b64.DecodeStream(alpha, overlap=True)
+        dt = _dev(text, off_in)
+        db = torch.full((3 * (m // 4) + 8,), 0xA5, dtype=torch.uint8, device=DEV)
+        o = p = 0
+        while p < m:
+            k = min(int(rng.integers(1, 250_000)), m - p)
+            c = ds.out_len(k)
+            ds.update(dt[p: p + k], out=db[o: o + max(c, 1)])
+            o += c
+            p += k
+        tail, info = ds.end(out=db[o: o + max(ds.end_len(), 1)])
+        err, stt, olen = info.tolist()
+        got = db[:olen].cpu().numpy()
     elif api == "unpadded":  # the same text with its '=' stripped (R13), one call
         t_u = text[: text.size - int(np.sum(text[-2:] == pad))] if text.size >= 4 else text
         if t_u.size % 4 == 1:
