@@ -28,4 +28,4 @@ run 1g "(enc|dec)_fast_kernel" 2 2 python tools/prof_case.py --op both --n 10737
 run batch "enc_generic|dec_batch_bulk|dec_batch_strfinal|dec_batch_prep" 1 4 python tools/prof_case.py --op batch --reps 2
 run decu "dec_fast" 2 2 python tools/prof_case.py --op decu --n 67108864 --reps 2
 run encu "enc_fast" 2 2 python tools/prof_case.py --op encu --n 67108864 --reps 2
-run ws "ws_line_kernel|ws_line_reprobe" 3 4 python tools/ws_probe.py 268435456 irregular
+run ws "ws_line_kernel" 3 1 python tools/ws_probe.py 268435456 mime

@@ -16,6 +16,12 @@ import synth  # noqa: E402
 
 
 def main():
+    if os.environ.get("B64_LIB_PATH"):  # another build of the library (A/B)
+        import ctypes
+        path = os.environ["B64_LIB_PATH"]
+        probe = ctypes.CDLL(path)
+        b64._lib.LIB_PATH = path
+        b64._lib.SIGNATURES = [sg for sg in b64._lib.SIGNATURES if hasattr(probe, sg[0])]
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 30
     dev = torch.device("cuda:0")
     x = synth.device_data(n, seed=0)
