@@ -15,7 +15,8 @@ LIB = sys.argv[1] if len(sys.argv) > 1 else "paper_1910_05109_b200/libb64gpu.so"
 # kernel (mangled-name substring) -> (bulk store mnemonic, base64 chars per loop trip per warp, note)
 KERNELS = [
     ("enc_fast_kernelILi2", "STG.E.ENL2.256", 1024, "enc_fast_kernel<2>: 768 B -> 1024 chars per warp trip (D=2 unrolled: 2 chunks)"),
-    ("dec_fast_kernelILi2", "STG.E.64", 1024, "dec_fast_kernel<2>: 1024 chars -> 768 B per warp trip (D=2 unrolled: 2 chunks)"),
+    ("dec_fast_kernelILi2ELb0", "STG.E.64", 1024, "dec_fast_kernel<2>: 1024 chars -> 768 B per warp trip (D=2 unrolled: 2 chunks)"),
+    ("enc_fastu_kernelILi1ELb0", "STG.E.ENL2.256", 1024, "enc_fastu_kernel<1> (misaligned encode): 768 B -> 1024 chars per warp trip"),
     ("codec_group_kernelILi2", "STG.E.ENL2.256", 1024, "codec_group_kernel<2>, encode role"),
     ("dec_batch_bulk_kernelILi2", "STG.E.64", 1024, "dec_batch_bulk_kernel<2> (configs[3] decode)"),
     ("enc_generic_kernel", "STG.E.ENL2.256", 32, "enc_generic_kernel, flattened unit loop: 24 B -> 32 chars per LANE trip"),
