@@ -2,7 +2,8 @@
 """Whitespace-skipping decode timing: 1 GiB of data (or argv[1] bytes) as MIME text (76-char
 lines + CRLF), CUDA events, L2 flushed, median of 10.  argv[2]: "mime" (default, the line
 path), "irregular" (one stray blank in the middle: line pass, then the general path) or
-"start" (a stray blank after the first line: the general path almost at once)."""
+"start" (a stray blank after the first line), or "random" (lines of 60, 72, 84 and 76 chars in
+turn, each followed by LF: no uniform layout, the general path for the whole text)."""
 import json
 import os
 import statistics
@@ -40,7 +41,18 @@ def main():
     if m % 76:
         mime[-2:] = torch.tensor([13, 10], dtype=torch.uint8, device=dev)
     mode = sys.argv[2] if len(sys.argv) > 2 else "mime"
-    if mode != "mime":
+    if mode == "random":  # period of 4 lines: 60 + 72 + 84 + 76 = 292 chars, + 4 LF
+        rows = m // 292
+        body = t[: rows * 292].view(rows, 292)
+        v2 = torch.empty(rows, 296, dtype=torch.uint8, device=dev)
+        c = d = 0
+        for ln in (60, 72, 84, 76):
+            v2[:, d: d + ln] = body[:, c: c + ln]
+            v2[:, d + ln] = 10
+            c += ln
+            d += ln + 1
+        mime = torch.cat([v2.view(-1), t[rows * 292:]])
+    elif mode != "mime":
         at = mime.numel() // 2 if mode == "irregular" else 100
         mime = torch.cat([mime[:at], torch.tensor([32], dtype=torch.uint8, device=dev), mime[at:]])
     out = torch.empty(b64.decoded_len_max(mime.numel()), dtype=torch.uint8, device=dev)
