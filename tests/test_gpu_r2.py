@@ -751,3 +751,28 @@ def test_encode_stream_overlap_vs_oracle(b64, ai):
             assert torch.equal(b, outs[0])
         h = outs[0].cpu().numpy()
         assert np.array_equal(h[: ref.size], ref) and (h[ref.size:] == 0xA5).all(), (ai, pieces[:2])
+
+
+def test_decode_ws_general_path_errors_across_tiles(b64):
+    """The general path's one-pass compaction (tiles of 8 chunks of 4 KiB, decoupled look-back)
+    and its error mapping: one bad char at a time in the first chunk, at a tile boundary, deep in
+    the middle and in the last tile of a 2.5 MB irregular text; whitespace-only tails of several
+    chunks; the same texts decoded twice in a row (the tile states are reset per call)."""
+    x = synth.data(1_900_003, seed=61)
+    text = oracle.encode(x)
+    t = _wrap(text, 45, 61, b"\r\n \t")
+    tile = 8 * 4096
+    keep = np.nonzero(~np.isin(t, np.frombuffer(b"\r\n \t", np.uint8)))[0]
+    for target in (5, tile - 1, tile, 3 * tile + 17, t.size // 2, t.size - 40):
+        p = int(keep[np.searchsorted(keep, target)])
+        t2 = t.copy()
+        t2[p] = ord("%")
+        ref, rerr, rst = oracle.decode_ws(t2)
+        for _ in range(2):
+            out, err = b64.decode_ws(torch.from_numpy(t2).to(DEV))
+            assert err == rerr == p, (target, err, rerr)
+            assert np.array_equal(out.cpu().numpy(), ref)
+    t3 = np.concatenate([t, np.frombuffer(b" \r\n\t" * 5000, np.uint8)])  # 20 KB of trailing whitespace
+    ref, rerr, _ = oracle.decode_ws(t3)
+    out, err = b64.decode_ws(torch.from_numpy(t3).to(DEV))
+    assert err == rerr == -1 and np.array_equal(out.cpu().numpy(), ref)
