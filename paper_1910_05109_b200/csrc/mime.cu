@@ -790,16 +790,17 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
 }
 
 // One-pass general path (round 2): count and compaction in ONE read of the text, by
-// decoupled look-back over tiles of kWsTileChunks chunks (one chunk per warp).  A CTA takes
-// the next tile from a counter (tiles start in order, so every predecessor is owned by a
-// running CTA), compacts its chunks into shared memory, publishes the tile's aggregate, sums
-// the predecessors' published words back to the nearest inclusive prefix (warp 0, 32 tiles
-// per probe), publishes its inclusive prefix and copies the compacted bytes out.  The
-// count kernel's full read of the text and the scan kernel disappear; the per-chunk counts
-// and per-tile bases stay for ws_finalize_kernel's error mapping (its K = kWsTileChunks).
-// State words: bits 62-63 = 0 empty / 1 aggregate / 2 inclusive prefix, bits 0-61 the value;
-// word 0 of the state array is the tile counter, tile t's word is [1 + t] (zeroed per call).
-constexpr int kWsTileChunks = kThreads / 32;
+// decoupled look-back over the chunks.  Each warp takes the next chunk from a counter (chunks
+// start in order, so every predecessor is owned by a running warp), compacts it into its
+// shared buffer, publishes the chunk's kept count, sums the predecessors' published words back
+// to the nearest inclusive prefix (32 chunks per probe, one per lane), publishes its own
+// inclusive prefix and copies the compacted bytes out -- warps never wait for each other
+// except through the look-back.  The count kernel's full read of the text and the scan kernel
+// disappear; the per-chunk counts and bases stay for ws_finalize_kernel's error mapping
+// (K = 1).  State words: bits 62-63 = 0 empty / 1 count / 2 inclusive prefix, bits 0-61 the
+// value; word 0 of the state array is the chunk counter, chunk c's word is [1 + c] (zeroed
+// per call).
+constexpr int kWsTileChunks = 1;
 constexpr unsigned long long kTileAgg = 1ull << 62, kTileIncl = 2ull << 62, kTileVal = (1ull << 62) - 1;
 
 __device__ __forceinline__ void tile_publish(unsigned long long* p, unsigned long long v) {
@@ -819,8 +820,6 @@ ws_compact1_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, unsigne
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(16) uint8_t s_buf[kThreads / 32][kWsChunk + 16];
     __shared__ uint32_t s_sel[16];
-    __shared__ int32_t s_wcnt[kThreads / 32];
-    __shared__ int64_t s_tile, s_prefix;
     griddep_launch_dependents();
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
     if (threadIdx.x < 16) {
@@ -832,6 +831,7 @@ ws_compact1_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, unsigne
     }
     griddep_wait();
     state = after_wait(state);
+    __syncthreads();
     if (__ldcg(&li->mode) != 0) return;
     const WsSuffix sx = ws_suffix(in, li);
     const int64_t k0 = __ldcg(&li->k0);
@@ -840,67 +840,48 @@ ws_compact1_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, unsigne
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
-    const int64_t ntiles = (nch + kWsTileChunks - 1) / kWsTileChunks;
     const bool vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
     uint8_t* buf = &s_buf[wib][0];
-    __syncthreads();
     for (;;) {
-        if (threadIdx.x == 0) s_tile = int64_t(atomicAdd(state, 1ull));
-        __syncthreads();
-        const int64_t t = s_tile;
-        if (t >= ntiles) break;
-        const int64_t c = t * kWsTileChunks + wib;
-        int n_kept = 0;
-        if (c < nch) n_kept = ws_compact_chunk<SW>(in, m, c * kWsChunk, sx.excl, vec, lut, s_sel, buf, lane);
+        unsigned long long tk = 0;
+        if (lane == 0) tk = atomicAdd(state, 1ull);
+        const int64_t t = int64_t(__shfl_sync(kFull, tk, 0));
+        if (t >= nch) break;
+        const int n_kept = ws_compact_chunk<SW>(in, m, t * kWsChunk, sx.excl, vec, lut, s_sel, buf, lane);
+        int64_t prefix = 0;
+        if (t == 0) {
+            if (lane == 0) tile_publish(state + 1, kTileIncl | uint64_t(n_kept));
+        } else {
+            if (lane == 0) tile_publish(state + 1 + t, kTileAgg | uint64_t(n_kept));
+            // look back: lane l reads chunk p - l; sum counts down to the nearest inclusive prefix
+            int64_t p = t - 1;
+            for (;;) {
+                const int64_t q = p - lane;
+                unsigned long long v = q >= 0 ? tile_peek(state + 1 + q) : kTileIncl;
+                while (__any_sync(kFull, (v >> 62) == 0))  // until all 32 probed chunks published
+                    if ((v >> 62) == 0) v = tile_peek(state + 1 + q);
+                const uint32_t incl = __ballot_sync(kFull, (v >> 62) == 2);
+                const int first = incl ? __ffs(incl) - 1 : 32;  // lanes up to the first inclusive one
+                int64_t mine = (lane <= first && q >= 0) ? int64_t(v & kTileVal) : 0;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(kFull, mine, d);
+                prefix += mine;
+                if (incl) break;
+                p -= 32;
+            }
+            if (lane == 0) tile_publish(state + 1 + t, kTileIncl | uint64_t(prefix + n_kept));
+        }
         if (lane == 0) {
-            s_wcnt[wib] = n_kept;
-            if (c < nch) counts[c] = n_kept;
-        }
-        __syncthreads();
-        if (wib == 0) {
-            int64_t agg = 0;
-#pragma unroll
-            for (int w = 0; w < kThreads / 32; ++w) agg += s_wcnt[w];
-            int64_t prefix = 0;
-            if (t == 0) {
-                if (lane == 0) tile_publish(state + 1, kTileIncl | uint64_t(agg));
-            } else {
-                if (lane == 0) tile_publish(state + 1 + t, kTileAgg | uint64_t(agg));
-                // look back: lane l reads tile p - l; sum aggregates down to the nearest inclusive
-                int64_t p = t - 1;
-                for (;;) {
-                    const int64_t q = p - lane;
-                    unsigned long long v = q >= 0 ? tile_peek(state + 1 + q) : kTileIncl;
-                    // wait until all 32 probed tiles have published something
-                    while (__any_sync(kFull, (v >> 62) == 0)) {
-                        if ((v >> 62) == 0) v = tile_peek(state + 1 + q);
-                    }
-                    const uint32_t incl = __ballot_sync(kFull, (v >> 62) == 2);
-                    // lanes up to (and including) the first inclusive one contribute
-                    const int first = incl ? __ffs(incl) - 1 : 32;
-                    int64_t mine = lane <= first && q >= 0 ? int64_t(v & kTileVal) : 0;
-#pragma unroll
-                    for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(kFull, mine, d);
-                    prefix += mine;
-                    if (incl) break;
-                    p -= 32;
-                }
-                if (lane == 0) tile_publish(state + 1 + t, kTileIncl | uint64_t(prefix + agg));
-            }
-            if (lane == 0) {
-                tile_base[t] = k0 + prefix;
-                s_prefix = prefix;
-                if (t == ntiles - 1) {
-                    m_out[0] = k0 + prefix + agg;  // the total kept count
-                    m_out[1] = k0;                 // where the suffix starts in the compacted text
-                }
+            counts[t] = n_kept;
+            tile_base[t] = k0 + prefix;
+            if (t == nch - 1) {
+                m_out[0] = k0 + prefix + n_kept;  // the total kept count
+                m_out[1] = k0;                    // where the suffix starts in the compacted text
             }
         }
-        __syncthreads();
-        int64_t off = s_prefix;
-        for (int w = 0; w < wib; ++w) off += s_wcnt[w];
-        ws_copy_out(buf, n_kept, dst + k0 + off, lane);
-        __syncthreads();  // buffers and counts reused by the next tile
+        __syncwarp();
+        ws_copy_out(buf, n_kept, dst + k0 + prefix, lane);
+        __syncwarp();  // the buffer is reused by the next chunk
     }
 }
 
