@@ -28,7 +28,7 @@ struct DevInfo {
     int sms = 0;
     int occ_group[4] = {0, 0, 0, 0};  // min over the enc / dec / codec group kernels
     int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_enc_gen = 0, occ_dec_gen = 0;
-    int occ_batch_bulk = 0, occ_fastu[3][8] = {}, occ_enc_fastu = 0, occ_ws_compact1 = 0;
+    int occ_batch_bulk = 0, occ_fastu[3][8] = {}, occ_enc_fastu = 0;
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -90,10 +90,6 @@ const DevInfo* dev_info() {
         cudaSuccess)
         return nullptr;
     info.occ_enc_fastu = info.occ_enc_fastu < 1 ? 1 : info.occ_enc_fastu;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.occ_ws_compact1, ws_compact1_kernel<true>, kThreads, 0) !=
-        cudaSuccess)
-        return nullptr;
-    info.occ_ws_compact1 = info.occ_ws_compact1 < 1 ? 1 : info.occ_ws_compact1;
     if (cudaFuncSetAttribute(dec_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
         cudaFuncSetAttribute(ws_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         return nullptr;
@@ -501,8 +497,8 @@ int b64_decode_unpadded(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b6
 // ---------------------------------------------------------------- whitespace-skipping decode (mime.cu)
 namespace {
 struct WsLayout {
-    int64_t nch, ncta, K, ntiles;
-    int64_t off_counts, off_tot, off_base, off_mc, off_state, off_tbase, total;
+    int64_t nch, ncta, K;
+    int64_t off_counts, off_tot, off_base, off_mc, total;
 };
 int64_t up256(int64_t v) { return (v + 255) / 256 * 256; }
 WsLayout ws_layout(int64_t m) {
@@ -517,11 +513,7 @@ WsLayout ws_layout(int64_t m) {
     L.off_tot = L.off_counts + up256(4 * (L.nch + 1));
     L.off_base = L.off_tot + up256(8 * kWsMaxCtas);
     L.off_mc = L.off_base + up256(8 * kWsMaxCtas);
-    // the one-pass compaction's tile states (word 0: the tile counter) and tile bases
-    L.ntiles = (L.nch + kWsTileChunks - 1) / kWsTileChunks;
-    L.off_state = L.off_mc + 256;
-    L.off_tbase = L.off_state + up256(8 * (L.ntiles + 1));
-    L.total = L.off_tbase + up256(8 * (L.ntiles > 0 ? L.ntiles : 1)) + 256;  // + slack to align the caller's pointer
+    L.total = L.off_mc + 256 + 256;  // + slack to align the caller's pointer
     return L;
 }
 }  // namespace
@@ -590,14 +582,6 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
     // the mode)
     WsLine* li = reinterpret_cast<WsLine*>(base + L.off_mc + 64);
     const WsLine* lic = li;
-    static const bool one_pass = [] {  // B64_WS_ONEPASS=0: the count / scan / compact kernels (A/B)
-        const char* e = std::getenv("B64_WS_ONEPASS");
-        return !(e && e[0] == '0');
-    }();
-    unsigned long long* tstate = reinterpret_cast<unsigned long long*>(base + L.off_state);
-    int64_t* tbase = reinterpret_cast<int64_t*>(base + L.off_tbase);
-    // (a memset, before the first kernel: the one-pass compaction's tile counter and states)
-    if (one_pass && cudaMemsetAsync(tstate, 0, size_t(8 * (L.ntiles + 1)), s) != cudaSuccess) return B64_ECUDA;
     launch(ws_line_probe_kernel, 1, 32, s, d_in, m, wt, li, mc);
     // up to kLineSegs line segments (B64_WS_SEGS overrides, >= 1): a text whose layout breaks
     // somewhere (a stray byte) is cut there and the rest probed again; after the last one the
@@ -611,29 +595,21 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
         launch(ws_line_kernel, int64_t(di->sms) * B64_LINE_MINB, kLineThreads, s, d_in, m, wt, li, d_out);
         launch(ws_line_reprobe_kernel, 1, kPatchThreads, s, d_in, m, wt, li, d_out, seg == nseg - 1 ? 1 : 0);
     }
-    if (one_pass) {
-        const int64_t grid = std::min<int64_t>(L.ntiles > 0 ? L.ntiles : 1, int64_t(di->sms) * di->occ_ws_compact1);
-        launch(sw ? ws_compact1_kernel<true> : ws_compact1_kernel<false>, grid, kThreads, s, d_in, m, wt, tstate,
-               counts, tbase, comp, mc, lic);
-    } else {
-        launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot, lic);
-        launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc, lic);
-        launch(sw ? ws_compact_kernel<true> : ws_compact_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K,
-               static_cast<const int32_t*>(counts), static_cast<const int64_t*>(cbase), comp, lic);
-    }
+    launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot, lic);
+    launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc, lic);
+    launch(sw ? ws_compact_kernel<true> : ws_compact_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, static_cast<const int32_t*>(counts),
+           static_cast<const int64_t*>(cbase), comp, lic);
     {  // strict decode of the compacted text; its length m' is read on the device
         const int64_t blocks = balanced_blocks(m / 1024, int64_t(di->sms) * cap_bps(di->occ_dec_fast[1]));
         launch(dec_fast_kernel<1>, blocks, kThreads, s, static_cast<const uint8_t*>(comp), m, d_out, dec_tab(a),
                int64_t(0), 1, reinterpret_cast<unsigned long long*>(d_err_off), static_cast<int64_t*>(nullptr),
                static_cast<const int64_t*>(mc), StreamJoin{});
     }
-    // error mapping: per-CTA bases of K chunks, or the one-pass path's per-tile bases
     launch(ws_finalize_kernel, 1, 32, s, d_err_off, d_status, d_out_len, static_cast<const int64_t*>(mc), d_in, m,
-           static_cast<const uint8_t*>(comp), wt, uint32_t(a->pad), one_pass ? int64_t(kWsTileChunks) : L.K,
-           int(one_pass ? L.ntiles : L.ncta), static_cast<const int32_t*>(counts),
-           static_cast<const int64_t*>(one_pass ? tbase : cbase), lic, d_out,
+           static_cast<const uint8_t*>(comp), wt, uint32_t(a->pad), L.K, int(L.ncta),
+           static_cast<const int32_t*>(counts), static_cast<const int64_t*>(cbase), lic, d_out,
            uint32_t((a->flags & B64_ALPHA_LENIENT) ? 1 : 0));
-    g_launches.fetch_add((one_pass ? 3 : 5) + 2 * nseg, std::memory_order_relaxed);
+    g_launches.fetch_add(5 + 2 * nseg, std::memory_order_relaxed);
     return launched();
 }
 

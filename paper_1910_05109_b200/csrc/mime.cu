@@ -644,88 +644,6 @@ __global__ void __launch_bounds__(1024) ws_scan_kernel(const int64_t* __restrict
     }
 }
 
-// The kept bytes of chunk [b0, b0 + kWsChunk) of the (suffix) text, compacted into the warp's
-// shared buffer `buf`; returns their count.  Bytes before `excl` are not kept.
-template <bool SW>
-__device__ __forceinline__ int ws_compact_chunk(const uint8_t* __restrict__ in, int64_t m, int64_t b0, int64_t excl,
-                                                bool vec, const uint8_t* lut, const uint32_t* s_sel, uint8_t* buf,
-                                                int lane) {
-    const int len = int(min(int64_t(kWsChunk), m - b0));
-    int n_kept = 0;
-    if (vec && len == kWsChunk && b0 >= excl) {
-        // 32 rows of 128 B, lane l holding word l of a row (lane-linear LDG.32, 8 rows in
-        // flight): a lane's kept bytes go to consecutive positions ~4 bytes after the
-        // previous lane's, so the byte stores of a row hit distinct banks (the 16-byte-per-
-        // lane layout put lanes 8 apart on one bank: 4-way conflicts on every byte store).
-        // Per row: a 4-bit keep mask, the kept bytes packed by one PRMT (selector table in
-        // shared memory), their count; the counts of 4 rows ride in one word (8 bits each,
-        // <= 128) so ONE warp scan serves 4 rows.
-#pragma unroll 1
-        for (int g = 0; g < kWsChunk / 1024; ++g) {
-            uint32_t w[8];
-#pragma unroll
-            for (int r = 0; r < 8; ++r) w[r] = ld32_nc(in + b0 + (g * 8 + r) * 128 + lane * 4);
-            uint32_t km[8], pc[2] = {0u, 0u};
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                km[r] = keep4<SW>(lut, w[r]);
-                pc[r >> 2] |= uint32_t(__popc(km[r])) << (8 * (r & 3));
-            }
-            uint32_t ex[2], tot[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t x = pc[h];
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t y = __shfl_up_sync(kFull, x, d);
-                    if (lane >= d) x += y;
-                }
-                tot[h] = __shfl_sync(kFull, x, 31);
-                ex[h] = x - pc[h];
-            }
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const int pos = n_kept + int((ex[r >> 2] >> (8 * (r & 3))) & 0xffu);
-                const uint32_t cw = __byte_perm(w[r], 0u, s_sel[km[r]]);
-                const int cnt = __popc(km[r]);
-                if (cnt > 0) buf[pos] = uint8_t(cw);
-                if (cnt > 1) buf[pos + 1] = uint8_t(cw >> 8);
-                if (cnt > 2) buf[pos + 2] = uint8_t(cw >> 16);
-                if (cnt > 3) buf[pos + 3] = uint8_t(cw >> 24);
-                n_kept += int((tot[r >> 2] >> (8 * (r & 3))) & 0xffu);
-            }
-        }
-    } else {
-        for (int i0 = 0; i0 < len; i0 += 32) {
-            const int i = i0 + lane;
-            const uint32_t c = i < len ? in[b0 + i] : 0u;
-            const bool keep = i < len && b0 + i >= excl && ws_keep(lut, c);
-            const uint32_t bal = __ballot_sync(kFull, keep);
-            if (keep) buf[n_kept + __popc(bal & ((1u << lane) - 1u))] = uint8_t(c);
-            n_kept += __popc(bal);
-        }
-    }
-    return n_kept;
-}
-
-// The warp's compacted bytes buf[0, n_kept) to d: byte head up to 4-alignment, words, byte tail.
-__device__ __forceinline__ void ws_copy_out(const uint8_t* buf, int n_kept, uint8_t* d, int lane) {
-    const int head = int((4 - (reinterpret_cast<uintptr_t>(d) & 3)) & 3);
-    const int h = head < n_kept ? head : n_kept;
-    if (lane < h) d[lane] = buf[lane];
-    const int nw = (n_kept - h) >> 2;
-    // word t of the output = buffer bytes [h + 4t, h + 4t + 4): two aligned shared words + a
-    // funnel shift (h < 4 is uniform; the second word may lie past the kept bytes -- unused)
-    const uint32_t* bw = reinterpret_cast<const uint32_t*>(buf);
-    const uint32_t fsh = uint32_t(h) * 8;
-    for (int t = lane; t < nw; t += 32) {
-        const uint32_t v = __funnelshift_r(bw[t], bw[t + 1], fsh);
-        *reinterpret_cast<uint32_t*>(d + h + 4 * t) = v;
-    }
-    const int tail0 = h + 4 * nw;
-    if (lane < n_kept - tail0) d[tail0 + lane] = buf[tail0 + lane];
-}
-
 template <bool SW>
 __global__ void __launch_bounds__(kThreads)
 ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K, const int32_t* __restrict__ counts,
@@ -782,106 +700,79 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
         const int64_t off = s_pref[seg] + mine;
 
         const int64_t b0 = (c_lo + j) * kWsChunk;
-        const int n_kept = ws_compact_chunk<SW>(in, m, b0, sx.excl, vec, lut, s_sel, buf, lane);
-        __syncwarp();
-        ws_copy_out(buf, n_kept, dst + off, lane);
-        __syncwarp();
-    }
-}
-
-// One-pass general path (round 2): count and compaction in ONE read of the text, by
-// decoupled look-back over the chunks.  Each warp takes the next chunk from a counter (chunks
-// start in order, so every predecessor is owned by a running warp), compacts it into its
-// shared buffer, publishes the chunk's kept count, sums the predecessors' published words back
-// to the nearest inclusive prefix (32 chunks per probe, one per lane), publishes its own
-// inclusive prefix and copies the compacted bytes out -- warps never wait for each other
-// except through the look-back.  The count kernel's full read of the text and the scan kernel
-// disappear; the per-chunk counts and bases stay for ws_finalize_kernel's error mapping
-// (K = 1).  State words: bits 62-63 = 0 empty / 1 count / 2 inclusive prefix, bits 0-61 the
-// value; word 0 of the state array is the chunk counter, chunk c's word is [1 + c] (zeroed
-// per call).
-constexpr int kWsTileChunks = 1;
-constexpr unsigned long long kTileAgg = 1ull << 62, kTileIncl = 2ull << 62, kTileVal = (1ull << 62) - 1;
-
-__device__ __forceinline__ void tile_publish(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long tile_peek(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-template <bool SW>
-__global__ void __launch_bounds__(kThreads)
-ws_compact1_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, unsigned long long* __restrict__ state,
-                   int32_t* __restrict__ counts, int64_t* __restrict__ tile_base, uint8_t* __restrict__ dst,
-                   int64_t* __restrict__ m_out, const WsLine* __restrict__ li) {
-    __shared__ __align__(256) uint32_t s_lut[64];
-    __shared__ __align__(16) uint8_t s_buf[kThreads / 32][kWsChunk + 16];
-    __shared__ uint32_t s_sel[16];
-    griddep_launch_dependents();
-    if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
-    if (threadIdx.x < 16) {
-        uint32_t sel = 0x4444u;
-        int k = 0;
-        for (int b = 0; b < 4; ++b)
-            if (threadIdx.x & (1 << b)) sel = (sel & ~(0xFu << (4 * k))) | (uint32_t(b) << (4 * k)), ++k;
-        s_sel[threadIdx.x] = sel;
-    }
-    griddep_wait();
-    state = after_wait(state);
-    __syncthreads();
-    if (__ldcg(&li->mode) != 0) return;
-    const WsSuffix sx = ws_suffix(in, li);
-    const int64_t k0 = __ldcg(&li->k0);
-    in += sx.A;
-    m -= sx.A;
-    const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
-    const bool vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
-    uint8_t* buf = &s_buf[wib][0];
-    for (;;) {
-        unsigned long long tk = 0;
-        if (lane == 0) tk = atomicAdd(state, 1ull);
-        const int64_t t = int64_t(__shfl_sync(kFull, tk, 0));
-        if (t >= nch) break;
-        const int n_kept = ws_compact_chunk<SW>(in, m, t * kWsChunk, sx.excl, vec, lut, s_sel, buf, lane);
-        int64_t prefix = 0;
-        if (t == 0) {
-            if (lane == 0) tile_publish(state + 1, kTileIncl | uint64_t(n_kept));
-        } else {
-            if (lane == 0) tile_publish(state + 1 + t, kTileAgg | uint64_t(n_kept));
-            // look back: lane l reads chunk p - l; sum counts down to the nearest inclusive prefix
-            int64_t p = t - 1;
-            for (;;) {
-                const int64_t q = p - lane;
-                unsigned long long v = q >= 0 ? tile_peek(state + 1 + q) : kTileIncl;
-                while (__any_sync(kFull, (v >> 62) == 0))  // until all 32 probed chunks published
-                    if ((v >> 62) == 0) v = tile_peek(state + 1 + q);
-                const uint32_t incl = __ballot_sync(kFull, (v >> 62) == 2);
-                const int first = incl ? __ffs(incl) - 1 : 32;  // lanes up to the first inclusive one
-                int64_t mine = (lane <= first && q >= 0) ? int64_t(v & kTileVal) : 0;
+        const int len = int(min(int64_t(kWsChunk), m - b0));
+        int n_kept = 0;
+        if (vec && len == kWsChunk && b0 >= sx.excl) {
+            // 32 rows of 128 B, lane l holding word l of a row (lane-linear LDG.32, 8 rows in
+            // flight): a lane's kept bytes go to consecutive positions ~4 bytes after the
+            // previous lane's, so the byte stores of a row hit distinct banks (the 16-byte-per-
+            // lane layout put lanes 8 apart on one bank: 4-way conflicts on every byte store).
+            // Per row: a 4-bit keep mask, the kept bytes packed by one PRMT (selector table in
+            // shared memory), their count; the counts of 4 rows ride in one word (8 bits each,
+            // <= 128) so ONE warp scan serves 4 rows.
+#pragma unroll 1
+            for (int g = 0; g < kWsChunk / 1024; ++g) {
+                uint32_t w[8];
 #pragma unroll
-                for (int d = 16; d > 0; d >>= 1) mine += __shfl_xor_sync(kFull, mine, d);
-                prefix += mine;
-                if (incl) break;
-                p -= 32;
+                for (int r = 0; r < 8; ++r) w[r] = ld32_nc(in + b0 + (g * 8 + r) * 128 + lane * 4);
+                uint32_t km[8], pc[2] = {0u, 0u};
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    km[r] = keep4<SW>(lut, w[r]);
+                    pc[r >> 2] |= uint32_t(__popc(km[r])) << (8 * (r & 3));
+                }
+                uint32_t ex[2], tot[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t x = pc[h];
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(kFull, x, d);
+                        if (lane >= d) x += y;
+                    }
+                    tot[h] = __shfl_sync(kFull, x, 31);
+                    ex[h] = x - pc[h];
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int pos = n_kept + int((ex[r >> 2] >> (8 * (r & 3))) & 0xffu);
+                    const uint32_t cw = __byte_perm(w[r], 0u, s_sel[km[r]]);
+                    const int cnt = __popc(km[r]);
+                    if (cnt > 0) buf[pos] = uint8_t(cw);
+                    if (cnt > 1) buf[pos + 1] = uint8_t(cw >> 8);
+                    if (cnt > 2) buf[pos + 2] = uint8_t(cw >> 16);
+                    if (cnt > 3) buf[pos + 3] = uint8_t(cw >> 24);
+                    n_kept += int((tot[r >> 2] >> (8 * (r & 3))) & 0xffu);
+                }
             }
-            if (lane == 0) tile_publish(state + 1 + t, kTileIncl | uint64_t(prefix + n_kept));
-        }
-        if (lane == 0) {
-            counts[t] = n_kept;
-            tile_base[t] = k0 + prefix;
-            if (t == nch - 1) {
-                m_out[0] = k0 + prefix + n_kept;  // the total kept count
-                m_out[1] = k0;                    // where the suffix starts in the compacted text
+        } else {
+            for (int i0 = 0; i0 < len; i0 += 32) {
+                const int i = i0 + lane;
+                const uint32_t c = i < len ? in[b0 + i] : 0u;
+                const bool keep = i < len && b0 + i >= sx.excl && ws_keep(lut, c);
+                const uint32_t bal = __ballot_sync(kFull, keep);
+                if (keep) buf[n_kept + __popc(bal & ((1u << lane) - 1u))] = uint8_t(c);
+                n_kept += __popc(bal);
             }
         }
         __syncwarp();
-        ws_copy_out(buf, n_kept, dst + k0 + prefix, lane);
-        __syncwarp();  // the buffer is reused by the next chunk
+        // copy the compacted chunk to dst + off: byte head up to 4-alignment, words, byte tail
+        uint8_t* d = dst + off;
+        const int head = int((4 - (reinterpret_cast<uintptr_t>(d) & 3)) & 3);
+        const int h = head < n_kept ? head : n_kept;
+        if (lane < h) d[lane] = buf[lane];
+        const int nw = (n_kept - h) >> 2;
+        // word t of the output = buffer bytes [h + 4t, h + 4t + 4): two aligned shared words + a
+        // funnel shift (h < 4 is uniform; the second word may lie past the kept bytes -- unused)
+        const uint32_t* bw = reinterpret_cast<const uint32_t*>(buf);
+        const uint32_t fsh = uint32_t(h) * 8;
+        for (int t = lane; t < nw; t += 32) {
+            const uint32_t v = __funnelshift_r(bw[t], bw[t + 1], fsh);
+            *reinterpret_cast<uint32_t*>(d + h + 4 * t) = v;
+        }
+        const int tail0 = h + 4 * nw;
+        if (lane < n_kept - tail0) d[tail0 + lane] = buf[tail0 + lane];
+        __syncwarp();
     }
 }
 
@@ -1162,14 +1053,13 @@ ws_finalize_kernel(int64_t* err_off, int32_t* status, int64_t* out_len, const in
     }
     in += sx.A;
     m -= sx.A;
-    const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
-    // CTA (or one-pass tile) holding compacted index e: the last b with cta_base[b] <= e, among
-    // the groups of K chunks the suffix has (the one-pass path writes no base beyond them)
-    int lo = 0, hi = int(min(int64_t(ncta), (nch + K - 1) / K)) - 1;
+    // CTA holding compacted index e: the last b with cta_base[b] <= e
+    int lo = 0, hi = ncta - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (cta_base[mid] <= e) lo = mid; else hi = mid - 1;
     }
+    const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
     int64_t run = cta_base[lo];
     int64_t c = int64_t(lo) * K;
     const int64_t c_end = min(c + K, nch);

@@ -754,10 +754,10 @@ def test_encode_stream_overlap_vs_oracle(b64, ai):
 
 
 def test_decode_ws_general_path_errors_across_tiles(b64):
-    """The general path's one-pass compaction (tiles of 8 chunks of 4 KiB, decoupled look-back)
-    and its error mapping: one bad char at a time in the first chunk, at a tile boundary, deep in
-    the middle and in the last tile of a 2.5 MB irregular text; whitespace-only tails of several
-    chunks; the same texts decoded twice in a row (the tile states are reset per call)."""
+    """The general path (count / scan / compaction over 4 KiB chunks grouped per CTA) and its
+    error mapping: one bad char at a time in the first chunk, at 32 KiB, deep in the middle and
+    in the last chunks of a 2.5 MB irregular text; a whitespace-only tail of several chunks; the
+    same texts decoded twice in a row."""
     x = synth.data(1_900_003, seed=61)
     text = oracle.encode(x)
     t = _wrap(text, 45, 61, b"\r\n \t")
