@@ -389,14 +389,26 @@ __device__ __forceinline__ int32_t div_small(int32_t x, int32_t d, float inv) {
 #ifndef B64_LINE_MINB
 #define B64_LINE_MINB 6
 #endif
+#ifndef B64_LINE_TMA
+#define B64_LINE_TMA 1
+#endif
 __global__ void __launch_bounds__(kLineThreads, B64_LINE_MINB)
 ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li,
                uint8_t* __restrict__ out) {
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(16) uint8_t s_stage[kLineThreads / 32][kLineStage];
     __shared__ __align__(16) uint8_t s_comp[kLineThreads / 32][kLineBlk + 48];
+#if B64_LINE_TMA
+    __shared__ __align__(8) uint64_t s_lbar[kLineThreads / 32];
+#endif
     griddep_launch_dependents();
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
+#if B64_LINE_TMA
+    if ((threadIdx.x & 31) == 0) {
+        mbar_init(smem_u32(&s_lbar[threadIdx.x >> 5]), 1);
+        mbar_init_fence();
+    }
+#endif
     griddep_wait();
     __syncthreads();
     if (__ldcg(&li->mode) != 1) return;
@@ -426,17 +438,54 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
     const int32_t step_col = int32_t(W * kLineBlk - step_lines * L);
     bool irregular = false;
     int64_t bad = INT64_MAX;  // first invalid kept index seen by this lane
+    // a step's text span: [b0, b0 + 16 nch) holds its kept chars and the separators after them
+    // (b0 = its first char rounded down to 16 bytes)
+    auto span = [&](int64_t itx, int64_t l0, int32_t c0, int64_t& o0x, int64_t& b0x, int& nchx) {
+        const int64_t K0x = itx * kLineBlk, K1x = min(K0x + kLineBlk, mc);
+        const int32_t rlx = int32_t(K1x - 1 - K0x) + c0;  // last char, relative to line l0's start
+        const int32_t dllx = div_small(rlx, L, invL);
+        o0x = li_off + l0 * P + c0;
+        const int64_t o1x = min(m, o0x + int64_t(dllx) * P + (rlx - dllx * L - c0) + 1 + S);
+        b0x = o0x - int64_t(reinterpret_cast<uintptr_t>(in + o0x) & 15);
+        nchx = int((o1x - b0x + 15) >> 4);
+    };
+#if B64_LINE_TMA
+    // the span is staged by ONE bulk async copy per step, issued as soon as the previous step's
+    // compaction has read the stage -- it lands while that step decodes
+    const uint32_t bar = smem_u32(&s_lbar[threadIdx.x >> 5]);
+    const uint32_t stg_s = smem_u32(stg);
+    uint32_t phase = 0;
+    bool pending = false;
+    int64_t o0n = 0, b0n = 0;
+    int nchn = 0;
+    auto stage_async = [&](int64_t b0x, int nchx) {
+        if (lane == 0) {
+            fence_proxy_async_smem();  // the stage's previous reads (generic proxy) before the copy
+            mbar_expect_tx(bar, uint32_t(16 * nchx));
+            bulk_g2s(stg_s, in + b0x, uint32_t(16 * nchx), bar);
+        }
+        pending = true;
+    };
+    if (it * kLineBlk < mc && it < __ldcg(&li->fail)) {
+        span(it, line0, col0, o0n, b0n, nchn);
+        stage_async(b0n, nchn);
+    }
+#endif
     for (; it * kLineBlk < mc; it += W) {
         if (it >= __ldcg(&li->fail)) break;  // a block before this one broke the layout
         const int64_t K0 = it * kLineBlk, K1 = min(K0 + kLineBlk, mc);
-        const int32_t rl = int32_t(K1 - 1 - K0) + col0;  // last char, relative to line0's start
-        const int32_t dll = div_small(rl, L, invL);
-        const int64_t o0 = li_off + line0 * P + col0;
-        const int64_t o1 = min(m, o0 + int64_t(dll) * P + (rl - dll * L - col0) + 1 + S);
-        const int64_t b0 = o0 - int64_t(reinterpret_cast<uintptr_t>(in + o0) & 15);
-        const int nch = int((o1 - b0 + 15) >> 4);
+#if B64_LINE_TMA
+        const int64_t o0 = o0n, b0 = b0n;
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        pending = false;
+#else
+        int64_t o0, b0;
+        int nch;
+        span(it, line0, col0, o0, b0, nch);
         for (int c = lane; c < nch; c += 32)
             *reinterpret_cast<uint4*>(stg + 16 * c) = ld128_nc(in + b0 + 16 * c);
+#endif
         __syncwarp();
         const int32_t sb = int32_t(o0 - b0) - col0;  // stage offset of line0's first char
         const int32_t krel = int32_t(K1 - K0);         // kept chars in this step
@@ -466,6 +515,20 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
             }
         }
         __syncwarp();
+#if B64_LINE_TMA
+        {  // the stage is free: the next step's span starts loading now
+            int64_t l1 = line0 + step_lines;
+            int32_t c1 = col0 + step_col;
+            if (c1 >= L) {
+                c1 -= L;
+                ++l1;
+            }
+            if ((it + W) * kLineBlk < mc) {
+                span(it + W, l1, c1, o0n, b0n, nchn);
+                stage_async(b0n, nchn);
+            }
+        }
+#endif
         // 2. decode the compacted chars, 32 per lane and unit (the fast kernels' per-lane code)
 #pragma unroll 1
         for (int u = 0; u < kLineBlk / 1024; ++u) {
@@ -530,6 +593,9 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
             ++line0;
         }
     }
+#if B64_LINE_TMA
+    if (pending) mbar_wait(bar, phase);  // no bulk copy may still be landing when the CTA exits
+#endif
     const unsigned hi = __reduce_min_sync(kFull, unsigned(uint64_t(bad) >> 32));
     const unsigned lo = __reduce_min_sync(kFull, unsigned(uint64_t(bad) >> 32) == hi ? unsigned(bad) : ~0u);
     if (lane == 0 && hi != 0x7FFFFFFFu)
