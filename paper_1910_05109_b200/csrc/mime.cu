@@ -217,6 +217,9 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
 // over the rest -- not the general path over everything.
 constexpr int kPatchThreads = 256;
 constexpr int kPatchWin = 8192;  // text bytes staged: the block's 4096 kept chars and at least one more
+// the patch CTA decodes a whole block with 4 quads per thread (B64_LINE_BLK is not free: 2048
+// measured slower on the line path anyway, 0.74 vs 0.64 ms per GiB)
+static_assert(kLineBlk == 16 * kPatchThreads && kLineBlk <= kPatchWin / 2, "reprobe block geometry");
 
 __global__ void __launch_bounds__(kPatchThreads)
 ws_line_reprobe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __restrict__ li,
