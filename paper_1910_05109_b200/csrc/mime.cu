@@ -506,6 +506,7 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
             const uint32_t sh = uint32_t(so & 3) * 8;
             uint32_t lo = sw[0];
             const int nw = (c_end - c_beg + 3) >> 2;
+#pragma unroll 4  // (a full line is 19 words at L = 76: 0.646 -> 0.624 ms per GiB of MIME vs no unroll)
             for (int k = 0; k < nw; ++k) {
                 const uint32_t hi = sw[k + 1];
                 cw[(d_beg >> 2) + k] = __funnelshift_r(lo, hi, sh);
