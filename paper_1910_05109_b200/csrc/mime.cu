@@ -780,7 +780,7 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
             // Per row: a 4-bit keep mask, the kept bytes packed by one PRMT (selector table in
             // shared memory), their count; the counts of 4 rows ride in one word (8 bits each,
             // <= 128) so ONE warp scan serves 4 rows.
-#pragma unroll 1
+#pragma unroll  // (all 4 groups: 48 instead of 59 registers, 1.81 -> 1.78 ms per GiB on the general path)
             for (int g = 0; g < kWsChunk / 1024; ++g) {
                 uint32_t w[8];
 #pragma unroll
