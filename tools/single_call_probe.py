@@ -16,6 +16,11 @@ import synth  # noqa: E402
 
 
 def main():
+    if os.environ.get("B64_LIB_PATH"):  # another build of the library (A/B)
+        path = os.environ["B64_LIB_PATH"]
+        probe = ctypes.CDLL(path)
+        b64._lib.LIB_PATH = path
+        b64._lib.SIGNATURES = [sg for sg in b64._lib.SIGNATURES if hasattr(probe, sg[0])]
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 67108864
     reps = 30
     L = b64._lib.lib()
