@@ -127,7 +127,8 @@ __device__ __forceinline__ int64_t line_orig(int64_t e, int64_t L, int64_t P) { 
 // kLineProbe bytes), ms = the first non-whitespace byte at or after start (searched in
 // kLineProbe bytes); p = the first whitespace byte after ms gives the line length.
 __device__ void probe_layout(const uint8_t* __restrict__ in, int64_t start, int64_t m, const uint8_t* lut,
-                             int lane, WsLine& w) {
+                             int lane, WsLine& w, bool& early_fail) {
+    early_fail = false;
     int64_t me = -1;
     for (int64_t j0 = m; j0 > start && m - j0 < kLineProbe && me < 0; j0 -= 32) {
         const int64_t i = j0 - 1 - lane;
@@ -180,6 +181,17 @@ __device__ void probe_layout(const uint8_t* __restrict__ in, int64_t start, int6
                 w.mode = 1; w.L = int32_t(L); w.s = s; w.v0 = int32_t(v0); w.nfull = nfull; w.r = r;
                 w.mc = nfull * L + r - v0; w.off = ms - v0;
                 w.sep = int32_t(in[p]) | int32_t(s > 1 ? in[p + 1] : 0) << 8;
+                // the separators of the first block's first 32 lines, one per lane: a layout that
+                // breaks there is known broken before the line kernel runs (w.fail = 0: its grid
+                // exits at once and the reprobe patches block 0) -- a failed attempt costs three
+                // small launches instead of one wave of line-kernel blocks
+                const int64_t j = lane;
+                bool broke = false;
+                if (j < nfull && (j + 1) * L - v0 <= kLineBlk) {
+                    const int64_t sp = w.off + j * P + L;
+                    broke = in[sp] != in[p] || (s > 1 && in[sp + 1] != in[p + 1]);
+                }
+                early_fail = __any_sync(kFull, broke);
             }
         }
     }
@@ -196,9 +208,10 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
     griddep_wait();
     __syncwarp();
     WsLine w;
-    probe_layout(in, 0, m, reinterpret_cast<const uint8_t*>(s_lut), lane, w);
+    bool early_fail;
+    probe_layout(in, 0, m, reinterpret_cast<const uint8_t*>(s_lut), lane, w, early_fail);
     if (lane) return;
-    w.cell = kErrNone; w.k0 = 0; w.fail = LLONG_MAX; w.errk = kErrNone; w.errt = -1;
+    w.cell = kErrNone; w.k0 = 0; w.fail = early_fail ? 0 : LLONG_MAX; w.errk = kErrNone; w.errt = -1;
     mc_general[0] = 0;  // the general path's decode does nothing unless its scan runs
     mc_general[1] = 0;
     *li = w;
@@ -356,8 +369,9 @@ ws_line_reprobe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsL
     // ---- the next segment: probe the rest (warp 0) or hand it to the general path
     if (wid) return;
     WsLine w;
+    bool early_fail = false;
     if (!general) {
-        probe_layout(in, p1, m, lut, lane, w);
+        probe_layout(in, p1, m, lut, lane, w, early_fail);
         if (w.mode == 0) w.off = p1;
     }
     if (lane) return;
@@ -367,7 +381,7 @@ ws_line_reprobe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsL
     } else {
         w.k0 = k0 + kLineBlk;
     }
-    w.cell = kErrNone; w.fail = LLONG_MAX; w.errk = s_errk; w.errt = s_errt;
+    w.cell = kErrNone; w.fail = early_fail ? 0 : LLONG_MAX; w.errk = s_errk; w.errt = s_errt;
     *li = w;
 }
 
