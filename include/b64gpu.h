@@ -20,16 +20,17 @@
  *    are written to device memory (err_off / status).
  *  - Input bytes are only read and output bytes only written inside the
  *    ranges stated per call, with one exception: the generic (unaligned /
- *    batched) kernels may read whole naturally aligned 16-byte blocks that
- *    contain input bytes -- at most 15 bytes before the first and after the
- *    last input byte, never a block that holds no input byte.  A block that
- *    holds an input byte lies in the same 256-byte-aligned region as that
- *    byte, and cudaMalloc (and the torch caching allocator) hands out whole
- *    256-byte-aligned regions, so such reads stay inside the allocation; a
- *    caller passing a sub-allocation must keep the 16-byte blocks that
- *    contain its bytes readable (compute-sanitizer memcheck log:
- *    profiles/sanitizer_r2.txt).  The values read there never affect a
- *    result.
+ *    batched) and whitespace kernels may read whole naturally aligned 16-byte
+ *    blocks that contain input bytes, and the unaligned fast decode whole
+ *    aligned 32-byte blocks -- at most 15 (31) bytes before the first and
+ *    after the last input byte, never a block that holds no input byte.  A
+ *    block that holds an input byte lies in the same 256-byte-aligned region
+ *    as that byte, and cudaMalloc (and the torch caching allocator) hands out
+ *    whole 256-byte-aligned regions, so such reads stay inside the allocation;
+ *    a caller passing a sub-allocation must keep the 32-byte blocks that
+ *    contain its bytes readable (checked by hardware: tests/test_guard_pages.py
+ *    puts every buffer of every entry point against an unmapped page).  The
+ *    values read there never affect a result.
  *  - Inputs and outputs must not overlap.
  */
 #ifndef B64GPU_H

@@ -3,7 +3,10 @@ small sizes -- fast and generic kernels, the single-launch cluster kernels, the 
 last-CTA finalize, the stream joins, the whitespace paths, the batch kernels and offsets, the
 emulated peer combine -- each result checked against the oracle.
 
-Run under the four tools (tools/sanitize.sh, log summary in profiles/sanitizer_r2.txt):
+Meant for the four compute-sanitizer tools (tools/sanitize.sh).  compute-sanitizer was closed on
+this project's GPU pool (runs under it left GPUs needing a reset), so the bounds check is done
+by the hardware instead (tests/test_guard_pages.py: every buffer against an unmapped page);
+this file still runs in the plain `-m gpu` pass.  With the tool:
 
     PYTORCH_NO_CUDA_MEMORY_CACHING=1 compute-sanitizer --tool memcheck \\
         python -m pytest tests/test_sanitize.py -m sanitize -q
