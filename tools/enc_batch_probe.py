@@ -1,9 +1,9 @@
 #!/usr/bin/env python3
-"""configs[3] batch encode timing (10^6 log-uniform strings, 5.9 GB), for A/B of the
-enc_generic_kernel variants (B64_ENC_TMA=0/1 in the environment): median of CUDA-event times
-after an L2 flush, plus a checksum of the output so the variants can be compared.
+"""configs[3] batch encode timing (10^6 log-uniform strings, 5.9 GB), for A/B of
+enc_generic_kernel variants (another build via B64_LIB_PATH): median of CUDA-event times after
+an L2 flush, plus a checksum of the output so the variants can be compared.
 
-    B64_ENC_TMA=1 python tools/enc_batch_probe.py [reps]
+    [B64_LIB_PATH=variant.so] python tools/enc_batch_probe.py [reps]
 """
 import os
 import statistics
@@ -45,7 +45,7 @@ def main():
     ck = int((w * torch.arange(1, w.numel() + 1, device="cuda", dtype=torch.int64)).sum().item())
     ms = statistics.median(ts)
     alg = off[-1] + enc.numel()
-    print({"lib": os.path.basename(b64._lib.LIB_PATH), "tma": os.environ.get("B64_ENC_TMA", "default"), "ms": round(ms, 4), "min_ms": round(min(ts), 4),
+    print({"lib": os.path.basename(b64._lib.LIB_PATH), "ms": round(ms, 4), "min_ms": round(min(ts), 4),
            "alg_gbs": round(alg / ms / 1e6, 1), "checksum": ck})
 
 
