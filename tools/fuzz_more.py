@@ -46,7 +46,7 @@ def main():
         done += 1
         if time.time() - t0 > secs:
             break
-    print({"examples": done, "seconds": round(time.time() - t0, 1)})
+    print({"examples": done, "seconds": round(time.time() - t0, 1), "kernel_launches": b64.launch_count()})
 
 
 if __name__ == "__main__":
