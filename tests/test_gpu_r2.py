@@ -776,3 +776,31 @@ def test_decode_ws_general_path_errors_across_tiles(b64):
     ref, rerr, _ = oracle.decode_ws(t3)
     out, err = b64.decode_ws(torch.from_numpy(t3).to(DEV))
     assert err == rerr == -1 and np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_stream_overlap_errors_at_piece_boundaries(b64):
+    """Overlap mode: a bad char at a piece's first char (the join quad, decoded after the wait
+    by the EARLY kernel's last thread), at its last char (held back for the next piece) or in
+    the middle of a later piece (the bulk's error path, which waits before its atomicMin): the
+    reported first error is the oracle's every time, in both modes."""
+    x = synth.data(4_500_000, seed=91)
+    text = oracle.encode(x)
+    piece = (1 << 20) + 1
+    cuts = list(range(0, text.size, piece))
+    for where in ("first", "last", "mid"):
+        for k in (1, 3):
+            t = text.copy()
+            if where == "first":
+                p = cuts[k]
+            elif where == "last":
+                p = cuts[k + 1] - 1
+            else:
+                p = cuts[k] + piece // 2
+            t[p] = ord("?")
+            dt = torch.from_numpy(t).to(DEV)
+            pieces = [min(piece, t.size - c) for c in cuts]
+            ref, rerr, rst = oracle.decode(t)
+            assert rerr == p
+            for overlap in (False, True):
+                _, info = _stream_into(b64, dt, b64.standard(), pieces, overlap=overlap)
+                assert info[:2] == [rerr, rst], (where, k, overlap, info, rerr)
