@@ -28,7 +28,7 @@ struct DevInfo {
     int sms = 0;
     int occ_group[4] = {0, 0, 0, 0};  // min over the enc / dec / codec group kernels
     int occ_enc_fast[4] = {0, 0, 0, 0}, occ_dec_fast[4] = {0, 0, 0, 0}, occ_enc_gen = 0, occ_dec_gen = 0;
-    int occ_batch_bulk = 0, occ_fastu[3][8] = {}, occ_enc_fastu = 0;
+    int occ_batch_bulk = 0, occ_fastu[3][8] = {}, occ_enc_fastu = 0, occ_ws_count = 0, occ_ws_compact = 0;
 };
 constexpr int kMaxDev = 64;
 DevInfo g_dev[kMaxDev];
@@ -90,6 +90,16 @@ const DevInfo* dev_info() {
         cudaSuccess)
         return nullptr;
     info.occ_enc_fastu = info.occ_enc_fastu < 1 ? 1 : info.occ_enc_fastu;
+    {
+        int a = 0, b = 0, c = 0, d2 = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, ws_count_kernel<true>, kThreads, 0) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ws_count_kernel<false>, kThreads, 0) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, ws_compact_kernel<true>, kThreads, 0) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d2, ws_compact_kernel<false>, kThreads, 0) != cudaSuccess)
+            return nullptr;
+        info.occ_ws_count = std::max(1, std::min(a, b));
+        info.occ_ws_compact = std::max(1, std::min(c, d2));
+    }
     if (cudaFuncSetAttribute(dec_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
         cudaFuncSetAttribute(ws_small_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         return nullptr;
@@ -504,7 +514,13 @@ int64_t up256(int64_t v) { return (v + 255) / 256 * 256; }
 WsLayout ws_layout(int64_t m) {
     WsLayout L;
     L.nch = (m + kWsChunk - 1) / kWsChunk;
-    L.ncta = L.nch < kWsMaxCtas ? (L.nch > 0 ? L.nch : 1) : kWsMaxCtas;
+    // groups of the general path (count / compaction, K chunks each, taken by resident CTAs from
+    // a counter): 4096 once that still leaves >= 16 chunks per group, else 1024 -- measured on
+    // random layouts (tools/ws_probe.py random) with one CTA per group: 1 GiB of data 1.74 ms with
+    // 1024, 1.66 with 2048, 1.62 with 4096, 1.63 / 1.68 with 8192 / 16384; 256 MiB 0.511 / 0.502
+    // / 0.502 with 1024 / 2048 / 4096 (0.54 with 1384); 64 MiB 0.216 with 1024, 0.241 with 4096
+    const int64_t want = L.nch >= int64_t(16) * kWsMaxCtas ? kWsMaxCtas : 1024;
+    L.ncta = L.nch < want ? (L.nch > 0 ? L.nch : 1) : want;
     L.K = (L.nch + L.ncta - 1) / L.ncta;
     if (L.K < 1) L.K = 1;
     L.ncta = (L.nch + L.K - 1) / L.K;
@@ -595,10 +611,15 @@ int b64_decode_ws(const uint8_t* d_in, int64_t m, uint8_t* d_out, const b64_alph
         launch(ws_line_kernel, int64_t(di->sms) * B64_LINE_MINB, kLineThreads, s, d_in, m, wt, li, d_out);
         launch(ws_line_reprobe_kernel, 1, kPatchThreads, s, d_in, m, wt, li, d_out, seg == nseg - 1 ? 1 : 0);
     }
-    launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, counts, tot, lic);
+    // the count / compaction kernels: resident grids taking the L.ncta groups from counters
+    unsigned long long* gctr = reinterpret_cast<unsigned long long*>(mc + 2);
+    launch(sw ? ws_count_kernel<true> : ws_count_kernel<false>,
+           std::min<int64_t>(L.ncta, int64_t(di->sms) * di->occ_ws_count), kThreads, s, d_in, m, wt, L.K, counts, tot,
+           lic, L.ncta, gctr);
     launch(ws_scan_kernel, 1, 1024, s, static_cast<const int64_t*>(tot), int(L.ncta), cbase, mc, lic);
-    launch(sw ? ws_compact_kernel<true> : ws_compact_kernel<false>, L.ncta, kThreads, s, d_in, m, wt, L.K, static_cast<const int32_t*>(counts),
-           static_cast<const int64_t*>(cbase), comp, lic);
+    launch(sw ? ws_compact_kernel<true> : ws_compact_kernel<false>,
+           std::min<int64_t>(L.ncta, int64_t(di->sms) * di->occ_ws_compact), kThreads, s, d_in, m, wt, L.K,
+           static_cast<const int32_t*>(counts), static_cast<const int64_t*>(cbase), comp, lic, L.ncta, gctr + 1);
     {  // strict decode of the compacted text; its length m' is read on the device
         const int64_t blocks = balanced_blocks(m / 1024, int64_t(di->sms) * cap_bps(di->occ_dec_fast[1]));
         launch(dec_fast_kernel<1>, blocks, kThreads, s, static_cast<const uint8_t*>(comp), m, d_out, dec_tab(a),

@@ -43,7 +43,10 @@
 namespace b64 {
 
 constexpr int kWsChunk = 4096;     // bytes per chunk (one warp at a time)
-constexpr int kWsMaxCtas = 1024;   // the scan kernel scans the CTA totals in one CTA
+#ifndef B64_WS_MAX_CTAS
+#define B64_WS_MAX_CTAS 4096
+#endif
+constexpr int kWsMaxCtas = B64_WS_MAX_CTAS;  // the scan kernel scans the CTA totals in one CTA (4 per thread)
 constexpr uint8_t kSkip = 0x40;    // class value of a skipped byte in the ws table
 
 struct WsTab { uint32_t w[64]; };  // 256 entries: 6-bit value, kInvalid, or kSkip
@@ -214,6 +217,8 @@ ws_line_probe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLin
     w.cell = kErrNone; w.k0 = 0; w.fail = early_fail ? 0 : LLONG_MAX; w.errk = kErrNone; w.errt = -1;
     mc_general[0] = 0;  // the general path's decode does nothing unless its scan runs
     mc_general[1] = 0;
+    mc_general[2] = 0;  // the count / compaction kernels' group counters
+    mc_general[3] = 0;
     *li = w;
 }
 
@@ -636,12 +641,13 @@ __device__ __forceinline__ WsSuffix ws_suffix(const uint8_t* in, const WsLine* l
 template <bool SW>
 __global__ void __launch_bounds__(kThreads)
 ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K, int32_t* __restrict__ counts,
-                int64_t* __restrict__ cta_tot, const WsLine* __restrict__ li) {
+                int64_t* __restrict__ cta_tot, const WsLine* __restrict__ li, int64_t ngroups,
+                unsigned long long* __restrict__ ctr) {
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ unsigned long long s_tot;
+    __shared__ int64_t s_vb;
     griddep_launch_dependents();
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
-    if (threadIdx.x == 0) s_tot = 0;
     griddep_wait();
     __syncthreads();
     if (__ldcg(&li->mode) != 0) return;  // line mode: ws_line_kernel did it all
@@ -651,8 +657,18 @@ ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K,
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
-    const int64_t c_lo = int64_t(blockIdx.x) * K, c_hi = min(c_lo + K, nch);
     const bool vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    // groups of K chunks taken from a counter (the probe kernel zeroes it): a resident grid, so a
+    // call that ends on the line path launches few CTAs, and groups are balanced dynamically
+    for (;;) {
+    if (threadIdx.x == 0) {
+        s_vb = int64_t(atomicAdd(ctr, 1ull));
+        s_tot = 0;
+    }
+    __syncthreads();
+    const int64_t vb = s_vb;
+    if (vb >= ngroups) break;
+    const int64_t c_lo = vb * K, c_hi = min(c_lo + K, nch);
     uint32_t mine = 0;
     for (int64_t c = c_lo + wib; c < c_hi; c += kThreads / 32) {
         const int64_t b0 = c * kWsChunk;
@@ -688,21 +704,29 @@ ws_count_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K,
     }
     if (lane == 0) atomicAdd(&s_tot, (unsigned long long)mine);
     __syncthreads();
-    if (threadIdx.x == 0) cta_tot[blockIdx.x] = int64_t(s_tot);
+    if (threadIdx.x == 0) cta_tot[vb] = int64_t(s_tot);
+    __syncthreads();  // s_vb / s_tot are reused by the next group
+    }
 }
 
 // One CTA: exclusive scan of n (<= 1024) CTA totals -> cta_base; *m_out = sum.
 __global__ void __launch_bounds__(1024) ws_scan_kernel(const int64_t* __restrict__ cta_tot, int n,
                                                        int64_t* __restrict__ cta_base, int64_t* __restrict__ m_out,
                                                        const WsLine* __restrict__ li) {
+    constexpr int E = (kWsMaxCtas + 1023) / 1024;  // totals per thread (consecutive)
     __shared__ int64_t s_warp[32];
     griddep_launch_dependents();
     griddep_wait();
     if (__ldcg(&li->mode) != 0) return;
     const int64_t k0 = __ldcg(&li->k0);  // kept chars the line segments decoded before the suffix
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int64_t v = t < n ? cta_tot[t] : 0;
-    int64_t x = v;  // inclusive warp scan
+    int64_t e[E], v = 0;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        e[i] = E * t + i < n ? cta_tot[E * t + i] : 0;
+        v += e[i];
+    }
+    int64_t x = v;  // inclusive warp scan of the per-thread sums
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         const int64_t y = __shfl_up_sync(kFull, x, d);
@@ -720,8 +744,12 @@ __global__ void __launch_bounds__(1024) ws_scan_kernel(const int64_t* __restrict
         s_warp[lane] = s;  // inclusive over warps
     }
     __syncthreads();
-    const int64_t before = (w ? s_warp[w - 1] : 0) + x - v;
-    if (t < n) cta_base[t] = k0 + before;
+    int64_t before = (w ? s_warp[w - 1] : 0) + x - v;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+        if (E * t + i < n) cta_base[E * t + i] = k0 + before;
+        before += e[i];
+    }
     if (t == 0) {
         m_out[0] = k0 + s_warp[31];  // the total kept count
         m_out[1] = k0;               // where the suffix starts in the compacted text (dec_fast_kernel)
@@ -731,7 +759,8 @@ __global__ void __launch_bounds__(1024) ws_scan_kernel(const int64_t* __restrict
 template <bool SW>
 __global__ void __launch_bounds__(kThreads)
 ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t K, const int32_t* __restrict__ counts,
-                  const int64_t* __restrict__ cta_base, uint8_t* __restrict__ dst, const WsLine* __restrict__ li) {
+                  const int64_t* __restrict__ cta_base, uint8_t* __restrict__ dst, const WsLine* __restrict__ li,
+                  int64_t ngroups, unsigned long long* __restrict__ ctr) {
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(16) uint8_t s_buf[kThreads / 32][kWsChunk + 16];
     __shared__ int64_t s_pref[kThreads];   // per-thread partial sums of the CTA's chunk counts
@@ -753,9 +782,17 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
     const uint8_t* lut = reinterpret_cast<const uint8_t*>(s_lut);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t nch = (m + kWsChunk - 1) / kWsChunk;
-    const int64_t c_lo = int64_t(blockIdx.x) * K, c_hi = min(c_lo + K, nch);
+    uint8_t* buf = &s_buf[wib][0];
+    const bool vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    __shared__ int64_t s_vb;
+    for (;;) {  // groups of K chunks from a counter, as ws_count_kernel
+    if (threadIdx.x == 0) s_vb = int64_t(atomicAdd(ctr, 1ull));
+    __syncthreads();
+    const int64_t vb = s_vb;
+    if (vb >= ngroups) break;
+    const int64_t c_lo = vb * K, c_hi = min(c_lo + K, nch);
     const int64_t nloc = c_hi > c_lo ? c_hi - c_lo : 0;
-    // exclusive prefix of the CTA's chunk counts: thread t sums the chunks
+    // exclusive prefix of the group's chunk counts: thread t sums the chunks
     // [t*per, (t+1)*per); s_pref[t] becomes the exclusive prefix of those sums
     const int64_t per = (nloc + kThreads - 1) / kThreads;
     int64_t part = 0;
@@ -763,7 +800,7 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
     s_pref[threadIdx.x] = part;
     __syncthreads();
     if (threadIdx.x == 0) {
-        int64_t run = cta_base[blockIdx.x];
+        int64_t run = cta_base[vb];
         for (int t = 0; t < kThreads; ++t) {
             const int64_t v = s_pref[t];
             s_pref[t] = run;
@@ -771,8 +808,6 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
         }
     }
     __syncthreads();
-    uint8_t* buf = &s_buf[wib][0];
-    const bool vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
     for (int64_t j = wib; j < nloc; j += kThreads / 32) {
         // output offset of chunk c_lo + j: the prefix of its segment plus the
         // counts of the segment's chunks before it (fewer than `per`)
@@ -857,6 +892,8 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
         const int tail0 = h + 4 * nw;
         if (lane < n_kept - tail0) d[tail0 + lane] = buf[tail0 + lane];
         __syncwarp();
+    }
+    __syncthreads();  // s_vb / s_pref are reused by the next group
     }
 }
 
