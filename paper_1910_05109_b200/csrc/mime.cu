@@ -764,6 +764,7 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
     __shared__ __align__(256) uint32_t s_lut[64];
     __shared__ __align__(16) uint8_t s_buf[kThreads / 32][kWsChunk + 16];
     __shared__ int64_t s_pref[kThreads];   // per-thread partial sums of the CTA's chunk counts
+    __shared__ int64_t s_wtot[kThreads / 32];
     __shared__ uint32_t s_sel[16];         // PRMT selector packing the kept bytes of a 4-bit mask
     griddep_launch_dependents();
     if (threadIdx.x < 64) s_lut[threadIdx.x] = tab.w[threadIdx.x];
@@ -797,15 +798,18 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
     const int64_t per = (nloc + kThreads - 1) / kThreads;
     int64_t part = 0;
     for (int64_t j = threadIdx.x * per; j < min(nloc, int64_t(threadIdx.x + 1) * per); ++j) part += counts[c_lo + j];
-    s_pref[threadIdx.x] = part;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t run = cta_base[vb];
-        for (int t = 0; t < kThreads; ++t) {
-            const int64_t v = s_pref[t];
-            s_pref[t] = run;
-            run += v;
+    {  // block-wide exclusive scan of the parts (warp scans + the warps' totals)
+        int64_t x = part;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int64_t y = __shfl_up_sync(kFull, x, d);
+            if (lane >= d) x += y;
         }
+        if (lane == 31) s_wtot[wib] = x;
+        __syncthreads();
+        int64_t before = cta_base[vb];
+        for (int w2 = 0; w2 < wib; ++w2) before += s_wtot[w2];
+        s_pref[threadIdx.x] = before + x - part;
     }
     __syncthreads();
     for (int64_t j = wib; j < nloc; j += kThreads / 32) {
