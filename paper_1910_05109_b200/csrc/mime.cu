@@ -5,15 +5,17 @@
 // The bytes 0x09-0x0D and 0x20 that are not alphabet chars are removed and the
 // rest is decoded under the strict rules; errors are reported at their
 // position in the ORIGINAL text.  Stream compaction on the GPU, four kernels:
-//   1. ws_count_kernel    per 4 KiB chunk: number of kept chars; per CTA total
-//                         (CTA b owns the K consecutive chunks [bK, bK + K));
-//                         a warp loads its whole chunk at once (8 lane-linear
-//                         LDG.128 per lane) before the table look-ups;
-//   2. ws_scan_kernel     one CTA: exclusive scan of the <= 1024 CTA totals and
-//                         the compacted length m';
-//   3. ws_compact_kernel  each CTA scans its own K chunk counts in shared
-//                         memory; a warp loads its whole chunk (8 x LDG.128
-//                         per lane), compacts it through a per-warp shared
+//   1. ws_count_kernel    per 4 KiB chunk: number of kept chars; per group
+//                         total (group b = the K consecutive chunks [bK, bK +
+//                         K); 1024 groups, or 4096 from 256 MiB of text on,
+//                         taken from a counter by a resident grid); a warp
+//                         loads its whole chunk at once (8 lane-linear LDG.128
+//                         per lane) before the table look-ups;
+//   2. ws_scan_kernel     one CTA: exclusive scan of the <= 4096 group totals
+//                         and the compacted length m';
+//   3. ws_compact_kernel  groups from a counter again; each scans its own K
+//                         chunk counts (block scan); a warp compacts its chunk
+//                         (rows of lane-linear LDG.32) through a per-warp shared
 //                         buffer (16-bit keep mask per lane, one warp prefix
 //                         sum per 512 B) and writes it with 4-byte stores
 //                         (funnel-shifted from aligned shared words) into the
@@ -33,11 +35,12 @@
 // guesses the layout, ws_line_kernel decodes straight from the text in one
 // pass and verifies every byte; the general kernels above then return at once
 // (they run when the layout does not hold).  Measured (1 GiB of data as MIME
-// lines of 76 chars + CRLF): 0.70 ms (line kernel ~175 us per 256 MiB, issue-
-// bound); the general path 1.67 ms (per 256 MiB: count 72 us, compact 238
-// us, decode ~100 us; the compaction is issue-bound; alphabets without
-// whitespace chars use an arithmetic per-byte test, ws_bits, for the keep
-// masks).  The byte-at-a-time first version took 3.7 ms.
+// lines of 76 chars + CRLF): 0.62 ms (line kernel ~154 us per 256 MiB with the
+// bulk-copy staging, issue-bound); the general path 1.64 ms on a random layout
+// (per 256 MiB: count ~70 us, compact ~240 us, decode ~100 us; the compaction
+// is issue-bound; alphabets without whitespace chars use an arithmetic
+// per-byte test, ws_bits, for the keep masks).  The byte-at-a-time first
+// version took 3.7 ms.
 #include "b64_device.cuh"
 
 namespace b64 {
