@@ -380,6 +380,10 @@ ws_line_reprobe_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsL
     bool early_fail = false;
     if (!general) {
         probe_layout(in, p1, m, lut, lane, w, early_fail);
+        // a layout that breaks again within the first block after a break is not line-structured
+        // here (lines of varying length): the general path takes the rest now, not after two
+        // more segment attempts that would each fail at their first block
+        if (early_fail) w.mode = 0;
         if (w.mode == 0) w.off = p1;
     }
     if (lane) return;
