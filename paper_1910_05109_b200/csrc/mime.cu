@@ -45,6 +45,14 @@
 
 namespace b64 {
 
+#ifndef B64_WS_STORE_ALL
+#define B64_WS_STORE_ALL 1
+#endif
+#if B64_WS_STORE_ALL == 2
+#define B64_WS_SYNC() ((void)0)
+#else
+#define B64_WS_SYNC() __syncwarp()
+#endif
 constexpr int kWsChunk = 4096;     // bytes per chunk (one warp at a time)
 #ifndef B64_WS_MAX_CTAS
 #define B64_WS_MAX_CTAS 4096
@@ -867,11 +875,30 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
                 for (int r = 0; r < 8; ++r) {
                     const int pos = n_kept + int((ex[r >> 2] >> (8 * (r & 3))) & 0xffu);
                     const uint32_t cw = __byte_perm(w[r], 0u, s_sel[km[r]]);
+#if B64_WS_STORE_ALL
+                    // All 4 bytes stored, the highest byte position first, one warp-wide store
+                    // per position with a __syncwarp between: a lane's bytes past its kept count
+                    // land on the next lanes' slots (pos + cnt on) and are overwritten by their
+                    // stores of lower byte positions, which come later; past the row's last kept
+                    // byte they are overwritten by the next row's stores or lie past the chunk's
+                    // kept bytes (slack).  A lane with nothing kept (its pos is the next lane's)
+                    // writes to a scratch word past the slack.  Branch-free, against a chain of
+                    // count tests that ptxas compiles to branches.
+                    const int sp = km[r] ? pos : kWsChunk + 8;
+                    buf[sp + 3] = uint8_t(cw >> 24);
+                    B64_WS_SYNC();
+                    buf[sp + 2] = uint8_t(cw >> 16);
+                    B64_WS_SYNC();
+                    buf[sp + 1] = uint8_t(cw >> 8);
+                    B64_WS_SYNC();
+                    buf[sp] = uint8_t(cw);
+#else
                     const int cnt = __popc(km[r]);
                     if (cnt > 0) buf[pos] = uint8_t(cw);
                     if (cnt > 1) buf[pos + 1] = uint8_t(cw >> 8);
                     if (cnt > 2) buf[pos + 2] = uint8_t(cw >> 16);
                     if (cnt > 3) buf[pos + 3] = uint8_t(cw >> 24);
+#endif
                     n_kept += int((tot[r >> 2] >> (8 * (r & 3))) & 0xffu);
                 }
             }
