@@ -921,12 +921,12 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
         const int nw = (n_kept - h) >> 2;
         // word t of the output = buffer bytes [h + 4t, h + 4t + 4): two aligned shared words + a
         // funnel shift (h < 4 is uniform; the second word may lie past the kept bytes -- unused)
-        const uint32_t* bw = reinterpret_cast<const uint32_t*>(buf);
+        // (pointers stepped by the warp's stride: the unrolled copies address with immediate
+        // offsets instead of a 64-bit add per store)
+        const uint32_t* bw = reinterpret_cast<const uint32_t*>(buf) + lane;
+        uint32_t* dw = reinterpret_cast<uint32_t*>(d + h) + lane;
         const uint32_t fsh = uint32_t(h) * 8;
-        for (int t = lane; t < nw; t += 32) {
-            const uint32_t v = __funnelshift_r(bw[t], bw[t + 1], fsh);
-            *reinterpret_cast<uint32_t*>(d + h + 4 * t) = v;
-        }
+        for (int t = lane; t < nw; t += 32, bw += 32, dw += 32) *dw = __funnelshift_r(bw[0], bw[1], fsh);
         const int tail0 = h + 4 * nw;
         if (lane < n_kept - tail0) d[tail0 + lane] = buf[tail0 + lane];
         __syncwarp();
