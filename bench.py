@@ -1128,8 +1128,29 @@ def next_rows(b64, synth, torch, dev, timeit):
     ws = torch.empty(int(L.b64_decode_ws_workspace_bytes(mw)), dtype=torch.uint8, device=dev)
     ms = timeit(wsd, reps=5)
     assert int(info[0].item()) == -1 and int(info[2].item()) == n
-    res["whitespace_irregular"] = dict(rate(ms, mw, n), note="MIME text + one stray blank: line pass, then the "
-                                                             "general path (~4.75 B per char moved)")
+    res["whitespace_irregular"] = dict(rate(ms, mw, n), note="MIME text + one stray blank: the line pass keeps the "
+                                                             "verified blocks, patches the broken one and probes the "
+                                                             "rest again (line segments)")
+    # no uniform layout at all: lines of 60, 72, 84 and 76 chars in turn, each + LF -- the general
+    # path (count / scan / compact / decode, ~4.75 B per char moved) for the whole text
+    del tw, ws
+    rows_ = m // 292
+    body = t[: rows_ * 292].view(rows_, 292)
+    v2 = torch.empty(rows_, 296, dtype=torch.uint8, device=dev)
+    c_ = d_ = 0
+    for ln in (60, 72, 84, 76):
+        v2[:, d_: d_ + ln] = body[:, c_: c_ + ln]
+        v2[:, d_ + ln] = 10
+        c_ += ln
+        d_ += ln + 1
+    tw = torch.cat([v2.view(-1), t[rows_ * 292:]])
+    del body, v2
+    mw = tw.numel()
+    ws = torch.empty(int(L.b64_decode_ws_workspace_bytes(mw)), dtype=torch.uint8, device=dev)
+    ms = timeit(wsd, reps=5)
+    assert int(info[0].item()) == -1 and int(info[2].item()) == n
+    res["whitespace_random_lines"] = dict(rate(ms, mw, n), note="lines of 60/72/84/76 chars + LF in turn (no uniform "
+                                                                "layout): the general path over the whole text")
     del tw, ws
     # streaming: the strict text in 64 MiB pieces (plus the carry joins and the end call)
     carry = torch.zeros(8, dtype=torch.uint8, device=dev)
