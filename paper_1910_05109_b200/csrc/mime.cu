@@ -85,6 +85,13 @@ __device__ __forceinline__ uint32_t ws_bits(uint32_t x) {
     return (~nz | (ge9 & ~ge14)) & ~x & 0x80808080u;
 }
 
+// PTX prmt with the selector used as given (__byte_perm masks it with 0x7777 first: one LOP3)
+__device__ __forceinline__ uint32_t prmt_raw(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
 // keep-mask of the 4 bytes of x (bit b = byte b kept), either way
 template <bool SW>
 __device__ __forceinline__ uint32_t keep4(const uint8_t* lut, uint32_t x) {
@@ -873,8 +880,10 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
                 }
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
-                    const int pos = n_kept + int((ex[r >> 2] >> (8 * (r & 3))) & 0xffu);
-                    const uint32_t cw = __byte_perm(w[r], 0u, s_sel[km[r]]);
+                    // (byte r & 3 of the packed prefix by one PRMT; the selector table's nibbles
+                    // are 0-4, so the raw prmt needs no masking of its selector)
+                    const int pos = n_kept + int(__byte_perm(ex[r >> 2], 0u, 0x4440u | (r & 3)));
+                    const uint32_t cw = prmt_raw(w[r], 0u, s_sel[km[r]]);
 #if B64_WS_STORE_ALL
                     // All 4 bytes stored, the highest byte position first, one warp-wide store
                     // per position with a __syncwarp between: a lane's bytes past its kept count
@@ -899,7 +908,7 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
                     if (cnt > 2) buf[pos + 2] = uint8_t(cw >> 16);
                     if (cnt > 3) buf[pos + 3] = uint8_t(cw >> 24);
 #endif
-                    n_kept += int((tot[r >> 2] >> (8 * (r & 3))) & 0xffu);
+                    n_kept += int(__byte_perm(tot[r >> 2], 0u, 0x4440u | (r & 3)));
                 }
             }
         } else {
