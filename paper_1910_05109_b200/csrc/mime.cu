@@ -96,8 +96,16 @@ __device__ __forceinline__ uint32_t prmt_raw(uint32_t a, uint32_t b, uint32_t se
 template <bool SW>
 __device__ __forceinline__ uint32_t keep4(const uint8_t* lut, uint32_t x) {
     if (SW) {
-        const uint32_t k = ~ws_bits(x) & 0x80808080u;
-        return ((k >> 7) | (k >> 14) | (k >> 21) | (k >> 28)) & 0xFu;
+        // the kept flags (bit 7 of each byte: ws_bits inverted, folded by ptxas into its LOP3s),
+        // gathered by one multiply: bits 7 / 15 / 23 / 31 land on 28 / 29 / 30 / 31 and every
+        // cross product on a distinct lower bit (7, 14, 15, 21, 22, 23: no carries into the top)
+        const uint32_t y = x & 0x7F7F7F7Fu;
+        const uint32_t z = y ^ 0x20202020u;
+        const uint32_t nz = (z + 0x7F7F7F7Fu) | z;   // bit 7: byte != 0x20
+        const uint32_t ge9 = y + 0x77777777u;        // bit 7: byte >= 0x09
+        const uint32_t ge14 = y + 0x72727272u;       // bit 7: byte >= 0x0E
+        const uint32_t k = ((nz & ~(ge9 & ~ge14)) | x) & 0x80808080u;
+        return (k * 0x00204081u) >> 28;
     }
     return ws_keep4(lut, x);
 }
