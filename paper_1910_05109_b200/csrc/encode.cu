@@ -14,6 +14,8 @@
 //   byte ranges, one per warp; a warp encodes every 24-byte unit (8 triples ->
 //   32 chars) whose first byte lies in its range, so long strings spread over
 //   many warps and short strings pack many per warp.
+#include <cstddef>
+
 #include "b64_device.cuh"
 
 namespace b64 {
@@ -297,6 +299,12 @@ __device__ __forceinline__ void fix24(const Raw24& r, uint32_t (&w)[6]) {
     for (int i = 0; i < 6; ++i) w[i] = __funnelshift_r(ws ? v[i + 1] : v[i], ws ? v[i + 2] : v[i + 1], sh);
 }
 
+__device__ __forceinline__ int64_t lds_s64(uint32_t a) {
+    int64_t v;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+
 __device__ __forceinline__ int64_t warp_exclusive_scan(int64_t v, int lane, int64_t* total) {
     int64_t x = v;
 #pragma unroll
@@ -390,23 +398,29 @@ enc_generic_kernel(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, Of
         __syncwarp();
         // flattened units of the batch's long strings, one unit ahead in flight; each lane's
         // owner string only moves forward (j grows), so it is tracked, not searched
+        // (the owner is tracked as the shared address of its pre[] entry: one register, and
+        // no per-unit recomputation of the list's base under the 48-register cap)
         int64_t j = lane;
-        int o = 0;
+        uint32_t oa = smem_u32(&wl.pre[0]);
+        constexpr uint32_t kSrc = offsetof(EncWarpList, src) - offsetof(EncWarpList, pre);
+        constexpr uint32_t kDst = offsetof(EncWarpList, dst) - offsetof(EncWarpList, pre);
         Raw24 nr;
         int64_t ndst = 0;
         if (j < nu_all) {
-            while (wl.pre[o + 1] <= j) ++o;
-            ld24_raw(in + wl.src[o] + 24 * (j - wl.pre[o]), nr);
-            ndst = wl.dst[o] + 32 * (j - wl.pre[o]);
+            while (lds_s64(oa + 8) <= j) oa += 8;
+            const int64_t po = lds_s64(oa);
+            ld24_raw(in + lds_s64(oa + kSrc) + 24 * (j - po), nr);
+            ndst = lds_s64(oa + kDst) + 32 * (j - po);
         }
         for (; j < nu_all; j += 32) {
             const Raw24 cr = nr;
             const int64_t cdst = ndst;
             const int64_t jn = j + 32;
             if (jn < nu_all) {
-                while (wl.pre[o + 1] <= jn) ++o;
-                ld24_raw(in + wl.src[o] + 24 * (jn - wl.pre[o]), nr);
-                ndst = wl.dst[o] + 32 * (jn - wl.pre[o]);
+                while (lds_s64(oa + 8) <= jn) oa += 8;
+                const int64_t po = lds_s64(oa);
+                ld24_raw(in + lds_s64(oa + kSrc) + 24 * (jn - po), nr);
+                ndst = lds_s64(oa + kDst) + 32 * (jn - po);
             }
             uint32_t wv[6], ov[8];
             fix24(cr, wv);
