@@ -493,7 +493,11 @@ def test_decode_ws_general_path_large(b64, alpha_kind):
     for n in (700_001, 3_000_000):
         x = synth.data(n, seed=n)
         text = oracle.encode(x, chars)
-        for v, t in enumerate((_wrap(text, 60, n, ws), _wrap(text, 7, n + 1, ws), _wrap(text[:-1], 30, n + 2, ws))):
+        # (the 4th layout: whitespace runs of up to 200 bytes -- words, lanes and whole 128-byte
+        # rows with nothing kept, which the compaction's branch-free stores send to a scratch word)
+        long_ws = ws[:2] * 100
+        for v, t in enumerate((_wrap(text, 60, n, ws), _wrap(text, 7, n + 1, ws), _wrap(text[:-1], 30, n + 2, ws),
+                               _wrap(text, 40, n + 3, long_ws))):
             if v == 0:
                 t = t.copy()
                 t[t.size // 3] = ord("*")
@@ -518,6 +522,14 @@ def _insert(t, pos, b):
     return np.concatenate([t[:pos], np.frombuffer(b, np.uint8), t[pos:]])
 
 
+def _varying(m, lens=(60, 72, 84, 76)):
+    i, k = 0, 0
+    while i < m:
+        yield i, lens[k % len(lens)]
+        i += lens[k % len(lens)]
+        k += 1
+
+
 def test_decode_ws_line_segments(b64):
     """Line-structured text whose layout breaks (a stray blank, a missing or doubled line break,
     a change of line length): the line pass keeps the verified blocks, probes the rest again
@@ -540,6 +552,10 @@ def test_decode_ws_line_segments(b64):
         "double_crlf": _insert(mime, 78 * 12000, b"\r\n"),
         "relayout": np.concatenate([_mime_lines(t[: 76 * 10000], 76), _mime_lines(t[76 * 10000:], 64, b"\n")]),
         "block_boundary": _insert(mime, (4096 // 76) * 78 * 3, b" "),
+        # no uniform layout (lines of 60 / 72 / 84 / 76 chars in turn): the first segment and
+        # the reprobed one break in their first block, and the general path takes the rest
+        "varying_lines": np.concatenate([np.concatenate([t[i: i + L], np.frombuffer(b"\n", np.uint8)])
+                                         for i, L in _varying(t.size)]),
     }
     for name, tv in list(cases.items()):
         cases[name + "+err_before"] = tv.copy()
