@@ -568,6 +568,10 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
             }
         }
         __syncwarp();
+        if (krel < kLineBlk) {  // the segment's last step: 32 valid chars after its kept ones, so
+            reinterpret_cast<uint8_t*>(cw)[krel + lane] = 'A';  // the unit loads past them vote
+            __syncwarp();                                        // nothing (no per-quad mask)
+        }
 #if B64_LINE_TMA
         {  // the stage is free: the next step's span starts loading now
             int64_t l1 = line0 + step_lines;
@@ -593,12 +597,10 @@ ws_line_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, WsLine* __r
             const uint4 a1 = *reinterpret_cast<const uint4*>(cw + (ru >> 2) + 4);
             const uint32_t x[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
             uint32_t v[8], err = 0;
+            // (every quad votes: past the step's kept chars the buffer holds 'A's; the final
+            // quad's '=' is sorted out below)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                uint32_t eq = 0;
-                v[q] = dec_quad_s(x[q], lb, eq);
-                if (q < nq) err |= eq;  // (the final quad's '=' is sorted out below)
-            }
+            for (int q = 0; q < 8; ++q) v[q] = dec_quad_s(x[q], lb, err);
             irregular |= (err & kSkip) != 0;
             const bool tail = nq < 8 || q0 + 7 >= qfin;  // a partial unit or the final quad's
             if (err & kInvalid) {
