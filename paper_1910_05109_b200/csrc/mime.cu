@@ -932,21 +932,33 @@ ws_compact_kernel(const uint8_t* __restrict__ in, int64_t m, WsTab tab, int64_t 
             }
         }
         __syncwarp();
-        // copy the compacted chunk to dst + off: byte head up to 4-alignment, words, byte tail
+        // copy the compacted chunk to dst + off: byte head up to 8-alignment, 8-byte units, byte
+        // tail.  Unit t of the output = buffer bytes [h + 8t, h + 8t + 8): three aligned shared
+        // words a = h / 4 + 2t .. a + 2 (one LDS.64 on the even-aligned pair, one LDS.32) and two
+        // funnel shifts by h % 4 (h < 8 is uniform; the last word may lie past the kept bytes --
+        // unused).  Pointers stepped by the warp's stride: immediate-offset addressing.
         uint8_t* d = dst + off;
-        const int head = int((4 - (reinterpret_cast<uintptr_t>(d) & 3)) & 3);
+        const int head = int((8 - (reinterpret_cast<uintptr_t>(d) & 7)) & 7);
         const int h = head < n_kept ? head : n_kept;
         if (lane < h) d[lane] = buf[lane];
-        const int nw = (n_kept - h) >> 2;
-        // word t of the output = buffer bytes [h + 4t, h + 4t + 4): two aligned shared words + a
-        // funnel shift (h < 4 is uniform; the second word may lie past the kept bytes -- unused)
-        // (pointers stepped by the warp's stride: the unrolled copies address with immediate
-        // offsets instead of a 64-bit add per store)
-        const uint32_t* bw = reinterpret_cast<const uint32_t*>(buf) + lane;
-        uint32_t* dw = reinterpret_cast<uint32_t*>(d + h) + lane;
-        const uint32_t fsh = uint32_t(h) * 8;
-        for (int t = lane; t < nw; t += 32, bw += 32, dw += 32) *dw = __funnelshift_r(bw[0], bw[1], fsh);
-        const int tail0 = h + 4 * nw;
+        const int nu = (n_kept - h) >> 3;
+        const uint32_t* bw = reinterpret_cast<const uint32_t*>(buf) + (h >> 2) + 2 * lane;
+        uint2* dw = reinterpret_cast<uint2*>(d + h) + lane;
+        const uint32_t fsh = uint32_t(h & 3) * 8;
+        if ((h >> 2) == 0) {
+            for (int t = lane; t < nu; t += 32, bw += 64, dw += 32) {
+                const uint2 p = *reinterpret_cast<const uint2*>(bw);
+                const uint32_t c = bw[2];
+                *dw = make_uint2(__funnelshift_r(p.x, p.y, fsh), __funnelshift_r(p.y, c, fsh));
+            }
+        } else {
+            for (int t = lane; t < nu; t += 32, bw += 64, dw += 32) {
+                const uint32_t a0 = bw[0];
+                const uint2 p = *reinterpret_cast<const uint2*>(bw + 1);
+                *dw = make_uint2(__funnelshift_r(a0, p.x, fsh), __funnelshift_r(p.x, p.y, fsh));
+            }
+        }
+        const int tail0 = h + 8 * nu;
         if (lane < n_kept - tail0) d[tail0 + lane] = buf[tail0 + lane];
         __syncwarp();
     }
