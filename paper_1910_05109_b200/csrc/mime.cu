@@ -17,7 +17,7 @@
 //                         chunk counts (block scan); a warp compacts its chunk
 //                         (rows of lane-linear LDG.32) through a per-warp shared
 //                         buffer (16-bit keep mask per lane, one warp prefix
-//                         sum per 512 B) and writes it with 4-byte stores
+//                         sum per 512 B) and writes it with 8-byte stores
 //                         (funnel-shifted from aligned shared words) into the
 //                         workspace (byte-at-a-time paths for an unaligned
 //                         input and the last chunk);
@@ -35,24 +35,23 @@
 // guesses the layout, ws_line_kernel decodes straight from the text in one
 // pass and verifies every byte; the general kernels above then return at once
 // (they run when the layout does not hold).  Measured (1 GiB of data as MIME
-// lines of 76 chars + CRLF): 0.62 ms (line kernel ~154 us per 256 MiB with the
-// bulk-copy staging, issue-bound); the general path 1.64 ms on a random layout
-// (per 256 MiB: count ~70 us, compact ~240 us, decode ~100 us; the compaction
+// lines of 76 chars + CRLF): 0.60 ms (line kernel ~149 us per 256 MiB with the
+// bulk-copy staging, issue-bound); the general path 1.50 ms on a random layout
+// (per 256 MiB: count ~70 us, compact ~199 us, decode ~100 us; the compaction
 // is issue-bound; alphabets without whitespace chars use an arithmetic
-// per-byte test, ws_bits, for the keep masks).  The byte-at-a-time first
-// version took 3.7 ms.
+// per-byte test for the keep masks).  The byte-at-a-time first version took
+// 3.7 ms.
 #include "b64_device.cuh"
 
 namespace b64 {
 
+// ws_compact_kernel's byte stores: 1 = all four byte positions, highest first, __syncwarp between
+// (branch-free, the default); 0 = the earlier per-count tests (A/B only).  The __syncwarps are
+// required: without them ptxas reorders a lane's four stores and the overwrite order is lost.
 #ifndef B64_WS_STORE_ALL
 #define B64_WS_STORE_ALL 1
 #endif
-#if B64_WS_STORE_ALL == 2
-#define B64_WS_SYNC() ((void)0)
-#else
 #define B64_WS_SYNC() __syncwarp()
-#endif
 constexpr int kWsChunk = 4096;     // bytes per chunk (one warp at a time)
 #ifndef B64_WS_MAX_CTAS
 #define B64_WS_MAX_CTAS 4096
