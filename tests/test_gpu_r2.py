@@ -573,6 +573,26 @@ def test_decode_ws_line_segments(b64):
         assert np.array_equal(o.cpu().numpy(), ref), name
 
 
+def test_decode_ws_line_path_ragged_end(b64):
+    """The line kernel's last step: its kept chars end anywhere in a 32-char unit (the unit
+    loads past them read filler, not stale chars), with an incomplete final group (LENGTH),
+    an invalid char or a pad in it, an error in the last full quad, and a final line of every
+    length mod 4 -- against the oracle (error offset in the original text, exact bytes)."""
+    x = synth.data(600_000, seed=71)
+    t = oracle.encode(x)
+    tails = {"len0": b"", "AB": b"AB", "ABC": b"ABC", "A": b"A", "A*": b"A*", "*B": b"*B", "A=": b"A=",
+             "AB=": b"AB=", "AB C": b"AB C", "ABCD": b"ABCD", "AB*D": b"AB*D"}
+    for cut in (0, 4, 36, 72, 1000):
+        body = t[: t.size - cut]
+        for name, tail in tails.items():
+            tv = np.concatenate([body, np.frombuffer(tail, np.uint8)])
+            mime = _mime_lines(tv, 76)
+            ref, rerr, rst = oracle.decode_ws(mime)
+            o, err = b64.decode_ws(torch.from_numpy(mime).to(DEV))
+            assert err == rerr, (cut, name, err, rerr)
+            assert np.array_equal(o.cpu().numpy(), ref), (cut, name)
+
+
 # ------------------------------------------------------------------ decode -> consumer (f3)
 
 def test_decode_consume_vs_oracle(b64):
